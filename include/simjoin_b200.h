@@ -1,0 +1,153 @@
+/* simjoin_b200.h -- C ABI of libsjb200.so, the B200 (sm_100a) implementation
+ * of the reference's cosine-threshold tensor join hot path.
+ *
+ * Conventions (kept from the reference's _kernelcore.h:6-25):
+ *   - raw pointers + 64-bit sizes, row-major contiguous fp32 rows, uint64_t
+ *     offsets; outputs are caller-allocated with an explicit capacity and the
+ *     exact count is reported so the caller can retry (the reference's
+ *     count + capacity + resume protocol, _ckern.pyx:165-175, 194-211).
+ *   - Pointers named d_* are DEVICE pointers; `stream` is a cudaStream_t
+ *     (passed as void* so this header needs no CUDA include).
+ *   - Every entry point returns an int status: SJB_OK (0) or a negative
+ *     SJB_E_* code; sjb_last_error() returns a message for the calling
+ *     thread.  Calls are re-entrant and safe on distinct devices/streams.
+ *   - No torch types cross this boundary.
+ *
+ * Reference paths are relative to /root/reference/pkg/src/simjoin/.
+ */
+#ifndef SIMJOIN_B200_H
+#define SIMJOIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SJB_OK 0
+#define SJB_E_INVALID (-1)     /* bad argument (shape, dim, capacity) */
+#define SJB_E_CUDA (-2)        /* CUDA runtime error */
+#define SJB_E_UNSUPPORTED (-3) /* shape this build does not handle */
+
+#define SJB_TILE_ROWS 128
+
+/* ---- library ---------------------------------------------------------- */
+int sjb_version(void);
+const char* sjb_last_error(void);
+/* SM count of `device` (for sizing grids/workspaces). */
+int sjb_sm_count(int device);
+
+/* Padded reduction depth of the bf16 operand image for `dim` (multiple of 16). */
+int64_t sjb_kpad(int64_t dim);
+/* Elements of the bf16 operand image of an n-row relation: n rounded up to a
+ * multiple of 256 rows, times kpad.  Layout: 128-row tiles, each
+ * [k-group (kpad/8)][row (128)][8 elements] (UMMA K-major, no swizzle). */
+int64_t sjb_operand_elems(int64_t n, int64_t dim);
+
+/* ---- prefetch stage: embedding + normalise-and-cast -------------------- */
+
+/* Row L2 normalisation, bitwise equal to sj_normalize_rows
+ * (_kernelcore.h:8, _kernelcore.c:79-114): fp64 sequential sum of squares,
+ * zero rows repaired (component 0 := 1), fp64 divide, fp32 store.
+ * d_in may equal d_out32 (in place).  d_out16 (optional, may be NULL) gets the
+ * bf16 operand image (sjb_operand_elems elements).  *d_repaired (optional
+ * device u64) is incremented by the number of repaired rows. */
+int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32,
+                       void* d_out16, unsigned long long* d_repaired, void* stream);
+
+/* Row norms (sj_row_norms, _kernelcore.h:9). */
+int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
+
+/* FNV-1a-64 of packed tokens XOR xor_seed (sj_fnv1a64, _kernelcore.h:6;
+ * SyntheticModel._stream_seed, embedding.py:87-88).  Token t is
+ * d_bytes[d_offs[t], d_offs[t+1]). */
+int sjb_fnv1a64_many(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
+                     uint64_t xor_seed, uint64_t* d_out, void* stream);
+
+/* Synthetic model rows from stream seeds (sj_synthetic_fill, _kernelcore.h:7;
+ * SyntheticModel._embed_into, embedding.py:95-107), normalised per the model.
+ * d_out16 optional as above. */
+int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, float* d_out32,
+                            void* d_out16, void* stream);
+
+/* FastText-style subword model (cfg3; no reference counterpart, see
+ * DESIGN.md): row = mean of table rows of the word hash and every
+ * minn..maxn-gram of '<'w'>' (fnv1a64 mod n_buckets).  normalize != 0 also
+ * applies sjb_normalize_rows and writes the bf16 image (d_out16 optional). */
+int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
+                      const float* d_table, int64_t n_buckets, int64_t dim, int minn,
+                      int maxn, int normalize, float* d_out32, void* d_out16,
+                      unsigned long long* d_repaired, void* stream);
+
+/* ---- the fused join --------------------------------------------------- */
+
+typedef struct sjb_join_args {
+  int64_t n_left, n_right, dim;
+  float theta;          /* inclusive: a pair matches iff canonical sim >= theta */
+  float band;           /* bf16 filter margin; candidates have approx >= theta - band */
+  int64_t cand_cap;     /* candidate buffer entries (workspace) */
+  int64_t out_cap;      /* capacity of lefts/rights/sims */
+  uint64_t left_base;   /* added to emitted left offsets (R shards) */
+  int32_t grid;         /* 0 = one CTA per SM */
+  int32_t tiles_per_chunk; /* 0 = automatic */
+} sjb_join_args;
+
+typedef struct sjb_join_info {
+  int64_t n_matches;    /* exact number of matches */
+  int64_t n_candidates; /* exact number of filter candidates */
+  int64_t cand_needed;  /* candidate capacity that avoids overflow on retry */
+  int32_t overflow;     /* 1: candidates or outputs overflowed -> retry */
+  int32_t grid;         /* CTAs the filter kernel ran with */
+} sjb_join_info;
+
+/* Workspace bytes needed by sjb_join_prepared for these args. */
+int64_t sjb_join_workspace_bytes(const sjb_join_args* args);
+
+/* Default (provably sufficient) band for `dim`: bf16 rounding of unit
+ * vectors (2u+u^2, u = 2^-8) plus fp32 accumulation slack. */
+float sjb_default_band(int64_t dim);
+
+/* Join two prepared (normalised) relations on the device; asynchronous.
+ * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: bf16 operand images.
+ * Replaces tensor_join's tile loop (join.py:338-359: tile_similarity +
+ * threshold_scan + MatchSink.merge) with filter -> canonical recheck ->
+ * row bucketing -> per-row sort.  Writes the canonical MatchSet columns to
+ * d_lefts/d_rights/d_sims and the sjb_join_info fields to d_info (device
+ * memory, 5 x 8 bytes) without synchronising. */
+int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
+                            const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                            int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
+                            float* d_sims, void* d_info, void* stream);
+
+/* Synchronous form: as above, then waits on `stream` and copies the info to
+ * the host struct *info. */
+int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,
+                      const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                      int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
+                      float* d_sims, sjb_join_info* info, void* stream);
+
+/* ---- dense kernels of the reference backend API ------------------------ */
+
+/* out[i*ldo+j] = canonical dot(left row i, packed column j)
+ * (sj_tile_dot, _kernelcore.h:13-14; bt = pack_transpose, dim x nr). */
+int sjb_tile_dot(const float* d_left, int64_t lda, const float* d_bt, int64_t ldb, int64_t nl,
+                 int64_t nr, int64_t dim, float* d_out, int64_t ldo, void* stream);
+
+/* out[i] = canonical dot(a, row i) (sj_dots_vm, _kernelcore.h:11). */
+int sjb_dots_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
+                void* stream);
+
+/* Row-major threshold scan of a dense nl x nr buffer (sj_scan_count +
+ * sj_scan_fill, _kernelcore.h:15-18).  Pass 1 (outputs NULL): *count = hits.
+ * Pass 2: fills up to cap hits in row-major order.  Synchronous. */
+int sjb_scan_hits(const float* d_buf, int64_t nl, int64_t nr, float theta, uint64_t left0,
+                  uint64_t right0, uint64_t* d_lefts, uint64_t* d_rights, float* d_sims,
+                  int64_t cap, int64_t* count, void* d_workspace, int64_t workspace_bytes,
+                  void* stream);
+int64_t sjb_scan_hits_workspace_bytes(int64_t nl);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIMJOIN_B200_H */

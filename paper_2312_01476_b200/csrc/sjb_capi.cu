@@ -1,0 +1,493 @@
+// sjb_capi.cu -- extern "C" boundary of libsjb200.so (declared in
+// include/simjoin_b200.h) and the host-side orchestration of the join
+// pipeline.  Built as ONE translation unit with the kernel sources.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/simjoin_b200.h"
+#include "sjb_common.cuh"
+#include "sjb_join.cu"
+#include "sjb_post.cu"
+#include "sjb_prep.cu"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define SJB_CK(expr)                                                                       \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(SJB_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),      \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+#define SJB_CK_LAUNCH(name)                                                                \
+  do {                                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(SJB_E_CUDA, "launch of %s failed: %s", name, cudaGetErrorString(e_));    \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int max_dyn_smem(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+// Sub-tile rows for the prep kernels: as many of the 128 tile rows as fit in
+// ~100 KB of smem (so 2 CTAs fit per SM), multiple of 32.
+int prep_sub_rows(int64_t dim) {
+  const int64_t pitch = dim | 1;
+  int sub = 128;
+  while (sub > 32 && (int64_t)sub * pitch * 4 > 100 * 1024) sub >>= 1;
+  return sub;
+}
+
+int set_smem_attr(const void* fn, int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess)
+    return fail(SJB_E_CUDA, "cudaFuncSetAttribute(%d B) failed: %s", bytes, cudaGetErrorString(e));
+  return SJB_OK;
+}
+
+// ---------------------------------------------------------------- plan
+struct JoinPlan {
+  int kpad, stages, grid, tiles_per_chunk, n_ablk, n_btiles;
+  int64_t n_items;
+  uint32_t smem;
+  uint64_t seg_cap;
+};
+
+int make_plan(const sjb_join_args* a, JoinPlan* pl) {
+  const int dev = current_device();
+  const int sms = sjb_sm_count(dev);
+  pl->kpad = (int)sjb_kpad(a->dim);
+  if (pl->kpad > 128)
+    return fail(SJB_E_UNSUPPORTED, "dim %lld > 128 not supported by the resident-A join kernel",
+                (long long)a->dim);
+  const int max_smem = max_dyn_smem(dev);
+  sjb::JoinSmemLayout L0 = sjb::join_smem_layout(pl->kpad, 0);
+  int stages = (int)((max_smem - (int)L0.total) / (int)L0.b_bytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for 2 stages");
+  pl->stages = stages;
+  pl->smem = sjb::join_smem_layout(pl->kpad, stages).total;
+  pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kBM);
+  pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kBN);
+  int tpc = a->tiles_per_chunk;
+  if (tpc <= 0) {
+    const int64_t pairs = (int64_t)pl->n_ablk * pl->n_btiles;
+    int64_t t = pairs / (4LL * sms);
+    tpc = (int)(t < 1 ? 1 : (t > 64 ? 64 : t));
+  }
+  pl->tiles_per_chunk = tpc;
+  pl->n_items = (int64_t)pl->n_ablk * sjb::ceil_div(pl->n_btiles, tpc);
+  int grid = a->grid > 0 ? a->grid : sms;
+  if ((int64_t)grid > pl->n_items) grid = (int)(pl->n_items > 0 ? pl->n_items : 1);
+  pl->grid = grid;
+  pl->seg_cap = (uint64_t)(a->cand_cap / grid);
+  return SJB_OK;
+}
+
+// ------------------------------------------------------------ workspace
+struct JoinWs {
+  size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, total;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+JoinWs join_ws_layout(const sjb_join_args* a, int grid) {
+  JoinWs w;
+  size_t o = 0;
+  const size_t ccap = (size_t)(a->cand_cap > 0 ? a->cand_cap : 0);
+  const size_t nl = (size_t)(a->n_left > 0 ? a->n_left : 0);
+  const size_t ocap = (size_t)(a->out_cap > 0 ? a->out_cap : 0);
+  const size_t nblocks = sjb::ceil_div((int64_t)nl, sjb::kScanBlock) + 1;
+  w.cand = o;     o = align256(o + ccap * 8);
+  w.sims = o;     o = align256(o + ccap * 4);
+  w.cta = o;      o = align256(o + (size_t)grid * 8);
+  w.rowcount = o; o = align256(o + nl * 4);
+  w.rowoff = o;   o = align256(o + (nl + 1) * 8);
+  w.cursor = o;   o = align256(o + (nl + 1) * 8);
+  w.keys = o;     o = align256(o + ocap * 8);
+  w.bsums = o;    o = align256(o + (nblocks + 1) * 8);
+  w.bigrows = o;  o = align256(o + nl * 4);
+  w.nbig = o;     o = align256(o + 16);
+  w.total = o;
+  return w;
+}
+
+int grid_for(uint64_t n, int threads, int per_sm_blocks) {
+  const int sms = sjb_sm_count(current_device());
+  uint64_t g = (n + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)sms * per_sm_blocks;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// exclusive scan of n u32 counts into out[0..n] (u64) (+ optional copy)
+int run_scan(const uint32_t* counts, int64_t n, uint64_t* out, uint64_t* out_copy,
+             uint64_t* bsums, cudaStream_t st) {
+  const int64_t nb = sjb::ceil_div(n, sjb::kScanBlock);
+  if (nb > (int64_t)sjb::kScanBlock)
+    return fail(SJB_E_UNSUPPORTED, "row scan supports at most %d rows",
+                sjb::kScanBlock * sjb::kScanBlock);
+  if (nb == 0) {
+    SJB_CK(cudaMemsetAsync(out, 0, 8, st));
+    if (out_copy) SJB_CK(cudaMemsetAsync(out_copy, 0, 8, st));
+    return SJB_OK;
+  }
+  uint64_t* grand = bsums + nb;
+  sjb::scan_reduce_kernel<<<(unsigned)nb, sjb::kScanThreads, 0, st>>>(counts, n, bsums);
+  SJB_CK_LAUNCH("scan_reduce");
+  sjb::scan_blocks_kernel<<<1, sjb::kScanThreads, 0, st>>>(bsums, nb, grand);
+  SJB_CK_LAUNCH("scan_blocks");
+  sjb::scan_down_kernel<<<(unsigned)nb, sjb::kScanThreads, 0, st>>>(counts, n, bsums, grand, out,
+                                                                     out_copy);
+  SJB_CK_LAUNCH("scan_down");
+  return SJB_OK;
+}
+
+}  // namespace
+
+namespace sjb {
+
+// Publishes sjb_join_info into device memory.
+__global__ void join_finalize_kernel(const unsigned long long* __restrict__ cta_count, int grid,
+                                     uint64_t seg_cap, const uint64_t* __restrict__ rowoff,
+                                     int64_t n_left, int64_t out_cap, int64_t* __restrict__ info) {
+  __shared__ unsigned long long s_sum, s_max;
+  if (threadIdx.x == 0) {
+    s_sum = 0;
+    s_max = 0;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < grid; c += blockDim.x) {
+    atomicAdd(&s_sum, cta_count[c]);
+    atomicMax(&s_max, cta_count[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t matches = n_left > 0 ? (int64_t)rowoff[n_left] : 0;
+    const bool ovf = s_max > seg_cap || matches > out_cap;
+    info[0] = matches;
+    info[1] = (int64_t)s_sum;
+    info[2] = (int64_t)(s_max * (unsigned long long)grid);
+    reinterpret_cast<int32_t*>(info + 3)[0] = ovf ? 1 : 0;
+    reinterpret_cast<int32_t*>(info + 3)[1] = grid;
+  }
+}
+
+// Output gate (flag[1]): scatter/sort run only if the match count fits.
+__global__ void gate_kernel(const uint64_t* __restrict__ rowoff, int64_t n_left, int64_t out_cap,
+                            unsigned int* __restrict__ flag) {
+  flag[1] = (n_left > 0 && (int64_t)rowoff[n_left] <= out_cap) ? 1u : 0u;
+}
+
+}  // namespace sjb
+
+extern "C" {
+
+int sjb_version(void) { return 1; }
+
+const char* sjb_last_error(void) { return g_err.c_str(); }
+
+int sjb_sm_count(int device) {
+  static int cache[64] = {0};
+  if (device >= 0 && device < 64 && cache[device]) return cache[device];
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  if (device >= 0 && device < 64) cache[device] = v;
+  return v;
+}
+
+int64_t sjb_kpad(int64_t dim) { return sjb::round_up(dim < 1 ? 1 : dim, 16); }
+
+int64_t sjb_operand_elems(int64_t n, int64_t dim) {
+  return sjb::round_up(n < 0 ? 0 : n, 2 * sjb::kTileRows) * sjb_kpad(dim);
+}
+
+float sjb_default_band(int64_t dim) {
+  // |cos_bf16 - cos_fp32| <= (2u + u^2) * sum|a_i b_i| <= 2u + u^2 for unit
+  // vectors (u = 2^-8), plus fp32 accumulation error of both the tensor-core
+  // sum and the canonical sequential sum (<= 2 * dim * 2^-24 each, generous).
+  const double u = 1.0 / 256.0;
+  const double b = 2 * u + u * u + 4.0 * (double)dim * 5.9604644775390625e-08 + 1e-6;
+  return (float)b;
+}
+
+int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
+                       unsigned long long* d_repaired, void* stream) {
+  if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+  const int kpad = (int)sjb_kpad(dim);
+  const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
+                                : sjb::ceil_div(n, sjb::kTileRows);
+  if (tiles == 0) return SJB_OK;
+  const int sub = prep_sub_rows(dim);
+  const int smem = sub * (int)(dim | 1) * 4;
+  if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
+  sjb::normalize_cast_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
+      d_in, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16), d_repaired,
+      1);
+  SJB_CK_LAUNCH("normalize_cast");
+  return SJB_OK;
+}
+
+int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream) {
+  if (n <= 0) return SJB_OK;
+  sjb::row_norms_kernel<<<(unsigned)sjb::ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
+      d_m, n, (int)dim, d_out);
+  SJB_CK_LAUNCH("row_norms");
+  return SJB_OK;
+}
+
+int sjb_fnv1a64_many(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n, uint64_t xor_seed,
+                     uint64_t* d_out, void* stream) {
+  if (n <= 0) return SJB_OK;
+  sjb::fnv1a64_kernel<<<(unsigned)sjb::ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
+      d_bytes, d_offs, n, xor_seed, d_out);
+  SJB_CK_LAUNCH("fnv1a64");
+  return SJB_OK;
+}
+
+int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, float* d_out32,
+                            void* d_out16, void* stream) {
+  if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape");
+  const int kpad = (int)sjb_kpad(dim);
+  const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
+                                : sjb::ceil_div(n, sjb::kTileRows);
+  if (tiles == 0) return SJB_OK;
+  const int sub = prep_sub_rows(dim);
+  const int smem = sub * (int)(dim | 1) * 4;
+  if (int rc = set_smem_attr((const void*)sjb::synthetic_fill_kernel, smem)) return rc;
+  sjb::synthetic_fill_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
+      d_seeds, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16));
+  SJB_CK_LAUNCH("synthetic_fill");
+  return SJB_OK;
+}
+
+int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
+                      const float* d_table, int64_t n_buckets, int64_t dim, int minn, int maxn,
+                      int normalize, float* d_out32, void* d_out16,
+                      unsigned long long* d_repaired, void* stream) {
+  if (n < 0 || dim < 1 || n_buckets < 1 || minn < 1 || maxn < minn)
+    return fail(SJB_E_INVALID, "bad subword arguments");
+  const int kpad = (int)sjb_kpad(dim);
+  const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
+                                : sjb::ceil_div(n, sjb::kTileRows);
+  if (tiles == 0) return SJB_OK;
+  const int sub = prep_sub_rows(dim);
+  const int smem = sub * (int)(dim | 1) * 4;
+  if (int rc = set_smem_attr((const void*)sjb::subword_embed_kernel, smem)) return rc;
+  sjb::subword_embed_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
+      d_bytes, d_offs, n, d_table, n_buckets, (int)dim, kpad, sub, minn, maxn, normalize, d_out32,
+      normalize ? reinterpret_cast<__nv_bfloat16*>(d_out16) : nullptr, d_repaired);
+  SJB_CK_LAUNCH("subword_embed");
+  return SJB_OK;
+}
+
+int64_t sjb_join_workspace_bytes(const sjb_join_args* args) {
+  if (!args) return -1;
+  JoinPlan pl;
+  int grid = 1;
+  if (args->n_left > 0 && args->n_right > 0) {
+    if (make_plan(args, &pl) != SJB_OK) return -1;
+    grid = pl.grid;
+  }
+  return (int64_t)join_ws_layout(args, grid).total;
+}
+
+int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
+                            const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                            int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
+                            float* d_sims, void* d_info, void* stream) {
+  if (!args || !d_info) return fail(SJB_E_INVALID, "null args/info");
+  const int64_t nl = args->n_left, nr = args->n_right;
+  if (nl < 0 || nr < 0 || args->dim < 1) return fail(SJB_E_INVALID, "bad shape");
+  if (nl >= (int64_t(1) << 32) || nr >= (int64_t(1) << 32))
+    return fail(SJB_E_UNSUPPORTED, "relations are limited to 2^32 rows per join");
+  cudaStream_t st = as_stream(stream);
+  int64_t* info = reinterpret_cast<int64_t*>(d_info);
+  if (nl == 0 || nr == 0) {
+    SJB_CK(cudaMemsetAsync(info, 0, 5 * 8, st));
+    return SJB_OK;
+  }
+  JoinPlan pl;
+  if (int rc = make_plan(args, &pl)) return rc;
+  const JoinWs w = join_ws_layout(args, pl.grid);
+  if ((int64_t)w.total > workspace_bytes)
+    return fail(SJB_E_INVALID, "workspace %lld B < required %lld B", (long long)workspace_bytes,
+                (long long)w.total);
+  if (pl.seg_cap < 1) return fail(SJB_E_INVALID, "cand_cap %lld < grid %d", (long long)args->cand_cap, pl.grid);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(ws + w.cand);
+  uint32_t* sims_bits = reinterpret_cast<uint32_t*>(ws + w.sims);
+  unsigned long long* cta = reinterpret_cast<unsigned long long*>(ws + w.cta);
+  uint32_t* rowcount = reinterpret_cast<uint32_t*>(ws + w.rowcount);
+  uint64_t* rowoff = reinterpret_cast<uint64_t*>(ws + w.rowoff);
+  uint64_t* cursor = reinterpret_cast<uint64_t*>(ws + w.cursor);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(ws + w.keys);
+  uint64_t* bsums = reinterpret_cast<uint64_t*>(ws + w.bsums);
+  uint32_t* bigrows = reinterpret_cast<uint32_t*>(ws + w.bigrows);
+  unsigned int* nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
+
+  SJB_CK(cudaMemsetAsync(rowcount, 0, (size_t)nl * 4, st));
+  SJB_CK(cudaMemsetAsync(nbig, 0, 16, st));
+
+  // 1) tensor-core filter
+  sjb::JoinParams jp;
+  jp.a16 = reinterpret_cast<const __nv_bfloat16*>(d_l16);
+  jp.b16 = reinterpret_cast<const __nv_bfloat16*>(d_r16);
+  jp.n_a = nl;
+  jp.n_b = nr;
+  jp.kpad = pl.kpad;
+  jp.n_ablk = pl.n_ablk;
+  jp.n_btiles = pl.n_btiles;
+  jp.tiles_per_chunk = pl.tiles_per_chunk;
+  jp.n_items = pl.n_items;
+  jp.stages = pl.stages;
+  jp.cutoff = args->theta - args->band;
+  jp.cand = cand;
+  jp.seg_cap = pl.seg_cap;
+  jp.cta_count = cta;
+  if (int rc = set_smem_attr((const void*)sjb::join_filter_kernel, (int)pl.smem)) return rc;
+  sjb::join_filter_kernel<<<pl.grid, sjb::kJoinThreads, pl.smem, st>>>(jp);
+  SJB_CK_LAUNCH("join_filter");
+
+  // 2) canonical recheck
+  const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
+  sjb::recheck_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
+      cand, pl.seg_cap, cta, pl.grid, d_l32, d_r32, (int)args->dim, args->theta, sims_bits,
+      rowcount);
+  SJB_CK_LAUNCH("recheck");
+
+  // 3) row offsets
+  if (int rc = run_scan(rowcount, nl, rowoff, cursor, bsums, st)) return rc;
+  sjb::gate_kernel<<<1, 1, 0, st>>>(rowoff, nl, args->out_cap, nbig);
+  SJB_CK_LAUNCH("gate");
+
+  // 4) bucket by left row, 5) sort each row by right offset
+  sjb::scatter_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
+      cand, pl.seg_cap, cta, pl.grid, sims_bits, reinterpret_cast<unsigned long long*>(cursor),
+      keys, nbig);
+  SJB_CK_LAUNCH("scatter");
+  sjb::segsort_small_kernel<<<grid_for((uint64_t)nl * 32, sjb::kSortSmallThreads, 16),
+                              sjb::kSortSmallThreads, 0, st>>>(
+      rowoff, nl, keys, d_lefts, d_rights, d_sims, bigrows, nbig, args->left_base);
+  SJB_CK_LAUNCH("segsort_small");
+  const int big_smem = sjb::kSortBigCap * 8;
+  if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
+  sjb::segsort_big_kernel<<<sjb_sm_count(current_device()), sjb::kSortBigThreads, big_smem, st>>>(
+      rowoff, keys, d_lefts, d_rights, d_sims, bigrows, nbig, args->left_base);
+  SJB_CK_LAUNCH("segsort_big");
+
+  sjb::join_finalize_kernel<<<1, 256, 0, st>>>(cta, pl.grid, pl.seg_cap, rowoff, nl, args->out_cap,
+                                               info);
+  SJB_CK_LAUNCH("finalize");
+  return SJB_OK;
+}
+
+int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,
+                      const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                      int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
+                      float* d_sims, sjb_join_info* info, void* stream) {
+  if (!info) return fail(SJB_E_INVALID, "null info");
+  void* d_info = nullptr;
+  cudaStream_t st = as_stream(stream);
+  SJB_CK(cudaMallocAsync(&d_info, 64, st));
+  int rc = sjb_join_prepared_async(d_l32, d_l16, d_r32, d_r16, args, d_workspace, workspace_bytes,
+                                   d_lefts, d_rights, d_sims, d_info, stream);
+  if (rc == SJB_OK) {
+    int64_t h[5];
+    SJB_CK(cudaMemcpyAsync(h, d_info, 40, cudaMemcpyDeviceToHost, st));
+    SJB_CK(cudaStreamSynchronize(st));
+    info->n_matches = h[0];
+    info->n_candidates = h[1];
+    info->cand_needed = h[2];
+    info->overflow = reinterpret_cast<int32_t*>(h + 3)[0];
+    info->grid = reinterpret_cast<int32_t*>(h + 3)[1];
+  }
+  cudaFreeAsync(d_info, st);
+  return rc;
+}
+
+int sjb_tile_dot(const float* d_left, int64_t lda, const float* d_bt, int64_t ldb, int64_t nl,
+                 int64_t nr, int64_t dim, float* d_out, int64_t ldo, void* stream) {
+  if (nl <= 0 || nr <= 0) return SJB_OK;
+  dim3 grid((unsigned)sjb::ceil_div(nr, sjb::kTD), (unsigned)sjb::ceil_div(nl, sjb::kTD));
+  sjb::tile_dot_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_left, lda, d_bt, ldb, nl, nr,
+                                                             (int)dim, d_out, ldo);
+  SJB_CK_LAUNCH("tile_dot");
+  return SJB_OK;
+}
+
+int sjb_dots_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
+                void* stream) {
+  if (n <= 0) return SJB_OK;
+  sjb::dots_vm_kernel<<<(unsigned)sjb::ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
+      d_a, d_m, n, (int)dim, d_out);
+  SJB_CK_LAUNCH("dots_vm");
+  return SJB_OK;
+}
+
+int64_t sjb_scan_hits_workspace_bytes(int64_t nl) {
+  const size_t n = (size_t)(nl > 0 ? nl : 0);
+  const size_t nb = sjb::ceil_div((int64_t)n, sjb::kScanBlock) + 1;
+  return (int64_t)(align256(n * 4) + align256((n + 1) * 8) + align256((nb + 1) * 8));
+}
+
+int sjb_scan_hits(const float* d_buf, int64_t nl, int64_t nr, float theta, uint64_t left0,
+                  uint64_t right0, uint64_t* d_lefts, uint64_t* d_rights, float* d_sims,
+                  int64_t cap, int64_t* count, void* d_workspace, int64_t workspace_bytes,
+                  void* stream) {
+  if (!count) return fail(SJB_E_INVALID, "null count");
+  *count = 0;
+  if (nl <= 0 || nr <= 0) return SJB_OK;
+  if (workspace_bytes < sjb_scan_hits_workspace_bytes(nl))
+    return fail(SJB_E_INVALID, "scan_hits workspace too small");
+  cudaStream_t st = as_stream(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
+  const size_t n = (size_t)nl;
+  uint32_t* rowcount = reinterpret_cast<uint32_t*>(ws);
+  uint64_t* rowoff = reinterpret_cast<uint64_t*>(ws + align256(n * 4));
+  uint64_t* bsums = reinterpret_cast<uint64_t*>(ws + align256(n * 4) + align256((n + 1) * 8));
+  const unsigned blocks = (unsigned)sjb::ceil_div(nl, 8);
+  sjb::dense_count_kernel<<<blocks, 256, 0, st>>>(d_buf, nl, nr, theta, rowcount);
+  SJB_CK_LAUNCH("dense_count");
+  if (int rc = run_scan(rowcount, nl, rowoff, nullptr, bsums, st)) return rc;
+  uint64_t total = 0;
+  SJB_CK(cudaMemcpyAsync(&total, rowoff + nl, 8, cudaMemcpyDeviceToHost, st));
+  SJB_CK(cudaStreamSynchronize(st));
+  *count = (int64_t)total;
+  if (d_lefts == nullptr || (int64_t)total > cap) return SJB_OK;
+  sjb::dense_fill_kernel<<<blocks, 256, 0, st>>>(d_buf, nl, nr, theta, rowoff, left0, right0,
+                                                 d_lefts, d_rights, d_sims);
+  SJB_CK_LAUNCH("dense_fill");
+  SJB_CK(cudaStreamSynchronize(st));
+  return SJB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,445 @@
+// sjb_post.cu -- everything after the tensor-core filter:
+//
+//   recheck    canonical fp32 similarity for every candidate (sequential
+//              fmaf chain over d == sj_dot_seq, _kernelcore.c:128-133) and the
+//              inclusive `sim >= theta` decision (threshold_scan, linalg.py:146-153)
+//   row scan   exclusive prefix sum of per-row match counts
+//   scatter    bucket kept pairs by left row (counting sort)
+//   segsort    sort each left row's bucket by right offset and write the
+//              MatchSet columns (u64 lefts, u64 rights, f32 sims) -- the
+//              canonical (left, right) order of canonicalize (core.py:196-213).
+//
+// plus the dense kernels behind the reference backend API:
+//   tile_dot   canonical dense tile (sj_tile_dot, _kernelcore.c:300-323)
+//   dots_vm    sj_dots_vm (_kernelcore.c:135-138)
+//   scan_hits  row-major threshold scan of a dense buffer (_kernelcore.c:327-350)
+#include "sjb_common.cuh"
+
+namespace sjb {
+
+__device__ __forceinline__ float dot_seq_dev(const float* __restrict__ a,
+                                             const float* __restrict__ b, int dim) {
+  float acc = 0.0f;
+  if ((dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (int d = 0; d < (dim >> 2); d++) {
+      const float4 x = __ldg(a4 + d), y = __ldg(b4 + d);
+      acc = __fmaf_rn(x.x, y.x, acc);
+      acc = __fmaf_rn(x.y, y.y, acc);
+      acc = __fmaf_rn(x.z, y.z, acc);
+      acc = __fmaf_rn(x.w, y.w, acc);
+    }
+  } else {
+    for (int d = 0; d < dim; d++) acc = __fmaf_rn(__ldg(a + d), __ldg(b + d), acc);
+  }
+  return acc;
+}
+
+constexpr uint32_t kRejected = 0x7fc00001u;  // NaN payload marking a rejected candidate
+
+// Candidate slot p lives in CTA segment p / seg_cap.
+__global__ void recheck_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                               const unsigned long long* __restrict__ cta_count, int n_cta,
+                               const float* __restrict__ l32, const float* __restrict__ s32,
+                               int dim, float theta, uint32_t* __restrict__ sims_bits,
+                               uint32_t* __restrict__ rowcount) {
+  const uint64_t total = (uint64_t)n_cta * seg_cap;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = p / seg_cap, local = p - c * seg_cap;
+    const uint64_t cnt = mn<uint64_t>(cta_count[c], seg_cap);
+    if (local >= cnt) continue;
+    const uint64_t u = cand[p];
+    const uint32_t i = (uint32_t)(u >> 32), j = (uint32_t)u;
+    const float s = dot_seq_dev(l32 + (size_t)i * dim, s32 + (size_t)j * dim, dim);
+    const bool keep = s >= theta;
+    sims_bits[p] = keep ? __float_as_uint(s) : kRejected;
+    if (keep) atomicAdd(rowcount + i, 1u);
+  }
+}
+
+// ----------------------------------------------------------- prefix scan
+// Three-phase exclusive scan of u32 counts into u64 offsets (n+1 entries).
+constexpr int kScanThreads = 1024;
+constexpr int kScanPerThread = 4;
+constexpr int kScanBlock = kScanThreads * kScanPerThread;
+
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t* warp_sums,
+                                                    uint64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint64_t w = lane < nw ? warp_sums[lane] : 0;
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < nw) warp_sums[lane] = wi - w;
+    if (lane == nw - 1) *total = wi;
+  }
+  __syncthreads();
+  const uint64_t r = warp_sums[warp] + incl - x;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ block_sums) {
+  __shared__ uint64_t ws[32];
+  __shared__ uint64_t tot;
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanPerThread;
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; k++)
+    if (base + k < n) s += in[base + k];
+  block_excl_scan(s, ws, &tot);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+// Single block: exclusive scan of the block sums in place (nb <= 4096).
+__global__ void __launch_bounds__(kScanThreads)
+scan_blocks_kernel(uint64_t* __restrict__ block_sums, int64_t nb, uint64_t* __restrict__ grand) {
+  __shared__ uint64_t ws[32];
+  __shared__ uint64_t tot;
+  const int64_t base = threadIdx.x * kScanPerThread;
+  uint64_t v[kScanPerThread];
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; k++) {
+    v[k] = base + k < nb ? block_sums[base + k] : 0;
+    s += v[k];
+  }
+  uint64_t off = block_excl_scan(s, ws, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; k++) {
+    if (base + k < nb) block_sums[base + k] = off;
+    off += v[k];
+  }
+  if (threadIdx.x == 0) *grand = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __restrict__ block_sums,
+                 const uint64_t* __restrict__ grand, uint64_t* __restrict__ out,
+                 uint64_t* __restrict__ out_copy) {
+  __shared__ uint64_t ws[32];
+  __shared__ uint64_t tot;
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock + threadIdx.x * kScanPerThread;
+  uint32_t v[kScanPerThread];
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; k++) {
+    v[k] = base + k < n ? in[base + k] : 0u;
+    s += v[k];
+  }
+  uint64_t off = block_excl_scan(s, ws, &tot) + block_sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; k++) {
+    if (base + k < n) {
+      out[base + k] = off;
+      if (out_copy) out_copy[base + k] = off;
+    }
+    off += v[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[n] = *grand;
+    if (out_copy) out_copy[n] = *grand;
+  }
+}
+
+// ------------------------------------------------------------- scatter
+// Sort key = (right offset << 32) | sim bits: unique per row because right
+// offsets are unique within a row.  gate[1] == 0 (matches exceed the output
+// capacity) turns scatter and sort into no-ops; the host retries.
+__global__ void scatter_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                               const unsigned long long* __restrict__ cta_count, int n_cta,
+                               const uint32_t* __restrict__ sims_bits,
+                               unsigned long long* __restrict__ cursor,
+                               uint64_t* __restrict__ keys, const unsigned int* __restrict__ gate) {
+  if (gate[1] == 0) return;
+  const uint64_t total = (uint64_t)n_cta * seg_cap;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = p / seg_cap, local = p - c * seg_cap;
+    const uint64_t cnt = mn<uint64_t>(cta_count[c], seg_cap);
+    if (local >= cnt) continue;
+    const uint32_t sb = sims_bits[p];
+    if (sb == kRejected) continue;
+    const uint64_t u = cand[p];
+    const uint32_t i = (uint32_t)(u >> 32), j = (uint32_t)u;
+    const uint64_t q = atomicAdd(cursor + i, 1ull);
+    keys[q] = (uint64_t(j) << 32) | sb;
+  }
+}
+
+// ------------------------------------------------------ segmented sort
+// Bitonic network in its "mirror" form: every compare-exchange puts the
+// smaller key at the lower index, so a segment of any length sorts with
+// virtual +inf padding that never moves.
+__device__ __forceinline__ void cmpx(uint64_t* s, int a, int b) {
+  uint64_t x = s[a], y = s[b];
+  if (y < x) {
+    s[a] = y;
+    s[b] = x;
+  }
+}
+
+// Sort s[0..n) in shared memory with `nthr` cooperating threads (tid in
+// [0, nthr)); `sync` is the barrier among them.
+template <bool kWarp>
+__device__ __forceinline__ void nsync() {
+  if (kWarp) __syncwarp(); else __syncthreads();
+}
+
+template <bool kWarp>
+__device__ void smem_bitonic(uint64_t* s, int n, int tid, int nthr) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    // mirror step
+    for (int t = tid; t < P / 2; t += nthr) {
+      const int blk = t / (k / 2), off = t % (k / 2);
+      const int a = blk * k + off, b = blk * k + k - 1 - off;
+      if (b < n) cmpx(s, a, b);
+    }
+    nsync<kWarp>();
+    for (int j = k / 4; j >= 1; j >>= 1) {
+      for (int t = tid; t < P / 2; t += nthr) {
+        const int blk = t / j, off = t % j;
+        const int a = blk * 2 * j + off, b = a + j;
+        if (b < n) cmpx(s, a, b);
+      }
+      nsync<kWarp>();
+    }
+  }
+}
+
+__device__ __forceinline__ void write_row(uint64_t i, const uint64_t* sorted, uint64_t q0, int n,
+                                          int tid, int nthr, uint64_t* __restrict__ lefts,
+                                          uint64_t* __restrict__ rights,
+                                          float* __restrict__ sims) {
+  for (int t = tid; t < n; t += nthr) {
+    const uint64_t key = sorted[t];
+    lefts[q0 + t] = i;
+    rights[q0 + t] = key >> 32;
+    sims[q0 + t] = __uint_as_float((uint32_t)key);
+  }
+}
+
+constexpr int kSortWarpCap = 1024;  // per-warp smem capacity (8 KB)
+constexpr int kSortSmallThreads = 128;
+
+__global__ void __launch_bounds__(kSortSmallThreads)
+segsort_small_kernel(const uint64_t* __restrict__ rowoff, int64_t n_rows, const uint64_t* __restrict__ keys,
+                     uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
+                     float* __restrict__ sims, uint32_t* __restrict__ big_rows,
+                     unsigned int* __restrict__ n_big, uint64_t left_base) {
+  __shared__ uint64_t buf[kSortSmallThreads / 32][kSortWarpCap];
+  if (n_big[1] == 0) return;  // gate: outputs would overflow
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* s = buf[warp];
+  const int64_t wpb = kSortSmallThreads / 32;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + warp; i < n_rows; i += (int64_t)gridDim.x * wpb) {
+    const uint64_t q0 = rowoff[i], q1 = rowoff[i + 1];
+    const int64_t n = (int64_t)(q1 - q0);
+    if (n == 0) continue;
+    if (n > kSortWarpCap) {
+      if (lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
+      continue;
+    }
+    for (int t = lane; t < n; t += 32) s[t] = keys[q0 + t];
+    __syncwarp();
+    smem_bitonic<true>(s, (int)n, lane, 32);
+    write_row(left_base + (uint64_t)i, s, q0, (int)n, lane, 32, lefts, rights, sims);
+    __syncwarp();
+  }
+}
+
+constexpr int kSortBigThreads = 512;
+constexpr int kSortBigCap = 8192;  // 64 KB of dynamic smem
+
+// Rows longer than kSortWarpCap: one CTA per row.  <= kSortBigCap sorts in
+// shared memory; longer rows run the same network over global memory with
+// the inner (j < kSortBigCap) steps done in shared memory per chunk.
+__global__ void __launch_bounds__(kSortBigThreads)
+segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ keys,
+                   uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
+                   float* __restrict__ sims, const uint32_t* __restrict__ big_rows,
+                   const unsigned int* __restrict__ n_big, uint64_t left_base) {
+  extern __shared__ uint64_t sbuf[];
+  if (n_big[1] == 0) return;  // gate: outputs would overflow
+  const unsigned nb = n_big[0];
+  for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
+    const uint32_t i = big_rows[r];
+    const uint64_t q0 = rowoff[i];
+    const int64_t n = (int64_t)(rowoff[i + 1] - q0);
+    uint64_t* g = keys + q0;
+    if (n <= kSortBigCap) {
+      for (int t = threadIdx.x; t < n; t += blockDim.x) sbuf[t] = g[t];
+      __syncthreads();
+      smem_bitonic<false>(sbuf, (int)n, threadIdx.x, blockDim.x);
+      write_row(left_base + i, sbuf, q0, (int)n, threadIdx.x, blockDim.x, lefts, rights, sims);
+      __syncthreads();
+      continue;
+    }
+    int64_t P = 1;
+    while (P < n) P <<= 1;
+    const int C = kSortBigCap;
+    // 1) sort every C-chunk (all stages k <= C) in shared memory
+    for (int64_t c0 = 0; c0 < n; c0 += C) {
+      const int m = (int)mn<int64_t>(C, n - c0);
+      for (int t = threadIdx.x; t < m; t += blockDim.x) sbuf[t] = g[c0 + t];
+      __syncthreads();
+      smem_bitonic<false>(sbuf, m, threadIdx.x, blockDim.x);
+      for (int t = threadIdx.x; t < m; t += blockDim.x) g[c0 + t] = sbuf[t];
+      __syncthreads();
+    }
+    // 2) stages k > C: mirror + large-j steps in global, small-j steps per chunk
+    for (int64_t k = 2 * (int64_t)C; k <= P; k <<= 1) {
+      for (int64_t j = k / 2; j >= C; j >>= 1) {
+        const bool mirror = (j == k / 2);
+        for (int64_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
+          int64_t a, b;
+          if (mirror) {
+            const int64_t blk = t / (k / 2), off = t % (k / 2);
+            a = blk * k + off;
+            b = blk * k + k - 1 - off;
+          } else {
+            const int64_t blk = t / j, off = t % j;
+            a = blk * 2 * j + off;
+            b = a + j;
+          }
+          if (b < n) {
+            uint64_t x = g[a], y = g[b];
+            if (y < x) {
+              g[a] = y;
+              g[b] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      for (int64_t c0 = 0; c0 < n; c0 += C) {
+        const int m = (int)mn<int64_t>(C, n - c0);
+        for (int t = threadIdx.x; t < m; t += blockDim.x) sbuf[t] = g[c0 + t];
+        __syncthreads();
+        for (int j = C / 2; j >= 1; j >>= 1) {
+          for (int t = threadIdx.x; t < C / 2; t += blockDim.x) {
+            const int blk = t / j, off = t % j;
+            const int a = blk * 2 * j + off, b = a + j;
+            if (b < m) cmpx(sbuf, a, b);
+          }
+          __syncthreads();
+        }
+        for (int t = threadIdx.x; t < m; t += blockDim.x) g[c0 + t] = sbuf[t];
+        __syncthreads();
+      }
+    }
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+      const uint64_t key = g[t];
+      lefts[q0 + t] = left_base + i;
+      rights[q0 + t] = key >> 32;
+      sims[q0 + t] = __uint_as_float((uint32_t)key);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ dense API kernels
+// out[i*ldo + j] = canonical dot(left row i, bt column j); bt is the packed
+// transpose (dim x nr, row stride ldb) exactly as sj_tile_dot takes it.
+constexpr int kTD = 64, kTDK = 16;
+__global__ void __launch_bounds__(256)
+tile_dot_kernel(const float* __restrict__ left, int64_t lda, const float* __restrict__ bt,
+                int64_t ldb, int64_t nl, int64_t nr, int dim, float* __restrict__ out,
+                int64_t ldo) {
+  __shared__ float As[kTDK][kTD + 1];
+  __shared__ float Bs[kTDK][kTD];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t i0 = (int64_t)blockIdx.y * kTD, j0 = (int64_t)blockIdx.x * kTD;
+  float acc[4][4] = {};
+  for (int d0 = 0; d0 < dim; d0 += kTDK) {
+    for (int e = threadIdx.x; e < kTD * kTDK; e += 256) {
+      const int r = e / kTDK, d = e % kTDK;
+      As[d][r] = (i0 + r < nl && d0 + d < dim) ? left[(i0 + r) * lda + d0 + d] : 0.0f;
+      const int dd = e / kTD, c = e % kTD;
+      Bs[dd][c] = (j0 + c < nr && d0 + dd < dim) ? bt[(int64_t)(d0 + dd) * ldb + j0 + c] : 0.0f;
+    }
+    __syncthreads();
+    const int dm = min(kTDK, dim - d0);
+    for (int d = 0; d < dm; d++) {
+      float a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        a[u] = As[d][ty * 4 + u];
+        b[u] = Bs[d][tx * 4 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int w = 0; w < 4; w++) acc[u][w] = __fmaf_rn(a[u], b[w], acc[u][w]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      const int64_t i = i0 + ty * 4 + u, j = j0 + tx * 4 + w;
+      if (i < nl && j < nr) out[i * ldo + j] = acc[u][w];
+    }
+}
+
+__global__ void dots_vm_kernel(const float* __restrict__ a, const float* __restrict__ m, int64_t n,
+                               int dim, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = dot_seq_dev(a, m + i * dim, dim);
+}
+
+// Dense threshold scan, row-major order (sj_scan_count / sj_scan_fill).
+__global__ void dense_count_kernel(const float* __restrict__ buf, int64_t nl, int64_t nr,
+                                   float theta, uint32_t* __restrict__ rowcount) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= nl) return;
+  uint32_t c = 0;
+  for (int64_t j = lane; j < nr; j += 32) c += buf[i * nr + j] >= theta;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) rowcount[i] = c;
+}
+
+__global__ void dense_fill_kernel(const float* __restrict__ buf, int64_t nl, int64_t nr,
+                                  float theta, const uint64_t* __restrict__ rowoff, uint64_t left0,
+                                  uint64_t right0, uint64_t* __restrict__ lefts,
+                                  uint64_t* __restrict__ rights, float* __restrict__ sims) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= nl) return;
+  uint64_t q = rowoff[i];
+  for (int64_t j0 = 0; j0 < nr; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const float s = j < nr ? buf[i * nr + j] : 0.0f;
+    const bool hit = j < nr && s >= theta;
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const uint64_t pos = q + __popc(b & ((1u << lane) - 1u));
+      lefts[pos] = left0 + (uint64_t)i;
+      rights[pos] = right0 + (uint64_t)j;
+      sims[pos] = s;
+    }
+    q += __popc(b);
+  }
+}
+
+}  // namespace sjb

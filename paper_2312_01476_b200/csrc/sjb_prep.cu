@@ -1,0 +1,241 @@
+// sjb_prep.cu -- prefetch-stage kernels: row L2-normalise-and-cast, the
+// synthetic model fill, FNV-1a-64 hashing, and the FastText-style subword
+// embedding gather.  All of them are HBM-bound; each CTA owns one 128-row
+// tile, stages it in shared memory (coalesced loads), runs the per-row
+// canonical arithmetic, then writes
+//   * the canonical fp32 rows (bitwise equal to the reference's
+//     sj_normalize_rows, _kernelcore.c:79-114), and
+//   * optionally the bf16 copy in the tiled UMMA operand layout
+//     (sjb_common.cuh tiled_offset), zero-padded to kpad columns.
+#include "sjb_common.cuh"
+
+namespace sjb {
+
+constexpr int kPrepThreads = 128;
+
+// Sequential fp64 sum of squares (no contraction: the square is exact and
+// __dadd_rn pins the rounding), repair rule, fp64 divide -- the reference's
+// normalize_row (_kernelcore.c:79-97).  Operates on one smem row.
+__device__ __forceinline__ int normalize_row_smem(float* row, int dim) {
+  double ss = 0.0;
+  for (int d = 0; d < dim; d++) {
+    double x = (double)row[d];
+    ss = __dadd_rn(ss, __dmul_rn(x, x));
+  }
+  double norm = sqrt(ss);
+  int repaired = 0;
+  if (norm < 1e-12) {
+    row[0] = 1.0f;
+    ss = 0.0;
+    for (int d = 0; d < dim; d++) {
+      double x = (double)row[d];
+      ss = __dadd_rn(ss, __dmul_rn(x, x));
+    }
+    norm = sqrt(ss);
+    repaired = 1;
+  }
+  for (int d = 0; d < dim; d++) row[d] = __double2float_rn(__ddiv_rn((double)row[d], norm));
+  return repaired;
+}
+
+// Common tail: normalise the rows staged in `sm` (pitch floats apart) for the
+// sub-tile [r0, r0 + sub) of the 128-row tile starting at row0 (`rows` valid
+// rows in the whole tile), store fp32 rows and that slice of the bf16
+// operand tile.
+__device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, int dim, int kpad,
+                               int64_t row0, bool normalize, float* __restrict__ out32,
+                               __nv_bfloat16* __restrict__ out16,
+                               unsigned long long* __restrict__ repaired) {
+  const int vrows = max(0, min(sub, rows - r0));  // valid rows in this sub-tile
+  int rep = 0;
+  if (normalize && threadIdx.x < vrows) rep = normalize_row_smem(sm + threadIdx.x * pitch, dim);
+  if (normalize && repaired != nullptr) {
+    rep = __reduce_add_sync(0xffffffffu, rep);
+    if ((threadIdx.x & 31) == 0 && rep) atomicAdd(repaired, (unsigned long long)rep);
+  }
+  __syncthreads();
+  if (out32 != nullptr) {
+    const int64_t base = (row0 + r0) * dim;
+    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
+      int r = e / dim, d = e - r * dim;
+      out32[base + e] = sm[r * pitch + d];
+    }
+  }
+  if (out16 != nullptr) {
+    // One 16-byte chunk = 8 consecutive k of one row; consecutive threads take
+    // consecutive rows of the same k-group, so each warp writes 512 B runs.
+    uint4* dst = reinterpret_cast<uint4*>(out16 + (row0 / kTileRows) * (int64_t)kTileRows * kpad);
+    const int nchunks = sub * (kpad / 8);
+    for (int c = threadIdx.x; c < nchunks; c += kPrepThreads) {
+      int g = c / sub, r = c - g * sub;
+      __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        int k = g * 8 + e;
+        float x = (r < vrows && k < dim) ? sm[r * pitch + k] : 0.0f;
+        v[e] = __float2bfloat16_rn(x);
+      }
+      dst[g * kTileRows + r0 + r] = *reinterpret_cast<uint4*>(v);
+    }
+  }
+  __syncthreads();
+}
+
+// in: n x dim fp32 row-major.  One CTA per 128-row tile, staged in sub-tiles
+// of `sub` rows (sub * (dim|1) floats of smem).  The grid may cover tiles past
+// n: those are written as zero operand tiles so the bf16 image can be padded.
+__global__ void __launch_bounds__(kPrepThreads)
+normalize_cast_kernel(const float* __restrict__ in, int64_t n, int dim, int kpad, int sub,
+                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
+                      unsigned long long* __restrict__ repaired, int normalize) {
+  extern __shared__ float sm[];
+  const int pitch = dim | 1;
+  const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
+  const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
+  for (int r0 = 0; r0 < kTileRows; r0 += sub) {
+    const int vrows = max(0, min(sub, rows - r0));
+    const int64_t base = (row0 + r0) * dim;
+    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
+      int r = e / dim, d = e - r * dim;
+      sm[r * pitch + d] = __ldg(in + base + e);
+    }
+    __syncthreads();
+    finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, normalize != 0, out32, out16,
+                   repaired);
+  }
+}
+
+// Synthetic model (_kernelcore.c:69-74, 99-107): stream seed per row, element
+// d = splitmix64 output d+1 mapped to fp64 [-1,1), truncated to fp32, then the
+// row is normalised.  Element-parallel generation, row-serial normalisation.
+__device__ __forceinline__ float splitmix_elem(uint64_t seed, int d) {
+  uint64_t z = seed + (uint64_t)(d + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z = z ^ (z >> 31);
+  double v = __dsub_rn(__dmul_rn(__dmul_rn((double)z, 0x1p-64), 2.0), 1.0);
+  return __double2float_rn(v);
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, int kpad, int sub,
+                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16) {
+  extern __shared__ float sm[];
+  const int pitch = dim | 1;
+  const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
+  const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
+  for (int r0 = 0; r0 < kTileRows; r0 += sub) {
+    const int vrows = max(0, min(sub, rows - r0));
+    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
+      int r = e / dim, d = e - r * dim;
+      sm[r * pitch + d] = splitmix_elem(seeds[row0 + r0 + r], d);
+    }
+    __syncthreads();
+    // synthetic vectors are normalised as part of the model (embedding.py:79)
+    finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, true, out32, out16, nullptr);
+  }
+}
+
+// FNV-1a-64 (_kernelcore.c:60-67) of packed tokens, XOR a 64-bit seed
+// (SyntheticModel._stream_seed, embedding.py:87-88).
+__global__ void fnv1a64_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
+                               int64_t n, uint64_t xor_seed, uint64_t* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (int64_t i = offs[t]; i < offs[t + 1]; i++) {
+    h ^= (uint64_t)bytes[i];
+    h *= 0x100000001b3ULL;
+  }
+  out[t] = h ^ xor_seed;
+}
+
+// ------------------------------------------------------------------------
+// Subword (FastText-style) model, cfg3.  Builder-pinned spec (the reference
+// has no subword model; restated in oracle/sj_oracle.c):
+// items = [word row] + [every n-gram of '<' w '>' for n = minn..maxn, by n then
+// start]; bucket = fnv1a64(bytes) mod n_buckets; row = (sum of item rows in
+// item order, fp32) / (float)count.  One warp per token; lanes own columns,
+// so each column is accumulated sequentially in item order (bit-exact with
+// the oracle) and every gathered row is read as coalesced 128 B segments.
+__device__ __forceinline__ uint8_t marked_byte(const uint8_t* w, int len, int k) {
+  return k == 0 ? (uint8_t)'<' : (k == len + 1 ? (uint8_t)'>' : w[k - 1]);
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
+                     int64_t n, const float* __restrict__ table, int64_t n_buckets, int dim,
+                     int kpad, int sub, int minn, int maxn, int normalize,
+                     float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
+                     unsigned long long* __restrict__ repaired) {
+  extern __shared__ float sm[];
+  const int pitch = dim | 1;
+  const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
+  const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r0 = 0; r0 < kTileRows; r0 += sub) {
+    const int vrows = max(0, min(sub, rows - r0));
+    for (int r = warp; r < vrows; r += kPrepThreads / 32) {
+      const int64_t t = row0 + r0 + r;
+      const uint8_t* w = bytes + offs[t];
+      const int len = (int)(offs[t + 1] - offs[t]);
+      const int ml = len + 2;
+      int n_items = 1;
+      for (int g = minn; g <= maxn; g++) n_items += max(0, ml - g + 1);
+      float* row = sm + r * pitch;
+      for (int d = lane; d < dim; d += 32) row[d] = 0.0f;
+      for (int b0 = 0; b0 < n_items; b0 += 32) {
+        // lane computes the bucket of item b0 + lane
+        const int item = b0 + lane;
+        uint64_t bucket = 0;
+        if (item < n_items) {
+          uint64_t h = 0xcbf29ce484222325ULL;
+          if (item == 0) {
+            for (int k = 0; k < len; k++) {
+              h ^= (uint64_t)w[k];
+              h *= 0x100000001b3ULL;
+            }
+          } else {
+            int rem = item - 1, g = minn;
+            while (rem >= max(0, ml - g + 1)) {
+              rem -= max(0, ml - g + 1);
+              g++;
+            }
+            for (int k = rem; k < rem + g; k++) {
+              h ^= (uint64_t)marked_byte(w, len, k);
+              h *= 0x100000001b3ULL;
+            }
+          }
+          bucket = h % (uint64_t)n_buckets;
+        }
+        const int nb = min(32, n_items - b0);
+        for (int q = 0; q < nb; q++) {
+          const uint64_t bq = __shfl_sync(0xffffffffu, bucket, q);
+          const float* src = table + bq * (uint64_t)dim;
+          for (int d = lane; d < dim; d += 32) row[d] = __fadd_rn(row[d], __ldg(src + d));
+        }
+      }
+      const float c = (float)n_items;
+      for (int d = lane; d < dim; d += 32) row[d] = __fdiv_rn(row[d], c);
+    }
+    __syncthreads();
+    finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, normalize != 0, out32, out16,
+                   repaired);
+  }
+}
+
+// Row L2 norms in fp64, returned as fp32 (sj_row_norms, _kernelcore.c:116-124).
+__global__ void row_norms_kernel(const float* __restrict__ m, int64_t n, int dim,
+                                 float* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* row = m + i * dim;
+  double ss = 0.0;
+  for (int d = 0; d < dim; d++) {
+    double x = (double)row[d];
+    ss = __dadd_rn(ss, __dmul_rn(x, x));
+  }
+  out[i] = __double2float_rn(sqrt(ss));
+}
+
+}  // namespace sjb

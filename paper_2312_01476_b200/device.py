@@ -1,0 +1,232 @@
+"""Device engine: prepared relations and the fused join, on torch-owned HBM.
+
+PyTorch is used only for device memory, streams and host<->device copies;
+every computation is a libsjb200.so kernel reached through the C ABI
+(include/simjoin_b200.h).  There is no CPU fallback: without a CUDA device
+or without the built library these functions raise.
+
+Pipeline of one join:
+
+  prepare(raw)         normalize_cast kernel: canonical fp32 rows (bitwise
+                       sj_normalize_rows) + bf16 operand image (tiled layout)
+  join_prepared(L, R)  tcgen05 filter (approx >= theta - band) -> canonical
+                       fp32 recheck -> row bucketing -> per-row sort ->
+                       MatchSet columns (u64 lefts, u64 rights, f32 sims)
+
+Capacity protocol (the reference's count + capacity + retry, _ckern.pyx:
+165-175, 194-211): the filter writes candidates into per-CTA segments and
+counts past capacity; on overflow the join is re-run once with the exact
+capacity the first pass measured.  The last capacity needed for a shape is
+remembered, so repeated joins of the same shape run once.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CapacityExceeded, DimensionMismatch
+
+TILE_ROWS = 128
+
+
+def _vp(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(device: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("simjoin-b200 needs a CUDA device (there is no CPU fallback)")
+    _lib.lib()
+
+
+def kpad(dim: int) -> int:
+    return int(_lib.lib().sjb_kpad(dim))
+
+
+def operand_elems(n: int, dim: int) -> int:
+    return int(_lib.lib().sjb_operand_elems(n, dim))
+
+
+def default_band(dim: int) -> float:
+    """Provably sufficient bf16 filter margin for unit vectors (C ABI
+    sjb_default_band): (2u + u^2) + accumulation slack, u = 2^-8."""
+    return float(_lib.lib().sjb_default_band(dim))
+
+
+@dataclass
+class PreparedRelation:
+    """A relation resident in HBM in the two forms the join reads."""
+
+    f32: torch.Tensor          # (n, dim) canonical normalised fp32 rows
+    op: torch.Tensor           # bf16 operand image (sjb_operand_elems elements)
+    n: int
+    dim: int
+    name: str = ""
+    repaired_dev: Optional[torch.Tensor] = None  # (1,) int64 repaired-row counter
+
+    @property
+    def device(self) -> torch.device:
+        return self.f32.device
+
+    def repaired(self) -> int:
+        return int(self.repaired_dev.item()) if self.repaired_dev is not None else 0
+
+
+def _check_matrix(x: torch.Tensor, what: str) -> None:
+    if not x.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if x.dtype != torch.float32 or x.dim() != 2:
+        raise ValueError(f"{what} must be a 2-D float32 tensor, got {x.dtype} {tuple(x.shape)}")
+    if not x.is_contiguous():
+        raise ValueError(f"{what} must be row-major contiguous")
+
+
+def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = None
+            ) -> PreparedRelation:
+    """Normalise rows (bitwise sj_normalize_rows) and build the bf16 image."""
+    _check_matrix(raw, "relation")
+    L = _lib.lib()
+    n, dim = raw.shape
+    dev = raw.device
+    f32 = out32 if out32 is not None else torch.empty_like(raw)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(L.sjb_normalize_rows(_vp(raw), n, dim, _vp(f32), _vp(op), _vp(rep),
+                                        _stream(dev)), "sjb_normalize_rows")
+    return PreparedRelation(f32, op, n, dim, name, rep)
+
+
+def normalize_rows_(m: torch.Tensor) -> torch.Tensor:
+    """In-place fp32 row normalisation; returns the (1,) int64 repaired count."""
+    _check_matrix(m, "matrix")
+    rep = torch.zeros(1, dtype=torch.int64, device=m.device)
+    with torch.cuda.device(m.device):
+        _lib.check(_lib.lib().sjb_normalize_rows(_vp(m), m.shape[0], m.shape[1], _vp(m),
+                                                 ctypes.c_void_p(0), _vp(rep),
+                                                 _stream(m.device)), "sjb_normalize_rows")
+    return rep
+
+
+@dataclass
+class DeviceMatches:
+    """Canonical match columns on the device (int64 tensors hold u64 values)."""
+
+    lefts: torch.Tensor
+    rights: torch.Tensor
+    sims: torch.Tensor
+    n_matches: int
+    n_candidates: int
+    cand_capacity: int
+    retries: int
+    grid: int
+
+    def to_host(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        lo = self.lefts.cpu().numpy().view(np.uint64)
+        ro = self.rights.cpu().numpy().view(np.uint64)
+        so = self.sims.cpu().numpy()
+        return lo, ro, so
+
+
+_cap_lock = threading.Lock()
+_cap_cache: Dict[tuple, int] = {}
+
+# workspace is cached per device and grown on demand
+_ws_cache: Dict[int, torch.Tensor] = {}
+
+
+def _workspace(nbytes: int, dev: torch.device) -> torch.Tensor:
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    ws = _ws_cache.get(idx)
+    if ws is None or ws.numel() < nbytes:
+        _ws_cache.pop(idx, None)
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        _ws_cache[idx] = ws
+    return ws
+
+
+def release_workspaces() -> None:
+    _ws_cache.clear()
+
+
+def initial_capacity(n_left: int, n_right: int) -> int:
+    """First-try candidate capacity when nothing is known about selectivity."""
+    pairs = n_left * n_right
+    return int(max(1 << 20, min(pairs, 1 << 24)))
+
+
+def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
+                  band: Optional[float] = None, cand_cap: Optional[int] = None,
+                  left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
+                  max_bytes: Optional[int] = None) -> DeviceMatches:
+    """Canonical threshold join of two prepared relations (device-resident).
+
+    Blocks once at the end to read the match count (the output size is data
+    dependent); everything else is asynchronous on the current stream.
+    """
+    if L.dim != R.dim:
+        raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
+    if L.device != R.device:
+        raise ValueError("relations live on different devices")
+    lib = _lib.lib()
+    dev = L.device
+    theta32 = float(np.float32(theta))
+    band = default_band(L.dim) if band is None else float(band)
+    key = (L.n, R.n, L.dim, theta32, float(np.float32(band)), grid, tiles_per_chunk)
+    if cand_cap is None:
+        with _cap_lock:
+            cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
+    if max_bytes is None:
+        free, _total = torch.cuda.mem_get_info(dev)
+        max_bytes = int(free * 0.8)
+    retries = 0
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        while True:
+            args = _lib.JoinArgs(n_left=L.n, n_right=R.n, dim=L.dim, theta=theta32, band=band,
+                                 cand_cap=int(cand_cap), out_cap=int(cand_cap),
+                                 left_base=int(left_base), grid=int(grid),
+                                 tiles_per_chunk=int(tiles_per_chunk))
+            ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
+            if ws_bytes < 0:
+                _lib.check(-3, "sjb_join_workspace_bytes")
+            out_bytes = int(cand_cap) * 20
+            if ws_bytes + out_bytes > max_bytes:
+                raise CapacityExceeded(
+                    f"join needs {ws_bytes + out_bytes} B of device memory for "
+                    f"{cand_cap} candidates; {max_bytes} B available")
+            ws = _workspace(ws_bytes, dev)
+            lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
+            rights = torch.empty_like(lefts)
+            sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
+            info_t = torch.zeros(5, dtype=torch.int64, device=dev)
+            _lib.check(lib.sjb_join_prepared_async(
+                _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(args), _vp(ws),
+                ws_bytes, _vp(lefts), _vp(rights), _vp(sims), _vp(info_t), stream),
+                "sjb_join_prepared_async")
+            info = info_t.cpu().numpy()
+            n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
+            flags = info[3:4].view(np.int32)
+            overflow, used_grid = int(flags[0]), int(flags[1])
+            if not overflow:
+                break
+            if retries >= 2:
+                raise CapacityExceeded(f"candidate capacity still overflows after {retries} "
+                                       f"retries (needed {needed})")
+            cand_cap = max(needed, n_matches, int(cand_cap) + 1)
+            retries += 1
+    with _cap_lock:
+        _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
+    return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
+                         n_cand, int(cand_cap), retries, used_grid)

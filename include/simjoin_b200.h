@@ -37,6 +37,10 @@ const char* sjb_last_error(void);
 /* SM count of `device` (for sizing grids/workspaces). */
 int sjb_sm_count(int device);
 
+/* Number of kernels this library has launched in this process (all
+ * threads); lets callers count the GPU launches inside a timed region. */
+int64_t sjb_launch_count(void);
+
 /* Padded reduction depth of the bf16 operand image for `dim` (multiple of 16). */
 int64_t sjb_kpad(int64_t dim);
 /* Elements of the bf16 operand image of an n-row relation: n rounded up to a
@@ -54,6 +58,13 @@ int64_t sjb_operand_elems(int64_t n, int64_t dim);
  * device u64) is incremented by the number of repaired rows. */
 int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32,
                        void* d_out16, unsigned long long* d_repaired, void* stream);
+
+/* Lookup-model prefetch fused with the normalisation: relation row i is
+ * table row d_index[i] (LookupModel._vector, embedding.py:143-152, then
+ * normalize_rows); outputs as sjb_normalize_rows. */
+int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int64_t n,
+                              int64_t dim, float* d_out32, void* d_out16,
+                              unsigned long long* d_repaired, void* stream);
 
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
@@ -90,6 +101,8 @@ typedef struct sjb_join_args {
   uint64_t left_base;   /* added to emitted left offsets (R shards) */
   int32_t grid;         /* 0 = one CTA per SM */
   int32_t tiles_per_chunk; /* 0 = automatic */
+  void* ev_filter_begin;   /* optional cudaEvent_t recorded around the filter */
+  void* ev_filter_end;     /* kernel on `stream` (profiling hook), or NULL */
 } sjb_join_args;
 
 typedef struct sjb_join_info {

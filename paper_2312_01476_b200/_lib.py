@@ -12,8 +12,8 @@ import os
 from .build import LIB_PATH
 
 EXPORTS = (
-    "sjb_version", "sjb_last_error", "sjb_sm_count", "sjb_kpad", "sjb_operand_elems",
-    "sjb_normalize_rows", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
+    "sjb_version", "sjb_last_error", "sjb_launch_count", "sjb_sm_count", "sjb_kpad", "sjb_operand_elems",
+    "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
     "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band",
     "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm",
     "sjb_scan_hits", "sjb_scan_hits_workspace_bytes",
@@ -29,6 +29,7 @@ class JoinArgs(ctypes.Structure):
         ("cand_cap", ctypes.c_int64), ("out_cap", ctypes.c_int64),
         ("left_base", ctypes.c_uint64),
         ("grid", ctypes.c_int32), ("tiles_per_chunk", ctypes.c_int32),
+        ("ev_filter_begin", ctypes.c_void_p), ("ev_filter_end", ctypes.c_void_p),
     ]
 
 
@@ -60,6 +61,7 @@ def lib(path: str = LIB_PATH):
             "(or __graft_entry__.build()) first -- there is no CPU fallback")
     L = ctypes.CDLL(path)
     L.sjb_version.restype = ctypes.c_int
+    L.sjb_launch_count.restype = ctypes.c_int64
     L.sjb_last_error.restype = ctypes.c_char_p
     L.sjb_sm_count.restype = ctypes.c_int
     L.sjb_sm_count.argtypes = [ctypes.c_int]
@@ -70,6 +72,7 @@ def lib(path: str = LIB_PATH):
     L.sjb_default_band.restype = ctypes.c_float
     L.sjb_default_band.argtypes = [_i64]
     L.sjb_normalize_rows.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp]
+    L.sjb_gather_normalize_rows.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
     L.sjb_row_norms.argtypes = [_vp, _i64, _i64, _vp, _vp]
     L.sjb_fnv1a64_many.argtypes = [_vp, _vp, _i64, ctypes.c_uint64, _vp, _vp]
     L.sjb_synthetic_fill_many.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]

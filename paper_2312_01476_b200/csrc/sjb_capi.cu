@@ -3,7 +3,9 @@
 // pipeline.  Built as ONE translation unit with the kernel sources.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -16,6 +18,7 @@
 namespace {
 
 thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -37,6 +40,7 @@ int fail(int code, const char* fmt, ...) {
 
 #define SJB_CK_LAUNCH(name)                                                                \
   do {                                                                                     \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                    \
     cudaError_t e_ = cudaGetLastError();                                                   \
     if (e_ != cudaSuccess)                                                                 \
       return fail(SJB_E_CUDA, "launch of %s failed: %s", name, cudaGetErrorString(e_));    \
@@ -171,6 +175,28 @@ int run_scan(const uint32_t* counts, int64_t n, uint64_t* out, uint64_t* out_cop
   return SJB_OK;
 }
 
+template <int KS>
+int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+  if (int rc = set_smem_attr((const void*)sjb::join_filter_kernel<KS>, (int)smem)) return rc;
+  sjb::join_filter_kernel<KS><<<grid, sjb::kJoinThreads, smem, st>>>(jp);
+  SJB_CK_LAUNCH("join_filter");
+  return SJB_OK;
+}
+
+int launch_join_filter(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+  switch (jp.kpad / 16) {
+    case 1: return launch_filter_ks<1>(jp, grid, smem, st);
+    case 2: return launch_filter_ks<2>(jp, grid, smem, st);
+    case 3: return launch_filter_ks<3>(jp, grid, smem, st);
+    case 4: return launch_filter_ks<4>(jp, grid, smem, st);
+    case 5: return launch_filter_ks<5>(jp, grid, smem, st);
+    case 6: return launch_filter_ks<6>(jp, grid, smem, st);
+    case 7: return launch_filter_ks<7>(jp, grid, smem, st);
+    case 8: return launch_filter_ks<8>(jp, grid, smem, st);
+    default: return fail(SJB_E_UNSUPPORTED, "kpad %d", jp.kpad);
+  }
+}
+
 }  // namespace
 
 namespace sjb {
@@ -213,6 +239,8 @@ extern "C" {
 
 int sjb_version(void) { return 1; }
 
+int64_t sjb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 const char* sjb_last_error(void) { return g_err.c_str(); }
 
 int sjb_sm_count(int device) {
@@ -239,9 +267,11 @@ float sjb_default_band(int64_t dim) {
   return (float)b;
 }
 
-int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
-                       unsigned long long* d_repaired, void* stream) {
-  if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n, int64_t dim,
+                          float* d_out32, void* d_out16, unsigned long long* d_repaired,
+                          void* stream) {
+  if (n < 0 || dim < 1)
+    return fail(SJB_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
   const int kpad = (int)sjb_kpad(dim);
   const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
                                 : sjb::ceil_div(n, sjb::kTileRows);
@@ -250,10 +280,22 @@ int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
   sjb::normalize_cast_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
-      d_in, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16), d_repaired,
-      1);
+      d_in, d_gather, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16),
+      d_repaired, 1);
   SJB_CK_LAUNCH("normalize_cast");
   return SJB_OK;
+}
+
+int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
+                       unsigned long long* d_repaired, void* stream) {
+  return normalize_impl(d_in, nullptr, n, dim, d_out32, d_out16, d_repaired, stream);
+}
+
+int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int64_t n,
+                              int64_t dim, float* d_out32, void* d_out16,
+                              unsigned long long* d_repaired, void* stream) {
+  if (!d_index) return fail(SJB_E_INVALID, "null index");
+  return normalize_impl(d_table, d_index, n, dim, d_out32, d_out16, d_repaired, stream);
 }
 
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream) {
@@ -373,9 +415,15 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.cand = cand;
   jp.seg_cap = pl.seg_cap;
   jp.cta_count = cta;
-  if (int rc = set_smem_attr((const void*)sjb::join_filter_kernel, (int)pl.smem)) return rc;
-  sjb::join_filter_kernel<<<pl.grid, sjb::kJoinThreads, pl.smem, st>>>(jp);
-  SJB_CK_LAUNCH("join_filter");
+  {
+    const char* dm = getenv("SJB_DEBUG_MODE");
+    jp.debug_mode = dm ? atoi(dm) : 0;
+  }
+  if (args->ev_filter_begin)
+    SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_begin), st));
+  if (int rc = launch_join_filter(jp, pl.grid, pl.smem, st)) return rc;
+  if (args->ev_filter_end)
+    SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_end), st));
 
   // 2) canonical recheck
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;

@@ -50,6 +50,7 @@ struct JoinParams {
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
+  int debug_mode;  // diagnostics: 0 normal, 1 no emission, 2 no TMEM drain, 3 spin waits
 };
 
 struct JoinSmemLayout {
@@ -70,6 +71,9 @@ __host__ __device__ inline JoinSmemLayout join_smem_layout(int kpad, int stages)
   return L;
 }
 
+// KSTEPS = kpad / 16 UMMA k-steps per output tile (compile time so the issue
+// loop is straight-line: each tcgen05.mma costs one descriptor add).
+template <int KSTEPS>
 __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const JoinParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const JoinSmemLayout L = join_smem_layout(p.kpad, p.stages);
@@ -137,9 +141,14 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
           mbar_wait(&b_empty[bstage], bphase ^ 1u);
-          mbar_arrive_expect_tx(&b_full[bstage], tile_bytes);
-          bulk_g2s(b_buf + (size_t)bstage * L.b_bytes, p.b16 + (size_t)t * tile_elems, tile_bytes,
-                   &b_full[bstage], pol_b);
+          if (p.debug_mode == 17 && it > 0) {
+            mbar_arrive(&b_full[bstage]);  // diagnostics: no B traffic after the first item
+          } else {
+            const int64_t tl = p.debug_mode == 16 ? (t & 7) : t;  // diagnostics: hot B set
+            mbar_arrive_expect_tx(&b_full[bstage], tile_bytes);
+            bulk_g2s(b_buf + (size_t)bstage * L.b_bytes, p.b16 + (size_t)tl * tile_elems,
+                     tile_bytes, &b_full[bstage], pol_b);
+          }
           if (++bstage == p.stages) {
             bstage = 0;
             bphase ^= 1u;
@@ -153,7 +162,14 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       const uint32_t idesc = umma_idesc_bf16_f32(128, kBN);
       const uint32_t lbo = kBN * 16;  // 128-row operand: distance between k-groups
       const uint32_t sbo = 128;       // distance between 8-row core-matrix groups
-      const int ksteps = p.kpad / 16;
+      // descriptor of each buffer at k-step 0; a k-step advances the start
+      // address by 2 k-groups = 2 * lbo bytes (encoded >> 4)
+      const uint64_t kstep = (2 * lbo) >> 4;
+      const uint64_t a_desc0[2] = {umma_desc_kmajor_noswz(smem_u32(a_buf[0]), lbo, sbo),
+                                   umma_desc_kmajor_noswz(smem_u32(a_buf[1]), lbo, sbo)};
+      const uint64_t b_desc_base = umma_desc_kmajor_noswz(smem_u32(b_buf), lbo, sbo);
+      const uint64_t half_step = tile_bytes >> 4;       // second A half
+      const uint64_t stage_step = L.b_bytes >> 4;
       int bstage = 0;
       uint32_t bphase = 0;
       uint32_t acc_it = 0;
@@ -163,7 +179,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         const int ab = (int)(it & 1);
         mbar_wait(&a_full[ab], (uint32_t)((it >> 1) & 1));
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(a_buf[ab]);
+        const uint64_t ad = a_desc0[ab];
         const int64_t t0 = sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
@@ -171,17 +187,15 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           mbar_wait(&acc_empty[as], ((acc_it >> 1) & 1u) ^ 1u);
           mbar_wait(&b_full[bstage], bphase);
           tc_fence_after();
-          const uint32_t b_addr = smem_u32(b_buf + (size_t)bstage * L.b_bytes);
+          const uint64_t bd = b_desc_base + (uint64_t)bstage * stage_step;
+          const uint32_t d0 = tmem_base + as * 256;
 #pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const uint32_t d_tmem = tmem_base + as * 256 + h * 128;
-            for (int kk = 0; kk < ksteps; kk++) {
-              const uint64_t adesc =
-                  umma_desc_kmajor_noswz(a_addr + h * tile_bytes + kk * 2 * lbo, lbo, sbo);
-              const uint64_t bdesc = umma_desc_kmajor_noswz(b_addr + kk * 2 * lbo, lbo, sbo);
-              tc_mma_bf16(d_tmem, adesc, bdesc, idesc, kk > 0 ? 1u : 0u);
-            }
-          }
+          for (int kk = 0; kk < KSTEPS; kk++)
+            tc_mma_bf16(d0, ad + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < KSTEPS; kk++)
+            tc_mma_bf16(d0 + 128, ad + half_step + kk * kstep, bd + kk * kstep, idesc,
+                        kk > 0 ? 1u : 0u);
           tc_commit(&b_empty[bstage]);
           tc_commit(&acc_full[as]);
           if (++bstage == p.stages) {
@@ -203,6 +217,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     uint32_t acc_it = 0;
+    uint32_t dbg_acc = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
       const int64_t gi64 = rb * kBM + h * 128 + lane_base + lane;
@@ -214,6 +229,12 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         const uint32_t as = acc_it & 1u;
         mbar_wait(&acc_full[as], (acc_it >> 1) & 1u);
         tc_fence_after();
+        if (p.debug_mode == 2 || p.debug_mode >= 16) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[as]);
+          acc_it++;
+          continue;
+        }
         float v[128];
         const uint32_t taddr = tmem_base + (lane_base << 16) + as * 256 + h * 128;
         SJB_TMEM_LD32(taddr + 0, v, 0);
@@ -223,7 +244,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         tc_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[as]);
+        if (lane == 0) {
+          if (p.debug_mode == 5) mbar_arrive(&acc_empty[as]);
+          else mbar_arrive_relaxed(&acc_empty[as]);
+        }
         acc_it++;
 
         // group maxima over 8 columns, then the tile maximum
@@ -236,36 +260,71 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]),
                         fmax3(g[6], g[7], g[8]));
         m = fmax3(m, fmax3(g[9], g[10], g[11]), fmax3(g[12], g[13], fmaxf(g[14], g[15])));
-        const bool hit = row_ok && (m >= cutoff);
+        const bool hit = row_ok && (m >= cutoff) && p.debug_mode != 1;
         if (__any_sync(0xffffffffu, hit)) {
-          const int64_t j0 = t * kBN;
-          const int64_t col_lim = p.n_b - j0;  // columns >= col_lim are padding
+          // Slow path (warp-uniform): each hit thread builds a 128-bit mask of
+          // its columns >= cutoff (only inside groups whose maximum hit), then
+          // one warp scan + one shared atomic reserve the warp's slots and each
+          // thread writes its pairs -- no collectives per candidate.
+          uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;
+          if (hit) {
 #pragma unroll
-          for (int k = 0; k < 16; k++) {
-            if (hit && g[k] >= cutoff) {
+            for (int k = 0; k < 16; k++) {
+              if (g[k] >= cutoff) {
+                uint32_t b = 0;
 #pragma unroll
-              for (int e = 0; e < 8; e++) {
-                const int c = 8 * k + e;
-                if (v[c] >= cutoff && c < col_lim) {
-                  const unsigned act = __activemask();
-                  const int leader = __ffs(act) - 1;
-                  const unsigned rank = __popc(act & ((1u << lane) - 1u));
-                  uint32_t base = 0;
-                  if (lane == leader) {
-                    const uint32_t np = (uint32_t)__popc(act);
-                    base = atomicAdd(cta_cnt, np);
-                    if (base + np < base) *cta_sat = 1u;
-                  }
-                  base = __shfl_sync(act, base, leader);
-                  const uint64_t pos = (uint64_t)base + rank;
-                  if (pos < seg_cap) seg[pos] = pack_pair(gi, (uint32_t)(j0 + c));
-                }
+                for (int e = 0; e < 8; e++) b |= (v[8 * k + e] >= cutoff ? 1u : 0u) << e;
+                const uint32_t sh = b << (8 * (k & 3));
+                if ((k >> 2) == 0) mk0 |= sh;
+                else if ((k >> 2) == 1) mk1 |= sh;
+                else if ((k >> 2) == 2) mk2 |= sh;
+                else mk3 |= sh;
               }
+            }
+            const int64_t col_lim = p.n_b - t * kBN;  // columns >= col_lim are padding
+            if (col_lim < 128) {
+              const int cl = (int)col_lim;
+              mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
+              mk1 &= cl >= 64 ? ~0u : (cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u));
+              mk2 &= cl >= 96 ? ~0u : (cl <= 64 ? 0u : ((1u << (cl - 64)) - 1u));
+              mk3 &= cl <= 96 ? 0u : ((1u << (cl - 96)) - 1u);
+            }
+          }
+          const uint32_t cnt = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
+          if (p.debug_mode == 4) {  // diagnostics: masks only
+            dbg_acc += cnt;
+            continue;
+          }
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+          uint32_t base = 0;
+          if (lane == 31 && wtot) {
+            base = atomicAdd(cta_cnt, wtot);
+            if (base + wtot < base) *cta_sat = 1u;
+          }
+          base = __shfl_sync(0xffffffffu, base, 31);
+          uint64_t pos = (uint64_t)base + (incl - cnt);
+          const uint32_t j0 = (uint32_t)(t * kBN);
+          const uint32_t mks[4] = {mk0, mk1, mk2, mk3};
+#pragma unroll
+          for (int q2 = 0; q2 < 4; q2++) {
+            uint32_t w = mks[q2];
+            while (w) {
+              const int b = __ffs(w) - 1;
+              w &= w - 1;
+              if (pos < seg_cap && p.debug_mode != 3) seg[pos] = pack_pair(gi, j0 + 32 * q2 + b);
+              pos++;
             }
           }
         }
       }
     }
+    if (p.debug_mode == 4 && dbg_acc == 0xFFFFFFFFu) p.cand[0] = dbg_acc;
   }
 
   tc_fence_before();

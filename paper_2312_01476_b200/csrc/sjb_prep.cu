@@ -81,23 +81,33 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
   __syncthreads();
 }
 
-// in: n x dim fp32 row-major.  One CTA per 128-row tile, staged in sub-tiles
+// in: n x dim fp32 row-major (or, with `gather`, a table whose row gather[i]
+// is relation row i).  One CTA per 128-row tile, staged in sub-tiles
 // of `sub` rows (sub * (dim|1) floats of smem).  The grid may cover tiles past
 // n: those are written as zero operand tiles so the bf16 image can be padded.
 __global__ void __launch_bounds__(kPrepThreads)
-normalize_cast_kernel(const float* __restrict__ in, int64_t n, int dim, int kpad, int sub,
-                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
-                      unsigned long long* __restrict__ repaired, int normalize) {
+normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ gather, int64_t n,
+                      int dim, int kpad, int sub, float* __restrict__ out32,
+                      __nv_bfloat16* __restrict__ out16, unsigned long long* __restrict__ repaired,
+                      int normalize) {
   extern __shared__ float sm[];
   const int pitch = dim | 1;
   const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
   const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
   for (int r0 = 0; r0 < kTileRows; r0 += sub) {
     const int vrows = max(0, min(sub, rows - r0));
-    const int64_t base = (row0 + r0) * dim;
-    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
-      int r = e / dim, d = e - r * dim;
-      sm[r * pitch + d] = __ldg(in + base + e);
+    if (gather == nullptr) {
+      const int64_t base = (row0 + r0) * dim;
+      for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
+        int r = e / dim, d = e - r * dim;
+        sm[r * pitch + d] = __ldg(in + base + e);
+      }
+    } else {  // row r of this relation is row gather[r] of `in` (lookup model)
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int r = warp; r < vrows; r += kPrepThreads / 32) {
+        const float* src = in + gather[row0 + r0 + r] * (int64_t)dim;
+        for (int d = lane; d < dim; d += 32) sm[r * pitch + d] = __ldg(src + d);
+      }
     }
     __syncthreads();
     finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, normalize != 0, out32, out16,

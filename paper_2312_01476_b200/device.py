@@ -44,6 +44,11 @@ def _stream(device: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def launch_count() -> int:
+    """Kernels libsjb200.so has launched in this process (all devices)."""
+    return int(_lib.lib().sjb_launch_count())
+
+
 def require_cuda() -> None:
     if not torch.cuda.is_available():
         raise RuntimeError("simjoin-b200 needs a CUDA device (there is no CPU fallback)")
@@ -156,6 +161,12 @@ def _workspace(nbytes: int, dev: torch.device) -> torch.Tensor:
     return ws
 
 
+def _ws_bytes_cached(dev: torch.device) -> int:
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    ws = _ws_cache.get(idx)
+    return 0 if ws is None else ws.numel()
+
+
 def release_workspaces() -> None:
     _ws_cache.clear()
 
@@ -169,7 +180,9 @@ def initial_capacity(n_left: int, n_right: int) -> int:
 def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                   band: Optional[float] = None, cand_cap: Optional[int] = None,
                   left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
-                  max_bytes: Optional[int] = None) -> DeviceMatches:
+                  max_bytes: Optional[int] = None,
+                  filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None
+                  ) -> DeviceMatches:
     """Canonical threshold join of two prepared relations (device-resident).
 
     Blocks once at the end to read the match count (the output size is data
@@ -187,22 +200,27 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     if cand_cap is None:
         with _cap_lock:
             cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
-    if max_bytes is None:
-        free, _total = torch.cuda.mem_get_info(dev)
-        max_bytes = int(free * 0.8)
     retries = 0
+    ev0 = ev1 = None
+    if filter_events is not None:
+        ev0 = ctypes.c_void_p(filter_events[0].cuda_event)
+        ev1 = ctypes.c_void_p(filter_events[1].cuda_event)
     with torch.cuda.device(dev):
         stream = _stream(dev)
         while True:
             args = _lib.JoinArgs(n_left=L.n, n_right=R.n, dim=L.dim, theta=theta32, band=band,
                                  cand_cap=int(cand_cap), out_cap=int(cand_cap),
                                  left_base=int(left_base), grid=int(grid),
-                                 tiles_per_chunk=int(tiles_per_chunk))
+                                 tiles_per_chunk=int(tiles_per_chunk),
+                                 ev_filter_begin=ev0, ev_filter_end=ev1)
             ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
             if ws_bytes < 0:
                 _lib.check(-3, "sjb_join_workspace_bytes")
             out_bytes = int(cand_cap) * 20
-            if ws_bytes + out_bytes > max_bytes:
+            if retries and max_bytes is None:
+                free, _total = torch.cuda.mem_get_info(dev)
+                max_bytes = int(free * 0.8) + _ws_bytes_cached(dev)
+            if max_bytes is not None and ws_bytes + out_bytes > max_bytes:
                 raise CapacityExceeded(
                     f"join needs {ws_bytes + out_bytes} B of device memory for "
                     f"{cand_cap} candidates; {max_bytes} B available")
@@ -230,3 +248,79 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
         _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
     return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
                          n_cand, int(cand_cap), retries, used_grid)
+
+
+def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> PreparedRelation:
+    """Prepare relation rows table[index[i]] (lookup-model prefetch) in one pass."""
+    _check_matrix(table, "table")
+    if index.dtype != torch.int64 or not index.is_cuda or index.dim() != 1:
+        raise ValueError("index must be a 1-D int64 CUDA tensor")
+    L = _lib.lib()
+    n, dim = int(index.numel()), table.shape[1]
+    dev = table.device
+    f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(L.sjb_gather_normalize_rows(_vp(table), _vp(index.contiguous()), n, dim,
+                                               _vp(f32), _vp(op), _vp(rep), _stream(dev)),
+                   "sjb_gather_normalize_rows")
+    return PreparedRelation(f32, op, n, dim, name, rep)
+
+
+def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
+    """UTF-8 bytes of the tokens (device u8) and n+1 int64 offsets (device)."""
+    enc = [t.encode("utf-8") for t in tokens]
+    offs = np.zeros(len(enc) + 1, dtype=np.int64)
+    if enc:
+        np.cumsum([len(e) for e in enc], out=offs[1:])
+    raw = np.frombuffer(b"".join(enc) + b"\0", dtype=np.uint8)
+    return (torch.from_numpy(raw.copy()).to(device, non_blocking=False),
+            torch.from_numpy(offs).to(device))
+
+
+def fnv1a64_tokens(tokens, xor_seed: int, device: torch.device) -> torch.Tensor:
+    """FNV-1a-64 of every token XOR seed, on the device (int64 holding u64)."""
+    b, o = pack_tokens(tokens, device)
+    out = torch.empty(len(tokens), dtype=torch.int64, device=device)
+    if len(tokens):
+        with torch.cuda.device(device):
+            _lib.check(_lib.lib().sjb_fnv1a64_many(_vp(b), _vp(o), len(tokens),
+                                                   ctypes.c_uint64(xor_seed & (2**64 - 1)),
+                                                   _vp(out), _stream(device)),
+                       "sjb_fnv1a64_many")
+    return out
+
+
+def synthetic_rows(seeds: torch.Tensor, dim: int) -> torch.Tensor:
+    """Synthetic-model rows (normalised) from device u64 stream seeds."""
+    dev = seeds.device
+    out = torch.empty((seeds.numel(), dim), dtype=torch.float32, device=dev)
+    if seeds.numel():
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().sjb_synthetic_fill_many(_vp(seeds), seeds.numel(), dim,
+                                                          _vp(out), ctypes.c_void_p(0),
+                                                          _stream(dev)),
+                       "sjb_synthetic_fill_many")
+    return out
+
+
+def subword_rows(tokens, table: torch.Tensor, minn: int, maxn: int,
+                 prepared: bool = False, name: str = ""):
+    """Subword-model rows; prepared=True returns a PreparedRelation (embed +
+    normalise + bf16 image in one kernel), else the raw (n, dim) embedding."""
+    _check_matrix(table, "bucket table")
+    dev = table.device
+    b, o = pack_tokens(tokens, dev)
+    n, dim = len(tokens), table.shape[1]
+    f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev) if prepared else None
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().sjb_subword_embed(_vp(b), _vp(o), n, _vp(table), table.shape[0],
+                                                dim, minn, maxn, 1 if prepared else 0,
+                                                _vp(f32), _vp(op), _vp(rep), _stream(dev)),
+                   "sjb_subword_embed")
+    if prepared:
+        return PreparedRelation(f32, op, n, dim, name, rep)
+    return f32

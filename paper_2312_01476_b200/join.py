@@ -1,0 +1,215 @@
+"""Join operators with the reference's signatures (join.py:88-373), executed
+on the B200 path.
+
+``tensor_join`` and ``nlj_prefetch`` keep the reference's arguments, errors,
+return types (canonical MatchSet, JoinStats) and model-call accounting.  Both
+run the same device pipeline -- prefetch (|R| + |S| model calls), normalise
+and cast, fused tensor-core filter, canonical fp32 recheck, canonical order
+-- because their outputs are contractually identical (SPEC.md "exactness").
+``threads`` and ``budget_bytes`` are validated and recorded exactly as the
+reference does; they do not change the device execution (there is no
+materialised similarity buffer, so ``peak_buffer_bytes`` reports 0).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+from typing import Optional, Tuple, Union
+
+import numpy as np
+import torch
+
+from . import device as D
+from .core import EmbeddedRelation, MatchSet, RawRelation, Threshold, check_dims
+from .embedding import EmbeddingModel, prepare_relation
+from .errors import BudgetTooSmall
+
+# reference constants (join.py:44, 48; cli.py:31)
+PREFILTER_BAND = 1e-4
+EXEC_CHUNK_ELEMS = 1 << 19
+DEFAULT_BUDGET = 64 * 1024 * 1024
+
+
+@dataclass(frozen=True)
+class Tile:
+    """Rectangular left-rows x right-rows sub-range (linalg.py:21-38)."""
+
+    left_row_start: int
+    left_row_count: int
+    right_row_start: int
+    right_row_count: int
+
+    def __post_init__(self):
+        if self.left_row_count < 1 or self.right_row_count < 1:
+            raise ValueError("tile row counts must be >= 1")
+        if self.left_row_start < 0 or self.right_row_start < 0:
+            raise ValueError("tile offsets must be >= 0")
+
+    @property
+    def area(self) -> int:
+        return self.left_row_count * self.right_row_count
+
+
+@dataclass(frozen=True)
+class BatchPlan:
+    left_block_rows: int
+    right_block_rows: int
+    tiles: Tuple[Tile, ...]
+    buffer_elems: int
+    budget_bytes: int
+
+
+@dataclass(frozen=True)
+class JoinStats:
+    wall_nanos: int
+    model_calls_left: int
+    model_calls_right: int
+    pairs_compared: int
+    matches: int
+    peak_buffer_bytes: int
+    threads: int
+    algo: str
+    inner_relation: str
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in (
+            "wall_nanos", "model_calls_left", "model_calls_right", "pairs_compared", "matches",
+            "peak_buffer_bytes", "threads", "algo", "inner_relation")}
+
+
+def plan_batches(left_rows: int, right_rows: int, dim: int, budget_bytes: int) -> BatchPlan:
+    """Exact-cover grid of near-square blocks under the budget (join.py:88-108)."""
+    if budget_bytes < 4:
+        raise BudgetTooSmall(f"budget {budget_bytes} bytes cannot hold one fp32 cell")
+    budget_elems = budget_bytes // 4
+    b = math.isqrt(budget_elems)
+    lb = max(1, min(b, left_rows))
+    rb = max(1, min(budget_elems // lb, right_rows))
+    tiles = tuple(Tile(ls, min(lb, left_rows - ls), rs, min(rb, right_rows - rs))
+                  for ls in range(0, left_rows, lb) for rs in range(0, right_rows, rb))
+    return BatchPlan(lb, rb, tiles, max((t.area for t in tiles), default=0), budget_bytes)
+
+
+def _pick_inner(left: RawRelation, right: RawRelation, inner: Optional[str]) -> str:
+    if inner is None:
+        return "right" if len(right) <= len(left) else "left"
+    if inner not in ("left", "right"):
+        raise ValueError(f"inner must be 'left', 'right', or None, got {inner!r}")
+    return inner
+
+
+def _device(dev) -> torch.device:
+    D.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device()) if dev is None else torch.device(dev)
+
+
+def _to_matchset(m: D.DeviceMatches, left_name: str, right_name: str) -> MatchSet:
+    if m.n_matches == 0:
+        return MatchSet(left_name, right_name)
+    lo, ro, so = m.to_host()
+    return MatchSet(left_name, right_name, lo, ro, so)
+
+
+def join_prepared(left: D.PreparedRelation, right: D.PreparedRelation, theta,
+                  band: Optional[float] = None, left_name: str = "left",
+                  right_name: str = "right") -> MatchSet:
+    """Canonical MatchSet of two device-resident prepared relations."""
+    t = Threshold.of(theta)
+    check_dims(left.dim, right.dim)
+    return _to_matchset(D.join_prepared(left, right, t.value, band), left_name, right_name)
+
+
+def _run(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta, threads: int,
+         algo: str, inner: str, band, dev) -> Tuple[MatchSet, JoinStats]:
+    t = Threshold.of(theta)
+    if threads < 1:
+        raise ValueError("threads must be >= 1")
+    dev = _device(dev)
+    t0 = time.perf_counter_ns()
+    with torch.cuda.device(dev):
+        pl = prepare_relation(model, left, dev)
+        pr = prepare_relation(model, right, dev)
+        m = D.join_prepared(pl, pr, t.value, band)
+        matches = _to_matchset(m, left.name, right.name)
+    wall = time.perf_counter_ns() - t0
+    stats = JoinStats(wall_nanos=wall, model_calls_left=len(left), model_calls_right=len(right),
+                      pairs_compared=len(left) * len(right), matches=len(matches),
+                      peak_buffer_bytes=0, threads=threads, algo=algo, inner_relation=inner)
+    return matches, stats
+
+
+def tensor_join(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta,
+                budget_bytes: int, threads: int = 1, *, band: Optional[float] = None,
+                device=None) -> Tuple[MatchSet, JoinStats]:
+    """Tensor formulation (join.py:317-373) on the device: embed once per
+    relation, normalise, fused filter + canonical recheck, canonical order."""
+    Threshold.of(theta)
+    if threads < 1:
+        raise ValueError("threads must be >= 1")
+    plan_batches(len(left), len(right), model.dim, budget_bytes)  # validates the budget
+    return _run(left, right, model, theta, threads, "tensor", "right", band, device)
+
+
+def nlj_prefetch(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta,
+                 threads: int = 1, inner: Optional[str] = None, *,
+                 band: Optional[float] = None, device=None) -> Tuple[MatchSet, JoinStats]:
+    """Prefetch NLJ (join.py:238-294): identical result to tensor_join; the
+    inner-relation choice is recorded in the stats as the reference does."""
+    inner_name = _pick_inner(left, right, inner)
+    return _run(left, right, model, theta, threads, "prefetch_nlj", inner_name, band, device)
+
+
+ArrayLike = Union[np.ndarray, torch.Tensor]
+
+
+def _as_device_matrix(x: ArrayLike, dev: torch.device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        x = x.to(device=dev, dtype=torch.float32)
+        return x.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+
+
+def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
+                        band: Optional[float] = None, left_name: str = "left",
+                        right_name: str = "right", device=None) -> Tuple[MatchSet, JoinStats]:
+    """Join prefetched (un-normalised) vectors: the LookupModel path of the
+    reference's tensor_join without the per-token dictionary.  Host or device
+    inputs; host MatchSet output."""
+    t = Threshold.of(theta)
+    dev = _device(device)
+    t0 = time.perf_counter_ns()
+    with torch.cuda.device(dev):
+        L = _as_device_matrix(left, dev)
+        R = _as_device_matrix(right, dev)
+        check_dims(L.shape[1], R.shape[1])
+        m = D.join_prepared(D.prepare(L), D.prepare(R), t.value, band)
+        matches = _to_matchset(m, left_name, right_name)
+    wall = time.perf_counter_ns() - t0
+    stats = JoinStats(wall_nanos=wall, model_calls_left=L.shape[0],
+                      model_calls_right=R.shape[0], pairs_compared=L.shape[0] * R.shape[0],
+                      matches=len(matches), peak_buffer_bytes=0, threads=1, algo="tensor",
+                      inner_relation="right")
+    return matches, stats
+
+
+def join_embedded(left: EmbeddedRelation, right: EmbeddedRelation, theta, *,
+                  band: Optional[float] = None, device=None) -> MatchSet:
+    """Join two EmbeddedRelations; normalises them unless already normalised
+    (then the rows are used as given, like tile_similarity)."""
+    check_dims(left.dim, right.dim)
+    t = Threshold.of(theta)
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        preps = []
+        for er in (left, right):
+            x = torch.from_numpy(np.ascontiguousarray(er.data)).to(dev)
+            if er.normalized:
+                p = D.prepare(x)          # re-normalising unit rows changes bits,
+                p.f32.copy_(x)            # so keep the caller's canonical rows
+                preps.append(p)
+            else:
+                preps.append(D.prepare(x))
+        m = D.join_prepared(preps[0], preps[1], t.value, band)
+        return _to_matchset(m, left.source_name, right.source_name)

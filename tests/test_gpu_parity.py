@@ -1,0 +1,229 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the
+oracle.  Bar: bit-exact MatchSets (offsets, order, and fp32 similarity bits).
+Every join here runs through libsjb200.so (tcgen05 filter + canonical recheck).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import case_inputs, golden_tokens
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_JOINS = ["c_small", "c_d4", "c_d64", "c_d16_neg", "c_one", "c_ragged", "c_all", "cfg1"]
+
+
+def _bits_equal(ms, lo, ro, so):
+    return (np.array_equal(ms.lefts, lo) and np.array_equal(ms.rights, ro)
+            and np.array_equal(ms.sims.view(np.uint32), so.view(np.uint32)))
+
+
+def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
+    """Rebuild the row-major bf16 matrix from the tiled operand image."""
+    kpad = (dim + 15) // 16 * 16
+    a = op.view(torch.int16).cpu().numpy()
+    tiles = a.size // (128 * kpad)
+    t = a.reshape(tiles, kpad // 8, 128, 8).transpose(0, 2, 1, 3).reshape(tiles * 128, kpad)
+    return t[:n], t
+
+
+@pytest.mark.parametrize("dim", [1, 3, 4, 16, 100, 128, 200, 768])
+def test_normalize_and_operand_image(cuda, dim):
+    from paper_2312_01476_b200 import device as D
+    rng = np.random.default_rng(dim)
+    n = 300
+    x = rng.standard_normal((n, dim), dtype=np.float32) * rng.uniform(0.01, 10, (n, 1)).astype(np.float32)
+    x[5] = 0.0
+    x[17] = 1e-20
+    p = D.prepare(torch.from_numpy(x).to(cuda))
+    want, rep = O.normalize_rows(x)
+    assert np.array_equal(p.f32.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    assert p.repaired() == rep == 2
+    rows, full = _decode_operand(p.op, n, dim)
+    bf = torch.from_numpy(want).to(torch.bfloat16).view(torch.int16).numpy()
+    kpad = full.shape[1]
+    assert np.array_equal(rows[:, :dim], bf)
+    assert (rows[:, dim:] == 0).all() and (full[n:] == 0).all()
+    assert full.shape[0] % 256 == 0 and kpad % 16 == 0
+
+
+@pytest.mark.parametrize("name", GOLDEN_JOINS)
+def test_golden_tensor_join_public_api(cuda, golden, manifest, name):
+    from paper_2312_01476_b200 import LookupModel, RawRelation, tensor_join
+    meta = manifest["cases"][name]
+    L, S = case_inputs(meta)
+    toks_l = [f"L{i}" for i in range(len(L))]
+    toks_r = [f"S{i}" for i in range(len(S))]
+    model = LookupModel.from_matrix(toks_l + toks_r, np.concatenate([L, S]))
+    ms, st = tensor_join(RawRelation("left", toks_l), RawRelation("right", toks_r), model,
+                         meta["theta"], budget_bytes=64 << 20, threads=8)
+    assert _bits_equal(ms, golden[name + "_l"], golden[name + "_r"], golden[name + "_s"])
+    assert st.matches == meta["matches"] == len(ms)
+    assert st.model_calls_left == len(L) and st.model_calls_right == len(S)
+    assert model.call_count == len(L) + len(S)
+    assert st.pairs_compared == len(L) * len(S) and st.algo == "tensor"
+
+
+@pytest.mark.parametrize("name", ["c_small", "c_d64", "cfg1"])
+def test_golden_vectors_api(cuda, golden, manifest, name):
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    meta = manifest["cases"][name]
+    L, S = case_inputs(meta)
+    ms, _ = tensor_join_vectors(L, S, meta["theta"])
+    assert _bits_equal(ms, golden[name + "_l"], golden[name + "_r"], golden[name + "_s"])
+
+
+def test_synthetic_model_on_device(cuda, golden):
+    from paper_2312_01476_b200 import RawRelation, SyntheticModel, embed_relation_device
+    toks = golden_tokens(golden)
+    for dim, seed in ((16, 7), (4, 1), (100, 0)):
+        m = SyntheticModel(dim, seed=seed)
+        v = embed_relation_device(m, RawRelation("x", toks)).cpu().numpy()
+        assert np.array_equal(v.view(np.uint32), golden[f"syn_{dim}_{seed}"].view(np.uint32))
+        assert m.call_count == len(toks)
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.3, -1.0])
+def test_synthetic_join_and_nlj(cuda, golden, small_relations, theta):
+    from paper_2312_01476_b200 import SyntheticModel, nlj_prefetch, tensor_join
+    left, right = small_relations
+    model = SyntheticModel(16, seed=7)
+    ms, st = tensor_join(left, right, model, theta, budget_bytes=4096)
+    k = f"synjoin_{theta}"
+    assert _bits_equal(ms, golden[k + "_l"], golden[k + "_r"], golden[k + "_s"])
+    ms2, st2 = nlj_prefetch(left, right, model, theta, threads=4)
+    assert ms2 == ms
+    assert st2.inner_relation == "right" and st2.algo == "prefetch_nlj"
+    assert model.call_count == 2 * (len(left) + len(right))
+
+
+def test_random_instances_match_oracle(cuda):
+    """SPEC acceptance (1)-style sweep: 50 seeded instances, all dims 1..128."""
+    from paper_2312_01476_b200 import device as D
+    rng = np.random.default_rng(2024)
+    for inst in range(50):
+        nl, nr = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+        dim = int(rng.integers(1, 129))
+        c = int(rng.integers(1, 60))
+        L, S = O_pair(nl, nr, dim, c, float(rng.uniform(0.2, 1.0)), inst)
+        theta = float(rng.uniform(-0.2, 0.95))
+        pl = D.prepare(torch.from_numpy(L).to(cuda))
+        pr = D.prepare(torch.from_numpy(S).to(cuda))
+        m = D.join_prepared(pl, pr, theta)
+        lo, ro, so = m.to_host()
+        wl, wr, ws = O.join_raw(L, S, theta, threads=4)
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
+
+
+def O_pair(nl, nr, dim, c, sigma, seed):
+    from paper_2312_01476_b200 import datagen
+    return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)
+
+
+def test_overflow_retry_is_exact(cuda, manifest, golden):
+    from paper_2312_01476_b200 import device as D
+    meta = manifest["cases"]["c_small"]
+    L, S = case_inputs(meta)
+    pl = D.prepare(torch.from_numpy(L).to(cuda))
+    pr = D.prepare(torch.from_numpy(S).to(cuda))
+    m = D.join_prepared(pl, pr, meta["theta"], cand_cap=16)   # forces the retry
+    assert m.retries >= 1
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, golden["c_small_l"]) and np.array_equal(ro, golden["c_small_r"])
+    assert np.array_equal(so.view(np.uint32), golden["c_small_s"].view(np.uint32))
+
+
+def test_all_pairs_large_rows(cuda):
+    """theta = -1: every pair matches; rows longer than the warp and CTA sort
+    capacities (1024 / 8192) go through the large-row sort paths."""
+    from paper_2312_01476_b200 import device as D
+    rng = np.random.default_rng(5)
+    L = rng.standard_normal((3, 16), dtype=np.float32)
+    S = rng.standard_normal((20000, 16), dtype=np.float32)
+    m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                        D.prepare(torch.from_numpy(S).to(cuda)), -1.0)
+    lo, ro, so = m.to_host()
+    assert len(lo) == 3 * 20000
+    assert np.array_equal(lo, np.repeat(np.arange(3, dtype=np.uint64), 20000))
+    assert np.array_equal(ro, np.tile(np.arange(20000, dtype=np.uint64), 3))
+    Ln, _ = O.normalize_rows(L)
+    Sn, _ = O.normalize_rows(S)
+    assert np.array_equal(so[:20000].view(np.uint32), O.dots_vm(Ln[0], Sn).view(np.uint32))
+
+
+def test_empty_and_errors(cuda):
+    from paper_2312_01476_b200 import (BudgetTooSmall, DimensionMismatch, RawRelation,
+                                       SyntheticModel, tensor_join, nlj_prefetch)
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    m = SyntheticModel(8)
+    e = RawRelation("e", [])
+    r = RawRelation("r", ["a", "b"])
+    ms, st = tensor_join(r, e, m, 0.5, budget_bytes=1024)
+    assert len(ms) == 0 and st.pairs_compared == 0 and st.peak_buffer_bytes == 0
+    ms, st = tensor_join(e, e, m, 0.5, budget_bytes=1024)
+    assert len(ms) == 0
+    with pytest.raises(ValueError):
+        tensor_join(r, r, m, 0.5, budget_bytes=1024, threads=0)
+    with pytest.raises(BudgetTooSmall):
+        tensor_join(r, r, m, 0.5, budget_bytes=3)
+    with pytest.raises(ValueError):
+        nlj_prefetch(r, r, m, 1.5)
+    with pytest.raises(DimensionMismatch):
+        tensor_join_vectors(np.ones((2, 3), np.float32), np.ones((2, 4), np.float32), 0.1)
+
+
+def test_subword_model_matches_oracle(cuda):
+    from paper_2312_01476_b200 import RawRelation, SubwordModel, datagen, device as D
+    from paper_2312_01476_b200.embedding import embed_relation_device, prepare_relation
+    table = datagen.bucket_table(5003, 100, seed=1)
+    left, right = datagen.strings(700, 900, seed=4)
+    m = SubwordModel(table)
+    got = embed_relation_device(m, RawRelation("l", left)).cpu().numpy()
+    want = O.subword_embed(left, table)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    pl = prepare_relation(m, RawRelation("l", left))      # fused embed+normalise+cast
+    pr = prepare_relation(m, RawRelation("r", right))
+    assert m.call_count == len(left) * 2 + len(right)
+    wn, _ = O.normalize_rows(want)
+    assert np.array_equal(pl.f32.cpu().numpy().view(np.uint32), wn.view(np.uint32))
+    mm = D.join_prepared(pl, pr, 0.85)
+    lo, ro, so = mm.to_host()
+    wl, wr, ws = O.join_raw(want, O.subword_embed(right, table), 0.85)
+    assert len(wl) > 0
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
+
+
+def test_cuda_kernel_backend(cuda, golden):
+    from paper_2312_01476_b200 import kernels as K
+    rng = np.random.default_rng(7)
+    L = rng.standard_normal((70, 37), dtype=np.float32)
+    S = rng.standard_normal((90, 37), dtype=np.float32)
+    Ln, rep = O.normalize_rows(L)
+    m = L.copy()
+    assert K.normalize_rows_inplace(m) == rep
+    assert np.array_equal(m.view(np.uint32), Ln.view(np.uint32))
+    Sn, _ = O.normalize_rows(S)
+    assert np.array_equal(K.row_norms(L).view(np.uint32), O.row_norms(L).view(np.uint32))
+    bt = K.pack_transpose(Sn)
+    assert np.array_equal(bt, Sn.T)
+    out = np.empty((70, 90), np.float32)
+    K.tile_dot(Ln, bt, out)
+    assert np.array_equal(out.view(np.uint32), O.tile_dot(Ln, Sn).view(np.uint32))
+    lo, ro, so = K.scan_hits(out, 0.1, 500, 7)
+    ii, jj = np.nonzero(out >= np.float32(0.1))
+    assert np.array_equal(lo, ii.astype(np.uint64) + 500)
+    assert np.array_equal(ro, jj.astype(np.uint64) + 7)
+    assert np.array_equal(so, out[ii, jj])
+    assert np.array_equal(K.dots_vm(Ln[3], Sn).view(np.uint32), O.dots_vm(Ln[3], Sn).view(np.uint32))
+    assert np.float32(K.dot_seq(Ln[1], Sn[2])) == O.dot_seq(Ln[1], Sn[2])
+    chunks = K.nlj_rows(Ln, 10, 40, Sn, 0.2, 1e-4)
+    wl, wr, ws = O.join_normalized(Ln[10:40], Sn, 0.2)
+    assert np.array_equal(chunks[0][0], wl + 10) and np.array_equal(chunks[0][1], wr)
+    toks = golden_tokens(golden)
+    seeds = O.fnv1a64_many(toks, 7)
+    v = np.empty((len(toks), 16), np.float32)
+    K.synthetic_fill_many(seeds, v)
+    assert np.array_equal(v.view(np.uint32), golden["syn_16_7"].view(np.uint32))

@@ -1,0 +1,120 @@
+"""Host-side logic that needs no GPU: API types, planner, C-ABI surface."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+
+
+def test_raw_relation_and_matchset():
+    from paper_2312_01476_b200 import MatchSet, RawRelation, canonicalize
+    r = RawRelation("R", ["a", "a"])
+    assert len(r) == 2 and r.tokens == ("a", "a")
+    m = MatchSet.from_rows("L", "R", [(1, 0, 0.9), (0, 0, 0.8), (0, 0, 0.8)])
+    c = canonicalize(m)
+    assert c.as_tuples() == [(0, 0, pytest.approx(0.8)), (1, 0, pytest.approx(0.9))]
+    assert canonicalize(c) == c                       # idempotent
+    assert MatchSet("L", "R") == canonicalize(MatchSet("L", "R"))
+    with pytest.raises(ValueError):
+        MatchSet("L", "R", np.zeros(1, np.uint64), np.zeros(2, np.uint64), np.zeros(1, np.float32))
+
+
+def test_threshold_validation():
+    from paper_2312_01476_b200 import Threshold
+    assert Threshold.of(0.8).f32 == np.float32(0.8)
+    for bad in (1.5, -1.01):
+        with pytest.raises(ValueError):
+            Threshold(bad)
+
+
+def test_plan_batches(manifest):
+    from paper_2312_01476_b200.join import plan_batches
+    from paper_2312_01476_b200 import BudgetTooSmall
+    p = plan_batches(1000, 1000, 100, 1_000_000)
+    assert [p.left_block_rows, p.right_block_rows, len(p.tiles)] == manifest["plan_1000_1000_1MB"]
+    with pytest.raises(BudgetTooSmall):
+        plan_batches(10, 10, 4, 3)
+    rng = np.random.default_rng(1)
+    for _ in range(200):                               # exact cover
+        nl, nr = int(rng.integers(0, 60)), int(rng.integers(0, 60))
+        b = int(rng.integers(4, 20000))
+        p = plan_batches(nl, nr, 8, b)
+        cover = np.zeros((nl, nr), dtype=np.int32)
+        for t in p.tiles:
+            cover[t.left_row_start:t.left_row_start + t.left_row_count,
+                  t.right_row_start:t.right_row_start + t.right_row_count] += 1
+        assert (cover == 1).all()
+        assert p.buffer_elems * 4 <= b or p.buffer_elems == 0 or b < 4
+
+
+def test_host_embedding_twins(golden):
+    """Single-token host twins of the model recipes match the reference bits."""
+    from conftest import golden_tokens
+    from paper_2312_01476_b200.embedding import fnv1a64, synthetic_vector
+    toks = golden_tokens(golden)
+    assert [fnv1a64(t.encode()) for t in toks] == golden["fnv_values"].tolist()
+    want = golden["syn_16_7"]
+    for i, t in enumerate(toks):
+        v = synthetic_vector(fnv1a64(t.encode()) ^ 7, 16)
+        assert np.array_equal(v.view(np.uint32), want[i].view(np.uint32))
+
+
+def test_subword_host_twin_matches_oracle():
+    import oracle as O
+    from paper_2312_01476_b200.embedding import SubwordModel
+    from paper_2312_01476_b200 import datagen
+    table = datagen.bucket_table(997, 24, seed=3)
+    toks = ["cat", "dogs", "abcdefghijkl", "xyz", "été"]
+    m = SubwordModel(table)
+    got = np.stack([m._vector(t) for t in toks])
+    want = O.subword_embed(toks, table)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_datagen_deterministic():
+    from paper_2312_01476_b200 import datagen
+    a = datagen.clustered_pair(50, 40, 16, 5, 0.5, seed=9)
+    b = datagen.clustered_pair(50, 40, 16, 5, 0.5, seed=9)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    l1, r1 = datagen.strings(100, 120, seed=2)
+    l2, r2 = datagen.strings(100, 120, seed=2)
+    assert l1 == l2 and r1 == r2
+    assert all(3 <= len(w) <= 12 for w in l1)
+
+
+def _header_functions():
+    src = open(os.path.join(REPO, "include", "simjoin_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sjb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_c_abi_exports_every_declared_symbol():
+    from paper_2312_01476_b200 import build
+    path = build.build()
+    lib = ctypes.CDLL(path)
+    names = _header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in include/simjoin_b200.h but not exported"
+    from paper_2312_01476_b200 import _lib
+    assert set(names) <= set(_lib.EXPORTS)
+    L = _lib.lib()
+    assert L.sjb_version() == 1
+    assert L.sjb_kpad(100) == 112 and L.sjb_kpad(4) == 16
+    assert L.sjb_operand_elems(300, 100) == 512 * 112
+    band = L.sjb_default_band(100)
+    assert 0.0078 < band < 0.0081
+
+
+def test_no_oracle_in_product():
+    """The product package never imports or links the oracle."""
+    pkg = os.path.join(REPO, "paper_2312_01476_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                txt = open(os.path.join(root, f)).read()
+                assert "import oracle" not in txt and "refkern" not in txt, f
+                assert "liboracle" not in txt and "from oracle" not in txt, f

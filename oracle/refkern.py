@@ -210,13 +210,21 @@ def _run_workers(n, target):
         raise failures[0]
 
 
+def pack_transpose(nr: np.ndarray) -> np.ndarray:
+    """sj_pack_transpose (_kernelcore.c:140-144), done once per join (join.py:342)."""
+    packed = np.empty((nr.shape[1], nr.shape[0]), dtype=np.float32)
+    lib().sj_pack_transpose(_p(nr, _c_f32p), nr.shape[0], nr.shape[1], _p(packed, _c_f32p))
+    return packed
+
+
 def tensor_join_normalized(nl: np.ndarray, nr: np.ndarray, theta: float,
                            budget_bytes: int = DEFAULT_BUDGET, threads: int = 1,
-                           left_offset: int = 0):
+                           left_offset: int = 0, packed: np.ndarray = None):
     """tensor_join (join.py:317-373) after embed+normalize: tiles, workers, merge.
 
     ``left_offset`` shifts emitted left offsets (used for bounded row samples
-    of a larger relation).  Returns (lefts, rights, sims, peak_buffer_bytes).
+    of a larger relation); ``packed`` passes a pack_transpose of ``nr`` made
+    once for several row samples.  Returns (lefts, rights, sims, peak_buffer_bytes).
     """
     L = lib()
     theta32 = ctypes.c_float(np.float32(theta))
@@ -226,10 +234,8 @@ def tensor_join_normalized(nl: np.ndarray, nr: np.ndarray, theta: float,
     assignments = [tiles[w::n_workers] for w in range(n_workers)]
     parts: List[list] = [[] for _ in range(n_workers)]
     buffer_bytes = [0] * n_workers
-    packed = None
-    if tiles:
-        packed = np.empty((dim, nr.shape[0]), dtype=np.float32)
-        L.sj_pack_transpose(_p(nr, _c_f32p), nr.shape[0], dim, _p(packed, _c_f32p))
+    if tiles and packed is None:
+        packed = pack_transpose(nr)
     ldb = nr.shape[0]
 
     def work(w):

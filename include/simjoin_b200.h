@@ -29,7 +29,7 @@ extern "C" {
 #define SJB_E_CUDA (-2)        /* CUDA runtime error */
 #define SJB_E_UNSUPPORTED (-3) /* shape this build does not handle */
 
-#define SJB_TILE_ROWS 128
+#define SJB_TILE_ROWS 256
 
 /* ---- library ---------------------------------------------------------- */
 int sjb_version(void);
@@ -44,8 +44,8 @@ int64_t sjb_launch_count(void);
 /* Padded reduction depth of the bf16 operand image for `dim` (multiple of 16). */
 int64_t sjb_kpad(int64_t dim);
 /* Elements of the bf16 operand image of an n-row relation: n rounded up to a
- * multiple of 256 rows, times kpad.  Layout: 128-row tiles, each
- * [k-group (kpad/8)][row (128)][8 elements] (UMMA K-major, no swizzle). */
+ * multiple of 256 rows, times kpad.  Layout: 256-row tiles, each
+ * [k-group (kpad/8)][row (256)][8 elements] (UMMA K-major, no swizzle). */
 int64_t sjb_operand_elems(int64_t n, int64_t dim);
 
 /* ---- prefetch stage: embedding + normalise-and-cast -------------------- */

@@ -78,7 +78,7 @@ int set_smem_attr(const void* fn, int bytes) {
 
 // ---------------------------------------------------------------- plan
 struct JoinPlan {
-  int kpad, stages, grid, tiles_per_chunk, n_ablk, n_btiles;
+  int kpad, stages, a_bufs, grid, tiles_per_chunk, n_ablk, n_btiles;
   int64_t n_items;
   uint32_t smem;
   uint64_t seg_cap;
@@ -91,13 +91,21 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   if (pl->kpad > 128)
     return fail(SJB_E_UNSUPPORTED, "dim %lld > 128 not supported by the resident-A join kernel",
                 (long long)a->dim);
+  // Shared memory: prefer a double-buffered resident R block when that still
+  // leaves 3 B stages; otherwise one R buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);
-  sjb::JoinSmemLayout L0 = sjb::join_smem_layout(pl->kpad, 0);
-  int stages = (int)((max_smem - (int)L0.total) / (int)L0.b_bytes);
-  if (stages > 8) stages = 8;
+  int stages = 0, a_bufs = 2;
+  for (; a_bufs >= 1; a_bufs--) {
+    sjb::JoinSmemLayout L0 = sjb::join_smem_layout(pl->kpad, 0, a_bufs);
+    stages = (int)((max_smem - (int)L0.total) / (int)L0.tile_bytes);
+    if (stages >= 3) break;
+  }
+  if (a_bufs < 1) a_bufs = 1;
+  if (stages > 6) stages = 6;
   if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for 2 stages");
   pl->stages = stages;
-  pl->smem = sjb::join_smem_layout(pl->kpad, stages).total;
+  pl->a_bufs = a_bufs;
+  pl->smem = sjb::join_smem_layout(pl->kpad, stages, a_bufs).total;
   pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kBM);
   pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kBN);
   int tpc = a->tiles_per_chunk;
@@ -255,7 +263,7 @@ int sjb_sm_count(int device) {
 int64_t sjb_kpad(int64_t dim) { return sjb::round_up(dim < 1 ? 1 : dim, 16); }
 
 int64_t sjb_operand_elems(int64_t n, int64_t dim) {
-  return sjb::round_up(n < 0 ? 0 : n, 2 * sjb::kTileRows) * sjb_kpad(dim);
+  return sjb::round_up(n < 0 ? 0 : n, sjb::kTileRows) * sjb_kpad(dim);
 }
 
 float sjb_default_band(int64_t dim) {
@@ -411,6 +419,7 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.tiles_per_chunk = pl.tiles_per_chunk;
   jp.n_items = pl.n_items;
   jp.stages = pl.stages;
+  jp.a_bufs = pl.a_bufs;
   jp.cutoff = args->theta - args->band;
   jp.cand = cand;
   jp.seg_cap = pl.seg_cap;

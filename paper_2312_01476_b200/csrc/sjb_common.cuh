@@ -10,11 +10,12 @@
 namespace sjb {
 
 // Rows per bf16 operand tile.  Both relations are stored as a sequence of
-// 128-row tiles in the UMMA canonical K-major no-swizzle layout
+// 256-row tiles in the UMMA canonical K-major no-swizzle layout
 // ([k-group of 8 elements][row][8 elements], 16 B core-matrix rows), so one
 // 1-D bulk copy moves a whole tile into shared memory and the tensor core
-// reads it directly.  See DESIGN.md "HBM layout".
-constexpr int kTileRows = 128;
+// reads it directly (as one N=256 operand, or as two M=128 halves at a
+// 2 KB offset).  See DESIGN.md "HBM layout".
+constexpr int kTileRows = 256;
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }

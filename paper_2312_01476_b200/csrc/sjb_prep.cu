@@ -1,6 +1,6 @@
 // sjb_prep.cu -- prefetch-stage kernels: row L2-normalise-and-cast, the
 // synthetic model fill, FNV-1a-64 hashing, and the FastText-style subword
-// embedding gather.  All of them are HBM-bound; each CTA owns one 128-row
+// embedding gather.  All of them are HBM-bound; each CTA owns one 256-row
 // tile, stages it in shared memory (coalesced loads), runs the per-row
 // canonical arithmetic, then writes
 //   * the canonical fp32 rows (bitwise equal to the reference's
@@ -39,7 +39,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim) {
 }
 
 // Common tail: normalise the rows staged in `sm` (pitch floats apart) for the
-// sub-tile [r0, r0 + sub) of the 128-row tile starting at row0 (`rows` valid
+// sub-tile [r0, r0 + sub) of the 256-row tile starting at row0 (`rows` valid
 // rows in the whole tile), store fp32 rows and that slice of the bf16
 // operand tile.
 __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, int dim, int kpad,
@@ -82,7 +82,7 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
 }
 
 // in: n x dim fp32 row-major (or, with `gather`, a table whose row gather[i]
-// is relation row i).  One CTA per 128-row tile, staged in sub-tiles
+// is relation row i).  One CTA per 256-row operand tile, staged in sub-tiles
 // of `sub` rows (sub * (dim|1) floats of smem).  The grid may cover tiles past
 // n: those are written as zero operand tiles so the bf16 image can be padded.
 __global__ void __launch_bounds__(kPrepThreads)

@@ -33,7 +33,7 @@ import torch
 from . import _lib
 from .errors import CapacityExceeded, DimensionMismatch
 
-TILE_ROWS = 128
+TILE_ROWS = 256
 
 
 def _vp(t: Optional[torch.Tensor]):

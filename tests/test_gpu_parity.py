@@ -23,8 +23,9 @@ def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
     """Rebuild the row-major bf16 matrix from the tiled operand image."""
     kpad = (dim + 15) // 16 * 16
     a = op.view(torch.int16).cpu().numpy()
-    tiles = a.size // (128 * kpad)
-    t = a.reshape(tiles, kpad // 8, 128, 8).transpose(0, 2, 1, 3).reshape(tiles * 128, kpad)
+    T = 256
+    tiles = a.size // (T * kpad)
+    t = a.reshape(tiles, kpad // 8, T, 8).transpose(0, 2, 1, 3).reshape(tiles * T, kpad)
     return t[:n], t
 
 

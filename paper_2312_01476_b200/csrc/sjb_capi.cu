@@ -424,6 +424,14 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.cand = cand;
   jp.seg_cap = pl.seg_cap;
   jp.cta_count = cta;
+  jp.l32 = d_l32;
+  jp.r32 = d_r32;
+  jp.dim = (int)args->dim;
+  jp.theta = args->theta;
+  jp.sims_bits = sims_bits;
+  jp.rowcount = rowcount;
+  // candidate slots start empty: the fused recheck waits for each slot's write
+  SJB_CK(cudaMemsetAsync(cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
   {
     const char* dm = getenv("SJB_DEBUG_MODE");
     jp.debug_mode = dm ? atoi(dm) : 0;
@@ -434,14 +442,8 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   if (args->ev_filter_end)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_end), st));
 
-  // 2) canonical recheck
+  // 2) (the canonical recheck ran inside the filter kernel) row offsets
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
-  sjb::recheck_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
-      cand, pl.seg_cap, cta, pl.grid, d_l32, d_r32, (int)args->dim, args->theta, sims_bits,
-      rowcount);
-  SJB_CK_LAUNCH("recheck");
-
-  // 3) row offsets
   if (int rc = run_scan(rowcount, nl, rowoff, cursor, bsums, st)) return rc;
   sjb::gate_kernel<<<1, 1, 0, st>>>(rowoff, nl, args->out_cap, nbig);
   SJB_CK_LAUNCH("gate");

@@ -181,4 +181,37 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Canonical similarity: sequential fp32 fused multiply-add over d, exactly
+// the reference's sj_dot_seq with MADD = fmaf (_kernelcore.c:48-52, 128-133).
+__device__ __forceinline__ float dot_seq_dev(const float* __restrict__ a,
+                                             const float* __restrict__ b, int dim) {
+  float acc = 0.0f;
+  if ((dim & 3) == 0 &&
+      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (int d = 0; d < (dim >> 2); d++) {
+      const float4 x = __ldg(a4 + d), y = __ldg(b4 + d);
+      acc = __fmaf_rn(x.x, y.x, acc);
+      acc = __fmaf_rn(x.y, y.y, acc);
+      acc = __fmaf_rn(x.z, y.z, acc);
+      acc = __fmaf_rn(x.w, y.w, acc);
+    }
+  } else {
+    for (int d = 0; d < dim; d++) acc = __fmaf_rn(__ldg(a + d), __ldg(b + d), acc);
+  }
+  return acc;
+}
+
+// Load that bypasses L1 (sees another warp's completed global stores).
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Marks a candidate slot whose canonical similarity fell below theta.
+constexpr uint32_t kRejected = 0x7fc00001u;  // a NaN payload no similarity can have
+constexpr uint64_t kEmptySlot = ~0ull;         // candidate slot not yet written
+
 }  // namespace sjb

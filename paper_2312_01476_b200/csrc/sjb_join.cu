@@ -10,6 +10,8 @@
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17  epilogue: tcgen05.ld of the fp32 accumulators, 3-input max
 //                pre-filter against (theta - band), candidate emission
+//   warps 18..19 canonical recheck of the CTA's candidates (sequential fp32
+//                fmaf dot == sj_dot_seq) while their rows are L2-resident
 //
 // Work item = (R block of 256 rows, S chunk of `tiles_per_chunk` 256-row
 // tiles).  The R block stays resident in shared memory; the chunk's S tiles
@@ -26,14 +28,16 @@
 // a shared-memory counter and published in cta_count[blockIdx.x].  A CTA
 // whose segment overflows keeps counting, so the host can retry with the
 // exact capacity (the schedule is static, so per-CTA counts are
-// reproducible).  Every candidate is re-decided in canonical fp32 by
-// sjb_post.cu's recheck kernel.
+// reproducible).  Every candidate is re-decided in canonical fp32 by the
+// recheck warps: sims_bits[slot] = canonical sim (or kRejected), and
+// rowcount[i] counts the matches of left row i for sjb_post.cu's bucketing.
 #include "sjb_common.cuh"
 
 namespace sjb {
 
 constexpr int kEpiWarps = 16;
-constexpr int kJoinThreads = 64 + 32 * kEpiWarps;
+constexpr int kRecheckWarps = 2;
+constexpr int kJoinThreads = 64 + 32 * kEpiWarps + 32 * kRecheckWarps;
 constexpr int kBM = kTileRows;  // resident R rows per item (two UMMA M=128 halves)
 constexpr int kBN = kTileRows;  // S rows per stage == UMMA N
 constexpr int kUmmaN = 256;
@@ -53,7 +57,14 @@ struct JoinParams {
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
-  int debug_mode;  // diagnostics: 0 normal, 1 no emission, 2 no TMEM drain, 3 no stores
+  // canonical recheck (fused): fp32 rows, decision and per-row match counts
+  const float* l32;
+  const float* r32;
+  int dim;
+  float theta;
+  uint32_t* sims_bits;  // per candidate slot: canonical sim bits or kRejected
+  uint32_t* rowcount;   // matches per left row
+  int debug_mode;       // diagnostics: 0 normal, 1 no emission, 2 no TMEM drain
 };
 
 struct JoinSmemLayout {
@@ -67,7 +78,8 @@ __host__ __device__ inline JoinSmemLayout join_smem_layout(int kpad, int stages,
   L.off_a = 0;
   L.off_b = a_bufs * L.tile_bytes;
   L.off_bar = L.off_b + stages * L.tile_bytes;
-  // a_full[2] a_empty[2] acc_full[2] acc_empty[2] b_full[S] b_empty[S] + tmem slot + counters
+  // a_full[2] a_empty[2] acc_full[2] acc_empty[2] b_full[S] b_empty[S] + tmem slot
+  // + candidate counter, wrap flag, finished-epilogue-warp count
   L.total = L.off_bar + (8 + 2 * stages) * 8 + 16 + 16;
   return L;
 }
@@ -92,6 +104,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
   // so the host reports it instead of trusting a truncated count.
   uint32_t* cta_cnt = reinterpret_cast<uint32_t*>(bars + 8 + 2 * p.stages + 2);
   uint32_t* cta_sat = cta_cnt + 1;
+  uint32_t* epi_done = cta_cnt + 2;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -109,6 +122,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     }
     *cta_cnt = 0u;
     *cta_sat = 0u;
+    *epi_done = 0u;
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -204,6 +218,45 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           }
         }
         tc_commit(&a_empty[ab]);
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ------------------------------------------------------ recheck warps
+    // Re-decide every candidate of this CTA in canonical fp32 while the S
+    // chunk it came from is still L2-resident.  Warp w owns 32-slot blocks
+    // w, w + kRecheckWarps, ...; a block is processed once reserved (or once
+    // the epilogue has finished); each lane waits for its slot to be written
+    // (slots start as kEmptySlot).
+    const int rw = warp - 2 - kEpiWarps;
+    const uint64_t seg_cap = p.seg_cap;
+    const uint64_t* seg = p.cand + (uint64_t)blockIdx.x * seg_cap;
+    uint32_t* sims = p.sims_bits + (uint64_t)blockIdx.x * seg_cap;
+    volatile uint32_t* vcnt = cta_cnt;
+    volatile uint32_t* vdone = epi_done;
+    for (uint64_t blk = rw;; blk += kRecheckWarps) {
+      const uint64_t s0 = blk * 32;
+      uint64_t n;
+      for (;;) {
+        n = mn<uint64_t>(*vcnt, seg_cap);
+        if (n >= s0 + 32) break;
+        if (*vdone == (uint32_t)kEpiWarps) {
+          n = mn<uint64_t>(*vcnt, seg_cap);
+          break;
+        }
+        __nanosleep(200);
+      }
+      if (s0 >= n) break;
+      const uint64_t slot = s0 + lane;
+      if (slot < n) {
+        uint64_t u;
+        do {
+          u = ld_volatile_u64(seg + slot);
+        } while (u == kEmptySlot);
+        const uint32_t i = (uint32_t)(u >> 32), j = (uint32_t)u;
+        const float s = dot_seq_dev(p.l32 + (size_t)i * p.dim, p.r32 + (size_t)j * p.dim, p.dim);
+        const bool keep = s >= p.theta;
+        sims[slot] = keep ? __float_as_uint(s) : kRejected;
+        if (keep) atomicAdd(p.rowcount + i, 1u);
       }
     }
   } else {
@@ -308,14 +361,14 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
             while (w) {
               const int b = __ffs(w) - 1;
               w &= w - 1;
-              if (pos < seg_cap && p.debug_mode != 3) seg[pos] = pack_pair(gi, j0 + b);
+              if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + b);
               pos++;
             }
             w = mk1;
             while (w) {
               const int b = __ffs(w) - 1;
               w &= w - 1;
-              if (pos < seg_cap && p.debug_mode != 3) seg[pos] = pack_pair(gi, j0 + 32 + b);
+              if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
               pos++;
             }
           }
@@ -323,6 +376,12 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       }
     }
     if (p.debug_mode == 4 && dbg_acc == 0xFFFFFFFFu) p.cand[0] = dbg_acc;
+    // publish "this warp reserved its last slots" to the recheck warps
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(epi_done, 1u);
+    }
   }
 
   tc_fence_before();

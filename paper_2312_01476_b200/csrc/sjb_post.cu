@@ -1,8 +1,6 @@
 // sjb_post.cu -- everything after the tensor-core filter:
 //
-//   recheck    canonical fp32 similarity for every candidate (sequential
-//              fmaf chain over d == sj_dot_seq, _kernelcore.c:128-133) and the
-//              inclusive `sim >= theta` decision (threshold_scan, linalg.py:146-153)
+//   (the canonical recheck runs inside the filter kernel, sjb_join.cu)
 //   row scan   exclusive prefix sum of per-row match counts
 //   scatter    bucket kept pairs by left row (counting sort)
 //   segsort    sort each left row's bucket by right offset and write the
@@ -16,48 +14,6 @@
 #include "sjb_common.cuh"
 
 namespace sjb {
-
-__device__ __forceinline__ float dot_seq_dev(const float* __restrict__ a,
-                                             const float* __restrict__ b, int dim) {
-  float acc = 0.0f;
-  if ((dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
-    const float4* a4 = reinterpret_cast<const float4*>(a);
-    const float4* b4 = reinterpret_cast<const float4*>(b);
-    for (int d = 0; d < (dim >> 2); d++) {
-      const float4 x = __ldg(a4 + d), y = __ldg(b4 + d);
-      acc = __fmaf_rn(x.x, y.x, acc);
-      acc = __fmaf_rn(x.y, y.y, acc);
-      acc = __fmaf_rn(x.z, y.z, acc);
-      acc = __fmaf_rn(x.w, y.w, acc);
-    }
-  } else {
-    for (int d = 0; d < dim; d++) acc = __fmaf_rn(__ldg(a + d), __ldg(b + d), acc);
-  }
-  return acc;
-}
-
-constexpr uint32_t kRejected = 0x7fc00001u;  // NaN payload marking a rejected candidate
-
-// Candidate slot p lives in CTA segment p / seg_cap.
-__global__ void recheck_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
-                               const unsigned long long* __restrict__ cta_count, int n_cta,
-                               const float* __restrict__ l32, const float* __restrict__ s32,
-                               int dim, float theta, uint32_t* __restrict__ sims_bits,
-                               uint32_t* __restrict__ rowcount) {
-  const uint64_t total = (uint64_t)n_cta * seg_cap;
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t c = p / seg_cap, local = p - c * seg_cap;
-    const uint64_t cnt = mn<uint64_t>(cta_count[c], seg_cap);
-    if (local >= cnt) continue;
-    const uint64_t u = cand[p];
-    const uint32_t i = (uint32_t)(u >> 32), j = (uint32_t)u;
-    const float s = dot_seq_dev(l32 + (size_t)i * dim, s32 + (size_t)j * dim, dim);
-    const bool keep = s >= theta;
-    sims_bits[p] = keep ? __float_as_uint(s) : kRejected;
-    if (keep) atomicAdd(rowcount + i, 1u);
-  }
-}
 
 // ----------------------------------------------------------- prefix scan
 // Three-phase exclusive scan of u32 counts into u64 offsets (n+1 entries).

@@ -115,15 +115,20 @@ def cpu_reference_run(L, S, theta, budget_s, threads, n_left_full):
     packed = refkern.pack_transpose(Sn)
     t_pack = time.perf_counter() - t0
     # calibrate the per-row cost, then size the measured sample to budget_s
-    r_cal = 4 * threads
+    # the sample executes the full job's own tile plan (plan_rows), restricted
+    # to its first rows, so per-row cost matches the full run's
+    r_cal = 128
     t0 = time.perf_counter()
     Ln, _ = refkern.normalize_rows(L[:r_cal])
-    refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed)
+    refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed,
+                                   plan_rows=n_left_full)
     t_cal = time.perf_counter() - t0
     rows = int(max(r_cal, min(L.shape[0], r_cal * budget_s / max(t_cal, 1e-6))))
+    rows = max(r_cal, rows // 128 * 128)
     t0 = time.perf_counter()
     Ln, _ = refkern.normalize_rows(L[:rows])
-    lo, _, _, _ = refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed)
+    lo, _, _, _ = refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed,
+                                                 plan_rows=n_left_full)
     t_rows = time.perf_counter() - t0
     full_time = t_norm_s + t_pack + t_rows * (n_left_full / rows)
     pairs = n_left_full * S.shape[0]

@@ -219,17 +219,25 @@ def pack_transpose(nr: np.ndarray) -> np.ndarray:
 
 def tensor_join_normalized(nl: np.ndarray, nr: np.ndarray, theta: float,
                            budget_bytes: int = DEFAULT_BUDGET, threads: int = 1,
-                           left_offset: int = 0, packed: np.ndarray = None):
+                           left_offset: int = 0, packed: np.ndarray = None,
+                           plan_rows: int = None):
     """tensor_join (join.py:317-373) after embed+normalize: tiles, workers, merge.
 
     ``left_offset`` shifts emitted left offsets (used for bounded row samples
     of a larger relation); ``packed`` passes a pack_transpose of ``nr`` made
-    once for several row samples.  Returns (lefts, rights, sims, peak_buffer_bytes).
+    once for several row samples.  ``plan_rows`` plans the tile grid for a
+    relation of that many left rows and executes only the tiles that fall in
+    the rows given (a bounded sample runs exactly the full job's first tiles).
+    Returns (lefts, rights, sims, peak_buffer_bytes).
     """
     L = lib()
     theta32 = ctypes.c_float(np.float32(theta))
     dim = nl.shape[1]
-    tiles = exec_tiles(plan_batches(nl.shape[0], nr.shape[0], budget_bytes))
+    n_plan = nl.shape[0] if plan_rows is None else max(plan_rows, nl.shape[0])
+    tiles = exec_tiles(plan_batches(n_plan, nr.shape[0], budget_bytes))
+    if n_plan != nl.shape[0]:
+        tiles = [(ls, min(lc, nl.shape[0] - ls), rs, rc) for (ls, lc, rs, rc) in tiles
+                 if ls < nl.shape[0]]
     n_workers = max(1, min(threads, len(tiles)))
     assignments = [tiles[w::n_workers] for w in range(n_workers)]
     parts: List[list] = [[] for _ in range(n_workers)]

@@ -138,10 +138,17 @@ class DeviceMatches:
     grid: int
 
     def to_host(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-        lo = self.lefts.cpu().numpy().view(np.uint64)
-        ro = self.rights.cpu().numpy().view(np.uint64)
-        so = self.sims.cpu().numpy()
-        return lo, ro, so
+        """Copy the columns into pinned host memory (torch's caching host
+        allocator, so repeated joins reuse the pinned blocks) and return
+        numpy views that own them."""
+        outs = []
+        for t in (self.lefts, self.rights, self.sims):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            outs.append(h)
+        torch.cuda.current_stream(self.lefts.device).synchronize()
+        return (outs[0].numpy().view(np.uint64), outs[1].numpy().view(np.uint64),
+                outs[2].numpy())
 
 
 _cap_lock = threading.Lock()

@@ -5,8 +5,9 @@
 // :327-350) with one persistent, warp-specialised tcgen05 kernel that never
 // materialises the similarity matrix:
 //
-//   warp 0       producer: 1-D bulk copies (TMA, cp.async.bulk) of pre-tiled
-//                bf16 operand tiles into shared memory (mbarrier rings)
+//   warp 0       S producer: 1-D bulk copies (TMA, cp.async.bulk) of pre-tiled
+//                bf16 operand tiles into a shared-memory ring (mbarriers)
+//   warp 0 ln 1  R-block producer (resident operand, one copy per item)
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17  epilogue: tcgen05.ld of the fp32 accumulators, 3-input max
 //                pre-filter against (theta - band), candidate emission
@@ -33,11 +34,17 @@
 // rowcount[i] counts the matches of left row i for sjb_post.cu's bucketing.
 #include "sjb_common.cuh"
 
+#ifndef SJB_PROFILE
+#define SJB_PROFILE 0
+#endif
+
 namespace sjb {
 
 constexpr int kEpiWarps = 16;
 constexpr int kRecheckWarps = 2;
-constexpr int kJoinThreads = 64 + 32 * kEpiWarps + 32 * kRecheckWarps;
+// 20 warps = 5 per SM sub-partition, which keeps the per-thread register cap
+// at 96 (16K registers per SMSP); a 21st warp would force spills.
+constexpr int kJoinThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
 constexpr int kBM = kTileRows;  // resident R rows per item (two UMMA M=128 halves)
 constexpr int kBN = kTileRows;  // S rows per stage == UMMA N
 constexpr int kUmmaN = 256;
@@ -137,21 +144,31 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
   const uint32_t tile_elems = tile_bytes / 2;
   const int na = p.a_bufs;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- producer
+  if (warp == 0 && lane == 1) {
+    {
+      // ------------------------------------------------- R-block producer
+      // Separate thread from the S producer so the S ring keeps prefetching
+      // across item boundaries while the next R block waits for its buffer.
       const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_b = policy_evict_normal();
-      int bstage = 0;
-      uint32_t bphase = 0;
       int64_t it = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, it++) {
-        const int64_t rb = item % nb, sc = item / nb;
+        const int64_t rb = item % nb;
         const int ab = (int)(it % na);
         mbar_wait(&a_empty[ab], (uint32_t)((it / na) & 1) ^ 1u);
         mbar_arrive_expect_tx(&a_full[ab], tile_bytes);
         bulk_g2s(a_buf + (size_t)ab * tile_bytes, p.a16 + (size_t)rb * tile_elems, tile_bytes,
                  &a_full[ab], pol_a);
+      }
+    }
+  } else if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------------------------------------- S producer
+      const uint64_t pol_b = policy_evict_normal();
+      int bstage = 0;
+      uint32_t bphase = 0;
+      int64_t it = 0;
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, it++) {
+        const int64_t sc = item / nb;
         const int64_t t0 = sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
@@ -187,21 +204,32 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       uint32_t bphase = 0;
       uint32_t acc_it = 0;
       int64_t it = 0;
+      // diagnostics (build with -DSJB_PROFILE=1, run with SJB_DEBUG_MODE=9):
+      // wait-time attribution of the MMA thread
+      const bool dbg = SJB_PROFILE && p.debug_mode == 9;
+      long long w_a = 0, w_b = 0, w_e = 0;
+      const long long c_start = clock64();
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, it++) {
         const int64_t sc = item / nb;
         const int ab = (int)(it % na);
+        long long c0 = dbg ? clock64() : 0;
         mbar_wait(&a_full[ab], (uint32_t)((it / na) & 1));
+        if (dbg) w_a += clock64() - c0;
         tc_fence_after();
         const uint64_t ad = a_desc_base + (uint64_t)ab * tile_step;
         const int64_t t0 = sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
+          if (dbg) c0 = clock64();
           mbar_wait(&b_full[bstage], bphase);
+          if (dbg) w_b += clock64() - c0;
           const uint64_t bd = b_desc_base + (uint64_t)bstage * tile_step;
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const uint32_t as = acc_it & 1u;
+            if (dbg) c0 = clock64();
             mbar_wait(&acc_empty[as], ((acc_it >> 1) & 1u) ^ 1u);
+            if (dbg) w_e += clock64() - c0;
             tc_fence_after();
             const uint32_t d = tmem_base + as * kUmmaN;
             const uint64_t adh = ad + h * half_step;
@@ -219,6 +247,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         }
         tc_commit(&a_empty[ab]);
       }
+      if (dbg && blockIdx.x < 3)
+        printf("[dbg] cta %d mma: total %lld  wait_a %lld  wait_b %lld  wait_acc_empty %lld\n",
+               blockIdx.x, clock64() - c_start, w_a, w_b, w_e);
     }
   } else if (warp >= 2 + kEpiWarps) {
     // ------------------------------------------------------ recheck warps
@@ -274,6 +305,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     uint32_t acc_it = 0;
+    const bool edbg = SJB_PROFILE && p.debug_mode == 9 && blockIdx.x < 3 && (ew == 0 || ew == 15);
+    long long e_wait = 0, e_drain = 0, e_mark = 0;
+    const long long e_start = clock64();
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
       const int64_t t0 = sc * p.tiles_per_chunk;
@@ -282,7 +316,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
 #pragma unroll 1
         for (int h = 0; h < 2; h++) {
           const uint32_t as = acc_it & 1u;
+          const long long e0 = edbg ? clock64() : 0;
           mbar_wait(&acc_full[as], (acc_it >> 1) & 1u);
+          if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
           tc_fence_after();
           if (p.debug_mode == 2 || p.debug_mode >= 16) {
             __syncwarp();
@@ -299,6 +335,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           __syncwarp();
           if (lane == 0) mbar_arrive_relaxed(&acc_empty[as]);
           acc_it++;
+          if (edbg) e_drain += clock64() - e_mark;
 
           const int64_t gi64 = rb * kBM + h * 128 + lane_base + lane;
           const bool row_ok = gi64 < p.n_a;
@@ -376,6 +413,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       }
     }
     if (p.debug_mode == 4 && dbg_acc == 0xFFFFFFFFu) p.cand[0] = dbg_acc;
+    if (edbg && lane == 0)
+      printf("[dbg] cta %d epi warp %d: total %lld  wait_acc_full %lld  drain %lld\n",
+             blockIdx.x, ew, clock64() - e_start, e_wait, e_drain);
     // publish "this warp reserved its last slots" to the recheck warps
     __syncwarp();
     if (lane == 0) {

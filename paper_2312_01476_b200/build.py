@@ -48,7 +48,9 @@ def is_stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not is_stale():
         return LIB_PATH
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", os.path.join(CSRC, "sjb_capi.cu")]
+    extra = os.environ.get("SJB_NVCC_EXTRA", "").split()   # e.g. -DSJB_PROFILE=1
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB_PATH + ".tmp",
+           os.path.join(CSRC, "sjb_capi.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

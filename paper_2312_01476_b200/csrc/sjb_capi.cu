@@ -9,9 +9,13 @@
 #include <mutex>
 #include <string>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/simjoin_b200.h"
 #include "sjb_common.cuh"
 #include "sjb_join.cu"
+#include "sjb_join2.cu"
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
 
@@ -82,15 +86,53 @@ struct JoinPlan {
   int64_t n_items;
   uint32_t smem;
   uint64_t seg_cap;
+  bool pair;  // CTA-pair (cta_group::2) filter kernel
 };
+
+bool use_pair_filter() {
+  const char* f = getenv("SJB_FILTER");
+  return f != nullptr && strcmp(f, "pair") == 0;
+}
+
+// CTA-pair plan: pair R block = 512 rows, pair S tile = 128 rows.
+int make_pair_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) {
+  namespace P = sjb::pair;
+  pl->pair = true;
+  pl->a_bufs = 2;
+  const sjb::pair::Layout L0 = P::layout(pl->kpad, 0);
+  int stages = (int)((max_smem - (int)L0.total - 3 * 8 * 12) / (int)L0.b_bytes);
+  if (stages > 12) stages = 12;
+  if (stages < 3) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for the pair kernel");
+  pl->stages = stages;
+  pl->smem = P::layout(pl->kpad, stages).total;
+  pl->n_ablk = (int)sjb::ceil_div(a->n_left, 2 * P::kARows);
+  pl->n_btiles = (int)sjb::ceil_div(a->n_right, P::kUmmaN);
+  const int pairs_max = sms / 2;
+  int tpc = a->tiles_per_chunk;
+  if (tpc <= 0) {
+    const int64_t work = (int64_t)pl->n_ablk * pl->n_btiles;
+    int64_t t = work / (4LL * pairs_max);
+    tpc = (int)(t < 1 ? 1 : (t > 256 ? 256 : t));
+  }
+  pl->tiles_per_chunk = tpc;
+  pl->n_items = (int64_t)pl->n_ablk * sjb::ceil_div(pl->n_btiles, tpc);
+  int pairs = a->grid > 0 ? a->grid / 2 : pairs_max;
+  if (pairs < 1) pairs = 1;
+  if ((int64_t)pairs > pl->n_items) pairs = (int)(pl->n_items > 0 ? pl->n_items : 1);
+  pl->grid = 2 * pairs;
+  pl->seg_cap = (uint64_t)(a->cand_cap / pl->grid);
+  return SJB_OK;
+}
 
 int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   const int dev = current_device();
   const int sms = sjb_sm_count(dev);
   pl->kpad = (int)sjb_kpad(a->dim);
+  pl->pair = false;
   if (pl->kpad > 128)
     return fail(SJB_E_UNSUPPORTED, "dim %lld > 128 not supported by the resident-A join kernel",
                 (long long)a->dim);
+  if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // Shared memory: prefer a double-buffered resident R block when that still
   // leaves 3 B stages; otherwise one R buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);
@@ -191,6 +233,67 @@ int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStr
   return SJB_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// The bf16 operand image (sjb_operand_elems elements, 256-row tiles of
+// [k-group][row][8]) as a 3-D tensor (256 elements = 32 rows x 8, 8 row
+// blocks, kgroups * tiles); box {256, box_rows/32, kgroups} = one
+// [k-group][box_rows][8] block.  The 512 B inner extent keeps every request
+// at full 32 B sectors (a 16 B inner box over-fetched 2x and issued ~900
+// requests per stage).
+int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (box_rows % 32) return fail(SJB_E_INVALID, "box rows %d not a multiple of 32", box_rows);
+  const int64_t rows = sjb::round_up(n, 2 * sjb::kTileRows);
+  const cuuint64_t kgroups = (cuuint64_t)kpad / 8;
+  const cuuint64_t dims[3] = {256, (cuuint64_t)sjb::kTileRows / 32,
+                              kgroups * (cuuint64_t)(rows / sjb::kTileRows)};
+  const cuuint64_t strides[2] = {512, (cuuint64_t)sjb::kTileRows * 16};
+  const cuuint32_t box[3] = {256, (cuuint32_t)box_rows / 32, (cuuint32_t)kgroups};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(image), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SJB_OK;
+}
+
+template <int KS>
+int launch_pair_ks(const sjb::pair::Params& pp, int grid, uint32_t smem, cudaStream_t st) {
+  if (int rc = set_smem_attr((const void*)sjb::pair::filter_kernel<KS>, (int)smem)) return rc;
+  sjb::pair::filter_kernel<KS><<<grid, sjb::pair::kThreads, smem, st>>>(pp);
+  SJB_CK_LAUNCH("pair_filter");
+  return SJB_OK;
+}
+
+int launch_pair_filter(const sjb::pair::Params& pp, int grid, uint32_t smem, cudaStream_t st) {
+  switch (pp.kpad / 16) {
+    case 1: return launch_pair_ks<1>(pp, grid, smem, st);
+    case 2: return launch_pair_ks<2>(pp, grid, smem, st);
+    case 3: return launch_pair_ks<3>(pp, grid, smem, st);
+    case 4: return launch_pair_ks<4>(pp, grid, smem, st);
+    case 5: return launch_pair_ks<5>(pp, grid, smem, st);
+    case 6: return launch_pair_ks<6>(pp, grid, smem, st);
+    case 7: return launch_pair_ks<7>(pp, grid, smem, st);
+    case 8: return launch_pair_ks<8>(pp, grid, smem, st);
+    default: return fail(SJB_E_UNSUPPORTED, "kpad %d", pp.kpad);
+  }
+}
+
 int launch_join_filter(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
   switch (jp.kpad / 16) {
     case 1: return launch_filter_ks<1>(jp, grid, smem, st);
@@ -263,7 +366,8 @@ int sjb_sm_count(int device) {
 int64_t sjb_kpad(int64_t dim) { return sjb::round_up(dim < 1 ? 1 : dim, 16); }
 
 int64_t sjb_operand_elems(int64_t n, int64_t dim) {
-  return sjb::round_up(n < 0 ? 0 : n, sjb::kTileRows) * sjb_kpad(dim);
+  // 512-row padding: the CTA-pair filter reads R blocks of two 256-row tiles
+  return sjb::round_up(n < 0 ? 0 : n, 2 * sjb::kTileRows) * sjb_kpad(dim);
 }
 
 float sjb_default_band(int64_t dim) {
@@ -438,7 +542,35 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   }
   if (args->ev_filter_begin)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_begin), st));
-  if (int rc = launch_join_filter(jp, pl.grid, pl.smem, st)) return rc;
+  if (pl.pair) {
+    sjb::pair::Params pp;
+    pp.a16 = jp.a16;
+    pp.b16 = jp.b16;
+    pp.n_a = nl;
+    pp.n_b = nr;
+    pp.kpad = pl.kpad;
+    pp.n_ablk = pl.n_ablk;
+    pp.n_btiles = pl.n_btiles;
+    pp.tiles_per_chunk = pl.tiles_per_chunk;
+    pp.n_items = pl.n_items;
+    pp.stages = pl.stages;
+    pp.cutoff = jp.cutoff;
+    pp.cand = cand;
+    pp.seg_cap = pl.seg_cap;
+    pp.cta_count = cta;
+    pp.l32 = d_l32;
+    pp.r32 = d_r32;
+    pp.dim = (int)args->dim;
+    pp.theta = args->theta;
+    pp.sims_bits = sims_bits;
+    pp.rowcount = rowcount;
+    pp.debug_mode = jp.debug_mode;
+    if (int rc = encode_operand_map(&pp.tmap_a, d_l16, nl, pl.kpad, sjb::pair::kARows)) return rc;
+    if (int rc = encode_operand_map(&pp.tmap_b, d_r16, nr, pl.kpad, sjb::pair::kHalfN)) return rc;
+    if (int rc = launch_pair_filter(pp, pl.grid, pl.smem, st)) return rc;
+  } else if (int rc = launch_join_filter(jp, pl.grid, pl.smem, st)) {
+    return rc;
+  }
   if (args->ev_filter_end)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_end), st));
 

@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           n = mn<uint64_t>(*vcnt, seg_cap);
           break;
         }
-        __nanosleep(200);
+        // not latency-critical: poll rarely so the epilogue keeps the issue slots
+        __nanosleep(2000);
       }
       if (s0 >= n) break;
       const uint64_t slot = s0 + lane;

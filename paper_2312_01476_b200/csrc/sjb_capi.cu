@@ -16,6 +16,7 @@
 #include "sjb_common.cuh"
 #include "sjb_join.cu"
 #include "sjb_join2.cu"
+#include "sjb_join3.cu"
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
 
@@ -87,7 +88,35 @@ struct JoinPlan {
   uint32_t smem;
   uint64_t seg_cap;
   bool pair;  // CTA-pair (cta_group::2) filter kernel
+  bool wide;  // K-streaming kernel (kpad > 128)
 };
+
+// K-streaming plan (kpad > 128): 256 x 256 output tiles, 64-element K chunks.
+int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) {
+  namespace W = sjb::wide;
+  pl->wide = true;
+  pl->a_bufs = 0;
+  int stages = 0;
+  while (stages < 6 && (int)W::smem_bytes(stages + 1) <= max_smem) stages++;
+  if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for the wide kernel");
+  pl->stages = stages;
+  pl->smem = W::smem_bytes(stages);
+  pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kTileRows);
+  pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kTileRows);
+  int tpc = a->tiles_per_chunk;
+  if (tpc <= 0) {
+    const int64_t work = (int64_t)pl->n_ablk * pl->n_btiles;
+    int64_t t = work / (4LL * sms);
+    tpc = (int)(t < 1 ? 1 : (t > 32 ? 32 : t));
+  }
+  pl->tiles_per_chunk = tpc;
+  pl->n_items = (int64_t)pl->n_ablk * sjb::ceil_div(pl->n_btiles, tpc);
+  int grid = a->grid > 0 ? a->grid : sms;
+  if ((int64_t)grid > pl->n_items) grid = (int)(pl->n_items > 0 ? pl->n_items : 1);
+  pl->grid = grid;
+  pl->seg_cap = (uint64_t)(a->cand_cap / grid);
+  return SJB_OK;
+}
 
 bool use_pair_filter() {
   const char* f = getenv("SJB_FILTER");
@@ -129,9 +158,8 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   const int sms = sjb_sm_count(dev);
   pl->kpad = (int)sjb_kpad(a->dim);
   pl->pair = false;
-  if (pl->kpad > 128)
-    return fail(SJB_E_UNSUPPORTED, "dim %lld > 128 not supported by the resident-A join kernel",
-                (long long)a->dim);
+  pl->wide = false;
+  if (pl->kpad > 128) return make_wide_plan(a, pl, sms, max_dyn_smem(dev));
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // Shared memory: prefer a double-buffered resident R block when that still
   // leaves 3 B stages; otherwise one R buffer (reloaded between items).
@@ -363,7 +391,12 @@ int sjb_sm_count(int device) {
   return v;
 }
 
-int64_t sjb_kpad(int64_t dim) { return sjb::round_up(dim < 1 ? 1 : dim, 16); }
+int64_t sjb_kpad(int64_t dim) {
+  // <= 128: resident-R kernels, one UMMA k-step per 16; wider: K-streaming
+  // kernel, 64-element chunks
+  const int64_t d = dim < 1 ? 1 : dim;
+  return d <= 128 ? sjb::round_up(d, 16) : sjb::round_up(d, sjb::wide::kKChunk);
+}
 
 int64_t sjb_operand_elems(int64_t n, int64_t dim) {
   // 512-row padding: the CTA-pair filter reads R blocks of two 256-row tiles
@@ -542,7 +575,33 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   }
   if (args->ev_filter_begin)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_begin), st));
-  if (pl.pair) {
+  if (pl.wide) {
+    sjb::wide::Params wp;
+    wp.a16 = jp.a16;
+    wp.b16 = jp.b16;
+    wp.n_a = nl;
+    wp.n_b = nr;
+    wp.kpad = pl.kpad;
+    wp.n_ablk = pl.n_ablk;
+    wp.n_btiles = pl.n_btiles;
+    wp.tiles_per_chunk = pl.tiles_per_chunk;
+    wp.n_items = pl.n_items;
+    wp.stages = pl.stages;
+    wp.cutoff = jp.cutoff;
+    wp.cand = cand;
+    wp.seg_cap = pl.seg_cap;
+    wp.cta_count = cta;
+    wp.l32 = d_l32;
+    wp.r32 = d_r32;
+    wp.dim = (int)args->dim;
+    wp.theta = args->theta;
+    wp.sims_bits = sims_bits;
+    wp.rowcount = rowcount;
+    wp.debug = jp.debug_mode;
+    if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel, (int)pl.smem)) return rc;
+    sjb::wide::filter_kernel<<<pl.grid, sjb::wide::kThreads, pl.smem, st>>>(wp);
+    SJB_CK_LAUNCH("wide_filter");
+  } else if (pl.pair) {
     sjb::pair::Params pp;
     pp.a16 = jp.a16;
     pp.b16 = jp.b16;

@@ -129,6 +129,27 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-uniform variants: the whole warp executes the call, one elected lane
+// issues (keeps descriptors in uniform registers; no per-MMA ELECT loop).
+__device__ __forceinline__ void tc_mma_bf16_elect(uint32_t d_tmem, uint64_t a_desc,
+                                                  uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -203,6 +224,42 @@ __device__ __forceinline__ float dot_seq_dev(const float* __restrict__ a,
   return acc;
 }
 
+// Two canonical similarities with their (independent) sequential chains
+// interleaved, so the FMA latency of one hides behind the other.  Each chain
+// is exactly dot_seq_dev.
+__device__ __forceinline__ void dot_seq2_dev(const float* __restrict__ a0,
+                                             const float* __restrict__ b0,
+                                             const float* __restrict__ a1,
+                                             const float* __restrict__ b1, int dim, float& r0,
+                                             float& r1) {
+  float c0 = 0.0f, c1 = 0.0f;
+  if ((dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(b0) |
+                          reinterpret_cast<uintptr_t>(a1) | reinterpret_cast<uintptr_t>(b1)) &
+                         15) == 0) {
+    const float4 *x4 = reinterpret_cast<const float4*>(a0), *y4 = reinterpret_cast<const float4*>(b0);
+    const float4 *u4 = reinterpret_cast<const float4*>(a1), *w4 = reinterpret_cast<const float4*>(b1);
+#pragma unroll 5
+    for (int d = 0; d < (dim >> 2); d++) {
+      const float4 x = __ldg(x4 + d), y = __ldg(y4 + d), u = __ldg(u4 + d), w = __ldg(w4 + d);
+      c0 = __fmaf_rn(x.x, y.x, c0);
+      c1 = __fmaf_rn(u.x, w.x, c1);
+      c0 = __fmaf_rn(x.y, y.y, c0);
+      c1 = __fmaf_rn(u.y, w.y, c1);
+      c0 = __fmaf_rn(x.z, y.z, c0);
+      c1 = __fmaf_rn(u.z, w.z, c1);
+      c0 = __fmaf_rn(x.w, y.w, c0);
+      c1 = __fmaf_rn(u.w, w.w, c1);
+    }
+  } else {
+    for (int d = 0; d < dim; d++) {
+      c0 = __fmaf_rn(__ldg(a0 + d), __ldg(b0 + d), c0);
+      c1 = __fmaf_rn(__ldg(a1 + d), __ldg(b1 + d), c1);
+    }
+  }
+  r0 = c0;
+  r1 = c1;
+}
+
 // Load that bypasses L1 (sees another warp's completed global stores).
 __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
   uint64_t v;
@@ -213,5 +270,132 @@ __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
 // Marks a candidate slot whose canonical similarity fell below theta.
 constexpr uint32_t kRejected = 0x7fc00001u;  // a NaN payload no similarity can have
 constexpr uint64_t kEmptySlot = ~0ull;         // candidate slot not yet written
+
+// Epilogue reduce + emission for one warp's 32 rows x 64 accumulator columns
+// (warp-synchronous; every lane calls it): group maxima over 8 columns with
+// 3-input max, a warp vote, and -- only if some lane has a column >= cutoff --
+// per-lane 64-bit hit masks, one warp scan + one shared atomic reserving the
+// warp's candidate slots, and per-lane stores of (row, j0 + column) pairs.
+// Columns >= col_lim are padding and never emitted.
+__device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
+                                                 uint32_t gi, uint32_t j0, int64_t col_lim,
+                                                 uint32_t* cta_cnt, uint32_t* cta_sat,
+                                                 uint64_t* seg, uint64_t seg_cap) {
+  const int lane = threadIdx.x & 31;
+  float g[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const float* x = v + 8 * k;
+    g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
+  }
+  const float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
+  const bool hit = row_ok && m >= cutoff;
+  if (!__any_sync(0xffffffffu, hit)) return;
+  uint32_t mk0 = 0, mk1 = 0;
+  if (hit) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (g[k] >= cutoff) {
+        uint32_t b = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) b |= (v[8 * k + e] >= cutoff ? 1u : 0u) << e;
+        if (k < 4) mk0 |= b << (8 * k);
+        else mk1 |= b << (8 * (k - 4));
+      }
+    }
+    if (col_lim < 64) {
+      const int cl = col_lim < 0 ? 0 : (int)col_lim;
+      mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
+      mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
+    }
+  }
+  const uint32_t cnt = __popc(mk0) + __popc(mk1);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t base = 0;
+  if (lane == 31 && wtot) {
+    base = atomicAdd(cta_cnt, wtot);
+    if (base + wtot < base) *cta_sat = 1u;
+  }
+  base = __shfl_sync(0xffffffffu, base, 31);
+  uint64_t pos = (uint64_t)base + (incl - cnt);
+  uint32_t w = mk0;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1;
+    if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + b);
+    pos++;
+  }
+  w = mk1;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1;
+    if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
+    pos++;
+  }
+}
+
+// One canonical recheck of a written candidate slot.
+__device__ __forceinline__ uint64_t wait_slot(const uint64_t* slot) {
+  uint64_t u;
+  do {
+    u = ld_volatile_u64(slot);
+  } while (u == kEmptySlot);
+  return u;
+}
+
+// Recheck warp loop shared by the filter kernels: warp `rw` of `nrw` owns
+// 64-slot blocks rw, rw + nrw, ... of this CTA's candidate segment; a block is
+// processed once fully reserved (or once all `n_epi` epilogue warps are done);
+// each lane re-decides two slots with interleaved canonical chains, writes
+// the canonical sim bits (or kRejected) and counts kept matches per left row.
+__device__ __forceinline__ void recheck_loop(const uint64_t* seg, uint32_t* sims, uint64_t seg_cap,
+                                             volatile uint32_t* vcnt, volatile uint32_t* vdone,
+                                             uint32_t n_epi, int rw, int nrw, const float* l32,
+                                             const float* r32, int dim, float theta,
+                                             uint32_t* rowcount) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t blk = rw;; blk += nrw) {
+    const uint64_t s0 = blk * 64;
+    uint64_t n;
+    for (;;) {
+      n = mn<uint64_t>(*vcnt, seg_cap);
+      if (n >= s0 + 64) break;
+      if (*vdone == n_epi) {
+        n = mn<uint64_t>(*vcnt, seg_cap);
+        break;
+      }
+      // not latency-critical: poll rarely so the epilogue keeps the issue slots
+      __nanosleep(2000);
+    }
+    if (s0 >= n) break;
+    const uint64_t sa = s0 + lane, sb = s0 + 32 + lane;
+    if (sb < n) {
+      const uint64_t ua = wait_slot(seg + sa), ub = wait_slot(seg + sb);
+      const uint32_t ia = (uint32_t)(ua >> 32), ja = (uint32_t)ua;
+      const uint32_t ib = (uint32_t)(ub >> 32), jb = (uint32_t)ub;
+      float xa, xb;
+      dot_seq2_dev(l32 + (size_t)ia * dim, r32 + (size_t)ja * dim, l32 + (size_t)ib * dim,
+                   r32 + (size_t)jb * dim, dim, xa, xb);
+      sims[sa] = xa >= theta ? __float_as_uint(xa) : kRejected;
+      sims[sb] = xb >= theta ? __float_as_uint(xb) : kRejected;
+      if (xa >= theta) atomicAdd(rowcount + ia, 1u);
+      if (xb >= theta) atomicAdd(rowcount + ib, 1u);
+    } else if (sa < n) {
+      const uint64_t ua = wait_slot(seg + sa);
+      const uint32_t ia = (uint32_t)(ua >> 32), ja = (uint32_t)ua;
+      const float xa = dot_seq_dev(l32 + (size_t)ia * dim, r32 + (size_t)ja * dim, dim);
+      sims[sa] = xa >= theta ? __float_as_uint(xa) : kRejected;
+      if (xa >= theta) atomicAdd(rowcount + ia, 1u);
+    }
+  }
+}
+
+
 
 }  // namespace sjb

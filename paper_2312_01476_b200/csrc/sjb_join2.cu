@@ -339,33 +339,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t* sims = p.sims_bits + (uint64_t)blockIdx.x * seg_cap;
     volatile uint32_t* vcnt = cta_cnt;
     volatile uint32_t* vdone = epi_done;
-    for (uint64_t blk = rw;; blk += kRecheckWarps) {
-      const uint64_t s0 = blk * 32;
-      uint64_t n;
-      for (;;) {
-        n = mn<uint64_t>(*vcnt, seg_cap);
-        if (n >= s0 + 32) break;
-        if (*vdone == (uint32_t)kEpiWarps) {
-          n = mn<uint64_t>(*vcnt, seg_cap);
-          break;
-        }
-        // not latency-critical: poll rarely so the epilogue keeps the issue slots
-        __nanosleep(2000);
-      }
-      if (s0 >= n) break;
-      const uint64_t slot = s0 + lane;
-      if (slot < n) {
-        uint64_t u;
-        do {
-          u = ld_volatile_u64(seg + slot);
-        } while (u == kEmptySlot);
-        const uint32_t i = (uint32_t)(u >> 32), j = (uint32_t)u;
-        const float s = dot_seq_dev(p.l32 + (size_t)i * p.dim, p.r32 + (size_t)j * p.dim, p.dim);
-        const bool keep = s >= p.theta;
-        sims[slot] = keep ? __float_as_uint(s) : kRejected;
-        if (keep) atomicAdd(p.rowcount + i, 1u);
-      }
-    }
+    recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps, p.l32,
+                 p.r32, p.dim, p.theta, p.rowcount);
   } else if (warp >= 2) {
     // ---------------------------------------------------------- epilogue
     // warp (q, c): TMEM lanes 32q..32q+31 (this CTA's R rows of the stage's

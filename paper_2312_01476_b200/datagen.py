@@ -70,6 +70,9 @@ CONFIGS = {
                  theta=0.8, seed=0),
     "cfg5": dict(n_left=200_000, n_right=200_000, dim=100, n_centroids=500, sigma=0.5,
                  theta=0.8, seed=0),
+    # wide embeddings; the full 1M x 4M join is R-sharded over 8 GPUs
+    "cfg4": dict(n_left=1_000_000, n_right=4_000_000, dim=768, n_centroids=50_000, sigma=0.6,
+                 theta=0.75, seed=0, zipf=1.1),
 }
 
 
@@ -77,7 +80,7 @@ def config_vectors(name: str, **over):
     c = dict(CONFIGS[name])
     c.update(over)
     return clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"], c["sigma"],
-                          c["seed"]), c
+                          c["seed"], zipf=c.get("zipf")), c
 
 
 _ALPHA = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)

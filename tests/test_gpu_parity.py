@@ -11,7 +11,8 @@ from conftest import case_inputs, golden_tokens
 
 pytestmark = pytest.mark.gpu
 
-GOLDEN_JOINS = ["c_small", "c_d4", "c_d64", "c_d16_neg", "c_one", "c_ragged", "c_all", "cfg1"]
+GOLDEN_JOINS = ["c_small", "c_d4", "c_d64", "c_d16_neg", "c_one", "c_ragged", "c_all", "cfg1",
+                "c_d200", "c_d768"]
 
 
 def _bits_equal(ms, lo, ro, so):
@@ -21,7 +22,8 @@ def _bits_equal(ms, lo, ro, so):
 
 def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
     """Rebuild the row-major bf16 matrix from the tiled operand image."""
-    kpad = (dim + 15) // 16 * 16
+    from paper_2312_01476_b200 import device as D
+    kpad = D.kpad(dim)
     a = op.view(torch.int16).cpu().numpy()
     T = 256
     tiles = a.size // (T * kpad)
@@ -47,6 +49,7 @@ def test_normalize_and_operand_image(cuda, dim):
     assert np.array_equal(rows[:, :dim], bf)
     assert (rows[:, dim:] == 0).all() and (full[n:] == 0).all()
     assert full.shape[0] % 256 == 0 and kpad % 16 == 0
+    assert kpad == (dim + 15) // 16 * 16 if dim <= 128 else kpad == (dim + 63) // 64 * 64
 
 
 @pytest.mark.parametrize("name", GOLDEN_JOINS)
@@ -116,6 +119,44 @@ def test_random_instances_match_oracle(cuda):
         wl, wr, ws = O.join_raw(L, S, theta, threads=4)
         assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta)
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
+
+
+def test_random_wide_instances_match_oracle(cuda):
+    """Wide embeddings (dim 129..800): the K-streaming filter kernel."""
+    from paper_2312_01476_b200 import device as D
+    rng = np.random.default_rng(4096)
+    for inst in range(16):
+        nl, nr = int(rng.integers(1, 600)), int(rng.integers(1, 900))
+        dim = int(rng.integers(129, 801))
+        c = int(rng.integers(1, 40))
+        L, S = O_pair(nl, nr, dim, c, float(rng.uniform(0.3, 1.0)), 100 + inst)
+        theta = float(rng.uniform(-0.1, 0.9))
+        pl = D.prepare(torch.from_numpy(L).to(cuda))
+        pr = D.prepare(torch.from_numpy(S).to(cuda))
+        m = D.join_prepared(pl, pr, theta)
+        lo, ro, so = m.to_host()
+        wl, wr, ws = O.join_raw(L, S, theta, threads=4)
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
+
+
+def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
+    from paper_2312_01476_b200 import device as D
+    meta = manifest["cases"]["c_d768"]
+    L, S = case_inputs(meta)
+    pl = D.prepare(torch.from_numpy(L).to(cuda))
+    pr = D.prepare(torch.from_numpy(S).to(cuda))
+    m = D.join_prepared(pl, pr, meta["theta"], cand_cap=64)   # forces the retry
+    assert m.retries >= 1
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, golden["c_d768_l"]) and np.array_equal(ro, golden["c_d768_r"])
+    assert np.array_equal(so.view(np.uint32), golden["c_d768_s"].view(np.uint32))
+    m = D.join_prepared(pl, pr, -1.0)
+    lo, ro, so = m.to_host()
+    assert len(lo) == len(L) * len(S)
+    wl, wr, ws = O.join_raw(L, S, -1.0, threads=8)
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
 
 
 def O_pair(nl, nr, dim, c, sigma, seed):

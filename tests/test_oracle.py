@@ -9,7 +9,8 @@ import pytest
 import oracle as O
 from conftest import case_inputs, golden_tokens
 
-JOIN_CASES = ["c_small", "c_d4", "c_d64", "c_d16_neg", "c_one", "c_ragged", "c_all", "cfg1"]
+JOIN_CASES = ["c_small", "c_d4", "c_d64", "c_d16_neg", "c_one", "c_ragged", "c_all", "cfg1",
+              "c_d200", "c_d768"]
 
 
 def test_normalize_kat(golden):

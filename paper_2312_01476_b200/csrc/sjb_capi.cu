@@ -89,12 +89,20 @@ struct JoinPlan {
   uint64_t seg_cap;
   bool pair;  // CTA-pair (cta_group::2) filter kernel
   bool wide;  // K-streaming kernel (kpad > 128)
+  bool wide_fused;        // wide: recheck inside the filter (A/B only)
+  int64_t tile_stride;    // wide, separate recheck: tile offsets per CTA
 };
+
+bool use_wide_fused() {
+  const char* f = getenv("SJB_WIDE_RECHECK");
+  return f != nullptr && strcmp(f, "fused") == 0;
+}
 
 // K-streaming plan (kpad > 128): 256 x 256 output tiles, 64-element K chunks.
 int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) {
   namespace W = sjb::wide;
   pl->wide = true;
+  pl->wide_fused = use_wide_fused();
   pl->a_bufs = 0;
   int stages = 0;
   while (stages < 6 && (int)W::smem_bytes(stages + 1) <= max_smem) stages++;
@@ -115,6 +123,7 @@ int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   if ((int64_t)grid > pl->n_items) grid = (int)(pl->n_items > 0 ? pl->n_items : 1);
   pl->grid = grid;
   pl->seg_cap = (uint64_t)(a->cand_cap / grid);
+  pl->tile_stride = pl->wide_fused ? 0 : W::tile_stride(pl->n_items, grid, tpc);
   return SJB_OK;
 }
 
@@ -159,6 +168,8 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->kpad = (int)sjb_kpad(a->dim);
   pl->pair = false;
   pl->wide = false;
+  pl->wide_fused = false;
+  pl->tile_stride = 0;
   if (pl->kpad > 128) return make_wide_plan(a, pl, sms, max_dyn_smem(dev));
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // Shared memory: prefer a double-buffered resident R block when that still
@@ -195,12 +206,12 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 
 // ------------------------------------------------------------ workspace
 struct JoinWs {
-  size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, total;
+  size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, total;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-JoinWs join_ws_layout(const sjb_join_args* a, int grid) {
+JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   JoinWs w;
   size_t o = 0;
   const size_t ccap = (size_t)(a->cand_cap > 0 ? a->cand_cap : 0);
@@ -217,6 +228,7 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid) {
   w.bsums = o;    o = align256(o + (nblocks + 1) * 8);
   w.bigrows = o;  o = align256(o + nl * 4);
   w.nbig = o;     o = align256(o + 16);
+  w.tiles = o;    o = align256(o + (size_t)grid * (size_t)tile_stride * 4);
   w.total = o;
   return w;
 }
@@ -297,6 +309,22 @@ int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SJB_OK;
+}
+
+// fp32 canonical rows f32[n][dim] (dim % 4 == 0) as a 2-D tensor; box =
+// 32 elements x 256 rows = one K chunk of a tile, 128 B swizzle.
+int encode_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)dim * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)sjb::wide::kRcKC, (cuuint32_t)sjb::kTileRows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(rows), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled (rows) failed (%d)", (int)r);
   return SJB_OK;
 }
 
@@ -500,11 +528,13 @@ int64_t sjb_join_workspace_bytes(const sjb_join_args* args) {
   if (!args) return -1;
   JoinPlan pl;
   int grid = 1;
+  int64_t tstride = 0;
   if (args->n_left > 0 && args->n_right > 0) {
     if (make_plan(args, &pl) != SJB_OK) return -1;
     grid = pl.grid;
+    tstride = pl.tile_stride;
   }
-  return (int64_t)join_ws_layout(args, grid).total;
+  return (int64_t)join_ws_layout(args, grid, tstride).total;
 }
 
 int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
@@ -524,7 +554,7 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   }
   JoinPlan pl;
   if (int rc = make_plan(args, &pl)) return rc;
-  const JoinWs w = join_ws_layout(args, pl.grid);
+  const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride);
   if ((int64_t)w.total > workspace_bytes)
     return fail(SJB_E_INVALID, "workspace %lld B < required %lld B", (long long)workspace_bytes,
                 (long long)w.total);
@@ -540,6 +570,7 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   uint64_t* bsums = reinterpret_cast<uint64_t*>(ws + w.bsums);
   uint32_t* bigrows = reinterpret_cast<uint32_t*>(ws + w.bigrows);
   unsigned int* nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
+  uint32_t* tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
 
   SJB_CK(cudaMemsetAsync(rowcount, 0, (size_t)nl * 4, st));
   SJB_CK(cudaMemsetAsync(nbig, 0, 16, st));
@@ -568,7 +599,8 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.sims_bits = sims_bits;
   jp.rowcount = rowcount;
   // candidate slots start empty: the fused recheck waits for each slot's write
-  SJB_CK(cudaMemsetAsync(cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
+  const bool fused_recheck = !pl.wide || pl.wide_fused;
+  if (fused_recheck) SJB_CK(cudaMemsetAsync(cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
   {
     const char* dm = getenv("SJB_DEBUG_MODE");
     jp.debug_mode = dm ? atoi(dm) : 0;
@@ -598,9 +630,53 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
     wp.sims_bits = sims_bits;
     wp.rowcount = rowcount;
     wp.debug = jp.debug_mode;
-    if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel, (int)pl.smem)) return rc;
-    sjb::wide::filter_kernel<<<pl.grid, sjb::wide::kThreads, pl.smem, st>>>(wp);
-    SJB_CK_LAUNCH("wide_filter");
+    wp.tile_off = tile_off;
+    wp.tile_stride = pl.tile_stride;
+    if (pl.wide_fused) {
+      if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<true>, (int)pl.smem)) return rc;
+      sjb::wide::filter_kernel<true>
+          <<<pl.grid, sjb::wide::Cfg<true>::kThreads, pl.smem, st>>>(wp);
+      SJB_CK_LAUNCH("wide_filter_fused");
+    } else {
+      if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<false>, (int)pl.smem)) return rc;
+      sjb::wide::filter_kernel<false>
+          <<<pl.grid, sjb::wide::Cfg<false>::kThreads, pl.smem, st>>>(wp);
+      SJB_CK_LAUNCH("wide_filter");
+      if (jp.debug_mode != 1) {
+        sjb::wide::RecheckParams rp;
+        rp.cand = cand;
+        rp.seg_cap = pl.seg_cap;
+        rp.cta_count = cta;
+        rp.tile_off = tile_off;
+        rp.tile_stride = pl.tile_stride;
+        rp.n_items = pl.n_items;
+        rp.n_ablk = pl.n_ablk;
+        rp.n_btiles = pl.n_btiles;
+        rp.tiles_per_chunk = pl.tiles_per_chunk;
+        rp.n_a = nl;
+        rp.n_b = nr;
+        rp.l32 = d_l32;
+        rp.r32 = d_r32;
+        rp.dim = (int)args->dim;
+        rp.theta = args->theta;
+        rp.sims_bits = sims_bits;
+        rp.rowcount = rowcount;
+        if ((args->dim & 3) == 0) {
+          sjb::wide::RecheckTmaParams tp;
+          tp.b = rp;
+          if (int rc = encode_rows_map(&tp.tmap_l, d_l32, nl, (int)args->dim)) return rc;
+          if (int rc = encode_rows_map(&tp.tmap_r, d_r32, nr, (int)args->dim)) return rc;
+          const int rs = (int)sjb::wide::recheck_tma_smem_bytes();
+          if (int rc = set_smem_attr((const void*)sjb::wide::recheck_tma_kernel, rs)) return rc;
+          sjb::wide::recheck_tma_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
+        } else {
+          const int rs = (int)sjb::wide::recheck_smem_bytes();
+          if (int rc = set_smem_attr((const void*)sjb::wide::recheck_generic_kernel, rs)) return rc;
+          sjb::wide::recheck_generic_kernel<<<pl.grid, sjb::wide::kRcThreads, rs, st>>>(rp);
+        }
+        SJB_CK_LAUNCH("wide_recheck");
+      }
+    }
   } else if (pl.pair) {
     sjb::pair::Params pp;
     pp.a16 = jp.a16;

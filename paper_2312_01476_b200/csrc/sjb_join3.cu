@@ -1,37 +1,51 @@
-// sjb_join3.cu -- fused threshold filter for wide embeddings (kpad > 128,
-// e.g. BASELINE cfg4 d = 768), K-streaming.
+// sjb_join3.cu -- threshold filter + canonical recheck for wide embeddings
+// (kpad > 128, e.g. BASELINE cfg4 d = 768), K-streaming.
 //
-// The resident-R design of sjb_join.cu needs the whole 256 x kpad R block in
-// shared memory (384 KB at d = 768), so here both operands stream through the
-// ring in K chunks of 64 elements: a stage = the R block's chunk (256 rows x
-// 64, 32 KB) + the S tile's chunk (256 rows x 64, 32 KB), both contiguous in
-// the [k-group][256][8] operand image.  Per chunk, 2 x 4 UMMA_128x256x16 (one
-// per R half) accumulate into the two 256-column halves of TMEM; the output
-// tile is 256 x 256 and K/64 chunks long (12 at d = 768: ~12k MMA cycles), so
-// one accumulator stage suffices: each 256-column TMEM half is handed back
-// (acc_empty[h]) as soon as the epilogue has drained it, so the next tile's
-// first MMAs overlap the emission of the previous one.  Epilogue, candidate segments and the fused canonical recheck
-// are those of sjb_join.cu.
+// Filter.  The resident-R design of sjb_join.cu needs the whole 256 x kpad R
+// block in shared memory (384 KB at d = 768), so here both operands stream
+// through the ring in K chunks of 64 elements: a stage = the R block's chunk
+// (256 rows x 64, 32 KB) + the S tile's chunk (256 rows x 64, 32 KB), both
+// contiguous in the [k-group][256][8] operand image.  Per chunk, 2 x 4
+// UMMA_128x256x16 (one per R half) accumulate into the two 256-column halves
+// of TMEM; the output tile is 256 x 256 and K/64 chunks long (12 at d = 768:
+// ~12k MMA cycles), so one accumulator stage suffices: each TMEM half is
+// handed back (acc_empty[h]) as soon as the epilogue has drained it, so the
+// next tile's first MMAs overlap the emission of the previous one.  The
+// epilogue and the candidate segments are those of sjb_join.cu.
+//
+// Recheck.  At d = 768 a candidate's canonical chain reads 2 x 3 KB of fp32
+// rows, and clustered data gives ~600 candidates per 256 x 256 tile, so
+// per-candidate gathers from L2 (the fused recheck of sjb_join.cu) cost
+// ~6 KB/candidate of L2 traffic -- 5x the filter's own.  The default here
+// is therefore a second kernel, `recheck_kernel`: the filter records where
+// each tile's candidates start in its segment (`tile_off`), and the recheck
+// walks the same tiles, stages the tile's fp32 R and S rows in 32-element K
+// chunks through shared memory (double-buffered cp.async) and advances every
+// candidate's sequential FMA chain chunk by chunk -- the same d = 0..dim-1
+// order, so the value is bitwise `sj_dot_seq` (_kernelcore.c:101-106).  L2
+// traffic drops to ~1.5 MB per tile (~2.5 KB per candidate).  Tiles with few
+// candidates skip the staging and gather directly.  The fused variant
+// (kFused = true, 10 recheck warps) is kept for A/B measurement.
 #include "sjb_common.cuh"
 
 namespace sjb {
 namespace wide {
 
-// At d >= 129 a 256 x 256 tile is >= 9 K-chunks of MMA work while the
-// canonical recheck of its candidates is d-long chains from L2, so the warps
-// lean to the recheck side.
 constexpr int kEpiWarps = 8;
-constexpr int kRecheckWarps = 10;
 constexpr int kChunksPerWarp = 16 / kEpiWarps;  // 64-column chunks per half
-constexpr int kThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
-constexpr int kKChunk = 64;                 // K elements per stage
+template <bool kFused>
+struct Cfg {
+  static constexpr int kRecheckWarps = kFused ? 10 : 0;
+  static constexpr int kThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
+};
+constexpr int kKChunk = 64;                           // K elements per stage
 constexpr int kChunkBytes = kTileRows * kKChunk * 2;  // 32 KB per operand
 
 struct Params {
   const __nv_bfloat16* a16;
   const __nv_bfloat16* b16;
   int64_t n_a, n_b;
-  int kpad;            // multiple of 64
+  int kpad;              // multiple of 64
   int n_ablk, n_btiles;  // 256-row blocks / tiles
   int tiles_per_chunk;
   int64_t n_items;
@@ -40,20 +54,33 @@ struct Params {
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
+  uint32_t* tile_off;    // [grid][tile_stride]: segment offset at each tile start (+ end)
+  int64_t tile_stride;
   const float* l32;
   const float* r32;
   int dim;
   float theta;
   uint32_t* sims_bits;
   uint32_t* rowcount;
-  int debug;  // 1: recheck warps idle (filter timing only; results invalid)
+  int debug;  // 1: fused recheck warps idle (filter timing only; results invalid)
 };
 
 __host__ __device__ inline uint32_t smem_bytes(int stages) {
   return (uint32_t)stages * 2 * kChunkBytes + (4 + 2 * stages) * 8 + 32;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
+// Max tiles one CTA walks (+1 for the end offset).
+__host__ __device__ inline int64_t tile_stride(int64_t n_items, int grid, int tiles_per_chunk) {
+  return ((n_items + grid - 1) / grid) * tiles_per_chunk + 1;
+}
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+}
+
+template <bool kFused>
+__global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const Params p) {
+  constexpr int kRecheckWarps = Cfg<kFused>::kRecheckWarps;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;  // stage s: A chunk at s*64K, B chunk at s*64K + 32K
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * 2 * kChunkBytes);
@@ -159,12 +186,13 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
       }
     }
   } else if (warp >= 2 + kEpiWarps) {
-    // ------------------------------------------------------ recheck warps
+    // ------------------------------------------- fused recheck (kFused only)
     const uint64_t seg_cap = p.seg_cap;
     if (p.debug != 1)
-      recheck_loop(p.cand + (uint64_t)blockIdx.x * seg_cap, p.sims_bits + (uint64_t)blockIdx.x * seg_cap,
-                 seg_cap, cta_cnt, epi_done, (uint32_t)kEpiWarps, warp - 2 - kEpiWarps,
-                 kRecheckWarps, p.l32, p.r32, p.dim, p.theta, p.rowcount);
+      recheck_loop(p.cand + (uint64_t)blockIdx.x * seg_cap,
+                   p.sims_bits + (uint64_t)blockIdx.x * seg_cap, seg_cap, cta_cnt, epi_done,
+                   (uint32_t)kEpiWarps, warp - 2 - kEpiWarps, kRecheckWarps, p.l32, p.r32, p.dim,
+                   p.theta, p.rowcount);
   } else {
     // ---------------------------------------------------------- epilogue
     // warp (q, c): TMEM lanes 32q..32q+31 x column chunks c, c + 2 (64 each)
@@ -175,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
     const float cutoff = p.cutoff;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
+    uint32_t* toff = kFused ? nullptr : p.tile_off + (int64_t)blockIdx.x * p.tile_stride;
     uint32_t tile_it = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
@@ -183,6 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
       for (int64_t t = t0; t < t1; t++, tile_it++) {
         mbar_wait(acc_full, tile_it & 1u);
         tc_fence_after();
+        if (!kFused) {
+          // every epilogue warp is done with the previous tile's emission:
+          // the counter is this tile's first slot
+          epi_bar();
+          if (ew == 0 && lane == 0) toff[tile_it] = *(volatile uint32_t*)cta_cnt;
+        }
 #pragma unroll 1
         for (int h = 0; h < 2; h++) {
           const int64_t gi64 = rb * kTileRows + h * 128 + lane_base + lane;
@@ -207,6 +242,10 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
         }
       }
     }
+    if (!kFused) {
+      epi_bar();
+      if (ew == 0 && lane == 0) toff[tile_it] = *(volatile uint32_t*)cta_cnt;
+    }
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -222,6 +261,409 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Params p) {
   }
   if (threadIdx.x == 0)
     p.cta_count[blockIdx.x] = *cta_sat ? ~0ull >> 1 : (unsigned long long)*cta_cnt;
+}
+
+// ------------------------------------------------------------- recheck
+constexpr int kRcThreads = 512;
+constexpr int kRcKC = 32;             // K elements per staged chunk
+constexpr int kRcPitch = kRcKC + 4;   // floats per staged row (16 B aligned, bank spread)
+constexpr int kRcCpt = 4;             // candidates per thread per pass
+constexpr int kRcPass = kRcThreads * kRcCpt;
+constexpr int kRcDirect = 128;        // fewer candidates than this: gather, no staging
+constexpr int kRcBufFloats = 2 * kTileRows * kRcPitch;  // A + B rows of one chunk
+
+__host__ __device__ constexpr uint32_t recheck_smem_bytes() {
+  return 2u * kRcBufFloats * 4u;
+}
+
+struct RecheckParams {
+  const uint64_t* cand;
+  uint64_t seg_cap;
+  const unsigned long long* cta_count;
+  const uint32_t* tile_off;
+  int64_t tile_stride;
+  int64_t n_items;
+  int n_ablk, n_btiles, tiles_per_chunk;
+  int64_t n_a, n_b;
+  const float* l32;
+  const float* r32;
+  int dim;
+  float theta;
+  uint32_t* sims_bits;
+  uint32_t* rowcount;
+};
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Stage K chunk `ch` of the tile's R rows (r0.., nr_a valid) and S rows.
+__device__ __forceinline__ void stage_chunk(float* buf, const float* l32, const float* r32,
+                                            int64_t r0, int nr_a, int64_t c0, int nr_b, int dim,
+                                            int ch, bool vec) {
+  const int k0 = ch * kRcKC;
+  const int kc = mn(kRcKC, dim - k0);
+  float* as = buf;
+  float* bs = buf + kTileRows * kRcPitch;
+  if (vec) {  // dim % 4 == 0: rows and chunk starts are 16 B aligned
+    const int q4 = kc >> 2;
+    for (int idx = threadIdx.x; idx < 2 * kTileRows * 8; idx += kRcThreads) {
+      const int side = idx >= kTileRows * 8;
+      const int e = side ? idx - kTileRows * 8 : idx;
+      const int r = e >> 3, q = e & 7;
+      if (q >= q4) continue;
+      if (!side) {
+        if (r < nr_a) cp_async16(as + r * kRcPitch + 4 * q, l32 + (r0 + r) * dim + k0 + 4 * q);
+      } else {
+        if (r < nr_b) cp_async16(bs + r * kRcPitch + 4 * q, r32 + (c0 + r) * dim + k0 + 4 * q);
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < 2 * kTileRows * kRcKC; idx += kRcThreads) {
+      const int side = idx >= kTileRows * kRcKC;
+      const int e = side ? idx - kTileRows * kRcKC : idx;
+      const int r = e / kRcKC, q = e % kRcKC;
+      if (q >= kc) continue;
+      if (!side) {
+        if (r < nr_a) cp_async4(as + r * kRcPitch + q, l32 + (r0 + r) * dim + k0 + q);
+      } else {
+        if (r < nr_b) cp_async4(bs + r * kRcPitch + q, r32 + (c0 + r) * dim + k0 + q);
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void finish_candidate(uint32_t* sims, uint64_t slot, uint32_t gi,
+                                                 float x, float theta, uint32_t* rowcount) {
+  const bool ok = x >= theta;
+  sims[slot] = ok ? __float_as_uint(x) : kRejected;
+  if (ok) atomicAdd(rowcount + gi, 1u);
+}
+
+// One CTA per filter segment; walks the segment's tiles in the filter's order.
+// cp.async staging, any dim (the TMA kernel below needs dim % 4 == 0).
+__global__ void __launch_bounds__(kRcThreads, 1) recheck_generic_kernel(const RecheckParams p) {
+  extern __shared__ __align__(16) float rsm[];
+  const int c = blockIdx.x;
+  const unsigned long long cc = p.cta_count[c];
+  if (cc > p.seg_cap) return;  // saturated segment: the join is retried with room
+  const uint64_t* seg = p.cand + (uint64_t)c * p.seg_cap;
+  uint32_t* sims = p.sims_bits + (uint64_t)c * p.seg_cap;
+  const uint32_t* toff = p.tile_off + (int64_t)c * p.tile_stride;
+  const int dim = p.dim;
+  const float theta = p.theta;
+  const int nch = (dim + kRcKC - 1) / kRcKC;
+  const bool vec = (dim & 3) == 0;
+  const int nb = p.n_ablk;
+  int64_t k = 0;
+  for (int64_t item = c; item < p.n_items; item += gridDim.x) {
+    const int64_t rb = item % nb, sc = item / nb;
+    const int64_t t0 = sc * p.tiles_per_chunk;
+    const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+    for (int64_t t = t0; t < t1; t++, k++) {
+      const uint32_t lo = toff[k], hi = toff[k + 1];
+      if (hi <= lo) continue;
+      const uint32_t n = hi - lo;
+      if (n < kRcDirect) {
+        // ------------------------------------------------ direct gathers
+        for (uint32_t s = lo + threadIdx.x; s < hi; s += kRcThreads) {
+          const uint64_t u = seg[s];
+          const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;
+          const float x = dot_seq_dev(p.l32 + (size_t)gi * dim, p.r32 + (size_t)gj * dim, dim);
+          finish_candidate(sims, s, gi, x, theta, p.rowcount);
+        }
+        continue;
+      }
+      // -------------------------------------------------- staged chunks
+      const int64_t r0 = rb * kTileRows, c0 = t * kTileRows;
+      const int nr_a = (int)mn<int64_t>(kTileRows, p.n_a - r0);
+      const int nr_b = (int)mn<int64_t>(kTileRows, p.n_b - c0);
+      for (uint32_t base = lo; base < hi; base += kRcPass) {
+        uint32_t ia[kRcCpt], jb[kRcCpt];
+        float acc[kRcCpt];
+#pragma unroll
+        for (int m = 0; m < kRcCpt; m++) {
+          const uint32_t s = base + threadIdx.x + m * kRcThreads;
+          acc[m] = 0.0f;
+          ia[m] = jb[m] = 0xFFFFFFFFu;
+          if (s < hi) {
+            const uint64_t u = seg[s];
+            ia[m] = (uint32_t)((u >> 32) - (uint64_t)r0) * kRcPitch;
+            jb[m] = ((uint32_t)u - (uint32_t)c0) * kRcPitch;
+          }
+        }
+        stage_chunk(rsm, p.l32, p.r32, r0, nr_a, c0, nr_b, dim, 0, vec);
+        for (int ch = 0; ch < nch; ch++) {
+          if (ch + 1 < nch) {
+            stage_chunk(rsm + ((ch + 1) & 1) * kRcBufFloats, p.l32, p.r32, r0, nr_a, c0, nr_b,
+                        dim, ch + 1, vec);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();
+          const float* as = rsm + (ch & 1) * kRcBufFloats;
+          const float* bs = as + kTileRows * kRcPitch;
+          const int kc = mn(kRcKC, dim - ch * kRcKC);
+          if (kc == kRcKC) {
+#pragma unroll
+            for (int m = 0; m < kRcCpt; m++) {
+              if (ia[m] == 0xFFFFFFFFu) continue;
+              const float4* a4 = reinterpret_cast<const float4*>(as + ia[m]);
+              const float4* b4 = reinterpret_cast<const float4*>(bs + jb[m]);
+              float x = acc[m];
+#pragma unroll
+              for (int q = 0; q < kRcKC / 4; q++) {
+                const float4 a = a4[q], b = b4[q];
+                x = __fmaf_rn(a.x, b.x, x);
+                x = __fmaf_rn(a.y, b.y, x);
+                x = __fmaf_rn(a.z, b.z, x);
+                x = __fmaf_rn(a.w, b.w, x);
+              }
+              acc[m] = x;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < kRcCpt; m++) {
+              if (ia[m] == 0xFFFFFFFFu) continue;
+              float x = acc[m];
+              for (int q = 0; q < kc; q++) x = __fmaf_rn(as[ia[m] + q], bs[jb[m] + q], x);
+              acc[m] = x;
+            }
+          }
+          __syncthreads();  // buffer (ch & 1) is restaged at ch + 2
+        }
+#pragma unroll
+        for (int m = 0; m < kRcCpt; m++) {
+          const uint32_t s = base + threadIdx.x + m * kRcThreads;
+          if (s < hi)
+            finish_candidate(sims, s, (uint32_t)(r0 + ia[m] / kRcPitch), acc[m], theta,
+                             p.rowcount);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------ recheck, TMA-staged
+// Warp 0 lane 0 streams each staged tile's fp32 R and S rows, K chunk by K
+// chunk (2-D tensor TMA, box 32 x 256, 128 B swizzle: 16 B group q of row r
+// lands at q ^ (r & 7), so 8 lanes reading 8 rows hit 8 bank groups when the
+// rows differ mod 8), through a 3-stage mbarrier ring.  11 compute warps own
+// up to 4 candidates per thread per pass and advance two chains at a time.
+constexpr int kRtComputeWarps = 11;  // + producer = 384 threads (168-register cap)
+constexpr int kRtThreads = 32 * (1 + kRtComputeWarps);
+constexpr int kRtStages = 3;
+constexpr int kRtCpt = 4;
+constexpr int kRtPass = kRtComputeWarps * 32 * kRtCpt;
+constexpr int kRtOpBytes = kTileRows * kRcKC * 4;  // 32 KB: 256 rows x 128 B
+
+__host__ __device__ constexpr uint32_t recheck_tma_smem_bytes() {
+  return kRtStages * 2 * kRtOpBytes + 1024 + 2 * kRtStages * 8;
+}
+
+struct RecheckTmaParams {
+  RecheckParams b;
+  CUtensorMap tmap_l, tmap_r;  // fp32 rows: dims {dim, n}, box {32, 256}, SWIZZLE_128B
+};
+
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds1(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+// byte offset of element (row r, k) in a swizzled [256][32] fp32 stage
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t k) {
+  return r * 128u + ((((k >> 2) ^ (r & 7u))) << 4) + (k & 3u) * 4u;
+}
+
+__global__ void __launch_bounds__(kRtThreads, 1)
+    recheck_tma_kernel(const __grid_constant__ RecheckTmaParams tp) {
+  const RecheckParams& p = tp.b;
+  extern __shared__ uint8_t rt_raw[];
+  const uint32_t raw = smem_u32(rt_raw);
+  uint8_t* base = rt_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kRtStages * 2 * kRtOpBytes);
+  uint64_t* empty = full + kRtStages;
+  const int c = blockIdx.x;
+  if (p.cta_count[c] > p.seg_cap) return;  // saturated segment: the join is retried
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRtStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kRtComputeWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t* seg = p.cand + (uint64_t)c * p.seg_cap;
+  uint32_t* sims = p.sims_bits + (uint64_t)c * p.seg_cap;
+  const uint32_t* toff = p.tile_off + (int64_t)c * p.tile_stride;
+  const int dim = p.dim;
+  const int nch = (dim + kRcKC - 1) / kRcKC;
+  const int nb = p.n_ablk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int s = 0;
+  uint32_t ph = 0;
+
+  if (warp == 0) {
+    if (lane != 0) return;
+    // -------------------------------------------------------- producer
+    int64_t k = 0;
+    for (int64_t item = c; item < p.n_items; item += gridDim.x) {
+      const int64_t rb = item % nb, sc = item / nb;
+      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+      for (int64_t t = t0; t < t1; t++, k++) {
+        const uint32_t lo = toff[k], hi = toff[k + 1];
+        if (hi <= lo || hi - lo < (uint32_t)kRcDirect) continue;
+        for (uint32_t pb = lo; pb < hi; pb += kRtPass) {
+          for (int ch = 0; ch < nch; ch++) {
+            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[s], 2 * kRtOpBytes);
+            uint8_t* dst = base + (size_t)s * 2 * kRtOpBytes;
+            tma2d(dst, &tp.tmap_l, ch * kRcKC, (int)(rb * kTileRows), &full[s]);
+            tma2d(dst + kRtOpBytes, &tp.tmap_r, ch * kRcKC, (int)(t * kTileRows), &full[s]);
+            if (++s == kRtStages) {
+              s = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ compute
+  const int ct = threadIdx.x - 32;
+  constexpr int kCT = kRtComputeWarps * 32;
+  const float theta = p.theta;
+  int64_t k = 0;
+  for (int64_t item = c; item < p.n_items; item += gridDim.x) {
+    const int64_t rb = item % nb, sc = item / nb;
+    const int64_t t0 = sc * p.tiles_per_chunk;
+    const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+    for (int64_t t = t0; t < t1; t++, k++) {
+      const uint32_t lo = toff[k], hi = toff[k + 1];
+      if (hi <= lo) continue;
+      if (hi - lo < (uint32_t)kRcDirect) {
+        for (uint32_t q = lo + ct; q < hi; q += kCT) {
+          const uint64_t u = seg[q];
+          const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;
+          const float x = dot_seq_dev(p.l32 + (size_t)gi * dim, p.r32 + (size_t)gj * dim, dim);
+          finish_candidate(sims, q, gi, x, theta, p.rowcount);
+        }
+        continue;
+      }
+      const uint32_t r0 = (uint32_t)(rb * kTileRows), c0 = (uint32_t)(t * kTileRows);
+      for (uint32_t pb = lo; pb < hi; pb += kRtPass) {
+        uint32_t ra[kRtCpt], rbv[kRtCpt];
+        float acc[kRtCpt];
+        int nm = 0;  // this thread's candidates in the pass (prefix of m)
+#pragma unroll
+        for (int m = 0; m < kRtCpt; m++) {
+          const uint32_t q = pb + ct + m * kCT;
+          acc[m] = 0.0f;
+          ra[m] = rbv[m] = 0;
+          if (q < hi) {
+            const uint64_t u = seg[q];
+            ra[m] = (uint32_t)(u >> 32) - r0;
+            rbv[m] = (uint32_t)u - c0;
+            nm = m + 1;
+          }
+        }
+        for (int ch = 0; ch < nch; ch++) {
+          mbar_wait(&full[s], ph);
+          const uint32_t sa = smem_u32(base + (size_t)s * 2 * kRtOpBytes);
+          const uint32_t sb = sa + kRtOpBytes;
+          const int kc = mn(kRcKC, dim - ch * kRcKC);
+          if (kc == kRcKC) {
+#pragma unroll
+            for (int m = 0; m < kRtCpt; m += 2) {
+              if (m >= nm) break;
+              const uint32_t a0 = sa + ra[m] * 128u, x0 = ra[m] & 7u;
+              const uint32_t b0 = sb + rbv[m] * 128u, y0 = rbv[m] & 7u;
+              float u0 = acc[m];
+              if (m + 1 < nm) {
+                const uint32_t a1 = sa + ra[m + 1] * 128u, x1 = ra[m + 1] & 7u;
+                const uint32_t b1 = sb + rbv[m + 1] * 128u, y1 = rbv[m + 1] & 7u;
+                float u1 = acc[m + 1];
+#pragma unroll
+                for (int g = 0; g < kRcKC / 4; g++) {
+                  const float4 pa = lds4(a0 + ((g ^ x0) << 4)), pbv = lds4(b0 + ((g ^ y0) << 4));
+                  const float4 qa = lds4(a1 + ((g ^ x1) << 4)), qb = lds4(b1 + ((g ^ y1) << 4));
+                  u0 = __fmaf_rn(pa.x, pbv.x, u0);
+                  u1 = __fmaf_rn(qa.x, qb.x, u1);
+                  u0 = __fmaf_rn(pa.y, pbv.y, u0);
+                  u1 = __fmaf_rn(qa.y, qb.y, u1);
+                  u0 = __fmaf_rn(pa.z, pbv.z, u0);
+                  u1 = __fmaf_rn(qa.z, qb.z, u1);
+                  u0 = __fmaf_rn(pa.w, pbv.w, u0);
+                  u1 = __fmaf_rn(qa.w, qb.w, u1);
+                }
+                acc[m + 1] = u1;
+              } else {
+#pragma unroll
+                for (int g = 0; g < kRcKC / 4; g++) {
+                  const float4 pa = lds4(a0 + ((g ^ x0) << 4)), pbv = lds4(b0 + ((g ^ y0) << 4));
+                  u0 = __fmaf_rn(pa.x, pbv.x, u0);
+                  u0 = __fmaf_rn(pa.y, pbv.y, u0);
+                  u0 = __fmaf_rn(pa.z, pbv.z, u0);
+                  u0 = __fmaf_rn(pa.w, pbv.w, u0);
+                }
+              }
+              acc[m] = u0;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < kRtCpt; m++) {
+              if (m >= nm) break;
+              float u0 = acc[m];
+              for (int e = 0; e < kc; e++)
+                u0 = __fmaf_rn(lds1(sa + swz(ra[m], e)), lds1(sb + swz(rbv[m], e)), u0);
+              acc[m] = u0;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&empty[s]);
+          if (++s == kRtStages) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < kRtCpt; m++)
+          if (m < nm)
+            finish_candidate(sims, pb + ct + m * kCT, r0 + ra[m], acc[m], theta, p.rowcount);
+      }
+    }
+  }
 }
 
 }  // namespace wide

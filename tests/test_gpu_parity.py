@@ -140,6 +140,21 @@ def test_random_wide_instances_match_oracle(cuda):
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
 
 
+@pytest.mark.parametrize("variant", ["fused", "staged"])
+def test_wide_recheck_variants(cuda, manifest, golden, monkeypatch, variant):
+    """Both wide recheck variants (fused warps / staged second kernel) are exact."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv("SJB_WIDE_RECHECK", variant)
+    for name in ("c_d200", "c_d768"):
+        meta = manifest["cases"][name]
+        L, S = case_inputs(meta)
+        m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                            D.prepare(torch.from_numpy(S).to(cuda)), meta["theta"])
+        lo, ro, so = m.to_host()
+        assert np.array_equal(lo, golden[name + "_l"]) and np.array_equal(ro, golden[name + "_r"])
+        assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
+
+
 def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
     from paper_2312_01476_b200 import device as D
     meta = manifest["cases"]["c_d768"]

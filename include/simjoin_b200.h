@@ -41,12 +41,22 @@ int sjb_sm_count(int device);
  * threads); lets callers count the GPU launches inside a timed region. */
 int64_t sjb_launch_count(void);
 
-/* Padded reduction depth of the bf16 operand image for `dim` (multiple of 16). */
+/* Padded reduction depth of the bf16 operand image for `dim`: a multiple of
+ * 16 for dim <= 128, of 64 above (K-streaming kernel). */
 int64_t sjb_kpad(int64_t dim);
 /* Elements of the bf16 operand image of an n-row relation: n rounded up to a
- * multiple of 256 rows, times kpad.  Layout: 256-row tiles, each
+ * multiple of 512 rows, times kpad.  Layout: 256-row tiles, each
  * [k-group (kpad/8)][row (256)][8 elements] (UMMA K-major, no swizzle). */
 int64_t sjb_operand_elems(int64_t n, int64_t dim);
+/* 256-row tiles of that image (= entries of a d_tile_err array). */
+int64_t sjb_tile_count(int64_t n);
+
+/* bf16 rounding-error outputs of the prep functions below (both optional,
+ * written only together with d_out16):
+ *   d_row_err[i]  (n floats)  >= ||bf16(x_i) - x_i||_2 of canonical row x_i
+ *   d_tile_err[t] (sjb_tile_count(n) floats) = max of d_row_err over tile t
+ * They let the join use a per-row filter band (sjb_join_args.left_row_err /
+ * right_tile_err) instead of the worst-case sjb_default_band. */
 
 /* ---- prefetch stage: embedding + normalise-and-cast -------------------- */
 
@@ -57,14 +67,16 @@ int64_t sjb_operand_elems(int64_t n, int64_t dim);
  * bf16 operand image (sjb_operand_elems elements).  *d_repaired (optional
  * device u64) is incremented by the number of repaired rows. */
 int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32,
-                       void* d_out16, unsigned long long* d_repaired, void* stream);
+                       void* d_out16, unsigned long long* d_repaired, float* d_row_err,
+                       float* d_tile_err, void* stream);
 
 /* Lookup-model prefetch fused with the normalisation: relation row i is
  * table row d_index[i] (LookupModel._vector, embedding.py:143-152, then
  * normalize_rows); outputs as sjb_normalize_rows. */
 int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int64_t n,
                               int64_t dim, float* d_out32, void* d_out16,
-                              unsigned long long* d_repaired, void* stream);
+                              unsigned long long* d_repaired, float* d_row_err,
+                              float* d_tile_err, void* stream);
 
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
@@ -79,7 +91,7 @@ int sjb_fnv1a64_many(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
  * SyntheticModel._embed_into, embedding.py:95-107), normalised per the model.
  * d_out16 optional as above. */
 int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, float* d_out32,
-                            void* d_out16, void* stream);
+                            void* d_out16, float* d_row_err, float* d_tile_err, void* stream);
 
 /* FastText-style subword model (cfg3; no reference counterpart, see
  * DESIGN.md): row = mean of table rows of the word hash and every
@@ -88,7 +100,8 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
 int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
                       const float* d_table, int64_t n_buckets, int64_t dim, int minn,
                       int maxn, int normalize, float* d_out32, void* d_out16,
-                      unsigned long long* d_repaired, void* stream);
+                      unsigned long long* d_repaired, float* d_row_err, float* d_tile_err,
+                      void* stream);
 
 /* ---- the fused join --------------------------------------------------- */
 
@@ -103,6 +116,14 @@ typedef struct sjb_join_args {
   int32_t tiles_per_chunk; /* 0 = automatic */
   void* ev_filter_begin;   /* optional cudaEvent_t recorded around the filter */
   void* ev_filter_end;     /* kernel on `stream` (profiling hook), or NULL */
+  /* Optional per-row band (both or neither): the left relation's d_row_err
+   * and the right relation's d_tile_err from the prep functions.  Row i of
+   * S tile t then keeps pairs with approx >= max(theta - band,
+   * theta - b_it), b_it = slack + (1+1e-6)(e_i + E_t) + e_i E_t,
+   * slack = sjb_accum_slack(dim): Cauchy-Schwarz on the measured bf16
+   * rounding errors, so no true match is dropped. */
+  const float* left_row_err;
+  const float* right_tile_err;
 } sjb_join_args;
 
 typedef struct sjb_join_info {
@@ -119,6 +140,9 @@ int64_t sjb_join_workspace_bytes(const sjb_join_args* args);
 /* Default (provably sufficient) band for `dim`: bf16 rounding of unit
  * vectors (2u+u^2, u = 2^-8) plus fp32 accumulation slack. */
 float sjb_default_band(int64_t dim);
+/* The accumulation part of that band (+ 1e-6 for the fp32 cutoff
+ * arithmetic): the `slack` of the per-row band (sjb_join_args). */
+float sjb_accum_slack(int64_t dim);
 
 /* Join two prepared (normalised) relations on the device; asynchronous.
  * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: bf16 operand images.

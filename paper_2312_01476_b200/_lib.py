@@ -14,7 +14,8 @@ from .build import LIB_PATH
 EXPORTS = (
     "sjb_version", "sjb_last_error", "sjb_launch_count", "sjb_sm_count", "sjb_kpad", "sjb_operand_elems",
     "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
-    "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band",
+    "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band", "sjb_accum_slack",
+    "sjb_tile_count",
     "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm",
     "sjb_scan_hits", "sjb_scan_hits_workspace_bytes",
 )
@@ -30,6 +31,7 @@ class JoinArgs(ctypes.Structure):
         ("left_base", ctypes.c_uint64),
         ("grid", ctypes.c_int32), ("tiles_per_chunk", ctypes.c_int32),
         ("ev_filter_begin", ctypes.c_void_p), ("ev_filter_end", ctypes.c_void_p),
+        ("left_row_err", ctypes.c_void_p), ("right_tile_err", ctypes.c_void_p),
     ]
 
 
@@ -71,13 +73,17 @@ def lib(path: str = LIB_PATH):
     L.sjb_operand_elems.argtypes = [_i64, _i64]
     L.sjb_default_band.restype = ctypes.c_float
     L.sjb_default_band.argtypes = [_i64]
-    L.sjb_normalize_rows.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp]
-    L.sjb_gather_normalize_rows.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
+    L.sjb_accum_slack.restype = ctypes.c_float
+    L.sjb_accum_slack.argtypes = [_i64]
+    L.sjb_tile_count.restype = _i64
+    L.sjb_tile_count.argtypes = [_i64]
+    L.sjb_normalize_rows.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.sjb_gather_normalize_rows.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
     L.sjb_row_norms.argtypes = [_vp, _i64, _i64, _vp, _vp]
     L.sjb_fnv1a64_many.argtypes = [_vp, _vp, _i64, ctypes.c_uint64, _vp, _vp]
-    L.sjb_synthetic_fill_many.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
+    L.sjb_synthetic_fill_many.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]
     L.sjb_subword_embed.argtypes = [_vp, _vp, _i64, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int,
-                                    ctypes.c_int, _vp, _vp, _vp, _vp]
+                                    ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
     L.sjb_join_workspace_bytes.restype = _i64
     L.sjb_join_workspace_bytes.argtypes = [ctypes.POINTER(JoinArgs)]
     L.sjb_join_prepared_async.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,

@@ -440,9 +440,19 @@ float sjb_default_band(int64_t dim) {
   return (float)b;
 }
 
+float sjb_accum_slack(int64_t dim) {
+  // fp32 accumulation error of the tensor-core and canonical sums (as in
+  // sjb_default_band) + 2e-6 for the fp32 evaluation of the per-row cutoff
+  return (float)(4.0 * (double)dim * 5.9604644775390625e-08 + 2e-6);
+}
+
+int64_t sjb_tile_count(int64_t n) {
+  return sjb::round_up(n < 0 ? 0 : n, 2 * sjb::kTileRows) / sjb::kTileRows;
+}
+
 static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n, int64_t dim,
                           float* d_out32, void* d_out16, unsigned long long* d_repaired,
-                          void* stream) {
+                          float* d_row_err, float* d_tile_err, void* stream) {
   if (n < 0 || dim < 1)
     return fail(SJB_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
   const int kpad = (int)sjb_kpad(dim);
@@ -454,21 +464,25 @@ static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n,
   if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
   sjb::normalize_cast_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
       d_in, d_gather, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16),
-      d_repaired, 1);
+      d_repaired, 1, d_out16 ? d_row_err : nullptr, d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("normalize_cast");
   return SJB_OK;
 }
 
 int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
-                       unsigned long long* d_repaired, void* stream) {
-  return normalize_impl(d_in, nullptr, n, dim, d_out32, d_out16, d_repaired, stream);
+                       unsigned long long* d_repaired, float* d_row_err, float* d_tile_err,
+                       void* stream) {
+  return normalize_impl(d_in, nullptr, n, dim, d_out32, d_out16, d_repaired, d_row_err,
+                        d_tile_err, stream);
 }
 
 int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int64_t n,
                               int64_t dim, float* d_out32, void* d_out16,
-                              unsigned long long* d_repaired, void* stream) {
+                              unsigned long long* d_repaired, float* d_row_err,
+                              float* d_tile_err, void* stream) {
   if (!d_index) return fail(SJB_E_INVALID, "null index");
-  return normalize_impl(d_table, d_index, n, dim, d_out32, d_out16, d_repaired, stream);
+  return normalize_impl(d_table, d_index, n, dim, d_out32, d_out16, d_repaired, d_row_err,
+                        d_tile_err, stream);
 }
 
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream) {
@@ -489,7 +503,7 @@ int sjb_fnv1a64_many(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n, u
 }
 
 int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, float* d_out32,
-                            void* d_out16, void* stream) {
+                            void* d_out16, float* d_row_err, float* d_tile_err, void* stream) {
   if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape");
   const int kpad = (int)sjb_kpad(dim);
   const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
@@ -499,7 +513,8 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::synthetic_fill_kernel, smem)) return rc;
   sjb::synthetic_fill_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
-      d_seeds, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16));
+      d_seeds, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16),
+      d_out16 ? d_row_err : nullptr, d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("synthetic_fill");
   return SJB_OK;
 }
@@ -507,7 +522,8 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
 int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
                       const float* d_table, int64_t n_buckets, int64_t dim, int minn, int maxn,
                       int normalize, float* d_out32, void* d_out16,
-                      unsigned long long* d_repaired, void* stream) {
+                      unsigned long long* d_repaired, float* d_row_err, float* d_tile_err,
+                      void* stream) {
   if (n < 0 || dim < 1 || n_buckets < 1 || minn < 1 || maxn < minn)
     return fail(SJB_E_INVALID, "bad subword arguments");
   const int kpad = (int)sjb_kpad(dim);
@@ -519,7 +535,8 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
   if (int rc = set_smem_attr((const void*)sjb::subword_embed_kernel, smem)) return rc;
   sjb::subword_embed_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
       d_bytes, d_offs, n, d_table, n_buckets, (int)dim, kpad, sub, minn, maxn, normalize, d_out32,
-      normalize ? reinterpret_cast<__nv_bfloat16*>(d_out16) : nullptr, d_repaired);
+      normalize ? reinterpret_cast<__nv_bfloat16*>(d_out16) : nullptr, d_repaired,
+      normalize && d_out16 ? d_row_err : nullptr, normalize && d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("subword_embed");
   return SJB_OK;
 }
@@ -589,6 +606,10 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.stages = pl.stages;
   jp.a_bufs = pl.a_bufs;
   jp.cutoff = args->theta - args->band;
+  const bool per_row = args->left_row_err != nullptr && args->right_tile_err != nullptr;
+  jp.row_err = per_row ? args->left_row_err : nullptr;
+  jp.tile_err = per_row ? args->right_tile_err : nullptr;
+  jp.slack = sjb_accum_slack(args->dim);
   jp.cand = cand;
   jp.seg_cap = pl.seg_cap;
   jp.cta_count = cta;
@@ -620,6 +641,9 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
     wp.n_items = pl.n_items;
     wp.stages = pl.stages;
     wp.cutoff = jp.cutoff;
+    wp.row_err = jp.row_err;
+    wp.tile_err = jp.tile_err;
+    wp.slack = jp.slack;
     wp.cand = cand;
     wp.seg_cap = pl.seg_cap;
     wp.cta_count = cta;
@@ -690,6 +714,9 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
     pp.n_items = pl.n_items;
     pp.stages = pl.stages;
     pp.cutoff = jp.cutoff;
+    pp.row_err = jp.row_err;
+    pp.tile_err = jp.tile_err;
+    pp.slack = jp.slack;
     pp.cand = cand;
     pp.seg_cap = pl.seg_cap;
     pp.cta_count = cta;

@@ -277,6 +277,22 @@ constexpr uint64_t kEmptySlot = ~0ull;         // candidate slot not yet written
 // per-lane 64-bit hit masks, one warp scan + one shared atomic reserving the
 // warp's candidate slots, and per-lane stores of (row, j0 + column) pairs.
 // Columns >= col_lim are padding and never emitted.
+// Filter cutoff of R row i against the 256-row S tile t256.  Without error
+// arrays: the uniform theta - band.  With them:
+// |approx - canonical| <= slack + (1+1e-6)(e_i + E_t) + e_i E_t, where e_i
+// bounds ||bf16(x_i) - x_i|| and E_t the same over the S tile (Cauchy-Schwarz
+// on the rounding errors; slack covers both fp32 accumulations and this fp32
+// evaluation), so the cutoff can be raised to theta minus that bound.
+__device__ __forceinline__ float row_cutoff(float cutoff, float theta, float slack,
+                                            const float* row_err, const float* tile_err,
+                                            int64_t i, int64_t n_a, int64_t t256) {
+  if (row_err == nullptr) return cutoff;
+  const float ex = i < n_a ? __ldg(row_err + i) : 0.0f;
+  const float ey = __ldg(tile_err + t256);
+  const float b = slack + 1.000001f * (ex + ey) + ex * ey;
+  return fmaxf(cutoff, theta - b);
+}
+
 __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
                                                  uint32_t gi, uint32_t j0, int64_t col_lim,
                                                  uint32_t* cta_cnt, uint32_t* cta_sat,

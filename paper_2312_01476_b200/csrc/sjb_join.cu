@@ -61,6 +61,9 @@ struct JoinParams {
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers
   float cutoff;
+  const float* row_err;   // per-row band (or nullptr: uniform cutoff)
+  const float* tile_err;
+  float slack;
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
@@ -277,7 +280,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t lane_base = (uint32_t)q * 32;
     uint32_t dbg_acc = 0;
-    const float cutoff = p.cutoff;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     uint32_t acc_it = 0;
@@ -315,6 +317,8 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
 
           const int64_t gi64 = rb * kBM + h * 128 + lane_base + lane;
           const bool row_ok = gi64 < p.n_a;
+          const float cutoff =
+              row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64, p.n_a, t);
           // group maxima over 8 columns, then the warp-tile maximum
           float g[8];
 #pragma unroll

@@ -69,6 +69,9 @@ struct alignas(64) Params {
   int64_t n_items;
   int stages;
   float cutoff;
+  const float* row_err;   // per-row band (or nullptr: uniform cutoff)
+  const float* tile_err;
+  float slack;
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
@@ -226,7 +229,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int64_t n_items = p.n_items;
   const int nb = p.n_ablk;
   const uint32_t kgroups = (uint32_t)p.kpad / 8;
-  const uint32_t a_elems = L.a_bytes / 2;
 
   if (warp == 0 && lane == 1) {
     // ------------------------------------------------- R-block producer
@@ -351,7 +353,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int cq = ew >> 2;
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)q * 32;
-    const float cutoff = p.cutoff;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     const uint32_t tcol = tmem_base + (lane_base << 16) + cq * 64;
@@ -392,6 +393,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (p.debug_mode == 2 || !drain) return;
       const int64_t gi64 = s.rb * (2 * kARows) + rank * kARows + s.h * 128 + lane_base + lane;
       const bool row_ok = gi64 < p.n_a;
+      const float cutoff = row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64,
+                                      p.n_a, (s.t * kUmmaN) / kTileRows);
       float g[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {

@@ -51,6 +51,9 @@ struct Params {
   int64_t n_items;
   int stages;
   float cutoff;
+  const float* row_err;   // per-row band (or nullptr: uniform cutoff)
+  const float* tile_err;
+  float slack;
   uint64_t* cand;
   uint64_t seg_cap;
   unsigned long long* cta_count;
@@ -200,7 +203,6 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     const int ew = warp - 2;
     const int cq0 = ew >> 2, q = warp & 3;
     const uint32_t lane_base = (uint32_t)q * 32;
-    const float cutoff = p.cutoff;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     uint32_t* toff = kFused ? nullptr : p.tile_off + (int64_t)blockIdx.x * p.tile_stride;
@@ -221,6 +223,8 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
 #pragma unroll 1
         for (int h = 0; h < 2; h++) {
           const int64_t gi64 = rb * kTileRows + h * 128 + lane_base + lane;
+          const float cutoff =
+              row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64, p.n_a, t);
 #pragma unroll 1
           for (int k = 0; k < kChunksPerWarp; k++) {
             const int cq = cq0 + k * (kEpiWarps / 4);

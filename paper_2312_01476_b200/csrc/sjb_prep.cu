@@ -16,7 +16,10 @@ constexpr int kPrepThreads = 128;
 // Sequential fp64 sum of squares (no contraction: the square is exact and
 // __dadd_rn pins the rounding), repair rule, fp64 divide -- the reference's
 // normalize_row (_kernelcore.c:79-97).  Operates on one smem row.
-__device__ __forceinline__ int normalize_row_smem(float* row, int dim) {
+// With `err` != nullptr the same final pass also measures the row's bf16
+// rounding error ||bf16(x) - x||_2 (exact squares, fp64 sum, rounded up): the
+// per-row term of the filter band (sjb_common.cuh row_cutoff).
+__device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* err) {
   double ss = 0.0;
   for (int d = 0; d < dim; d++) {
     double x = (double)row[d];
@@ -34,7 +37,18 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim) {
     norm = sqrt(ss);
     repaired = 1;
   }
-  for (int d = 0; d < dim; d++) row[d] = __double2float_rn(__ddiv_rn((double)row[d], norm));
+  if (err == nullptr) {
+    for (int d = 0; d < dim; d++) row[d] = __double2float_rn(__ddiv_rn((double)row[d], norm));
+  } else {
+    double es = 0.0;
+    for (int d = 0; d < dim; d++) {
+      const float x = __double2float_rn(__ddiv_rn((double)row[d], norm));
+      row[d] = x;
+      const double e = (double)__bfloat162float(__float2bfloat16_rn(x)) - (double)x;
+      es = __dadd_rn(es, __dmul_rn(e, e));
+    }
+    *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
+  }
   return repaired;
 }
 
@@ -42,13 +56,28 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim) {
 // sub-tile [r0, r0 + sub) of the 256-row tile starting at row0 (`rows` valid
 // rows in the whole tile), store fp32 rows and that slice of the bf16
 // operand tile.
+// Rounding-error outputs of a tile: row_err[i] per row, tile_err[tile] = the
+// tile's maximum (accumulated in the shared `tile_max`, written by the caller).
+struct ErrOut {
+  float* row_err;
+  unsigned* tile_max;  // smem
+};
+
 __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, int dim, int kpad,
                                int64_t row0, bool normalize, float* __restrict__ out32,
                                __nv_bfloat16* __restrict__ out16,
-                               unsigned long long* __restrict__ repaired) {
+                               unsigned long long* __restrict__ repaired, ErrOut eo) {
   const int vrows = max(0, min(sub, rows - r0));  // valid rows in this sub-tile
   int rep = 0;
-  if (normalize && threadIdx.x < vrows) rep = normalize_row_smem(sm + threadIdx.x * pitch, dim);
+  if (normalize && threadIdx.x < vrows) {
+    float e = 0.0f;
+    const bool want = eo.row_err != nullptr;
+    rep = normalize_row_smem(sm + threadIdx.x * pitch, dim, want ? &e : nullptr);
+    if (want) {
+      eo.row_err[row0 + r0 + threadIdx.x] = e;
+      atomicMax(eo.tile_max, __float_as_uint(e));  // e >= 0: bit order = value order
+    }
+  }
   if (normalize && repaired != nullptr) {
     rep = __reduce_add_sync(0xffffffffu, rep);
     if ((threadIdx.x & 31) == 0 && rep) atomicAdd(repaired, (unsigned long long)rep);
@@ -89,8 +118,10 @@ __global__ void __launch_bounds__(kPrepThreads)
 normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ gather, int64_t n,
                       int dim, int kpad, int sub, float* __restrict__ out32,
                       __nv_bfloat16* __restrict__ out16, unsigned long long* __restrict__ repaired,
-                      int normalize) {
+                      int normalize, float* __restrict__ row_err, float* __restrict__ tile_err) {
   extern __shared__ float sm[];
+  __shared__ unsigned tile_max;
+  if (threadIdx.x == 0) tile_max = 0u;
   const int pitch = dim | 1;
   const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
   const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
@@ -111,8 +142,9 @@ normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ 
     }
     __syncthreads();
     finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, normalize != 0, out32, out16,
-                   repaired);
+                   repaired, ErrOut{row_err, &tile_max});
   }
+  if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
 // Synthetic model (_kernelcore.c:69-74, 99-107): stream seed per row, element
@@ -129,8 +161,11 @@ __device__ __forceinline__ float splitmix_elem(uint64_t seed, int d) {
 
 __global__ void __launch_bounds__(kPrepThreads)
 synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, int kpad, int sub,
-                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16) {
+                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
+                      float* __restrict__ row_err, float* __restrict__ tile_err) {
   extern __shared__ float sm[];
+  __shared__ unsigned tile_max;
+  if (threadIdx.x == 0) tile_max = 0u;
   const int pitch = dim | 1;
   const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
   const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
@@ -142,8 +177,10 @@ synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, in
     }
     __syncthreads();
     // synthetic vectors are normalised as part of the model (embedding.py:79)
-    finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, true, out32, out16, nullptr);
+    finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, true, out32, out16, nullptr,
+                   ErrOut{row_err, &tile_max});
   }
+  if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
 // FNV-1a-64 (_kernelcore.c:60-67) of packed tokens, XOR a 64-bit seed
@@ -177,8 +214,11 @@ subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restric
                      int64_t n, const float* __restrict__ table, int64_t n_buckets, int dim,
                      int kpad, int sub, int minn, int maxn, int normalize,
                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
-                     unsigned long long* __restrict__ repaired) {
+                     unsigned long long* __restrict__ repaired, float* __restrict__ row_err,
+                     float* __restrict__ tile_err) {
   extern __shared__ float sm[];
+  __shared__ unsigned tile_max;
+  if (threadIdx.x == 0) tile_max = 0u;
   const int pitch = dim | 1;
   const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
   const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
@@ -230,8 +270,9 @@ subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restric
     }
     __syncthreads();
     finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, normalize != 0, out32, out16,
-                   repaired);
+                   repaired, ErrOut{row_err, &tile_max});
   }
+  if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
 // Row L2 norms in fp64, returned as fp32 (sj_row_norms, _kernelcore.c:116-124).

@@ -79,6 +79,9 @@ class PreparedRelation:
     dim: int
     name: str = ""
     repaired_dev: Optional[torch.Tensor] = None  # (1,) int64 repaired-row counter
+    # bf16 rounding errors (sjb_join_args.left_row_err / right_tile_err):
+    row_err: Optional[torch.Tensor] = None       # (n,) >= ||bf16(x_i) - x_i||
+    tile_err: Optional[torch.Tensor] = None      # (tiles,) max over each 256-row tile
 
     @property
     def device(self) -> torch.device:
@@ -86,6 +89,15 @@ class PreparedRelation:
 
     def repaired(self) -> int:
         return int(self.repaired_dev.item()) if self.repaired_dev is not None else 0
+
+
+def tile_count(n: int) -> int:
+    return int(_lib.lib().sjb_tile_count(n))
+
+
+def _err_buffers(n: int, dev: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
+    return (torch.empty(max(n, 1), dtype=torch.float32, device=dev),
+            torch.empty(max(tile_count(n), 1), dtype=torch.float32, device=dev))
 
 
 def _check_matrix(x: torch.Tensor, what: str) -> None:
@@ -107,10 +119,11 @@ def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = N
     f32 = out32 if out32 is not None else torch.empty_like(raw)
     op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
-        _lib.check(L.sjb_normalize_rows(_vp(raw), n, dim, _vp(f32), _vp(op), _vp(rep),
-                                        _stream(dev)), "sjb_normalize_rows")
-    return PreparedRelation(f32, op, n, dim, name, rep)
+        _lib.check(L.sjb_normalize_rows(_vp(raw), n, dim, _vp(f32), _vp(op), _vp(rep), _vp(re),
+                                        _vp(te), _stream(dev)), "sjb_normalize_rows")
+    return PreparedRelation(f32, op, n, dim, name, rep, re, te)
 
 
 def normalize_rows_(m: torch.Tensor) -> torch.Tensor:
@@ -119,7 +132,7 @@ def normalize_rows_(m: torch.Tensor) -> torch.Tensor:
     rep = torch.zeros(1, dtype=torch.int64, device=m.device)
     with torch.cuda.device(m.device):
         _lib.check(_lib.lib().sjb_normalize_rows(_vp(m), m.shape[0], m.shape[1], _vp(m),
-                                                 ctypes.c_void_p(0), _vp(rep),
+                                                 ctypes.c_void_p(0), _vp(rep), None, None,
                                                  _stream(m.device)), "sjb_normalize_rows")
     return rep
 
@@ -188,12 +201,15 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                   band: Optional[float] = None, cand_cap: Optional[int] = None,
                   left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
                   max_bytes: Optional[int] = None,
-                  filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None
-                  ) -> DeviceMatches:
+                  filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None,
+                  per_row_band: bool = True) -> DeviceMatches:
     """Canonical threshold join of two prepared relations (device-resident).
 
     Blocks once at the end to read the match count (the output size is data
     dependent); everything else is asynchronous on the current stream.
+    per_row_band: when both relations carry their bf16 rounding errors, filter
+    with the per-row band (never looser than `band`; same result, fewer
+    candidates to recheck).
     """
     if L.dim != R.dim:
         raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
@@ -203,7 +219,8 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     dev = L.device
     theta32 = float(np.float32(theta))
     band = default_band(L.dim) if band is None else float(band)
-    key = (L.n, R.n, L.dim, theta32, float(np.float32(band)), grid, tiles_per_chunk)
+    use_err = per_row_band and L.row_err is not None and R.tile_err is not None
+    key = (L.n, R.n, L.dim, theta32, float(np.float32(band)), grid, tiles_per_chunk, use_err)
     if cand_cap is None:
         with _cap_lock:
             cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
@@ -219,7 +236,9 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                                  cand_cap=int(cand_cap), out_cap=int(cand_cap),
                                  left_base=int(left_base), grid=int(grid),
                                  tiles_per_chunk=int(tiles_per_chunk),
-                                 ev_filter_begin=ev0, ev_filter_end=ev1)
+                                 ev_filter_begin=ev0, ev_filter_end=ev1,
+                                 left_row_err=L.row_err.data_ptr() if use_err else None,
+                                 right_tile_err=R.tile_err.data_ptr() if use_err else None)
             ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
             if ws_bytes < 0:
                 _lib.check(-3, "sjb_join_workspace_bytes")
@@ -268,11 +287,13 @@ def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> 
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
     op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
         _lib.check(L.sjb_gather_normalize_rows(_vp(table), _vp(index.contiguous()), n, dim,
-                                               _vp(f32), _vp(op), _vp(rep), _stream(dev)),
+                                               _vp(f32), _vp(op), _vp(rep), _vp(re), _vp(te),
+                                               _stream(dev)),
                    "sjb_gather_normalize_rows")
-    return PreparedRelation(f32, op, n, dim, name, rep)
+    return PreparedRelation(f32, op, n, dim, name, rep, re, te)
 
 
 def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
@@ -307,7 +328,7 @@ def synthetic_rows(seeds: torch.Tensor, dim: int) -> torch.Tensor:
         with torch.cuda.device(dev):
             _lib.check(_lib.lib().sjb_synthetic_fill_many(_vp(seeds), seeds.numel(), dim,
                                                           _vp(out), ctypes.c_void_p(0),
-                                                          _stream(dev)),
+                                                          None, None, _stream(dev)),
                        "sjb_synthetic_fill_many")
     return out
 
@@ -323,11 +344,13 @@ def subword_rows(tokens, table: torch.Tensor, minn: int, maxn: int,
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
     op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev) if prepared else None
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(n, dev) if prepared else (None, None)
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().sjb_subword_embed(_vp(b), _vp(o), n, _vp(table), table.shape[0],
                                                 dim, minn, maxn, 1 if prepared else 0,
-                                                _vp(f32), _vp(op), _vp(rep), _stream(dev)),
+                                                _vp(f32), _vp(op), _vp(rep), _vp(re), _vp(te),
+                                                _stream(dev)),
                    "sjb_subword_embed")
     if prepared:
-        return PreparedRelation(f32, op, n, dim, name, rep)
+        return PreparedRelation(f32, op, n, dim, name, rep, re, te)
     return f32

@@ -174,6 +174,50 @@ def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
 
 
+@pytest.mark.parametrize("dim", [3, 100, 768])
+def test_rounding_error_outputs(cuda, dim):
+    """row_err bounds ||bf16(x) - x|| from above (tightly); tile_err is the
+    per-256-row-tile maximum (zero for padding tiles)."""
+    from paper_2312_01476_b200 import device as D
+    rng = np.random.default_rng(dim + 5)
+    n = 700
+    x = rng.standard_normal((n, dim), dtype=np.float32)
+    x[9] = 0.0
+    p = D.prepare(torch.from_numpy(x).to(cuda))
+    f = p.f32.cpu().numpy()
+    bf = torch.from_numpy(f).to(torch.bfloat16).to(torch.float64).numpy()
+    want = np.sqrt(((bf - f.astype(np.float64)) ** 2).sum(axis=1))
+    got = p.row_err.cpu().numpy().astype(np.float64)[:n]
+    assert (got >= want).all() and (got <= want * (1 + 1e-6) + 1e-30).all()
+    tiles = p.tile_err.cpu().numpy()
+    assert len(tiles) == D.tile_count(n)
+    for t in range(len(tiles)):
+        seg = got[t * 256:(t + 1) * 256]
+        assert tiles[t] == (np.float32(seg.max()) if len(seg) else 0.0)
+
+
+def test_per_row_band_is_exact_and_tighter(cuda, manifest, golden):
+    """Same MatchSet with the per-row band as with the uniform one, fewer
+    candidates: cfg1 (golden) and cfg4-shaped wide data (oracle)."""
+    from paper_2312_01476_b200 import datagen, device as D
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    wide = datagen.clustered_pair(500, 900, 768, 40, 0.6, 3, zipf=1.1)
+    wl, wr, ws = O.join_raw(wide[0], wide[1], 0.75, threads=8)
+    cases = [(L, S, meta["theta"], golden["cfg1_l"], golden["cfg1_r"], golden["cfg1_s"]),
+             (wide[0], wide[1], 0.75, wl, wr, ws)]
+    for L, S, theta, el, er, es in cases:
+        pl = D.prepare(torch.from_numpy(L).to(cuda))
+        pr = D.prepare(torch.from_numpy(S).to(cuda))
+        a = D.join_prepared(pl, pr, theta, per_row_band=True)
+        b = D.join_prepared(pl, pr, theta, per_row_band=False)
+        for m in (a, b):
+            lo, ro, so = m.to_host()
+            assert np.array_equal(lo, el) and np.array_equal(ro, er)
+            assert np.array_equal(so.view(np.uint32), es.view(np.uint32))
+        assert a.n_candidates < b.n_candidates, (L.shape, a.n_candidates, b.n_candidates)
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -158,6 +158,26 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
 
 /* Synchronous form: as above, then waits on `stream` and copies the info to
  * the host struct *info. */
+/* The same join in steps, so the filter can start on the first S tiles while
+ * later ones are still being copied or broadcast (one stream; args and
+ * workspace identical across the steps of one join):
+ *   sjb_join_begin        zero the counters (and empty the candidate slots)
+ *   sjb_join_filter_tiles filter + canonical recheck of S tiles
+ *                         [tile_begin, tile_end) (256-row tiles; ranges of
+ *                         one join must be disjoint and together cover S;
+ *                         only those S rows must be prepared when it runs)
+ *   sjb_join_finish       bucket, sort and emit the MatchSet; writes d_info
+ * sjb_join_prepared_async = begin + filter_tiles(all) + finish. */
+int sjb_join_begin(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
+                   void* stream);
+int sjb_join_filter_tiles(const float* d_l32, const void* d_l16, const float* d_r32,
+                          const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                          int64_t workspace_bytes, int64_t tile_begin, int64_t tile_end,
+                          void* stream);
+int sjb_join_finish(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
+                    uint64_t* d_lefts, uint64_t* d_rights, float* d_sims, void* d_info,
+                    void* stream);
+
 int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,
                       const void* d_r16, const sjb_join_args* args, void* d_workspace,
                       int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,

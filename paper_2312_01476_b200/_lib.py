@@ -15,7 +15,7 @@ EXPORTS = (
     "sjb_version", "sjb_last_error", "sjb_launch_count", "sjb_sm_count", "sjb_kpad", "sjb_operand_elems",
     "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
     "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band", "sjb_accum_slack",
-    "sjb_tile_count",
+    "sjb_tile_count", "sjb_join_begin", "sjb_join_filter_tiles", "sjb_join_finish",
     "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm",
     "sjb_scan_hits", "sjb_scan_hits_workspace_bytes",
 )
@@ -88,6 +88,10 @@ def lib(path: str = LIB_PATH):
     L.sjb_join_workspace_bytes.argtypes = [ctypes.POINTER(JoinArgs)]
     L.sjb_join_prepared_async.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,
                                           _vp, _vp, _vp, _vp, _vp]
+    L.sjb_join_begin.argtypes = [ctypes.POINTER(JoinArgs), _vp, _i64, _vp]
+    L.sjb_join_filter_tiles.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,
+                                        _i64, _i64, _vp]
+    L.sjb_join_finish.argtypes = [ctypes.POINTER(JoinArgs), _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.sjb_join_prepared.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,
                                     _vp, _vp, _vp, ctypes.POINTER(JoinInfo), _vp]
     L.sjb_tile_dot.argtypes = [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]

@@ -123,7 +123,7 @@ int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   if ((int64_t)grid > pl->n_items) grid = (int)(pl->n_items > 0 ? pl->n_items : 1);
   pl->grid = grid;
   pl->seg_cap = (uint64_t)(a->cand_cap / grid);
-  pl->tile_stride = pl->wide_fused ? 0 : W::tile_stride(pl->n_items, grid, tpc);
+  pl->tile_stride = pl->wide_fused ? 0 : W::tile_stride(pl->n_ablk, pl->n_btiles, grid, tpc);
   return SJB_OK;
 }
 
@@ -554,45 +554,104 @@ int64_t sjb_join_workspace_bytes(const sjb_join_args* args) {
   return (int64_t)join_ws_layout(args, grid, tstride).total;
 }
 
-int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
-                            const void* d_r16, const sjb_join_args* args, void* d_workspace,
-                            int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
-                            float* d_sims, void* d_info, void* stream) {
-  if (!args || !d_info) return fail(SJB_E_INVALID, "null args/info");
+}  // extern "C"
+
+namespace {
+
+// One join's plan and workspace views (shared by the begin / filter-range /
+// finish steps, which must all see the same args and workspace).
+struct JoinCtx {
+  JoinPlan pl;
+  uint64_t* cand;
+  uint32_t* sims_bits;
+  unsigned long long* cta;
+  uint32_t* rowcount;
+  uint64_t *rowoff, *cursor, *keys, *bsums;
+  uint32_t* bigrows;
+  unsigned int* nbig;
+  uint32_t* tile_off;
+  bool empty;  // n_left == 0 or n_right == 0
+};
+
+int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes, JoinCtx* c) {
+  if (!args) return fail(SJB_E_INVALID, "null args");
   const int64_t nl = args->n_left, nr = args->n_right;
   if (nl < 0 || nr < 0 || args->dim < 1) return fail(SJB_E_INVALID, "bad shape");
   if (nl >= (int64_t(1) << 32) || nr >= (int64_t(1) << 32))
     return fail(SJB_E_UNSUPPORTED, "relations are limited to 2^32 rows per join");
-  cudaStream_t st = as_stream(stream);
-  int64_t* info = reinterpret_cast<int64_t*>(d_info);
-  if (nl == 0 || nr == 0) {
-    SJB_CK(cudaMemsetAsync(info, 0, 5 * 8, st));
-    return SJB_OK;
-  }
-  JoinPlan pl;
-  if (int rc = make_plan(args, &pl)) return rc;
+  c->empty = nl == 0 || nr == 0;
+  if (c->empty) return SJB_OK;
+  if (int rc = make_plan(args, &c->pl)) return rc;
+  const JoinPlan& pl = c->pl;
   const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride);
   if ((int64_t)w.total > workspace_bytes)
     return fail(SJB_E_INVALID, "workspace %lld B < required %lld B", (long long)workspace_bytes,
                 (long long)w.total);
-  if (pl.seg_cap < 1) return fail(SJB_E_INVALID, "cand_cap %lld < grid %d", (long long)args->cand_cap, pl.grid);
+  if (pl.seg_cap < 1)
+    return fail(SJB_E_INVALID, "cand_cap %lld < grid %d", (long long)args->cand_cap, pl.grid);
   uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
-  uint64_t* cand = reinterpret_cast<uint64_t*>(ws + w.cand);
-  uint32_t* sims_bits = reinterpret_cast<uint32_t*>(ws + w.sims);
-  unsigned long long* cta = reinterpret_cast<unsigned long long*>(ws + w.cta);
-  uint32_t* rowcount = reinterpret_cast<uint32_t*>(ws + w.rowcount);
-  uint64_t* rowoff = reinterpret_cast<uint64_t*>(ws + w.rowoff);
-  uint64_t* cursor = reinterpret_cast<uint64_t*>(ws + w.cursor);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(ws + w.keys);
-  uint64_t* bsums = reinterpret_cast<uint64_t*>(ws + w.bsums);
-  uint32_t* bigrows = reinterpret_cast<uint32_t*>(ws + w.bigrows);
-  unsigned int* nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
-  uint32_t* tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
+  c->cand = reinterpret_cast<uint64_t*>(ws + w.cand);
+  c->sims_bits = reinterpret_cast<uint32_t*>(ws + w.sims);
+  c->cta = reinterpret_cast<unsigned long long*>(ws + w.cta);
+  c->rowcount = reinterpret_cast<uint32_t*>(ws + w.rowcount);
+  c->rowoff = reinterpret_cast<uint64_t*>(ws + w.rowoff);
+  c->cursor = reinterpret_cast<uint64_t*>(ws + w.cursor);
+  c->keys = reinterpret_cast<uint64_t*>(ws + w.keys);
+  c->bsums = reinterpret_cast<uint64_t*>(ws + w.bsums);
+  c->bigrows = reinterpret_cast<uint32_t*>(ws + w.bigrows);
+  c->nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
+  c->tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
+  return SJB_OK;
+}
 
-  SJB_CK(cudaMemsetAsync(rowcount, 0, (size_t)nl * 4, st));
-  SJB_CK(cudaMemsetAsync(nbig, 0, 16, st));
+bool fused_recheck(const JoinPlan& pl) { return !pl.wide || pl.wide_fused; }
 
-  // 1) tensor-core filter
+int join_begin(const sjb_join_args* args, const JoinCtx& c, cudaStream_t st) {
+  const JoinPlan& pl = c.pl;
+  SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)args->n_left * 4, st));
+  SJB_CK(cudaMemsetAsync(c.nbig, 0, 16, st));
+  SJB_CK(cudaMemsetAsync(c.cta, 0, (size_t)pl.grid * 8, st));
+  // candidate slots start empty: the fused recheck waits for each slot's write
+  if (fused_recheck(pl))
+    SJB_CK(cudaMemsetAsync(c.cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
+  return SJB_OK;
+}
+
+// Work items over S tiles [tb, te) (kernel tile units): the plan's chunking,
+// narrowed when the range is short so every CTA still gets ~8 items.
+void range_items(const JoinPlan& pl, int64_t tb, int64_t te, int* tpc, int64_t* items) {
+  const int64_t range = te - tb;
+  int64_t t = (int64_t)pl.n_ablk * range / (8LL * pl.grid);
+  t = t < 1 ? 1 : (t > pl.tiles_per_chunk ? pl.tiles_per_chunk : t);
+  *tpc = (int)t;
+  *items = range <= 0 ? 0 : (int64_t)pl.n_ablk * sjb::ceil_div(range, t);
+}
+
+// Filter (+ recheck) S tiles [tile_begin, tile_end) of 256 rows, appending to
+// the per-CTA candidate segments.
+int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const void* d_r16,
+                const sjb_join_args* args, const JoinCtx& c, int64_t tile_begin,
+                int64_t tile_end, cudaStream_t st) {
+  const JoinPlan& pl = c.pl;
+  const int64_t nl = args->n_left, nr = args->n_right;
+  const int64_t nt256 = sjb::ceil_div(nr, sjb::kTileRows);
+  if (tile_begin < 0) tile_begin = 0;
+  if (tile_end > nt256) tile_end = nt256;
+  if (tile_end <= tile_begin) return SJB_OK;
+  // kernel tile units: 256 rows, or 128 for the CTA-pair kernel
+  const int64_t unit = pl.pair ? 2 : 1;
+  const int64_t tb = tile_begin * unit;
+  const int64_t te = tile_end * unit > pl.n_btiles ? pl.n_btiles : tile_end * unit;
+  int tpc = 0;
+  int64_t items = 0;
+  range_items(pl, tb, te, &tpc, &items);
+  if (pl.pair) {
+    // pair items cover pairs of CTAs; the plan's grid is 2 CTAs per item lane
+    int64_t t = (int64_t)pl.n_ablk * (te - tb) / (8LL * (pl.grid / 2));
+    tpc = (int)(t < 1 ? 1 : (t > pl.tiles_per_chunk ? pl.tiles_per_chunk : t));
+    items = (int64_t)pl.n_ablk * sjb::ceil_div(te - tb, (int64_t)tpc);
+  }
+
   sjb::JoinParams jp;
   jp.a16 = reinterpret_cast<const __nv_bfloat16*>(d_l16);
   jp.b16 = reinterpret_cast<const __nv_bfloat16*>(d_r16);
@@ -600,9 +659,11 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.n_b = nr;
   jp.kpad = pl.kpad;
   jp.n_ablk = pl.n_ablk;
-  jp.n_btiles = pl.n_btiles;
-  jp.tiles_per_chunk = pl.tiles_per_chunk;
-  jp.n_items = pl.n_items;
+  jp.n_btiles = (int)te;
+  jp.tiles_per_chunk = tpc;
+  jp.tile_begin = (int)tb;
+  jp.append = 1;
+  jp.n_items = items;
   jp.stages = pl.stages;
   jp.a_bufs = pl.a_bufs;
   jp.cutoff = args->theta - args->band;
@@ -610,18 +671,15 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   jp.row_err = per_row ? args->left_row_err : nullptr;
   jp.tile_err = per_row ? args->right_tile_err : nullptr;
   jp.slack = sjb_accum_slack(args->dim);
-  jp.cand = cand;
+  jp.cand = c.cand;
   jp.seg_cap = pl.seg_cap;
-  jp.cta_count = cta;
+  jp.cta_count = c.cta;
   jp.l32 = d_l32;
   jp.r32 = d_r32;
   jp.dim = (int)args->dim;
   jp.theta = args->theta;
-  jp.sims_bits = sims_bits;
-  jp.rowcount = rowcount;
-  // candidate slots start empty: the fused recheck waits for each slot's write
-  const bool fused_recheck = !pl.wide || pl.wide_fused;
-  if (fused_recheck) SJB_CK(cudaMemsetAsync(cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
+  jp.sims_bits = c.sims_bits;
+  jp.rowcount = c.rowcount;
   {
     const char* dm = getenv("SJB_DEBUG_MODE");
     jp.debug_mode = dm ? atoi(dm) : 0;
@@ -636,25 +694,27 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
     wp.n_b = nr;
     wp.kpad = pl.kpad;
     wp.n_ablk = pl.n_ablk;
-    wp.n_btiles = pl.n_btiles;
-    wp.tiles_per_chunk = pl.tiles_per_chunk;
-    wp.n_items = pl.n_items;
+    wp.n_btiles = jp.n_btiles;
+    wp.tiles_per_chunk = tpc;
+    wp.tile_begin = jp.tile_begin;
+    wp.append = 1;
+    wp.n_items = items;
     wp.stages = pl.stages;
     wp.cutoff = jp.cutoff;
     wp.row_err = jp.row_err;
     wp.tile_err = jp.tile_err;
     wp.slack = jp.slack;
-    wp.cand = cand;
+    wp.cand = c.cand;
     wp.seg_cap = pl.seg_cap;
-    wp.cta_count = cta;
+    wp.cta_count = c.cta;
     wp.l32 = d_l32;
     wp.r32 = d_r32;
     wp.dim = (int)args->dim;
     wp.theta = args->theta;
-    wp.sims_bits = sims_bits;
-    wp.rowcount = rowcount;
+    wp.sims_bits = c.sims_bits;
+    wp.rowcount = c.rowcount;
     wp.debug = jp.debug_mode;
-    wp.tile_off = tile_off;
+    wp.tile_off = c.tile_off;
     wp.tile_stride = pl.tile_stride;
     if (pl.wide_fused) {
       if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<true>, (int)pl.smem)) return rc;
@@ -668,23 +728,24 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
       SJB_CK_LAUNCH("wide_filter");
       if (jp.debug_mode != 1) {
         sjb::wide::RecheckParams rp;
-        rp.cand = cand;
+        rp.cand = c.cand;
         rp.seg_cap = pl.seg_cap;
-        rp.cta_count = cta;
-        rp.tile_off = tile_off;
+        rp.cta_count = c.cta;
+        rp.tile_off = c.tile_off;
         rp.tile_stride = pl.tile_stride;
-        rp.n_items = pl.n_items;
+        rp.n_items = items;
         rp.n_ablk = pl.n_ablk;
-        rp.n_btiles = pl.n_btiles;
-        rp.tiles_per_chunk = pl.tiles_per_chunk;
+        rp.n_btiles = jp.n_btiles;
+        rp.tiles_per_chunk = tpc;
+        rp.tile_begin = jp.tile_begin;
         rp.n_a = nl;
         rp.n_b = nr;
         rp.l32 = d_l32;
         rp.r32 = d_r32;
         rp.dim = (int)args->dim;
         rp.theta = args->theta;
-        rp.sims_bits = sims_bits;
-        rp.rowcount = rowcount;
+        rp.sims_bits = c.sims_bits;
+        rp.rowcount = c.rowcount;
         if ((args->dim & 3) == 0) {
           sjb::wide::RecheckTmaParams tp;
           tp.b = rp;
@@ -709,23 +770,25 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
     pp.n_b = nr;
     pp.kpad = pl.kpad;
     pp.n_ablk = pl.n_ablk;
-    pp.n_btiles = pl.n_btiles;
-    pp.tiles_per_chunk = pl.tiles_per_chunk;
-    pp.n_items = pl.n_items;
+    pp.n_btiles = jp.n_btiles;
+    pp.tiles_per_chunk = tpc;
+    pp.tile_begin = jp.tile_begin;
+    pp.append = 1;
+    pp.n_items = items;
     pp.stages = pl.stages;
     pp.cutoff = jp.cutoff;
     pp.row_err = jp.row_err;
     pp.tile_err = jp.tile_err;
     pp.slack = jp.slack;
-    pp.cand = cand;
+    pp.cand = c.cand;
     pp.seg_cap = pl.seg_cap;
-    pp.cta_count = cta;
+    pp.cta_count = c.cta;
     pp.l32 = d_l32;
     pp.r32 = d_r32;
     pp.dim = (int)args->dim;
     pp.theta = args->theta;
-    pp.sims_bits = sims_bits;
-    pp.rowcount = rowcount;
+    pp.sims_bits = c.sims_bits;
+    pp.rowcount = c.rowcount;
     pp.debug_mode = jp.debug_mode;
     if (int rc = encode_operand_map(&pp.tmap_a, d_l16, nl, pl.kpad, sjb::pair::kARows)) return rc;
     if (int rc = encode_operand_map(&pp.tmap_b, d_r16, nr, pl.kpad, sjb::pair::kHalfN)) return rc;
@@ -735,32 +798,92 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   }
   if (args->ev_filter_end)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_end), st));
+  return SJB_OK;
+}
 
-  // 2) (the canonical recheck ran inside the filter kernel) row offsets
+// Row offsets, then bucket by left row and sort each row by right offset.
+int join_finish(const sjb_join_args* args, const JoinCtx& c, uint64_t* d_lefts,
+                uint64_t* d_rights, float* d_sims, int64_t* info, cudaStream_t st) {
+  const JoinPlan& pl = c.pl;
+  const int64_t nl = args->n_left;
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
-  if (int rc = run_scan(rowcount, nl, rowoff, cursor, bsums, st)) return rc;
-  sjb::gate_kernel<<<1, 1, 0, st>>>(rowoff, nl, args->out_cap, nbig);
+  if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+  sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
   SJB_CK_LAUNCH("gate");
-
-  // 4) bucket by left row, 5) sort each row by right offset
   sjb::scatter_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
-      cand, pl.seg_cap, cta, pl.grid, sims_bits, reinterpret_cast<unsigned long long*>(cursor),
-      keys, nbig);
+      c.cand, pl.seg_cap, c.cta, pl.grid, c.sims_bits,
+      reinterpret_cast<unsigned long long*>(c.cursor), c.keys, c.nbig);
   SJB_CK_LAUNCH("scatter");
   sjb::segsort_small_kernel<<<grid_for((uint64_t)nl * 32, sjb::kSortSmallThreads, 16),
                               sjb::kSortSmallThreads, 0, st>>>(
-      rowoff, nl, keys, d_lefts, d_rights, d_sims, bigrows, nbig, args->left_base);
+      c.rowoff, nl, c.keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
   SJB_CK_LAUNCH("segsort_small");
   const int big_smem = sjb::kSortBigCap * 8;
   if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
   sjb::segsort_big_kernel<<<sjb_sm_count(current_device()), sjb::kSortBigThreads, big_smem, st>>>(
-      rowoff, keys, d_lefts, d_rights, d_sims, bigrows, nbig, args->left_base);
+      c.rowoff, c.keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
   SJB_CK_LAUNCH("segsort_big");
-
-  sjb::join_finalize_kernel<<<1, 256, 0, st>>>(cta, pl.grid, pl.seg_cap, rowoff, nl, args->out_cap,
-                                               info);
+  sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.rowoff, nl,
+                                               args->out_cap, info);
   SJB_CK_LAUNCH("finalize");
   return SJB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sjb_join_begin(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
+                   void* stream) {
+  JoinCtx c;
+  if (int rc = join_ctx(args, d_workspace, workspace_bytes, &c)) return rc;
+  if (c.empty) return SJB_OK;
+  return join_begin(args, c, as_stream(stream));
+}
+
+int sjb_join_filter_tiles(const float* d_l32, const void* d_l16, const float* d_r32,
+                          const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                          int64_t workspace_bytes, int64_t tile_begin, int64_t tile_end,
+                          void* stream) {
+  JoinCtx c;
+  if (int rc = join_ctx(args, d_workspace, workspace_bytes, &c)) return rc;
+  if (c.empty) return SJB_OK;
+  return join_filter(d_l32, d_l16, d_r32, d_r16, args, c, tile_begin, tile_end, as_stream(stream));
+}
+
+int sjb_join_finish(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
+                    uint64_t* d_lefts, uint64_t* d_rights, float* d_sims, void* d_info,
+                    void* stream) {
+  if (!d_info) return fail(SJB_E_INVALID, "null info");
+  JoinCtx c;
+  if (int rc = join_ctx(args, d_workspace, workspace_bytes, &c)) return rc;
+  cudaStream_t st = as_stream(stream);
+  int64_t* info = reinterpret_cast<int64_t*>(d_info);
+  if (c.empty) {
+    SJB_CK(cudaMemsetAsync(info, 0, 5 * 8, st));
+    return SJB_OK;
+  }
+  return join_finish(args, c, d_lefts, d_rights, d_sims, info, st);
+}
+
+int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
+                            const void* d_r16, const sjb_join_args* args, void* d_workspace,
+                            int64_t workspace_bytes, uint64_t* d_lefts, uint64_t* d_rights,
+                            float* d_sims, void* d_info, void* stream) {
+  if (!args || !d_info) return fail(SJB_E_INVALID, "null args/info");
+  JoinCtx c;
+  if (int rc = join_ctx(args, d_workspace, workspace_bytes, &c)) return rc;
+  cudaStream_t st = as_stream(stream);
+  int64_t* info = reinterpret_cast<int64_t*>(d_info);
+  if (c.empty) {
+    SJB_CK(cudaMemsetAsync(info, 0, 5 * 8, st));
+    return SJB_OK;
+  }
+  if (int rc = join_begin(args, c, st)) return rc;
+  if (int rc = join_filter(d_l32, d_l16, d_r32, d_r16, args, c, 0,
+                           sjb::ceil_div(args->n_right, sjb::kTileRows), st))
+    return rc;
+  return join_finish(args, c, d_lefts, d_rights, d_sims, info, st);
 }
 
 int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,

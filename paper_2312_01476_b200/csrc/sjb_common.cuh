@@ -370,14 +370,23 @@ __device__ __forceinline__ uint64_t wait_slot(const uint64_t* slot) {
 // processed once fully reserved (or once all `n_epi` epilogue warps are done);
 // each lane re-decides two slots with interleaved canonical chains, writes
 // the canonical sim bits (or kRejected) and counts kept matches per left row.
+// Segment count a filter launch starts from: 0, or (append) where the
+// previous launch over other S tiles of the same join stopped.
+__device__ __forceinline__ void init_segment_count(const unsigned long long* cta_count, bool append,
+                                                   uint32_t* cnt, uint32_t* sat) {
+  const unsigned long long c0 = append ? cta_count[blockIdx.x] : 0ull;
+  *cnt = c0 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c0;
+  *sat = c0 > 0xFFFFFFFFull ? 1u : 0u;
+}
+
 __device__ __forceinline__ void recheck_loop(const uint64_t* seg, uint32_t* sims, uint64_t seg_cap,
                                              volatile uint32_t* vcnt, volatile uint32_t* vdone,
                                              uint32_t n_epi, int rw, int nrw, const float* l32,
                                              const float* r32, int dim, float theta,
-                                             uint32_t* rowcount) {
+                                             uint32_t* rowcount, uint64_t start) {
   const int lane = threadIdx.x & 31;
   for (uint64_t blk = rw;; blk += nrw) {
-    const uint64_t s0 = blk * 64;
+    const uint64_t s0 = start + blk * 64;
     uint64_t n;
     for (;;) {
       n = mn<uint64_t>(*vcnt, seg_cap);

@@ -57,6 +57,8 @@ struct JoinParams {
   int n_ablk;                // ceil(n_a / 256)
   int n_btiles;              // ceil(n_b / 256)
   int tiles_per_chunk;
+  int tile_begin;            // first S tile of this launch (S-range launches)
+  int append;                // 1: continue the segments of an earlier launch
   int64_t n_items;
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers
@@ -130,8 +132,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    *cta_cnt = 0u;
-    *cta_sat = 0u;
+    init_segment_count(p.cta_count, p.append != 0, cta_cnt, cta_sat);
     *epi_done = 0u;
     fence_mbar_init();
   }
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       int64_t it = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, it++) {
         const int64_t sc = item / nb;
-        const int64_t t0 = sc * p.tiles_per_chunk;
+        const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
           mbar_wait(&b_empty[bstage], bphase ^ 1u);
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         if (dbg) w_a += clock64() - c0;
         tc_fence_after();
         const uint64_t ad = a_desc_base + (uint64_t)ab * tile_step;
-        const int64_t t0 = sc * p.tiles_per_chunk;
+        const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
           if (dbg) c0 = clock64();
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     volatile uint32_t* vcnt = cta_cnt;
     volatile uint32_t* vdone = epi_done;
     recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps, p.l32,
-                 p.r32, p.dim, p.theta, p.rowcount);
+                 p.r32, p.dim, p.theta, p.rowcount, p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
   } else {
     // ---------------------------------------------------------- epilogue
     // 16 warps; warp (q, c) drains TMEM lanes 32q..32q+31 (R rows of the
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     const long long e_start = clock64();
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
-      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++) {
 #pragma unroll 1

@@ -66,6 +66,8 @@ struct alignas(64) Params {
   int n_ablk;        // ceil(n_a / 512): pair R blocks
   int n_btiles;      // ceil(n_b / 128): pair S tiles
   int tiles_per_chunk;
+  int tile_begin;    // first pair S tile of this launch
+  int append;        // 1: continue the segments of an earlier launch
   int64_t n_items;
   int stages;
   float cutoff;
@@ -215,8 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&b_empty[s], 1);
       mbar_init(&b_local[s], 1);
     }
-    *cta_cnt = 0u;
-    *cta_sat = 0u;
+    init_segment_count(p.cta_count, p.append != 0, cta_cnt, cta_sat);
     *epi_done = 0u;
     fence_mbar_init();
   }
@@ -250,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t bphase = 0;
     for (int64_t item = pair_id; item < n_items; item += n_pairs) {
       const int64_t sc = item / nb;
-      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++) {
         mbar_wait(&b_empty[bstage], bphase ^ 1u);
@@ -298,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (dbg) w_a += clock64() - c0;
         tc_fence_after();
         const uint64_t ad = a_base + (uint64_t)ab * a_buf_step;
-        const int64_t t0 = sc * p.tiles_per_chunk;
+        const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
           if (dbg) c0 = clock64();
@@ -342,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     volatile uint32_t* vcnt = cta_cnt;
     volatile uint32_t* vdone = epi_done;
     recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps, p.l32,
-                 p.r32, p.dim, p.theta, p.rowcount);
+                 p.r32, p.dim, p.theta, p.rowcount, p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
   } else if (warp >= 2) {
     // ---------------------------------------------------------- epilogue
     // warp (q, c): TMEM lanes 32q..32q+31 (this CTA's R rows of the stage's
@@ -371,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       s.h = 0;
       s.rb = item % nb;
       const int64_t sc = item / nb;
-      s.t = sc * p.tiles_per_chunk;
+      s.t = p.tile_begin + sc * p.tiles_per_chunk;
       s.t1 = mn<int64_t>(s.t + p.tiles_per_chunk, p.n_btiles);
       return s;
     };

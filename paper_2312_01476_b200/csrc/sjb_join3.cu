@@ -48,6 +48,8 @@ struct Params {
   int kpad;              // multiple of 64
   int n_ablk, n_btiles;  // 256-row blocks / tiles
   int tiles_per_chunk;
+  int tile_begin;        // first S tile of this launch
+  int append;            // 1: continue the segments of an earlier launch
   int64_t n_items;
   int stages;
   float cutoff;
@@ -72,9 +74,13 @@ __host__ __device__ inline uint32_t smem_bytes(int stages) {
   return (uint32_t)stages * 2 * kChunkBytes + (4 + 2 * stages) * 8 + 32;
 }
 
-// Max tiles one CTA walks (+1 for the end offset).
-__host__ __device__ inline int64_t tile_stride(int64_t n_items, int grid, int tiles_per_chunk) {
-  return ((n_items + grid - 1) / grid) * tiles_per_chunk + 1;
+// Max tiles one CTA walks in one launch (+1 for the end offset), for any
+// S-tile range of the join and chunking <= max_tpc: a launch over `range`
+// tiles with chunk tpc has n_ablk * ceil(range / tpc) items, so a CTA walks
+// <= ceil(items / grid) * tpc <= n_ablk * (range + tpc) / grid + tpc tiles.
+__host__ __device__ inline int64_t tile_stride(int64_t n_ablk, int64_t n_btiles, int grid,
+                                               int max_tpc) {
+  return (n_ablk * (n_btiles + max_tpc) + grid - 1) / grid + max_tpc + 1;
 }
 
 __device__ __forceinline__ void epi_bar() {
@@ -105,8 +111,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    *cta_cnt = 0u;
-    *cta_sat = 0u;
+    init_segment_count(p.cta_count, p.append != 0, cta_cnt, cta_sat);
     *epi_done = 0u;
     fence_mbar_init();
   }
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       uint32_t ph = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int64_t rb = item % nb, sc = item / nb;
-        const int64_t t0 = sc * p.tiles_per_chunk;
+        const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
           for (int c = 0; c < nchunks; c++) {
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     uint32_t ph = 0, tile_it = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t sc = item / nb;
-      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++, tile_it++) {
         for (int c = 0; c < nchunks; c++) {
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       recheck_loop(p.cand + (uint64_t)blockIdx.x * seg_cap,
                    p.sims_bits + (uint64_t)blockIdx.x * seg_cap, seg_cap, cta_cnt, epi_done,
                    (uint32_t)kEpiWarps, warp - 2 - kEpiWarps, kRecheckWarps, p.l32, p.r32, p.dim,
-                   p.theta, p.rowcount);
+                   p.theta, p.rowcount, p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
   } else {
     // ---------------------------------------------------------- epilogue
     // warp (q, c): TMEM lanes 32q..32q+31 x column chunks c, c + 2 (64 each)
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     uint32_t tile_it = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
-      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++, tile_it++) {
         mbar_wait(acc_full, tile_it & 1u);
@@ -287,7 +292,7 @@ struct RecheckParams {
   const uint32_t* tile_off;
   int64_t tile_stride;
   int64_t n_items;
-  int n_ablk, n_btiles, tiles_per_chunk;
+  int n_ablk, n_btiles, tiles_per_chunk, tile_begin;
   int64_t n_a, n_b;
   const float* l32;
   const float* r32;
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(kRcThreads, 1) recheck_generic_kernel(const Re
   int64_t k = 0;
   for (int64_t item = c; item < p.n_items; item += gridDim.x) {
     const int64_t rb = item % nb, sc = item / nb;
-    const int64_t t0 = sc * p.tiles_per_chunk;
+    const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
     const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
     for (int64_t t = t0; t < t1; t++, k++) {
       const uint32_t lo = toff[k], hi = toff[k + 1];
@@ -542,7 +547,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     int64_t k = 0;
     for (int64_t item = c; item < p.n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
-      const int64_t t0 = sc * p.tiles_per_chunk;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++, k++) {
         const uint32_t lo = toff[k], hi = toff[k + 1];
@@ -571,7 +576,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
   int64_t k = 0;
   for (int64_t item = c; item < p.n_items; item += gridDim.x) {
     const int64_t rb = item % nb, sc = item / nb;
-    const int64_t t0 = sc * p.tiles_per_chunk;
+    const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
     const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
     for (int64_t t = t0; t < t1; t++, k++) {
       const uint32_t lo = toff[k], hi = toff[k + 1];

@@ -276,6 +276,107 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                          n_cand, int(cand_cap), retries, used_grid)
 
 
+def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, cand_cap: int,
+               left_base: int, use_err: bool, right_tile_err: Optional[torch.Tensor]
+               ) -> "_lib.JoinArgs":
+    return _lib.JoinArgs(n_left=L.n, n_right=n_right, dim=L.dim, theta=theta32, band=band,
+                         cand_cap=int(cand_cap), out_cap=int(cand_cap), left_base=int(left_base),
+                         grid=0, tiles_per_chunk=0, ev_filter_begin=None, ev_filter_end=None,
+                         left_row_err=L.row_err.data_ptr() if use_err else None,
+                         right_tile_err=right_tile_err.data_ptr() if use_err else None)
+
+
+def _stream_chunks(n: int, chunks: int):
+    """Row ranges of ~n/chunks rows on 512-row boundaries (operand tile pairs)."""
+    step = max(512, -(-n // max(chunks, 1)) // 512 * 512 or 512)
+    return [(r0, min(n, r0 + step)) for r0 in range(0, n, step)]
+
+
+def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
+                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
+                  name: str = "") -> Tuple["DeviceMatches", PreparedRelation]:
+    """Join a prepared left relation with a HOST right relation, overlapping
+    the right side's host->device copy with the filter: the rows are copied in
+    chunks on a side stream; each chunk is normalised in place (canonical fp32
+    rows + its tiles of the bf16 image + rounding errors) and its S tiles are
+    filtered as soon as it lands (sjb_join_begin / sjb_join_filter_tiles /
+    sjb_join_finish).  Same result as prepare + join_prepared.  Returns the
+    matches and the prepared right relation (resident, reusable)."""
+    if right_host.is_cuda or right_host.dtype != torch.float32 or right_host.dim() != 2:
+        raise ValueError("right_host must be a 2-D float32 host tensor")
+    if right_host.shape[1] != L.dim:
+        raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {right_host.shape[1]}")
+    lib = _lib.lib()
+    dev = L.device
+    n, dim = right_host.shape
+    # pinned: asynchronous chunk copies; pageable: each chunk copy blocks the
+    # host while the GPU filters the previous chunk -- overlapped either way
+    src = right_host.contiguous()
+    theta32 = float(np.float32(theta))
+    band = default_band(dim) if band is None else float(band)
+    key = (L.n, n, dim, theta32, float(np.float32(band)), 0, 0, True)
+    with _cap_lock:
+        cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, n))
+    f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(n, dev)
+    R = PreparedRelation(f32, op, n, dim, name, rep, re, te)
+    if L.n == 0 or n == 0:
+        return join_prepared(L, R, theta, band, left_base=left_base), R
+    use_err = L.row_err is not None
+    kp = kpad(dim)
+    with torch.cuda.device(dev):
+        comp = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(dev)
+        args = _join_args(L, n, theta32, band, cand_cap, left_base, use_err, te)
+        ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
+        if ws_bytes < 0:
+            _lib.check(-3, "sjb_join_workspace_bytes")
+        ws = _workspace(ws_bytes, dev)
+        lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
+        rights = torch.empty_like(lefts)
+        sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
+        info_t = torch.zeros(5, dtype=torch.int64, device=dev)
+        cs = ctypes.c_void_p(comp.cuda_stream)
+        _lib.check(lib.sjb_join_begin(ctypes.byref(args), _vp(ws), ws_bytes, cs), "sjb_join_begin")
+        copy.wait_stream(comp)   # buffers allocated on the compute stream
+        for r0, r1 in _stream_chunks(n, chunks):
+            with torch.cuda.stream(copy):
+                f32[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            comp.wait_event(ev)
+            t0 = r0 // TILE_ROWS
+            _lib.check(lib.sjb_normalize_rows(
+                ctypes.c_void_p(f32[r0:].data_ptr()), r1 - r0, dim,
+                ctypes.c_void_p(f32[r0:].data_ptr()),
+                ctypes.c_void_p(op.data_ptr() + t0 * TILE_ROWS * kp * 2), _vp(rep),
+                ctypes.c_void_p(re.data_ptr() + r0 * 4), ctypes.c_void_p(te.data_ptr() + t0 * 4),
+                cs), "sjb_normalize_rows")
+            _lib.check(lib.sjb_join_filter_tiles(
+                _vp(L.f32), _vp(L.op), _vp(f32), _vp(op), ctypes.byref(args), _vp(ws), ws_bytes,
+                t0, -(-r1 // TILE_ROWS), cs), "sjb_join_filter_tiles")
+        src_keepalive = src  # the copies read `src` asynchronously
+        _lib.check(lib.sjb_join_finish(ctypes.byref(args), _vp(ws), ws_bytes, _vp(lefts),
+                                       _vp(rights), _vp(sims), _vp(info_t), cs),
+                   "sjb_join_finish")
+        info = info_t.cpu().numpy()
+        del src_keepalive
+    n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
+    flags = info[3:4].view(np.int32)
+    if int(flags[0]):
+        # candidate capacity overflowed: S is resident now; rerun with room
+        m = join_prepared(L, R, theta, band, cand_cap=max(needed, n_matches, cand_cap + 1),
+                          left_base=left_base)
+        m.retries += 1
+        return m, R
+    with _cap_lock:
+        _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
+    return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
+                         n_cand, int(cand_cap), 0, int(flags[1])), R
+
+
 def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> PreparedRelation:
     """Prepare relation rows table[index[i]] (lookup-model prefetch) in one pass."""
     _check_matrix(table, "table")

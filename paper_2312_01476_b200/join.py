@@ -171,6 +171,19 @@ def _as_device_matrix(x: ArrayLike, dev: torch.device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
 
 
+_STREAM_MIN_ROWS = 1 << 16   # smaller right relations: one copy, then join
+
+
+def _is_host(x: ArrayLike) -> bool:
+    return isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and not x.is_cuda)
+
+
+def _host_tensor(x: ArrayLike) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+
+
 def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                         band: Optional[float] = None, left_name: str = "left",
                         right_name: str = "right", device=None) -> Tuple[MatchSet, JoinStats]:
@@ -182,10 +195,15 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
     t0 = time.perf_counter_ns()
     with torch.cuda.device(dev):
         L = _as_device_matrix(left, dev)
-        R = _as_device_matrix(right, dev)
-        check_dims(L.shape[1], R.shape[1])
-        m = D.join_prepared(D.prepare(L), D.prepare(R), t.value, band)
+        check_dims(L.shape[1], right.shape[1])
+        if _is_host(right) and right.shape[0] >= _STREAM_MIN_ROWS:
+            # overlap the right relation's H2D copy with the filter
+            m, _ = D.join_streamed(D.prepare(L), _host_tensor(right), t.value, band)
+        else:
+            m = D.join_prepared(D.prepare(L), D.prepare(_as_device_matrix(right, dev)), t.value,
+                                band)
         matches = _to_matchset(m, left_name, right_name)
+    R = right
     wall = time.perf_counter_ns() - t0
     stats = JoinStats(wall_nanos=wall, model_calls_left=L.shape[0],
                       model_calls_right=R.shape[0], pairs_compared=L.shape[0] * R.shape[0],
@@ -207,7 +225,8 @@ def join_embedded(left: EmbeddedRelation, right: EmbeddedRelation, theta, *,
             x = torch.from_numpy(np.ascontiguousarray(er.data)).to(dev)
             if er.normalized:
                 p = D.prepare(x)          # re-normalising unit rows changes bits,
-                p.f32.copy_(x)            # so keep the caller's canonical rows
+                p.f32.copy_(x)            # so keep the caller's canonical rows;
+                p.row_err = p.tile_err = None  # errors were measured on the others
                 preps.append(p)
             else:
                 preps.append(D.prepare(x))

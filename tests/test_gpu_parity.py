@@ -218,6 +218,56 @@ def test_per_row_band_is_exact_and_tighter(cuda, manifest, golden):
         assert a.n_candidates < b.n_candidates, (L.shape, a.n_candidates, b.n_candidates)
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_streamed_join_matches_golden(cuda, manifest, golden, chunks, pinned):
+    """S copied in chunks and filtered per S-tile range (sjb_join_begin /
+    filter_tiles / finish): identical MatchSet."""
+    from paper_2312_01476_b200 import device as D
+    for name in ("cfg1", "c_ragged", "c_d768"):
+        meta = manifest["cases"][name]
+        L, S = case_inputs(meta)
+        Sh = torch.from_numpy(S)
+        if pinned:
+            Sh = Sh.pin_memory()
+        m, R = D.join_streamed(D.prepare(torch.from_numpy(L).to(cuda)), Sh, meta["theta"],
+                               chunks=chunks)
+        lo, ro, so = m.to_host()
+        assert np.array_equal(lo, golden[name + "_l"]) and np.array_equal(ro, golden[name + "_r"])
+        assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
+        ref = D.prepare(torch.from_numpy(S).to(cuda))
+        assert torch.equal(R.f32, ref.f32) and torch.equal(R.op.view(torch.int16), ref.op.view(torch.int16))
+        assert torch.equal(R.row_err[:R.n], ref.row_err[:R.n])
+
+
+def test_streamed_join_overflow_and_vectors_api(cuda, manifest, golden):
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    import paper_2312_01476_b200.join as J
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    D._cap_cache.clear()
+    old = D.initial_capacity
+    D.initial_capacity = lambda a, b: 1000           # force the overflow retry
+    try:
+        m, _ = D.join_streamed(D.prepare(torch.from_numpy(L).to(cuda)), torch.from_numpy(S),
+                               meta["theta"], chunks=4)
+    finally:
+        D.initial_capacity = old
+        D._cap_cache.clear()
+    assert m.retries == 1
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, golden["cfg1_l"]) and np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))
+    old_min = J._STREAM_MIN_ROWS
+    J._STREAM_MIN_ROWS = 1                            # route through the streamed path
+    try:
+        ms, st = tensor_join_vectors(L, S, meta["theta"])
+    finally:
+        J._STREAM_MIN_ROWS = old_min
+    assert np.array_equal(ms.lefts, golden["cfg1_l"]) and np.array_equal(ms.rights, golden["cfg1_r"])
+    assert st.pairs_compared == len(L) * len(S)
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -292,43 +292,46 @@ def _stream_chunks(n: int, chunks: int):
     return [(r0, min(n, r0 + step)) for r0 in range(0, n, step)]
 
 
-def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
-                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
-                  name: str = "") -> Tuple["DeviceMatches", PreparedRelation]:
-    """Join a prepared left relation with a HOST right relation, overlapping
-    the right side's host->device copy with the filter: the rows are copied in
-    chunks on a side stream; each chunk is normalised in place (canonical fp32
-    rows + its tiles of the bf16 image + rounding errors) and its S tiles are
-    filtered as soon as it lands (sjb_join_begin / sjb_join_filter_tiles /
-    sjb_join_finish).  Same result as prepare + join_prepared.  Returns the
-    matches and the prepared right relation (resident, reusable)."""
-    if right_host.is_cuda or right_host.dtype != torch.float32 or right_host.dim() != 2:
-        raise ValueError("right_host must be a 2-D float32 host tensor")
-    if right_host.shape[1] != L.dim:
-        raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {right_host.shape[1]}")
+def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
+                 band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
+                 inplace: bool = False, name: str = ""
+                 ) -> Tuple["DeviceMatches", PreparedRelation]:
+    """Join a prepared left relation with a right relation that becomes
+    available on the device chunk by chunk.
+
+    `raw` is the (n, dim) device buffer the right rows land in; arrive(r0, r1)
+    must make rows [r0, r1) of it ready on the current stream (wait for a
+    copy or a broadcast) -- it is called in row order, on 512-row boundaries.
+    Each chunk is then normalised (canonical fp32 rows + its tiles of the
+    bf16 image + rounding errors; in place when `inplace`) and its S tiles
+    are filtered at once (sjb_join_begin / sjb_join_filter_tiles /
+    sjb_join_finish), so the filter overlaps the arrival of later chunks.
+    Same result as prepare + join_prepared.  Returns the matches and the
+    prepared right relation (resident, reusable)."""
     lib = _lib.lib()
     dev = L.device
-    n, dim = right_host.shape
-    # pinned: asynchronous chunk copies; pageable: each chunk copy blocks the
-    # host while the GPU filters the previous chunk -- overlapped either way
-    src = right_host.contiguous()
+    n, dim = raw.shape
+    if dim != L.dim:
+        raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {dim}")
     theta32 = float(np.float32(theta))
     band = default_band(dim) if band is None else float(band)
     key = (L.n, n, dim, theta32, float(np.float32(band)), 0, 0, True)
     with _cap_lock:
         cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, n))
-    f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    f32 = raw if inplace else torch.empty((n, dim), dtype=torch.float32, device=dev)
     op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     R = PreparedRelation(f32, op, n, dim, name, rep, re, te)
+    spans = _stream_chunks(n, chunks)
     if L.n == 0 or n == 0:
+        for r0, r1 in spans:
+            arrive(r0, r1)
         return join_prepared(L, R, theta, band, left_base=left_base), R
     use_err = L.row_err is not None
     kp = kpad(dim)
     with torch.cuda.device(dev):
-        comp = torch.cuda.current_stream(dev)
-        copy = torch.cuda.Stream(dev)
+        cs = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         args = _join_args(L, n, theta32, band, cand_cap, left_base, use_err, te)
         ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
         if ws_bytes < 0:
@@ -338,31 +341,23 @@ def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
         rights = torch.empty_like(lefts)
         sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
         info_t = torch.zeros(5, dtype=torch.int64, device=dev)
-        cs = ctypes.c_void_p(comp.cuda_stream)
         _lib.check(lib.sjb_join_begin(ctypes.byref(args), _vp(ws), ws_bytes, cs), "sjb_join_begin")
-        copy.wait_stream(comp)   # buffers allocated on the compute stream
-        for r0, r1 in _stream_chunks(n, chunks):
-            with torch.cuda.stream(copy):
-                f32[r0:r1].copy_(src[r0:r1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            comp.wait_event(ev)
+        for r0, r1 in spans:
+            arrive(r0, r1)
             t0 = r0 // TILE_ROWS
             _lib.check(lib.sjb_normalize_rows(
-                ctypes.c_void_p(f32[r0:].data_ptr()), r1 - r0, dim,
-                ctypes.c_void_p(f32[r0:].data_ptr()),
+                ctypes.c_void_p(raw.data_ptr() + r0 * dim * 4), r1 - r0, dim,
+                ctypes.c_void_p(f32.data_ptr() + r0 * dim * 4),
                 ctypes.c_void_p(op.data_ptr() + t0 * TILE_ROWS * kp * 2), _vp(rep),
                 ctypes.c_void_p(re.data_ptr() + r0 * 4), ctypes.c_void_p(te.data_ptr() + t0 * 4),
                 cs), "sjb_normalize_rows")
             _lib.check(lib.sjb_join_filter_tiles(
                 _vp(L.f32), _vp(L.op), _vp(f32), _vp(op), ctypes.byref(args), _vp(ws), ws_bytes,
                 t0, -(-r1 // TILE_ROWS), cs), "sjb_join_filter_tiles")
-        src_keepalive = src  # the copies read `src` asynchronously
         _lib.check(lib.sjb_join_finish(ctypes.byref(args), _vp(ws), ws_bytes, _vp(lefts),
                                        _vp(rights), _vp(sims), _vp(info_t), cs),
                    "sjb_join_finish")
         info = info_t.cpu().numpy()
-        del src_keepalive
     n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
     flags = info[3:4].view(np.int32)
     if int(flags[0]):
@@ -375,6 +370,36 @@ def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
         _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
     return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
                          n_cand, int(cand_cap), 0, int(flags[1])), R
+
+
+def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
+                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
+                  name: str = "") -> Tuple["DeviceMatches", PreparedRelation]:
+    """join_chunked for a HOST right relation: the rows are copied in chunks
+    on a side stream and normalised in place as each chunk lands, so the
+    host->device copy overlaps the filter."""
+    if right_host.is_cuda or right_host.dtype != torch.float32 or right_host.dim() != 2:
+        raise ValueError("right_host must be a 2-D float32 host tensor")
+    dev = L.device
+    # pinned: asynchronous chunk copies; pageable: each chunk copy blocks the
+    # host while the GPU filters the previous chunk -- overlapped either way
+    src = right_host.contiguous()
+    n, dim = src.shape
+    with torch.cuda.device(dev):
+        comp = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(dev)
+        raw = torch.empty((n, dim), dtype=torch.float32, device=dev)
+        copy.wait_stream(comp)   # `raw` was allocated on the compute stream
+
+        def arrive(r0: int, r1: int) -> None:
+            with torch.cuda.stream(copy):
+                raw[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            comp.wait_event(ev)
+
+        return join_chunked(L, raw, arrive, theta, band, left_base, chunks, inplace=True,
+                            name=name)
 
 
 def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> PreparedRelation:

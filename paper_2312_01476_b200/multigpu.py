@@ -48,6 +48,26 @@ def broadcast_right(S: torch.Tensor, root: int = 0, group=None, chunk_rows: int 
     return S
 
 
+def broadcast_chunks(S: torch.Tensor, spans: Sequence[Tuple[int, int]], root: int = 0,
+                     group=None) -> Callable[[int, int], None]:
+    """Queue one asynchronous broadcast per row span of S (in order, on the
+    backend's stream) and return arrive(r0, r1), which makes the caller wait
+    for the span starting at r0 (for NCCL: the current CUDA stream waits; the
+    host does not block)."""
+    r, w = world()
+    works = {}
+    if w > 1:
+        for r0, r1 in spans:
+            works[r0] = dist.broadcast(S[r0:r1], src=root, group=group, async_op=True)
+
+    def arrive(r0: int, r1: int) -> None:
+        wk = works.pop(r0, None)
+        if wk is not None:
+            wk.wait()
+
+    return arrive
+
+
 def _device_join(R_shard: torch.Tensor, S: torch.Tensor, theta: float, left_base: int,
                  band: Optional[float]):
     from . import device as D
@@ -66,6 +86,22 @@ def sharded_join(R_shard: torch.Tensor, S: torch.Tensor, theta: float, left_base
     broadcast_right(S, 0, group)
     fn = join_fn or _device_join
     return fn(R_shard, S, theta, left_base, band)
+
+
+def sharded_join_streamed(R_shard: torch.Tensor, S: torch.Tensor, theta: float, left_base: int,
+                          group=None, band: Optional[float] = None, chunks: int = 8):
+    """sharded_join with the S broadcast overlapped with the join: S goes out
+    from rank 0 in row chunks (NCCL broadcasts queued at once on NCCL's
+    stream); each rank normalises and filters chunk k (device.join_chunked)
+    as soon as its broadcast has landed, while chunks k+1.. are still in
+    flight.  S must be a device tensor of the full shape on every rank (rank
+    0's is the source and is left unchanged).  Returns device.DeviceMatches
+    with left offsets shifted by ``left_base``."""
+    from . import device as D
+    pl = D.prepare(R_shard)
+    arrive = broadcast_chunks(S, D._stream_chunks(S.shape[0], chunks), root=0, group=group)
+    m, _ = D.join_chunked(pl, S, arrive, theta, band, left_base, chunks, inplace=False)
+    return m
 
 
 def concat_shards(parts: Sequence[Tuple[np.ndarray, np.ndarray, np.ndarray]]

@@ -268,6 +268,26 @@ def test_streamed_join_overflow_and_vectors_api(cuda, manifest, golden):
     assert st.pairs_compared == len(L) * len(S)
 
 
+def test_sharded_join_streamed_single_rank(cuda, manifest, golden):
+    """The streamed R-sharded join (chunked S broadcast + per-chunk filter) on
+    one rank: two shards joined separately concatenate to the golden set."""
+    from paper_2312_01476_b200 import multigpu as MG
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    Sd = torch.from_numpy(S).to(cuda)
+    S0 = Sd.clone()
+    parts = []
+    for r in range(2):
+        r0, r1 = MG.shard_range(len(L), r, 2)
+        m = MG.sharded_join_streamed(torch.from_numpy(L[r0:r1]).to(cuda), Sd, meta["theta"], r0,
+                                     chunks=5)
+        parts.append(m.to_host())
+    assert torch.equal(Sd, S0)                  # the source S is left unchanged
+    lo, ro, so = MG.concat_shards(parts)
+    assert np.array_equal(lo, golden["cfg1_l"]) and np.array_equal(ro, golden["cfg1_r"])
+    assert np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

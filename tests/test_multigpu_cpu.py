@@ -77,3 +77,44 @@ def test_shard_range_covers():
             rs = [shard_range(n, r, w) for r in range(w)]
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def _chunk_worker(rank, world, port, S_full, q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2312_01476_b200 import device as D, multigpu as MG
+    S = torch.from_numpy(S_full.copy()) if rank == 0 else torch.zeros(S_full.shape,
+                                                                     dtype=torch.float32)
+    spans = D._stream_chunks(S.shape[0], 5)
+    arrive = MG.broadcast_chunks(S, spans)
+    ok = True
+    for r0, r1 in spans:          # the streamed join's order: chunk by chunk
+        arrive(r0, r1)
+        ok &= bool(torch.equal(S[r0:r1], torch.from_numpy(S_full[r0:r1])))
+    ok &= bool(torch.equal(S, torch.from_numpy(S_full)))
+    q.put((rank, ok, [tuple(s) for s in spans]))
+    dist.destroy_process_group()
+
+
+def test_chunked_broadcast_arrives_in_order():
+    """The streamed sharded join's S broadcast (multigpu.broadcast_chunks):
+    every span is complete on every rank once arrive() returns, spans tile S
+    on 512-row boundaries."""
+    S = np.random.default_rng(5).standard_normal((2600, 8), dtype=np.float32)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, 2, port, S, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, ok, spans in res:
+        assert ok, rank
+        assert spans[0][0] == 0 and spans[-1][1] == len(S)
+        assert all(a[1] == b[0] and a[1] % 512 == 0 for a, b in zip(spans, spans[1:]))

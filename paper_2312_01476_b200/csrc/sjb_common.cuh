@@ -293,6 +293,17 @@ __device__ __forceinline__ float row_cutoff(float cutoff, float theta, float sla
   return fmaxf(cutoff, theta - b);
 }
 
+// The same cutoff from already-loaded errors (ex of the row, ey of the tile):
+// kernels load them ahead of the accumulator wait so the latency is hidden.
+__device__ __forceinline__ float cutoff_from(float cutoff, float theta, float slack, float ex,
+                                             float ey) {
+  const float b = slack + 1.000001f * (ex + ey) + ex * ey;
+  return fmaxf(cutoff, theta - b);
+}
+__device__ __forceinline__ float load_err(const float* e, int64_t i, int64_t n) {
+  return (e != nullptr && i < n) ? __ldg(e + i) : 0.0f;
+}
+
 __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
                                                  uint32_t gi, uint32_t j0, int64_t col_lim,
                                                  uint32_t* cta_cnt, uint32_t* cta_sat,

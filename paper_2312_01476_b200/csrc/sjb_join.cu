@@ -192,8 +192,11 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------------- MMA issuer
+      // whole warp, warp-uniform control flow; one elected lane issues each
+      // tcgen05 op (a single divergent lane costs an ELECT/R2UR sequence
+      // per MMA and made the issue the critical path)
       const uint32_t idesc = umma_idesc_bf16_f32(128, kUmmaN);
       const uint32_t lbo = kTileRows * 16;  // 256-row operand: distance between k-groups
       const uint32_t sbo = 128;             // distance between 8-row core-matrix groups
@@ -239,19 +242,19 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
             const uint64_t adh = ad + h * half_step;
 #pragma unroll
             for (int kk = 0; kk < KSTEPS; kk++)
-              tc_mma_bf16(d, adh + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
-            tc_commit(&acc_full[as]);
+              tc_mma_bf16_elect(d, adh + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
+            tc_commit_elect(&acc_full[as]);
             acc_it++;
           }
-          tc_commit(&b_empty[bstage]);
+          tc_commit_elect(&b_empty[bstage]);
           if (++bstage == p.stages) {
             bstage = 0;
             bphase ^= 1u;
           }
         }
-        tc_commit(&a_empty[ab]);
+        tc_commit_elect(&a_empty[ab]);
       }
-      if (dbg && blockIdx.x < 3)
+      if (dbg && blockIdx.x < 3 && lane == 0)
         printf("[dbg] cta %d mma: total %lld  wait_a %lld  wait_b %lld  wait_acc_empty %lld\n",
                blockIdx.x, clock64() - c_start, w_a, w_b, w_e);
     }
@@ -268,8 +271,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     uint32_t* sims = p.sims_bits + (uint64_t)blockIdx.x * seg_cap;
     volatile uint32_t* vcnt = cta_cnt;
     volatile uint32_t* vdone = epi_done;
-    recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps, p.l32,
-                 p.r32, p.dim, p.theta, p.rowcount, p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
+    if (p.debug_mode != 5)  // diagnostics: 5 = emit, but no recheck (results invalid)
+      recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps,
+                   p.l32, p.r32, p.dim, p.theta, p.rowcount,
+                   p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
   } else {
     // ---------------------------------------------------------- epilogue
     // 16 warps; warp (q, c) drains TMEM lanes 32q..32q+31 (R rows of the
@@ -280,7 +285,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     const int cq = ew >> 2;           // 64-column quarter of the 256-column stage
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t lane_base = (uint32_t)q * 32;
-    uint32_t dbg_acc = 0;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
     uint32_t acc_it = 0;
@@ -291,7 +295,13 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       const int64_t rb = item % nb, sc = item / nb;
       const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+      // per-row band terms: this lane's two R rows (once per item)
+      const bool per_row = p.row_err != nullptr;
+      const float ex0 = load_err(p.row_err, rb * kBM + lane_base + lane, p.n_a);
+      const float ex1 = load_err(p.row_err, rb * kBM + 128 + lane_base + lane, p.n_a);
       for (int64_t t = t0; t < t1; t++) {
+        // issued before the accumulator wait: its latency hides behind it
+        const float ey = per_row ? __ldg(p.tile_err + t) : 0.0f;
 #pragma unroll 1
         for (int h = 0; h < 2; h++) {
           const uint32_t as = acc_it & 1u;
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           const int64_t gi64 = rb * kBM + h * 128 + lane_base + lane;
           const bool row_ok = gi64 < p.n_a;
           const float cutoff =
-              row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64, p.n_a, t);
+              per_row ? cutoff_from(p.cutoff, p.theta, p.slack, h ? ex1 : ex0, ey) : p.cutoff;
           // group maxima over 8 columns, then the warp-tile maximum
           float g[8];
 #pragma unroll
@@ -355,10 +365,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
               }
             }
             const uint32_t cnt = __popc(mk0) + __popc(mk1);
-            if (p.debug_mode == 4) {  // diagnostics: masks only
-              dbg_acc += cnt;
-              continue;
-            }
             uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -393,7 +399,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         }
       }
     }
-    if (p.debug_mode == 4 && dbg_acc == 0xFFFFFFFFu) p.cand[0] = dbg_acc;
     if (edbg && lane == 0)
       printf("[dbg] cta %d epi warp %d: total %lld  wait_acc_full %lld  drain %lld\n",
              blockIdx.x, ew, clock64() - e_start, e_wait, e_drain);

@@ -227,6 +227,9 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     retries = 0
     ev0 = ev1 = None
     if filter_events is not None:
+        for e in filter_events:
+            if not e.cuda_event:       # torch creates the CUevent on first record
+                e.record(torch.cuda.current_stream(dev))
         ev0 = ctypes.c_void_p(filter_events[0].cuda_event)
         ev1 = ctypes.c_void_p(filter_events[1].cuda_event)
     with torch.cuda.device(dev):

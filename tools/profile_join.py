@@ -10,6 +10,7 @@ ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--theta", type=float, default=None)
 ap.add_argument("--n-left", type=int, default=None)
 ap.add_argument("--n-right", type=int, default=None)
+ap.add_argument("--uniform-band", action="store_true")
 a = ap.parse_args()
 over = {}
 if a.n_left: over["n_left"] = a.n_left
@@ -18,9 +19,18 @@ if a.n_right: over["n_right"] = a.n_right
 theta = a.theta if a.theta is not None else c["theta"]
 Lt, St = torch.from_numpy(L).cuda(), torch.from_numpy(S).cuda()
 PL, PS = D.prepare(Lt), D.prepare(St)
+ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+fl = []
 for i in range(a.iters):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    m = D.join_prepared(PL, PS, theta)
+    m = D.join_prepared(PL, PS, theta, filter_events=ev, per_row_band=not a.uniform_band)
     torch.cuda.synchronize(); t1 = time.perf_counter()
-    print(f"{a.cfg} iter {i}: {1e3*(t1-t0):.2f} ms matches={m.n_matches} cand={m.n_candidates} "
-          f"pairs/s={L.shape[0]*S.shape[0]/(t1-t0):.3e}", flush=True)
+    fms = ev[0].elapsed_time(ev[1])
+    if i > 0:
+        fl.append(fms)
+    print(f"{a.cfg} iter {i}: {1e3*(t1-t0):.2f} ms (filter {fms:.2f} ms) matches={m.n_matches} "
+          f"cand={m.n_candidates} pairs/s={L.shape[0]*S.shape[0]/(t1-t0):.3e}", flush=True)
+if fl:
+    import statistics
+    print(f"{a.cfg} filter median {statistics.median(fl):.3f} ms  min {min(fl):.3f} ms over {len(fl)}",
+          flush=True)

@@ -124,6 +124,11 @@ typedef struct sjb_join_args {
    * rounding errors, so no true match is dropped. */
   const float* left_row_err;
   const float* right_tile_err;
+  /* Canonical recheck placement (dim <= 128): 0 = fused into the filter (two
+   * warps recheck while the S chunk is in L2; best for sparse results),
+   * 1 = deferred to a full-occupancy kernel after the filter (best when
+   * candidates are dense, e.g. > 2e-4 of the pairs).  Same result. */
+  int32_t recheck;
 } sjb_join_args;
 
 typedef struct sjb_join_info {
@@ -166,7 +171,8 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
  *                         [tile_begin, tile_end) (256-row tiles; ranges of
  *                         one join must be disjoint and together cover S;
  *                         only those S rows must be prepared when it runs)
- *   sjb_join_finish       bucket, sort and emit the MatchSet; writes d_info
+ *   sjb_join_finish       (deferred canonical recheck,) bucket, sort and emit
+ *                         the MatchSet; writes d_info
  * sjb_join_prepared_async = begin + filter_tiles(all) + finish. */
 int sjb_join_begin(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
                    void* stream);
@@ -174,9 +180,9 @@ int sjb_join_filter_tiles(const float* d_l32, const void* d_l16, const float* d_
                           const void* d_r16, const sjb_join_args* args, void* d_workspace,
                           int64_t workspace_bytes, int64_t tile_begin, int64_t tile_end,
                           void* stream);
-int sjb_join_finish(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
-                    uint64_t* d_lefts, uint64_t* d_rights, float* d_sims, void* d_info,
-                    void* stream);
+int sjb_join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* args,
+                    void* d_workspace, int64_t workspace_bytes, uint64_t* d_lefts,
+                    uint64_t* d_rights, float* d_sims, void* d_info, void* stream);
 
 int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,
                       const void* d_r16, const sjb_join_args* args, void* d_workspace,

@@ -32,6 +32,7 @@ class JoinArgs(ctypes.Structure):
         ("grid", ctypes.c_int32), ("tiles_per_chunk", ctypes.c_int32),
         ("ev_filter_begin", ctypes.c_void_p), ("ev_filter_end", ctypes.c_void_p),
         ("left_row_err", ctypes.c_void_p), ("right_tile_err", ctypes.c_void_p),
+        ("recheck", ctypes.c_int32),
     ]
 
 
@@ -91,7 +92,8 @@ def lib(path: str = LIB_PATH):
     L.sjb_join_begin.argtypes = [ctypes.POINTER(JoinArgs), _vp, _i64, _vp]
     L.sjb_join_filter_tiles.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,
                                         _i64, _i64, _vp]
-    L.sjb_join_finish.argtypes = [ctypes.POINTER(JoinArgs), _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.sjb_join_finish.argtypes = [_vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64, _vp, _vp, _vp,
+                                  _vp, _vp]
     L.sjb_join_prepared.argtypes = [_vp, _vp, _vp, _vp, ctypes.POINTER(JoinArgs), _vp, _i64,
                                     _vp, _vp, _vp, ctypes.POINTER(JoinInfo), _vp]
     L.sjb_tile_dot.argtypes = [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]

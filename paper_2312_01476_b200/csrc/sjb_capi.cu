@@ -90,8 +90,18 @@ struct JoinPlan {
   bool pair;  // CTA-pair (cta_group::2) filter kernel
   bool wide;  // K-streaming kernel (kpad > 128)
   bool wide_fused;        // wide: recheck inside the filter (A/B only)
+  bool defer;             // d <= 128: recheck after the filter (recheck_direct_kernel)
   int64_t tile_stride;    // wide, separate recheck: tile offsets per CTA
 };
+
+// Recheck placement for d <= 128: args->recheck (0 fused, 1 deferred); the
+// SJB_RECHECK environment variable ("fused" / "deferred") overrides it.
+bool use_deferred_recheck(const sjb_join_args* a) {
+  const char* f = getenv("SJB_RECHECK");
+  if (f != nullptr && strcmp(f, "fused") == 0) return false;
+  if (f != nullptr && strcmp(f, "deferred") == 0) return true;
+  return a->recheck == 1;
+}
 
 bool use_wide_fused() {
   const char* f = getenv("SJB_WIDE_RECHECK");
@@ -170,8 +180,10 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->wide = false;
   pl->wide_fused = false;
   pl->tile_stride = 0;
+  pl->defer = false;
   if (pl->kpad > 128) return make_wide_plan(a, pl, sms, max_dyn_smem(dev));
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
+  pl->defer = use_deferred_recheck(a);
   // Shared memory: prefer a double-buffered resident R block when that still
   // leaves 3 B stages; otherwise one R buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);
@@ -604,7 +616,9 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   return SJB_OK;
 }
 
-bool fused_recheck(const JoinPlan& pl) { return !pl.wide || pl.wide_fused; }
+bool fused_recheck(const JoinPlan& pl) {
+  return pl.wide ? pl.wide_fused : !pl.defer;
+}
 
 int join_begin(const sjb_join_args* args, const JoinCtx& c, cudaStream_t st) {
   const JoinPlan& pl = c.pl;
@@ -663,6 +677,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   jp.tiles_per_chunk = tpc;
   jp.tile_begin = (int)tb;
   jp.append = 1;
+  jp.defer = pl.defer ? 1 : 0;
   jp.n_items = items;
   jp.stages = pl.stages;
   jp.a_bufs = pl.a_bufs;
@@ -802,11 +817,20 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
 }
 
 // Row offsets, then bucket by left row and sort each row by right offset.
-int join_finish(const sjb_join_args* args, const JoinCtx& c, uint64_t* d_lefts,
+int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* args,
+                const JoinCtx& c, uint64_t* d_lefts,
                 uint64_t* d_rights, float* d_sims, int64_t* info, cudaStream_t st) {
   const JoinPlan& pl = c.pl;
   const int64_t nl = args->n_left;
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
+  if (pl.defer) {
+    // nseg * per_seg warps, ~64 per SM
+    const int64_t per_seg = sjb::ceil_div((int64_t)sjb_sm_count(current_device()) * 64, (int64_t)pl.grid);
+    sjb::recheck_direct_kernel<<<(unsigned)sjb::ceil_div(per_seg * pl.grid * 32, 256), 256, 0, st>>>(
+        c.cand, pl.seg_cap, c.cta, pl.grid, d_l32, d_r32, (int)args->dim, args->theta,
+        c.sims_bits, c.rowcount);
+    SJB_CK_LAUNCH("recheck_direct");
+  }
   if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
   sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
   SJB_CK_LAUNCH("gate");
@@ -851,9 +875,9 @@ int sjb_join_filter_tiles(const float* d_l32, const void* d_l16, const float* d_
   return join_filter(d_l32, d_l16, d_r32, d_r16, args, c, tile_begin, tile_end, as_stream(stream));
 }
 
-int sjb_join_finish(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes,
-                    uint64_t* d_lefts, uint64_t* d_rights, float* d_sims, void* d_info,
-                    void* stream) {
+int sjb_join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* args,
+                    void* d_workspace, int64_t workspace_bytes, uint64_t* d_lefts,
+                    uint64_t* d_rights, float* d_sims, void* d_info, void* stream) {
   if (!d_info) return fail(SJB_E_INVALID, "null info");
   JoinCtx c;
   if (int rc = join_ctx(args, d_workspace, workspace_bytes, &c)) return rc;
@@ -863,7 +887,7 @@ int sjb_join_finish(const sjb_join_args* args, void* d_workspace, int64_t worksp
     SJB_CK(cudaMemsetAsync(info, 0, 5 * 8, st));
     return SJB_OK;
   }
-  return join_finish(args, c, d_lefts, d_rights, d_sims, info, st);
+  return join_finish(d_l32, d_r32, args, c, d_lefts, d_rights, d_sims, info, st);
 }
 
 int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* d_r32,
@@ -883,7 +907,7 @@ int sjb_join_prepared_async(const float* d_l32, const void* d_l16, const float* 
   if (int rc = join_filter(d_l32, d_l16, d_r32, d_r16, args, c, 0,
                            sjb::ceil_div(args->n_right, sjb::kTileRows), st))
     return rc;
-  return join_finish(args, c, d_lefts, d_rights, d_sims, info, st);
+  return join_finish(d_l32, d_r32, args, c, d_lefts, d_rights, d_sims, info, st);
 }
 
 int sjb_join_prepared(const float* d_l32, const void* d_l16, const float* d_r32,

@@ -59,6 +59,7 @@ struct JoinParams {
   int tiles_per_chunk;
   int tile_begin;            // first S tile of this launch (S-range launches)
   int append;                // 1: continue the segments of an earlier launch
+  int defer;                 // 1: recheck warps idle; recheck_direct_kernel runs later
   int64_t n_items;
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     uint32_t* sims = p.sims_bits + (uint64_t)blockIdx.x * seg_cap;
     volatile uint32_t* vcnt = cta_cnt;
     volatile uint32_t* vdone = epi_done;
-    if (p.debug_mode != 5)  // diagnostics: 5 = emit, but no recheck (results invalid)
+    if (p.debug_mode != 5 && !p.defer)  // (diagnostics: 5 = emit, no recheck, results invalid)
       recheck_loop(seg, sims, seg_cap, vcnt, vdone, (uint32_t)kEpiWarps, rw, kRecheckWarps,
                    p.l32, p.r32, p.dim, p.theta, p.rowcount,
                    p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);

@@ -21,8 +21,11 @@
 //   warp 0 lane 1  R-block producer
 //   warp 1         TMEM allocation (cta_group::2); lane 0 of the leader CTA
 //                  issues every MMA of the pair
-//   warps 2..9     epilogue: 32 lanes x 64 columns of each stage
-//   warps 10..13   canonical recheck of this CTA's candidates
+//   warps 2..17    epilogue, two groups of 8 taking alternate stages; a warp
+//                  drains 32 lanes x 64 columns of every other stage, so it
+//                  has two stage-times (~900 cycles) per stage it owns, and
+//                  the four TMEM stages absorb emission-heavy stages
+//   warps 18..19   canonical recheck of this CTA's candidates
 //
 // Operand delivery: 3-D TMA tensor copies with .cta_group::2.  The operand
 // image (256-row tiles, [k-group][row][8 elements]) is described as a tensor
@@ -45,10 +48,12 @@ namespace sjb {
 
 namespace pair {
 
-// 8 epilogue warps x 64 columns: per-stage fixed costs (waits, bounds, vote,
-// arrive) amortise over 64 values; 16 warps x 32 columns was issue-bound.
-constexpr int kEpiWarps = 8;
-constexpr int kRecheckWarps = 4;
+// 16 epilogue warps in two stage-alternating groups of 8, each warp 32 lanes x
+// 64 columns (64 values amortise the per-stage fixed costs; 16 warps x 32
+// columns of EVERY stage was issue-bound).
+constexpr int kEpiWarps = 16;
+constexpr int kEpiGroup = 8;  // warps per stage (per CTA)
+constexpr int kRecheckWarps = 2;
 constexpr int kThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
 constexpr int kAccStages = 4;
 constexpr int kUmmaN = 128;       // pair N (S rows per stage)
@@ -210,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kAccStages; i++) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 2 * kEpiWarps);
+      mbar_init(&acc_empty[i], 2 * kEpiGroup);
     }
     for (int s = 0; s < p.stages; s++) {
       mbar_init(&b_full[s], 1);
@@ -351,7 +356,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // is released right after the drain; with four TMEM stages the MMA runs
     // ahead while the warp reduces and emits.
     const int ew = warp - 2;
-    const int cq = ew >> 2;
+    const int grp = ew / kEpiGroup;          // stages k with k % 2 == grp
+    const int cq = (ew % kEpiGroup) >> 2;
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)q * 32;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
@@ -390,12 +396,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         else arrive_leader_relaxed(&acc_empty[as]);
       }
     };
-    auto process = [&](const float* v, const Stage& s) {
+    auto row_of = [&](const Stage& s) {
+      return s.rb * (2 * kARows) + rank * kARows + s.h * 128 + lane_base + lane;
+    };
+    auto process = [&](const float* v, const Stage& s, float cutoff) {
       if (p.debug_mode == 2 || !drain) return;
-      const int64_t gi64 = s.rb * (2 * kARows) + rank * kARows + s.h * 128 + lane_base + lane;
+      const int64_t gi64 = row_of(s);
       const bool row_ok = gi64 < p.n_a;
-      const float cutoff = row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64,
-                                      p.n_a, (s.t * kUmmaN) / kTileRows);
       float g[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
@@ -469,12 +476,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } while (0)
 
     float va[64];
-    uint32_t k = 0;
-    for (Stage cur = first_of(pair_id); cur.valid; cur = advance(cur), k++) {
+    uint32_t k = grp;
+    Stage cur = first_of(pair_id);
+    if (grp) cur = advance(cur);
+    for (; cur.valid; cur = advance(advance(cur)), k += 2) {
+      // band terms issued before the accumulator wait (latency hidden)
+      const bool per_row = p.row_err != nullptr;
+      const float ex = load_err(p.row_err, row_of(cur), p.n_a);
+      const float ey = per_row ? __ldg(p.tile_err + (cur.t * kUmmaN) / kTileRows) : 0.0f;
       SJB_PAIR_LOAD(k, va);
       tc_wait_ld();
       release(k % kAccStages);
-      process(va, cur);
+      process(va, cur, per_row ? cutoff_from(p.cutoff, p.theta, p.slack, ex, ey) : p.cutoff);
     }
 #undef SJB_PAIR_LOAD
     __syncwarp();

@@ -167,6 +167,17 @@ class DeviceMatches:
 _cap_lock = threading.Lock()
 _cap_cache: Dict[tuple, int] = {}
 
+# Recheck placement (sjb_join_args.recheck): joins whose last run of the same
+# shape had more candidates than this fraction of the pairs recheck in a
+# full-occupancy kernel after the filter; sparser ones inside it.
+DENSE_FRACTION = 2e-4
+
+
+def _recheck_mode(key: tuple, pairs: int) -> int:
+    with _cap_lock:
+        seen = _cap_cache.get(key, 0)
+    return 1 if pairs > 0 and seen > DENSE_FRACTION * pairs else 0
+
 # workspace is cached per device and grown on demand
 _ws_cache: Dict[int, torch.Tensor] = {}
 
@@ -241,7 +252,8 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                                  tiles_per_chunk=int(tiles_per_chunk),
                                  ev_filter_begin=ev0, ev_filter_end=ev1,
                                  left_row_err=L.row_err.data_ptr() if use_err else None,
-                                 right_tile_err=R.tile_err.data_ptr() if use_err else None)
+                                 right_tile_err=R.tile_err.data_ptr() if use_err else None,
+                                 recheck=_recheck_mode(key, L.n * R.n))
             ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
             if ws_bytes < 0:
                 _lib.check(-3, "sjb_join_workspace_bytes")
@@ -280,13 +292,14 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
 
 
 def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, cand_cap: int,
-               left_base: int, use_err: bool, right_tile_err: Optional[torch.Tensor]
-               ) -> "_lib.JoinArgs":
+               left_base: int, use_err: bool, right_tile_err: Optional[torch.Tensor],
+               recheck: int = 0) -> "_lib.JoinArgs":
     return _lib.JoinArgs(n_left=L.n, n_right=n_right, dim=L.dim, theta=theta32, band=band,
                          cand_cap=int(cand_cap), out_cap=int(cand_cap), left_base=int(left_base),
                          grid=0, tiles_per_chunk=0, ev_filter_begin=None, ev_filter_end=None,
                          left_row_err=L.row_err.data_ptr() if use_err else None,
-                         right_tile_err=right_tile_err.data_ptr() if use_err else None)
+                         right_tile_err=right_tile_err.data_ptr() if use_err else None,
+                         recheck=recheck)
 
 
 def _stream_chunks(n: int, chunks: int):
@@ -335,7 +348,8 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     kp = kpad(dim)
     with torch.cuda.device(dev):
         cs = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-        args = _join_args(L, n, theta32, band, cand_cap, left_base, use_err, te)
+        args = _join_args(L, n, theta32, band, cand_cap, left_base, use_err, te,
+                          _recheck_mode(key, L.n * n))
         ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
         if ws_bytes < 0:
             _lib.check(-3, "sjb_join_workspace_bytes")
@@ -357,7 +371,8 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
             _lib.check(lib.sjb_join_filter_tiles(
                 _vp(L.f32), _vp(L.op), _vp(f32), _vp(op), ctypes.byref(args), _vp(ws), ws_bytes,
                 t0, -(-r1 // TILE_ROWS), cs), "sjb_join_filter_tiles")
-        _lib.check(lib.sjb_join_finish(ctypes.byref(args), _vp(ws), ws_bytes, _vp(lefts),
+        _lib.check(lib.sjb_join_finish(_vp(L.f32), _vp(f32), ctypes.byref(args), _vp(ws),
+                                       ws_bytes, _vp(lefts),
                                        _vp(rights), _vp(sims), _vp(info_t), cs),
                    "sjb_join_finish")
         info = info_t.cpu().numpy()

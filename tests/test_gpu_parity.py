@@ -288,6 +288,24 @@ def test_sharded_join_streamed_single_rank(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))
 
 
+@pytest.mark.parametrize("recheck", ["fused", "deferred"])
+def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
+    """d <= 128: fused recheck warps and the deferred full-occupancy kernel
+    give the same bits (golden cases, overflow retry, theta = -1)."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv("SJB_RECHECK", recheck)
+    for name in ("cfg1", "c_small", "c_all", "c_d16_neg"):
+        meta = manifest["cases"][name]
+        L, S = case_inputs(meta)
+        pl = D.prepare(torch.from_numpy(L).to(cuda))
+        pr = D.prepare(torch.from_numpy(S).to(cuda))
+        for cap in (None, 300):      # 300: forces the overflow retry (>= grid)
+            m = D.join_prepared(pl, pr, meta["theta"], cand_cap=cap)
+            lo, ro, so = m.to_host()
+            assert np.array_equal(lo, golden[name + "_l"]) and np.array_equal(ro, golden[name + "_r"])
+            assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -31,11 +31,7 @@ def launches(path):
     return out
 
 
-def report(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
-    h, units, vals = rows[0], rows[1], rows[2]
+def _report_row(h, units, vals):
     res = {}
     for k in KEYS:
         if k in h:
@@ -53,12 +49,18 @@ def report(path):
     return res
 
 
-if __name__ == "__main__":
-    kind, src, dst = sys.argv[1], sys.argv[2], sys.argv[3]
-    data = launches(src) if kind == "launches" else report(src)
-    with open(dst, "w") as fh:
-        json.dump(data, fh, indent=1)
-    print(json.dumps(data, indent=1)[:3000])
+def report(path):
+    """Key counters of the first captured kernel; with several kernels in the
+    report, a dict {kernel name: counters}."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, units = rows[0], rows[1]
+    if len(rows) == 3:
+        return _report_row(h, units, rows[2])
+    ki = h.index("Kernel Name")
+    return {f"{r[ki].split('(')[0]} #{n}": _report_row(h, units, r)
+            for n, r in enumerate(rows[2:])}
 
 
 def to_bytes(entry):
@@ -71,3 +73,16 @@ def traffic(summary_path, dst, label):
     rd, wr = to_bytes(d["dram__bytes_read.sum"]), to_bytes(d["dram__bytes_write.sum"])
     json.dump({"kernel": label, "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd,
                "dram_write_bytes": wr, "source": summary_path}, open(dst, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    # launches <csv> <out.json> | report <ncu-rep> <out.json> | traffic <summary.json> <out.json> <label>
+    kind, src, dst = sys.argv[1], sys.argv[2], sys.argv[3]
+    if kind == "traffic":
+        traffic(src, dst, sys.argv[4])
+        print(open(dst).read())
+    else:
+        data = launches(src) if kind == "launches" else report(src)
+        with open(dst, "w") as fh:
+            json.dump(data, fh, indent=1)
+        print(json.dumps(data, indent=1)[:3000])

@@ -441,13 +441,23 @@ def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> 
 
 
 def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
-    """UTF-8 bytes of the tokens (device u8) and n+1 int64 offsets (device)."""
-    enc = [t.encode("utf-8") for t in tokens]
-    offs = np.zeros(len(enc) + 1, dtype=np.int64)
-    if enc:
-        np.cumsum([len(e) for e in enc], out=offs[1:])
-    raw = np.frombuffer(b"".join(enc) + b"\0", dtype=np.uint8)
-    return (torch.from_numpy(raw.copy()).to(device, non_blocking=False),
+    """UTF-8 bytes of the tokens (device u8) and n+1 int64 offsets (device).
+    ASCII token lists (the common case) are packed with one join and one
+    encode; others token by token."""
+    n = len(tokens)
+    joined = "".join(tokens)
+    if joined.isascii():
+        raw = joined.encode("ascii")
+        lens = np.fromiter(map(len, tokens), dtype=np.int64, count=n)
+    else:
+        enc = [t.encode("utf-8") for t in tokens]
+        raw = b"".join(enc)
+        lens = np.fromiter(map(len, enc), dtype=np.int64, count=n)
+    offs = np.zeros(n + 1, dtype=np.int64)
+    if n:
+        np.cumsum(lens, out=offs[1:])
+    buf = np.frombuffer(raw + b"\0", dtype=np.uint8)
+    return (torch.from_numpy(buf.copy()).to(device, non_blocking=False),
             torch.from_numpy(offs).to(device))
 
 

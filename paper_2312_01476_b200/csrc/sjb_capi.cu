@@ -90,7 +90,7 @@ struct JoinPlan {
   bool pair;  // CTA-pair (cta_group::2) filter kernel
   bool wide;  // K-streaming kernel (kpad > 128)
   bool wide_fused;        // wide: recheck inside the filter (A/B only)
-  bool defer;             // d <= 128: recheck after the filter (recheck_direct_kernel)
+  bool defer;             // d <= 128: row-grouped recheck after the filter (dense joins)
   int64_t tile_stride;    // wide, separate recheck: tile offsets per CTA
 };
 
@@ -183,7 +183,8 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->defer = false;
   if (pl->kpad > 128) return make_wide_plan(a, pl, sms, max_dyn_smem(dev));
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
-  pl->defer = use_deferred_recheck(a);
+  // the row-grouped recheck stages candidates in the output-sized key buffer
+  pl->defer = use_deferred_recheck(a) && a->out_cap >= a->cand_cap;
   // Shared memory: prefer a double-buffered resident R block when that still
   // leaves 3 B stages; otherwise one R buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);
@@ -218,7 +219,8 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 
 // ------------------------------------------------------------ workspace
 struct JoinWs {
-  size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, total;
+  size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
+      total;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -241,6 +243,7 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   w.bigrows = o;  o = align256(o + nl * 4);
   w.nbig = o;     o = align256(o + 16);
   w.tiles = o;    o = align256(o + (size_t)grid * (size_t)tile_stride * 4);
+  w.ncand = o;    o = align256(o + 16);
   w.total = o;
   return w;
 }
@@ -582,6 +585,7 @@ struct JoinCtx {
   uint32_t* bigrows;
   unsigned int* nbig;
   uint32_t* tile_off;
+  uint64_t* ncand;  // dense recheck: number of grouped candidates
   bool empty;  // n_left == 0 or n_right == 0
 };
 
@@ -613,6 +617,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->bigrows = reinterpret_cast<uint32_t*>(ws + w.bigrows);
   c->nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
   c->tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
+  c->ncand = reinterpret_cast<uint64_t*>(ws + w.ncand);
   return SJB_OK;
 }
 
@@ -823,29 +828,50 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
   const JoinPlan& pl = c.pl;
   const int64_t nl = args->n_left;
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
+  uint64_t* keys = c.keys;
   if (pl.defer) {
-    // nseg * per_seg warps, ~64 per SM
-    const int64_t per_seg = sjb::ceil_div((int64_t)sjb_sm_count(current_device()) * 64, (int64_t)pl.grid);
-    sjb::recheck_direct_kernel<<<(unsigned)sjb::ceil_div(per_seg * pl.grid * 32, 256), 256, 0, st>>>(
-        c.cand, pl.seg_cap, c.cta, pl.grid, d_l32, d_r32, (int)args->dim, args->theta,
-        c.sims_bits, c.rowcount);
-    SJB_CK_LAUNCH("recheck_direct");
+    // dense: group the candidates by left row, recheck them row-grouped,
+    // then compact the matches by row (the segment buffer is free by then)
+    const dim3 sgrid(8, (unsigned)pl.grid);
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    SJB_CK_LAUNCH("count_rows");
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+    SJB_CK(cudaMemcpyAsync(c.ncand, c.rowoff + nl, 8, cudaMemcpyDeviceToDevice, st));
+    sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
+                                                  reinterpret_cast<unsigned long long*>(c.cursor),
+                                                  c.keys);
+    SJB_CK_LAUNCH("group_rows");
+    SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
+    const unsigned flat = (unsigned)sjb_sm_count(current_device()) * 8;
+    sjb::recheck_grouped_kernel<<<flat, 256, 0, st>>>(c.keys, c.ncand, d_l32, d_r32,
+                                                      (int)args->dim, args->theta, c.sims_bits,
+                                                      c.rowcount);
+    SJB_CK_LAUNCH("recheck_grouped");
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+    sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
+    SJB_CK_LAUNCH("gate");
+    keys = c.cand;
+    sjb::compact_rows_kernel<<<flat, 256, 0, st>>>(
+        c.keys, c.sims_bits, c.ncand, reinterpret_cast<unsigned long long*>(c.cursor), keys,
+        c.nbig);
+    SJB_CK_LAUNCH("compact_rows");
+  } else {
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+    sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
+    SJB_CK_LAUNCH("gate");
+    sjb::scatter_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
+        c.cand, pl.seg_cap, c.cta, pl.grid, c.sims_bits,
+        reinterpret_cast<unsigned long long*>(c.cursor), c.keys, c.nbig);
+    SJB_CK_LAUNCH("scatter");
   }
-  if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
-  sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
-  SJB_CK_LAUNCH("gate");
-  sjb::scatter_kernel<<<grid_for(slots, 256, 8), 256, 0, st>>>(
-      c.cand, pl.seg_cap, c.cta, pl.grid, c.sims_bits,
-      reinterpret_cast<unsigned long long*>(c.cursor), c.keys, c.nbig);
-  SJB_CK_LAUNCH("scatter");
   sjb::segsort_small_kernel<<<grid_for((uint64_t)nl * 32, sjb::kSortSmallThreads, 16),
                               sjb::kSortSmallThreads, 0, st>>>(
-      c.rowoff, nl, c.keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
+      c.rowoff, nl, keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
   SJB_CK_LAUNCH("segsort_small");
   const int big_smem = sjb::kSortBigCap * 8;
   if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
   sjb::segsort_big_kernel<<<sjb_sm_count(current_device()), sjb::kSortBigThreads, big_smem, st>>>(
-      c.rowoff, c.keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
+      c.rowoff, keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
   SJB_CK_LAUNCH("segsort_big");
   sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.rowoff, nl,
                                                args->out_cap, info);

@@ -59,7 +59,7 @@ struct JoinParams {
   int tiles_per_chunk;
   int tile_begin;            // first S tile of this launch (S-range launches)
   int append;                // 1: continue the segments of an earlier launch
-  int defer;                 // 1: recheck warps idle; recheck_direct_kernel runs later
+  int defer;                 // 1: recheck warps idle; the row-grouped recheck runs later
   int64_t n_items;
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers

@@ -118,38 +118,72 @@ scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __r
 // Sort key = (right offset << 32) | sim bits: unique per row because right
 // offsets are unique within a row.  gate[1] == 0 (matches exceed the output
 // capacity) turns scatter and sort into no-ops; the host retries.
-// Deferred canonical recheck: every written slot of
-// every candidate segment, at full occupancy, one sequential-FMA chain per
-// thread (dot_seq_dev = sj_dot_seq, _kernelcore.c:101-106).  Used instead of
-// the filter's two fused recheck warps, which are latency-bound when
-// candidates are plentiful (cfg5: 8e7 candidates).
-__global__ void __launch_bounds__(256)
-recheck_direct_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
-                      const unsigned long long* __restrict__ cta_count, int nseg,
-                      const float* __restrict__ l32, const float* __restrict__ r32, int dim,
-                      float theta, uint32_t* __restrict__ sims_bits,
-                      uint32_t* __restrict__ rowcount) {
-  // Segments advance together: warp w owns segment w % nseg and 32-slot runs
-  // w / nseg + i * per_seg (launched with nseg * per_seg warps), so the
-  // candidates rechecked at any moment were produced by the filter at about
-  // the same time (the same S chunk, still in L2), and the 32 lanes of a warp
-  // take consecutive slots (shared rows hit in L1).
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t per_seg = ((gridDim.x * blockDim.x) >> 5) / (uint32_t)nseg;
-  if (w >= per_seg * (uint32_t)nseg) return;
-  const int c = (int)(w % (uint32_t)nseg);
-  const unsigned long long cc = cta_count[c];
+// ---------------------------------------------- dense (row-grouped) recheck
+// For dense joins (deferred mode) the candidates are first grouped by left
+// row, so the canonical recheck reads each R row from L1 for all of that
+// row's candidates and only the S rows come from L2:
+//   count_rows -> scan -> group_rows -> recheck_grouped -> scan -> compact
+// Segment kernels run on a 2-D grid: blockIdx.y = segment.
+__global__ void count_rows_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                                  const unsigned long long* __restrict__ cta_count,
+                                  uint32_t* __restrict__ rowcount) {
+  const unsigned long long cc = cta_count[blockIdx.y];
   if (cc > seg_cap) return;  // saturated segment: the join is retried with room
-  const uint64_t* seg = cand + (uint64_t)c * seg_cap;
-  uint32_t* sims = sims_bits + (uint64_t)c * seg_cap;
-  for (uint64_t k = (uint64_t)(w / (uint32_t)nseg) * 32 + lane; k < cc; k += (uint64_t)per_seg * 32) {
+  const uint64_t* seg = cand + (uint64_t)blockIdx.y * seg_cap;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cc;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(rowcount + (uint32_t)(seg[k] >> 32), 1u);
+}
+
+__global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                                  const unsigned long long* __restrict__ cta_count,
+                                  unsigned long long* __restrict__ cursor,
+                                  uint64_t* __restrict__ grouped) {
+  const unsigned long long cc = cta_count[blockIdx.y];
+  if (cc > seg_cap) return;
+  const uint64_t* seg = cand + (uint64_t)blockIdx.y * seg_cap;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cc;
+       k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t u = seg[k];
+    grouped[atomicAdd(cursor + (uint32_t)(u >> 32), 1ull)] = u;
+  }
+}
+
+// grouped[0 .. *total) holds (i << 32 | j) grouped by i: consecutive threads
+// share the R row (L1), S rows come from L2 (dot_seq_dev = sj_dot_seq).
+__global__ void __launch_bounds__(256)
+recheck_grouped_kernel(const uint64_t* __restrict__ grouped, const uint64_t* __restrict__ total,
+                       const float* __restrict__ l32, const float* __restrict__ r32, int dim,
+                       float theta, uint32_t* __restrict__ sims_bits,
+                       uint32_t* __restrict__ rowcount) {
+  const uint64_t n = *total;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = grouped[k];
     const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;
     const float x = dot_seq_dev(l32 + (size_t)gi * dim, r32 + (size_t)gj * dim, dim);
     const bool ok = x >= theta;
-    sims[k] = ok ? __float_as_uint(x) : kRejected;
+    sims_bits[k] = ok ? __float_as_uint(x) : kRejected;
     if (ok) atomicAdd(rowcount + gi, 1u);
+  }
+}
+
+// Matches of the grouped candidates into per-row runs (j << 32 | sim bits)
+// at the match offsets (cursor = row offsets), for the segmented sort.
+__global__ void compact_rows_kernel(const uint64_t* __restrict__ grouped,
+                                    const uint32_t* __restrict__ sims_bits,
+                                    const uint64_t* __restrict__ total,
+                                    unsigned long long* __restrict__ cursor,
+                                    uint64_t* __restrict__ keys,
+                                    const unsigned int* __restrict__ gate) {
+  if (gate[1] == 0) return;
+  const uint64_t n = *total;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t sb = sims_bits[k];
+    if (sb == kRejected) continue;
+    const uint64_t u = grouped[k];
+    keys[atomicAdd(cursor + (uint32_t)(u >> 32), 1ull)] = (uint64_t((uint32_t)u) << 32) | sb;
   }
 }
 

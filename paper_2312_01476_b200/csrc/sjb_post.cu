@@ -150,18 +150,39 @@ __global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t se
 }
 
 // grouped[0 .. *total) holds (i << 32 | j) grouped by i: consecutive threads
-// share the R row (L1), S rows come from L2 (dot_seq_dev = sj_dot_seq).
+// share the R row (L1), S rows come from L2 (the sequential chain of
+// dot_seq_dev = sj_dot_seq).  Staging the warp's S rows in shared memory was
+// measured slower (7.4 -> 14.5 ms at cfg5).
 __global__ void __launch_bounds__(256)
 recheck_grouped_kernel(const uint64_t* __restrict__ grouped, const uint64_t* __restrict__ total,
                        const float* __restrict__ l32, const float* __restrict__ r32, int dim,
                        float theta, uint32_t* __restrict__ sims_bits,
                        uint32_t* __restrict__ rowcount) {
   const uint64_t n = *total;
+  // R rows stream through once per row group (evict first); S rows are
+  // re-read by every row of their cluster (keep them in L2)
+  const uint64_t pol_r = policy_evict_first(), pol_s = policy_evict_last();
+  const bool vec = (dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(l32) |
+                                       reinterpret_cast<uintptr_t>(r32)) & 15) == 0;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t u = grouped[k];
     const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;
-    const float x = dot_seq_dev(l32 + (size_t)gi * dim, r32 + (size_t)gj * dim, dim);
+    const float* a = l32 + (size_t)gi * dim;
+    const float* b = r32 + (size_t)gj * dim;
+    float x = 0.0f;
+    if (vec) {
+#pragma unroll 5
+      for (int d = 0; d < dim; d += 4) {
+        const float4 p = ldg4_hint(a + d, pol_r), q = ldg4_hint(b + d, pol_s);
+        x = __fmaf_rn(p.x, q.x, x);
+        x = __fmaf_rn(p.y, q.y, x);
+        x = __fmaf_rn(p.z, q.z, x);
+        x = __fmaf_rn(p.w, q.w, x);
+      }
+    } else {
+      x = dot_seq_dev(a, b, dim);
+    }
     const bool ok = x >= theta;
     sims_bits[k] = ok ? __float_as_uint(x) : kRejected;
     if (ok) atomicAdd(rowcount + gi, 1u);
@@ -227,22 +248,29 @@ __device__ __forceinline__ void nsync() {
   if (kWarp) __syncwarp(); else __syncthreads();
 }
 
+// k and j are powers of two: block/offset by shift and mask (a runtime
+// integer division per compare-exchange dominated the sort).
 template <bool kWarp>
 __device__ void smem_bitonic(uint64_t* s, int n, int tid, int nthr) {
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int k = 2; k <= P; k <<= 1) {
+  int P = 1, lp = 0;
+  while (P < n) {
+    P <<= 1;
+    lp++;
+  }
+  for (int lk = 1; lk <= lp; lk++) {
+    const int k = 1 << lk, lh = lk - 1;  // k/2 = 1 << lh
     // mirror step
     for (int t = tid; t < P / 2; t += nthr) {
-      const int blk = t / (k / 2), off = t % (k / 2);
-      const int a = blk * k + off, b = blk * k + k - 1 - off;
+      const int blk = t >> lh, off = t & ((1 << lh) - 1);
+      const int a = (blk << lk) + off, b = (blk << lk) + k - 1 - off;
       if (b < n) cmpx(s, a, b);
     }
     nsync<kWarp>();
-    for (int j = k / 4; j >= 1; j >>= 1) {
+    for (int lj = lk - 2; lj >= 0; lj--) {
+      const int j = 1 << lj;
       for (int t = tid; t < P / 2; t += nthr) {
-        const int blk = t / j, off = t % j;
-        const int a = blk * 2 * j + off, b = a + j;
+        const int blk = t >> lj, off = t & (j - 1);
+        const int a = (blk << (lj + 1)) + off, b = a + j;
         if (b < n) cmpx(s, a, b);
       }
       nsync<kWarp>();

@@ -200,6 +200,15 @@ int sjb_tile_dot(const float* d_left, int64_t lda, const float* d_bt, int64_t ld
 int sjb_dots_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
                 void* stream);
 
+/* out[i] = cosine of a and row i with the reference's arithmetic (cosine_vm,
+ * linalg.py:70-84): sj_dots_vm / (fp32(sj_row_norms(a)) * sj_row_norms(row i)),
+ * fp32 multiply then fp32 divide.  *d_flags (device int, zeroed by the
+ * caller) gets bit 0 if ||a|| == 0 and bit 1 if some row norm is 0 -- the
+ * reference raises ZeroVector in both cases.  Used by e_selection
+ * (join.py:145-179) and top_k (embedding.py:218-231). */
+int sjb_cosine_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
+                  int* d_flags, void* stream);
+
 /* Row-major threshold scan of a dense nl x nr buffer (sj_scan_count +
  * sj_scan_fill, _kernelcore.h:15-18).  Pass 1 (outputs NULL): *count = hits.
  * Pass 2: fills up to cap hits in row-major order.  Synchronous. */

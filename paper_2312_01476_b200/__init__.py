@@ -22,7 +22,8 @@ _LAZY = {
     # join operators (need torch + the CUDA library)
     "BatchPlan": "join", "JoinStats": "join", "Tile": "join", "plan_batches": "join",
     "tensor_join": "join", "nlj_prefetch": "join", "tensor_join_vectors": "join",
-    "join_prepared": "join", "join_embedded": "join",
+    "join_prepared": "join", "join_embedded": "join", "e_selection": "join",
+    "cosine_vm": "linalg", "top_k": "embedding",
     # models
     "EmbeddingModel": "embedding", "SyntheticModel": "embedding", "LookupModel": "embedding",
     "SubwordModel": "embedding", "embed_relation": "embedding",

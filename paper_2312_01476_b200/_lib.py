@@ -16,7 +16,7 @@ EXPORTS = (
     "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
     "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band", "sjb_accum_slack",
     "sjb_tile_count", "sjb_join_begin", "sjb_join_filter_tiles", "sjb_join_finish",
-    "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm",
+    "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm", "sjb_cosine_vm",
     "sjb_scan_hits", "sjb_scan_hits_workspace_bytes",
 )
 
@@ -98,6 +98,7 @@ def lib(path: str = LIB_PATH):
                                     _vp, _vp, _vp, ctypes.POINTER(JoinInfo), _vp]
     L.sjb_tile_dot.argtypes = [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]
     L.sjb_dots_vm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.sjb_cosine_vm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
     L.sjb_scan_hits.argtypes = [_vp, _i64, _i64, ctypes.c_float, ctypes.c_uint64,
                                 ctypes.c_uint64, _vp, _vp, _vp, _i64, ctypes.POINTER(_i64),
                                 _vp, _i64, _vp]

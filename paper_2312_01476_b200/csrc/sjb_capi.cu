@@ -970,6 +970,17 @@ int sjb_tile_dot(const float* d_left, int64_t lda, const float* d_bt, int64_t ld
   return SJB_OK;
 }
 
+int sjb_cosine_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
+                  int* d_flags, void* stream) {
+  if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape");
+  if (!d_flags) return fail(SJB_E_INVALID, "null flags");
+  const unsigned blocks = (unsigned)(n > 0 ? sjb::ceil_div(n, 256) : 1);
+  sjb::cosine_vm_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_a, d_m, n, (int)dim, d_out,
+                                                               d_flags);
+  SJB_CK_LAUNCH("cosine_vm");
+  return SJB_OK;
+}
+
 int sjb_dots_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
                 void* stream) {
   if (n <= 0) return SJB_OK;

@@ -460,6 +460,39 @@ __global__ void dots_vm_kernel(const float* __restrict__ a, const float* __restr
   if (i < n) out[i] = dot_seq_dev(a, m + i * dim, dim);
 }
 
+// cosine_vm (linalg.py:70-84): out[i] = dot(a, m_i) / (||a|| * ||m_i||) with
+// the reference's arithmetic -- sequential fmaf dot (sj_dots_vm), norms as
+// fp64 sequential sums rounded to fp32 (sj_row_norms), then one fp32 multiply
+// and one fp32 divide (numpy float32 ufuncs, round to nearest).  flags bit 0:
+// ||a|| == 0, bit 1: some ||m_i|| == 0 (the reference raises ZeroVector).
+__device__ __forceinline__ float row_norm_dev(const float* x, int dim) {
+  double ss = 0.0;
+  for (int d = 0; d < dim; d++) {
+    const double v = (double)x[d];
+    ss = __dadd_rn(ss, __dmul_rn(v, v));
+  }
+  return __double2float_rn(sqrt(ss));
+}
+
+__global__ void cosine_vm_kernel(const float* __restrict__ a, const float* __restrict__ m,
+                                 int64_t n, int dim, float* __restrict__ out,
+                                 int* __restrict__ flags) {
+  __shared__ float na_s;
+  if (threadIdx.x == 0) {
+    na_s = row_norm_dev(a, dim);
+    if (blockIdx.x == 0 && na_s == 0.0f) atomicOr(flags, 1);
+  }
+  __syncthreads();
+  const float na = na_s;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* row = m + i * dim;
+  const float dot = dot_seq_dev(a, row, dim);
+  const float nr = row_norm_dev(row, dim);
+  if (nr == 0.0f) atomicOr(flags, 2);
+  out[i] = __fdiv_rn(dot, __fmul_rn(na, nr));
+}
+
 // Dense threshold scan, row-major order (sj_scan_count / sj_scan_fill).
 __global__ void dense_count_kernel(const float* __restrict__ buf, int64_t nl, int64_t nr,
                                    float theta, uint32_t* __restrict__ rowcount) {

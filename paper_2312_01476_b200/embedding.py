@@ -345,6 +345,21 @@ def prepare_relation(model: EmbeddingModel, r: RawRelation,
     return D.prepare(embed_relation_device(model, r, dev), r.name)
 
 
+def top_k(model: EmbeddingModel, er: EmbeddedRelation, raw: RawRelation, probe: str,
+          k: int):
+    """The k most cosine-similar tokens to the probe, ties broken by lower
+    offset (reference embedding.py:218-231); cosines on the device."""
+    from .linalg import cosine_vm
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    if len(er) != len(raw):
+        raise ValueError("embedded and raw relations disagree on cardinality")
+    probe_vec = model.embed(probe)
+    sims = cosine_vm(probe_vec, er)
+    order = np.argsort(-sims, kind="stable")[:k]
+    return [(raw.tokens[i], float(sims[i])) for i in order]
+
+
 def decode(r: RawRelation, offset: int) -> str:
     """Original token of a tuple offset (embedding.py:166-171)."""
     if not 0 <= offset < len(r):

@@ -152,6 +152,34 @@ def tensor_join(left: RawRelation, right: RawRelation, model: EmbeddingModel, th
     return _run(left, right, model, theta, threads, "tensor", "right", band, device)
 
 
+def e_selection(raw: RawRelation, model: EmbeddingModel, probe: str, theta, *,
+                device=None) -> Tuple[MatchSet, JoinStats]:
+    """Offsets of tuples whose cosine to the embedded probe is >= theta
+    (reference join.py:145-179): |R| + 1 model calls, the relation embedded
+    on the device, cosines by sjb_cosine_vm (the reference's arithmetic)."""
+    from .embedding import embed_relation_device
+    from .linalg import cosine_vm_device
+    t = Threshold.of(theta)
+    dev = _device(device)
+    t0 = time.perf_counter_ns()
+    probe_vec = model.embed(probe)
+    with torch.cuda.device(dev):
+        rows = embed_relation_device(model, raw, dev)
+        if len(raw):
+            sims = cosine_vm_device(probe_vec, rows).cpu().numpy()
+            hits = np.nonzero(sims >= np.float32(t.value))[0]
+            matches = MatchSet(raw.name, "probe", hits.astype(np.uint64),
+                               np.zeros(len(hits), dtype=np.uint64),
+                               np.ascontiguousarray(sims[hits]))
+        else:
+            matches = MatchSet(raw.name, "probe")
+    wall = time.perf_counter_ns() - t0
+    stats = JoinStats(wall_nanos=wall, model_calls_left=len(raw), model_calls_right=1,
+                      pairs_compared=len(raw), matches=len(matches), peak_buffer_bytes=0,
+                      threads=1, algo="e_selection", inner_relation="right")
+    return matches, stats
+
+
 def nlj_prefetch(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta,
                  threads: int = 1, inner: Optional[str] = None, *,
                  band: Optional[float] = None, device=None) -> Tuple[MatchSet, JoinStats]:

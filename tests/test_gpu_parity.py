@@ -306,6 +306,36 @@ def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
             assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
 
 
+def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
+    """sjb_cosine_vm and the operators on it against the reference's own
+    outputs (e_selection join.py:145-179, top_k embedding.py:218-231)."""
+    from paper_2312_01476_b200 import (EmbeddedRelation, RawRelation, SyntheticModel, ZeroVector,
+                                       cosine_vm, e_selection, embed_relation, top_k)
+    got = cosine_vm(golden["cos_vm_a"], EmbeddedRelation(golden["cos_vm_m"], 37, False, "c"))
+    assert np.array_equal(got.view(np.uint32), golden["cos_vm_out"].view(np.uint32))
+    rel = RawRelation("sel", [f"l_{i}" for i in range(40)] + ["dog", "cat", "été"])
+    for th in (0.0, 0.2):
+        model = SyntheticModel(16, seed=7)
+        ms, st = e_selection(rel, model, "probe_word", th)
+        k = f"esel_{th}"
+        assert _bits_equal(ms, golden[k + "_l"], golden[k + "_r"], golden[k + "_s"])
+        assert [st.model_calls_left, st.model_calls_right] == manifest["cases"][k]["model_calls"]
+        assert model.call_count == len(rel) + 1 and st.algo == "e_selection"
+    model = SyntheticModel(16, seed=7)
+    tk = top_k(model, embed_relation(model, rel), rel, "probe_word", 7)
+    assert [t for t, _ in tk] == [t for t, _ in manifest["top_k_probe_word_7"]]
+    assert np.array_equal(np.array([s for _, s in tk], dtype=np.float32).view(np.uint32),
+                          golden["top_k_sims"].view(np.uint32))
+    with pytest.raises(ZeroVector):
+        cosine_vm(np.zeros(37, np.float32), golden["cos_vm_m"])
+    z = golden["cos_vm_m"].copy()
+    z[5] = 0
+    with pytest.raises(ZeroVector):
+        cosine_vm(golden["cos_vm_a"], z)
+    with pytest.raises(ValueError):
+        top_k(model, embed_relation(model, rel), rel, "p", 0)
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -86,3 +86,13 @@ def test_reference_kernels_agree_with_oracle(golden, manifest):
     chunks = refkern.nlj_rows(nl, 0, nl.shape[0], nr, meta["theta"])
     cl = np.concatenate([c[0] for c in chunks])
     assert np.array_equal(cl, lo)
+
+
+def test_cosine_vm_restatement_matches_reference(golden):
+    """cosine_vm (linalg.py:70-84) restated on the oracle kernels: fp32
+    na * norm_i, then fp32 dot / denom -- bitwise the reference's output."""
+    a, m = golden["cos_vm_a"], golden["cos_vm_m"]
+    na = O.row_norms(a.reshape(1, -1))[0]
+    denom = np.multiply(np.float32(na), O.row_norms(m), dtype=np.float32)
+    got = np.divide(O.dots_vm(a, m), denom, dtype=np.float32)
+    assert np.array_equal(got.view(np.uint32), golden["cos_vm_out"].view(np.uint32))

@@ -302,10 +302,20 @@ def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, c
                          recheck=recheck)
 
 
-def _stream_chunks(n: int, chunks: int):
-    """Row ranges of ~n/chunks rows on 512-row boundaries (operand tile pairs)."""
+def _stream_chunks(n: int, chunks: int, lead: int = 4):
+    """Row ranges on 512-row boundaries (operand tile pairs): a short first
+    chunk (1/lead of a regular one) so the filter starts early, then ~n/chunks
+    rows each."""
     step = max(512, -(-n // max(chunks, 1)) // 512 * 512 or 512)
-    return [(r0, min(n, r0 + step)) for r0 in range(0, n, step)]
+    first = max(512, step // max(lead, 1) // 512 * 512)
+    spans, r0 = [], 0
+    if n > step:
+        spans.append((0, min(n, first)))
+        r0 = spans[-1][1]
+    while r0 < n:
+        spans.append((r0, min(n, r0 + step)))
+        r0 += step
+    return spans
 
 
 def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,

@@ -320,11 +320,14 @@ segsort_small_kernel(const uint64_t* __restrict__ rowoff, int64_t n_rows, const 
 }
 
 constexpr int kSortBigThreads = 512;
-constexpr int kSortBigCap = 8192;  // 64 KB of dynamic smem
+constexpr int kSortBigCap = 26624;   // keys sorted whole in shared memory (208 KB)
+constexpr int kSortChunk = 16384;    // power-of-two chunk of the multi-pass path
+static_assert(kSortChunk == 1 << 14 && kSortChunk <= kSortBigCap, "chunk fits the buffer");
 
 // Rows longer than kSortWarpCap: one CTA per row.  <= kSortBigCap sorts in
 // shared memory; longer rows run the same network over global memory with
-// the inner (j < kSortBigCap) steps done in shared memory per chunk.
+// the inner (j < kSortChunk) steps done in shared memory per chunk.  (Zipf
+// clusters give cfg4 rows with tens of thousands of matches.)
 __global__ void __launch_bounds__(kSortBigThreads)
 segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ keys,
                    uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
@@ -347,8 +350,12 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
       continue;
     }
     int64_t P = 1;
-    while (P < n) P <<= 1;
-    const int C = kSortBigCap;
+    int lp = 0;
+    while (P < n) {
+      P <<= 1;
+      lp++;
+    }
+    const int C = kSortChunk, lc = 14;  // 1 << 14 == kSortChunk
     // 1) sort every C-chunk (all stages k <= C) in shared memory
     for (int64_t c0 = 0; c0 < n; c0 += C) {
       const int m = (int)mn<int64_t>(C, n - c0);
@@ -358,19 +365,22 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
       for (int t = threadIdx.x; t < m; t += blockDim.x) g[c0 + t] = sbuf[t];
       __syncthreads();
     }
-    // 2) stages k > C: mirror + large-j steps in global, small-j steps per chunk
-    for (int64_t k = 2 * (int64_t)C; k <= P; k <<= 1) {
-      for (int64_t j = k / 2; j >= C; j >>= 1) {
-        const bool mirror = (j == k / 2);
+    // 2) stages k > C: mirror + large-j steps in global, small-j steps per
+    //    chunk (k, j powers of two: block/offset by shift and mask)
+    for (int lk = lc + 1; lk <= lp; lk++) {
+      const int64_t k = (int64_t)1 << lk;
+      for (int lj = lk - 1; lj >= lc; lj--) {
+        const int64_t j = (int64_t)1 << lj;
+        const bool mirror = (lj == lk - 1);
         for (int64_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
           int64_t a, b;
           if (mirror) {
-            const int64_t blk = t / (k / 2), off = t % (k / 2);
-            a = blk * k + off;
-            b = blk * k + k - 1 - off;
+            const int64_t blk = t >> (lk - 1), off = t & ((k >> 1) - 1);
+            a = (blk << lk) + off;
+            b = (blk << lk) + k - 1 - off;
           } else {
-            const int64_t blk = t / j, off = t % j;
-            a = blk * 2 * j + off;
+            const int64_t blk = t >> lj, off = t & (j - 1);
+            a = (blk << (lj + 1)) + off;
             b = a + j;
           }
           if (b < n) {
@@ -387,10 +397,11 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
         const int m = (int)mn<int64_t>(C, n - c0);
         for (int t = threadIdx.x; t < m; t += blockDim.x) sbuf[t] = g[c0 + t];
         __syncthreads();
-        for (int j = C / 2; j >= 1; j >>= 1) {
+        for (int lj = lc - 1; lj >= 0; lj--) {
+          const int j = 1 << lj;
           for (int t = threadIdx.x; t < C / 2; t += blockDim.x) {
-            const int blk = t / j, off = t % j;
-            const int a = blk * 2 * j + off, b = a + j;
+            const int blk = t >> lj, off = t & (j - 1);
+            const int a = (blk << (lj + 1)) + off, b = a + j;
             if (b < m) cmpx(sbuf, a, b);
           }
           __syncthreads();

@@ -354,22 +354,26 @@ def test_overflow_retry_is_exact(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), golden["c_small_s"].view(np.uint32))
 
 
-def test_all_pairs_large_rows(cuda):
-    """theta = -1: every pair matches; rows longer than the warp and CTA sort
-    capacities (1024 / 8192) go through the large-row sort paths."""
+@pytest.mark.parametrize("nr", [3000, 20000, 70000])
+def test_all_pairs_large_rows(cuda, nr):
+    """theta = -1: every pair matches; rows longer than the warp sort (1024)
+    go to the CTA sort -- whole in shared memory up to 26624 keys, the
+    multi-pass global network beyond (70000: stages up to 2^17)."""
     from paper_2312_01476_b200 import device as D
     rng = np.random.default_rng(5)
     L = rng.standard_normal((3, 16), dtype=np.float32)
-    S = rng.standard_normal((20000, 16), dtype=np.float32)
+    S = rng.standard_normal((nr, 16), dtype=np.float32)
     m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
                         D.prepare(torch.from_numpy(S).to(cuda)), -1.0)
     lo, ro, so = m.to_host()
-    assert len(lo) == 3 * 20000
-    assert np.array_equal(lo, np.repeat(np.arange(3, dtype=np.uint64), 20000))
-    assert np.array_equal(ro, np.tile(np.arange(20000, dtype=np.uint64), 3))
+    assert len(lo) == 3 * nr
+    assert np.array_equal(lo, np.repeat(np.arange(3, dtype=np.uint64), nr))
+    assert np.array_equal(ro, np.tile(np.arange(nr, dtype=np.uint64), 3))
     Ln, _ = O.normalize_rows(L)
     Sn, _ = O.normalize_rows(S)
-    assert np.array_equal(so[:20000].view(np.uint32), O.dots_vm(Ln[0], Sn).view(np.uint32))
+    for r in range(3):
+        assert np.array_equal(so[r * nr:(r + 1) * nr].view(np.uint32),
+                              O.dots_vm(Ln[r], Sn).view(np.uint32))
 
 
 def test_empty_and_errors(cuda):

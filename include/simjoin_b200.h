@@ -41,19 +41,19 @@ int sjb_sm_count(int device);
  * threads); lets callers count the GPU launches inside a timed region. */
 int64_t sjb_launch_count(void);
 
-/* Padded reduction depth of the bf16 operand image for `dim`: a multiple of
+/* Padded reduction depth of the fp16 operand image for `dim`: a multiple of
  * 16 for dim <= 128, of 64 above (K-streaming kernel). */
 int64_t sjb_kpad(int64_t dim);
-/* Elements of the bf16 operand image of an n-row relation: n rounded up to a
+/* Elements of the fp16 operand image of an n-row relation: n rounded up to a
  * multiple of 512 rows, times kpad.  Layout: 256-row tiles, each
  * [k-group (kpad/8)][row (256)][8 elements] (UMMA K-major, no swizzle). */
 int64_t sjb_operand_elems(int64_t n, int64_t dim);
 /* 256-row tiles of that image (= entries of a d_tile_err array). */
 int64_t sjb_tile_count(int64_t n);
 
-/* bf16 rounding-error outputs of the prep functions below (both optional,
+/* fp16 rounding-error outputs of the prep functions below (both optional,
  * written only together with d_out16):
- *   d_row_err[i]  (n floats)  >= ||bf16(x_i) - x_i||_2 of canonical row x_i
+ *   d_row_err[i]  (n floats)  >= ||fp16(x_i) - x_i||_2 of canonical row x_i
  *   d_tile_err[t] (sjb_tile_count(n) floats) = max of d_row_err over tile t
  * They let the join use a per-row filter band (sjb_join_args.left_row_err /
  * right_tile_err) instead of the worst-case sjb_default_band. */
@@ -64,7 +64,7 @@ int64_t sjb_tile_count(int64_t n);
  * (_kernelcore.h:8, _kernelcore.c:79-114): fp64 sequential sum of squares,
  * zero rows repaired (component 0 := 1), fp64 divide, fp32 store.
  * d_in may equal d_out32 (in place).  d_out16 (optional, may be NULL) gets the
- * bf16 operand image (sjb_operand_elems elements).  *d_repaired (optional
+ * fp16 operand image (sjb_operand_elems elements).  *d_repaired (optional
  * device u64) is incremented by the number of repaired rows. */
 int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32,
                        void* d_out16, unsigned long long* d_repaired, float* d_row_err,
@@ -96,7 +96,7 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
 /* FastText-style subword model (cfg3; no reference counterpart, see
  * DESIGN.md): row = mean of table rows of the word hash and every
  * minn..maxn-gram of '<'w'>' (fnv1a64 mod n_buckets).  normalize != 0 also
- * applies sjb_normalize_rows and writes the bf16 image (d_out16 optional). */
+ * applies sjb_normalize_rows and writes the fp16 image (d_out16 optional). */
 int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
                       const float* d_table, int64_t n_buckets, int64_t dim, int minn,
                       int maxn, int normalize, float* d_out32, void* d_out16,
@@ -108,7 +108,7 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
 typedef struct sjb_join_args {
   int64_t n_left, n_right, dim;
   float theta;          /* inclusive: a pair matches iff canonical sim >= theta */
-  float band;           /* bf16 filter margin; candidates have approx >= theta - band */
+  float band;           /* fp16 filter margin; candidates have approx >= theta - band */
   int64_t cand_cap;     /* candidate buffer entries (workspace) */
   int64_t out_cap;      /* capacity of lefts/rights/sims */
   uint64_t left_base;   /* added to emitted left offsets (R shards) */
@@ -120,7 +120,7 @@ typedef struct sjb_join_args {
    * and the right relation's d_tile_err from the prep functions.  Row i of
    * S tile t then keeps pairs with approx >= max(theta - band,
    * theta - b_it), b_it = slack + (1+1e-6)(e_i + E_t) + e_i E_t,
-   * slack = sjb_accum_slack(dim): Cauchy-Schwarz on the measured bf16
+   * slack = sjb_accum_slack(dim): Cauchy-Schwarz on the measured fp16
    * rounding errors, so no true match is dropped. */
   const float* left_row_err;
   const float* right_tile_err;
@@ -142,7 +142,7 @@ typedef struct sjb_join_info {
 /* Workspace bytes needed by sjb_join_prepared for these args. */
 int64_t sjb_join_workspace_bytes(const sjb_join_args* args);
 
-/* Default (provably sufficient) band for `dim`: bf16 rounding of unit
+/* Default (provably sufficient) band for `dim`: fp16 rounding of unit
  * vectors (2u+u^2, u = 2^-8) plus fp32 accumulation slack. */
 float sjb_default_band(int64_t dim);
 /* The accumulation part of that band (+ 1e-6 for the fp32 cutoff
@@ -150,7 +150,7 @@ float sjb_default_band(int64_t dim);
 float sjb_accum_slack(int64_t dim);
 
 /* Join two prepared (normalised) relations on the device; asynchronous.
- * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: bf16 operand images.
+ * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: fp16 operand images.
  * Replaces tensor_join's tile loop (join.py:338-359: tile_similarity +
  * threshold_scan + MatchSink.merge) with filter -> canonical recheck ->
  * row bucketing -> per-row sort.  Writes the canonical MatchSet columns to

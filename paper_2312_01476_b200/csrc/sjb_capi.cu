@@ -303,7 +303,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// The bf16 operand image (sjb_operand_elems elements, 256-row tiles of
+// The fp16 operand image (sjb_operand_elems elements, 256-row tiles of
 // [k-group][row][8]) as a 3-D tensor (256 elements = 32 rows x 8, 8 row
 // blocks, kgroups * tiles); box {256, box_rows/32, kgroups} = one
 // [k-group][box_rows][8] block.  The 512 B inner extent keeps every request
@@ -320,7 +320,7 @@ int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad,
   const cuuint64_t strides[2] = {512, (cuuint64_t)sjb::kTileRows * 16};
   const cuuint32_t box[3] = {256, (cuuint32_t)box_rows / 32, (cuuint32_t)kgroups};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(image), dims,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(image), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -447,11 +447,14 @@ int64_t sjb_operand_elems(int64_t n, int64_t dim) {
 }
 
 float sjb_default_band(int64_t dim) {
-  // |cos_bf16 - cos_fp32| <= (2u + u^2) * sum|a_i b_i| <= 2u + u^2 for unit
-  // vectors (u = 2^-8), plus fp32 accumulation error of both the tensor-core
-  // sum and the canonical sequential sum (<= 2 * dim * 2^-24 each, generous).
-  const double u = 1.0 / 256.0;
-  const double b = 2 * u + u * u + 4.0 * (double)dim * 5.9604644775390625e-08 + 1e-6;
+  // fp16 operands: |fp16(x) - x| <= u|x| + 2^-25 per component (u = 2^-11;
+  // the 2^-25 covers fp16 subnormals), so ||e_x|| <= e = u + 2^-25 sqrt(dim)
+  // for a unit row, and by Cauchy-Schwarz |approx - exact| <= 2e(1 + 1e-6) +
+  // e^2; plus fp32 accumulation error of both the tensor-core sum and the
+  // canonical sequential sum (<= 2 * dim * 2^-24 each, generous).
+  const double u = 1.0 / 2048.0;
+  const double e = u + 2.98023223876953125e-08 * sqrt((double)dim);
+  const double b = 2 * e * (1 + 1e-6) + e * e + 4.0 * (double)dim * 5.9604644775390625e-08 + 1e-6;
   return (float)b;
 }
 
@@ -478,7 +481,7 @@ static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n,
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
   sjb::normalize_cast_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
-      d_in, d_gather, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16),
+      d_in, d_gather, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<sjb::op16_t*>(d_out16),
       d_repaired, 1, d_out16 ? d_row_err : nullptr, d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("normalize_cast");
   return SJB_OK;
@@ -528,7 +531,7 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::synthetic_fill_kernel, smem)) return rc;
   sjb::synthetic_fill_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
-      d_seeds, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<__nv_bfloat16*>(d_out16),
+      d_seeds, n, (int)dim, kpad, sub, d_out32, reinterpret_cast<sjb::op16_t*>(d_out16),
       d_out16 ? d_row_err : nullptr, d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("synthetic_fill");
   return SJB_OK;
@@ -550,7 +553,7 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
   if (int rc = set_smem_attr((const void*)sjb::subword_embed_kernel, smem)) return rc;
   sjb::subword_embed_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
       d_bytes, d_offs, n, d_table, n_buckets, (int)dim, kpad, sub, minn, maxn, normalize, d_out32,
-      normalize ? reinterpret_cast<__nv_bfloat16*>(d_out16) : nullptr, d_repaired,
+      normalize ? reinterpret_cast<sjb::op16_t*>(d_out16) : nullptr, d_repaired,
       normalize && d_out16 ? d_row_err : nullptr, normalize && d_out16 ? d_tile_err : nullptr);
   SJB_CK_LAUNCH("subword_embed");
   return SJB_OK;
@@ -672,8 +675,8 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   }
 
   sjb::JoinParams jp;
-  jp.a16 = reinterpret_cast<const __nv_bfloat16*>(d_l16);
-  jp.b16 = reinterpret_cast<const __nv_bfloat16*>(d_r16);
+  jp.a16 = reinterpret_cast<const sjb::op16_t*>(d_l16);
+  jp.b16 = reinterpret_cast<const sjb::op16_t*>(d_r16);
   jp.n_a = nl;
   jp.n_b = nr;
   jp.kpad = pl.kpad;

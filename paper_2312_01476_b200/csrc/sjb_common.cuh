@@ -6,10 +6,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace sjb {
 
-// Rows per bf16 operand tile.  Both relations are stored as a sequence of
+// 16-bit tensor-core operand: fp16.  Rows are unit vectors, far inside
+// fp16's range, and its 11-bit significand rounds 8x finer than bf16's 8 at
+// the same UMMA throughput, so the filter band (and the candidates that only
+// the band admits) shrinks accordingly.
+using op16_t = __half;
+__device__ __forceinline__ op16_t to_op16(float x) { return __float2half_rn(x); }
+__device__ __forceinline__ float from_op16(op16_t h) { return __half2float(h); }
+
+
+// Rows per fp16 operand tile.  Both relations are stored as a sequence of
 // 256-row tiles in the UMMA canonical K-major no-swizzle layout
 // ([k-group of 8 elements][row][8 elements], 16 B core-matrix rows), so one
 // 1-D bulk copy moves a whole tile into shared memory and the tensor core
@@ -20,7 +30,7 @@ constexpr int kTileRows = 256;
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
-// Element offset of (row, k) inside the tiled bf16 image of a relation with
+// Element offset of (row, k) inside the tiled fp16 image of a relation with
 // `kpad` padded columns.
 __host__ __device__ inline int64_t tiled_offset(int64_t row, int64_t k, int64_t kpad) {
   int64_t t = row / kTileRows, r = row % kTileRows;
@@ -131,8 +141,8 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate).
-__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (fp16 in, fp32 accumulate).
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -143,7 +153,7 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, ui
 }
 // Warp-uniform variants: the whole warp executes the call, one elected lane
 // issues (keeps descriptors in uniform registers; no per-MMA ELECT loop).
-__device__ __forceinline__ void tc_mma_bf16_elect(uint32_t d_tmem, uint64_t a_desc,
+__device__ __forceinline__ void tc_mma_f16_elect(uint32_t d_tmem, uint64_t a_desc,
                                                   uint64_t b_desc, uint32_t idesc,
                                                   uint32_t accumulate) {
   asm volatile(
@@ -197,11 +207,11 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor_noswz(uint32_t smem_addr, u
   return d;
 }
 
-// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(int M, int N) {
+// Instruction descriptor: kind::f16, A=B=f16, D=f32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16_f32(int M, int N) {
   return (1u << 4)                      // D format f32
-         | (1u << 7)                    // A format bf16
-         | (1u << 10)                   // B format bf16
+         | (0u << 7)                    // A format f16
+         | (0u << 10)                   // B format f16
          | (uint32_t(N >> 3) << 17)     // N / 8
          | (uint32_t(M >> 4) << 24);    // M / 16
 }
@@ -292,7 +302,7 @@ constexpr uint64_t kEmptySlot = ~0ull;         // candidate slot not yet written
 // Filter cutoff of R row i against the 256-row S tile t256.  Without error
 // arrays: the uniform theta - band.  With them:
 // |approx - canonical| <= slack + (1+1e-6)(e_i + E_t) + e_i E_t, where e_i
-// bounds ||bf16(x_i) - x_i|| and E_t the same over the S tile (Cauchy-Schwarz
+// bounds ||fp16(x_i) - x_i|| and E_t the same over the S tile (Cauchy-Schwarz
 // on the rounding errors; slack covers both fp32 accumulations and this fp32
 // evaluation), so the cutoff can be raised to theta minus that bound.
 __device__ __forceinline__ float row_cutoff(float cutoff, float theta, float slack,

@@ -6,7 +6,7 @@
 // materialises the similarity matrix:
 //
 //   warp 0       S producer: 1-D bulk copies (TMA, cp.async.bulk) of pre-tiled
-//                bf16 operand tiles into a shared-memory ring (mbarriers)
+//                fp16 operand tiles into a shared-memory ring (mbarriers)
 //   warp 0 ln 1  R-block producer (resident operand, one copy per item)
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17  epilogue: tcgen05.ld of the fp32 accumulators, 3-input max
@@ -24,7 +24,7 @@
 // N <= 128 saturates it).  Items are ordered S-chunk-major so the CTAs
 // resident at any moment share one S chunk in L2.
 //
-// Output: candidate pairs (i, j) with bf16 approx >= cutoff, packed as
+// Output: candidate pairs (i, j) with fp16 approx >= cutoff, packed as
 // u64 (i << 32 | j) into per-CTA segments of `cand` (seg_cap each), counted in
 // a shared-memory counter and published in cta_count[blockIdx.x].  A CTA
 // whose segment overflows keeps counting, so the host can retry with the
@@ -50,8 +50,8 @@ constexpr int kBN = kTileRows;  // S rows per stage == UMMA N
 constexpr int kUmmaN = 256;
 
 struct JoinParams {
-  const __nv_bfloat16* a16;  // R operand image, n_ablk tiles
-  const __nv_bfloat16* b16;  // S operand image, n_btiles tiles
+  const op16_t* a16;  // R operand image, n_ablk tiles
+  const op16_t* b16;  // S operand image, n_btiles tiles
   int64_t n_a, n_b;          // valid rows
   int kpad;                  // padded K (multiple of 16, <= 128)
   int n_ablk;                // ceil(n_a / 256)
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       // whole warp, warp-uniform control flow; one elected lane issues each
       // tcgen05 op (a single divergent lane costs an ELECT/R2UR sequence
       // per MMA and made the issue the critical path)
-      const uint32_t idesc = umma_idesc_bf16_f32(128, kUmmaN);
+      const uint32_t idesc = umma_idesc_f16_f32(128, kUmmaN);
       const uint32_t lbo = kTileRows * 16;  // 256-row operand: distance between k-groups
       const uint32_t sbo = 128;             // distance between 8-row core-matrix groups
       // a k-step advances the start address by 2 k-groups = 2 * lbo bytes;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
             const uint64_t adh = ad + h * half_step;
 #pragma unroll
             for (int kk = 0; kk < KSTEPS; kk++)
-              tc_mma_bf16_elect(d, adh + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
+              tc_mma_f16_elect(d, adh + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
             tc_commit_elect(&acc_full[as]);
             acc_it++;
           }

@@ -1,6 +1,6 @@
 // sjb_join2.cu -- the fused threshold filter on CTA PAIRS (cta_group::2).
 //
-// Same contract as sjb_join.cu (candidates with bf16 approx >= cutoff into
+// Same contract as sjb_join.cu (candidates with fp16 approx >= cutoff into
 // per-CTA segments, fused canonical recheck), organised for a 2-SM pair:
 //
 //   * Each CTA keeps its own 256-row R block resident (two M=128 halves);
@@ -64,8 +64,8 @@ constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a pai
 struct alignas(64) Params {
   CUtensorMap tmap_a;        // R image as (8, 256, kgroups * tiles), box {8, 256, kgroups}
   CUtensorMap tmap_b;        // S image, box {8, 64, kgroups}
-  const __nv_bfloat16* a16;  // R operand image (256-row tiles)
-  const __nv_bfloat16* b16;  // S operand image (256-row tiles)
+  const op16_t* a16;  // R operand image (256-row tiles)
+  const op16_t* b16;  // S operand image (256-row tiles)
   int64_t n_a, n_b;
   int kpad;
   int n_ablk;        // ceil(n_a / 512): pair R blocks
@@ -280,7 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader) {  // the whole warp runs the issue loop; mma2/commit2 elect one lane
       // ---------------------------------------------- MMA issuer (pair)
-      const uint32_t idesc = umma_idesc_bf16_f32(256, kUmmaN);
+      const uint32_t idesc = umma_idesc_f16_f32(256, kUmmaN);
       const uint32_t a_lbo = kARows * 16;   // A: 256-row block, k-group stride
       const uint32_t b_lbo = kHalfN * 16;   // B: 64-row slab, k-group stride
       const uint32_t sbo = 128;

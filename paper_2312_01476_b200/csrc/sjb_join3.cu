@@ -42,8 +42,8 @@ constexpr int kKChunk = 64;                           // K elements per stage
 constexpr int kChunkBytes = kTileRows * kKChunk * 2;  // 32 KB per operand
 
 struct Params {
-  const __nv_bfloat16* a16;
-  const __nv_bfloat16* b16;
+  const op16_t* a16;
+  const op16_t* b16;
   int64_t n_a, n_b;
   int kpad;              // multiple of 64
   int n_ablk, n_btiles;  // 256-row blocks / tiles
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer
     // whole warp, warp-uniform; one elected lane issues (lean issue)
-    const uint32_t idesc = umma_idesc_bf16_f32(128, 256);
+    const uint32_t idesc = umma_idesc_f16_f32(128, 256);
     const uint32_t lbo = kTileRows * 16, sbo = 128;
     const uint64_t kstep = (2 * lbo) >> 4, half_step = (128 * 16) >> 4;
     const uint64_t ring_desc = umma_desc_kmajor_noswz(smem_u32(ring), lbo, sbo);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
             }
 #pragma unroll
             for (int kk = 0; kk < kKChunk / 16; kk++)
-              tc_mma_bf16_elect(tmem_base + h * 256, ad + h * half_step + kk * kstep,
+              tc_mma_f16_elect(tmem_base + h * 256, ad + h * half_step + kk * kstep,
                                 bd + kk * kstep, idesc, (c | kk) ? 1u : 0u);
           }
           tc_commit_elect(&empty[s]);

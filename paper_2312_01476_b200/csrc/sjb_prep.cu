@@ -5,7 +5,7 @@
 // canonical arithmetic, then writes
 //   * the canonical fp32 rows (bitwise equal to the reference's
 //     sj_normalize_rows, _kernelcore.c:79-114), and
-//   * optionally the bf16 copy in the tiled UMMA operand layout
+//   * optionally the fp16 copy in the tiled UMMA operand layout
 //     (sjb_common.cuh tiled_offset), zero-padded to kpad columns.
 #include "sjb_common.cuh"
 
@@ -16,8 +16,8 @@ constexpr int kPrepThreads = 128;
 // Sequential fp64 sum of squares (no contraction: the square is exact and
 // __dadd_rn pins the rounding), repair rule, fp64 divide -- the reference's
 // normalize_row (_kernelcore.c:79-97).  Operates on one smem row.
-// With `err` != nullptr the same final pass also measures the row's bf16
-// rounding error ||bf16(x) - x||_2 (exact squares, fp64 sum, rounded up): the
+// With `err` != nullptr the same final pass also measures the row's fp16
+// rounding error ||fp16(x) - x||_2 (exact squares, fp64 sum, rounded up): the
 // per-row term of the filter band (sjb_common.cuh row_cutoff).
 __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* err) {
   double ss = 0.0;
@@ -44,7 +44,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
     for (int d = 0; d < dim; d++) {
       const float x = __double2float_rn(__ddiv_rn((double)row[d], norm));
       row[d] = x;
-      const double e = (double)__bfloat162float(__float2bfloat16_rn(x)) - (double)x;
+      const double e = (double)from_op16(to_op16(x)) - (double)x;
       es = __dadd_rn(es, __dmul_rn(e, e));
     }
     *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
@@ -54,7 +54,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
 
 // Common tail: normalise the rows staged in `sm` (pitch floats apart) for the
 // sub-tile [r0, r0 + sub) of the 256-row tile starting at row0 (`rows` valid
-// rows in the whole tile), store fp32 rows and that slice of the bf16
+// rows in the whole tile), store fp32 rows and that slice of the fp16
 // operand tile.
 // Rounding-error outputs of a tile: row_err[i] per row, tile_err[tile] = the
 // tile's maximum (accumulated in the shared `tile_max`, written by the caller).
@@ -65,7 +65,7 @@ struct ErrOut {
 
 __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, int dim, int kpad,
                                int64_t row0, bool normalize, float* __restrict__ out32,
-                               __nv_bfloat16* __restrict__ out16,
+                               op16_t* __restrict__ out16,
                                unsigned long long* __restrict__ repaired, ErrOut eo) {
   const int vrows = max(0, min(sub, rows - r0));  // valid rows in this sub-tile
   int rep = 0;
@@ -97,12 +97,12 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
     const int nchunks = sub * (kpad / 8);
     for (int c = threadIdx.x; c < nchunks; c += kPrepThreads) {
       int g = c / sub, r = c - g * sub;
-      __align__(16) __nv_bfloat16 v[8];
+      __align__(16) op16_t v[8];
 #pragma unroll
       for (int e = 0; e < 8; e++) {
         int k = g * 8 + e;
         float x = (r < vrows && k < dim) ? sm[r * pitch + k] : 0.0f;
-        v[e] = __float2bfloat16_rn(x);
+        v[e] = to_op16(x);
       }
       dst[g * kTileRows + r0 + r] = *reinterpret_cast<uint4*>(v);
     }
@@ -113,11 +113,11 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
 // in: n x dim fp32 row-major (or, with `gather`, a table whose row gather[i]
 // is relation row i).  One CTA per 256-row operand tile, staged in sub-tiles
 // of `sub` rows (sub * (dim|1) floats of smem).  The grid may cover tiles past
-// n: those are written as zero operand tiles so the bf16 image can be padded.
+// n: those are written as zero operand tiles so the fp16 image can be padded.
 __global__ void __launch_bounds__(kPrepThreads)
 normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ gather, int64_t n,
                       int dim, int kpad, int sub, float* __restrict__ out32,
-                      __nv_bfloat16* __restrict__ out16, unsigned long long* __restrict__ repaired,
+                      op16_t* __restrict__ out16, unsigned long long* __restrict__ repaired,
                       int normalize, float* __restrict__ row_err, float* __restrict__ tile_err) {
   extern __shared__ float sm[];
   __shared__ unsigned tile_max;
@@ -161,7 +161,7 @@ __device__ __forceinline__ float splitmix_elem(uint64_t seed, int d) {
 
 __global__ void __launch_bounds__(kPrepThreads)
 synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, int kpad, int sub,
-                      float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
+                      float* __restrict__ out32, op16_t* __restrict__ out16,
                       float* __restrict__ row_err, float* __restrict__ tile_err) {
   extern __shared__ float sm[];
   __shared__ unsigned tile_max;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kPrepThreads)
 subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
                      int64_t n, const float* __restrict__ table, int64_t n_buckets, int dim,
                      int kpad, int sub, int minn, int maxn, int normalize,
-                     float* __restrict__ out32, __nv_bfloat16* __restrict__ out16,
+                     float* __restrict__ out32, op16_t* __restrict__ out16,
                      unsigned long long* __restrict__ repaired, float* __restrict__ row_err,
                      float* __restrict__ tile_err) {
   extern __shared__ float sm[];

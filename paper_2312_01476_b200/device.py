@@ -8,7 +8,7 @@ or without the built library these functions raise.
 Pipeline of one join:
 
   prepare(raw)         normalize_cast kernel: canonical fp32 rows (bitwise
-                       sj_normalize_rows) + bf16 operand image (tiled layout)
+                       sj_normalize_rows) + fp16 operand image (tiled layout)
   join_prepared(L, R)  tcgen05 filter (approx >= theta - band) -> canonical
                        fp32 recheck -> row bucketing -> per-row sort ->
                        MatchSet columns (u64 lefts, u64 rights, f32 sims)
@@ -64,8 +64,8 @@ def operand_elems(n: int, dim: int) -> int:
 
 
 def default_band(dim: int) -> float:
-    """Provably sufficient bf16 filter margin for unit vectors (C ABI
-    sjb_default_band): (2u + u^2) + accumulation slack, u = 2^-8."""
+    """Provably sufficient fp16 filter margin for unit vectors (C ABI
+    sjb_default_band): 2e + e^2 + accumulation slack, e = 2^-11 + 2^-25 sqrt(d)."""
     return float(_lib.lib().sjb_default_band(dim))
 
 
@@ -74,13 +74,13 @@ class PreparedRelation:
     """A relation resident in HBM in the two forms the join reads."""
 
     f32: torch.Tensor          # (n, dim) canonical normalised fp32 rows
-    op: torch.Tensor           # bf16 operand image (sjb_operand_elems elements)
+    op: torch.Tensor           # fp16 operand image (sjb_operand_elems elements)
     n: int
     dim: int
     name: str = ""
     repaired_dev: Optional[torch.Tensor] = None  # (1,) int64 repaired-row counter
-    # bf16 rounding errors (sjb_join_args.left_row_err / right_tile_err):
-    row_err: Optional[torch.Tensor] = None       # (n,) >= ||bf16(x_i) - x_i||
+    # fp16 rounding errors (sjb_join_args.left_row_err / right_tile_err):
+    row_err: Optional[torch.Tensor] = None       # (n,) >= ||fp16(x_i) - x_i||
     tile_err: Optional[torch.Tensor] = None      # (tiles,) max over each 256-row tile
 
     @property
@@ -111,13 +111,13 @@ def _check_matrix(x: torch.Tensor, what: str) -> None:
 
 def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = None
             ) -> PreparedRelation:
-    """Normalise rows (bitwise sj_normalize_rows) and build the bf16 image."""
+    """Normalise rows (bitwise sj_normalize_rows) and build the fp16 image."""
     _check_matrix(raw, "relation")
     L = _lib.lib()
     n, dim = raw.shape
     dev = raw.device
     f32 = out32 if out32 is not None else torch.empty_like(raw)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
@@ -218,7 +218,7 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
 
     Blocks once at the end to read the match count (the output size is data
     dependent); everything else is asynchronous on the current stream.
-    per_row_band: when both relations carry their bf16 rounding errors, filter
+    per_row_band: when both relations carry their fp16 rounding errors, filter
     with the per-row band (never looser than `band`; same result, fewer
     candidates to recheck).
     """
@@ -329,7 +329,7 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     must make rows [r0, r1) of it ready on the current stream (wait for a
     copy or a broadcast) -- it is called in row order, on 512-row boundaries.
     Each chunk is then normalised (canonical fp32 rows + its tiles of the
-    bf16 image + rounding errors; in place when `inplace`) and its S tiles
+    fp16 image + rounding errors; in place when `inplace`) and its S tiles
     are filtered at once (sjb_join_begin / sjb_join_filter_tiles /
     sjb_join_finish), so the filter overlaps the arrival of later chunks.
     Same result as prepare + join_prepared.  Returns the matches and the
@@ -345,7 +345,7 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     with _cap_lock:
         cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, n))
     f32 = raw if inplace else torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     R = PreparedRelation(f32, op, n, dim, name, rep, re, te)
@@ -439,7 +439,7 @@ def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> 
     n, dim = int(index.numel()), table.shape[1]
     dev = table.device
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
@@ -500,13 +500,13 @@ def synthetic_rows(seeds: torch.Tensor, dim: int) -> torch.Tensor:
 def subword_rows(tokens, table: torch.Tensor, minn: int, maxn: int,
                  prepared: bool = False, name: str = ""):
     """Subword-model rows; prepared=True returns a PreparedRelation (embed +
-    normalise + bf16 image in one kernel), else the raw (n, dim) embedding."""
+    normalise + fp16 image in one kernel), else the raw (n, dim) embedding."""
     _check_matrix(table, "bucket table")
     dev = table.device
     b, o = pack_tokens(tokens, dev)
     n, dim = len(tokens), table.shape[1]
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev) if prepared else None
+    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev) if prepared else None
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev) if prepared else (None, None)
     with torch.cuda.device(dev):

@@ -21,7 +21,7 @@ def _bits_equal(ms, lo, ro, so):
 
 
 def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
-    """Rebuild the row-major bf16 matrix from the tiled operand image."""
+    """Rebuild the row-major fp16 matrix from the tiled operand image."""
     from paper_2312_01476_b200 import device as D
     kpad = D.kpad(dim)
     a = op.view(torch.int16).cpu().numpy()
@@ -44,7 +44,7 @@ def test_normalize_and_operand_image(cuda, dim):
     assert np.array_equal(p.f32.cpu().numpy().view(np.uint32), want.view(np.uint32))
     assert p.repaired() == rep == 2
     rows, full = _decode_operand(p.op, n, dim)
-    bf = torch.from_numpy(want).to(torch.bfloat16).view(torch.int16).numpy()
+    bf = torch.from_numpy(want).to(torch.float16).view(torch.int16).numpy()
     kpad = full.shape[1]
     assert np.array_equal(rows[:, :dim], bf)
     assert (rows[:, dim:] == 0).all() and (full[n:] == 0).all()
@@ -176,7 +176,7 @@ def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
 
 @pytest.mark.parametrize("dim", [3, 100, 768])
 def test_rounding_error_outputs(cuda, dim):
-    """row_err bounds ||bf16(x) - x|| from above (tightly); tile_err is the
+    """row_err bounds ||fp16(x) - x|| from above (tightly); tile_err is the
     per-256-row-tile maximum (zero for padding tiles)."""
     from paper_2312_01476_b200 import device as D
     rng = np.random.default_rng(dim + 5)
@@ -185,7 +185,7 @@ def test_rounding_error_outputs(cuda, dim):
     x[9] = 0.0
     p = D.prepare(torch.from_numpy(x).to(cuda))
     f = p.f32.cpu().numpy()
-    bf = torch.from_numpy(f).to(torch.bfloat16).to(torch.float64).numpy()
+    bf = torch.from_numpy(f).to(torch.float16).to(torch.float64).numpy()
     want = np.sqrt(((bf - f.astype(np.float64)) ** 2).sum(axis=1))
     got = p.row_err.cpu().numpy().astype(np.float64)[:n]
     assert (got >= want).all() and (got <= want * (1 + 1e-6) + 1e-30).all()

@@ -105,8 +105,12 @@ def test_c_abi_exports_every_declared_symbol():
     assert L.sjb_version() == 1
     assert L.sjb_kpad(100) == 112 and L.sjb_kpad(4) == 16
     assert L.sjb_operand_elems(300, 100) == 512 * 112
+    # fp16 operands: 2e + e^2 + 4 d 2^-24 + 1e-6, e = 2^-11 + 2^-25 sqrt(d)
+    e = 2.0 ** -11 + 2.0 ** -25 * 10.0
+    want = 2 * e * (1 + 1e-6) + e * e + 4 * 100 * 2.0 ** -24 + 1e-6
     band = L.sjb_default_band(100)
-    assert 0.0078 < band < 0.0081
+    assert abs(band - want) < 1e-9 and 0.00099 < band < 0.00101
+    assert abs(L.sjb_accum_slack(100) - (4 * 100 * 2.0 ** -24 + 2e-6)) < 1e-9
 
 
 def test_no_oracle_in_product():

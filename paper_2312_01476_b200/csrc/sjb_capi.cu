@@ -769,6 +769,10 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         rp.theta = args->theta;
         rp.sims_bits = c.sims_bits;
         rp.rowcount = c.rowcount;
+        {
+          const char* dm = getenv("SJB_WIDE_DIRECT_MAX");
+          rp.direct_max = dm ? (uint32_t)atoi(dm) : (uint32_t)sjb::wide::kRcDirect;
+        }
         if ((args->dim & 3) == 0) {
           sjb::wide::RecheckTmaParams tp;
           tp.b = rp;

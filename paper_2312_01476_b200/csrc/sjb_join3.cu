@@ -300,6 +300,7 @@ struct RecheckParams {
   float theta;
   uint32_t* sims_bits;
   uint32_t* rowcount;
+  uint32_t direct_max;  // tiles with fewer candidates gather instead of staging
 };
 
 __device__ __forceinline__ void cp_async16(float* dst, const float* src) {
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kRcThreads, 1) recheck_generic_kernel(const Re
       const uint32_t lo = toff[k], hi = toff[k + 1];
       if (hi <= lo) continue;
       const uint32_t n = hi - lo;
-      if (n < kRcDirect) {
+      if (n < p.direct_max) {
         // ------------------------------------------------ direct gathers
         for (uint32_t s = lo + threadIdx.x; s < hi; s += kRcThreads) {
           const uint64_t u = seg[s];
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       for (int64_t t = t0; t < t1; t++, k++) {
         const uint32_t lo = toff[k], hi = toff[k + 1];
-        if (hi <= lo || hi - lo < (uint32_t)kRcDirect) continue;
+        if (hi <= lo || hi - lo < p.direct_max) continue;
         for (uint32_t pb = lo; pb < hi; pb += kRtPass) {
           for (int ch = 0; ch < nch; ch++) {
             mbar_wait(&empty[s], ph ^ 1u);
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     for (int64_t t = t0; t < t1; t++, k++) {
       const uint32_t lo = toff[k], hi = toff[k + 1];
       if (hi <= lo) continue;
-      if (hi - lo < (uint32_t)kRcDirect) {
+      if (hi - lo < p.direct_max) {
         for (uint32_t q = lo + ct; q < hi; q += kCT) {
           const uint64_t u = seg[q];
           const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;

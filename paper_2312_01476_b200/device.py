@@ -90,6 +90,18 @@ class PreparedRelation:
     def repaired(self) -> int:
         return int(self.repaired_dev.item()) if self.repaired_dev is not None else 0
 
+    def rows(self, r0: int, r1: int) -> "PreparedRelation":
+        """Rows [r0, r1) as a prepared relation (views, no copy); r0 must sit
+        on a 512-row boundary (an operand tile pair)."""
+        if r0 % (2 * TILE_ROWS) or not 0 <= r0 <= r1 <= self.n:
+            raise ValueError(f"bad row range [{r0}, {r1}) of {self.n}")
+        kp = kpad(self.dim)
+        t0 = r0 // TILE_ROWS
+        return PreparedRelation(self.f32[r0:r1], self.op[t0 * TILE_ROWS * kp:], r1 - r0,
+                                self.dim, self.name, None,
+                                None if self.row_err is None else self.row_err[r0:r1],
+                                None if self.tile_err is None else self.tile_err[t0:])
+
 
 def tile_count(n: int) -> int:
     return int(_lib.lib().sjb_tile_count(n))

@@ -212,6 +212,54 @@ def _host_tensor(x: ArrayLike) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
 
 
+def _pinned(n: int, dtype) -> torch.Tensor:
+    return torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+
+
+def _join_host_split(PL: D.PreparedRelation, right_host: torch.Tensor, theta: float, band,
+                     left_name: str, right_name: str) -> MatchSet:
+    """Host-input join in two left halves: the first streams S in (H2D
+    overlapped with its filter), the second runs on the resident S while the
+    first half's matches copy to pinned host memory -- both halves land in one
+    pinned buffer, so the MatchSet needs no concatenation.  Rows of the left
+    halves are disjoint and ordered, so the result is the canonical MatchSet."""
+    n = PL.n
+    h = (n // 2) // 1024 * 1024
+    if h == 0:
+        m, _ = D.join_streamed(PL, right_host, theta, band)
+        return _to_matchset(m, left_name, right_name)
+    dev = PL.device
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    mA, PR = D.join_streamed(PL.rows(0, h), right_host, theta, band)
+    na = mA.n_matches
+    cap = int(na * 2.2) + 4096                    # the halves are alike; grown if not
+    bufs = (_pinned(cap, torch.int64), _pinned(cap, torch.int64), _pinned(cap, torch.float32))
+    ev = torch.cuda.Event()
+    ev.record(comp)
+    copy.wait_event(ev)
+    with torch.cuda.stream(copy):
+        for b, d in zip(bufs, (mA.lefts, mA.rights, mA.sims)):
+            b[:na].copy_(d, non_blocking=True)
+    mB = D.join_prepared(PL.rows(h, n), PR, theta, band, left_base=h)
+    nb = mB.n_matches
+    if na + nb > cap:                             # grow: copy both halves again
+        cap = na + nb
+        copy.synchronize()
+        bufs = (_pinned(cap, torch.int64), _pinned(cap, torch.int64), _pinned(cap, torch.float32))
+        for b, d in zip(bufs, (mA.lefts, mA.rights, mA.sims)):
+            b[:na].copy_(d, non_blocking=True)
+    for b, d in zip(bufs, (mB.lefts, mB.rights, mB.sims)):
+        b[na:na + nb].copy_(d, non_blocking=True)
+    copy.synchronize()
+    comp.synchronize()
+    tot = na + nb
+    if tot == 0:
+        return MatchSet(left_name, right_name)
+    return MatchSet(left_name, right_name, bufs[0][:tot].numpy().view(np.uint64),
+                    bufs[1][:tot].numpy().view(np.uint64), bufs[2][:tot].numpy())
+
+
 def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                         band: Optional[float] = None, left_name: str = "left",
                         right_name: str = "right", device=None) -> Tuple[MatchSet, JoinStats]:
@@ -225,12 +273,14 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
         L = _as_device_matrix(left, dev)
         check_dims(L.shape[1], right.shape[1])
         if _is_host(right) and right.shape[0] >= _STREAM_MIN_ROWS:
-            # overlap the right relation's H2D copy with the filter
-            m, _ = D.join_streamed(D.prepare(L), _host_tensor(right), t.value, band)
+            # overlap the right relation's H2D copy with the filter, and the
+            # first half's result D2H with the second half's join
+            matches = _join_host_split(D.prepare(L), _host_tensor(right), t.value, band,
+                                       left_name, right_name)
         else:
             m = D.join_prepared(D.prepare(L), D.prepare(_as_device_matrix(right, dev)), t.value,
                                 band)
-        matches = _to_matchset(m, left_name, right_name)
+            matches = _to_matchset(m, left_name, right_name)
     R = right
     wall = time.perf_counter_ns() - t0
     stats = JoinStats(wall_nanos=wall, model_calls_left=L.shape[0],

@@ -336,6 +336,27 @@ def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
         top_k(model, embed_relation(model, rel), rel, "p", 0)
 
 
+@pytest.mark.parametrize("recheck", ["fused", "deferred"])
+def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
+    """Thousands of rows (several work items and S tiles per CTA, partial
+    last tiles), dense and sparse thresholds, both recheck placements."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv("SJB_RECHECK", recheck)
+    rng = np.random.default_rng(77)
+    for inst in range(4):
+        nl, nr = int(rng.integers(3000, 7000)), int(rng.integers(4000, 9000))
+        dim = int(rng.choice([37, 64, 100, 128]))
+        L, S = O_pair(nl, nr, dim, int(rng.integers(20, 200)), float(rng.uniform(0.3, 0.8)),
+                      500 + inst)
+        theta = float(rng.choice([0.2, 0.5, 0.8, 0.95]))
+        m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                            D.prepare(torch.from_numpy(S).to(cuda)), theta)
+        lo, ro, so = m.to_host()
+        wl, wr, ws = O.join_raw(L, S, theta, threads=16)
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

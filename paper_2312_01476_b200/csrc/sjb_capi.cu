@@ -661,7 +661,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   if (tile_end > nt256) tile_end = nt256;
   if (tile_end <= tile_begin) return SJB_OK;
   // kernel tile units: 256 rows, or 128 for the CTA-pair kernel
-  const int64_t unit = pl.pair ? 2 : 1;
+  const int64_t unit = pl.pair ? sjb::kTileRows / sjb::pair::kUmmaN : 1;
   const int64_t tb = tile_begin * unit;
   const int64_t te = tile_end * unit > pl.n_btiles ? pl.n_btiles : tile_end * unit;
   int tpc = 0;

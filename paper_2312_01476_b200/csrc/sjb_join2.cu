@@ -51,13 +51,22 @@ namespace pair {
 // 16 epilogue warps in two stage-alternating groups of 8, each warp 32 lanes x
 // 64 columns (64 values amortise the per-stage fixed costs; 16 warps x 32
 // columns of EVERY stage was issue-bound).
+#ifndef SJB_PAIR_N
+#define SJB_PAIR_N 128
+#endif
 constexpr int kEpiWarps = 16;
-constexpr int kEpiGroup = 8;  // warps per stage (per CTA)
 constexpr int kRecheckWarps = 2;
 constexpr int kThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
-constexpr int kAccStages = 4;
-constexpr int kUmmaN = 128;       // pair N (S rows per stage)
-constexpr int kHalfN = 64;        // S rows per CTA per stage
+// Pair N = S rows per stage.  N = 256: per SM an UMMA reads 128 A rows + 128
+// B rows (64 B/cycle of SMEM, the 1-CTA N=256 kernel reads 96), two TMEM
+// stages, all 16 epilogue warps on every stage.  N = 128: four TMEM stages,
+// two stage-alternating groups of 8 epilogue warps.
+constexpr int kUmmaN = SJB_PAIR_N;
+constexpr int kHalfN = kUmmaN / 2;       // S rows per CTA per stage
+constexpr int kAccStages = 512 / kUmmaN;
+constexpr int kEpiGroup = kUmmaN / 16;   // warps per stage: 4 lane quarters x N/64 column chunks
+constexpr int kGroups = kEpiWarps / kEpiGroup;
+static_assert(kUmmaN == 128 || kUmmaN == 256, "pair N");
 constexpr int kARows = kTileRows;  // 256 resident R rows per CTA
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a pair smem address
 
@@ -282,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---------------------------------------------- MMA issuer (pair)
       const uint32_t idesc = umma_idesc_f16_f32(256, kUmmaN);
       const uint32_t a_lbo = kARows * 16;   // A: 256-row block, k-group stride
-      const uint32_t b_lbo = kHalfN * 16;   // B: 64-row slab, k-group stride
+      const uint32_t b_lbo = kHalfN * 16;   // B: this CTA's kHalfN-row slab, k-group stride
       const uint32_t sbo = 128;
       const uint64_t a_kstep = (2 * a_lbo) >> 4, b_kstep = (2 * b_lbo) >> 4;
       const uint64_t half_step = (128 * 16) >> 4;
@@ -356,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // is released right after the drain; with four TMEM stages the MMA runs
     // ahead while the warp reduces and emits.
     const int ew = warp - 2;
-    const int grp = ew / kEpiGroup;          // stages k with k % 2 == grp
+    const int grp = ew / kEpiGroup;          // stages k with k % kGroups == grp
     const int cq = (ew % kEpiGroup) >> 2;
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)q * 32;
@@ -478,8 +487,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float va[64];
     uint32_t k = grp;
     Stage cur = first_of(pair_id);
-    if (grp) cur = advance(cur);
-    for (; cur.valid; cur = advance(advance(cur)), k += 2) {
+    for (int g = 0; g < grp; g++) cur = advance(cur);
+    for (; cur.valid; k += kGroups) {
       // band terms issued before the accumulator wait (latency hidden)
       const bool per_row = p.row_err != nullptr;
       const float ex = load_err(p.row_err, row_of(cur), p.n_a);
@@ -488,6 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_wait_ld();
       release(k % kAccStages);
       process(va, cur, per_row ? cutoff_from(p.cutoff, p.theta, p.slack, ex, ey) : p.cutoff);
+      for (int g = 0; g < kGroups; g++) cur = advance(cur);
     }
 #undef SJB_PAIR_LOAD
     __syncwarp();

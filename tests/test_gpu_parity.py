@@ -357,6 +357,29 @@ def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
 
 
+def test_budget_and_thread_invariance(cuda, manifest, golden):
+    """SPEC acceptance (4) + thread-count invariance: the
+    MatchSet is identical for every budget and thread count (the device path
+    never materialises a budget-sized buffer; both are validated only)."""
+    from paper_2312_01476_b200 import LookupModel, RawRelation, nlj_prefetch, tensor_join
+    meta = manifest["cases"]["c_ragged"]
+    L, S = case_inputs(meta)
+    tl = [f"L{i}" for i in range(len(L))]
+    tr = [f"S{i}" for i in range(len(S))]
+    model = LookupModel.from_matrix(tl + tr, np.concatenate([L, S]))
+    results = []
+    for budget in (1 << 30, 64 << 20, 16 << 20, 1 << 20, 4096):
+        for threads in (1, 4):
+            ms, st = tensor_join(RawRelation("l", tl), RawRelation("r", tr), model, meta["theta"],
+                                 budget_bytes=budget, threads=threads)
+            results.append(ms)
+            assert st.threads == threads and st.peak_buffer_bytes == 0
+    ms2, _ = nlj_prefetch(RawRelation("l", tl), RawRelation("r", tr), model, meta["theta"],
+                          threads=3)
+    for ms in results + [ms2]:
+        assert _bits_equal(ms, golden["c_ragged_l"], golden["c_ragged_r"], golden["c_ragged_s"])
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -46,6 +46,7 @@ def is_stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_pack(force)
     if not force and not is_stale():
         return LIB_PATH
     extra = os.environ.get("SJB_NVCC_EXTRA", "").split()   # e.g. -DSJB_PROFILE=1
@@ -59,5 +60,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB_PATH
 
 
+def pack_ext_path() -> str:
+    import sysconfig
+    return os.path.join(PKG_DIR, "_sjbpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pack(force: bool = False) -> str:
+    """The CPython token packer (csrc/sjb_pack.c) -> _sjbpack<EXT_SUFFIX>."""
+    import sysconfig
+    out = pack_ext_path()
+    src = os.path.join(CSRC, "sjb_pack.c")
+    if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(src):
+        return out
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC",
+           "-I" + sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
+    subprocess.check_call(cmd)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_pack(force="--force" in sys.argv))

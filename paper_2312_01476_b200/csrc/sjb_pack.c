@@ -1,0 +1,77 @@
+/* sjb_pack.c -- host-side token packing for the device embedding kernels
+ * (subword model, synthetic-model hashing): a Python sequence of str ->
+ * (UTF-8 bytes of all tokens back to back + a trailing NUL, int64 offsets
+ * [n + 1]) in one pass over the sequence.  For compact ASCII strings
+ * PyUnicode_AsUTF8AndSize returns CPython's own buffer, so a token costs one
+ * memcpy.  Replaces device.pack_tokens' pure-Python path (~10 ms per 200k
+ * tokens on the GPU box host). */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <string.h>
+
+static PyObject* pack(PyObject* self, PyObject* arg) {
+  (void)self;
+  PyObject* fast = PySequence_Fast(arg, "tokens must be a sequence of str");
+  if (!fast) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
+  PyObject** items = PySequence_Fast_ITEMS(fast);
+  PyObject* offs = PyBytes_FromStringAndSize(NULL, (n + 1) * (Py_ssize_t)sizeof(int64_t));
+  size_t cap = (size_t)n * 16 + 64, pos = 0;
+  char* buf = (char*)PyMem_RawMalloc(cap);
+  if (!offs || !buf) {
+    Py_XDECREF(offs);
+    PyMem_RawFree(buf);
+    Py_DECREF(fast);
+    return PyErr_NoMemory();
+  }
+  int64_t* o = (int64_t*)PyBytes_AS_STRING(offs);
+  o[0] = 0;
+  /* one pass: each string object is touched once (they are scattered in the
+     heap; a second pass doubled the cache misses) */
+  for (Py_ssize_t i = 0; i < n; i++) {
+    if (!PyUnicode_Check(items[i])) {
+      PyErr_Format(PyExc_TypeError, "token %zd is not a str", i);
+      goto fail;
+    }
+    Py_ssize_t len = 0;
+    const char* s = PyUnicode_AsUTF8AndSize(items[i], &len);
+    if (!s) goto fail;
+    if (pos + (size_t)len + 1 > cap) {
+      while (pos + (size_t)len + 1 > cap) cap *= 2;
+      char* nb = (char*)PyMem_RawRealloc(buf, cap);
+      if (!nb) {
+        PyErr_NoMemory();
+        goto fail;
+      }
+      buf = nb;
+    }
+    memcpy(buf + pos, s, (size_t)len);
+    pos += (size_t)len;
+    o[i + 1] = (int64_t)pos;
+  }
+  buf[pos] = 0;
+  {
+    PyObject* data = PyBytes_FromStringAndSize(buf, (Py_ssize_t)pos + 1);
+    PyMem_RawFree(buf);
+    Py_DECREF(fast);
+    if (!data) {
+      Py_DECREF(offs);
+      return NULL;
+    }
+    return Py_BuildValue("NN", data, offs);
+  }
+fail:
+  PyMem_RawFree(buf);
+  Py_DECREF(offs);
+  Py_DECREF(fast);
+  return NULL;
+}
+
+static PyMethodDef methods[] = {
+    {"pack", pack, METH_O, "pack(tokens) -> (utf8 bytes + NUL, int64 offsets bytes)"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_sjbpack", NULL, -1, methods};
+
+PyMODINIT_FUNC PyInit__sjbpack(void) { return PyModule_Create(&module); }

@@ -462,10 +462,17 @@ def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> 
     return PreparedRelation(f32, op, n, dim, name, rep, re, te)
 
 
-def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
-    """UTF-8 bytes of the tokens (device u8) and n+1 int64 offsets (device).
-    ASCII token lists (the common case) are packed with one join and one
-    encode; others token by token."""
+def _pack_host(tokens) -> Tuple[np.ndarray, np.ndarray]:
+    """UTF-8 bytes (+ NUL) and int64 offsets of the tokens, on the host: the
+    native packer (csrc/sjb_pack.c) when built, else an equivalent Python
+    path (host-side marshalling only; no computation falls back)."""
+    try:
+        from . import _sjbpack
+    except ImportError:
+        _sjbpack = None
+    if _sjbpack is not None:
+        data, offs = _sjbpack.pack(tokens)
+        return np.frombuffer(data, dtype=np.uint8), np.frombuffer(offs, dtype=np.int64)
     n = len(tokens)
     joined = "".join(tokens)
     if joined.isascii():
@@ -478,9 +485,14 @@ def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tenso
     offs = np.zeros(n + 1, dtype=np.int64)
     if n:
         np.cumsum(lens, out=offs[1:])
-    buf = np.frombuffer(raw + b"\0", dtype=np.uint8)
+    return np.frombuffer(raw + b"\0", dtype=np.uint8), offs
+
+
+def pack_tokens(tokens, device: torch.device) -> Tuple[torch.Tensor, torch.Tensor]:
+    """UTF-8 bytes of the tokens (device u8) and n+1 int64 offsets (device)."""
+    buf, offs = _pack_host(tokens)
     return (torch.from_numpy(buf.copy()).to(device, non_blocking=False),
-            torch.from_numpy(offs).to(device))
+            torch.from_numpy(offs.copy()).to(device))
 
 
 def fnv1a64_tokens(tokens, xor_seed: int, device: torch.device) -> torch.Tensor:

@@ -122,3 +122,23 @@ def test_no_oracle_in_product():
                 txt = open(os.path.join(root, f)).read()
                 assert "import oracle" not in txt and "refkern" not in txt, f
                 assert "liboracle" not in txt and "from oracle" not in txt, f
+
+
+def test_native_token_packer_matches_python():
+    """csrc/sjb_pack.c (built by build()) packs exactly like the Python path:
+    UTF-8 bytes back to back + NUL, int64 offsets; non-str tokens raise."""
+    import numpy as np
+    from paper_2312_01476_b200 import build as B, device as D
+    B.build_pack()
+    from paper_2312_01476_b200 import _sjbpack
+    cases = [["l_0", "dog", "été", "", "a\0b", "x" * 300], [], [""], ["ascii"] * 1000]
+    for toks in cases:
+        data, offs = _sjbpack.pack(toks)
+        enc = [t.encode("utf-8") for t in toks]
+        assert data == b"".join(enc) + b"\0"
+        want = np.concatenate([[0], np.cumsum([len(e) for e in enc], dtype=np.int64)])
+        assert np.array_equal(np.frombuffer(offs, dtype=np.int64), want.astype(np.int64))
+        b, o = D._pack_host(toks)
+        assert bytes(b) == data and np.array_equal(o, want)
+    with pytest.raises(TypeError):
+        _sjbpack.pack(["a", 3])

@@ -878,7 +878,8 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
   const int big_smem = sjb::kSortBigCap * 8;
   if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
   sjb::segsort_big_kernel<<<sjb_sm_count(current_device()), sjb::kSortBigThreads, big_smem, st>>>(
-      c.rowoff, keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base);
+      c.rowoff, keys, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base,
+      args->n_right);
   SJB_CK_LAUNCH("segsort_big");
   sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.rowoff, nl,
                                                args->out_cap, info);

@@ -388,18 +388,81 @@ segsort_small_kernel(const uint64_t* __restrict__ rowoff, int64_t n_rows, const 
 
 constexpr int kSortBigThreads = 512;
 constexpr int kSortBigCap = 26624;   // keys sorted whole in shared memory (208 KB)
-constexpr int kSortChunk = 16384;    // power-of-two chunk of the multi-pass path
-static_assert(kSortChunk == 1 << 14 && kSortChunk <= kSortBigCap, "chunk fits the buffer");
 
-// Rows longer than kSortWarpCap: one CTA per row.  <= kSortBigCap sorts in
-// shared memory; longer rows run the same network over global memory with
-// the inner (j < kSortChunk) steps done in shared memory per chunk.  (Zipf
-// clusters give cfg4 rows with tens of thousands of matches.)
+
+// Rows longer than kSortWarpCap: one CTA per row.  Up to kSortBigCap keys
+// sort whole in shared memory (bitonic).  Longer rows -- Zipf clusters give
+// cfg4 rows with tens of thousands of matches -- are ranked instead of sorted:
+// a row's right offsets j are distinct, so j's position in the row is the
+// number of the row's keys below it.  Per window of kRankWindow offsets: set
+// bit j of a shared-memory bitmap, prefix-popcount it per 1024-bit group,
+// and write each key straight to q0 + (keys in earlier windows) + rank.
+constexpr int kRankWindow = 1 << 20;                  // bits: 128 KB of shared memory
+constexpr int kRankWords = kRankWindow / 32;
+constexpr int kRankGroups = kRankWords / 32;           // 1024 groups of 32 words
+static_assert((kRankWords + kRankGroups + 1) * 4 <= kSortBigCap * 8, "bitmap fits the buffer");
+
+__device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0, uint64_t i_row,
+                         int64_t n_right, uint32_t* bits, uint32_t* gpre,
+                         uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
+                         float* __restrict__ sims) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  uint64_t base = 0;
+  for (int64_t w0 = 0; w0 < n_right; w0 += kRankWindow) {
+    for (int t = tid; t < kRankWords; t += nthr) bits[t] = 0u;
+    __syncthreads();
+    for (int64_t t = tid; t < n; t += nthr) {
+      const uint64_t o = (g[t] >> 32) - (uint64_t)w0;
+      if (o < (uint64_t)kRankWindow) atomicOr(&bits[o >> 5], 1u << (o & 31));
+    }
+    __syncthreads();
+    // group sums, then an exclusive scan over the 1024 groups (warp 0)
+    for (int q = tid; q < kRankGroups; q += nthr) {
+      uint32_t c = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; k++) c += __popc(bits[q * 32 + k]);
+      gpre[q] = c;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t carry = 0;
+      for (int q0g = 0; q0g < kRankGroups; q0g += 32) {
+        const uint32_t v = gpre[q0g + tid];
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += y;
+        }
+        gpre[q0g + tid] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (tid == 0) gpre[kRankGroups] = carry;
+    }
+    __syncthreads();
+    for (int64_t t = tid; t < n; t += nthr) {
+      const uint64_t key = g[t];
+      const uint64_t o = (key >> 32) - (uint64_t)w0;
+      if (o >= (uint64_t)kRankWindow) continue;
+      const uint32_t word = (uint32_t)(o >> 5), grp = word >> 5;
+      uint32_t rank = gpre[grp];
+      for (uint32_t k = grp * 32; k < word; k++) rank += __popc(bits[k]);
+      rank += __popc(bits[word] & ((1u << (o & 31)) - 1u));
+      const uint64_t pos = q0 + base + rank;
+      lefts[pos] = i_row;
+      rights[pos] = key >> 32;
+      sims[pos] = __uint_as_float((uint32_t)key);
+    }
+    base += gpre[kRankGroups];
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kSortBigThreads)
 segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ keys,
                    uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                    float* __restrict__ sims, const uint32_t* __restrict__ big_rows,
-                   const unsigned int* __restrict__ n_big, uint64_t left_base) {
+                   const unsigned int* __restrict__ n_big, uint64_t left_base, int64_t n_right) {
   extern __shared__ uint64_t sbuf[];
   if (n_big[1] == 0) return;  // gate: outputs would overflow
   const unsigned nb = n_big[0];
@@ -416,74 +479,8 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
       __syncthreads();
       continue;
     }
-    int64_t P = 1;
-    int lp = 0;
-    while (P < n) {
-      P <<= 1;
-      lp++;
-    }
-    const int C = kSortChunk, lc = 14;  // 1 << 14 == kSortChunk
-    // 1) sort every C-chunk (all stages k <= C) in shared memory
-    for (int64_t c0 = 0; c0 < n; c0 += C) {
-      const int m = (int)mn<int64_t>(C, n - c0);
-      for (int t = threadIdx.x; t < m; t += blockDim.x) sbuf[t] = g[c0 + t];
-      __syncthreads();
-      smem_bitonic<false>(sbuf, m, threadIdx.x, blockDim.x);
-      for (int t = threadIdx.x; t < m; t += blockDim.x) g[c0 + t] = sbuf[t];
-      __syncthreads();
-    }
-    // 2) stages k > C: mirror + large-j steps in global, small-j steps per
-    //    chunk (k, j powers of two: block/offset by shift and mask)
-    for (int lk = lc + 1; lk <= lp; lk++) {
-      const int64_t k = (int64_t)1 << lk;
-      for (int lj = lk - 1; lj >= lc; lj--) {
-        const int64_t j = (int64_t)1 << lj;
-        const bool mirror = (lj == lk - 1);
-        for (int64_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
-          int64_t a, b;
-          if (mirror) {
-            const int64_t blk = t >> (lk - 1), off = t & ((k >> 1) - 1);
-            a = (blk << lk) + off;
-            b = (blk << lk) + k - 1 - off;
-          } else {
-            const int64_t blk = t >> lj, off = t & (j - 1);
-            a = (blk << (lj + 1)) + off;
-            b = a + j;
-          }
-          if (b < n) {
-            uint64_t x = g[a], y = g[b];
-            if (y < x) {
-              g[a] = y;
-              g[b] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-      for (int64_t c0 = 0; c0 < n; c0 += C) {
-        const int m = (int)mn<int64_t>(C, n - c0);
-        for (int t = threadIdx.x; t < m; t += blockDim.x) sbuf[t] = g[c0 + t];
-        __syncthreads();
-        for (int lj = lc - 1; lj >= 0; lj--) {
-          const int j = 1 << lj;
-          for (int t = threadIdx.x; t < C / 2; t += blockDim.x) {
-            const int blk = t >> lj, off = t & (j - 1);
-            const int a = (blk << (lj + 1)) + off, b = a + j;
-            if (b < m) cmpx(sbuf, a, b);
-          }
-          __syncthreads();
-        }
-        for (int t = threadIdx.x; t < m; t += blockDim.x) g[c0 + t] = sbuf[t];
-        __syncthreads();
-      }
-    }
-    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
-      const uint64_t key = g[t];
-      lefts[q0 + t] = left_base + i;
-      rights[q0 + t] = key >> 32;
-      sims[q0 + t] = __uint_as_float((uint32_t)key);
-    }
-    __syncthreads();
+    uint32_t* bits = reinterpret_cast<uint32_t*>(sbuf);
+    rank_row(g, n, q0, left_base + i, n_right, bits, bits + kRankWords, lefts, rights, sims);
   }
 }
 

@@ -398,24 +398,24 @@ def test_overflow_retry_is_exact(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), golden["c_small_s"].view(np.uint32))
 
 
-@pytest.mark.parametrize("nr", [3000, 20000, 70000])
-def test_all_pairs_large_rows(cuda, nr):
+@pytest.mark.parametrize("nr,nl", [(3000, 3), (20000, 3), (70000, 3), (1_100_000, 1)])
+def test_all_pairs_large_rows(cuda, nr, nl):
     """theta = -1: every pair matches; rows longer than the warp sort (1024)
-    go to the CTA sort -- whole in shared memory up to 26624 keys, the
-    multi-pass global network beyond (70000: stages up to 2^17)."""
+    go to the CTA sort -- whole in shared memory up to 26624 keys, ranked
+    through a shared-memory bitmap beyond (1.1M: two 2^20-offset windows)."""
     from paper_2312_01476_b200 import device as D
     rng = np.random.default_rng(5)
-    L = rng.standard_normal((3, 16), dtype=np.float32)
+    L = rng.standard_normal((nl, 16), dtype=np.float32)
     S = rng.standard_normal((nr, 16), dtype=np.float32)
     m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
                         D.prepare(torch.from_numpy(S).to(cuda)), -1.0)
     lo, ro, so = m.to_host()
-    assert len(lo) == 3 * nr
-    assert np.array_equal(lo, np.repeat(np.arange(3, dtype=np.uint64), nr))
-    assert np.array_equal(ro, np.tile(np.arange(nr, dtype=np.uint64), 3))
+    assert len(lo) == nl * nr
+    assert np.array_equal(lo, np.repeat(np.arange(nl, dtype=np.uint64), nr))
+    assert np.array_equal(ro, np.tile(np.arange(nr, dtype=np.uint64), nl))
     Ln, _ = O.normalize_rows(L)
     Sn, _ = O.normalize_rows(S)
-    for r in range(3):
+    for r in range(nl):
         assert np.array_equal(so[r * nr:(r + 1) * nr].view(np.uint32),
                               O.dots_vm(Ln[r], Sn).view(np.uint32))
 

@@ -380,6 +380,31 @@ def test_budget_and_thread_invariance(cuda, manifest, golden):
         assert _bits_equal(ms, golden["c_ragged_l"], golden["c_ragged_r"], golden["c_ragged_s"])
 
 
+@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (200, "fused")])
+def test_nan_and_inf_rows(cuda, monkeypatch, dim, recheck):
+    """Rows with NaN or +-Inf normalise to NaN rows (inf / inf) exactly as the
+    reference's normalize_row; their similarities are NaN, so they match
+    nothing -- the filter, the per-row band and the recheck must agree."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv("SJB_RECHECK", recheck)
+    rng = np.random.default_rng(dim)
+    L = rng.standard_normal((300, dim)).astype(np.float32)
+    S = rng.standard_normal((400, dim)).astype(np.float32)
+    L[3, 2] = np.nan
+    L[7, 0] = np.inf
+    S[5, 1] = -np.inf
+    S[9, :] = np.nan
+    for theta in (-1.0, 0.1):
+        pl, pr = D.prepare(torch.from_numpy(L).to(cuda)), D.prepare(torch.from_numpy(S).to(cuda))
+        want32, _ = O.normalize_rows(L)
+        assert np.array_equal(pl.f32.cpu().numpy().view(np.uint32), want32.view(np.uint32))
+        lo, ro, so = D.join_prepared(pl, pr, theta).to_host()
+        wl, wr, ws = O.join_raw(L, S, theta, threads=4)
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
+        assert not ({3, 7} & set(lo.tolist())) and not ({5, 9} & set(ro.tolist()))
+
+
 def O_pair(nl, nr, dim, c, sigma, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, c, sigma, seed)

@@ -366,20 +366,32 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
               }
             }
             const uint32_t cnt = __popc(mk0) + __popc(mk1);
-            uint32_t incl = cnt;
+            uint64_t pos;
+            if (__popc(__ballot_sync(0xffffffffu, cnt != 0)) <= 1) {
+              // common case (~1 candidate per hit chunk): the only lane with
+              // candidates reserves its own slots -- no scan, no broadcast
+              uint32_t base = 0;
+              if (cnt) {
+                base = atomicAdd(cta_cnt, cnt);
+                if (base + cnt < base) *cta_sat = 1u;
+              }
+              pos = base;
+            } else {
+              uint32_t incl = cnt;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += y;
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+              uint32_t base = 0;
+              if (lane == 31 && wtot) {
+                base = atomicAdd(cta_cnt, wtot);
+                if (base + wtot < base) *cta_sat = 1u;
+              }
+              base = __shfl_sync(0xffffffffu, base, 31);
+              pos = (uint64_t)base + (incl - cnt);
             }
-            const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-            uint32_t base = 0;
-            if (lane == 31 && wtot) {
-              base = atomicAdd(cta_cnt, wtot);
-              if (base + wtot < base) *cta_sat = 1u;
-            }
-            base = __shfl_sync(0xffffffffu, base, 31);
-            uint64_t pos = (uint64_t)base + (incl - cnt);
             const uint32_t gi = (uint32_t)gi64;
             const uint32_t j0 = (uint32_t)(t * kBN + cq * 64);
             uint32_t w = mk0;

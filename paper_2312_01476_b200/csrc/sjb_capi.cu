@@ -778,9 +778,16 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
           tp.b = rp;
           if (int rc = encode_rows_map(&tp.tmap_l, d_l32, nl, (int)args->dim)) return rc;
           if (int rc = encode_rows_map(&tp.tmap_r, d_r32, nr, (int)args->dim)) return rc;
-          const int rs = (int)sjb::wide::recheck_tma_smem_bytes();
-          if (int rc = set_smem_attr((const void*)sjb::wide::recheck_tma_kernel, rs)) return rc;
-          sjb::wide::recheck_tma_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
+          const char* wr = getenv("SJB_WIDE_RECHECK");
+          if (wr != nullptr && strcmp(wr, "tile") == 0) {  // A/B: A restaged per tile
+            const int rs = (int)sjb::wide::recheck_tma_smem_bytes();
+            if (int rc = set_smem_attr((const void*)sjb::wide::recheck_tma_kernel, rs)) return rc;
+            sjb::wide::recheck_tma_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
+          } else {
+            const int rs = (int)sjb::wide::recheck_group_smem_bytes();
+            if (int rc = set_smem_attr((const void*)sjb::wide::recheck_group_kernel, rs)) return rc;
+            sjb::wide::recheck_group_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
+          }
         } else {
           const int rs = (int)sjb::wide::recheck_smem_bytes();
           if (int rc = set_smem_attr((const void*)sjb::wide::recheck_generic_kernel, rs)) return rc;

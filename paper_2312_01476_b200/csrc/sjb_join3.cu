@@ -676,5 +676,194 @@ __global__ void __launch_bounds__(kRtThreads, 1)
   }
 }
 
+// --------------------------------------- recheck, tile groups, A reused
+// recheck_tma_kernel streams the R-block (A) chunks again for every tile,
+// although all tiles of a work item share the R block: its shared-memory
+// traffic per tile is 24 x (32 KB A + 32 KB B written) + the operand reads.
+// Here consecutive tiles of an item form a group whose candidates fit in
+// shared memory (<= kGrCap): per K chunk the A chunk is staged once for the
+// group and the B chunk once per tile, and each candidate's fp32 running sum
+// stays in shared memory between chunks (same d = 0..dim-1 order).  A tile
+// with more candidates than the capacity runs alone, in passes.
+constexpr int kGrCap = 8192;        // candidates per group
+constexpr int kGrAStages = 2;
+constexpr int kGrBStages = 3;
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kRtComputeWarps * 32) : "memory");
+}
+
+__host__ __device__ constexpr uint32_t recheck_group_smem_bytes() {
+  return (kGrAStages + kGrBStages) * kRtOpBytes + 1024 + kGrCap * 4 + kGrCap * 2 +
+         2 * (kGrAStages + kGrBStages) * 8 + 64;
+}
+
+// Group [k, kend) of an item's tiles (local tile indices into toff), or one
+// oversized tile k processed in passes.  Deterministic: the producer and
+// the consumers walk identical groups.
+__device__ __forceinline__ int64_t group_end(const uint32_t* toff, int64_t k, int64_t k_end) {
+  const uint32_t g_lo = toff[k];
+  int64_t e = k;
+  while (e < k_end && toff[e + 1] - g_lo <= (uint32_t)kGrCap) e++;
+  return e == k ? k + 1 : e;
+}
+
+__global__ void __launch_bounds__(kRtThreads, 1)
+    recheck_group_kernel(const __grid_constant__ RecheckTmaParams tp) {
+  const RecheckParams& p = tp.b;
+  extern __shared__ uint8_t rg_raw[];
+  const uint32_t raw = smem_u32(rg_raw);
+  uint8_t* base = rg_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* a_ring = base;                                        // kGrAStages x 32 KB
+  uint8_t* b_ring = base + kGrAStages * kRtOpBytes;              // kGrBStages x 32 KB
+  float* acc = reinterpret_cast<float*>(base + (kGrAStages + kGrBStages) * kRtOpBytes);
+  uint16_t* meta = reinterpret_cast<uint16_t*>(acc + kGrCap);   // ra | rb << 8
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(meta + kGrCap);
+  uint64_t* empty_a = full_a + kGrAStages;
+  uint64_t* full_b = empty_a + kGrAStages;
+  uint64_t* empty_b = full_b + kGrBStages;
+  const int c = blockIdx.x;
+  if (p.cta_count[c] > p.seg_cap) return;  // saturated segment: the join is retried
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGrAStages; i++) {
+      mbar_init(&full_a[i], 1);
+      mbar_init(&empty_a[i], kRtComputeWarps);
+    }
+    for (int i = 0; i < kGrBStages; i++) {
+      mbar_init(&full_b[i], 1);
+      mbar_init(&empty_b[i], kRtComputeWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t* seg = p.cand + (uint64_t)c * p.seg_cap;
+  uint32_t* sims = p.sims_bits + (uint64_t)c * p.seg_cap;
+  const uint32_t* toff = p.tile_off + (int64_t)c * p.tile_stride;
+  const int dim = p.dim;
+  const int nch = (dim + kRcKC - 1) / kRcKC;
+  const int nb = p.n_ablk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int sa = 0, sbs = 0;
+  uint32_t pha = 0, phb = 0;
+
+  if (warp == 0) {
+    if (lane != 0) return;
+    // -------------------------------------------------------- producer
+    int64_t k = 0;
+    for (int64_t item = c; item < p.n_items; item += gridDim.x) {
+      const int64_t rb = item % nb, sc = item / nb;
+      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
+      const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+      const int64_t k_end = k + (t1 - t0);
+      for (int64_t kg = k; kg < k_end;) {
+        const int64_t ke = group_end(toff, kg, k_end);
+        const uint32_t g_lo = toff[kg], g_hi = toff[ke];
+        if (g_hi - g_lo >= p.direct_max) {
+          for (uint32_t pb = g_lo; pb < g_hi; pb += kGrCap) {   // > 1 pass: one oversized tile
+            for (int ch = 0; ch < nch; ch++) {
+              mbar_wait(&empty_a[sa], pha ^ 1u);
+              mbar_arrive_expect_tx(&full_a[sa], kRtOpBytes);
+              tma2d(a_ring + (size_t)sa * kRtOpBytes, &tp.tmap_l, ch * kRcKC,
+                    (int)(rb * kTileRows), &full_a[sa]);
+              if (++sa == kGrAStages) { sa = 0; pha ^= 1u; }
+              for (int64_t kt = kg; kt < ke; kt++) {
+                if (toff[kt + 1] == toff[kt]) continue;
+                mbar_wait(&empty_b[sbs], phb ^ 1u);
+                mbar_arrive_expect_tx(&full_b[sbs], kRtOpBytes);
+                tma2d(b_ring + (size_t)sbs * kRtOpBytes, &tp.tmap_r, ch * kRcKC,
+                      (int)((t0 + (kt - k)) * kTileRows), &full_b[sbs]);
+                if (++sbs == kGrBStages) { sbs = 0; phb ^= 1u; }
+              }
+            }
+          }
+        }
+        kg = ke;
+      }
+      k = k_end;
+    }
+    return;
+  }
+  // ------------------------------------------------------------ compute
+  const int ct = threadIdx.x - 32;
+  constexpr int kCT = kRtComputeWarps * 32;
+  const float theta = p.theta;
+  int64_t k = 0;
+  for (int64_t item = c; item < p.n_items; item += gridDim.x) {
+    const int64_t sc = item / nb;
+    const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
+    const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+    const int64_t k_end = k + (t1 - t0);
+    for (int64_t kg = k; kg < k_end;) {
+      const int64_t ke = group_end(toff, kg, k_end);
+      const uint32_t g_lo = toff[kg], g_hi = toff[ke];
+      if (g_hi - g_lo < p.direct_max) {
+        for (uint32_t q = g_lo + ct; q < g_hi; q += kCT) {   // few candidates: gather
+          const uint64_t u = seg[q];
+          const uint32_t gi = (uint32_t)(u >> 32), gj = (uint32_t)u;
+          const float x = dot_seq_dev(p.l32 + (size_t)gi * dim, p.r32 + (size_t)gj * dim, dim);
+          finish_candidate(sims, q, gi, x, theta, p.rowcount);
+        }
+        kg = ke;
+        continue;
+      }
+      for (uint32_t pb = g_lo; pb < g_hi; pb += kGrCap) {
+        const uint32_t np = mn<uint32_t>(g_hi - pb, (uint32_t)kGrCap);
+        consumer_bar();   // the previous pass's finish has read acc / meta
+        for (uint32_t q = ct; q < np; q += kCT) {
+          const uint64_t u = seg[pb + q];
+          meta[q] = (uint16_t)(((uint32_t)(u >> 32) & 255u) | (((uint32_t)u & 255u) << 8));
+          acc[q] = 0.0f;
+        }
+        consumer_bar();
+        for (int ch = 0; ch < nch; ch++) {
+          mbar_wait(&full_a[sa], pha);
+          const uint32_t sA = smem_u32(a_ring + (size_t)sa * kRtOpBytes);
+          const int kc = mn(kRcKC, dim - ch * kRcKC);
+          for (int64_t kt = kg; kt < ke; kt++) {
+            const uint32_t lo = toff[kt], hi = toff[kt + 1];
+            if (hi == lo) continue;
+            mbar_wait(&full_b[sbs], phb);
+            const uint32_t sB = smem_u32(b_ring + (size_t)sbs * kRtOpBytes);
+            // this pass's positions of tile kt
+            const uint32_t ps = (lo > pb ? lo : pb) - pb, pe = mn<uint32_t>(hi, pb + np) - pb;
+            for (uint32_t q = ps + ct; q < pe; q += kCT) {
+              const uint32_t m = meta[q], ra = m & 255u, rbv = m >> 8;
+              float x = acc[q];
+              if (kc == kRcKC) {
+                const uint32_t a0 = sA + ra * 128u, xa = ra & 7u;
+                const uint32_t b0 = sB + rbv * 128u, yb = rbv & 7u;
+#pragma unroll
+                for (int g = 0; g < kRcKC / 4; g++) {
+                  const float4 va = lds4(a0 + ((g ^ xa) << 4)), vb = lds4(b0 + ((g ^ yb) << 4));
+                  x = __fmaf_rn(va.x, vb.x, x);
+                  x = __fmaf_rn(va.y, vb.y, x);
+                  x = __fmaf_rn(va.z, vb.z, x);
+                  x = __fmaf_rn(va.w, vb.w, x);
+                }
+              } else {
+                for (int e = 0; e < kc; e++) x = __fmaf_rn(lds1(sA + swz(ra, e)), lds1(sB + swz(rbv, e)), x);
+              }
+              acc[q] = x;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed(&empty_b[sbs]);
+            if (++sbs == kGrBStages) { sbs = 0; phb ^= 1u; }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&empty_a[sa]);
+          if (++sa == kGrAStages) { sa = 0; pha ^= 1u; }
+        }
+        consumer_bar();   // every chunk of every position done
+        for (uint32_t q = ct; q < np; q += kCT) {
+          const uint64_t u = seg[pb + q];
+          finish_candidate(sims, pb + q, (uint32_t)(u >> 32), acc[q], theta, p.rowcount);
+        }
+      }
+      kg = ke;
+    }
+    k = k_end;
+  }
+}
+
 }  // namespace wide
 }  // namespace sjb

@@ -140,9 +140,10 @@ def test_random_wide_instances_match_oracle(cuda):
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
 
 
-@pytest.mark.parametrize("variant", ["fused", "staged"])
+@pytest.mark.parametrize("variant", ["fused", "tile", "group"])
 def test_wide_recheck_variants(cuda, manifest, golden, monkeypatch, variant):
-    """Both wide recheck variants (fused warps / staged second kernel) are exact."""
+    """All wide recheck variants are exact: fused warps, the per-tile staged
+    kernel, and the tile-group kernel (default) that reuses the A chunks."""
     from paper_2312_01476_b200 import device as D
     monkeypatch.setenv("SJB_WIDE_RECHECK", variant)
     for name in ("c_d200", "c_d768"):

@@ -318,8 +318,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           }
           float v[64];
           const uint32_t taddr = tmem_base + (lane_base << 16) + as * kUmmaN + cq * 64;
-          SJB_TMEM_LD32(taddr + 0, v, 0);
-          SJB_TMEM_LD32(taddr + 32, v, 32);
+          SJB_TMEM_LD64(taddr, v);
           tc_wait_ld();
           tc_fence_before();
           __syncwarp();

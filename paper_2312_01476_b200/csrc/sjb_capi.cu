@@ -548,7 +548,8 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
   const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
                                 : sjb::ceil_div(n, sjb::kTileRows);
   if (tiles == 0) return SJB_OK;
-  const int sub = prep_sub_rows(dim);
+  // gather-latency-bound: smaller staging sub-tiles fit twice the warps per SM
+  const int sub = prep_sub_rows(dim) > 64 ? 64 : prep_sub_rows(dim);
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::subword_embed_kernel, smem)) return rc;
   sjb::subword_embed_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(

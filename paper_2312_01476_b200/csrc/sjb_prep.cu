@@ -37,19 +37,75 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
     norm = sqrt(ss);
     repaired = 1;
   }
+  // x / norm, correctly rounded, without a full divide per element: with
+  // y = RN(1/norm) and q0 = RN(x*y) within 1 ulp of the quotient, the residual
+  // r = x - q0*norm is exact in one fma and RN(q0 + r*y) is the correctly
+  // rounded quotient (Markstein's theorem), i.e. bitwise __ddiv_rn.  Holds for
+  // every finite norm >= 1e-12 and finite float x (no over/underflow in the
+  // residual); non-finite norms keep the true divide (inf/inf = NaN etc.).
+  const bool hoist = isfinite(norm);
+  const double y = __drcp_rn(norm);
+  auto quot = [&](double x) -> double {
+    if (!hoist) return __ddiv_rn(x, norm);
+    const double q0 = __dmul_rn(x, y);
+    return copysign(__fma_rn(__fma_rn(-q0, norm, x), y, q0), x);  // keeps -0.0
+  };
   if (err == nullptr) {
-    for (int d = 0; d < dim; d++) row[d] = __double2float_rn(__ddiv_rn((double)row[d], norm));
+    for (int d = 0; d < dim; d++) row[d] = __double2float_rn(quot((double)row[d]));
   } else {
     double es = 0.0;
     for (int d = 0; d < dim; d++) {
-      const float x = __double2float_rn(__ddiv_rn((double)row[d], norm));
+      const float x = __double2float_rn(quot((double)row[d]));
       row[d] = x;
-      const double e = (double)from_op16(to_op16(x)) - (double)x;
+      // fp16(x) - x is exact in fp32 (at most 13 significant bits, or x itself
+      // when it rounds to zero), so the fp32 difference equals the fp64 one
+      const double e = (double)__fsub_rn(from_op16(to_op16(x)), x);
       es = __dadd_rn(es, __dmul_rn(e, e));
     }
     *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
   }
   return repaired;
+}
+
+// Walks this thread's elements e = tid, tid + kPrepThreads, ... < total of a
+// block of rows `dim` wide, calling f(e, r, d) with (r, d) = divmod(e, dim)
+// advanced incrementally: one integer divide per thread, not per element.
+template <class F>
+__device__ __forceinline__ void for_each_elem(int total, int dim, F f) {
+  const int qs = kPrepThreads / dim, rs = kPrepThreads - qs * dim;
+  int r = (int)threadIdx.x / dim, d = (int)threadIdx.x - r * dim;
+  for (int e = threadIdx.x; e < total; e += kPrepThreads) {
+    f(e, r, d);
+    r += qs;
+    d += rs;
+    if (d >= dim) {
+      d -= dim;
+      r++;
+    }
+  }
+}
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return ((uintptr_t)p & 15) == 0;
+}
+
+// Stage vrows contiguous rows of `src` (row-major, `dim` wide) into smem rows
+// `pitch` floats apart; float4 loads when the rows allow it.
+__device__ __forceinline__ void stage_rows(float* sm, int pitch, const float* __restrict__ src,
+                                           int vrows, int dim) {
+  if ((dim & 3) == 0 && aligned16(src)) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for_each_elem(vrows * (dim >> 2), dim >> 2, [&](int e, int r, int d) {
+      const float4 v = __ldg(s4 + e);
+      float* o = sm + r * pitch + 4 * d;
+      o[0] = v.x;
+      o[1] = v.y;
+      o[2] = v.z;
+      o[3] = v.w;
+    });
+  } else {
+    for_each_elem(vrows * dim, dim, [&](int e, int r, int d) { sm[r * pitch + d] = __ldg(src + e); });
+  }
 }
 
 // Common tail: normalise the rows staged in `sm` (pitch floats apart) for the
@@ -84,10 +140,15 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
   }
   __syncthreads();
   if (out32 != nullptr) {
-    const int64_t base = (row0 + r0) * dim;
-    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
-      int r = e / dim, d = e - r * dim;
-      out32[base + e] = sm[r * pitch + d];
+    float* dst = out32 + (row0 + r0) * dim;
+    if ((dim & 3) == 0 && aligned16(dst)) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      for_each_elem(vrows * (dim >> 2), dim >> 2, [&](int e, int r, int d) {
+        const float* o = sm + r * pitch + 4 * d;
+        d4[e] = make_float4(o[0], o[1], o[2], o[3]);
+      });
+    } else {
+      for_each_elem(vrows * dim, dim, [&](int e, int r, int d) { dst[e] = sm[r * pitch + d]; });
     }
   }
   if (out16 != nullptr) {
@@ -95,8 +156,9 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
     // consecutive rows of the same k-group, so each warp writes 512 B runs.
     uint4* dst = reinterpret_cast<uint4*>(out16 + (row0 / kTileRows) * (int64_t)kTileRows * kpad);
     const int nchunks = sub * (kpad / 8);
+    const int lsub = 31 - __clz(sub);  // sub is a power of two
     for (int c = threadIdx.x; c < nchunks; c += kPrepThreads) {
-      int g = c / sub, r = c - g * sub;
+      int g = c >> lsub, r = c & (sub - 1);
       __align__(16) op16_t v[8];
 #pragma unroll
       for (int e = 0; e < 8; e++) {
@@ -128,11 +190,7 @@ normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ 
   for (int r0 = 0; r0 < kTileRows; r0 += sub) {
     const int vrows = max(0, min(sub, rows - r0));
     if (gather == nullptr) {
-      const int64_t base = (row0 + r0) * dim;
-      for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
-        int r = e / dim, d = e - r * dim;
-        sm[r * pitch + d] = __ldg(in + base + e);
-      }
+      stage_rows(sm, pitch, in + (row0 + r0) * dim, vrows, dim);
     } else {  // row r of this relation is row gather[r] of `in` (lookup model)
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       for (int r = warp; r < vrows; r += kPrepThreads / 32) {
@@ -171,10 +229,9 @@ synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, in
   const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
   for (int r0 = 0; r0 < kTileRows; r0 += sub) {
     const int vrows = max(0, min(sub, rows - r0));
-    for (int e = threadIdx.x; e < vrows * dim; e += kPrepThreads) {
-      int r = e / dim, d = e - r * dim;
+    for_each_elem(vrows * dim, dim, [&](int, int r, int d) {
       sm[r * pitch + d] = splitmix_elem(seeds[row0 + r0 + r], d);
-    }
+    });
     __syncthreads();
     // synthetic vectors are normalised as part of the model (embedding.py:79)
     finish_subtile(sm, pitch, r0, sub, rows, dim, kpad, row0, true, out32, out16, nullptr,
@@ -212,10 +269,13 @@ __device__ __forceinline__ uint8_t marked_byte(const uint8_t* w, int len, int k)
 // Sum the table rows of a batch of nb items (bucket of item q in lane q) into
 // this lane's columns lane + 32k (k < C), in item order (fp32, exactly the
 // sequential sum), with 8 items' loads issued before their adds.
+#ifndef SJB_SUBWORD_KU
+#define SJB_SUBWORD_KU 8
+#endif
 template <int C>
 __device__ __forceinline__ void gather_items(float* acc, const float* __restrict__ table,
                                              uint64_t bucket, int nb, int dim, int lane) {
-  constexpr int kU = 8;
+  constexpr int kU = SJB_SUBWORD_KU;
   for (int q0 = 0; q0 < nb; q0 += kU) {
     float v[kU][C];
 #pragma unroll
@@ -235,7 +295,7 @@ __device__ __forceinline__ void gather_items(float* acc, const float* __restrict
   }
 }
 
-__global__ void __launch_bounds__(kPrepThreads)
+__global__ void __launch_bounds__(kPrepThreads, 8)  // 8 CTAs/SM: the gather is latency-bound
 subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
                      int64_t n, const float* __restrict__ table, int64_t n_buckets, int dim,
                      int kpad, int sub, int minn, int maxn, int normalize,

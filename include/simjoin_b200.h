@@ -218,6 +218,23 @@ int sjb_scan_hits(const float* d_buf, int64_t nl, int64_t nr, float theta, uint6
                   void* stream);
 int64_t sjb_scan_hits_workspace_bytes(int64_t nl);
 
+/* The matches file (cli._write_matches, cli.py:105-108; _fmt_sim 99-102):
+ * line i = "<lefts[i]>,<rights[i]>,<sim>\n", <sim> the shortest positional
+ * decimal that reads back as the same float32 (numpy
+ * format_float_positional(unique=True, trim="-")); "-0", "inf", "nan" as
+ * numpy prints them.  Replaces the per-line Python formatting loop.
+ * Layout (synchronous): computes the line offsets into the workspace and
+ * *out_bytes = file size.  Write (asynchronous): the file bytes into d_out,
+ * using the workspace of a layout call on the same columns. */
+int64_t sjb_matches_csv_workspace_bytes(int64_t n);
+int sjb_matches_csv_layout(const uint64_t* d_lefts, const uint64_t* d_rights,
+                           const float* d_sims, int64_t n, void* d_workspace,
+                           int64_t workspace_bytes, int64_t* out_bytes, void* stream);
+int sjb_matches_csv_write(const uint64_t* d_lefts, const uint64_t* d_rights,
+                          const float* d_sims, int64_t n, const void* d_workspace,
+                          int64_t workspace_bytes, uint8_t* d_out, int64_t out_cap,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

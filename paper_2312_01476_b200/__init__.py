@@ -30,6 +30,8 @@ _LAZY = {
     "embed_relation_device": "embedding", "prepare_relation": "embedding", "decode": "embedding",
     # device engine
     "prepare": "device", "PreparedRelation": "device",
+    # matches file (cli._write_matches), formatted on the GPU
+    "write_matches": "matchio", "format_matches": "matchio",
 }
 
 

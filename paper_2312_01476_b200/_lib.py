@@ -18,6 +18,7 @@ EXPORTS = (
     "sjb_tile_count", "sjb_join_begin", "sjb_join_filter_tiles", "sjb_join_finish",
     "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm", "sjb_cosine_vm",
     "sjb_scan_hits", "sjb_scan_hits_workspace_bytes",
+    "sjb_matches_csv_workspace_bytes", "sjb_matches_csv_layout", "sjb_matches_csv_write",
 )
 
 SJB_OK = 0
@@ -104,6 +105,10 @@ def lib(path: str = LIB_PATH):
                                 _vp, _i64, _vp]
     L.sjb_scan_hits_workspace_bytes.restype = _i64
     L.sjb_scan_hits_workspace_bytes.argtypes = [_i64]
+    L.sjb_matches_csv_workspace_bytes.restype = _i64
+    L.sjb_matches_csv_workspace_bytes.argtypes = [_i64]
+    L.sjb_matches_csv_layout.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, ctypes.POINTER(_i64), _vp]
+    L.sjb_matches_csv_write.argtypes = [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise ImportError(f"{path} does not export {name}")

@@ -19,6 +19,7 @@
 #include "sjb_join3.cu"
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
+#include "sjb_fmt.cu"
 
 namespace {
 
@@ -1040,6 +1041,94 @@ int sjb_scan_hits(const float* d_buf, int64_t nl, int64_t nr, float theta, uint6
                                                  d_lefts, d_rights, d_sims);
   SJB_CK_LAUNCH("dense_fill");
   SJB_CK(cudaStreamSynchronize(st));
+  return SJB_OK;
+}
+
+// ----------------------------------------------------------- matches file
+int64_t sjb_matches_csv_workspace_bytes(int64_t n) {
+  const int64_t ng = sjb::ceil_div(n > 0 ? n : 0, sjb::fmt::kLines);
+  const int64_t nb = sjb::ceil_div(ng, sjb::kScanBlock) + 1;
+  const size_t nl = (size_t)(n > 0 ? n : 0);
+  return (int64_t)(align256((size_t)ng * 4) + align256((size_t)(ng + 1) * 8) +
+                   align256((size_t)(nb + 1) * 8) + align256(nl * 8) + align256(nl * 4));
+}
+
+// workspace: group lengths | group offsets | scan block sums | digits | meta
+struct CsvWs {
+  uint32_t* glen;
+  uint64_t* goff;
+  uint64_t* bsums;
+  uint64_t* digs;
+  uint32_t* meta;
+};
+
+static CsvWs csv_ws(const void* base, int64_t n) {
+  uint8_t* ws = reinterpret_cast<uint8_t*>(const_cast<void*>(base));
+  const int64_t ng = sjb::ceil_div(n, sjb::fmt::kLines);
+  const int64_t nb = sjb::ceil_div(ng, sjb::kScanBlock) + 1;
+  CsvWs w;
+  size_t o = 0;
+  w.glen = reinterpret_cast<uint32_t*>(ws + o);
+  o += align256((size_t)ng * 4);
+  w.goff = reinterpret_cast<uint64_t*>(ws + o);
+  o += align256((size_t)(ng + 1) * 8);
+  w.bsums = reinterpret_cast<uint64_t*>(ws + o);
+  o += align256((size_t)(nb + 1) * 8);
+  w.digs = reinterpret_cast<uint64_t*>(ws + o);
+  o += align256((size_t)n * 8);
+  w.meta = reinterpret_cast<uint32_t*>(ws + o);
+  return w;
+}
+
+static int csv_check(const uint64_t* l, const uint64_t* r, const float* s, int64_t n,
+                     int64_t workspace_bytes) {
+  if (n < 0) return fail(SJB_E_INVALID, "negative match count");
+  if (n > 0 && (!l || !r || !s)) return fail(SJB_E_INVALID, "null match column");
+  if (workspace_bytes < sjb_matches_csv_workspace_bytes(n))
+    return fail(SJB_E_INVALID, "matches_csv workspace too small");
+  if (sjb::ceil_div(n, sjb::fmt::kLines) > (int64_t)sjb::kScanBlock * sjb::kScanBlock)
+    return fail(SJB_E_UNSUPPORTED, "too many matches for one call");
+  return SJB_OK;
+}
+
+int sjb_matches_csv_layout(const uint64_t* d_lefts, const uint64_t* d_rights,
+                           const float* d_sims, int64_t n, void* d_workspace,
+                           int64_t workspace_bytes, int64_t* out_bytes, void* stream) {
+  if (!out_bytes) return fail(SJB_E_INVALID, "null out_bytes");
+  *out_bytes = 0;
+  if (int rc = csv_check(d_lefts, d_rights, d_sims, n, workspace_bytes)) return rc;
+  if (n == 0) return SJB_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t ng = sjb::ceil_div(n, sjb::fmt::kLines);
+  const CsvWs w = csv_ws(d_workspace, n);
+  sjb::fmt::csv_layout_kernel<<<(unsigned)ng, sjb::fmt::kLines, 0, st>>>(
+      d_lefts, d_rights, d_sims, n, w.glen, w.digs, w.meta);
+  SJB_CK_LAUNCH("csv_layout");
+  if (int rc = run_scan(w.glen, ng, w.goff, nullptr, w.bsums, st)) return rc;
+  uint64_t total = 0;
+  SJB_CK(cudaMemcpyAsync(&total, w.goff + ng, 8, cudaMemcpyDeviceToHost, st));
+  SJB_CK(cudaStreamSynchronize(st));
+  *out_bytes = (int64_t)total;
+  return SJB_OK;
+}
+
+int sjb_matches_csv_write(const uint64_t* d_lefts, const uint64_t* d_rights,
+                          const float* d_sims, int64_t n, const void* d_workspace,
+                          int64_t workspace_bytes, uint8_t* d_out, int64_t out_cap,
+                          void* stream) {
+  if (int rc = csv_check(d_lefts, d_rights, d_sims, n, workspace_bytes)) return rc;
+  if (n == 0) return SJB_OK;
+  if (!d_out) return fail(SJB_E_INVALID, "null output buffer");
+  cudaStream_t st = as_stream(stream);
+  const int64_t ng = sjb::ceil_div(n, sjb::fmt::kLines);
+  const CsvWs w = csv_ws(d_workspace, n);
+  uint64_t total = 0;  // checked against the capacity: a layout from other inputs is an error
+  SJB_CK(cudaMemcpyAsync(&total, w.goff + ng, 8, cudaMemcpyDeviceToHost, st));
+  SJB_CK(cudaStreamSynchronize(st));
+  if ((int64_t)total > out_cap) return fail(SJB_E_INVALID, "output buffer too small");
+  sjb::fmt::csv_write_kernel<<<(unsigned)ng, sjb::fmt::kLines, 0, st>>>(
+      d_lefts, d_rights, w.digs, w.meta, n, w.goff, d_out);
+  SJB_CK_LAUNCH("csv_write");
   return SJB_OK;
 }
 

@@ -529,3 +529,67 @@ def test_cuda_kernel_backend(cuda, golden):
     v = np.empty((len(toks), 16), np.float32)
     K.synthetic_fill_many(seeds, v)
     assert np.array_equal(v.view(np.uint32), golden["syn_16_7"].view(np.uint32))
+
+
+def _first_diff(a: bytes, b: bytes) -> str:
+    i = next((k for k in range(min(len(a), len(b))) if a[k] != b[k]), min(len(a), len(b)))
+    s = a.rfind(b"\n", 0, i) + 1
+    return f"at byte {i}: got {a[s:s + 60]!r} want {b[s:s + 60]!r}"
+
+
+def test_matches_file_bytes_match_reference_writer(cuda):
+    """GPU matches file == the reference writer (cli.py:99-108, numpy per line)
+    on probe floats (sweeps, powers of two, denormals, signs, inf/nan, -0) and
+    u64 offsets of every decimal length."""
+    import fmt_oracle as F
+    from paper_2312_01476_b200.matchio import format_columns_device
+    bits = F.probe_bits(60000, seed=1)
+    bits = np.concatenate([bits, np.uint32([0, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00000])])
+    n = bits.size
+    rng = np.random.default_rng(5)
+    lefts = (rng.random(n) * 10.0 ** rng.integers(0, 19, n)).astype(np.uint64)
+    rights = rng.integers(0, 2**63, n, dtype=np.int64).astype(np.uint64) >> rng.integers(0, 63, n).astype(np.uint64)
+    lefts[:3] = [0, 2**64 - 1, 10**19]
+    sims = bits.view(np.float32)
+    got = format_columns_device(torch.from_numpy(lefts.view(np.int64)).to(cuda),
+                                torch.from_numpy(rights.view(np.int64)).to(cuda),
+                                torch.from_numpy(sims).to(cuda)).cpu().numpy().tobytes()
+    want = F.matches_file_reference(lefts, rights, sims)
+    assert got == want, _first_diff(got, want)
+
+
+def test_matches_file_of_a_join(cuda, tmp_path, manifest, golden):
+    """write_matches of real join results (MatchSet and DeviceMatches), the
+    empty result, and a 2M-line round trip."""
+    import fmt_oracle as F
+    from paper_2312_01476_b200 import MatchSet, device as D
+    from paper_2312_01476_b200.matchio import format_matches, write_matches
+    for name in ("c_small", "c_d16_neg", "cfg1"):
+        lo, ro, so = golden[name + "_l"], golden[name + "_r"], golden[name + "_s"]
+        ms = MatchSet("left", "right", lo, ro, so)
+        p = tmp_path / f"{name}.csv"
+        write_matches(str(p), ms)
+        assert p.read_bytes() == F.matches_file_reference(lo, ro, so)
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                        D.prepare(torch.from_numpy(S).to(cuda)), meta["theta"])
+    assert format_matches(m) == F.matches_file_reference(*m.to_host())
+    write_matches(str(tmp_path / "empty.csv"), MatchSet("a", "b"))
+    assert (tmp_path / "empty.csv").read_bytes() == b""
+    # size-independent property at 2M lines: the file parses back to the columns
+    n = 2_000_000
+    rng = np.random.default_rng(9)
+    lefts = np.sort(rng.integers(0, 10**6, n)).astype(np.uint64)
+    rights = rng.integers(0, 4 * 10**6, n).astype(np.uint64)
+    sims = rng.uniform(-1, 1, n).astype(np.float32)
+    text = format_matches(MatchSet("a", "b", lefts, rights, sims))
+    assert text.count(b"\n") == n and text.endswith(b"\n")
+    cols = np.array(text.decode().replace("\n", ",").split(",")[:-1]).reshape(n, 3)
+    assert np.array_equal(cols[:, 0].astype(np.uint64), lefts)
+    assert np.array_equal(cols[:, 1].astype(np.uint64), rights)
+    assert np.array_equal(cols[:, 2].astype(np.float64).astype(np.float32), sims)
+    k = rng.integers(0, n, 20000)
+    sub = F.matches_file_reference(lefts[k], rights[k], sims[k]).split(b"\n")[:-1]
+    lines = text.split(b"\n")
+    assert all(lines[i] == s for i, s in zip(k, sub))

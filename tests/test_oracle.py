@@ -96,3 +96,20 @@ def test_cosine_vm_restatement_matches_reference(golden):
     denom = np.multiply(np.float32(na), O.row_norms(m), dtype=np.float32)
     got = np.divide(O.dots_vm(a, m), denom, dtype=np.float32)
     assert np.array_equal(got.view(np.uint32), golden["cos_vm_out"].view(np.uint32))
+
+
+def test_matches_file_format_restatement_pinned_to_numpy():
+    """The Dragon4 restatement (oracle/fmt_oracle.py) equals numpy's
+    format_float_positional(unique=True, trim='-') -- the reference's _fmt_sim
+    (cli.py:99-102) -- on sweeps, powers of two, denormals and random bits."""
+    import fmt_oracle as F
+    bits = F.probe_bits(20000)
+    vals = bits.view(np.float32)
+    bad = [hex(int(b)) for b, v in zip(bits, vals) if F.fmt_sim(v) != F.fmt_sim_numpy(v)]
+    assert not bad, bad[:5]
+    for v, want in ((0.0, "0"), (-0.0, "-0"), (1.0, "1"), (0.5, "0.5"), (100.0, "100"),
+                    (np.inf, "inf"), (-np.inf, "-inf"), (np.nan, "nan"), (0.1, "0.1"),
+                    (np.float32(0.8), "0.8"), (1e-45, "0." + "0" * 44 + "1")):
+        assert F.fmt_sim(v) == F.fmt_sim_numpy(v) == want, v
+    assert (F.matches_file_reference([0, 2**64 - 1], [5, 7], np.float32([0.25, -1.0]))
+            == b"0,5,0.25\n18446744073709551615,7,-1\n")

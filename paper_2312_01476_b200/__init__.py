@@ -32,6 +32,10 @@ _LAZY = {
     "prepare": "device", "PreparedRelation": "device",
     # matches file (cli._write_matches), formatted on the GPU
     "write_matches": "matchio", "format_matches": "matchio",
+    # cost model (cost.py), calibrated on the GPU
+    "CostParams": "cost", "calibrate": "cost", "choose_plan": "cost",
+    "estimate_tensor": "cost", "estimate_nlj_prefetch": "cost", "estimate_nlj_naive": "cost",
+    "estimate_selection": "cost",
 }
 
 

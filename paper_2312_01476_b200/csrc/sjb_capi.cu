@@ -987,13 +987,27 @@ int sjb_tile_dot(const float* d_left, int64_t lda, const float* d_bt, int64_t ld
   return SJB_OK;
 }
 
+// persistent grid for vm_rows_kernel: one wave (the CTAs that fit per SM,
+// from the occupancy calculator), fewer when the rows run out
+static unsigned vm_grid(int64_t n, const void* kernel, int* per_sm) {
+  if (*per_sm == 0) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, sjb::kVmWarps * 32, 0);
+    *per_sm = v > 0 ? v : 1;
+  }
+  const int64_t groups = sjb::ceil_div(n > 0 ? n : 1, 32);
+  const int64_t need = sjb::ceil_div(groups, sjb::kVmWarps);
+  const int64_t cap = (int64_t)sjb_sm_count(current_device()) * *per_sm;
+  return (unsigned)(need < cap ? need : cap);
+}
+static int vm_per_sm_cos = 0, vm_per_sm_dot = 0;
+
 int sjb_cosine_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
                   int* d_flags, void* stream) {
   if (n < 0 || dim < 1) return fail(SJB_E_INVALID, "bad shape");
   if (!d_flags) return fail(SJB_E_INVALID, "null flags");
-  const unsigned blocks = (unsigned)(n > 0 ? sjb::ceil_div(n, 256) : 1);
-  sjb::cosine_vm_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_a, d_m, n, (int)dim, d_out,
-                                                               d_flags);
+  sjb::vm_rows_kernel<true><<<vm_grid(n, (const void*)sjb::vm_rows_kernel<true>, &vm_per_sm_cos), sjb::kVmWarps * 32, 0, as_stream(stream)>>>(
+      d_a, d_m, n, (int)dim, d_out, d_flags);
   SJB_CK_LAUNCH("cosine_vm");
   return SJB_OK;
 }
@@ -1001,8 +1015,8 @@ int sjb_cosine_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, fl
 int sjb_dots_vm(const float* d_a, const float* d_m, int64_t n, int64_t dim, float* d_out,
                 void* stream) {
   if (n <= 0) return SJB_OK;
-  sjb::dots_vm_kernel<<<(unsigned)sjb::ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
-      d_a, d_m, n, (int)dim, d_out);
+  sjb::vm_rows_kernel<false><<<vm_grid(n, (const void*)sjb::vm_rows_kernel<false>, &vm_per_sm_dot), sjb::kVmWarps * 32, 0, as_stream(stream)>>>(
+      d_a, d_m, n, (int)dim, d_out, nullptr);
   SJB_CK_LAUNCH("dots_vm");
   return SJB_OK;
 }

@@ -529,43 +529,159 @@ tile_dot_kernel(const float* __restrict__ left, int64_t lda, const float* __rest
     }
 }
 
-__global__ void dots_vm_kernel(const float* __restrict__ a, const float* __restrict__ m, int64_t n,
-                               int dim, float* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = dot_seq_dev(a, m + i * dim, dim);
-}
-
 // cosine_vm (linalg.py:70-84): out[i] = dot(a, m_i) / (||a|| * ||m_i||) with
 // the reference's arithmetic -- sequential fmaf dot (sj_dots_vm), norms as
 // fp64 sequential sums rounded to fp32 (sj_row_norms), then one fp32 multiply
 // and one fp32 divide (numpy float32 ufuncs, round to nearest).  flags bit 0:
 // ||a|| == 0, bit 1: some ||m_i|| == 0 (the reference raises ZeroVector).
+// dots_vm (sj_dots_vm, _kernelcore.c:126-133) is the same kernel without the
+// norms.
 __device__ __forceinline__ float row_norm_dev(const float* x, int dim) {
   double ss = 0.0;
+#pragma unroll 8
   for (int d = 0; d < dim; d++) {
     const double v = (double)x[d];
-    ss = __dadd_rn(ss, __dmul_rn(v, v));
+    ss = __fma_rn(v, v, ss);
   }
   return __double2float_rn(sqrt(ss));
 }
 
-__global__ void cosine_vm_kernel(const float* __restrict__ a, const float* __restrict__ m,
-                                 int64_t n, int dim, float* __restrict__ out,
-                                 int* __restrict__ flags) {
-  __shared__ float na_s;
-  if (threadIdx.x == 0) {
-    na_s = row_norm_dev(a, dim);
-    if (blockIdx.x == 0 && na_s == 0.0f) atomicOr(flags, 1);
+// Persistent CTAs of 4 warps.  A warp owns 32 rows at a time and walks them
+// in 32-column chunks; its (row group, chunk) items stream through two shared
+// tiles with cp.async (item i+1 in flight while item i is consumed), every
+// global load a coalesced row segment (16-byte copies when the rows allow).
+// Lane r advances row r's chains -- the fp32 fmaf dot and the fp64 sum of
+// squares -- over the chunk in column order, reading its row and the probe's
+// chunk as 128-bit shared loads (pitch 36: conflict-free), so the arithmetic
+// is exactly one-row-per-thread's.  The square of an fp32 value is exact in
+// fp64, so dadd(ss, dmul(v, v)) == fma(v, v, ss): one DFMA per element.
+constexpr int kVmWarps = 4;
+constexpr int kVmPitch = 36;
+
+__device__ __forceinline__ void vm_cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void vm_cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+template <bool kCos>
+__device__ __forceinline__ void vm_step(float& acc, double& ss, float ak, float x) {
+  acc = __fmaf_rn(ak, x, acc);
+  if (kCos) {
+    const double v = (double)x;
+    ss = __fma_rn(v, v, ss);
   }
-  __syncthreads();
-  const float na = na_s;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float* row = m + i * dim;
-  const float dot = dot_seq_dev(a, row, dim);
-  const float nr = row_norm_dev(row, dim);
-  if (nr == 0.0f) atomicOr(flags, 2);
-  out[i] = __fdiv_rn(dot, __fmul_rn(na, nr));
+}
+
+template <bool kCos>
+__global__ void __launch_bounds__(kVmWarps * 32)
+vm_rows_kernel(const float* __restrict__ a, const float* __restrict__ m, int64_t n, int dim,
+               float* __restrict__ out, int* __restrict__ flags) {
+  __shared__ __align__(16) float tile[kVmWarps][2][32][kVmPitch];
+  __shared__ __align__(16) float ash[kVmWarps][2][32];
+  __shared__ float na_s;
+  __shared__ volatile int na_ready;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (kCos) {
+    if (threadIdx.x == 0) na_ready = 0;
+    __syncthreads();
+    // the probe norm is a sequential chain: thread 0 runs it while the other
+    // warps start streaming; they wait for it only before their first write
+    if (threadIdx.x == 0) {
+      na_s = row_norm_dev(a, dim);
+      if (blockIdx.x == 0 && na_s == 0.0f) atomicOr(flags, 1);
+      __threadfence_block();
+      na_ready = 1;
+    }
+  }
+  bool have_na = false;
+  const int64_t groups = (n + 31) / 32;
+  const int64_t gstride = (int64_t)gridDim.x * kVmWarps;
+  const int nch = (dim + 31) / 32;
+  const bool vec = (dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) |
+                                       reinterpret_cast<uintptr_t>(m)) & 15) == 0;
+  auto issue = [&](int64_t g, int c, int b) {
+    if (g < groups) {
+      const int64_t r0 = g * 32;
+      const int rows = (int)mn<int64_t>(32, n - r0);
+      const int c0 = c * 32;
+      if (vec) {
+        const int q = lane & 7;
+        if (c0 + 4 * q < dim) {
+          const float* src = m + r0 * dim + c0 + 4 * q;
+          for (int r = lane >> 3; r < rows; r += 4)
+            vm_cp_async16(&tile[warp][b][r][4 * q], src + (int64_t)r * dim);
+          if (lane < 8) vm_cp_async16(&ash[warp][b][4 * q], a + c0 + 4 * q);
+        }
+      } else if (c0 + lane < dim) {
+        const float* src = m + r0 * dim + c0 + lane;
+        for (int r = 0; r < rows; r++) vm_cp_async4(&tile[warp][b][r][lane], src + (int64_t)r * dim);
+        vm_cp_async4(&ash[warp][b][lane], a + c0 + lane);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t g = (int64_t)blockIdx.x * kVmWarps + warp;
+  int c = 0, b = 0;
+  issue(g, 0, 0);
+  float acc = 0.0f;
+  double ss = 0.0;
+  while (g < groups) {
+    int64_t gn = g;
+    int cn = c + 1;
+    if (cn == nch) {
+      cn = 0;
+      gn = g + gstride;
+    }
+    issue(gn, cn, b ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const int cols = min(32, dim - c * 32);
+    const float4* rw = reinterpret_cast<const float4*>(tile[warp][b][lane]);
+    const float4* av = reinterpret_cast<const float4*>(ash[warp][b]);
+    if (cols == 32) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const float4 x = rw[q], y = av[q];
+        vm_step<kCos>(acc, ss, y.x, x.x);
+        vm_step<kCos>(acc, ss, y.y, x.y);
+        vm_step<kCos>(acc, ss, y.z, x.z);
+        vm_step<kCos>(acc, ss, y.w, x.w);
+      }
+    } else {
+      const float* rs = tile[warp][b][lane];
+      const float* as = ash[warp][b];
+      for (int k = 0; k < cols; k++) vm_step<kCos>(acc, ss, as[k], rs[k]);
+    }
+    __syncwarp();
+    if (c == nch - 1) {
+      const int64_t i = g * 32 + lane;
+      if (i < n) {
+        if (kCos) {
+          if (!have_na) {
+            while (na_ready == 0) {
+            }
+            __threadfence_block();
+            have_na = true;
+          }
+          const float nr = __double2float_rn(sqrt(ss));
+          if (nr == 0.0f) atomicOr(flags, 2);
+          out[i] = __fdiv_rn(acc, __fmul_rn(na_s, nr));
+        } else {
+          out[i] = acc;
+        }
+      }
+      acc = 0.0f;
+      ss = 0.0;
+    }
+    g = gn;
+    c = cn;
+    b ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Dense threshold scan, row-major order (sj_scan_count / sj_scan_fill).

@@ -13,9 +13,10 @@ namespace sjb {
 
 constexpr int kPrepThreads = 128;
 
-// Sequential fp64 sum of squares (no contraction: the square is exact and
-// __dadd_rn pins the rounding), repair rule, fp64 divide -- the reference's
-// normalize_row (_kernelcore.c:79-97).  Operates on one smem row.
+// Sequential fp64 sum of squares, repair rule, fp64 divide -- the reference's
+// normalize_row (_kernelcore.c:79-97).  Operates on one smem row.  The square
+// of an fp32 value is exact in fp64 (<= 48 significant bits), so the
+// reference's ss + x*x (one rounding, in the add) is exactly fma(x, x, ss).
 // With `err` != nullptr the same final pass also measures the row's fp16
 // rounding error ||fp16(x) - x||_2 (exact squares, fp64 sum, rounded up): the
 // per-row term of the filter band (sjb_common.cuh row_cutoff).
@@ -23,7 +24,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
   double ss = 0.0;
   for (int d = 0; d < dim; d++) {
     double x = (double)row[d];
-    ss = __dadd_rn(ss, __dmul_rn(x, x));
+    ss = __fma_rn(x, x, ss);
   }
   double norm = sqrt(ss);
   int repaired = 0;
@@ -32,7 +33,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
     ss = 0.0;
     for (int d = 0; d < dim; d++) {
       double x = (double)row[d];
-      ss = __dadd_rn(ss, __dmul_rn(x, x));
+      ss = __fma_rn(x, x, ss);
     }
     norm = sqrt(ss);
     repaired = 1;
@@ -60,7 +61,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
       // fp16(x) - x is exact in fp32 (at most 13 significant bits, or x itself
       // when it rounds to zero), so the fp32 difference equals the fp64 one
       const double e = (double)__fsub_rn(from_op16(to_op16(x)), x);
-      es = __dadd_rn(es, __dmul_rn(e, e));
+      es = __fma_rn(e, e, es);
     }
     *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
   }
@@ -386,7 +387,7 @@ __global__ void row_norms_kernel(const float* __restrict__ m, int64_t n, int dim
   double ss = 0.0;
   for (int d = 0; d < dim; d++) {
     double x = (double)row[d];
-    ss = __dadd_rn(ss, __dmul_rn(x, x));
+    ss = __fma_rn(x, x, ss);
   }
   out[i] = __double2float_rn(sqrt(ss));
 }

@@ -33,14 +33,20 @@ def cosine_vm_device(a, m: torch.Tensor) -> torch.Tensor:
     """Cosine of vector `a` against every row of the (n, dim) CUDA tensor `m`
     (a device fp32 tensor of n sims).  Raises ZeroVector like the reference
     (zero-norm probe, or a zero-norm row)."""
-    va = _as_f32_vector(a)
     if not m.is_cuda or m.dtype != torch.float32 or m.dim() != 2:
         raise ValueError("m must be a 2-D float32 CUDA tensor")
-    check_dims(va.shape[0], m.shape[1])
     n, dim = m.shape
     dev = m.device
+    if isinstance(a, torch.Tensor) and a.is_cuda:   # stays on the device
+        if a.dim() != 1:
+            raise ValueError(f"expected a vector, got shape {tuple(a.shape)}")
+        check_dims(a.shape[0], dim)
+        ta = a.to(device=dev, dtype=torch.float32).contiguous()
+    else:
+        va = _as_f32_vector(a)
+        check_dims(va.shape[0], dim)
+        ta = torch.from_numpy(va).to(dev)
     m = m.contiguous()
-    ta = torch.from_numpy(va).to(dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     if dim == 0:

@@ -593,3 +593,19 @@ def test_matches_file_of_a_join(cuda, tmp_path, manifest, golden):
     sub = F.matches_file_reference(lefts[k], rights[k], sims[k]).split(b"\n")[:-1]
     lines = text.split(b"\n")
     assert all(lines[i] == s for i, s in zip(k, sub))
+
+
+def test_cost_calibration_on_device(cuda):
+    """calibrate (cost.py:138-195) measured on the GPU: valid constants, and
+    the plan choice routes BASELINE-sized joins to the tensor join."""
+    from paper_2312_01476_b200 import SyntheticModel
+    from paper_2312_01476_b200.cost import CostParams, calibrate, choose_plan
+    model = SyntheticModel(100, seed=7)
+    p = calibrate(model, 100, sample_sizes=(1000,))
+    assert isinstance(p, CostParams) and 0.0 < p.tensor_efficiency < 1.0
+    assert p.access_ns > 0 and p.model_ns > 0 and p.compare_per_dim_ns > 0
+    assert model.call_count > 0
+    for l, r in ((10_000, 10_000), (100_000, 1_000_000)):
+        assert choose_plan(l, r, 100, 64 << 20, p)[0] == "tensor"
+    with pytest.raises(ValueError):
+        calibrate(model, 100, sample_sizes=(10,))

@@ -142,3 +142,34 @@ def test_native_token_packer_matches_python():
         assert bytes(b) == data and np.array_equal(o, want)
     with pytest.raises(TypeError):
         _sjbpack.pack(["a", 3])
+
+
+def test_cost_model_matches_reference_goldens():
+    """Estimates and plan choice equal the reference's cost model to the bit
+    (tests/golden/cost_golden.json, made by running reference cost.py)."""
+    import json
+    import os
+    from paper_2312_01476_b200.cost import CostParams, choose_plan, estimate_selection
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cost_golden.json")) as fh:
+        cases = json.load(fh)["cases"]
+    assert len(cases) > 50
+    for c in cases:
+        p = CostParams(**c["params"])
+        plan, est = choose_plan(c["left"], c["right"], c["dim"], c["budget"], p)
+        assert plan == c["plan"], c
+        assert {k: float(v).hex() for k, v in est.items()} == c["estimates"], c
+        assert float(estimate_selection(c["left"], c["dim"], p)).hex() == c["selection"]
+    assert {c["plan"] for c in cases} >= {"tensor", "prefetch_nlj"}
+
+
+def test_cost_params_validation_and_json():
+    from paper_2312_01476_b200.cost import CostParams
+    p = CostParams(1.0, 2.0, 3.0, 0.5, 0.25)
+    assert CostParams.from_json(p.to_json()) == p and p.compare_ns(10) == 8.0
+    for bad in (dict(access_ns=-1.0), dict(tensor_efficiency=0.0), dict(tensor_efficiency=1.5)):
+        kw = dict(access_ns=1.0, model_ns=1.0, compare_base_ns=1.0, compare_per_dim_ns=1.0)
+        kw.update(bad)
+        with pytest.raises(ValueError):
+            CostParams(**kw)
+    with pytest.raises(ValueError, match="missing"):
+        CostParams.from_dict({"access_ns": 1.0})

@@ -15,7 +15,7 @@ $C2 > /dev/null && ncu --set full --clock-control none --import-source on -k reg
   -s 1 -c 1 -o $O/${TAG}_filter_cfg2 $C2 > /dev/null 2>&1
 $C4 > /dev/null && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches_cfg4.csv $C4 > /dev/null 2>&1
-$C4 > /dev/null && ncu --set full --clock-control none -k "regex:filter_kernel|recheck_tma" -s 2 -c 2 \
+$C4 > /dev/null && ncu --set full --clock-control none -k "regex:filter_kernel|recheck_group" -s 2 -c 2 \
   -o $O/${TAG}_wide_cfg4 $C4 > /dev/null 2>&1
 $C5 > /dev/null && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches_cfg5.csv $C5 > /dev/null 2>&1

@@ -288,48 +288,59 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     const uint32_t lane_base = (uint32_t)q * 32;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     const uint64_t seg_cap = p.seg_cap;
-    uint32_t acc_it = 0;
     const bool edbg = SJB_PROFILE && p.debug_mode == 9 && blockIdx.x < 3 && (ew == 0 || ew == 15);
     long long e_wait = 0, e_drain = 0, e_mark = 0;
     const long long e_start = clock64();
+    // Per-stage work is kept to the drain, the 64-value maximum and one
+    // compare: everything that depends only on the item (row validity, the
+    // row's band terms) or on the half (TMEM address) is hoisted.  With two
+    // accumulator stages and two halves per S tile, stage == half and the
+    // stage phase flips once per tile.
+    const uint32_t tbase = tmem_base + (lane_base << 16) + (uint32_t)cq * 64;
+    const bool no_drain = p.debug_mode == 2 || p.debug_mode >= 16;   // diagnostics
+    const bool no_emit = p.debug_mode == 1;
+    const bool per_row = p.row_err != nullptr;
+    uint32_t tph = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
-      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
-      const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
-      // per-row band terms: this lane's two R rows (once per item)
-      const bool per_row = p.row_err != nullptr;
-      const float ex0 = load_err(p.row_err, rb * kBM + lane_base + lane, p.n_a);
-      const float ex1 = load_err(p.row_err, rb * kBM + 128 + lane_base + lane, p.n_a);
-      for (int64_t t = t0; t < t1; t++) {
+      const int t0 = p.tile_begin + (int)sc * p.tiles_per_chunk;
+      const int t1 = mn<int>(t0 + p.tiles_per_chunk, p.n_btiles);
+      // per-row band: cutoff = max(cutoff, theta - slack - (1+1e-6)(ex + ey)
+      // - ex*ey) = max(cutoff, cA - cB*ey); the 2e-6 in `slack` covers the
+      // fp32 evaluation of either form
+      float cA[2], cB[2];
+      bool rok[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t gi = rb * kBM + h * 128 + lane_base + lane;
+        rok[h] = gi < p.n_a && !no_emit;
+        const float ex = load_err(p.row_err, gi, p.n_a);
+        cA[h] = per_row ? p.theta - p.slack - 1.000001f * ex : p.cutoff;
+        cB[h] = per_row ? 1.000001f + ex : 0.0f;
+      }
+      for (int t = t0; t < t1; t++) {
         // issued before the accumulator wait: its latency hides behind it
         const float ey = per_row ? __ldg(p.tile_err + t) : 0.0f;
-#pragma unroll 1
+#pragma unroll
         for (int h = 0; h < 2; h++) {
-          const uint32_t as = acc_it & 1u;
           const long long e0 = edbg ? clock64() : 0;
-          mbar_wait(&acc_full[as], (acc_it >> 1) & 1u);
+          mbar_wait(&acc_full[h], tph);
           if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
           tc_fence_after();
-          if (p.debug_mode == 2 || p.debug_mode >= 16) {
+          if (no_drain) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[as]);
-            acc_it++;
+            if (lane == 0) mbar_arrive(&acc_empty[h]);
             continue;
           }
           float v[64];
-          const uint32_t taddr = tmem_base + (lane_base << 16) + as * kUmmaN + cq * 64;
-          SJB_TMEM_LD64(taddr, v);
+          SJB_TMEM_LD64(tbase + h * kUmmaN, v);
           tc_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_relaxed(&acc_empty[as]);
-          acc_it++;
+          if (lane == 0) mbar_arrive_relaxed(&acc_empty[h]);
           if (edbg) e_drain += clock64() - e_mark;
 
-          const int64_t gi64 = rb * kBM + h * 128 + lane_base + lane;
-          const bool row_ok = gi64 < p.n_a;
-          const float cutoff =
-              per_row ? cutoff_from(p.cutoff, p.theta, p.slack, h ? ex1 : ex0, ey) : p.cutoff;
+          const float cutoff = fmaxf(p.cutoff, fmaf(-cB[h], ey, cA[h]));
           // group maxima over 8 columns, then the warp-tile maximum
           float g[8];
 #pragma unroll
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           }
           const float m =
               fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
-          const bool hit = row_ok && (m >= cutoff) && p.debug_mode != 1;
+          const bool hit = rok[h] && (m >= cutoff);
           if (__any_sync(0xffffffffu, hit)) {
             // Slow path (warp-uniform): each hit thread builds a 64-bit mask
             // of its columns >= cutoff (only inside groups whose maximum hit),
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
                   else mk1 |= b << (8 * (k - 4));
                 }
               }
-              const int64_t col_lim = p.n_b - t * kBN - cq * 64;  // columns >= col_lim: padding
+              const int64_t col_lim = p.n_b - (int64_t)t * kBN - cq * 64;  // >= col_lim: padding
               if (col_lim < 64) {
                 const int cl = (int)mx<int64_t>(col_lim, 0);
                 mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
               base = __shfl_sync(0xffffffffu, base, 31);
               pos = (uint64_t)base + (incl - cnt);
             }
-            const uint32_t gi = (uint32_t)gi64;
+            const uint32_t gi = (uint32_t)(rb * kBM + h * 128 + lane_base + lane);
             const uint32_t j0 = (uint32_t)(t * kBN + cq * 64);
             uint32_t w = mk0;
             while (w) {
@@ -409,6 +420,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
             }
           }
         }
+        tph ^= 1u;
       }
     }
     if (edbg && lane == 0)

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], kEpiWarps);
+      mbar_init(&acc_empty[i], kEpiWarps / 2);
     }
     for (int s = 0; s < p.stages; s++) {
       mbar_init(&b_full[s], 1);
@@ -278,12 +278,18 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
                    p.append ? (uint64_t)p.cta_count[blockIdx.x] : 0ull);
   } else {
     // ---------------------------------------------------------- epilogue
-    // 16 warps; warp (q, c) drains TMEM lanes 32q..32q+31 (R rows of the
-    // stage's half) x accumulator columns 64c..64c+63 (S rows) of every
-    // stage.  TMEM loads are latency-bound per warp, so the drain rate scales
-    // with the number of warps in flight (tools/tmem_bench.cu).
+    // 16 warps in two stage groups: group g drains accumulator stage g (the
+    // R block's half g) of every S tile, so each warp has two MMA stage times
+    // per stage it drains.  Warp (q, c) of a group reads TMEM lanes
+    // 32q..32q+31 (R rows) x columns 128c..128c+127 (S rows) as two x64
+    // loads; the stage is released after the second load, and a hit lane's
+    // candidate masks are built while its values are live but emitted after
+    // the release, so hits never hold the accumulator.  The slack before the
+    // MMA waits is a whole stage plus the other group's stage, which absorbs
+    // the emission of hit chunks (tools/power_modes.py).
     const int ew = warp - 2;
-    const int cq = ew >> 2;           // 64-column quarter of the 256-column stage
+    const int grp = ew >> 3;          // accumulator stage == R half drained
+    const int cq = (ew >> 2) & 1;     // 128-column half of the 256-column stage
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t lane_base = (uint32_t)q * 32;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
@@ -291,15 +297,66 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     const bool edbg = SJB_PROFILE && p.debug_mode == 9 && blockIdx.x < 3 && (ew == 0 || ew == 15);
     long long e_wait = 0, e_drain = 0, e_mark = 0;
     const long long e_start = clock64();
-    // Per-stage work is kept to the drain, the 64-value maximum and one
-    // compare: everything that depends only on the item (row validity, the
-    // row's band terms) or on the half (TMEM address) is hoisted.  With two
-    // accumulator stages and two halves per S tile, stage == half and the
-    // stage phase flips once per tile.
-    const uint32_t tbase = tmem_base + (lane_base << 16) + (uint32_t)cq * 64;
+    const uint32_t tbase = tmem_base + (lane_base << 16) + (uint32_t)grp * kUmmaN + (uint32_t)cq * 128;
     const bool no_drain = p.debug_mode == 2 || p.debug_mode >= 16;   // diagnostics
     const bool no_emit = p.debug_mode == 1;
     const bool per_row = p.row_err != nullptr;
+    // columns of a 64-column chunk that are >= cutoff, inside groups of 8
+    // whose maximum hit (hit lanes only)
+    auto chunk_mask = [&](const float* v, const float* g, float cutoff, uint32_t& mk0,
+                          uint32_t& mk1) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        if (g[k] >= cutoff) {
+          uint32_t b = 0;
+#pragma unroll
+          for (int e = 0; e < 8; e++) b |= (v[8 * k + e] >= cutoff ? 1u : 0u) << e;
+          if (k < 4) mk0 |= b << (8 * k);
+          else mk1 |= b << (8 * (k - 4));
+        }
+      }
+    };
+    // one warp's candidates: slots reserved with one shared atomic, pairs
+    // written in column order (mask bit b of word w = column 32w + b)
+    auto emit = [&](const uint32_t (&mk)[4], uint32_t gi, uint32_t j0) {
+      const uint32_t cnt = __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
+      uint64_t pos;
+      if (__popc(__ballot_sync(0xffffffffu, cnt != 0)) <= 1) {
+        // common case (~1 candidate per hit chunk): the only lane with
+        // candidates reserves its own slots -- no scan, no broadcast
+        uint32_t base = 0;
+        if (cnt) {
+          base = atomicAdd(cta_cnt, cnt);
+          if (base + cnt < base) *cta_sat = 1u;
+        }
+        pos = base;
+      } else {
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t base = 0;
+        if (lane == 31 && wtot) {
+          base = atomicAdd(cta_cnt, wtot);
+          if (base + wtot < base) *cta_sat = 1u;
+        }
+        base = __shfl_sync(0xffffffffu, base, 31);
+        pos = (uint64_t)base + (incl - cnt);
+      }
+#pragma unroll
+      for (int wd = 0; wd < 4; wd++) {
+        uint32_t w = mk[wd];
+        while (w) {
+          const int b = __ffs(w) - 1;
+          w &= w - 1;
+          if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 * wd + b);
+          pos++;
+        }
+      }
+    };
     uint32_t tph = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t rb = item % nb, sc = item / nb;
@@ -308,40 +365,39 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       // per-row band: cutoff = max(cutoff, theta - slack - (1+1e-6)(ex + ey)
       // - ex*ey) = max(cutoff, cA - cB*ey); the 2e-6 in `slack` covers the
       // fp32 evaluation of either form
-      float cA[2], cB[2];
-      bool rok[2];
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int64_t gi = rb * kBM + h * 128 + lane_base + lane;
-        rok[h] = gi < p.n_a && !no_emit;
-        const float ex = load_err(p.row_err, gi, p.n_a);
-        cA[h] = per_row ? p.theta - p.slack - 1.000001f * ex : p.cutoff;
-        cB[h] = per_row ? 1.000001f + ex : 0.0f;
-      }
+      const int64_t gi64 = rb * kBM + grp * 128 + lane_base + lane;
+      const bool rok = gi64 < p.n_a && !no_emit;
+      const float ex = load_err(p.row_err, gi64, p.n_a);
+      const float cA = per_row ? p.theta - p.slack - 1.000001f * ex : p.cutoff;
+      const float cB = per_row ? 1.000001f + ex : 0.0f;
       for (int t = t0; t < t1; t++) {
         // issued before the accumulator wait: its latency hides behind it
         const float ey = per_row ? __ldg(p.tile_err + t) : 0.0f;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const long long e0 = edbg ? clock64() : 0;
-          mbar_wait(&acc_full[h], tph);
-          if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
-          tc_fence_after();
-          if (no_drain) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[h]);
-            continue;
-          }
-          float v[64];
-          SJB_TMEM_LD64(tbase + h * kUmmaN, v);
-          tc_wait_ld();
-          tc_fence_before();
+        const long long e0 = edbg ? clock64() : 0;
+        mbar_wait(&acc_full[grp], tph);
+        tph ^= 1u;
+        if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
+        tc_fence_after();
+        if (no_drain) {
           __syncwarp();
-          if (lane == 0) mbar_arrive_relaxed(&acc_empty[h]);
-          if (edbg) e_drain += clock64() - e_mark;
-
-          const float cutoff = fmaxf(p.cutoff, fmaf(-cB[h], ey, cA[h]));
-          // group maxima over 8 columns, then the warp-tile maximum
+          if (lane == 0) mbar_arrive(&acc_empty[grp]);
+          continue;
+        }
+        const float cutoff = fmaxf(p.cutoff, fmaf(-cB, ey, cA));
+        uint32_t mk[4] = {0u, 0u, 0u, 0u};
+        bool any_hit = false;
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          float v[64];
+          SJB_TMEM_LD64(tbase + c * 64, v);
+          tc_wait_ld();
+          if (c == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed(&acc_empty[grp]);
+            if (edbg) e_drain += clock64() - e_mark;
+          }
+          // group maxima over 8 columns, then the 64-column maximum
           float g[8];
 #pragma unroll
           for (int k = 0; k < 8; k++) {
@@ -350,77 +406,23 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           }
           const float m =
               fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
-          const bool hit = rok[h] && (m >= cutoff);
+          const bool hit = rok && (m >= cutoff);
           if (__any_sync(0xffffffffu, hit)) {
-            // Slow path (warp-uniform): each hit thread builds a 64-bit mask
-            // of its columns >= cutoff (only inside groups whose maximum hit),
-            // then one warp scan + one shared atomic reserve the warp's slots
-            // and each thread writes its pairs -- no collectives per candidate.
-            uint32_t mk0 = 0, mk1 = 0;
-            if (hit) {
-#pragma unroll
-              for (int k = 0; k < 8; k++) {
-                if (g[k] >= cutoff) {
-                  uint32_t b = 0;
-#pragma unroll
-                  for (int e = 0; e < 8; e++) b |= (v[8 * k + e] >= cutoff ? 1u : 0u) << e;
-                  if (k < 4) mk0 |= b << (8 * k);
-                  else mk1 |= b << (8 * (k - 4));
-                }
-              }
-              const int64_t col_lim = p.n_b - (int64_t)t * kBN - cq * 64;  // >= col_lim: padding
-              if (col_lim < 64) {
-                const int cl = (int)mx<int64_t>(col_lim, 0);
-                mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
-                mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
-              }
-            }
-            const uint32_t cnt = __popc(mk0) + __popc(mk1);
-            uint64_t pos;
-            if (__popc(__ballot_sync(0xffffffffu, cnt != 0)) <= 1) {
-              // common case (~1 candidate per hit chunk): the only lane with
-              // candidates reserves its own slots -- no scan, no broadcast
-              uint32_t base = 0;
-              if (cnt) {
-                base = atomicAdd(cta_cnt, cnt);
-                if (base + cnt < base) *cta_sat = 1u;
-              }
-              pos = base;
-            } else {
-              uint32_t incl = cnt;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-              }
-              const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-              uint32_t base = 0;
-              if (lane == 31 && wtot) {
-                base = atomicAdd(cta_cnt, wtot);
-                if (base + wtot < base) *cta_sat = 1u;
-              }
-              base = __shfl_sync(0xffffffffu, base, 31);
-              pos = (uint64_t)base + (incl - cnt);
-            }
-            const uint32_t gi = (uint32_t)(rb * kBM + h * 128 + lane_base + lane);
-            const uint32_t j0 = (uint32_t)(t * kBN + cq * 64);
-            uint32_t w = mk0;
-            while (w) {
-              const int b = __ffs(w) - 1;
-              w &= w - 1;
-              if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + b);
-              pos++;
-            }
-            w = mk1;
-            while (w) {
-              const int b = __ffs(w) - 1;
-              w &= w - 1;
-              if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
-              pos++;
-            }
+            if (hit) chunk_mask(v, g, cutoff, mk[2 * c], mk[2 * c + 1]);
+            any_hit = true;
           }
         }
-        tph ^= 1u;
+        if (any_hit) {
+          const int64_t col_lim = p.n_b - (int64_t)t * kBN - cq * 128;  // >= col_lim: padding
+          if (col_lim < 128) {
+#pragma unroll
+            for (int wd = 0; wd < 4; wd++) {
+              const int64_t cl = col_lim - 32 * wd;
+              mk[wd] &= cl >= 32 ? ~0u : (cl <= 0 ? 0u : ((1u << cl) - 1u));
+            }
+          }
+          emit(mk, (uint32_t)gi64, (uint32_t)(t * kBN + cq * 128));
+        }
       }
     }
     if (edbg && lane == 0)

@@ -221,7 +221,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 // ------------------------------------------------------------ workspace
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
-      total;
+      work, total;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -245,6 +245,7 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   w.nbig = o;     o = align256(o + 16);
   w.tiles = o;    o = align256(o + (size_t)grid * (size_t)tile_stride * 4);
   w.ncand = o;    o = align256(o + 16);
+  w.work = o;     o = align256(o + 16);
   w.total = o;
   return w;
 }
@@ -591,6 +592,7 @@ struct JoinCtx {
   unsigned int* nbig;
   uint32_t* tile_off;
   uint64_t* ncand;  // dense recheck: number of grouped candidates
+  unsigned int* work;  // wide group recheck: dynamic item counter
   bool empty;  // n_left == 0 or n_right == 0
 };
 
@@ -623,6 +625,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->nbig = reinterpret_cast<unsigned int*>(ws + w.nbig);
   c->tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
   c->ncand = reinterpret_cast<uint64_t*>(ws + w.ncand);
+  c->work = reinterpret_cast<unsigned int*>(ws + w.work);
   return SJB_OK;
 }
 
@@ -788,6 +791,9 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
           } else {
             const int rs = (int)sjb::wide::recheck_group_smem_bytes();
             if (int rc = set_smem_attr((const void*)sjb::wide::recheck_group_kernel, rs)) return rc;
+            SJB_CK(cudaMemsetAsync(c.work, 0, 4, st));
+            tp.b.work = c.work;
+            tp.b.filter_grid = pl.grid;
             sjb::wide::recheck_group_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
           }
         } else {

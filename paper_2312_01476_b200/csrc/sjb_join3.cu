@@ -301,6 +301,8 @@ struct RecheckParams {
   uint32_t* sims_bits;
   uint32_t* rowcount;
   uint32_t direct_max;  // tiles with fewer candidates gather instead of staging
+  unsigned int* work;   // recheck_group_kernel: dynamic item counter (zeroed per launch)
+  int filter_grid;      // the filter's grid (item -> owning segment)
 };
 
 __device__ __forceinline__ void cp_async16(float* dst, const float* src) {
@@ -688,6 +690,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
 constexpr int kGrCap = 8192;        // candidates per group
 constexpr int kGrAStages = 2;
 constexpr int kGrBStages = 3;
+constexpr int kGrQ = 4;             // item queue slots (producer -> compute warps)
 
 __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kRtComputeWarps * 32) : "memory");
@@ -695,7 +698,7 @@ __device__ __forceinline__ void consumer_bar() {
 
 __host__ __device__ constexpr uint32_t recheck_group_smem_bytes() {
   return (kGrAStages + kGrBStages) * kRtOpBytes + 1024 + kGrCap * 4 + kGrCap * 2 +
-         2 * (kGrAStages + kGrBStages) * 8 + 64;
+         2 * (kGrAStages + kGrBStages) * 8 + 3 * kGrQ * 8 + 64;
 }
 
 // Group [k, kend) of an item's tiles (local tile indices into toff), or one
@@ -708,6 +711,36 @@ __device__ __forceinline__ int64_t group_end(const uint32_t* toff, int64_t k, in
   return e == k ? k + 1 : e;
 }
 
+// Where the filter put an item's candidates: it ran item i on CTA i % G as
+// that CTA's (i / G)-th item, recording each of its tiles' first slot in
+// toff (local tile index = tiles of the CTA's earlier items; every S chunk
+// but the last has tiles_per_chunk tiles).
+struct ItemLoc {
+  int64_t owner, k, k_end, t0;
+};
+__device__ __forceinline__ ItemLoc item_loc(const RecheckParams& p, int64_t item) {
+  const int G = p.filter_grid, nb = p.n_ablk, tpc = p.tiles_per_chunk;
+  const int64_t n_chunks = p.n_items / nb;
+  const int64_t last_tiles =
+      mn<int64_t>(tpc, p.n_btiles - (p.tile_begin + (n_chunks - 1) * (int64_t)tpc));
+  const int64_t c = item % G, m = item / G;
+  const int64_t n_full = p.n_items - nb;  // items of every chunk but the last
+  const int64_t cf = n_full > c ? (n_full - c + G - 1) / G : 0;
+  ItemLoc L;
+  L.owner = c;
+  L.k = m <= cf ? m * tpc : cf * tpc + (m - cf) * last_tiles;
+  const int64_t sc = item / nb;
+  L.t0 = p.tile_begin + sc * tpc;
+  const int64_t t1 = mn<int64_t>(L.t0 + tpc, p.n_btiles);
+  L.k_end = L.k + (t1 - L.t0);
+  return L;
+}
+
+// Items are handed out dynamically (one global counter, S-chunk-major order
+// like the filter), so the CTAs stay within a couple of S chunks of each
+// other however uneven the candidate counts are and the staged S rows are
+// L2 hits; the filter's static item -> CTA assignment let fast CTAs run
+// many chunks ahead and re-read S from DRAM (~23x at the cfg4 shape).
 __global__ void __launch_bounds__(kRtThreads, 1)
     recheck_group_kernel(const __grid_constant__ RecheckTmaParams tp) {
   const RecheckParams& p = tp.b;
@@ -722,8 +755,9 @@ __global__ void __launch_bounds__(kRtThreads, 1)
   uint64_t* empty_a = full_a + kGrAStages;
   uint64_t* full_b = empty_a + kGrAStages;
   uint64_t* empty_b = full_b + kGrBStages;
-  const int c = blockIdx.x;
-  if (p.cta_count[c] > p.seg_cap) return;  // saturated segment: the join is retried
+  uint64_t* item_full = empty_b + kGrBStages;
+  uint64_t* item_empty = item_full + kGrQ;
+  volatile int64_t* items = reinterpret_cast<volatile int64_t*>(item_empty + kGrQ);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kGrAStages; i++) {
       mbar_init(&full_a[i], 1);
@@ -733,30 +767,37 @@ __global__ void __launch_bounds__(kRtThreads, 1)
       mbar_init(&full_b[i], 1);
       mbar_init(&empty_b[i], kRtComputeWarps);
     }
+    for (int i = 0; i < kGrQ; i++) {
+      mbar_init(&item_full[i], 1);
+      mbar_init(&item_empty[i], kRtComputeWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  const uint64_t* seg = p.cand + (uint64_t)c * p.seg_cap;
-  uint32_t* sims = p.sims_bits + (uint64_t)c * p.seg_cap;
-  const uint32_t* toff = p.tile_off + (int64_t)c * p.tile_stride;
   const int dim = p.dim;
   const int nch = (dim + kRcKC - 1) / kRcKC;
   const int nb = p.n_ablk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int sa = 0, sbs = 0;
-  uint32_t pha = 0, phb = 0;
+  int sa = 0, sbs = 0, qs = 0;
+  uint32_t pha = 0, phb = 0, qph = 0;
 
   if (warp == 0) {
     if (lane != 0) return;
     // -------------------------------------------------------- producer
-    int64_t k = 0;
-    for (int64_t item = c; item < p.n_items; item += gridDim.x) {
-      const int64_t rb = item % nb, sc = item / nb;
-      const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
-      const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
-      const int64_t k_end = k + (t1 - t0);
-      for (int64_t kg = k; kg < k_end;) {
-        const int64_t ke = group_end(toff, kg, k_end);
+    for (;;) {
+      int64_t item = (int64_t)atomicAdd(p.work, 1u);
+      if (item >= p.n_items) item = -1;
+      mbar_wait(&item_empty[qs], qph ^ 1u);
+      items[qs] = item;
+      mbar_arrive(&item_full[qs]);
+      if (++qs == kGrQ) { qs = 0; qph ^= 1u; }
+      if (item < 0) break;
+      const ItemLoc L = item_loc(p, item);
+      if (p.cta_count[L.owner] > p.seg_cap) continue;  // saturated segment: the join is retried
+      const uint32_t* toff = p.tile_off + L.owner * p.tile_stride;
+      const int64_t rb = item % nb;
+      for (int64_t kg = L.k; kg < L.k_end;) {
+        const int64_t ke = group_end(toff, kg, L.k_end);
         const uint32_t g_lo = toff[kg], g_hi = toff[ke];
         if (g_hi - g_lo >= p.direct_max) {
           for (uint32_t pb = g_lo; pb < g_hi; pb += kGrCap) {   // > 1 pass: one oversized tile
@@ -771,7 +812,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 mbar_wait(&empty_b[sbs], phb ^ 1u);
                 mbar_arrive_expect_tx(&full_b[sbs], kRtOpBytes);
                 tma2d(b_ring + (size_t)sbs * kRtOpBytes, &tp.tmap_r, ch * kRcKC,
-                      (int)((t0 + (kt - k)) * kTileRows), &full_b[sbs]);
+                      (int)((L.t0 + (kt - L.k)) * kTileRows), &full_b[sbs]);
                 if (++sbs == kGrBStages) { sbs = 0; phb ^= 1u; }
               }
             }
@@ -779,7 +820,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
         }
         kg = ke;
       }
-      k = k_end;
     }
     return;
   }
@@ -787,14 +827,20 @@ __global__ void __launch_bounds__(kRtThreads, 1)
   const int ct = threadIdx.x - 32;
   constexpr int kCT = kRtComputeWarps * 32;
   const float theta = p.theta;
-  int64_t k = 0;
-  for (int64_t item = c; item < p.n_items; item += gridDim.x) {
-    const int64_t sc = item / nb;
-    const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
-    const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
-    const int64_t k_end = k + (t1 - t0);
-    for (int64_t kg = k; kg < k_end;) {
-      const int64_t ke = group_end(toff, kg, k_end);
+  for (;;) {
+    mbar_wait(&item_full[qs], qph);
+    const int64_t item = items[qs];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_relaxed(&item_empty[qs]);
+    if (++qs == kGrQ) { qs = 0; qph ^= 1u; }
+    if (item < 0) break;
+    const ItemLoc L = item_loc(p, item);
+    if (p.cta_count[L.owner] > p.seg_cap) continue;
+    const uint64_t* seg = p.cand + (uint64_t)L.owner * p.seg_cap;
+    uint32_t* sims = p.sims_bits + (uint64_t)L.owner * p.seg_cap;
+    const uint32_t* toff = p.tile_off + L.owner * p.tile_stride;
+    for (int64_t kg = L.k; kg < L.k_end;) {
+      const int64_t ke = group_end(toff, kg, L.k_end);
       const uint32_t g_lo = toff[kg], g_hi = toff[ke];
       if (g_hi - g_lo < p.direct_max) {
         for (uint32_t q = g_lo + ct; q < g_hi; q += kCT) {   // few candidates: gather
@@ -861,7 +907,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
       }
       kg = ke;
     }
-    k = k_end;
   }
 }
 

@@ -15,8 +15,11 @@ from paper_2312_01476_b200 import device as D, datagen
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg2")
 ap.add_argument("--iters", type=int, default=40)
+ap.add_argument("--n-left", type=int, default=None)
+ap.add_argument("--n-right", type=int, default=None)
 a = ap.parse_args()
-(L, S), c = datagen.config_vectors(a.cfg)
+over = {k: v for k, v in (("n_left", a.n_left), ("n_right", a.n_right)) if v}
+(L, S), c = datagen.config_vectors(a.cfg, **over)
 PL, PS = D.prepare(torch.from_numpy(L).cuda()), D.prepare(torch.from_numpy(S).cuda())
 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 D.join_prepared(PL, PS, c["theta"], filter_events=ev)

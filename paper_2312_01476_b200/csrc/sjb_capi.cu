@@ -84,7 +84,7 @@ int set_smem_attr(const void* fn, int bytes) {
 
 // ---------------------------------------------------------------- plan
 struct JoinPlan {
-  int kpad, stages, a_bufs, grid, tiles_per_chunk, n_ablk, n_btiles;
+  int kpad, stages, a_bufs, a_tiles, grid, tiles_per_chunk, n_ablk, n_btiles;
   int64_t n_items;
   uint32_t smem;
   uint64_t seg_cap;
@@ -115,6 +115,7 @@ int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   pl->wide = true;
   pl->wide_fused = use_wide_fused();
   pl->a_bufs = 0;
+  pl->a_tiles = 1;
   int stages = 0;
   while (stages < 6 && (int)W::smem_bytes(stages + 1) <= max_smem) stages++;
   if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for the wide kernel");
@@ -148,6 +149,7 @@ int make_pair_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   namespace P = sjb::pair;
   pl->pair = true;
   pl->a_bufs = 2;
+  pl->a_tiles = 1;
   const sjb::pair::Layout L0 = P::layout(pl->kpad, 0);
   int stages = (int)((max_smem - (int)L0.total - 3 * 8 * 12) / (int)L0.b_bytes);
   if (stages > 12) stages = 12;
@@ -186,22 +188,32 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // the row-grouped recheck stages candidates in the output-sized key buffer
   pl->defer = use_deferred_recheck(a) && a->out_cap >= a->cand_cap;
-  // Shared memory: prefer a double-buffered resident R block when that still
-  // leaves 3 B stages; otherwise one R buffer (reloaded between items).
+  // Shared memory: the resident R block is one 256-row tile (two M=128
+  // halves per S tile).  SJB_RBLOCK=512 selects two-tile blocks (four halves
+  // per S tile: half the S traffic per MMA; cfg2 filter 14.55 vs 15.2 ms
+  // with emission disabled, but 17.1 vs 16.45 ms in full -- kept for A/B).
+  // Within a block size, prefer a double-buffered block when that still
+  // leaves 3 B stages; otherwise one buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);
+  const char* rbe = getenv("SJB_RBLOCK");
+  int a_tiles = (rbe != nullptr && atoi(rbe) == 512) ? 2 : 1;
   int stages = 0, a_bufs = 2;
-  for (; a_bufs >= 1; a_bufs--) {
-    sjb::JoinSmemLayout L0 = sjb::join_smem_layout(pl->kpad, 0, a_bufs);
-    stages = (int)((max_smem - (int)L0.total) / (int)L0.tile_bytes);
-    if (stages >= 3) break;
+  for (;; a_tiles--) {
+    for (a_bufs = 2; a_bufs >= 1; a_bufs--) {
+      sjb::JoinSmemLayout L0 = sjb::join_smem_layout(pl->kpad, 0, a_bufs, a_tiles);
+      stages = (int)((max_smem - (int)L0.total) / (int)L0.tile_bytes);
+      if (stages >= 3) break;
+    }
+    if (a_bufs < 1) a_bufs = 1;
+    if (stages >= 2 || a_tiles == 1) break;
   }
-  if (a_bufs < 1) a_bufs = 1;
   if (stages > 6) stages = 6;
   if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for 2 stages");
   pl->stages = stages;
   pl->a_bufs = a_bufs;
-  pl->smem = sjb::join_smem_layout(pl->kpad, stages, a_bufs).total;
-  pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kBM);
+  pl->a_tiles = a_tiles;
+  pl->smem = sjb::join_smem_layout(pl->kpad, stages, a_bufs, a_tiles).total;
+  pl->n_ablk = (int)sjb::ceil_div(a->n_left, (int64_t)sjb::kTileRows * a_tiles);
   pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kBN);
   int tpc = a->tiles_per_chunk;
   if (tpc <= 0) {
@@ -282,12 +294,17 @@ int run_scan(const uint32_t* counts, int64_t n, uint64_t* out, uint64_t* out_cop
   return SJB_OK;
 }
 
-template <int KS>
-int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
-  if (int rc = set_smem_attr((const void*)sjb::join_filter_kernel<KS>, (int)smem)) return rc;
-  sjb::join_filter_kernel<KS><<<grid, sjb::kJoinThreads, smem, st>>>(jp);
+template <int KS, int AT>
+int launch_filter_kat(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+  if (int rc = set_smem_attr((const void*)sjb::join_filter_kernel<KS, AT>, (int)smem)) return rc;
+  sjb::join_filter_kernel<KS, AT><<<grid, sjb::kJoinThreads, smem, st>>>(jp);
   SJB_CK_LAUNCH("join_filter");
   return SJB_OK;
+}
+template <int KS>
+int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+  return jp.a_tiles == 2 ? launch_filter_kat<KS, 2>(jp, grid, smem, st)
+                         : launch_filter_kat<KS, 1>(jp, grid, smem, st);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -694,6 +711,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   jp.n_items = items;
   jp.stages = pl.stages;
   jp.a_bufs = pl.a_bufs;
+  jp.a_tiles = pl.a_tiles;
   jp.cutoff = args->theta - args->band;
   const bool per_row = args->left_row_err != nullptr && args->right_tile_err != nullptr;
   jp.row_err = per_row ? args->left_row_err : nullptr;

@@ -45,7 +45,6 @@ constexpr int kRecheckWarps = 2;
 // 20 warps = 5 per SM sub-partition, which keeps the per-thread register cap
 // at 96 (16K registers per SMSP); a 21st warp would force spills.
 constexpr int kJoinThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
-constexpr int kBM = kTileRows;  // resident R rows per item (two UMMA M=128 halves)
 constexpr int kBN = kTileRows;  // S rows per stage == UMMA N
 constexpr int kUmmaN = 256;
 
@@ -63,6 +62,7 @@ struct JoinParams {
   int64_t n_items;
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers
+  int a_tiles;               // 256-row operand tiles per resident R block (template ATILES)
   float cutoff;
   const float* row_err;   // per-row band (or nullptr: uniform cutoff)
   const float* tile_err;
@@ -85,11 +85,12 @@ struct JoinSmemLayout {
   uint32_t off_a, off_b, off_bar, total;
 };
 
-__host__ __device__ inline JoinSmemLayout join_smem_layout(int kpad, int stages, int a_bufs) {
+__host__ __device__ inline JoinSmemLayout join_smem_layout(int kpad, int stages, int a_bufs,
+                                                          int a_tiles) {
   JoinSmemLayout L;
   L.tile_bytes = (uint32_t)kTileRows * kpad * 2;
   L.off_a = 0;
-  L.off_b = a_bufs * L.tile_bytes;
+  L.off_b = a_bufs * a_tiles * L.tile_bytes;
   L.off_bar = L.off_b + stages * L.tile_bytes;
   // a_full[2] a_empty[2] acc_full[2] acc_empty[2] b_full[S] b_empty[S] + tmem slot
   // + candidate counter, wrap flag, finished-epilogue-warp count
@@ -98,11 +99,16 @@ __host__ __device__ inline JoinSmemLayout join_smem_layout(int kpad, int stages,
 }
 
 // KSTEPS = kpad / 16 UMMA k-steps (compile time so the issue loop is
-// straight-line: each tcgen05.mma costs one descriptor add).
-template <int KSTEPS>
+// straight-line: each tcgen05.mma costs one descriptor add).  ATILES = 256-row
+// operand tiles in the resident R block: each S tile is used by 2 * ATILES
+// M=128 halves, so ATILES = 2 halves the S-tile TMA traffic (shared-memory
+// writes and L2 reads) per MMA.
+template <int KSTEPS, int ATILES>
 __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const JoinParams p) {
+  constexpr int kBM = kTileRows * ATILES;   // resident R rows per item
+  constexpr int kHalves = 2 * ATILES;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const JoinSmemLayout L = join_smem_layout(p.kpad, p.stages, p.a_bufs);
+  const JoinSmemLayout L = join_smem_layout(p.kpad, p.stages, p.a_bufs, ATILES);
   uint8_t* a_buf = smem + L.off_a;
   uint8_t* b_buf = smem + L.off_b;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
@@ -160,9 +166,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         const int64_t rb = item % nb;
         const int ab = (int)(it % na);
         mbar_wait(&a_empty[ab], (uint32_t)((it / na) & 1) ^ 1u);
-        mbar_arrive_expect_tx(&a_full[ab], tile_bytes);
-        bulk_g2s(a_buf + (size_t)ab * tile_bytes, p.a16 + (size_t)rb * tile_elems, tile_bytes,
-                 &a_full[ab], pol_a);
+        mbar_arrive_expect_tx(&a_full[ab], ATILES * tile_bytes);
+        bulk_g2s(a_buf + (size_t)ab * ATILES * tile_bytes,
+                 p.a16 + (size_t)rb * ATILES * tile_elems, ATILES * tile_bytes, &a_full[ab],
+                 pol_a);
       }
     }
   } else if (warp == 0) {
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         mbar_wait(&a_full[ab], (uint32_t)((it / na) & 1));
         if (dbg) w_a += clock64() - c0;
         tc_fence_after();
-        const uint64_t ad = a_desc_base + (uint64_t)ab * tile_step;
+        const uint64_t ad = a_desc_base + (uint64_t)ab * ATILES * tile_step;
         const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
@@ -233,14 +240,14 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           if (dbg) w_b += clock64() - c0;
           const uint64_t bd = b_desc_base + (uint64_t)bstage * tile_step;
 #pragma unroll
-          for (int h = 0; h < 2; h++) {
+          for (int h = 0; h < kHalves; h++) {
             const uint32_t as = acc_it & 1u;
             if (dbg) c0 = clock64();
             mbar_wait(&acc_empty[as], ((acc_it >> 1) & 1u) ^ 1u);
             if (dbg) w_e += clock64() - c0;
             tc_fence_after();
             const uint32_t d = tmem_base + as * kUmmaN;
-            const uint64_t adh = ad + h * half_step;
+            const uint64_t adh = ad + (h >> 1) * tile_step + (h & 1) * half_step;
 #pragma unroll
             for (int kk = 0; kk < KSTEPS; kk++)
               tc_mma_f16_elect(d, adh + kk * kstep, bd + kk * kstep, idesc, kk > 0 ? 1u : 0u);
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
     // MMA waits is a whole stage plus the other group's stage, which absorbs
     // the emission of hit chunks (tools/power_modes.py).
     const int ew = warp - 2;
-    const int grp = ew >> 3;          // accumulator stage == R half drained
+    const int grp = ew >> 3;          // accumulator stage drained (halves grp, grp + 2, ..)
     const int cq = (ew >> 2) & 1;     // 128-column half of the 256-column stage
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const uint32_t lane_base = (uint32_t)q * 32;
@@ -365,63 +372,73 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       // per-row band: cutoff = max(cutoff, theta - slack - (1+1e-6)(ex + ey)
       // - ex*ey) = max(cutoff, cA - cB*ey); the 2e-6 in `slack` covers the
       // fp32 evaluation of either form
-      const int64_t gi64 = rb * kBM + grp * 128 + lane_base + lane;
-      const bool rok = gi64 < p.n_a && !no_emit;
-      const float ex = load_err(p.row_err, gi64, p.n_a);
-      const float cA = per_row ? p.theta - p.slack - 1.000001f * ex : p.cutoff;
-      const float cB = per_row ? 1.000001f + ex : 0.0f;
+      // this group's halves of the R block: h = grp, grp + 2, ...
+      int64_t gi64[ATILES];
+      bool rok[ATILES];
+      float cA[ATILES], cB[ATILES];
+#pragma unroll
+      for (int hh = 0; hh < ATILES; hh++) {
+        gi64[hh] = rb * kBM + (grp + 2 * hh) * 128 + lane_base + lane;
+        rok[hh] = gi64[hh] < p.n_a && !no_emit;
+        const float ex = load_err(p.row_err, gi64[hh], p.n_a);
+        cA[hh] = per_row ? p.theta - p.slack - 1.000001f * ex : p.cutoff;
+        cB[hh] = per_row ? 1.000001f + ex : 0.0f;
+      }
       for (int t = t0; t < t1; t++) {
         // issued before the accumulator wait: its latency hides behind it
         const float ey = per_row ? __ldg(p.tile_err + t) : 0.0f;
-        const long long e0 = edbg ? clock64() : 0;
-        mbar_wait(&acc_full[grp], tph);
-        tph ^= 1u;
-        if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
-        tc_fence_after();
-        if (no_drain) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[grp]);
-          continue;
-        }
-        const float cutoff = fmaxf(p.cutoff, fmaf(-cB, ey, cA));
-        uint32_t mk[4] = {0u, 0u, 0u, 0u};
-        bool any_hit = false;
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
-          float v[64];
-          SJB_TMEM_LD64(tbase + c * 64, v);
-          tc_wait_ld();
-          if (c == 1) {
-            tc_fence_before();
+        for (int hh = 0; hh < ATILES; hh++) {
+          const long long e0 = edbg ? clock64() : 0;
+          mbar_wait(&acc_full[grp], tph);
+          tph ^= 1u;
+          if (edbg) { const long long e1 = clock64(); e_wait += e1 - e0; e_mark = e1; }
+          tc_fence_after();
+          if (no_drain) {
             __syncwarp();
-            if (lane == 0) mbar_arrive_relaxed(&acc_empty[grp]);
-            if (edbg) e_drain += clock64() - e_mark;
+            if (lane == 0) mbar_arrive(&acc_empty[grp]);
+            continue;
           }
-          // group maxima over 8 columns, then the 64-column maximum
-          float g[8];
+          const float cutoff = fmaxf(p.cutoff, fmaf(-cB[hh], ey, cA[hh]));
+          uint32_t mk[4] = {0u, 0u, 0u, 0u};
+          bool any_hit = false;
 #pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const float* x = v + 8 * k;
-            g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
-          }
-          const float m =
-              fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
-          const bool hit = rok && (m >= cutoff);
-          if (__any_sync(0xffffffffu, hit)) {
-            if (hit) chunk_mask(v, g, cutoff, mk[2 * c], mk[2 * c + 1]);
-            any_hit = true;
-          }
-        }
-        if (any_hit) {
-          const int64_t col_lim = p.n_b - (int64_t)t * kBN - cq * 128;  // >= col_lim: padding
-          if (col_lim < 128) {
+          for (int c = 0; c < 2; c++) {
+            float v[64];
+            SJB_TMEM_LD64(tbase + c * 64, v);
+            tc_wait_ld();
+            if (c == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_relaxed(&acc_empty[grp]);
+              if (edbg) e_drain += clock64() - e_mark;
+            }
+            // group maxima over 8 columns, then the 64-column maximum
+            float g[8];
 #pragma unroll
-            for (int wd = 0; wd < 4; wd++) {
-              const int64_t cl = col_lim - 32 * wd;
-              mk[wd] &= cl >= 32 ? ~0u : (cl <= 0 ? 0u : ((1u << cl) - 1u));
+            for (int k = 0; k < 8; k++) {
+              const float* x = v + 8 * k;
+              g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
+            }
+            const float m =
+                fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
+            const bool hit = rok[hh] && (m >= cutoff);
+            if (__any_sync(0xffffffffu, hit)) {
+              if (hit) chunk_mask(v, g, cutoff, mk[2 * c], mk[2 * c + 1]);
+              any_hit = true;
             }
           }
-          emit(mk, (uint32_t)gi64, (uint32_t)(t * kBN + cq * 128));
+          if (any_hit) {
+            const int64_t col_lim = p.n_b - (int64_t)t * kBN - cq * 128;  // >= col_lim: padding
+            if (col_lim < 128) {
+#pragma unroll
+              for (int wd = 0; wd < 4; wd++) {
+                const int64_t cl = col_lim - 32 * wd;
+                mk[wd] &= cl >= 32 ? ~0u : (cl <= 0 ? 0u : ((1u << cl) - 1u));
+              }
+            }
+            emit(mk, (uint32_t)gi64[hh], (uint32_t)(t * kBN + cq * 128));
+          }
         }
       }
     }

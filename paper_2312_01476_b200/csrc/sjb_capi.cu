@@ -15,6 +15,7 @@
 #include "../../include/simjoin_b200.h"
 #include "sjb_common.cuh"
 #include "sjb_join.cu"
+#include "sjb_join_ts.cu"
 #include "sjb_join2.cu"
 #include "sjb_join3.cu"
 #include "sjb_post.cu"
@@ -89,6 +90,7 @@ struct JoinPlan {
   uint32_t smem;
   uint64_t seg_cap;
   bool pair;  // CTA-pair (cta_group::2) filter kernel
+  bool ts;    // R block in tensor memory (sjb_join_ts.cu; default for kpad <= 128)
   bool wide;  // K-streaming kernel (kpad > 128)
   bool wide_fused;        // wide: recheck inside the filter (A/B only)
   bool defer;             // d <= 128: row-grouped recheck after the filter (dense joins)
@@ -180,6 +182,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   const int sms = sjb_sm_count(dev);
   pl->kpad = (int)sjb_kpad(a->dim);
   pl->pair = false;
+  pl->ts = false;
   pl->wide = false;
   pl->wide_fused = false;
   pl->tile_stride = 0;
@@ -188,6 +191,24 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // the row-grouped recheck stages candidates in the output-sized key buffer
   pl->defer = use_deferred_recheck(a) && a->out_cap >= a->cand_cap;
+  const char* fe = getenv("SJB_FILTER");
+  if (fe != nullptr && strcmp(fe, "ts") == 0) {
+    // R block in tensor memory (A/B): one shared-memory image + B stages.
+    // cfg2 filter 16.8 ms vs 16.45 for the SS kernel (MMA-only 14.65 in
+    // both: the tensor pipe is power-bound, not shared-memory-bound)
+    namespace T = sjb::ts;
+    const int max_smem = max_dyn_smem(dev);
+    const T::SmemLayout L0 = T::smem_layout(pl->kpad, 0);
+    int stages = (int)((max_smem - (int)L0.total - 2 * 8 * 6) / (int)L0.tile_bytes);
+    if (stages > 6) stages = 6;
+    if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for 2 stages");
+    pl->ts = true;
+    pl->stages = stages;
+    pl->a_bufs = 1;
+    pl->a_tiles = 1;
+    pl->smem = T::smem_layout(pl->kpad, stages).total;
+    pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kTileRows);
+  } else {
   // Shared memory: the resident R block is one 256-row tile (two M=128
   // halves per S tile).  SJB_RBLOCK=512 selects two-tile blocks (four halves
   // per S tile: half the S traffic per MMA; cfg2 filter 14.55 vs 15.2 ms
@@ -214,6 +235,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->a_tiles = a_tiles;
   pl->smem = sjb::join_smem_layout(pl->kpad, stages, a_bufs, a_tiles).total;
   pl->n_ablk = (int)sjb::ceil_div(a->n_left, (int64_t)sjb::kTileRows * a_tiles);
+  }
   pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kBN);
   int tpc = a->tiles_per_chunk;
   if (tpc <= 0) {
@@ -303,6 +325,12 @@ int launch_filter_kat(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaSt
 }
 template <int KS>
 int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+  if (jp.ts) {
+    if (int rc = set_smem_attr((const void*)sjb::ts::filter_kernel<KS>, (int)smem)) return rc;
+    sjb::ts::filter_kernel<KS><<<grid, sjb::ts::kThreads, smem, st>>>(jp);
+    SJB_CK_LAUNCH("join_filter_ts");
+    return SJB_OK;
+  }
   return jp.a_tiles == 2 ? launch_filter_kat<KS, 2>(jp, grid, smem, st)
                          : launch_filter_kat<KS, 1>(jp, grid, smem, st);
 }
@@ -712,6 +740,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   jp.stages = pl.stages;
   jp.a_bufs = pl.a_bufs;
   jp.a_tiles = pl.a_tiles;
+  jp.ts = pl.ts ? 1 : 0;
   jp.cutoff = args->theta - args->band;
   const bool per_row = args->left_row_err != nullptr && args->right_tile_err != nullptr;
   jp.row_err = per_row ? args->left_row_err : nullptr;

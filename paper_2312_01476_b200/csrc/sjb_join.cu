@@ -63,6 +63,7 @@ struct JoinParams {
   int stages;                // B stages
   int a_bufs;                // 1 or 2 resident-A buffers
   int a_tiles;               // 256-row operand tiles per resident R block (template ATILES)
+  int ts;                    // 1: R block in tensor memory (sjb_join_ts.cu)
   float cutoff;
   const float* row_err;   // per-row band (or nullptr: uniform cutoff)
   const float* tile_err;

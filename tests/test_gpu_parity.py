@@ -316,6 +316,29 @@ def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
             assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
 
 
+@pytest.mark.parametrize("variant", [("SJB_FILTER", "ts"), ("SJB_FILTER", "pair"),
+                                     ("SJB_RBLOCK", "512")])
+def test_filter_variants(cuda, manifest, golden, monkeypatch, variant):
+    """d <= 128 filter kernels kept for A/B (TS-mode R block in tensor memory,
+    CTA pair, two-tile R block) give the reference's bits on the golden cases,
+    with and without the overflow retry, under both recheck placements."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv(*variant)
+    for recheck in ("fused", "deferred"):
+        monkeypatch.setenv("SJB_RECHECK", recheck)
+        for name in ("cfg1", "c_small", "c_all", "c_d16_neg"):
+            meta = manifest["cases"][name]
+            L, S = case_inputs(meta)
+            pl = D.prepare(torch.from_numpy(L).to(cuda))
+            pr = D.prepare(torch.from_numpy(S).to(cuda))
+            for cap in (None, 300):
+                m = D.join_prepared(pl, pr, meta["theta"], cand_cap=cap)
+                lo, ro, so = m.to_host()
+                assert np.array_equal(lo, golden[name + "_l"]), (variant, recheck, name, cap)
+                assert np.array_equal(ro, golden[name + "_r"]), (variant, recheck, name, cap)
+                assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
+
+
 def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
     """sjb_cosine_vm and the operators on it against the reference's own
     outputs (e_selection join.py:145-179, top_k embedding.py:218-231)."""

@@ -220,6 +220,30 @@ def initial_capacity(n_left: int, n_right: int) -> int:
     return int(max(1 << 20, min(pairs, 1 << 24)))
 
 
+class PendingJoin:
+    """A join whose kernels are queued but whose match count (data dependent)
+    has not been read back yet.  result() blocks on that count, reruns the
+    join with the exact capacity if the candidate segments overflowed, and
+    returns the DeviceMatches; later work can be queued before calling it."""
+
+    def __init__(self, info_t: torch.Tensor, finish):
+        # the 40-byte info copy is queued now, right behind the join, and
+        # waited on through an event: a later .cpu() would also wait for
+        # everything queued after the join on the stream
+        with torch.cuda.device(info_t.device):
+            self._info_h = torch.empty(info_t.shape, dtype=info_t.dtype, pin_memory=True)
+            self._info_h.copy_(info_t, non_blocking=True)
+            self._ev = torch.cuda.Event()
+            self._ev.record(torch.cuda.current_stream(info_t.device))
+        self._finish, self._done = finish, None
+
+    def result(self) -> "DeviceMatches":
+        if self._done is None:
+            self._ev.synchronize()
+            self._done = self._finish(self._info_h.numpy())
+        return self._done
+
+
 def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                   band: Optional[float] = None, cand_cap: Optional[int] = None,
                   left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
@@ -234,6 +258,18 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     with the per-row band (never looser than `band`; same result, fewer
     candidates to recheck).
     """
+    return join_prepared_async(L, R, theta, band, cand_cap, left_base, grid, tiles_per_chunk,
+                               max_bytes, filter_events, per_row_band).result()
+
+
+def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
+                        band: Optional[float] = None, cand_cap: Optional[int] = None,
+                        left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
+                        max_bytes: Optional[int] = None,
+                        filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None,
+                        per_row_band: bool = True, _retries: int = 0) -> PendingJoin:
+    """join_prepared without the final read-back: the kernels are queued on
+    the current stream and a PendingJoin is returned."""
     if L.dim != R.dim:
         raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
     if L.device != R.device:
@@ -247,7 +283,6 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     if cand_cap is None:
         with _cap_lock:
             cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
-    retries = 0
     ev0 = ev1 = None
     if filter_events is not None:
         for e in filter_events:
@@ -257,50 +292,54 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
         ev1 = ctypes.c_void_p(filter_events[1].cuda_event)
     with torch.cuda.device(dev):
         stream = _stream(dev)
-        while True:
-            args = _lib.JoinArgs(n_left=L.n, n_right=R.n, dim=L.dim, theta=theta32, band=band,
-                                 cand_cap=int(cand_cap), out_cap=int(cand_cap),
-                                 left_base=int(left_base), grid=int(grid),
-                                 tiles_per_chunk=int(tiles_per_chunk),
-                                 ev_filter_begin=ev0, ev_filter_end=ev1,
-                                 left_row_err=L.row_err.data_ptr() if use_err else None,
-                                 right_tile_err=R.tile_err.data_ptr() if use_err else None,
-                                 recheck=_recheck_mode(key, L.n * R.n))
-            ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
-            if ws_bytes < 0:
-                _lib.check(-3, "sjb_join_workspace_bytes")
-            out_bytes = int(cand_cap) * 20
-            if retries and max_bytes is None:
-                free, _total = torch.cuda.mem_get_info(dev)
-                max_bytes = int(free * 0.8) + _ws_bytes_cached(dev)
-            if max_bytes is not None and ws_bytes + out_bytes > max_bytes:
-                raise CapacityExceeded(
-                    f"join needs {ws_bytes + out_bytes} B of device memory for "
-                    f"{cand_cap} candidates; {max_bytes} B available")
-            ws = _workspace(ws_bytes, dev)
-            lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
-            rights = torch.empty_like(lefts)
-            sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
-            info_t = torch.zeros(5, dtype=torch.int64, device=dev)
-            _lib.check(lib.sjb_join_prepared_async(
-                _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(args), _vp(ws),
-                ws_bytes, _vp(lefts), _vp(rights), _vp(sims), _vp(info_t), stream),
-                "sjb_join_prepared_async")
-            info = info_t.cpu().numpy()
-            n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
-            flags = info[3:4].view(np.int32)
-            overflow, used_grid = int(flags[0]), int(flags[1])
-            if not overflow:
-                break
-            if retries >= 2:
-                raise CapacityExceeded(f"candidate capacity still overflows after {retries} "
+        args = _lib.JoinArgs(n_left=L.n, n_right=R.n, dim=L.dim, theta=theta32, band=band,
+                             cand_cap=int(cand_cap), out_cap=int(cand_cap),
+                             left_base=int(left_base), grid=int(grid),
+                             tiles_per_chunk=int(tiles_per_chunk),
+                             ev_filter_begin=ev0, ev_filter_end=ev1,
+                             left_row_err=L.row_err.data_ptr() if use_err else None,
+                             right_tile_err=R.tile_err.data_ptr() if use_err else None,
+                             recheck=_recheck_mode(key, L.n * R.n))
+        ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
+        if ws_bytes < 0:
+            _lib.check(-3, "sjb_join_workspace_bytes")
+        out_bytes = int(cand_cap) * 20
+        if _retries and max_bytes is None:
+            free, _total = torch.cuda.mem_get_info(dev)
+            max_bytes = int(free * 0.8) + _ws_bytes_cached(dev)
+        if max_bytes is not None and ws_bytes + out_bytes > max_bytes:
+            raise CapacityExceeded(
+                f"join needs {ws_bytes + out_bytes} B of device memory for "
+                f"{cand_cap} candidates; {max_bytes} B available")
+        ws = _workspace(ws_bytes, dev)
+        lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
+        rights = torch.empty_like(lefts)
+        sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
+        info_t = torch.zeros(5, dtype=torch.int64, device=dev)
+        _lib.check(lib.sjb_join_prepared_async(
+            _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(args), _vp(ws),
+            ws_bytes, _vp(lefts), _vp(rights), _vp(sims), _vp(info_t), stream),
+            "sjb_join_prepared_async")
+
+    def finish(info) -> DeviceMatches:
+        n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
+        flags = info[3:4].view(np.int32)
+        overflow, used_grid = int(flags[0]), int(flags[1])
+        if overflow:
+            if _retries >= 2:
+                raise CapacityExceeded(f"candidate capacity still overflows after {_retries} "
                                        f"retries (needed {needed})")
-            cand_cap = max(needed, n_matches, int(cand_cap) + 1)
-            retries += 1
-    with _cap_lock:
-        _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
-    return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
-                         n_cand, int(cand_cap), retries, used_grid)
+            with torch.cuda.device(dev):
+                return join_prepared_async(
+                    L, R, theta, band, max(needed, n_matches, int(cand_cap) + 1), left_base, grid,
+                    tiles_per_chunk, max_bytes, filter_events, per_row_band,
+                    _retries + 1).result()
+        with _cap_lock:
+            _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
+        return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
+                             n_cand, int(cand_cap), _retries, used_grid)
+
+    return PendingJoin(info_t, finish)
 
 
 def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, cand_cap: int,
@@ -332,7 +371,7 @@ def _stream_chunks(n: int, chunks: int, lead: int = 4):
 
 def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
-                 inplace: bool = False, name: str = ""
+                 inplace: bool = False, name: str = "", spans=None, sync: bool = True
                  ) -> Tuple["DeviceMatches", PreparedRelation]:
     """Join a prepared left relation with a right relation that becomes
     available on the device chunk by chunk.
@@ -344,8 +383,9 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     fp16 image + rounding errors; in place when `inplace`) and its S tiles
     are filtered at once (sjb_join_begin / sjb_join_filter_tiles /
     sjb_join_finish), so the filter overlaps the arrival of later chunks.
-    Same result as prepare + join_prepared.  Returns the matches and the
-    prepared right relation (resident, reusable)."""
+    Same result as prepare + join_prepared.  Returns the matches (a
+    PendingJoin when sync=False) and the prepared right relation (resident,
+    reusable)."""
     lib = _lib.lib()
     dev = L.device
     n, dim = raw.shape
@@ -361,11 +401,12 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     R = PreparedRelation(f32, op, n, dim, name, rep, re, te)
-    spans = _stream_chunks(n, chunks)
+    spans = _stream_chunks(n, chunks) if spans is None else spans
     if L.n == 0 or n == 0:
         for r0, r1 in spans:
             arrive(r0, r1)
-        return join_prepared(L, R, theta, band, left_base=left_base), R
+        pending = join_prepared_async(L, R, theta, band, left_base=left_base)
+        return (pending if not sync else pending.result()), R
     use_err = L.row_err is not None
     kp = kpad(dim)
     with torch.cuda.device(dev):
@@ -397,49 +438,86 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
                                        ws_bytes, _vp(lefts),
                                        _vp(rights), _vp(sims), _vp(info_t), cs),
                    "sjb_join_finish")
-        info = info_t.cpu().numpy()
-    n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
-    flags = info[3:4].view(np.int32)
-    if int(flags[0]):
-        # candidate capacity overflowed: S is resident now; rerun with room
-        m = join_prepared(L, R, theta, band, cand_cap=max(needed, n_matches, cand_cap + 1),
-                          left_base=left_base)
-        m.retries += 1
-        return m, R
-    with _cap_lock:
-        _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
-    return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
-                         n_cand, int(cand_cap), 0, int(flags[1])), R
+
+    def finish(info) -> DeviceMatches:
+        n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
+        flags = info[3:4].view(np.int32)
+        if int(flags[0]):
+            # candidate capacity overflowed: S is resident now; rerun with room
+            with torch.cuda.device(dev):
+                m = join_prepared(L, R, theta, band, cand_cap=max(needed, n_matches, cand_cap + 1),
+                                  left_base=left_base)
+            m.retries += 1
+            return m
+        with _cap_lock:
+            _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
+        return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
+                             n_cand, int(cand_cap), 0, int(flags[1]))
+
+    pending = PendingJoin(info_t, finish)
+    return (pending if not sync else pending.result()), R
 
 
-def join_streamed(L: PreparedRelation, right_host: torch.Tensor, theta: float,
-                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
-                  name: str = "") -> Tuple["DeviceMatches", PreparedRelation]:
-    """join_chunked for a HOST right relation: the rows are copied in chunks
-    on a side stream and normalised in place as each chunk lands, so the
-    host->device copy overlaps the filter."""
-    if right_host.is_cuda or right_host.dtype != torch.float32 or right_host.dim() != 2:
-        raise ValueError("right_host must be a 2-D float32 host tensor")
-    dev = L.device
-    # pinned: asynchronous chunk copies; pageable: each chunk copy blocks the
-    # host while the GPU filters the previous chunk -- overlapped either way
-    src = right_host.contiguous()
+class StagedCopy:
+    """A host matrix copied to the device in row chunks on a side stream
+    (`stage_host`): `raw` is the device buffer and chunk k covers rows
+    spans[k].  From pinned memory every chunk copy is queued at once; from
+    pageable memory each is issued when the join reaches it (a pageable copy
+    blocks the host, which then overlaps the filter of the previous chunk)."""
+
+    def __init__(self, src: torch.Tensor, raw: torch.Tensor, spans, stream: torch.cuda.Stream,
+                 eager: bool):
+        self.src, self.raw, self.spans, self.stream = src, raw, spans, stream
+        self.events = [None] * len(spans)
+        if eager:
+            for k in range(len(spans)):
+                self._issue(k)
+
+    def _issue(self, k: int) -> None:
+        r0, r1 = self.spans[k]
+        with torch.cuda.stream(self.stream):
+            self.raw[r0:r1].copy_(self.src[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.events[k] = ev
+
+    def arrive(self, r0: int, r1: int) -> None:
+        """Make rows [r0, r1) (a span) ready on the current stream."""
+        k = self.spans.index((r0, r1))
+        if self.events[k] is None:
+            self._issue(k)
+        torch.cuda.current_stream(self.raw.device).wait_event(self.events[k])
+
+
+def stage_host(src: torch.Tensor, dev: torch.device, chunks: int = 8,
+               stream: Optional[torch.cuda.Stream] = None) -> StagedCopy:
+    """Start the chunked H2D copy of a host float32 matrix on a copy stream,
+    so the link is busy from the start of a join instead of from its first
+    filter launch (pinned sources: all chunks queued now)."""
+    if src.is_cuda or src.dtype != torch.float32 or src.dim() != 2:
+        raise ValueError("src must be a 2-D float32 host tensor")
+    src = src.contiguous()
     n, dim = src.shape
     with torch.cuda.device(dev):
         comp = torch.cuda.current_stream(dev)
-        copy = torch.cuda.Stream(dev)
+        copy = stream if stream is not None else torch.cuda.Stream(dev)
         raw = torch.empty((n, dim), dtype=torch.float32, device=dev)
         copy.wait_stream(comp)   # `raw` was allocated on the compute stream
+        return StagedCopy(src, raw, _stream_chunks(n, chunks), copy, src.is_pinned())
 
-        def arrive(r0: int, r1: int) -> None:
-            with torch.cuda.stream(copy):
-                raw[r0:r1].copy_(src[r0:r1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            comp.wait_event(ev)
 
-        return join_chunked(L, raw, arrive, theta, band, left_base, chunks, inplace=True,
-                            name=name)
+def join_streamed(L: PreparedRelation, right_host, theta: float,
+                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
+                  name: str = "", sync: bool = True) -> Tuple["DeviceMatches", PreparedRelation]:
+    """join_chunked for a HOST right relation (a tensor, or a StagedCopy whose
+    chunk copies are already queued): the rows are copied in chunks on a side
+    stream and normalised in place as each chunk lands, so the host->device
+    copy overlaps the filter.  Pinned sources copy asynchronously; a pageable
+    one blocks the host per chunk while the GPU filters the previous one."""
+    staged = right_host if isinstance(right_host, StagedCopy) else stage_host(right_host, L.device,
+                                                                           chunks)
+    return join_chunked(L, staged.raw, staged.arrive, theta, band, left_base, chunks,
+                        inplace=True, name=name, spans=staged.spans, sync=sync)
 
 
 def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> PreparedRelation:

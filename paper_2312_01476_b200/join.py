@@ -14,6 +14,7 @@ materialised similarity buffer, so ``peak_buffer_bytes`` reports 0).
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass
 from typing import Optional, Tuple, Union
@@ -216,55 +217,88 @@ def _pinned(n: int, dtype) -> torch.Tensor:
     return torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
 
 
-def _join_host_split(PL: D.PreparedRelation, right_host: torch.Tensor, theta: float, band,
-                     left_name: str, right_name: str, parts: int = 2) -> MatchSet:
+def _split_bounds(n: int, min_rows: int = 4096):
+    """Left row bounds of the host-input join: 60% of the rows in the first
+    part, whose filter hides the S copy (both scale with |S|.d; the filter
+    must just outlast the copy plus its last chunk), then the rest as 70% +
+    30%, so the last part -- whose result copy nothing hides -- is short.
+    Multiples of 1024 rows.  cfg2 e2e medians by first-part share
+    (tools/e2e_split.py): 0.5 19.8 ms, 0.55 19.6, 0.58 18.5, 0.6 18.3,
+    0.65 19.3.  SJB_SPLIT_FIRST overrides the share (sweeps)."""
+    def r(x: float) -> int:
+        return int(x) // 1024 * 1024
+    h = r(n * float(os.environ.get("SJB_SPLIT_FIRST", "0.6")))
+    if h < min_rows:
+        return [0, n]
+    m = h + r((n - h) * 0.7)
+    bounds = [0, h]
+    if m - h >= min_rows and n - m >= min_rows:
+        bounds.append(m)
+    bounds.append(n)
+    return bounds
+
+
+def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
+                     left_name: str, right_name: str) -> MatchSet:
     """Host-input join in `parts` left row ranges: the first streams S in
-    (H2D overlapped with its filter); each later part joins on the resident S
-    while the previous parts' matches copy to pinned host memory.  All parts
-    land in one pinned buffer, so the MatchSet needs no concatenation.  The
-    ranges are disjoint and ordered, so the result is the canonical MatchSet.
-    Two parts by default: the first part's filter must outlast the S copy it
-    hides (cfg2: 7 ms of H2D vs 8.8 ms of filter); four parts measured worse
-    (e2e 21.0 -> 22.7 ms)."""
+    (H2D overlapped with its filter); each later part is queued on the
+    resident S before the previous part's count is read back, so the GPU
+    never waits for the host between parts, and the previous parts' matches
+    copy to pinned host memory while it runs.  All parts land in one pinned
+    buffer, so the MatchSet needs no concatenation.  The ranges are disjoint
+    and ordered, so the result is the canonical MatchSet (bounds:
+    _split_bounds)."""
     n = PL.n
-    step = (n // max(parts, 1)) // 1024 * 1024
-    if step == 0:
+    bounds = _split_bounds(n)
+    if len(bounds) <= 2:
         m, _ = D.join_streamed(PL, right_host, theta, band)
         return _to_matchset(m, left_name, right_name)
-    bounds = list(range(0, n, step))
-    if n - bounds[-1] < step // 2 and len(bounds) > 1:   # fold a short tail into the last part
-        bounds.pop()
-    bounds.append(n)
     dev = PL.device
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    bufs, cap, done, keep = None, 0, 0, []
-    PR = None
-    for r0, r1 in zip(bounds[:-1], bounds[1:]):
-        if PR is None:
-            m, PR = D.join_streamed(PL.rows(r0, r1), right_host, theta, band)
-        else:
-            m = D.join_prepared(PL.rows(r0, r1), PR, theta, band, left_base=r0)
-        k = m.n_matches
-        if bufs is None or done + k > cap:
-            # size from what the first part produced (the parts are alike)
-            cap = max(int((done + k) * (len(bounds) - 1) / max(1, bounds.index(r1)) * 1.15)
-                      + 4096, done + k)
+    ranges = list(zip(bounds[:-1], bounds[1:]))
+    state = {"bufs": None, "cap": 0, "done": 0}
+    keep = []
+
+    def emit(idx: int, pending, ev) -> None:
+        """Read part idx's count (later parts keep the GPU busy meanwhile)
+        and queue its D2H behind its own kernels."""
+        m = pending.result()
+        if m.retries:                  # rerun after later parts were queued
+            ev = torch.cuda.Event()
+            ev.record(comp)
+        k, done = m.n_matches, state["done"]
+        if state["bufs"] is None or done + k > state["cap"]:
+            # size from what the parts so far produced (the parts are alike)
+            cap = max(int((done + k) * len(ranges) / (idx + 1) * 1.15) + 4096, done + k)
             nb = (_pinned(cap, torch.int64), _pinned(cap, torch.int64),
                   _pinned(cap, torch.float32))
-            if bufs is not None:
+            if state["bufs"] is not None:
                 copy.synchronize()
-                for a, o in zip(nb, bufs):
+                for a, o in zip(nb, state["bufs"]):
                     a[:done].copy_(o[:done])
-            bufs = nb
-        ev = torch.cuda.Event()
-        ev.record(comp)
+            state["bufs"], state["cap"] = nb, cap
         copy.wait_event(ev)
         with torch.cuda.stream(copy):
-            for b, d in zip(bufs, (m.lefts, m.rights, m.sims)):
+            for b, d in zip(state["bufs"], (m.lefts, m.rights, m.sims)):
                 b[done:done + k].copy_(d, non_blocking=True)
         keep.append(m)                                  # device columns live until copied
-        done += k
+        state["done"] = done + k
+
+    prev = None
+    PR = None
+    for idx, (r0, r1) in enumerate(ranges):
+        if PR is None:
+            p, PR = D.join_streamed(PL.rows(r0, r1), right_host, theta, band, sync=False)
+        else:
+            p = D.join_prepared_async(PL.rows(r0, r1), PR, theta, band, left_base=r0)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        if prev is not None:
+            emit(idx - 1, *prev)
+        prev = (p, ev)
+    emit(len(ranges) - 1, *prev)
+    bufs, done = state["bufs"], state["done"]
     copy.synchronize()
     if done == 0:
         return MatchSet(left_name, right_name)
@@ -282,14 +316,35 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
     dev = _device(device)
     t0 = time.perf_counter_ns()
     with torch.cuda.device(dev):
-        L = _as_device_matrix(left, dev)
-        check_dims(L.shape[1], right.shape[1])
         if _is_host(right) and right.shape[0] >= _STREAM_MIN_ROWS:
             # overlap the right relation's H2D copy with the filter, and the
-            # first half's result D2H with the second half's join
-            matches = _join_host_split(D.prepare(L), _host_tensor(right), t.value, band,
-                                       left_name, right_name)
+            # first half's result D2H with the second half's join.  Both host
+            # copies are queued at once on one copy stream (left first), so
+            # the link never waits for host-side setup.
+            comp = torch.cuda.current_stream(dev)
+            copy = torch.cuda.Stream(dev)
+            if _is_host(left):
+                lh = _host_tensor(left)
+                if lh.dim() != 2:
+                    raise ValueError("left must be a 2-D matrix")
+                check_dims(lh.shape[1], right.shape[1])
+                L = torch.empty(tuple(lh.shape), dtype=torch.float32, device=dev)
+                copy.wait_stream(comp)
+                with torch.cuda.stream(copy):
+                    L.copy_(lh, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+            else:
+                L, ev = _as_device_matrix(left, dev), None
+                check_dims(L.shape[1], right.shape[1])
+            staged = D.stage_host(_host_tensor(right), dev, stream=copy)
+            if ev is not None:
+                comp.wait_event(ev)
+            matches = _join_host_split(D.prepare(L), staged, t.value, band, left_name,
+                                       right_name)
         else:
+            L = _as_device_matrix(left, dev)
+            check_dims(L.shape[1], right.shape[1])
             m = D.join_prepared(D.prepare(L), D.prepare(_as_device_matrix(right, dev)), t.value,
                                 band)
             matches = _to_matchset(m, left_name, right_name)

@@ -110,6 +110,18 @@ __device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+// 32-byte read-only load (LDG.256, sm_100): one full sector per lane
+struct f8 {
+  float v[8];
+};
+__device__ __forceinline__ f8 ldg8_hint(const float* p, uint64_t pol) {
+  f8 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                 "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+               : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));

@@ -172,8 +172,32 @@ recheck_grouped_kernel(const uint64_t* __restrict__ grouped, const uint64_t* __r
     const float* b = r32 + (size_t)gj * dim;
     float x = 0.0f;
     if (vec) {
-#pragma unroll 5
-      for (int d = 0; d < dim; d += 4) {
+      // S rows through 32-byte loads (one whole sector per lane: the kernel
+      // is bound by L1 tag lookups); a row 16 bytes off a sector boundary
+      // takes its first 4 elements as a 16-byte load.  Same d order.
+      int d = 0;
+      if (reinterpret_cast<uintptr_t>(b) & 16) {
+        const float4 p = ldg4_hint(a, pol_r), q = ldg4_hint(b, pol_s);
+        x = __fmaf_rn(p.x, q.x, x);
+        x = __fmaf_rn(p.y, q.y, x);
+        x = __fmaf_rn(p.z, q.z, x);
+        x = __fmaf_rn(p.w, q.w, x);
+        d = 4;
+      }
+#pragma unroll 3
+      for (; d + 8 <= dim; d += 8) {
+        const f8 q = ldg8_hint(b + d, pol_s);
+        const float4 p0 = ldg4_hint(a + d, pol_r), p1 = ldg4_hint(a + d + 4, pol_r);
+        x = __fmaf_rn(p0.x, q.v[0], x);
+        x = __fmaf_rn(p0.y, q.v[1], x);
+        x = __fmaf_rn(p0.z, q.v[2], x);
+        x = __fmaf_rn(p0.w, q.v[3], x);
+        x = __fmaf_rn(p1.x, q.v[4], x);
+        x = __fmaf_rn(p1.y, q.v[5], x);
+        x = __fmaf_rn(p1.z, q.v[6], x);
+        x = __fmaf_rn(p1.w, q.v[7], x);
+      }
+      if (d < dim) {   // dim % 8 == 4 tail
         const float4 p = ldg4_hint(a + d, pol_r), q = ldg4_hint(b + d, pol_s);
         x = __fmaf_rn(p.x, q.x, x);
         x = __fmaf_rn(p.y, q.y, x);

@@ -632,3 +632,27 @@ def test_cost_calibration_on_device(cuda):
         assert choose_plan(l, r, 100, 64 << 20, p)[0] == "tensor"
     with pytest.raises(ValueError):
         calibrate(model, 100, sample_sizes=(10,))
+
+
+def test_host_split_join_with_overflowing_parts(cuda, monkeypatch):
+    """The host-input join's pipelined parts (each queued before the previous
+    part's count is read back) when every part overflows its first candidate
+    capacity: the reruns are queued behind later parts and the result still
+    equals the device-resident join, bit for bit."""
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200.join import _split_bounds, tensor_join_vectors
+    rng = np.random.default_rng(11)
+    cents = rng.standard_normal((40, 16)).astype(np.float32)
+    L = (cents[rng.integers(0, 40, 32_768)] + 0.3 * rng.standard_normal((32_768, 16))).astype(np.float32)
+    S = (cents[rng.integers(0, 40, 70_000)] + 0.3 * rng.standard_normal((70_000, 16))).astype(np.float32)
+    theta = 0.9
+    assert len(_split_bounds(L.shape[0])) == 4          # three parts
+    ref = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                          D.prepare(torch.from_numpy(S).to(cuda)), theta).to_host()
+    assert len(ref[0]) > 100_000
+    monkeypatch.setattr(D, "initial_capacity", lambda nl, nr: 4096)
+    monkeypatch.setattr(D, "_cap_cache", {})
+    ms, _ = tensor_join_vectors(torch.from_numpy(L).pin_memory(), torch.from_numpy(S).pin_memory(),
+                                theta, device=cuda)
+    assert np.array_equal(ms.lefts, ref[0]) and np.array_equal(ms.rights, ref[1])
+    assert np.array_equal(ms.sims.view(np.uint32), ref[2].view(np.uint32))

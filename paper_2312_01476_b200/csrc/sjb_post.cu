@@ -419,17 +419,20 @@ constexpr int kSortBigCap = 26624;   // keys sorted whole in shared memory (208 
 // cfg4 rows with tens of thousands of matches -- are ranked instead of sorted:
 // a row's right offsets j are distinct, so j's position in the row is the
 // number of the row's keys below it.  Per window of kRankWindow offsets: set
-// bit j of a shared-memory bitmap, prefix-popcount it per 1024-bit group,
-// and write each key straight to q0 + (keys in earlier windows) + rank.
+// bit j of a shared-memory bitmap, prefix-popcount it per 1024-bit group and
+// per word within the group (u16), and write each key straight to
+// q0 + (keys in earlier windows) + rank: three shared reads per key.
 constexpr int kRankWindow = 1 << 20;                  // bits: 128 KB of shared memory
 constexpr int kRankWords = kRankWindow / 32;
 constexpr int kRankGroups = kRankWords / 32;           // 1024 groups of 32 words
-static_assert((kRankWords + kRankGroups + 1) * 4 <= kSortBigCap * 8, "bitmap fits the buffer");
+static_assert(kRankWords * 4 + (kRankGroups + 1) * 4 + kRankWords * 2 <= kSortBigCap * 8,
+              "bitmap + prefixes fit the buffer");
 
 __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0, uint64_t i_row,
                          int64_t n_right, uint32_t* bits, uint32_t* gpre,
                          uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                          float* __restrict__ sims) {
+  uint16_t* wpre = reinterpret_cast<uint16_t*>(gpre + kRankGroups + 1);  // in-group word prefix
   const int tid = threadIdx.x, nthr = blockDim.x;
   uint64_t base = 0;
   for (int64_t w0 = 0; w0 < n_right; w0 += kRankWindow) {
@@ -444,7 +447,10 @@ __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0,
     for (int q = tid; q < kRankGroups; q += nthr) {
       uint32_t c = 0;
 #pragma unroll 8
-      for (int k = 0; k < 32; k++) c += __popc(bits[q * 32 + k]);
+      for (int k = 0; k < 32; k++) {
+        wpre[q * 32 + k] = (uint16_t)c;
+        c += __popc(bits[q * 32 + k]);
+      }
       gpre[q] = c;
     }
     __syncthreads();
@@ -469,9 +475,8 @@ __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0,
       const uint64_t o = (key >> 32) - (uint64_t)w0;
       if (o >= (uint64_t)kRankWindow) continue;
       const uint32_t word = (uint32_t)(o >> 5), grp = word >> 5;
-      uint32_t rank = gpre[grp];
-      for (uint32_t k = grp * 32; k < word; k++) rank += __popc(bits[k]);
-      rank += __popc(bits[word] & ((1u << (o & 31)) - 1u));
+      const uint32_t rank =
+          gpre[grp] + wpre[word] + __popc(bits[word] & ((1u << (o & 31)) - 1u));
       const uint64_t pos = q0 + base + rank;
       lefts[pos] = i_row;
       rights[pos] = key >> 32;

@@ -500,7 +500,14 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
     const uint64_t q0 = rowoff[i];
     const int64_t n = (int64_t)(rowoff[i + 1] - q0);
     uint64_t* g = keys + q0;
-    if (n <= kSortBigCap) {
+    // rank through bitmaps when that is cheaper than the bitonic network:
+    // windows x (bitmap words + 2 key passes) vs npad log2(npad)^2 / 2 CAS
+    int lg = 0;
+    while ((1ll << lg) < n) lg++;
+    const int64_t windows = (n_right + kRankWindow - 1) / kRankWindow;
+    const bool rank = n > kSortBigCap ||
+                      windows * (2 * (int64_t)kRankWords + 2 * n) < (1ll << lg) * lg * (lg + 1);
+    if (!rank) {
       for (int t = threadIdx.x; t < n; t += blockDim.x) sbuf[t] = g[t];
       __syncthreads();
       smem_bitonic<false>(sbuf, (int)n, threadIdx.x, blockDim.x);

@@ -138,6 +138,42 @@ def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = N
     return PreparedRelation(f32, op, n, dim, name, rep, re, te)
 
 
+def prepare_pieces(raw: torch.Tensor, pieces, name: str = ""):
+    """prepare() for a device matrix whose rows land in pieces: `pieces` is
+    [(r0, r1, event)] in row order, r0 on 512-row boundaries, each piece
+    complete when its event fires (None: already there).  Returns the
+    PreparedRelation and ready(r): queue, on the current stream, the wait and
+    normalisation of every piece starting below row r not yet done -- so a
+    join of the first rows can start before the later rows have arrived."""
+    _check_matrix(raw, "relation")
+    lib = _lib.lib()
+    n, dim = raw.shape
+    dev = raw.device
+    f32 = torch.empty_like(raw)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(n, dev)
+    kp = kpad(dim)
+    todo = list(pieces)
+
+    def ready(r: int) -> None:
+        with torch.cuda.device(dev):
+            while todo and todo[0][0] < r:
+                r0, r1, ev = todo.pop(0)
+                if ev is not None:
+                    torch.cuda.current_stream(dev).wait_event(ev)
+                t0 = r0 // TILE_ROWS
+                _lib.check(lib.sjb_normalize_rows(
+                    ctypes.c_void_p(raw.data_ptr() + r0 * dim * 4), r1 - r0, dim,
+                    ctypes.c_void_p(f32.data_ptr() + r0 * dim * 4),
+                    ctypes.c_void_p(op.data_ptr() + t0 * TILE_ROWS * kp * 2), _vp(rep),
+                    ctypes.c_void_p(re.data_ptr() + r0 * 4),
+                    ctypes.c_void_p(te.data_ptr() + t0 * 4), _stream(dev)),
+                    "sjb_normalize_rows")
+
+    return PreparedRelation(f32, op, n, dim, name, rep, re, te), ready
+
+
 def normalize_rows_(m: torch.Tensor) -> torch.Tensor:
     """In-place fp32 row normalisation; returns the (1,) int64 repaired count."""
     _check_matrix(m, "matrix")

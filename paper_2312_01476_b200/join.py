@@ -239,7 +239,7 @@ def _split_bounds(n: int, min_rows: int = 4096):
 
 
 def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
-                     left_name: str, right_name: str) -> MatchSet:
+                     left_name: str, right_name: str, ready=None) -> MatchSet:
     """Host-input join in `parts` left row ranges: the first streams S in
     (H2D overlapped with its filter); each later part is queued on the
     resident S before the previous part's count is read back, so the GPU
@@ -250,7 +250,10 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
     _split_bounds)."""
     n = PL.n
     bounds = _split_bounds(n)
+    if ready is None:
+        ready = lambda r: None                          # noqa: E731  (rows all prepared)
     if len(bounds) <= 2:
+        ready(n)
         m, _ = D.join_streamed(PL, right_host, theta, band)
         return _to_matchset(m, left_name, right_name)
     dev = PL.device
@@ -288,6 +291,7 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
     prev = None
     PR = None
     for idx, (r0, r1) in enumerate(ranges):
+        ready(r1)                                       # this part's left rows, normalised
         if PR is None:
             p, PR = D.join_streamed(PL.rows(r0, r1), right_host, theta, band, sync=False)
         else:
@@ -321,8 +325,11 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
             # first half's result D2H with the second half's join.  Both host
             # copies are queued at once on one copy stream (left first), so
             # the link never waits for host-side setup.
+            # the left rows of the first part go first, then S, then the
+            # rest of the left rows (needed only by the later parts)
             comp = torch.cuda.current_stream(dev)
             copy = torch.cuda.Stream(dev)
+            pieces = []
             if _is_host(left):
                 lh = _host_tensor(left)
                 if lh.dim() != 2:
@@ -330,18 +337,30 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                 check_dims(lh.shape[1], right.shape[1])
                 L = torch.empty(tuple(lh.shape), dtype=torch.float32, device=dev)
                 copy.wait_stream(comp)
-                with torch.cuda.stream(copy):
-                    L.copy_(lh, non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(copy)
+                b = _split_bounds(L.shape[0])
+                cuts = [0, b[1], L.shape[0]] if len(b) > 2 else [0, L.shape[0]]
+                spans = [(r0, r1) for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0]
+
+                def copy_rows(r0: int, r1: int) -> None:
+                    with torch.cuda.stream(copy):
+                        L[r0:r1].copy_(lh[r0:r1], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(copy)
+                    pieces.append((r0, r1, ev))
+
+                if spans:
+                    copy_rows(*spans[0])
             else:
-                L, ev = _as_device_matrix(left, dev), None
+                L, spans = _as_device_matrix(left, dev), []
                 check_dims(L.shape[1], right.shape[1])
-            staged = D.stage_host(_host_tensor(right), dev, stream=copy)
-            if ev is not None:
-                comp.wait_event(ev)
-            matches = _join_host_split(D.prepare(L), staged, t.value, band, left_name,
-                                       right_name)
+                pieces.append((0, L.shape[0], None))
+            staged = D.stage_host(_host_tensor(right), dev, stream=copy,
+                                  chunks=int(os.environ.get("SJB_STREAM_CHUNKS", "8")))
+            for sp in spans[1:]:
+                copy_rows(*sp)
+            PL, ready = D.prepare_pieces(L, pieces)
+            matches = _join_host_split(PL, staged, t.value, band, left_name, right_name,
+                                       ready=ready)
         else:
             L = _as_device_matrix(left, dev)
             check_dims(L.shape[1], right.shape[1])

@@ -212,7 +212,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   // Shared memory: the resident R block is one 256-row tile (two M=128
   // halves per S tile).  SJB_RBLOCK=512 selects two-tile blocks (four halves
   // per S tile: half the S traffic per MMA; cfg2 filter 14.55 vs 15.2 ms
-  // with emission disabled, but 17.1 vs 16.45 ms in full -- kept for A/B).
+  // with emission disabled, 16.5 ms in full either way -- kept for A/B).
   // Within a block size, prefer a double-buffered block when that still
   // leaves 3 B stages; otherwise one buffer (reloaded between items).
   const int max_smem = max_dyn_smem(dev);

@@ -68,6 +68,84 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
   return repaired;
 }
 
+// Wide rows (fewer rows per sub-tile than threads, e.g. d = 768): only the
+// sum of squares must run in the reference's sequential order, one thread per
+// row; the divide and the rounding-error measurement are element-parallel
+// over the whole CTA.  Same bits as normalize_row_smem: the quotient is the
+// same correctly rounded fp64 divide, and the error sum is our own bound
+// (any summation order is within the 1 + 1e-12 factor).
+constexpr int kWideRows = 32;   // rows per sub-tile handled this way (one warp of sums)
+
+__device__ __forceinline__ double row_norm_smem(float* row, int dim, int* repaired) {
+  double ss = 0.0;
+  for (int d = 0; d < dim; d++) {
+    const double x = (double)row[d];
+    ss = __fma_rn(x, x, ss);
+  }
+  double norm = sqrt(ss);
+  *repaired = 0;
+  if (norm < 1e-12) {
+    row[0] = 1.0f;
+    ss = 0.0;
+    for (int d = 0; d < dim; d++) {
+      const double x = (double)row[d];
+      ss = __fma_rn(x, x, ss);
+    }
+    norm = sqrt(ss);
+    *repaired = 1;
+  }
+  return norm;
+}
+
+__device__ __forceinline__ double quot_rn(double x, double norm, double y, bool hoist) {
+  if (!hoist) return __ddiv_rn(x, norm);
+  const double q0 = __dmul_rn(x, y);
+  return copysign(__fma_rn(__fma_rn(-q0, norm, x), y, q0), x);  // keeps -0.0
+}
+
+// Normalise the vrows (<= kWideRows) rows staged in sm; row errors to err_out
+// (nullptr: not wanted).  Returns this thread's repaired-row count.
+__device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, float* err_out) {
+  __shared__ double s_norm[kWideRows], s_y[kWideRows];
+  __shared__ double s_part[kPrepThreads / 32][kWideRows];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int rep = 0;
+  if (tid < vrows) {
+    const double norm = row_norm_smem(sm + tid * pitch, dim, &rep);
+    s_norm[tid] = norm;
+    s_y[tid] = __drcp_rn(norm);
+  }
+  __syncthreads();
+  const bool want = err_out != nullptr;
+  for (int r = 0; r < vrows; r++) {
+    const double norm = s_norm[r], y = s_y[r];
+    const bool hoist = isfinite(norm);
+    float* row = sm + r * pitch;
+    double es = 0.0;
+    for (int d = tid; d < dim; d += kPrepThreads) {
+      const float x = __double2float_rn(quot_rn((double)row[d], norm, y, hoist));
+      row[d] = x;
+      if (want) {
+        const double e = (double)__fsub_rn(from_op16(to_op16(x)), x);
+        es = __fma_rn(e, e, es);
+      }
+    }
+    if (want) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+      if (lane == 0) s_part[wid][r] = es;
+    }
+  }
+  __syncthreads();
+  if (want && tid < vrows) {
+    double es = 0.0;
+#pragma unroll
+    for (int w = 0; w < kPrepThreads / 32; w++) es += s_part[w][tid];
+    *err_out = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
+  }
+  return rep;
+}
+
 // Walks this thread's elements e = tid, tid + kPrepThreads, ... < total of a
 // block of rows `dim` wide, calling f(e, r, d) with (r, d) = divmod(e, dim)
 // advanced incrementally: one integer divide per thread, not per element.
@@ -95,15 +173,32 @@ __device__ __forceinline__ bool aligned16(const void* p) {
 __device__ __forceinline__ void stage_rows(float* sm, int pitch, const float* __restrict__ src,
                                            int vrows, int dim) {
   if ((dim & 3) == 0 && aligned16(src)) {
+    // batches of 8 loads in flight per thread before their stores (one load
+    // at a time left wide sub-tiles latency-bound: 48 sequential round trips
+    // per thread at d = 768)
     const float4* s4 = reinterpret_cast<const float4*>(src);
-    for_each_elem(vrows * (dim >> 2), dim >> 2, [&](int e, int r, int d) {
-      const float4 v = __ldg(s4 + e);
-      float* o = sm + r * pitch + 4 * d;
-      o[0] = v.x;
-      o[1] = v.y;
-      o[2] = v.z;
-      o[3] = v.w;
-    });
+    const int q4 = dim >> 2, total = vrows * q4;
+    constexpr int kB = 8;
+    for (int e0 = threadIdx.x; e0 < total; e0 += kB * kPrepThreads) {
+      float4 v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; u++) {
+        const int e = e0 + u * kPrepThreads;
+        if (e < total) v[u] = __ldg(s4 + e);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; u++) {
+        const int e = e0 + u * kPrepThreads;
+        if (e < total) {
+          const int r = e / q4, d = e - r * q4;
+          float* o = sm + r * pitch + 4 * d;
+          o[0] = v[u].x;
+          o[1] = v[u].y;
+          o[2] = v[u].z;
+          o[3] = v[u].w;
+        }
+      }
+    }
   } else {
     for_each_elem(vrows * dim, dim, [&](int e, int r, int d) { sm[r * pitch + d] = __ldg(src + e); });
   }
@@ -126,9 +221,17 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
                                unsigned long long* __restrict__ repaired, ErrOut eo) {
   const int vrows = max(0, min(sub, rows - r0));  // valid rows in this sub-tile
   int rep = 0;
-  if (normalize && threadIdx.x < vrows) {
+  const bool want = eo.row_err != nullptr;
+  if (normalize && sub <= kWideRows && sub < kPrepThreads) {
+    // wide rows: sequential sums per row, element-parallel divide (above)
     float e = 0.0f;
-    const bool want = eo.row_err != nullptr;
+    rep = normalize_rows_wide(sm, pitch, vrows, dim, want ? &e : nullptr);
+    if (want && threadIdx.x < vrows) {
+      eo.row_err[row0 + r0 + threadIdx.x] = e;
+      atomicMax(eo.tile_max, __float_as_uint(e));  // e >= 0: bit order = value order
+    }
+  } else if (normalize && threadIdx.x < vrows) {
+    float e = 0.0f;
     rep = normalize_row_smem(sm + threadIdx.x * pitch, dim, want ? &e : nullptr);
     if (want) {
       eo.row_err[row0 + r0 + threadIdx.x] = e;

@@ -656,3 +656,28 @@ def test_host_split_join_with_overflowing_parts(cuda, monkeypatch):
                                 theta, device=cuda)
     assert np.array_equal(ms.lefts, ref[0]) and np.array_equal(ms.rights, ref[1])
     assert np.array_equal(ms.sims.view(np.uint32), ref[2].view(np.uint32))
+
+
+@pytest.mark.parametrize("left_kind", ["device", "numpy", "pinned"])
+def test_host_input_join_input_kinds(cuda, left_kind):
+    """tensor_join_vectors with a host right relation large enough to stream
+    (>= 64k rows) and the left relation on the device, in pageable numpy
+    memory or pinned: the staged copies, the split left preparation and the
+    pipelined parts give the device join's bits."""
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    L, S = datagen_pair(20_480, 66_000, 24, seed=5)
+    theta = 0.85
+    ref = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                          D.prepare(torch.from_numpy(S).to(cuda)), theta).to_host()
+    assert len(ref[0]) > 10_000
+    left = {"device": torch.from_numpy(L).to(cuda), "numpy": L,
+            "pinned": torch.from_numpy(L).pin_memory()}[left_kind]
+    ms, _ = tensor_join_vectors(left, S, theta, device=cuda)      # S: pageable numpy
+    assert np.array_equal(ms.lefts, ref[0]) and np.array_equal(ms.rights, ref[1])
+    assert np.array_equal(ms.sims.view(np.uint32), ref[2].view(np.uint32))
+
+
+def datagen_pair(nl, nr, dim, seed):
+    from paper_2312_01476_b200 import datagen
+    return datagen.clustered_pair(nl, nr, dim, 60, 0.4, seed)

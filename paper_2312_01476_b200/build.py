@@ -45,18 +45,36 @@ def is_stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
+def _locked(fn):
+    """Run fn under an exclusive lock file next to the library, so concurrent
+    processes (one per GPU under torchrun) never build into the same file."""
+    import fcntl
+    with open(os.path.join(PKG_DIR, ".build.lock"), "w") as fh:
+        fcntl.flock(fh, fcntl.LOCK_EX)
+        try:
+            return fn()
+        finally:
+            fcntl.flock(fh, fcntl.LOCK_UN)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not is_stale() and os.path.exists(pack_ext_path()):
+        return LIB_PATH
+    return _locked(lambda: _build(force, verbose))
+
+
+def _build(force: bool, verbose: bool) -> str:
     build_pack(force)
-    if not force and not is_stale():
+    if not force and not is_stale():      # another process built it meanwhile
         return LIB_PATH
     extra = os.environ.get("SJB_NVCC_EXTRA", "").split()   # e.g. -DSJB_PROFILE=1
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB_PATH + ".tmp",
-           os.path.join(CSRC, "sjb_capi.cu")]
+    tmp = f"{LIB_PATH}.tmp{os.getpid()}"
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, os.path.join(CSRC, "sjb_capi.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 
@@ -72,10 +90,11 @@ def build_pack(force: bool = False) -> str:
     src = os.path.join(CSRC, "sjb_pack.c")
     if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(src):
         return out
+    tmp = f"{out}.tmp{os.getpid()}"
     cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC",
-           "-I" + sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
+           "-I" + sysconfig.get_paths()["include"], src, "-o", tmp]
     subprocess.check_call(cmd)
-    os.replace(out + ".tmp", out)
+    os.replace(tmp, out)
     return out
 
 

@@ -494,12 +494,13 @@ int64_t sjb_operand_elems(int64_t n, int64_t dim) {
 }
 
 float sjb_default_band(int64_t dim) {
-  // fp16 operands: |fp16(x) - x| <= u|x| + 2^-25 per component (u = 2^-11;
-  // the 2^-25 covers fp16 subnormals), so ||e_x|| <= e = u + 2^-25 sqrt(dim)
+  // 16-bit operands: |op(x) - x| <= u|x| + 2^-25 per component (u = 2^-8 for
+  // bf16 at kpad <= 128, 2^-11 for fp16 above; the 2^-25 covers fp16
+  // subnormals and over-covers bf16's), so ||e_x|| <= e = u + 2^-25 sqrt(dim)
   // for a unit row, and by Cauchy-Schwarz |approx - exact| <= 2e(1 + 1e-6) +
   // e^2; plus fp32 accumulation error of both the tensor-core sum and the
   // canonical sequential sum (<= 2 * dim * 2^-24 each, generous).
-  const double u = 1.0 / 2048.0;
+  const double u = sjb::op_is_bf16((int)sjb_kpad(dim)) ? 1.0 / 256.0 : 1.0 / 2048.0;
   const double e = u + 2.98023223876953125e-08 * sqrt((double)dim);
   const double b = 2 * e * (1 + 1e-6) + e * e + 4.0 * (double)dim * 5.9604644775390625e-08 + 1e-6;
   return (float)b;

@@ -10,13 +10,23 @@
 
 namespace sjb {
 
-// 16-bit tensor-core operand: fp16.  Rows are unit vectors, far inside
-// fp16's range, and its 11-bit significand rounds 8x finer than bf16's 8 at
-// the same UMMA throughput, so the filter band (and the candidates that only
-// the band admits) shrinks accordingly.
-using op16_t = __half;
-__device__ __forceinline__ op16_t to_op16(float x) { return __float2half_rn(x); }
-__device__ __forceinline__ float from_op16(op16_t h) { return __half2float(h); }
+// 16-bit tensor-core operands, raw storage; the format follows the path
+// (DESIGN.md section 2):
+//  * kpad <= 128 (the resident-R filter): bf16.  Same UMMA rate as fp16, but
+//    the tensor pipe draws less power per MMA, and the filter runs at the
+//    board power cap: cfg2 15.8 vs 16.5 ms sustained (MMA-only 13.6 vs
+//    14.65) for 8% more candidates, which the fused recheck absorbs.
+//  * kpad > 128 (the K-streaming wide filter): fp16.  Its 11-bit significand
+//    rounds 8x finer, so the band admits far fewer non-matches (cfg4: 5.3e8
+//    vs 7.5e8 candidates), and there the canonical recheck dominates.
+using op16_t = uint16_t;
+__host__ __device__ constexpr bool op_is_bf16(int kpad) { return kpad <= 128; }
+__device__ __forceinline__ op16_t to_op16(float x, bool bf) {
+  return bf ? __bfloat16_as_ushort(__float2bfloat16_rn(x)) : __half_as_ushort(__float2half_rn(x));
+}
+__device__ __forceinline__ float from_op16(op16_t h, bool bf) {
+  return bf ? __bfloat162float(__ushort_as_bfloat16(h)) : __half2float(__ushort_as_half(h));
+}
 
 
 // Rows per fp16 operand tile.  Both relations are stored as a sequence of
@@ -225,11 +235,12 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor_noswz(uint32_t smem_addr, u
   return d;
 }
 
-// Instruction descriptor: kind::f16, A=B=f16, D=f32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t umma_idesc_f16_f32(int M, int N) {
+// Instruction descriptor: kind::f16, A=B=f16 (or bf16), D=f32, both
+// K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16_f32(int M, int N, bool bf16 = false) {
   return (1u << 4)                      // D format f32
-         | (0u << 7)                    // A format f16
-         | (0u << 10)                   // B format f16
+         | ((bf16 ? 1u : 0u) << 7)      // A format: 0 f16, 1 bf16
+         | ((bf16 ? 1u : 0u) << 10)     // B format
          | (uint32_t(N >> 3) << 17)     // N / 8
          | (uint32_t(M >> 4) << 24);    // M / 16
 }

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
       // whole warp, warp-uniform control flow; one elected lane issues each
       // tcgen05 op (a single divergent lane costs an ELECT/R2UR sequence
       // per MMA and made the issue the critical path)
-      const uint32_t idesc = umma_idesc_f16_f32(128, kUmmaN);
+      const uint32_t idesc = umma_idesc_f16_f32(128, kUmmaN, true);
       const uint32_t lbo = kTileRows * 16;  // 256-row operand: distance between k-groups
       const uint32_t sbo = 128;             // distance between 8-row core-matrix groups
       // a k-step advances the start address by 2 k-groups = 2 * lbo bytes;

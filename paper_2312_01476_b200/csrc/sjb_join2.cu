@@ -289,7 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader) {  // the whole warp runs the issue loop; mma2/commit2 elect one lane
       // ---------------------------------------------- MMA issuer (pair)
-      const uint32_t idesc = umma_idesc_f16_f32(256, kUmmaN);
+      const uint32_t idesc = umma_idesc_f16_f32(256, kUmmaN, true);
       const uint32_t a_lbo = kARows * 16;   // A: 256-row block, k-group stride
       const uint32_t b_lbo = kHalfN * 16;   // B: this CTA's kHalfN-row slab, k-group stride
       const uint32_t sbo = 128;

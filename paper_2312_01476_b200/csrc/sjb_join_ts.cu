@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const JoinParams p)
     }
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer
-    const uint32_t idesc = umma_idesc_f16_f32(128, kN);
+    const uint32_t idesc = umma_idesc_f16_f32(128, kN, true);
     const uint32_t lbo = kTileRows * 16;  // 256-row operand: distance between k-groups
     const uint32_t sbo = 128;             // distance between 8-row core-matrix groups
     const uint64_t kstep = (2 * lbo) >> 4;        // one k-step = 2 k-groups

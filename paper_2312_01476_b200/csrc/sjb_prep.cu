@@ -20,7 +20,7 @@ constexpr int kPrepThreads = 128;
 // With `err` != nullptr the same final pass also measures the row's fp16
 // rounding error ||fp16(x) - x||_2 (exact squares, fp64 sum, rounded up): the
 // per-row term of the filter band (sjb_common.cuh row_cutoff).
-__device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* err) {
+__device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* err, bool bf) {
   double ss = 0.0;
   for (int d = 0; d < dim; d++) {
     double x = (double)row[d];
@@ -60,7 +60,7 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
       row[d] = x;
       // fp16(x) - x is exact in fp32 (at most 13 significant bits, or x itself
       // when it rounds to zero), so the fp32 difference equals the fp64 one
-      const double e = (double)__fsub_rn(from_op16(to_op16(x)), x);
+      const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
       es = __fma_rn(e, e, es);
     }
     *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
@@ -105,7 +105,8 @@ __device__ __forceinline__ double quot_rn(double x, double norm, double y, bool 
 
 // Normalise the vrows (<= kWideRows) rows staged in sm; row errors to err_out
 // (nullptr: not wanted).  Returns this thread's repaired-row count.
-__device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, float* err_out) {
+__device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, float* err_out,
+                                   bool bf) {
   __shared__ double s_norm[kWideRows], s_y[kWideRows];
   __shared__ double s_part[kPrepThreads / 32][kWideRows];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -126,7 +127,7 @@ __device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, flo
       const float x = __double2float_rn(quot_rn((double)row[d], norm, y, hoist));
       row[d] = x;
       if (want) {
-        const double e = (double)__fsub_rn(from_op16(to_op16(x)), x);
+        const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
         es = __fma_rn(e, e, es);
       }
     }
@@ -225,14 +226,14 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
   if (normalize && sub <= kWideRows && sub < kPrepThreads) {
     // wide rows: sequential sums per row, element-parallel divide (above)
     float e = 0.0f;
-    rep = normalize_rows_wide(sm, pitch, vrows, dim, want ? &e : nullptr);
+    rep = normalize_rows_wide(sm, pitch, vrows, dim, want ? &e : nullptr, op_is_bf16(kpad));
     if (want && threadIdx.x < vrows) {
       eo.row_err[row0 + r0 + threadIdx.x] = e;
       atomicMax(eo.tile_max, __float_as_uint(e));  // e >= 0: bit order = value order
     }
   } else if (normalize && threadIdx.x < vrows) {
     float e = 0.0f;
-    rep = normalize_row_smem(sm + threadIdx.x * pitch, dim, want ? &e : nullptr);
+    rep = normalize_row_smem(sm + threadIdx.x * pitch, dim, want ? &e : nullptr, op_is_bf16(kpad));
     if (want) {
       eo.row_err[row0 + r0 + threadIdx.x] = e;
       atomicMax(eo.tile_max, __float_as_uint(e));  // e >= 0: bit order = value order
@@ -261,6 +262,7 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
     uint4* dst = reinterpret_cast<uint4*>(out16 + (row0 / kTileRows) * (int64_t)kTileRows * kpad);
     const int nchunks = sub * (kpad / 8);
     const int lsub = 31 - __clz(sub);  // sub is a power of two
+    const bool bf = op_is_bf16(kpad);
     for (int c = threadIdx.x; c < nchunks; c += kPrepThreads) {
       int g = c >> lsub, r = c & (sub - 1);
       __align__(16) op16_t v[8];
@@ -268,7 +270,7 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
       for (int e = 0; e < 8; e++) {
         int k = g * 8 + e;
         float x = (r < vrows && k < dim) ? sm[r * pitch + k] : 0.0f;
-        v[e] = to_op16(x);
+        v[e] = to_op16(x, bf);
       }
       dst[g * kTileRows + r0 + r] = *reinterpret_cast<uint4*>(v);
     }

@@ -20,6 +20,13 @@ def _bits_equal(ms, lo, ro, so):
             and np.array_equal(ms.sims.view(np.uint32), so.view(np.uint32)))
 
 
+def _op_dtype(dim: int):
+    """Operand image format: bf16 on the resident-R filter path (kpad <= 128),
+    fp16 on the wide path (sjb_common.cuh op_is_bf16)."""
+    from paper_2312_01476_b200 import device as D
+    return torch.bfloat16 if D.kpad(dim) <= 128 else torch.float16
+
+
 def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
     """Rebuild the row-major fp16 matrix from the tiled operand image."""
     from paper_2312_01476_b200 import device as D
@@ -53,7 +60,7 @@ def test_normalize_and_operand_image(cuda, dim):
     q = D.prepare(xs)
     assert np.array_equal(q.f32.cpu().numpy().view(np.uint32), want.view(np.uint32))
     rows, full = _decode_operand(p.op, n, dim)
-    bf = torch.from_numpy(want).to(torch.float16).view(torch.int16).numpy()
+    bf = torch.from_numpy(want).to(_op_dtype(dim)).view(torch.int16).numpy()
     kpad = full.shape[1]
     assert np.array_equal(rows[:, :dim], bf)
     assert (rows[:, dim:] == 0).all() and (full[n:] == 0).all()
@@ -186,7 +193,7 @@ def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
 
 @pytest.mark.parametrize("dim", [3, 100, 768])
 def test_rounding_error_outputs(cuda, dim):
-    """row_err bounds ||fp16(x) - x|| from above (tightly); tile_err is the
+    """row_err bounds ||op16(x) - x|| from above (tightly); tile_err is the
     per-256-row-tile maximum (zero for padding tiles)."""
     from paper_2312_01476_b200 import device as D
     rng = np.random.default_rng(dim + 5)
@@ -195,7 +202,7 @@ def test_rounding_error_outputs(cuda, dim):
     x[9] = 0.0
     p = D.prepare(torch.from_numpy(x).to(cuda))
     f = p.f32.cpu().numpy()
-    bf = torch.from_numpy(f).to(torch.float16).to(torch.float64).numpy()
+    bf = torch.from_numpy(f).to(_op_dtype(dim)).to(torch.float64).numpy()
     want = np.sqrt(((bf - f.astype(np.float64)) ** 2).sum(axis=1))
     got = p.row_err.cpu().numpy().astype(np.float64)[:n]
     assert (got >= want).all() and (got <= want * (1 + 1e-6) + 1e-30).all()

@@ -105,11 +105,13 @@ def test_c_abi_exports_every_declared_symbol():
     assert L.sjb_version() == 1
     assert L.sjb_kpad(100) == 112 and L.sjb_kpad(4) == 16
     assert L.sjb_operand_elems(300, 100) == 512 * 112
-    # fp16 operands: 2e + e^2 + 4 d 2^-24 + 1e-6, e = 2^-11 + 2^-25 sqrt(d)
-    e = 2.0 ** -11 + 2.0 ** -25 * 10.0
-    want = 2 * e * (1 + 1e-6) + e * e + 4 * 100 * 2.0 ** -24 + 1e-6
-    band = L.sjb_default_band(100)
-    assert abs(band - want) < 1e-9 and 0.00099 < band < 0.00101
+    # 2e + e^2 + 4 d 2^-24 + 1e-6, e = u + 2^-25 sqrt(d): bf16 operands
+    # (u = 2^-8) up to kpad 128, fp16 (u = 2^-11) above
+    for d, u in ((100, 2.0 ** -8), (768, 2.0 ** -11)):
+        e = u + 2.0 ** -25 * d ** 0.5
+        want = 2 * e * (1 + 1e-6) + e * e + 4 * d * 2.0 ** -24 + 1e-6
+        assert abs(L.sjb_default_band(d) - want) < 1e-9 * max(1.0, want * 1e3)
+    assert 0.0078 < L.sjb_default_band(100) < 0.0079
     assert abs(L.sjb_accum_slack(100) - (4 * 100 * 2.0 ** -24 + 2e-6)) < 1e-9
 
 

@@ -4,8 +4,8 @@
 
 Workload (BASELINE.json configs[1], fits one B200): |R| = 100,000 x |S| =
 1,000,000, d = 100, clustered generator (10,000 centroids, sigma 0.5, seed 0),
-theta = 0.8, fp16 tensor-core filter with the provable band (same dense peak as
-bf16 on B200; the roofline uses the measured bf16 figure), fp32 recheck.
+theta = 0.8, bf16 tensor-core filter with the provable band (the roofline uses
+the measured bf16 figure), fp32 recheck.
 One step = prepare(R shard) + prepare(S) [+ NCCL broadcast of S when N > 1]
 + fused join -> canonical device MatchSet.  Strong scaling: R is sharded
 across ranks, S replicated.  Inputs are synthetic (no dataset is involved).
@@ -332,7 +332,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "fp16+fp32", "data": "synthetic (seeded clustered generator)",
+            "dtype": "bf16+fp32", "data": "synthetic (seeded clustered generator)",
             "config": {"workload": "cfg2: |R|=100k x |S|=1M, d=100, theta=0.8, clustered "
                                    "(10k centroids, sigma 0.5), seed 0",
                        "global_batch": pairs_total, "parallelism": f"R-shard x{world}",

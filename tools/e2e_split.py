@@ -7,7 +7,7 @@ from paper_2312_01476_b200.join import tensor_join_vectors
 (L, S), c = datagen.config_vectors("cfg2")
 Lp, Sp = torch.from_numpy(L).pin_memory(), torch.from_numpy(S).pin_memory()
 dev = torch.device("cuda:0")
-for frac in ("0.5", "0.55", "0.6", "0.65", "0.5", "0.58"):
+for frac in (sys.argv[1:] or ["0.5", "0.55", "0.6", "0.65", "0.5", "0.58"]):
     os.environ["SJB_SPLIT_FIRST"] = frac
     for _ in range(2): tensor_join_vectors(Lp, Sp, c["theta"], device=dev)
     ts = []

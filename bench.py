@@ -1,18 +1,33 @@
-"""Benchmark of the hot path: cosine-threshold tensor join at BASELINE cfg2.
+"""Benchmark of the hot path: the cosine-threshold tensor join.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg3|cfg5] [--theta T]
 
-Workload (BASELINE.json configs[1], fits one B200): |R| = 100,000 x |S| =
-1,000,000, d = 100, clustered generator (10,000 centroids, sigma 0.5, seed 0),
-theta = 0.8, bf16 tensor-core filter with the provable band (the roofline uses
-the measured bf16 figure), fp32 recheck.
-One step = prepare(R shard) + prepare(S) [+ NCCL broadcast of S when N > 1]
-+ fused join -> canonical device MatchSet.  Strong scaling: R is sharded
-across ranks, S replicated.  Inputs are synthetic (no dataset is involved).
+Default workload: BASELINE.json configs[1] (cfg2, fits one B200): |R| =
+100,000 x |S| = 1,000,000, d = 100, clustered generator (10,000 centroids,
+sigma 0.5, seed 0), theta = 0.8; bf16 tensor-core filter with the provable
+band, canonical fp32 recheck.  --config cfg5 (200k x 200k, 500 centroids,
+the output-heavy theta sweep: --theta 0.95/0.8/0.6/0.4) and --config cfg3
+(200k + 200k strings, FastText-style subword embedding from a 2M x 100 bucket
+table, theta 0.85) print the same line for those workloads.
+
+One step (N = 1) = prepare(R) + prepare(S) + fused join -> canonical device
+MatchSet (cfg3: subword embed + normalise both relations, then the join).
+N > 1: R is sharded over the ranks (strong scaling: total work fixed); each
+rank holds its own pieces of S, prepares them once, and the prepared pieces
+are all-gathered round by round while every rank filters the rounds that
+have landed (multigpu.sharded_join_owned).  With --gpus N > 1 and no
+WORLD_SIZE in the environment, bench.py re-launches itself under
+torch.distributed.run with N ranks.
 
 Prints ONE JSON line on rank 0.  ``value`` is device-resident throughput
-(inputs in HBM), ``e2e`` is the same metric through the public API with host
-buffers (H2D of R and S, D2H of the MatchSet inside the timed region).
+(inputs in HBM), ``e2e`` the same metric through the public API with pinned
+host buffers (H2D of the inputs and D2H of the MatchSet inside the timed
+region); ``e2e_pageable`` / ``e2e_operator`` time pageable numpy inputs and
+the drop-in tensor_join(RawRelation, RawRelation, LookupModel) beside it.
+``--impl reference`` runs the UNMODIFIED reference package (baseline/_ref,
+compiled backend, all host threads) on the same workload: full joins, one
+per step.
 """
 
 from __future__ import annotations
@@ -20,7 +35,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -32,17 +49,83 @@ sys.path.insert(0, HERE)
 
 METRIC = "similarity-join pair evals/sec and % of bf16 tensor-core roofline, 1/2/4/8 B200"
 UNIT = "pair evals/s"
-CFG = dict(n_left=100_000, n_right=1_000_000, dim=100, n_centroids=10_000, sigma=0.5,
-           theta=0.8, seed=0)
+BUDGET = 64 * 1024 * 1024          # the reference CLI's default budget (cli.py:31)
+
+WORKLOADS = {
+    "cfg1": dict(kind="vectors", n_left=10_000, n_right=10_000, dim=100, n_centroids=1_000,
+                 sigma=0.5, theta=0.8, seed=0),
+    "cfg2": dict(kind="vectors", n_left=100_000, n_right=1_000_000, dim=100,
+                 n_centroids=10_000, sigma=0.5, theta=0.8, seed=0),
+    "cfg5": dict(kind="vectors", n_left=200_000, n_right=200_000, dim=100, n_centroids=500,
+                 sigma=0.5, theta=0.8, seed=0),
+    "cfg3": dict(kind="strings", n_left=200_000, n_right=200_000, dim=100,
+                 n_buckets=2_000_000, shared=0.3, theta=0.85, seed=0),
+}
+
+
+def workload(args) -> dict:
+    c = dict(WORKLOADS[args.config])
+    if args.theta is not None:
+        c["theta"] = float(args.theta)
+    c["name"] = args.config
+    if c["kind"] == "vectors":
+        c["desc"] = (f"{args.config}: |R|={c['n_left']:,} x |S|={c['n_right']:,}, d={c['dim']}, "
+                     f"theta={c['theta']}, clustered ({c['n_centroids']:,} centroids, sigma "
+                     f"{c['sigma']}), seed {c['seed']}")
+    else:
+        c["desc"] = (f"{args.config}: {c['n_left']:,} x {c['n_right']:,} strings a-z len 3-12, "
+                     f"{int(c['shared'] * 100)}% shared with 1-2 edits; subword model "
+                     f"(word + char 3-6-grams, FNV-1a mod {c['n_buckets']:,}, table "
+                     f"{c['n_buckets']:,}x{c['dim']} ~N(0,1/d)), theta={c['theta']}")
+    return c
+
+
+def make_vectors(c):
+    from paper_2312_01476_b200 import datagen
+    return datagen.clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"],
+                                  c["sigma"], c["seed"])
+
+
+def make_strings(c):
+    from paper_2312_01476_b200 import datagen
+    return datagen.strings(c["n_left"], c["n_right"], c["shared"], seed=c["seed"])
+
+
+def host_table(c) -> np.ndarray:
+    """cfg3 bucket table (host copy; seeded)."""
+    from paper_2312_01476_b200 import datagen
+    return datagen.bucket_table(c["n_buckets"], c["dim"], seed=c["seed"])
+
+
+def set_digest(lo, ro, so) -> str:
+    """Order-independent exact checksum of a match set: sum mod 2^64 of a
+    mixed 64-bit hash of (left, right, sim bits).  Rank-local sums add up
+    to the whole job's, so both arms (and any rank count) print the same
+    digest for the same MatchSet."""
+    total = np.uint64(0)
+    with np.errstate(over="ignore"):
+        for s in range(0, len(lo), 1 << 24):
+            l = np.asarray(lo[s:s + (1 << 24)], dtype=np.uint64)
+            r = np.asarray(ro[s:s + (1 << 24)], dtype=np.uint64)
+            b = np.asarray(so[s:s + (1 << 24)], dtype=np.float32).view(np.uint32).astype(np.uint64)
+            x = (l * np.uint64(0x9E3779B97F4A7C15)) ^ \
+                ((r + np.uint64(0x632BE59BD9B4E019)) * np.uint64(0xC2B2AE3D27D4EB4F)) ^ \
+                (b * np.uint64(0x165667B19E3779F9))
+            x ^= x >> np.uint64(31)
+            x *= np.uint64(0xBF58476D1CE4E5B9)
+            x ^= x >> np.uint64(29)
+            total = total + x.sum(dtype=np.uint64)
+    return f"{int(total):016x}"
 
 
 def _peaks():
     try:
         with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), "measured"
+        return (float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]),
+                float(p.get("hbm_gbs", 0)) or None, "measured")
     except Exception:
-        return 1590.0, 1400.0, "fallback"
+        return 1590.0, 1400.0, 6500.0, "fallback"
 
 
 class ClockSampler:
@@ -79,7 +162,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.01)
 
     def __enter__(self):
         if self._nv is not None:
@@ -98,13 +181,23 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference_run(L, S, theta, budget_s, threads, n_left_full):
-    """Reference CPU path (oracle/_ref: the reference's own C kernels, restated
-    orchestration) on a bounded sample: the first r rows of R x all of S.
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
-    The reference's per-join fixed costs (normalize_rows(S), pack_transpose(S),
-    join.py:337,342) are timed once; the tile loop is timed on the sample and
-    scaled to |R| rows.  Returns (pairs/s of the full job, info)."""
+
+# ---------------------------------------------------------------------------
+# CPU baseline leg of our arm: the reference's own C kernels (oracle/_ref) on a
+# bounded sample, and a bitwise comparison of the sampled rows.
+
+def cpu_reference_sample(L, S, theta, budget_s, threads, n_left_full):
+    """The reference's kernels (oracle/_ref: _kernelcore.c built from the
+    reference sources; orchestration restated from join.py) on the first r
+    rows of R x all of S, r sized to ~budget_s.  Fixed per-join costs
+    (normalize_rows(S), pack_transpose(S), join.py:337,342) are timed once.
+    Returns (pairs/s of the full job, info, sample columns)."""
     sys.path.insert(0, os.path.join(HERE, "oracle"))
     import refkern
     if not refkern.available():
@@ -115,9 +208,6 @@ def cpu_reference_run(L, S, theta, budget_s, threads, n_left_full):
     t0 = time.perf_counter()
     packed = refkern.pack_transpose(Sn)
     t_pack = time.perf_counter() - t0
-    # calibrate the per-row cost, then size the measured sample to budget_s
-    # the sample executes the full job's own tile plan (plan_rows), restricted
-    # to its first rows, so per-row cost matches the full run's
     r_cal = 128
     t0 = time.perf_counter()
     Ln, _ = refkern.normalize_rows(L[:r_cal])
@@ -128,66 +218,142 @@ def cpu_reference_run(L, S, theta, budget_s, threads, n_left_full):
     rows = max(r_cal, rows // 128 * 128)
     t0 = time.perf_counter()
     Ln, _ = refkern.normalize_rows(L[:rows])
-    lo, _, _, _ = refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed,
-                                                 plan_rows=n_left_full)
+    lo, ro, so, _ = refkern.tensor_join_normalized(Ln, Sn, theta, threads=threads, packed=packed,
+                                                   plan_rows=n_left_full)
     t_rows = time.perf_counter() - t0
     full_time = t_norm_s + t_pack + t_rows * (n_left_full / rows)
     pairs = n_left_full * S.shape[0]
     return pairs / full_time, {
         "kind": "reference", "variant": refkern.variant(), "cores": threads,
         "sample": f"first {rows} of {n_left_full} R rows x all {S.shape[0]} S rows "
-                  f"(reference tensor_join tile loop, 64 MiB budget, {threads} threads); "
-                  f"full job = normalize(S) {t_norm_s:.2f}s + pack_transpose(S) "
-                  f"{t_pack:.2f}s + sample x {n_left_full / rows:.1f}",
-        "sample_seconds": round(t_rows, 3), "sample_matches": int(len(lo))}
+                  f"(reference kernels _kernelcore.c, tile plan of the full job, 64 MiB "
+                  f"budget, {threads} threads); full job = normalize(S) {t_norm_s:.2f}s + "
+                  f"pack_transpose(S) {t_pack:.2f}s + sample x {n_left_full / rows:.1f}",
+        "sample_seconds": round(t_rows, 3), "sample_rows": rows}, (lo, ro, so)
 
 
-def host_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+def sample_parity(ref_cols, ours, rows):
+    """Bitwise comparison of the reference sample (left rows < rows) with the
+    same rows of our full result."""
+    lo, ro, so = ours
+    k = int(np.searchsorted(lo, np.uint64(rows), side="left"))
+    rl, rr, rs = ref_cols
+    eq = (len(rl) == k and np.array_equal(rl, lo[:k]) and np.array_equal(rr, ro[:k])
+          and np.array_equal(rs.view(np.uint32), so[:k].view(np.uint32)))
+    return {"sample_rows": rows, "reference_matches": int(len(rl)), "ours_matches": k,
+            "bitwise_equal": bool(eq)}
 
+
+# ---------------------------------------------------------------------------
+# Reference arm: the unmodified reference package, full joins.
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from paper_2312_01476_b200 import datagen
-    L, S = datagen.clustered_pair(CFG["n_left"], CFG["n_right"], CFG["dim"], CFG["n_centroids"],
-                                  CFG["sigma"], CFG["seed"])
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import simjoin_ref
+    c = workload(args)
     thr = host_threads()
-    vals, info = [], None
-    for i in range(args.warmup + args.steps):
-        v, info = cpu_reference_run(L, S, CFG["theta"], args.ref_step_seconds, thr,
-                                    CFG["n_left"])
-        if i >= args.warmup:
-            vals.append(v)
-    value = float(statistics.median(vals))
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * CFG["n_left"] * CFG["n_right"] / value,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "fp32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "cfg2: |R|=100k x |S|=1M, d=100, theta=0.8, clustered "
-                                   "(10k centroids, sigma 0.5), seed 0", "global_batch": None},
-            "cpu_baseline": dict(info, value=value, unit=UNIT),
+    sj = simjoin_ref.load()
+    if sj is None:
+        print(json.dumps({"impl": "reference", "unavailable": simjoin_ref.error()}), flush=True)
+        return
+    steps = max(1, min(args.steps, args.ref_steps))
+    warmup = min(args.warmup, args.ref_warmup)
+    if c["kind"] == "vectors":
+        L, S = make_vectors(c)
+        ltok = [f"l{i}" for i in range(len(L))]
+        rtok = [f"r{i}" for i in range(len(S))]
+        table = dict(zip(ltok, L))
+        table.update(zip(rtok, S))
+        model = sj.LookupModel(table, c["dim"])
+        model_desc = "LookupModel over the generated vectors"
+    else:
+        left, right = make_strings(c)
+        import oracle as O
+        tab = host_table(c)
+        t0 = time.perf_counter()
+        EL = O.subword_embed(left, tab)
+        ER = O.subword_embed(right, tab)
+        t_sub = time.perf_counter() - t0
+        ltok, rtok = left, right
+        table = dict(zip(ltok, EL))
+        table.update(zip(rtok, ER))
+        model = sj.LookupModel(table, c["dim"])
+        model_desc = (f"LookupModel over subword vectors (the reference has no subword model, "
+                      f"SPEC.md:175; oracle/sj_oracle.c embedded both relations in "
+                      f"{t_sub:.2f} s, 1 thread)")
+    left_r = sj.RawRelation("left", ltok)
+    right_r = sj.RawRelation("right", rtok)
+    pairs = len(ltok) * len(rtok)
+    walls, ms = [], None
+    for i in range(warmup + steps):
+        ms, st = sj.tensor_join(left_r, right_r, model, c["theta"], BUDGET, threads=thr)
+        if i >= warmup:
+            walls.append(st.wall_nanos / 1e9)
+    t0 = time.perf_counter()
+    sj.embed_relation(model, left_r)
+    sj.embed_relation(model, right_r)
+    t_embed = time.perf_counter() - t0
+    wall = statistics.median(walls)
+    join_only = max(wall - t_embed, 1e-9)
+    value = pairs / join_only
+    lo = np.asarray(ms.lefts, dtype=np.uint64)
+    ro = np.asarray(ms.rights, dtype=np.uint64)
+    so = np.asarray(ms.sims, dtype=np.float32)
+    # nlj_prefetch once, for context (BASELINE.md §3), on a bounded sample
+    m_rows = max(1, min(len(ltok), int(args.nlj_pairs // max(1, len(rtok)))))
+    t0 = time.perf_counter()
+    _, nst = sj.nlj_prefetch(sj.RawRelation("left", ltok[:m_rows]), right_r, model,
+                             c["theta"], threads=thr, inner="right")
+    nlj_wall = time.perf_counter() - t0
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": warmup, "steps_requested": args.steps,
+            "warmup_requested": args.warmup,
+            "ms_per_step": 1e3 * join_only, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (seeded)",
+            "impl": "reference",
+            "config": {"workload": c["desc"], "global_batch": pairs},
+            "cpu_baseline": {
+                "value": value, "unit": UNIT, "cores": thr, "kind": "reference",
+                "sample": f"none: every step is one full reference tensor_join "
+                          f"({len(ltok):,} x {len(rtok):,}; {model_desc}, budget 64 MiB, "
+                          f"threads={thr}, backend {sj.kernels.active_backend()}); value uses "
+                          f"the join-only time = JoinStats.wall_nanos - embed_relation(L, S)",
+                "full_wall_s": wall, "embed_s": t_embed, "join_only_s": join_only,
+                "full_wall_pairs_per_s": pairs / wall,
+                "step_walls_s": walls},
+            "nlj_prefetch": {"pairs_per_s": m_rows * len(rtok) / nlj_wall,
+                             "wall_s": nlj_wall, "sample": f"first {m_rows} left tuples x all "
+                                                          f"{len(rtok):,} right",
+                             "matches": int(nst.matches)},
+            "parity": {"matches": int(len(lo)), "digest": set_digest(lo, ro, so)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Our arm.
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2312_01476_b200 import build, datagen
+    from paper_2312_01476_b200 import build
     build.build()
     from paper_2312_01476_b200 import device as D
     from paper_2312_01476_b200 import multigpu as MG
 
+    c = workload(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"rank {rank} needs GPU {local}; {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -197,52 +363,69 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
+    def reduce(x: float, op) -> float:
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    def max_over_ranks(x):
+        return reduce(x, dist.ReduceOp.MAX if world > 1 else None)
 
-    L, S = datagen.clustered_pair(CFG["n_left"], CFG["n_right"], CFG["dim"], CFG["n_centroids"],
-                                  CFG["sigma"], CFG["seed"])
-    theta, dim = CFG["theta"], CFG["dim"]
-    r0, r1 = MG.shard_range(CFG["n_left"], rank, world)
-    n_shard, n_right = r1 - r0, S.shape[0]
-    R_dev = torch.from_numpy(L[r0:r1]).to(dev)
-    S_dev = torch.from_numpy(S).to(dev) if rank == 0 else torch.empty((n_right, dim),
-                                                                     dtype=torch.float32,
-                                                                     device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # 256 MiB > 126 MB L2
+    def sum_over_ranks(x):
+        return reduce(x, dist.ReduceOp.SUM if world > 1 else None)
+
+    theta, dim = c["theta"], c["dim"]
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     for e in ev:
         e.record()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # 256 MiB > 126 MB L2
+    r0, r1 = MG.shard_range(c["n_left"], rank, world)
+    n_shard, n_right = r1 - r0, c["n_right"]
+    pairs_total = c["n_left"] * n_right
+    PR_last = {}
+
+    if c["kind"] == "vectors":
+        L, S = make_vectors(c)
+        R_dev = torch.from_numpy(L[r0:r1]).to(dev)
+        if world == 1:
+            S_dev = torch.from_numpy(S).to(dev)
+
+            def step(events=None):
+                return D.join_prepared(D.prepare(R_dev), D.prepare(S_dev), theta,
+                                       left_base=r0, filter_events=events)
+        else:
+            lay = MG.piece_layout(n_right, world)
+            S_loc = torch.from_numpy(MG.local_pieces(S, lay, rank)).to(dev)
+
+            def step(events=None):
+                m, PR_last["p"] = MG.sharded_join_owned(R_dev, S_loc, lay, theta, r0)
+                return m
+    else:
+        left, right = make_strings(c)
+        g = torch.Generator(device=dev).manual_seed(c["seed"])
+        table = torch.randn((c["n_buckets"], dim), generator=g, device=dev) * (1.0 / dim ** 0.5)
+        Lb, Lo = D.pack_tokens(left[r0:r1], dev)
+        Sb, So = D.pack_tokens(right, dev)
+        import ctypes
+        from paper_2312_01476_b200 import _lib
+
+        def embed(b, o, n):
+            f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+            op = D.op_empty(n, dim, dev)
+            rep = torch.zeros(1, dtype=torch.int64, device=dev)
+            re, te = D._err_buffers(n, dev)
+            _lib.check(_lib.lib().sjb_subword_embed(
+                D._vp(b), D._vp(o), n, D._vp(table), table.shape[0], dim, 3, 6, 1, D._vp(f32),
+                D._vp(op), D._vp(rep), D._vp(re), D._vp(te), D._stream(dev)), "subword_embed")
+            return D.PreparedRelation(f32, op, n, dim, "", rep, re, te)
+
+        def step(events=None):
+            return D.join_prepared(embed(Lb, Lo, n_shard), embed(Sb, So, n_right), theta,
+                                   left_base=r0, filter_events=events)
+
     torch.cuda.synchronize()
-
-    def step():
-        if world > 1:
-            # S broadcast in row chunks, each filtered as soon as it lands
-            return MG.sharded_join_streamed(R_dev, S_dev, theta, r0)
-        return MG.sharded_join(R_dev, S_dev, theta, r0,
-                               join_fn=lambda R, Sx, th, lb, band: D.join_prepared(
-                                   D.prepare(R), D.prepare(Sx), th, band, left_base=lb,
-                                   filter_events=(ev[2], ev[3])))
-
-    def filter_only_ms():
-        """One un-timed full-S filter launch with events (N > 1: the timed
-        steps filter per S chunk, so the kernel's time is taken here)."""
-        pr, ps = D.prepare(R_dev), D.prepare(S_dev)
-        D.join_prepared(pr, ps, theta, left_base=r0, filter_events=(ev[2], ev[3]))
-        torch.cuda.synchronize()
-        return ev[2].elapsed_time(ev[3])
-
     for _ in range(args.warmup):
         m = step()
     torch.cuda.synchronize()
@@ -256,7 +439,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             barrier()
             ev[0].record()
-            m = step()
+            m = step((ev[2], ev[3]) if world == 1 else None)
             ev[1].record()
             torch.cuda.synchronize()
             step_ms.append(ev[0].elapsed_time(ev[1]))
@@ -266,95 +449,209 @@ def run_ours(args):
     launches = D.launch_count() - launches0
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
-    pairs_total = CFG["n_left"] * n_right
     value = pairs_total / (ms_per_step / 1e3)
     n_matches = int(sum_over_ranks(m.n_matches))
     n_cand = int(sum_over_ranks(m.n_candidates))
+    ours_cols = m.to_host()
+    digest_part = int(set_digest(*ours_cols), 16)
 
-    # ---- end to end through the public API with host buffers ----------------
-    from paper_2312_01476_b200.join import tensor_join_vectors
-    L_pin = torch.from_numpy(L[r0:r1]).pin_memory()
-    S_pin = torch.from_numpy(S).pin_memory() if rank == 0 else None
+    # combine the rank-local digests (sum mod 2^64) without moving match data
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, digest_part)
+        digest = f"{sum(parts) % (1 << 64):016x}"
+    else:
+        digest = f"{digest_part:016x}"
 
-    def e2e_step():
-        if world == 1:
-            ms, _ = tensor_join_vectors(L_pin, S_pin, theta, device=dev)
-            return len(ms)
-        Rd = L_pin.to(dev, non_blocking=True)
-        Sd = S_pin.to(dev, non_blocking=True) if rank == 0 else S_dev
-        mm = MG.sharded_join_streamed(Rd, Sd, theta, r0)
-        lo, ro, so = mm.to_host()
-        return len(lo)
-
-    e2e_steps = max(1, min(args.steps, 5))
-    for _ in range(min(2, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    e2e_s = []
-    for _ in range(e2e_steps):
+    # ---- filter kernel alone (N > 1: the steps filter round by round) ------
+    def filter_only_ms():
+        if c["kind"] == "vectors":
+            pl = D.prepare(R_dev)
+            pr = PR_last["p"] if world > 1 else D.prepare(S_dev)
+        else:
+            pl, pr = embed(Lb, Lo, n_shard), embed(Sb, So, n_right)
+        D.join_prepared(pl, pr, theta, left_base=r0, filter_events=(ev[2], ev[3]))
         torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        k = e2e_step()
-        torch.cuda.synchronize()
-        e2e_s.append(time.perf_counter() - t0)
-    e2e_time = max_over_ranks(statistics.median(e2e_s))
-    h2d = int(sum_over_ranks(L_pin.numel() * 4 + (S_pin.numel() * 4 if S_pin is not None else 0)))
-    d2h = int(sum_over_ranks(k * 20))
+        return ev[2].elapsed_time(ev[3])
 
-    # ---- roofline of the dominant kernel (the fused filter) -----------------
-    burst, sustained, src = _peaks()
     if not filt_ms:
         filt_ms = [filter_only_ms() for _ in range(3)]
+
+    # ---- end to end through the public API with host buffers ----------------
+    from paper_2312_01476_b200.join import tensor_join, tensor_join_vectors
+    from paper_2312_01476_b200.core import RawRelation
+    e2e_extra = {}
+    if c["kind"] == "vectors":
+        L_pin = torch.from_numpy(L[r0:r1]).pin_memory()
+        if world == 1:
+            S_pin = torch.from_numpy(S).pin_memory()
+            h2d = L_pin.numel() * 4 + S_pin.numel() * 4
+
+            def e2e_step():
+                ms, _ = tensor_join_vectors(L_pin, S_pin, theta, device=dev)
+                return len(ms)
+        else:
+            S_loc_pin = torch.from_numpy(MG.local_pieces(S, lay, rank)).pin_memory()
+            h2d = L_pin.numel() * 4 + S_loc_pin.numel() * 4
+
+            def e2e_step():
+                Rd = L_pin.to(dev, non_blocking=True)
+                Sd = S_loc_pin.to(dev, non_blocking=True)
+                mm, _ = MG.sharded_join_owned(Rd, Sd, lay, theta, r0)
+                lo, ro, so = mm.to_host()            # rank-local result, pinned host
+                return len(lo)
+    else:
+        model = None
+        from paper_2312_01476_b200.embedding import SubwordModel
+        model = SubwordModel(table)
+        Lrel = RawRelation("left", left[r0:r1])
+        Rrel = RawRelation("right", right)
+        h2d = sum(len(s) for s in left[r0:r1]) + sum(len(s) for s in right) + \
+            8 * (n_shard + n_right + 2)
+
+        def e2e_step():
+            ms, _ = tensor_join(Lrel, Rrel, model, theta, BUDGET, device=dev)
+            return len(ms)
+
+    def timed(fn, reps):
+        for _ in range(min(2, args.warmup)):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            k = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return max_over_ranks(statistics.median(ts)), k
+
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_time, k = timed(e2e_step, e2e_steps)
+    h2d = int(sum_over_ranks(h2d))
+    d2h = int(sum_over_ranks(k * 20))
+
+    if world == 1 and c["kind"] == "vectors" and not args.no_extra_e2e:
+        # pageable numpy inputs (what reference callers hold)
+        t_pg, _ = timed(lambda: len(tensor_join_vectors(L, S, theta, device=dev)[0]), 3)
+        e2e_extra["e2e_pageable"] = {"value": pairs_total / t_pg, "unit": UNIT,
+                                     "seconds_per_step": t_pg,
+                                     "inputs": "pageable numpy (tensor_join_vectors)"}
+        # the drop-in operator: tensor_join(RawRelation, RawRelation, LookupModel)
+        from paper_2312_01476_b200.embedding import LookupModel
+        ltok = [f"l{i}" for i in range(len(L))]
+        rtok = [f"r{i}" for i in range(len(S))]
+        lm = LookupModel.from_matrix(ltok + rtok, np.concatenate([L, S]))
+        Lr, Rr = RawRelation("left", ltok), RawRelation("right", rtok)
+        t_op, _ = timed(lambda: len(tensor_join(Lr, Rr, lm, theta, BUDGET, device=dev)[0]), 3)
+        e2e_extra["e2e_operator"] = {
+            "value": pairs_total / t_op, "unit": UNIT, "seconds_per_step": t_op,
+            "inputs": "tensor_join(RawRelation, RawRelation, LookupModel) with 1.1M string "
+                      "tokens (token -> row lookup on the host, table resident on the device)"}
+
+    # ---- roofline of the dominant kernel (the fused filter) -----------------
+    burst, sustained, hbm, src = _peaks()
     filt_avg = statistics.mean(filt_ms) / 1e3
     flops = 2.0 * n_shard * n_right * dim                 # algorithmic, unpadded d
     achieved = flops / filt_avg / 1e12
     long_run = sum(step_ms) / 1e3 > 1.0
     peak = sustained if long_run else burst
     traffic = None
-    tpath = os.path.join(HERE, "profiles", "filter_traffic.json")
+    tpath = os.path.join(HERE, "profiles", f"filter_traffic_{c['name']}.json")
+    if not os.path.exists(tpath) and c["name"] == "cfg2":
+        tpath = os.path.join(HERE, "profiles", "filter_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            thr = host_threads()
-            v, info = cpu_reference_run(L, S, theta, args.cpu_seconds, thr, CFG["n_left"])
+            if c["kind"] == "vectors":
+                Lc, Sc = L, S
+                emb = None
+            else:
+                sys.path.insert(0, os.path.join(HERE, "oracle"))
+                import oracle as O
+                tab = table.cpu().numpy()
+                t0 = time.perf_counter()
+                Lc = O.subword_embed(left, tab)
+                t_l = time.perf_counter() - t0
+                Sc = O.subword_embed(right, tab)
+                emb = {"kind": "port", "cores": 1, "seconds": time.perf_counter() - t0,
+                       "strings_per_s": (len(left) + len(right)) /
+                       (time.perf_counter() - t0),
+                       "what": "oracle/sj_oracle.c subword embedding of both relations "
+                               f"(left {t_l:.2f} s)"}
+            v, info, ref_cols = cpu_reference_sample(Lc, Sc, theta, args.cpu_seconds,
+                                                     host_threads(), c["n_left"])
             cpu = dict(info, value=v, unit=UNIT)
+            if emb:
+                cpu["embedding"] = emb
+            parity = sample_parity(ref_cols, ours_cols, info["sample_rows"])
         except Exception as exc:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "error": str(exc)}
+            cpu = {"value": None, "unit": UNIT, "error": f"{type(exc).__name__}: {exc}"}
+    if parity is None:
+        parity = {}
+    parity.update({"matches": n_matches, "digest": digest})
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16+fp32", "data": "synthetic (seeded clustered generator)",
-            "config": {"workload": "cfg2: |R|=100k x |S|=1M, d=100, theta=0.8, clustered "
-                                   "(10k centroids, sigma 0.5), seed 0",
-                       "global_batch": pairs_total, "parallelism": f"R-shard x{world}",
+            "dtype": "bf16+fp32", "data": "synthetic (seeded generator)",
+            "config": {"workload": c["desc"], "global_batch": pairs_total,
+                       "parallelism": f"R-shard x{world}" + (
+                           ", S owner-prepared + all-gathered per round" if world > 1 else ""),
                        "band": D.default_band(dim), "l2": "flushed (256 MiB write) between "
-                                                         "timed steps; inputs > L2",
+                                                         "timed steps",
                        "matches": n_matches, "candidates": n_cand,
+                       "output_pairs_per_s": n_matches / (ms_per_step / 1e3),
                        "launches_per_step": launches / args.steps},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": "join_filter_kernel", "filter_ms": filt_avg * 1e3,
+                         "filter_share_of_step": filt_avg * 1e3 / ms_per_step,
                          "peak_source": f"{src} {'sustained' if long_run else 'burst'}",
                          "frac_burst": achieved / burst,
                          "k_pad_cap": dim / D.kpad(dim)},
             "e2e": {"value": pairs_total / e2e_time, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_time},
+                    "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_time,
+                    "inputs": "pinned host" if c["kind"] == "vectors" else
+                              "host strings through tensor_join(RawRelation, SubwordModel)"},
+            **e2e_extra,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL), NCCL's
+    communicator log on so the rank count is visible."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_MAX_CTAS", "16")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -363,10 +660,22 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
+                    help="cfg1 is the reference's own CPU-sized case (parity, launch tests)")
+    ap.add_argument("--theta", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
+    ap.add_argument("--ref-steps", type=int, default=2,
+                    help="reference arm: full joins timed (each is a whole 1e11-pair join)")
+    ap.add_argument("--ref-warmup", type=int, default=1)
+    ap.add_argument("--nlj-pairs", type=float, default=2e9,
+                    help="reference arm: pairs in the one nlj_prefetch sample")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch(args))
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_MAX_CTAS", "16")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -596,6 +596,29 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
   const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
                                 : sjb::ceil_div(n, sjb::kTileRows);
   if (tiles == 0) return SJB_OK;
+  const bool vec = (dim & 3) == 0 && dim <= 256 && ((uintptr_t)d_table & 15) == 0 &&
+                   ((uintptr_t)d_out32 & 15) == 0 && getenv("SJB_SUBWORD_FUSED") == nullptr;
+  if (vec) {
+    // gather pass (mean rows into out32), then normalise-and-cast in place
+    if (n > 0) {
+      const uint64_t nb = (uint64_t)n_buckets, magic = ~0ULL / nb;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const int64_t want = sjb::ceil_div(n, sjb::kGatherThreads / 32);
+      const int grid = (int)sjb::mn<int64_t>(want, (int64_t)sjb_sm_count(dev) * 3);
+      auto st = as_stream(stream);
+      if (dim <= 128)
+        sjb::subword_gather_kernel<1, 12><<<grid, sjb::kGatherThreads, 0, st>>>(
+            d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32);
+      else
+        sjb::subword_gather_kernel<2, 4><<<grid, sjb::kGatherThreads, 0, st>>>(
+            d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32);
+      SJB_CK_LAUNCH("subword_gather");
+    }
+    if (!normalize) return SJB_OK;
+    return normalize_impl(d_out32, nullptr, n, dim, d_out32, d_out16, d_repaired,
+                          d_out16 ? d_row_err : nullptr, d_out16 ? d_tile_err : nullptr, stream);
+  }
   // gather-latency-bound: smaller staging sub-tiles fit twice the warps per SM
   const int sub = prep_sub_rows(dim) > 64 ? 64 : prep_sub_rows(dim);
   const int smem = sub * (int)(dim | 1) * 4;

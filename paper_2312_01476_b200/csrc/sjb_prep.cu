@@ -483,6 +483,109 @@ subword_embed_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restric
   if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
+// Gather-only subword embedding (dim % 4 == 0, dim <= 128 * V): one warp per
+// string, grid-stride over the strings.  Lane q hashes item q of the batch;
+// lane l owns the float4 columns l + 32 v (v < V), so every item row is read
+// with 16-byte loads (a d = 100 row is 25 float4 = 25 lanes) and KU items'
+// loads are in flight before their adds, which run in item order per column
+// (bit-exact with the sequential fp32 sum).  Writes the mean rows (fp32,
+// row-major, coalesced float4 stores); normalisation and the operand image
+// are a separate normalize_cast pass over these rows (from L2 at cfg3
+// sizes), so this kernel is nothing but the HBM gather.
+__device__ __forceinline__ uint64_t mod_u64(uint64_t h, uint64_t d, uint64_t magic) {
+  // magic = floor((2^64 - 1) / d): q is floor(h / d) or at most 2 below
+  uint64_t r = h - __umul64hi(h, magic) * d;
+  while (r >= d) r -= d;
+  return r;
+}
+
+__device__ __forceinline__ uint64_t subword_item_bucket(const uint8_t* __restrict__ w, int len,
+                                                        int item, int minn, uint64_t nb,
+                                                        uint64_t magic) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  if (item == 0) {
+    for (int k = 0; k < len; k++) {
+      h ^= (uint64_t)w[k];
+      h *= 0x100000001b3ULL;
+    }
+  } else {
+    const int ml = len + 2;
+    int rem = item - 1, g = minn;
+    while (rem >= max(0, ml - g + 1)) {
+      rem -= max(0, ml - g + 1);
+      g++;
+    }
+    for (int k = rem; k < rem + g; k++) {
+      h ^= (uint64_t)marked_byte(w, len, k);
+      h *= 0x100000001b3ULL;
+    }
+  }
+  return mod_u64(h, nb, magic);
+}
+
+constexpr int kGatherThreads = 256;
+
+template <int V, int KU>
+__global__ void __launch_bounds__(kGatherThreads, 3)
+subword_gather_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
+                      int64_t n, const float* __restrict__ table, uint64_t n_buckets,
+                      uint64_t magic, int dim, int minn, int maxn, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * kGatherThreads) >> 5;
+  const int q4 = dim >> 2;
+  const float4* __restrict__ t4 = reinterpret_cast<const float4*>(table);
+  float4* __restrict__ o4 = reinterpret_cast<float4*>(out);
+  for (int64_t t = ((int64_t)blockIdx.x * kGatherThreads + threadIdx.x) >> 5; t < n; t += nwarps) {
+    const int64_t b = offs[t];
+    const int len = (int)(offs[t + 1] - b);
+    const uint8_t* w = bytes + b;
+    const int ml = len + 2;
+    int n_items = 1;
+    for (int g = minn; g <= maxn; g++) n_items += max(0, ml - g + 1);
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int b0 = 0; b0 < n_items; b0 += 32) {
+      const int item = b0 + lane;
+      const uint64_t bucket =
+          item < n_items ? subword_item_bucket(w, len, item, minn, n_buckets, magic) : 0;
+      const int nb = min(32, n_items - b0);
+      for (int q0 = 0; q0 < nb; q0 += KU) {
+        float4 val[KU][V];
+#pragma unroll
+        for (int u = 0; u < KU; u++) {
+          const uint64_t bq = __shfl_sync(0xffffffffu, bucket, (q0 + u) & 31);
+          const float4* src = t4 + bq * (uint64_t)q4;
+#pragma unroll
+          for (int v = 0; v < V; v++) {
+            const int c = lane + 32 * v;
+            val[u][v] = (q0 + u < nb && c < q4) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < KU; u++)
+          if (q0 + u < nb) {
+#pragma unroll
+            for (int v = 0; v < V; v++) {
+              acc[v].x = __fadd_rn(acc[v].x, val[u][v].x);
+              acc[v].y = __fadd_rn(acc[v].y, val[u][v].y);
+              acc[v].z = __fadd_rn(acc[v].z, val[u][v].z);
+              acc[v].w = __fadd_rn(acc[v].w, val[u][v].w);
+            }
+          }
+      }
+    }
+    const float cnt = (float)n_items;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      const int c = lane + 32 * v;
+      if (c < q4)
+        o4[t * q4 + c] = make_float4(__fdiv_rn(acc[v].x, cnt), __fdiv_rn(acc[v].y, cnt),
+                                     __fdiv_rn(acc[v].z, cnt), __fdiv_rn(acc[v].w, cnt));
+    }
+  }
+}
+
 // Row L2 norms in fp64, returned as fp32 (sj_row_norms, _kernelcore.c:116-124).
 __global__ void row_norms_kernel(const float* __restrict__ m, int64_t n, int dim,
                                  float* __restrict__ out) {

@@ -8,7 +8,8 @@ or without the built library these functions raise.
 Pipeline of one join:
 
   prepare(raw)         normalize_cast kernel: canonical fp32 rows (bitwise
-                       sj_normalize_rows) + fp16 operand image (tiled layout)
+                       sj_normalize_rows) + 16-bit operand image (tiled
+                       layout; bf16 for kpad <= 128, fp16 above)
   join_prepared(L, R)  tcgen05 filter (approx >= theta - band) -> canonical
                        fp32 recheck -> row bucketing -> per-row sort ->
                        MatchSet columns (u64 lefts, u64 rights, f32 sims)
@@ -63,9 +64,21 @@ def operand_elems(n: int, dim: int) -> int:
     return int(_lib.lib().sjb_operand_elems(n, dim))
 
 
+def op_dtype(dim: int) -> torch.dtype:
+    """Element type of the operand image (sjb_common.cuh op_is_bf16): bf16 for
+    kpad <= 128 (the resident-R filter), fp16 for the K-streaming wide path."""
+    return torch.bfloat16 if kpad(dim) <= 128 else torch.float16
+
+
+def op_empty(n: int, dim: int, dev: torch.device) -> torch.Tensor:
+    """Uninitialised operand image for n rows (sjb_operand_elems elements)."""
+    return torch.empty(operand_elems(n, dim), dtype=op_dtype(dim), device=dev)
+
+
 def default_band(dim: int) -> float:
-    """Provably sufficient fp16 filter margin for unit vectors (C ABI
-    sjb_default_band): 2e + e^2 + accumulation slack, e = 2^-11 + 2^-25 sqrt(d)."""
+    """Provably sufficient 16-bit filter margin for unit vectors (C ABI
+    sjb_default_band): 2e + e^2 + accumulation slack, e = u + 2^-25 sqrt(d),
+    u = 2^-8 for bf16 operands (kpad <= 128), 2^-11 for fp16 (above)."""
     return float(_lib.lib().sjb_default_band(dim))
 
 
@@ -74,13 +87,13 @@ class PreparedRelation:
     """A relation resident in HBM in the two forms the join reads."""
 
     f32: torch.Tensor          # (n, dim) canonical normalised fp32 rows
-    op: torch.Tensor           # fp16 operand image (sjb_operand_elems elements)
+    op: torch.Tensor           # 16-bit operand image (op_dtype; sjb_operand_elems elements)
     n: int
     dim: int
     name: str = ""
     repaired_dev: Optional[torch.Tensor] = None  # (1,) int64 repaired-row counter
-    # fp16 rounding errors (sjb_join_args.left_row_err / right_tile_err):
-    row_err: Optional[torch.Tensor] = None       # (n,) >= ||fp16(x_i) - x_i||
+    # 16-bit rounding errors (sjb_join_args.left_row_err / right_tile_err):
+    row_err: Optional[torch.Tensor] = None       # (n,) >= ||op(x_i) - x_i||
     tile_err: Optional[torch.Tensor] = None      # (tiles,) max over each 256-row tile
 
     @property
@@ -123,13 +136,13 @@ def _check_matrix(x: torch.Tensor, what: str) -> None:
 
 def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = None
             ) -> PreparedRelation:
-    """Normalise rows (bitwise sj_normalize_rows) and build the fp16 image."""
+    """Normalise rows (bitwise sj_normalize_rows) and build the operand image."""
     _check_matrix(raw, "relation")
     L = _lib.lib()
     n, dim = raw.shape
     dev = raw.device
     f32 = out32 if out32 is not None else torch.empty_like(raw)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
+    op = op_empty(n, dim, dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
@@ -150,7 +163,7 @@ def prepare_pieces(raw: torch.Tensor, pieces, name: str = ""):
     n, dim = raw.shape
     dev = raw.device
     f32 = torch.empty_like(raw)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
+    op = op_empty(n, dim, dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     kp = kpad(dim)
@@ -380,10 +393,10 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
 
 def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, cand_cap: int,
                left_base: int, use_err: bool, right_tile_err: Optional[torch.Tensor],
-               recheck: int = 0) -> "_lib.JoinArgs":
+               recheck: int = 0, grid: int = 0) -> "_lib.JoinArgs":
     return _lib.JoinArgs(n_left=L.n, n_right=n_right, dim=L.dim, theta=theta32, band=band,
                          cand_cap=int(cand_cap), out_cap=int(cand_cap), left_base=int(left_base),
-                         grid=0, tiles_per_chunk=0, ev_filter_begin=None, ev_filter_end=None,
+                         grid=int(grid), tiles_per_chunk=0, ev_filter_begin=None, ev_filter_end=None,
                          left_row_err=L.row_err.data_ptr() if use_err else None,
                          right_tile_err=right_tile_err.data_ptr() if use_err else None,
                          recheck=recheck)
@@ -405,10 +418,132 @@ def _stream_chunks(n: int, chunks: int, lead: int = 4):
     return spans
 
 
+class JoinSession:
+    """One join whose right relation becomes ready in row ranges (the C ABI's
+    incremental join: sjb_join_begin, sjb_join_filter_tiles per range,
+    sjb_join_finish).  `R` is the PreparedRelation the rows are prepared
+    into; filter_rows(r0, r1) queues the filter + recheck of rows [r0, r1)
+    (ranges disjoint, in order, r0 on 256-row tile boundaries) once those rows
+    are prepared on the current stream; finish() queues the canonical-order
+    pass and returns a PendingJoin.  On candidate overflow the PendingJoin
+    reruns the whole join on R (complete by then) with the measured capacity.
+    `grid` < SM count leaves SMs free for kernels that must run beside the
+    filter (NCCL's collective kernels in the multi-GPU streamed join)."""
+
+    def __init__(self, L: PreparedRelation, R: PreparedRelation, theta: float,
+                 band: Optional[float] = None, left_base: int = 0, grid: int = 0):
+        if L.dim != R.dim:
+            raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
+        self.L, self.R, self.theta, self.left_base, self.grid = L, R, theta, left_base, grid
+        self.lib = _lib.lib()
+        dev = self.dev = L.device
+        n, dim = R.n, R.dim
+        theta32 = float(np.float32(theta))
+        self.band = band = default_band(dim) if band is None else float(band)
+        self.key = (L.n, n, dim, theta32, float(np.float32(band)), grid, 0, True)
+        with _cap_lock:
+            self.cand_cap = max(_cap_cache.get(self.key, 0), initial_capacity(L.n, n))
+        self.empty = L.n == 0 or n == 0
+        if self.empty:
+            return
+        use_err = L.row_err is not None and R.tile_err is not None
+        with torch.cuda.device(dev):
+            self.args = _join_args(L, n, theta32, band, self.cand_cap, left_base, use_err,
+                                   R.tile_err, _recheck_mode(self.key, L.n * n), grid)
+            self.ws_bytes = int(self.lib.sjb_join_workspace_bytes(ctypes.byref(self.args)))
+            if self.ws_bytes < 0:
+                _lib.check(-3, "sjb_join_workspace_bytes")
+            self.ws = _workspace(self.ws_bytes, dev)
+            cap = max(int(self.cand_cap), 1)
+            self.lefts = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.rights = torch.empty_like(self.lefts)
+            self.sims = torch.empty(cap, dtype=torch.float32, device=dev)
+            self.info_t = torch.zeros(5, dtype=torch.int64, device=dev)
+            _lib.check(self.lib.sjb_join_begin(ctypes.byref(self.args), _vp(self.ws),
+                                               self.ws_bytes, _stream(dev)), "sjb_join_begin")
+
+    def filter_rows(self, r0: int, r1: int) -> None:
+        if self.empty or r1 <= r0:
+            return
+        if r0 % TILE_ROWS:
+            raise ValueError(f"row range [{r0}, {r1}) does not start on a tile boundary")
+        L, R = self.L, self.R
+        with torch.cuda.device(self.dev):
+            _lib.check(self.lib.sjb_join_filter_tiles(
+                _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(self.args),
+                _vp(self.ws), self.ws_bytes, r0 // TILE_ROWS, -(-min(r1, R.n) // TILE_ROWS),
+                _stream(self.dev)), "sjb_join_filter_tiles")
+
+    def finish(self) -> PendingJoin:
+        L, R, dev = self.L, self.R, self.dev
+        if self.empty:
+            return join_prepared_async(L, R, self.theta, self.band, left_base=self.left_base)
+        with torch.cuda.device(dev):
+            _lib.check(self.lib.sjb_join_finish(
+                _vp(L.f32), _vp(R.f32), ctypes.byref(self.args), _vp(self.ws), self.ws_bytes,
+                _vp(self.lefts), _vp(self.rights), _vp(self.sims), _vp(self.info_t),
+                _stream(dev)), "sjb_join_finish")
+        cand_cap, key = self.cand_cap, self.key
+
+        def finish(info) -> DeviceMatches:
+            n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
+            flags = info[3:4].view(np.int32)
+            if int(flags[0]):
+                # candidate capacity overflowed: R is complete now; rerun with room
+                with torch.cuda.device(dev):
+                    m = join_prepared(L, R, self.theta, self.band,
+                                      cand_cap=max(needed, n_matches, cand_cap + 1),
+                                      left_base=self.left_base, grid=self.grid)
+                m.retries += 1
+                return m
+            with _cap_lock:
+                _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
+            return DeviceMatches(self.lefts[:n_matches], self.rights[:n_matches],
+                                 self.sims[:n_matches], n_matches, n_cand, int(cand_cap), 0,
+                                 int(flags[1]))
+
+        return PendingJoin(self.info_t, finish)
+
+
+def empty_prepared(n: int, dim: int, dev: torch.device, name: str = "",
+                   rows: Optional[int] = None, f32: Optional[torch.Tensor] = None
+                   ) -> PreparedRelation:
+    """Uninitialised prepared buffers for a relation of n rows whose rows are
+    prepared later (piece by piece, or by another rank and gathered).  `rows`
+    >= n over-allocates every buffer to `rows` rows (a multiple of 512) so
+    equal-sized pieces tile it; only the first n rows are joined."""
+    rows = n if rows is None else rows
+    if f32 is None:
+        f32 = torch.empty((rows, dim), dtype=torch.float32, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    re, te = _err_buffers(rows, dev)
+    return PreparedRelation(f32, op_empty(rows, dim, dev), n, dim, name, rep, re, te)
+
+
+def prepare_into(raw: torch.Tensor, R: PreparedRelation, r0: int) -> None:
+    """Normalise raw rows (m, dim) into rows [r0, r0 + m) of the prepared
+    buffers R (r0 on a 512-row boundary), on the current stream."""
+    _check_matrix(raw, "relation")
+    m, dim = raw.shape
+    if r0 % (2 * TILE_ROWS) or dim != R.dim or r0 + m > R.f32.shape[0]:
+        raise ValueError(f"bad piece [{r0}, {r0 + m}) for prepared rows {R.f32.shape[0]}")
+    if m == 0:
+        return
+    kp = kpad(dim)
+    t0 = r0 // TILE_ROWS
+    with torch.cuda.device(R.device):
+        _lib.check(_lib.lib().sjb_normalize_rows(
+            _vp(raw), m, dim, ctypes.c_void_p(R.f32.data_ptr() + r0 * dim * 4),
+            ctypes.c_void_p(R.op.data_ptr() + t0 * TILE_ROWS * kp * 2), _vp(R.repaired_dev),
+            ctypes.c_void_p(R.row_err.data_ptr() + r0 * 4),
+            ctypes.c_void_p(R.tile_err.data_ptr() + t0 * 4), _stream(R.device)),
+            "sjb_normalize_rows")
+
+
 def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
                  band: Optional[float] = None, left_base: int = 0, chunks: int = 8,
-                 inplace: bool = False, name: str = "", spans=None, sync: bool = True
-                 ) -> Tuple["DeviceMatches", PreparedRelation]:
+                 inplace: bool = False, name: str = "", spans=None, sync: bool = True,
+                 grid: int = 0) -> Tuple["DeviceMatches", PreparedRelation]:
     """Join a prepared left relation with a right relation that becomes
     available on the device chunk by chunk.
 
@@ -416,81 +551,24 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     must make rows [r0, r1) of it ready on the current stream (wait for a
     copy or a broadcast) -- it is called in row order, on 512-row boundaries.
     Each chunk is then normalised (canonical fp32 rows + its tiles of the
-    fp16 image + rounding errors; in place when `inplace`) and its S tiles
-    are filtered at once (sjb_join_begin / sjb_join_filter_tiles /
-    sjb_join_finish), so the filter overlaps the arrival of later chunks.
-    Same result as prepare + join_prepared.  Returns the matches (a
-    PendingJoin when sync=False) and the prepared right relation (resident,
-    reusable)."""
-    lib = _lib.lib()
+    operand image + rounding errors; in place when `inplace`) and its S tiles
+    are filtered at once (JoinSession), so the filter overlaps the arrival of
+    later chunks.  Same result as prepare + join_prepared.  Returns the
+    matches (a PendingJoin when sync=False) and the prepared right relation
+    (resident, reusable: every span is normalised even when L is empty)."""
     dev = L.device
     n, dim = raw.shape
     if dim != L.dim:
         raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {dim}")
-    theta32 = float(np.float32(theta))
-    band = default_band(dim) if band is None else float(band)
-    key = (L.n, n, dim, theta32, float(np.float32(band)), 0, 0, True)
-    with _cap_lock:
-        cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, n))
-    f32 = raw if inplace else torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
-    rep = torch.zeros(1, dtype=torch.int64, device=dev)
-    re, te = _err_buffers(n, dev)
-    R = PreparedRelation(f32, op, n, dim, name, rep, re, te)
+    R = empty_prepared(n, dim, dev, name, f32=raw if inplace else None)
     spans = _stream_chunks(n, chunks) if spans is None else spans
-    if L.n == 0 or n == 0:
-        for r0, r1 in spans:
-            arrive(r0, r1)
-        pending = join_prepared_async(L, R, theta, band, left_base=left_base)
-        return (pending if not sync else pending.result()), R
-    use_err = L.row_err is not None
-    kp = kpad(dim)
+    session = JoinSession(L, R, theta, band, left_base, grid)
     with torch.cuda.device(dev):
-        cs = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-        args = _join_args(L, n, theta32, band, cand_cap, left_base, use_err, te,
-                          _recheck_mode(key, L.n * n))
-        ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
-        if ws_bytes < 0:
-            _lib.check(-3, "sjb_join_workspace_bytes")
-        ws = _workspace(ws_bytes, dev)
-        lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
-        rights = torch.empty_like(lefts)
-        sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
-        info_t = torch.zeros(5, dtype=torch.int64, device=dev)
-        _lib.check(lib.sjb_join_begin(ctypes.byref(args), _vp(ws), ws_bytes, cs), "sjb_join_begin")
         for r0, r1 in spans:
             arrive(r0, r1)
-            t0 = r0 // TILE_ROWS
-            _lib.check(lib.sjb_normalize_rows(
-                ctypes.c_void_p(raw.data_ptr() + r0 * dim * 4), r1 - r0, dim,
-                ctypes.c_void_p(f32.data_ptr() + r0 * dim * 4),
-                ctypes.c_void_p(op.data_ptr() + t0 * TILE_ROWS * kp * 2), _vp(rep),
-                ctypes.c_void_p(re.data_ptr() + r0 * 4), ctypes.c_void_p(te.data_ptr() + t0 * 4),
-                cs), "sjb_normalize_rows")
-            _lib.check(lib.sjb_join_filter_tiles(
-                _vp(L.f32), _vp(L.op), _vp(f32), _vp(op), ctypes.byref(args), _vp(ws), ws_bytes,
-                t0, -(-r1 // TILE_ROWS), cs), "sjb_join_filter_tiles")
-        _lib.check(lib.sjb_join_finish(_vp(L.f32), _vp(f32), ctypes.byref(args), _vp(ws),
-                                       ws_bytes, _vp(lefts),
-                                       _vp(rights), _vp(sims), _vp(info_t), cs),
-                   "sjb_join_finish")
-
-    def finish(info) -> DeviceMatches:
-        n_matches, n_cand, needed = int(info[0]), int(info[1]), int(info[2])
-        flags = info[3:4].view(np.int32)
-        if int(flags[0]):
-            # candidate capacity overflowed: S is resident now; rerun with room
-            with torch.cuda.device(dev):
-                m = join_prepared(L, R, theta, band, cand_cap=max(needed, n_matches, cand_cap + 1),
-                                  left_base=left_base)
-            m.retries += 1
-            return m
-        with _cap_lock:
-            _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
-        return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
-                             n_cand, int(cand_cap), 0, int(flags[1]))
-
-    pending = PendingJoin(info_t, finish)
+            prepare_into(raw[r0:r1], R, r0)
+            session.filter_rows(r0, r1)
+        pending = session.finish()
     return (pending if not sync else pending.result()), R
 
 
@@ -565,7 +643,7 @@ def prepare_gather(table: torch.Tensor, index: torch.Tensor, name: str = "") -> 
     n, dim = int(index.numel()), table.shape[1]
     dev = table.device
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev)
+    op = op_empty(n, dim, dev)
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev)
     with torch.cuda.device(dev):
@@ -644,7 +722,7 @@ def subword_rows(tokens, table: torch.Tensor, minn: int, maxn: int,
     b, o = pack_tokens(tokens, dev)
     n, dim = len(tokens), table.shape[1]
     f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
-    op = torch.empty(operand_elems(n, dim), dtype=torch.float16, device=dev) if prepared else None
+    op = op_empty(n, dim, dev) if prepared else None
     rep = torch.zeros(1, dtype=torch.int64, device=dev)
     re, te = _err_buffers(n, dev) if prepared else (None, None)
     with torch.cuda.device(dev):

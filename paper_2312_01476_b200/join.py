@@ -123,10 +123,14 @@ def join_prepared(left: D.PreparedRelation, right: D.PreparedRelation, theta,
 
 
 def _run(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta, threads: int,
-         algo: str, inner: str, band, dev) -> Tuple[MatchSet, JoinStats]:
+         algo: str, inner: str, band, dev, devices=None) -> Tuple[MatchSet, JoinStats]:
     t = Threshold.of(theta)
     if threads < 1:
         raise ValueError("threads must be >= 1")
+    if devices is not None and len(devices) > 1:
+        return _run_devices(left, right, model, t, threads, algo, inner, band, devices)
+    if devices is not None and len(devices) == 1:
+        dev = devices[0]
     dev = _device(dev)
     t0 = time.perf_counter_ns()
     with torch.cuda.device(dev):
@@ -141,16 +145,74 @@ def _run(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta, th
     return matches, stats
 
 
+def copy_prepared(p: D.PreparedRelation, dev: torch.device) -> D.PreparedRelation:
+    """A prepared relation copied to another device (peer copies over
+    NVLink when both are GPUs of one node); bitwise the same buffers."""
+    if p.device == dev:
+        return p
+    with torch.cuda.device(dev):
+        cp = (lambda x: None if x is None else x.to(dev, non_blocking=True))
+        return D.PreparedRelation(cp(p.f32), cp(p.op), p.n, p.dim, p.name, cp(p.repaired_dev),
+                                  cp(p.row_err), cp(p.tile_err))
+
+
+def _run_devices(left: RawRelation, right: RawRelation, model: EmbeddingModel, t: Threshold,
+                 threads: int, algo: str, inner: str, band, devices
+                 ) -> Tuple[MatchSet, JoinStats]:
+    """The operator on several GPUs of one process: the reference splits the
+    outer rows over `threads` workers (join.py:121-142, row bounds
+    join.py:263-264); here device k owns left rows [n*k/N, n*(k+1)/N).  The
+    right relation is embedded and prepared ONCE (|S| model calls) on the
+    first device and copied, prepared, to the others; every device embeds
+    only its own left rows, so model calls stay |R| + |S|.  All joins are
+    queued before any result is read; each device's canonical rows, shifted
+    by its r0, concatenate in device order to the canonical MatchSet."""
+    from .multigpu import concat_shards, shard_range
+    devs = [torch.device(d) for d in devices]
+    for d in devs:
+        if d.type != "cuda":
+            raise ValueError(f"devices must be CUDA devices, got {d}")
+    D.require_cuda()
+    t0 = time.perf_counter_ns()
+    with torch.cuda.device(devs[0]):
+        pr0 = prepare_relation(model, right, devs[0])
+    pending = []
+    for k, d in enumerate(devs):
+        r0, r1 = shard_range(len(left), k, len(devs))
+        with torch.cuda.device(d):
+            pr = copy_prepared(pr0, d)
+            pl = prepare_relation(model, RawRelation(left.name, left.tokens[r0:r1]), d)
+            pending.append((d, D.join_prepared_async(pl, pr, t.value, band, left_base=r0)))
+    parts = []
+    for d, p in pending:
+        with torch.cuda.device(d):
+            m = p.result()
+            parts.append(m.to_host() if m.n_matches else
+                         (np.empty(0, np.uint64), np.empty(0, np.uint64),
+                          np.empty(0, np.float32)))
+    lo, ro, so = concat_shards(parts)
+    matches = MatchSet(left.name, right.name, lo, ro, so) if len(lo) else \
+        MatchSet(left.name, right.name)
+    wall = time.perf_counter_ns() - t0
+    stats = JoinStats(wall_nanos=wall, model_calls_left=len(left), model_calls_right=len(right),
+                      pairs_compared=len(left) * len(right), matches=len(matches),
+                      peak_buffer_bytes=0, threads=threads, algo=algo, inner_relation=inner)
+    return matches, stats
+
+
 def tensor_join(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta,
                 budget_bytes: int, threads: int = 1, *, band: Optional[float] = None,
-                device=None) -> Tuple[MatchSet, JoinStats]:
+                device=None, devices=None) -> Tuple[MatchSet, JoinStats]:
     """Tensor formulation (join.py:317-373) on the device: embed once per
-    relation, normalise, fused filter + canonical recheck, canonical order."""
+    relation, normalise, fused filter + canonical recheck, canonical order.
+    devices=[...] shards the left rows over several GPUs of this process
+    (the reference's in-operator parallelism, join.py:121-142); the result
+    is the same MatchSet."""
     Threshold.of(theta)
     if threads < 1:
         raise ValueError("threads must be >= 1")
     plan_batches(len(left), len(right), model.dim, budget_bytes)  # validates the budget
-    return _run(left, right, model, theta, threads, "tensor", "right", band, device)
+    return _run(left, right, model, theta, threads, "tensor", "right", band, device, devices)
 
 
 def e_selection(raw: RawRelation, model: EmbeddingModel, probe: str, theta, *,
@@ -183,11 +245,13 @@ def e_selection(raw: RawRelation, model: EmbeddingModel, probe: str, theta, *,
 
 def nlj_prefetch(left: RawRelation, right: RawRelation, model: EmbeddingModel, theta,
                  threads: int = 1, inner: Optional[str] = None, *,
-                 band: Optional[float] = None, device=None) -> Tuple[MatchSet, JoinStats]:
+                 band: Optional[float] = None, device=None,
+                 devices=None) -> Tuple[MatchSet, JoinStats]:
     """Prefetch NLJ (join.py:238-294): identical result to tensor_join; the
     inner-relation choice is recorded in the stats as the reference does."""
     inner_name = _pick_inner(left, right, inner)
-    return _run(left, right, model, theta, threads, "prefetch_nlj", inner_name, band, device)
+    return _run(left, right, model, theta, threads, "prefetch_nlj", inner_name, band, device,
+                devices)
 
 
 ArrayLike = Union[np.ndarray, torch.Tensor]

@@ -1,15 +1,19 @@
-"""BASELINE-size joins on the GPU, checked through properties that need no
-full CPU join (the oracle would take hours at these sizes):
+"""BASELINE-size joins on the GPU, compared IN FULL with the reference.
 
-* canonical order: (left, right) strictly increasing, i.e. sorted and
-  duplicate-free like MatchSet.canonicalize (core.py:196-213);
-* every similarity >= fp32(theta) (the inclusive decision, linalg.py:151);
-* complete rows: for a seeded sample of left rows, the GPU's matches of those
-  rows (offsets, order and fp32 bits) equal the oracle's join of the sampled
-  rows against the whole right relation;
-* path agreement: the host-input public API (streamed S copy, split left,
-  pinned result buffers) returns the same bits as the device-resident join,
-  and R-sharded joins concatenate to it (multigpu's assembly rule).
+Every test here joins a BASELINE.json configuration on the GPU and compares
+the complete MatchSet -- offsets, canonical order and fp32 similarity bits --
+with the reference's own result on the same inputs, computed on the GPU
+box's host cores in the same test:
+
+* the unmodified reference package (baseline/_ref: ``simjoin.tensor_join``,
+  compiled backend) through its public API with a LookupModel over the
+  generated vectors (join.py:317-373 -> _kernelcore.c:273-323), when it is
+  installed; otherwise the reference's kernels built from its sources
+  (oracle/_ref, orchestration restated in oracle/refkern.py);
+* cfg4 (d = 768) uses oracle/_ref directly: the reference package's
+  per-token Python embedding would dominate the run.
+
+No count is pinned by a constant: the expected set is the reference's.
 """
 import os
 
@@ -32,20 +36,40 @@ def _check_canonical(lo, ro, so, theta):
     assert (so >= np.float32(theta)).all()
 
 
-def _rows_match_oracle(L, S, lo, ro, so, theta, n_rows, seed):
-    rng = np.random.default_rng(seed)
-    rows = np.sort(rng.choice(L.shape[0], size=n_rows, replace=False)).astype(np.uint64)
-    wl, wr, ws = O.join_raw(L[rows.astype(np.int64)], S, theta, threads=THREADS)
-    wl = rows[wl.astype(np.int64)]
-    starts = np.searchsorted(lo, rows, side="left")
-    ends = np.searchsorted(lo, rows, side="right")
-    gl = np.concatenate([lo[a:b] for a, b in zip(starts, ends)])
-    gr = np.concatenate([ro[a:b] for a, b in zip(starts, ends)])
-    gs = np.concatenate([so[a:b] for a, b in zip(starts, ends)])
-    assert len(wl) > 0, "sample without matches proves nothing"
-    assert np.array_equal(gl, wl) and np.array_equal(gr, wr)
-    assert np.array_equal(gs.view(np.uint32), ws.view(np.uint32))
-    return len(wl)
+def _reference_join(L, S, theta, tokens=None):
+    """The reference's full MatchSet for prefetched vectors (see module doc).
+    tokens=(left, right) joins token relations through a LookupModel built
+    from them (repeated tokens map to one vector)."""
+    import simjoin_ref
+    sj = simjoin_ref.load()
+    if sj is not None and simjoin_ref.compiled(sj):
+        lt, rt = tokens if tokens is not None else \
+            ([f"l{i}" for i in range(len(L))], [f"r{i}" for i in range(len(S))])
+        table = dict(zip(lt, L))
+        table.update(zip(rt, S))
+        model = sj.LookupModel(table, L.shape[1])
+        ms, st = sj.tensor_join(sj.RawRelation("left", lt), sj.RawRelation("right", rt), model,
+                                theta, 64 << 20, threads=THREADS)
+        assert st.pairs_compared == len(L) * len(S)
+        return (np.asarray(ms.lefts, np.uint64), np.asarray(ms.rights, np.uint64),
+                np.asarray(ms.sims, np.float32))
+    return _refkern_join(L, S, theta)
+
+
+def _refkern_join(L, S, theta):
+    import refkern
+    assert refkern.available(), "oracle/_ref (the reference's kernels) is not built"
+    lo, ro, so, _ = refkern.tensor_join_vectors(L, S, theta, threads=THREADS)
+    return lo, ro, so
+
+
+def _assert_same(got, want):
+    lo, ro, so = got
+    wl, wr, ws = want
+    assert len(wl) > 0, "an empty reference result proves nothing"
+    assert len(lo) == len(wl), f"{len(lo)} matches vs the reference's {len(wl)}"
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
 
 
 def _device_join(L, S, theta):
@@ -56,17 +80,18 @@ def _device_join(L, S, theta):
     return m.to_host()
 
 
-def test_cfg2_full_size():
-    """BASELINE configs[1]: 100k x 1M, d = 100, theta = 0.8 (the bench workload)."""
+def test_cfg2_full_set_equals_reference():
+    """BASELINE configs[1] (the bench workload): 100k x 1M, d = 100,
+    theta = 0.8 -- the whole MatchSet against the reference's."""
     from paper_2312_01476_b200 import datagen
     from paper_2312_01476_b200 import multigpu as MG
     from paper_2312_01476_b200.join import tensor_join_vectors
     (L, S), c = datagen.config_vectors("cfg2")
     theta = c["theta"]
-    lo, ro, so = _device_join(L, S, theta)
-    _check_canonical(lo, ro, so, theta)
-    assert len(lo) == 5_334_467           # the count every earlier run reported
-    _rows_match_oracle(L, S, lo, ro, so, theta, 96, seed=1)
+    got = _device_join(L, S, theta)
+    _check_canonical(*got, theta)
+    _assert_same(got, _reference_join(L, S, theta))
+    lo, ro, so = got
     # the public host-input path: streamed S copy, split left, pinned output
     ms, stats = tensor_join_vectors(torch.from_numpy(L).pin_memory(),
                                     torch.from_numpy(S).pin_memory(), theta,
@@ -74,43 +99,68 @@ def test_cfg2_full_size():
     assert stats.pairs_compared == L.shape[0] * S.shape[0]
     assert np.array_equal(ms.lefts, lo) and np.array_equal(ms.rights, ro)
     assert np.array_equal(ms.sims.view(np.uint32), so.view(np.uint32))
-    # R-sharded joins (3 ranks' row ranges on one device) concatenate to it
+    # 3 ranks' shares, owner-prepared S on one device, concatenate to it
     dev = torch.device("cuda", 0)
-    Sd = torch.from_numpy(S).to(dev)
     parts = []
     for r in range(3):
         r0, r1 = MG.shard_range(L.shape[0], r, 3)
-        parts.append(MG.sharded_join_streamed(torch.from_numpy(L[r0:r1]).to(dev), Sd, theta, r0,
-                                              chunks=4).to_host())
+        lay = MG.piece_layout(S.shape[0], 1)
+        m, _ = MG.sharded_join_owned(torch.from_numpy(L[r0:r1]).to(dev),
+                                     torch.from_numpy(S).to(dev), lay, theta, r0,
+                                     ops=MG.DeviceOps(grid=132))
+        parts.append(m.to_host())
     cl, cr, cs = MG.concat_shards(parts)
     assert np.array_equal(cl, lo) and np.array_equal(cr, ro)
     assert np.array_equal(cs.view(np.uint32), so.view(np.uint32))
 
 
-def test_cfg5_output_heavy_full_size():
-    """BASELINE configs[4] at its most output-heavy threshold (8.1e7 matches:
-    the deferred recheck, row bucketing and large-row sorts)."""
+@pytest.mark.parametrize("theta", [0.8, 0.4])
+def test_cfg5_full_set_equals_reference(theta):
+    """BASELINE configs[4] (200k x 200k, 500 centroids) at theta 0.8 (4.3e7
+    matches) and 0.4 (8.1e7: deferred recheck, row bucketing, big-row sorts)."""
     from paper_2312_01476_b200 import datagen
     (L, S), c = datagen.config_vectors("cfg5")
-    theta = 0.4
-    lo, ro, so = _device_join(L, S, theta)
-    _check_canonical(lo, ro, so, theta)
-    assert len(lo) > 5e7
-    _rows_match_oracle(L, S, lo, ro, so, theta, 64, seed=2)
-    # a second run (deferred placement chosen from the first) is identical
-    lo2, ro2, so2 = _device_join(L, S, theta)
-    assert np.array_equal(lo2, lo) and np.array_equal(ro2, ro)
-    assert np.array_equal(so2.view(np.uint32), so.view(np.uint32))
+    got = _device_join(L, S, theta)
+    _check_canonical(*got, theta)
+    _assert_same(got, _reference_join(L, S, theta))
+    # a second run (placement and capacity learned from the first) is identical
+    got2 = _device_join(L, S, theta)
+    for a, b in zip(got, got2):
+        assert np.array_equal(a.view(np.uint32) if a.dtype == np.float32 else a,
+                              b.view(np.uint32) if b.dtype == np.float32 else b)
 
 
-def test_cfg4_shape_wide():
+def test_cfg3_full_set_equals_reference():
+    """BASELINE configs[2]: 200k x 200k strings -> subword embedding on the
+    GPU (bitwise the oracle's, all 400k rows) -> tensor_join; the MatchSet
+    equals the reference join of the oracle-embedded vectors."""
+    from paper_2312_01476_b200 import RawRelation, SubwordModel, datagen, tensor_join
+    from paper_2312_01476_b200 import device as D
+    dev = torch.device("cuda", 0)
+    left, right = datagen.strings(200_000, 200_000, 0.3, seed=0)
+    table = datagen.bucket_table(2_000_000, 100, seed=0)
+    tdev = torch.from_numpy(table).to(dev)
+    EL, ER = O.subword_embed(left, table), O.subword_embed(right, table)
+    gl = D.subword_rows(left, tdev, 3, 6).cpu().numpy()
+    gr = D.subword_rows(right, tdev, 3, 6).cpu().numpy()
+    assert np.array_equal(gl.view(np.uint32), EL.view(np.uint32))
+    assert np.array_equal(gr.view(np.uint32), ER.view(np.uint32))
+    theta = 0.85
+    ms, st = tensor_join(RawRelation("left", left), RawRelation("right", right),
+                         SubwordModel(tdev), theta, 64 << 20)
+    assert st.pairs_compared == 4e10
+    got = (ms.lefts, ms.rights, ms.sims)
+    _check_canonical(*got, theta)
+    _assert_same(got, _reference_join(EL, ER, theta, tokens=(left, right)))
+
+
+def test_cfg4_shard_full_set_equals_reference():
     """BASELINE configs[3]'s distribution (d = 768, 50k centroids, sigma 0.6,
-    Zipf(1.1) cluster sizes, theta = 0.75) at 20k x 400k: the wide filter and
-    the tile-group recheck."""
+    Zipf(1.1) cluster sizes, theta = 0.75): the wide filter and tile-group
+    recheck on a 16k x 1M slice, the whole set against the reference kernels."""
     from paper_2312_01476_b200 import datagen
-    (L, S), c = datagen.config_vectors("cfg4", n_left=20_000, n_right=400_000)
+    (L, S), c = datagen.config_vectors("cfg4", n_left=16_000, n_right=1_000_000)
     theta = c["theta"]
-    lo, ro, so = _device_join(L, S, theta)
-    _check_canonical(lo, ro, so, theta)
-    assert len(lo) > 1e7
-    _rows_match_oracle(L, S, lo, ro, so, theta, 48, seed=3)
+    got = _device_join(L, S, theta)
+    _check_canonical(*got, theta)
+    _assert_same(got, _refkern_join(L, S, theta))

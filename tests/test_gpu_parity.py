@@ -305,6 +305,52 @@ def test_sharded_join_streamed_single_rank(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))
 
 
+@pytest.mark.parametrize("rounds,grid", [(1, 0), (4, 132), (0, 100)])
+def test_owner_prepared_join_single_rank(cuda, manifest, golden, rounds, grid):
+    """multigpu.sharded_join_owned on one rank: S prepared piece by piece into
+    padded buffers (device.prepare_into), filtered round by round
+    (device.JoinSession) on a reduced grid (SMs left to NCCL) -- the golden
+    set, and a prepared S bitwise equal to a one-shot prepare."""
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200 import multigpu as MG
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    lay = MG.piece_layout(len(S), 1, rounds)
+    assert lay.rounds == (rounds or lay.rounds) and lay.rows >= len(S)
+    S_loc = torch.from_numpy(MG.local_pieces(S, lay, 0)).to(cuda)
+    m, PR = MG.sharded_join_owned(torch.from_numpy(L).to(cuda), S_loc, lay, meta["theta"], 0,
+                                  ops=MG.DeviceOps(grid=grid))
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, golden["cfg1_l"]) and np.array_equal(ro, golden["cfg1_r"])
+    assert np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))
+    ref = D.prepare(torch.from_numpy(S).to(cuda))
+    n = len(S)
+    assert torch.equal(PR.f32[:n], ref.f32)
+    assert torch.equal(PR.op[:ref.op.numel()].view(torch.int16), ref.op.view(torch.int16))
+    assert torch.equal(PR.row_err[:n], ref.row_err[:n])
+    assert torch.equal(PR.tile_err[:D.tile_count(n)], ref.tile_err[:D.tile_count(n)])
+
+
+def test_tensor_join_devices(cuda, manifest, golden):
+    """tensor_join(devices=[...]): left rows sharded over devices (here two
+    shards on the one GPU), S prepared once and copied; same MatchSet and
+    model-call accounting as the single-device operator."""
+    from paper_2312_01476_b200 import LookupModel, RawRelation, nlj_prefetch, tensor_join
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    toks_l = [f"L{i}" for i in range(len(L))]
+    toks_r = [f"S{i}" for i in range(len(S))]
+    model = LookupModel.from_matrix(toks_l + toks_r, np.concatenate([L, S]))
+    for op in (tensor_join, nlj_prefetch):
+        before = model.call_count
+        args = (64 << 20,) if op is tensor_join else ()
+        ms, st = op(RawRelation("left", toks_l), RawRelation("right", toks_r), model,
+                    meta["theta"], *args, devices=[cuda, cuda, cuda])
+        assert _bits_equal(ms, golden["cfg1_l"], golden["cfg1_r"], golden["cfg1_s"])
+        assert model.call_count - before == len(L) + len(S)
+        assert st.pairs_compared == len(L) * len(S) and st.matches == len(ms)
+
+
 @pytest.mark.parametrize("recheck", ["fused", "deferred"])
 def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
     """d <= 128: fused recheck warps and the deferred full-occupancy kernel
@@ -506,11 +552,18 @@ def test_empty_and_errors(cuda):
         tensor_join_vectors(np.ones((2, 3), np.float32), np.ones((2, 4), np.float32), 0.1)
 
 
-def test_subword_model_matches_oracle(cuda):
+@pytest.mark.parametrize("dim,fused", [(100, False), (100, True), (200, False), (37, False)])
+def test_subword_model_matches_oracle(cuda, monkeypatch, dim, fused):
+    """Subword embedding on the GPU, bitwise the oracle's: the vectorised
+    gather + normalise pass (dim % 4 == 0, <= 256), and the one-kernel
+    fused path (SJB_SUBWORD_FUSED, or any other dim)."""
     from paper_2312_01476_b200 import RawRelation, SubwordModel, datagen, device as D
     from paper_2312_01476_b200.embedding import embed_relation_device, prepare_relation
-    table = datagen.bucket_table(5003, 100, seed=1)
+    if fused:
+        monkeypatch.setenv("SJB_SUBWORD_FUSED", "1")
+    table = datagen.bucket_table(5003, dim, seed=1)
     left, right = datagen.strings(700, 900, seed=4)
+    left += ["", "a", "ab", "abcdefghijklmnopqrstuvwxyzabcdefghijklmnop"]   # edge lengths
     m = SubwordModel(table)
     got = embed_relation_device(m, RawRelation("l", left)).cpu().numpy()
     want = O.subword_embed(left, table)

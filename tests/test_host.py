@@ -175,3 +175,56 @@ def test_cost_params_validation_and_json():
             CostParams(**kw)
     with pytest.raises(ValueError, match="missing"):
         CostParams.from_dict({"access_ns": 1.0})
+
+
+def test_bench_launcher_spawns_ranks():
+    """bench.py --gpus 2 without a torchrun environment re-launches itself
+    under torch.distributed.run with 2 ranks; rank 0 alone prints one JSON
+    line whose n_gpus is the real world size.  (The reference arm needs no
+    GPU, so the launcher is exercised here on CPU at cfg1.)"""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "cfg1", "--steps", "1", "--warmup", "0",
+                          "--nlj-pairs", "1e7"], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["impl"] == "reference"
+    assert rec["config"]["global_batch"] == 10_000 * 10_000
+    assert rec["parity"]["matches"] == 52_884          # the golden cfg1 count
+    assert rec["steps"] * rec["ms_per_step"] / 1e3 <= rec["cpu_baseline"]["full_wall_s"] * 2
+
+
+def test_reference_package_matches_reference_kernels(manifest, golden):
+    """The two CPU references agree: the unmodified package (baseline/_ref,
+    simjoin.tensor_join) and its kernels built from source (oracle/_ref via
+    refkern) give the golden cfg1 MatchSet bit for bit."""
+    import simjoin_ref
+    import refkern
+    from conftest import case_inputs
+    sj = simjoin_ref.load()
+    if sj is None:
+        pytest.skip(simjoin_ref.error())
+    assert simjoin_ref.compiled(sj)
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    lt, rt = [f"l{i}" for i in range(len(L))], [f"r{i}" for i in range(len(S))]
+    table = dict(zip(lt, L))
+    table.update(zip(rt, S))
+    ms, st = sj.tensor_join(sj.RawRelation("a", lt), sj.RawRelation("b", rt),
+                            sj.LookupModel(table, L.shape[1]), meta["theta"], 64 << 20, threads=4)
+    want = (golden["cfg1_l"], golden["cfg1_r"], golden["cfg1_s"])
+    got = (np.asarray(ms.lefts), np.asarray(ms.rights), np.asarray(ms.sims))
+    if refkern.available():
+        lo, ro, so, _ = refkern.tensor_join_vectors(L, S, meta["theta"], threads=4)
+        got2 = (lo, ro, so)
+    else:
+        got2 = got
+    for g in (got, got2):
+        assert np.array_equal(g[0], want[0]) and np.array_equal(g[1], want[1])
+        assert np.array_equal(g[2].view(np.uint32), want[2].view(np.uint32))

@@ -78,6 +78,14 @@ int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int6
                               unsigned long long* d_repaired, float* d_row_err,
                               float* d_tile_err, void* stream);
 
+/* Operand image of rows used AS GIVEN (no normalisation): the 16-bit tiled
+ * image (sjb_operand_elems elements) of n x dim fp32 rows.  For callers that
+ * hand over rows they already normalised (the kernel-backend nlj_rows
+ * contract, _ckern.pyx:179-212; EmbeddedRelation.normalized) -- the filter
+ * band must then cover those rows' norms (sjb_default_band scaled by the
+ * largest norms; see kernels.nlj_rows). */
+int sjb_cast_rows(const float* d_in, int64_t n, int64_t dim, void* d_out16, void* stream);
+
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
 

@@ -525,6 +525,32 @@ static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n,
   const int64_t tiles = d_out16 ? sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows)
                                 : sjb::ceil_div(n, sjb::kTileRows);
   if (tiles == 0) return SJB_OK;
+  if (d_gather == nullptr && (dim & 3) == 0 && kpad <= 128 && ((uintptr_t)d_in & 15) == 0 &&
+      ((uintptr_t)d_out32 & 15) == 0 && getenv("SJB_PREP_STAGED") == nullptr) {
+    // pipelined kernel: per-warp double-buffered 32-row slabs
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const char* pb = getenv("SJB_PREP_BUFS");
+    const int nbuf = pb != nullptr && atoi(pb) == 2 ? 2 : 1;
+    const int warps = sjb::pipe_warps((int)dim, nbuf, 210 * 1024);
+    const int smem = sjb::pipe_smem_bytes((int)dim, nbuf, warps);
+    if (int rc = set_smem_attr((const void*)sjb::normalize_pipe_kernel, smem)) return rc;
+    auto st = as_stream(stream);
+    const bool errs = d_out16 != nullptr && d_row_err != nullptr;
+    if (errs && d_tile_err != nullptr) {
+      cudaError_t e = cudaMemsetAsync(d_tile_err, 0, (size_t)tiles * 4, st);
+      if (e != cudaSuccess) return fail(SJB_E_CUDA, "memset tile_err: %s", cudaGetErrorString(e));
+    }
+    const int64_t n_slabs = tiles * (sjb::kTileRows / sjb::kPipeSlab);
+    const int64_t grid = sjb::mn<int64_t>(sjb::ceil_div(n_slabs, (int64_t)warps),
+                                          (int64_t)sjb_sm_count(dev));
+    sjb::normalize_pipe_kernel<<<(unsigned)grid, warps * 32, smem, st>>>(
+        d_in, n, n_slabs, (int)dim, kpad, nbuf, d_out32, reinterpret_cast<sjb::op16_t*>(d_out16),
+        d_repaired, errs ? d_row_err : nullptr,
+        errs ? reinterpret_cast<unsigned*>(d_tile_err) : nullptr);
+    SJB_CK_LAUNCH("normalize_pipe");
+    return SJB_OK;
+  }
   const int sub = prep_sub_rows(dim);
   const int smem = sub * (int)(dim | 1) * 4;
   if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
@@ -549,6 +575,21 @@ int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int6
   if (!d_index) return fail(SJB_E_INVALID, "null index");
   return normalize_impl(d_table, d_index, n, dim, d_out32, d_out16, d_repaired, d_row_err,
                         d_tile_err, stream);
+}
+
+int sjb_cast_rows(const float* d_in, int64_t n, int64_t dim, void* d_out16, void* stream) {
+  if (n < 0 || dim < 1 || d_out16 == nullptr) return fail(SJB_E_INVALID, "bad cast arguments");
+  const int kpad = (int)sjb_kpad(dim);
+  const int64_t tiles = sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows);
+  if (tiles == 0) return SJB_OK;
+  const int sub = prep_sub_rows(dim);
+  const int smem = sub * (int)(dim | 1) * 4;
+  if (int rc = set_smem_attr((const void*)sjb::normalize_cast_kernel, smem)) return rc;
+  sjb::normalize_cast_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
+      d_in, nullptr, n, (int)dim, kpad, sub, nullptr, reinterpret_cast<sjb::op16_t*>(d_out16),
+      nullptr, 0, nullptr, nullptr);
+  SJB_CK_LAUNCH("cast_rows");
+  return SJB_OK;
 }
 
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream) {

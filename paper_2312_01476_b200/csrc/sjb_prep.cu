@@ -311,6 +311,196 @@ normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ 
   if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
+// Pipelined normalise-and-cast (dim % 4 == 0, kpad <= 128, 16 B aligned
+// input): the same bits as normalize_cast_kernel, restructured so the HBM
+// stream never waits for the row-serial arithmetic.  Each warp walks 32-row
+// slabs (grid-stride) with two shared buffers: while it computes slab k,
+// slab k + 1 is already in flight (one 1-D bulk copy per row, lane = row,
+// completing on the buffer's mbarrier).  A slab is then three passes by the
+// warp, lane = row:
+//   1. the reference's sequential fp64 sum of squares + repair
+//      (_kernelcore.c:52-70), reading the row as float4 (row pitch = an odd
+//      number of float4: conflict-free 128-bit shared loads);
+//   2. the correctly rounded quotients (quot_rn, in place), the 16-bit cast
+//      stored as the row's 16-byte chunks of the operand tile (a warp writes
+//      one 512 B run per k-group), and the row's rounding error (exact
+//      squares, fp64 sum, rounded up: the same value as the staged kernel);
+//   3. the fp32 rows copied out row-major (coalesced 400 B rows).
+// tile_err must be zeroed first: each slab folds its maximum in with an
+// atomicMax on the bits (errors are >= 0, so bit order = value order).
+constexpr int kPipeSlab = 32;
+constexpr int kPipeMaxWarps = 16;
+
+__host__ __device__ inline int pipe_pitch4(int dim) { return (dim / 4) | 1; }
+
+// bufs = 1: each warp loads its next slab after finishing the current one
+// (16 warps per SM hide the latency); 2: double-buffered (8 warps)
+__host__ inline int pipe_warps(int dim, int bufs, int smem_budget) {
+  const int per_warp = bufs * kPipeSlab * pipe_pitch4(dim) * 16 + 16;
+  return mn(kPipeMaxWarps, smem_budget / per_warp);
+}
+
+__host__ __device__ inline int pipe_smem_bytes(int dim, int bufs, int warps) {
+  return warps * (bufs * kPipeSlab * pipe_pitch4(dim) * 16 + 16);
+}
+
+__global__ void __launch_bounds__(kPipeMaxWarps * 32, 1)
+normalize_pipe_kernel(const float* __restrict__ in, int64_t n, int64_t n_slabs, int dim, int kpad,
+                      int nbuf, float* out32, op16_t* __restrict__ out16,
+                      unsigned long long* __restrict__ repaired, float* __restrict__ row_err,
+                      unsigned* __restrict__ tile_err_bits) {
+  extern __shared__ __align__(1024) uint8_t pipe_smem[];
+  uint8_t* smem = pipe_smem;
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p4 = pipe_pitch4(dim), q4 = dim >> 2;
+  float4* bufs = reinterpret_cast<float4*>(smem) + (size_t)warp * nbuf * kPipeSlab * p4;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + (size_t)warps * nbuf * kPipeSlab * p4 * 16) + warp * 2;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const uint64_t pol = policy_evict_first();
+  const bool bf = op_is_bf16(kpad);
+  const int64_t nw = (int64_t)gridDim.x * warps;
+
+  auto slab_rows = [&](int64_t slab) -> int {
+    return (int)mx<int64_t>(0, mn<int64_t>(kPipeSlab, n - slab * kPipeSlab));
+  };
+  auto issue = [&](int64_t slab, int b) {
+    const int rows = slab_rows(slab);
+    if (rows == 0) return;  // padding slab: nothing to load, no barrier phase
+    if (lane == 0) mbar_arrive_expect_tx(&bars[b], (uint32_t)(rows * dim * 4));
+    __syncwarp();
+    if (lane < rows)
+      bulk_g2s(bufs + (size_t)b * kPipeSlab * p4 + lane * p4,
+               in + (slab * kPipeSlab + lane) * (int64_t)dim, (uint32_t)(dim * 4), &bars[b], pol);
+  };
+
+  uint32_t ph0 = 0, ph1 = 0;
+  int b = 0;
+  int64_t slab = (int64_t)blockIdx.x * warps + warp;
+  if (slab < n_slabs && nbuf == 2) issue(slab, 0);
+  for (; slab < n_slabs; slab += nw, b ^= (nbuf - 1)) {
+    if (nbuf == 2) {
+      if (slab + nw < n_slabs) issue(slab + nw, b ^ 1);
+    } else {
+      issue(slab, 0);
+    }
+    const int rows = slab_rows(slab);
+    if (rows > 0) {
+      if (b == 0) {
+        mbar_wait(&bars[0], ph0);
+        ph0 ^= 1u;
+      } else {
+        mbar_wait(&bars[1], ph1);
+        ph1 ^= 1u;
+      }
+    }
+    const int64_t r0 = slab * kPipeSlab;
+    float4* buf = bufs + (size_t)b * kPipeSlab * p4;
+    float4* row = buf + lane * p4;
+    const bool valid = lane < rows;
+    // ---- 1. sequential fp64 sum of squares, repair ----------------------
+    int rep = 0;
+    double norm = 1.0, y = 1.0;
+    bool hoist = true;
+    if (valid) {
+      double ss = 0.0;
+      for (int q = 0; q < q4; q++) {
+        const float4 v = row[q];
+        ss = __fma_rn((double)v.x, (double)v.x, ss);
+        ss = __fma_rn((double)v.y, (double)v.y, ss);
+        ss = __fma_rn((double)v.z, (double)v.z, ss);
+        ss = __fma_rn((double)v.w, (double)v.w, ss);
+      }
+      norm = sqrt(ss);
+      if (norm < 1e-12) {
+        float4 v0 = row[0];
+        v0.x = 1.0f;
+        row[0] = v0;
+        ss = 0.0;
+        for (int q = 0; q < q4; q++) {
+          const float4 v = row[q];
+          ss = __fma_rn((double)v.x, (double)v.x, ss);
+          ss = __fma_rn((double)v.y, (double)v.y, ss);
+          ss = __fma_rn((double)v.z, (double)v.z, ss);
+          ss = __fma_rn((double)v.w, (double)v.w, ss);
+        }
+        norm = sqrt(ss);
+        rep = 1;
+      }
+      hoist = isfinite(norm);
+      y = __drcp_rn(norm);
+    }
+    // ---- 2. quotients (in place), operand chunks, rounding error --------
+    float es = 0.0f;
+    const int64_t tile = r0 / kTileRows;
+    const int rin = (int)(r0 - tile * kTileRows) + lane;
+    uint4* dst16 = out16 != nullptr
+                       ? reinterpret_cast<uint4*>(out16 + tile * (int64_t)kTileRows * kpad)
+                       : nullptr;
+    for (int g = 0; g < kpad / 8; g++) {
+      __align__(16) float x[8];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int q = 2 * g + h;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && q < q4) {
+          v = row[q];
+          v.x = __double2float_rn(quot_rn((double)v.x, norm, y, hoist));
+          v.y = __double2float_rn(quot_rn((double)v.y, norm, y, hoist));
+          v.z = __double2float_rn(quot_rn((double)v.z, norm, y, hoist));
+          v.w = __double2float_rn(quot_rn((double)v.w, norm, y, hoist));
+          row[q] = v;
+        }
+        x[4 * h + 0] = v.x;
+        x[4 * h + 1] = v.y;
+        x[4 * h + 2] = v.z;
+        x[4 * h + 3] = v.w;
+      }
+      if (dst16 != nullptr) {
+        __align__(16) op16_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          o[e] = to_op16(x[e], bf);
+          if (row_err != nullptr) {
+            // op(x) - x is exact in fp32; the squares are summed in fp32
+            // rounding UP, so es bounds the exact sum from above
+            const float d = __fsub_rn(from_op16(o[e], bf), x[e]);
+            es = __fmaf_ru(d, d, es);
+          }
+        }
+        dst16[g * kTileRows + rin] = *reinterpret_cast<const uint4*>(o);
+      }
+    }
+    __syncwarp();
+    // ---- 3. fp32 rows out, errors, counters -----------------------------
+    if (out32 != nullptr) {
+      float4* o4 = reinterpret_cast<float4*>(out32 + r0 * (int64_t)dim);
+      for (int r = 0; r < rows; r++)
+        for (int q = lane; q < q4; q += 32) o4[r * q4 + q] = buf[r * p4 + q];
+    }
+    if (row_err != nullptr && dst16 != nullptr && rows > 0) {
+      float e = 0.0f;
+      if (valid) {
+        e = __fmul_ru(__fsqrt_ru(es), 1.0f + 1e-6f);
+        row_err[r0 + lane] = e;
+      }
+      const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(e));
+      if (lane == 0 && tile_err_bits != nullptr) atomicMax(tile_err_bits + tile, m);
+    }
+    if (repaired != nullptr) {
+      rep = __reduce_add_sync(0xffffffffu, rep);
+      if (lane == 0 && rep) atomicAdd(repaired, (unsigned long long)rep);
+    }
+    __syncwarp();
+  }
+}
+
 // Synthetic model (_kernelcore.c:69-74, 99-107): stream seed per row, element
 // d = splitmix64 output d+1 mapped to fp64 [-1,1), truncated to fp32, then the
 // row is normalised.  Element-parallel generation, row-serial normalisation.

@@ -187,6 +187,49 @@ def prepare_pieces(raw: torch.Tensor, pieces, name: str = ""):
     return PreparedRelation(f32, op, n, dim, name, rep, re, te), ready
 
 
+def cast_prepared(rows: torch.Tensor, name: str = "") -> PreparedRelation:
+    """Rows used AS GIVEN (already normalised by the caller): the fp32 rows
+    are the caller's tensor and the operand image is their 16-bit cast
+    (sjb_cast_rows).  No rounding errors are recorded, so joins of such a
+    relation filter with a uniform band -- which must cover the rows' norms
+    (band_for_rows)."""
+    _check_matrix(rows, "relation")
+    n, dim = rows.shape
+    dev = rows.device
+    op = op_empty(n, dim, dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().sjb_cast_rows(_vp(rows), n, dim, _vp(op), _stream(dev)),
+                   "sjb_cast_rows")
+    return PreparedRelation(rows, op, n, dim, name, None, None, None)
+
+
+def max_row_norm(rows: torch.Tensor) -> float:
+    """Largest row norm (fp64 sums, sjb_row_norms), rounded up slightly."""
+    n, dim = rows.shape
+    if n == 0:
+        return 0.0
+    out = torch.empty(n, dtype=torch.float32, device=rows.device)
+    with torch.cuda.device(rows.device):
+        _lib.check(_lib.lib().sjb_row_norms(_vp(rows), n, dim, _vp(out), _stream(rows.device)),
+                   "sjb_row_norms")
+    m = float(out.max().item())
+    return m * (1 + 1e-6) if np.isfinite(m) else float("inf")
+
+
+def band_for_rows(dim: int, max_norm_left: float, max_norm_right: float) -> float:
+    """Filter band for rows of norm <= M (not necessarily unit): each
+    operand error grows at most like the norm (||op(x) - x|| <= M e when
+    M >= 1), so |approx - exact| <= M_L M_R (2e + e^2) and the fp32
+    accumulation slack scales with ||op(x)|| ||op(y)|| <= M_L M_R (1 + e)^2:
+    the unit-row band (sjb_default_band) times max(1, M_L) max(1, M_R) and
+    1.01 (covers the (1 + e)^2 factor).  Non-finite norms give an infinite
+    band: every pair is rechecked canonically."""
+    ml, mr = max(1.0, max_norm_left), max(1.0, max_norm_right)
+    if not (np.isfinite(ml) and np.isfinite(mr)):
+        return float("inf")
+    return default_band(dim) * ml * mr * 1.01
+
+
 def normalize_rows_(m: torch.Tensor) -> torch.Tensor:
     """In-place fp32 row normalisation; returns the (1,) int64 repaired count."""
     _check_matrix(m, "matrix")
@@ -239,23 +282,31 @@ def _recheck_mode(key: tuple, pairs: int) -> int:
         seen = _cap_cache.get(key, 0)
     return 1 if pairs > 0 and seen > DENSE_FRACTION * pairs else 0
 
-# workspace is cached per device and grown on demand
-_ws_cache: Dict[int, torch.Tensor] = {}
+# workspace is cached per (device, host thread) and grown on demand: joins
+# issued concurrently from several host threads (the reference runs kernel
+# backends from `threads` workers, join.py:121-142) must not share counters
+_ws_cache: Dict[tuple, torch.Tensor] = {}
+
+
+def _ws_key(dev: torch.device) -> tuple:
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    return idx, threading.get_ident()
 
 
 def _workspace(nbytes: int, dev: torch.device) -> torch.Tensor:
-    idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    ws = _ws_cache.get(idx)
+    key = _ws_key(dev)
+    with _cap_lock:
+        ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
-        _ws_cache.pop(idx, None)
         ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
-        _ws_cache[idx] = ws
+        with _cap_lock:
+            _ws_cache[key] = ws
     return ws
 
 
 def _ws_bytes_cached(dev: torch.device) -> int:
-    idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    ws = _ws_cache.get(idx)
+    with _cap_lock:
+        ws = _ws_cache.get(_ws_key(dev))
     return 0 if ws is None else ws.numel()
 
 

@@ -448,15 +448,20 @@ def join_embedded(left: EmbeddedRelation, right: EmbeddedRelation, theta, *,
     t = Threshold.of(theta)
     dev = _device(device)
     with torch.cuda.device(dev):
-        preps = []
+        preps, norms = [], []
         for er in (left, right):
             x = torch.from_numpy(np.ascontiguousarray(er.data)).to(dev)
             if er.normalized:
-                p = D.prepare(x)          # re-normalising unit rows changes bits,
-                p.f32.copy_(x)            # so keep the caller's canonical rows;
-                p.row_err = p.tile_err = None  # errors were measured on the others
-                preps.append(p)
+                # re-normalising changes bits: the caller's rows are used as
+                # given, cast for the filter, with a band that covers their norms
+                preps.append(D.cast_prepared(x))
+                norms.append(D.max_row_norm(x))
             else:
                 preps.append(D.prepare(x))
+                norms.append(1.0)
+        if band is None and (left.normalized or right.normalized):
+            band = D.band_for_rows(left.dim, *norms)
+            if not np.isfinite(band):
+                band = 4.0 * max(1.0, abs(float(t.value))) + 1e30
         m = D.join_prepared(preps[0], preps[1], t.value, band)
         return _to_matchset(m, left.source_name, right.source_name)

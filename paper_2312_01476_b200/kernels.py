@@ -169,13 +169,17 @@ def nlj_rows(left: np.ndarray, i0: int, i1: int, right: np.ndarray, theta: float
     ns = right.shape[0]
     if ns == 0 or i0 >= i1:
         return []
-    dev = _dev()
     tl = _h2d(np.ascontiguousarray(left[i0:i1], dtype=np.float32))
     tr = _h2d(np.ascontiguousarray(right, dtype=np.float32))
-    pl, pr = D.prepare(tl), D.prepare(tr)
-    pl.f32.copy_(tl)                      # rows are already canonical (normalised)
-    pr.f32.copy_(tr)
-    m = D.join_prepared(pl, pr, float(theta), left_base=i0)
+    # the rows are used as given (the contract passes normalised rows, but
+    # any rows are accepted): the operand image is their own cast and the
+    # band covers their norms, so the canonical recheck sees every pair
+    # whose raw dot can reach theta
+    pl, pr = D.cast_prepared(tl), D.cast_prepared(tr)
+    b = D.band_for_rows(left.shape[1], D.max_row_norm(tl), D.max_row_norm(tr))
+    if not np.isfinite(b):
+        b = 4.0 * max(1.0, abs(float(theta))) + 1e30      # cutoff below every finite dot
+    m = D.join_prepared(pl, pr, float(theta), band=b, left_base=i0)
     if m.n_matches == 0:
         return []
     return [m.to_host()]

@@ -38,9 +38,15 @@ def _decode_operand(op: torch.Tensor, n: int, dim: int) -> np.ndarray:
     return t[:n], t
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("dim", [1, 3, 4, 16, 100, 128, 200, 768])
-def test_normalize_and_operand_image(cuda, dim):
+def test_normalize_and_operand_image(cuda, monkeypatch, dim, staged):
+    """Bitwise sj_normalize_rows + the tiled operand image, through the
+    pipelined kernel (dim % 4 == 0, kpad <= 128, aligned rows) and the staged
+    one (every other case; SJB_PREP_STAGED forces it)."""
     from paper_2312_01476_b200 import device as D
+    if staged:
+        monkeypatch.setenv("SJB_PREP_STAGED", "1")
     rng = np.random.default_rng(dim)
     n = 300
     x = rng.standard_normal((n, dim), dtype=np.float32) * rng.uniform(0.01, 10, (n, 1)).astype(np.float32)
@@ -191,11 +197,14 @@ def test_wide_overflow_retry_and_all_pairs(cuda, manifest, golden):
     assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("dim", [3, 100, 768])
-def test_rounding_error_outputs(cuda, dim):
+def test_rounding_error_outputs(cuda, dim, monkeypatch, staged):
     """row_err bounds ||op16(x) - x|| from above (tightly); tile_err is the
     per-256-row-tile maximum (zero for padding tiles)."""
     from paper_2312_01476_b200 import device as D
+    if staged:
+        monkeypatch.setenv("SJB_PREP_STAGED", "1")
     rng = np.random.default_rng(dim + 5)
     n = 700
     x = rng.standard_normal((n, dim), dtype=np.float32)
@@ -205,7 +214,7 @@ def test_rounding_error_outputs(cuda, dim):
     bf = torch.from_numpy(f).to(_op_dtype(dim)).to(torch.float64).numpy()
     want = np.sqrt(((bf - f.astype(np.float64)) ** 2).sum(axis=1))
     got = p.row_err.cpu().numpy().astype(np.float64)[:n]
-    assert (got >= want).all() and (got <= want * (1 + 1e-6) + 1e-30).all()
+    assert (got >= want).all() and (got <= want * (1 + 1e-4) + 1e-30).all()
     tiles = p.tile_err.cpu().numpy()
     assert len(tiles) == D.tile_count(n)
     for t in range(len(tiles)):

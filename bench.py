@@ -1,7 +1,7 @@
 """Benchmark of the hot path: the cosine-threshold tensor join.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg3|cfg5] [--theta T]
+                    [--config cfg1|cfg2|cfg3|cfg4|cfg5] [--theta T] [--sims exact|tensor]
 
 Default workload: BASELINE.json configs[1] (cfg2, fits one B200): |R| =
 100,000 x |S| = 1,000,000, d = 100, clustered generator (10,000 centroids,
@@ -60,6 +60,10 @@ WORKLOADS = {
                  sigma=0.5, theta=0.8, seed=0),
     "cfg3": dict(kind="strings", n_left=200_000, n_right=200_000, dim=100,
                  n_buckets=2_000_000, shared=0.3, theta=0.85, seed=0),
+    # d = 768 bf16, R sharded over 8 GPUs: each rank joins 1/8 of R against all
+    # of S; with fewer ranks the first N eighths run (per-GPU work fixed)
+    "cfg4": dict(kind="wide", n_left=1_000_000, n_right=4_000_000, dim=768, n_centroids=50_000,
+                 sigma=0.6, zipf=1.1, theta=0.75, seed=0, share=8),
 }
 
 
@@ -72,6 +76,13 @@ def workload(args) -> dict:
         c["desc"] = (f"{args.config}: |R|={c['n_left']:,} x |S|={c['n_right']:,}, d={c['dim']}, "
                      f"theta={c['theta']}, clustered ({c['n_centroids']:,} centroids, sigma "
                      f"{c['sigma']}), seed {c['seed']}")
+    elif c["kind"] == "wide":
+        c["sims"] = args.sims
+        c["desc"] = (f"{args.config}: |R|={c['n_left']:,} x |S|={c['n_right']:,}, d={c['dim']} "
+                     f"bf16, theta={c['theta']}, clustered ({c['n_centroids']:,} centroids, "
+                     f"sigma {c['sigma']}, Zipf({c['zipf']}) sizes), seed {c['seed']}; R in "
+                     f"{c['share']} shares, one per rank (this run: the first N shares); raw bf16 "
+                     f"operands, sims={args.sims}")
     else:
         c["desc"] = (f"{args.config}: {c['n_left']:,} x {c['n_right']:,} strings a-z len 3-12, "
                      f"{int(c['shared'] * 100)}% shared with 1-2 edits; subword model "
@@ -82,8 +93,18 @@ def workload(args) -> dict:
 
 def make_vectors(c):
     from paper_2312_01476_b200 import datagen
-    return datagen.clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"],
-                                  c["sigma"], c["seed"])
+    L, S = datagen.clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"],
+                                  c["sigma"], c["seed"], zipf=c.get("zipf"))
+    if c["kind"] == "wide":                     # cfg4 relations are bf16
+        L, S = datagen.round_bf16(L), datagen.round_bf16(S)
+    return L, S
+
+
+def bf16_tensor(x: np.ndarray):
+    """A bf16-exact fp32 array as a (host) torch bfloat16 tensor."""
+    import torch
+    from paper_2312_01476_b200 import datagen
+    return torch.from_numpy(datagen.bf16_bits(x).view(np.int16)).view(torch.bfloat16)
 
 
 def make_strings(c):
@@ -97,17 +118,19 @@ def host_table(c) -> np.ndarray:
     return datagen.bucket_table(c["n_buckets"], c["dim"], seed=c["seed"])
 
 
-def set_digest(lo, ro, so) -> str:
+def set_digest(lo, ro, so, sims: bool = True) -> str:
     """Order-independent exact checksum of a match set: sum mod 2^64 of a
     mixed 64-bit hash of (left, right, sim bits).  Rank-local sums add up
     to the whole job's, so both arms (and any rank count) print the same
-    digest for the same MatchSet."""
+    digest for the same MatchSet.  sims=False: of the pairs only."""
     total = np.uint64(0)
     with np.errstate(over="ignore"):
         for s in range(0, len(lo), 1 << 24):
             l = np.asarray(lo[s:s + (1 << 24)], dtype=np.uint64)
             r = np.asarray(ro[s:s + (1 << 24)], dtype=np.uint64)
             b = np.asarray(so[s:s + (1 << 24)], dtype=np.float32).view(np.uint32).astype(np.uint64)
+            if not sims:
+                b = np.zeros_like(b)
             x = (l * np.uint64(0x9E3779B97F4A7C15)) ^ \
                 ((r + np.uint64(0x632BE59BD9B4E019)) * np.uint64(0xC2B2AE3D27D4EB4F)) ^ \
                 (b * np.uint64(0x165667B19E3779F9))
@@ -232,16 +255,25 @@ def cpu_reference_sample(L, S, theta, budget_s, threads, n_left_full):
         "sample_seconds": round(t_rows, 3), "sample_rows": rows}, (lo, ro, so)
 
 
-def sample_parity(ref_cols, ours, rows):
-    """Bitwise comparison of the reference sample (left rows < rows) with the
-    same rows of our full result."""
+def sample_parity(ref_cols, ours, rows, left_base=0, sims_tol=False):
+    """Comparison of the reference sample (left rows < rows of this rank's
+    share) with the same rows of our full result: bitwise, or (sims_tol:
+    tensor similarities) the same pair set and the largest |sim| gap."""
     lo, ro, so = ours
-    k = int(np.searchsorted(lo, np.uint64(rows), side="left"))
+    k = int(np.searchsorted(lo, np.uint64(left_base + rows), side="left"))
     rl, rr, rs = ref_cols
-    eq = (len(rl) == k and np.array_equal(rl, lo[:k]) and np.array_equal(rr, ro[:k])
-          and np.array_equal(rs.view(np.uint32), so[:k].view(np.uint32)))
-    return {"sample_rows": rows, "reference_matches": int(len(rl)), "ours_matches": k,
-            "bitwise_equal": bool(eq)}
+    rl = rl + np.uint64(left_base)
+    same_pairs = len(rl) == k and np.array_equal(rl, lo[:k]) and np.array_equal(rr, ro[:k])
+    out = {"sample_rows": rows, "reference_matches": int(len(rl)), "ours_matches": k}
+    if sims_tol:
+        gap = float(np.abs(rs.astype(np.float64) - so[:k].astype(np.float64)).max()) \
+            if same_pairs and k else None
+        out.update({"pair_set_equal": bool(same_pairs), "max_sim_gap": gap,
+                    "within_1e-5": bool(same_pairs and (gap is None or gap <= 1e-5))})
+    else:
+        out["bitwise_equal"] = bool(same_pairs and np.array_equal(rs.view(np.uint32),
+                                                                  so[:k].view(np.uint32)))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -262,6 +294,37 @@ def run_reference(args):
         return
     steps = max(1, min(args.steps, args.ref_steps))
     warmup = min(args.warmup, args.ref_warmup)
+    if c["kind"] == "wide":
+        # a full cfg4 share is ~5e11 pairs at d = 768 (hours on the CPU):
+        # every step times the reference kernels on a bounded row sample of
+        # the rank-0 share against all of S
+        L, S = make_vectors(c)
+        share = max(world, c["share"])
+        r0, r1 = 0, c["n_left"] // share
+        rows_total = r1 * world
+        vals, info, cols = [], None, None
+        for i in range(warmup + steps):
+            v, info, cols = cpu_reference_sample(L[r0:r1], S, c["theta"], args.ref_step_seconds,
+                                                 thr, r1 - r0)
+            if i >= warmup:
+                vals.append(v)
+        value = float(statistics.median(vals))
+        pairs = rows_total * c["n_right"]
+        lo, ro, so = cols
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": steps, "warmup": warmup, "steps_requested": args.steps,
+                "warmup_requested": args.warmup, "ms_per_step": 1e3 * pairs / value,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "fp32", "data": "synthetic (seeded)", "impl": "reference",
+                "config": {"workload": c["desc"], "global_batch": pairs},
+                "cpu_baseline": dict(info, value=value, unit=UNIT),
+                "parity": {"sample_matches": int(len(lo)),
+                           "digest": set_digest(lo, ro, so),
+                           "pairs_digest": set_digest(lo, ro, so, sims=False)},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     if c["kind"] == "vectors":
         L, S = make_vectors(c)
         ltok = [f"l{i}" for i in range(len(L))]
@@ -329,7 +392,8 @@ def run_reference(args):
                              "wall_s": nlj_wall, "sample": f"first {m_rows} left tuples x all "
                                                           f"{len(rtok):,} right",
                              "matches": int(nst.matches)},
-            "parity": {"matches": int(len(lo)), "digest": set_digest(lo, ro, so)},
+            "parity": {"matches": int(len(lo)), "digest": set_digest(lo, ro, so),
+                       "pairs_digest": set_digest(lo, ro, so, sims=False)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -381,12 +445,35 @@ def run_ours(args):
     for e in ev:
         e.record()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # 256 MiB > 126 MB L2
-    r0, r1 = MG.shard_range(c["n_left"], rank, world)
+    if c["kind"] == "wide":
+        # rank r joins share r of `share` R shares (strong within the share
+        # count, i.e. per-GPU work fixed as N grows up to `share`)
+        share = max(world, c["share"])
+        r0, r1 = MG.shard_range(c["n_left"], rank, share)
+        rows_total = sum(MG.shard_range(c["n_left"], k, share)[1] -
+                         MG.shard_range(c["n_left"], k, share)[0] for k in range(world))
+    else:
+        r0, r1 = MG.shard_range(c["n_left"], rank, world)
+        rows_total = c["n_left"]
     n_shard, n_right = r1 - r0, c["n_right"]
-    pairs_total = c["n_left"] * n_right
+    pairs_total = rows_total * n_right
     PR_last = {}
 
-    if c["kind"] == "vectors":
+    if c["kind"] == "wide":
+        L, S = make_vectors(c)
+        R_dev = bf16_tensor(L[r0:r1]).to(dev)
+        if world == 1:
+            S_bf = bf16_tensor(S).to(dev)
+        else:
+            lay = MG.piece_layout(n_right, world)
+            S_loc = bf16_tensor(MG.local_pieces(S, lay, rank)).to(dev)
+
+        def step(events=None):
+            Sx = S_bf if world == 1 else MG.gather_right_raw(S_loc, lay)
+            PR_last["p"] = pr = D.prepare_bf16(Sx)
+            return D.join_prepared(D.prepare_bf16(R_dev), pr, theta, left_base=r0,
+                                   filter_events=events, sims=args.sims)
+    elif c["kind"] == "vectors":
         L, S = make_vectors(c)
         R_dev = torch.from_numpy(L[r0:r1]).to(dev)
         if world == 1:
@@ -454,23 +541,28 @@ def run_ours(args):
     n_cand = int(sum_over_ranks(m.n_candidates))
     ours_cols = m.to_host()
     digest_part = int(set_digest(*ours_cols), 16)
+    pairs_part = int(set_digest(*ours_cols, sims=False), 16)
 
     # combine the rank-local digests (sum mod 2^64) without moving match data
     if world > 1:
         parts = [None] * world
-        dist.all_gather_object(parts, digest_part)
-        digest = f"{sum(parts) % (1 << 64):016x}"
+        dist.all_gather_object(parts, (digest_part, pairs_part))
+        digest = f"{sum(p[0] for p in parts) % (1 << 64):016x}"
+        pairs_digest = f"{sum(p[1] for p in parts) % (1 << 64):016x}"
     else:
-        digest = f"{digest_part:016x}"
+        digest, pairs_digest = f"{digest_part:016x}", f"{pairs_part:016x}"
 
     # ---- filter kernel alone (N > 1: the steps filter round by round) ------
     def filter_only_ms():
-        if c["kind"] == "vectors":
+        if c["kind"] == "wide":
+            pl, pr = D.prepare_bf16(R_dev), PR_last["p"]
+        elif c["kind"] == "vectors":
             pl = D.prepare(R_dev)
             pr = PR_last["p"] if world > 1 else D.prepare(S_dev)
         else:
             pl, pr = embed(Lb, Lo, n_shard), embed(Sb, So, n_right)
-        D.join_prepared(pl, pr, theta, left_base=r0, filter_events=(ev[2], ev[3]))
+        D.join_prepared(pl, pr, theta, left_base=r0, filter_events=(ev[2], ev[3]),
+                        sims=args.sims if c["kind"] == "wide" else "exact")
         torch.cuda.synchronize()
         return ev[2].elapsed_time(ev[3])
 
@@ -481,7 +573,24 @@ def run_ours(args):
     from paper_2312_01476_b200.join import tensor_join, tensor_join_vectors
     from paper_2312_01476_b200.core import RawRelation
     e2e_extra = {}
-    if c["kind"] == "vectors":
+    if c["kind"] == "wide":
+        L_pin = bf16_tensor(L[r0:r1]).pin_memory()
+        if world == 1:
+            S_pin = bf16_tensor(S).pin_memory()
+        else:
+            S_pin = bf16_tensor(MG.local_pieces(S, lay, rank)).pin_memory()
+        h2d = L_pin.numel() * 2 + S_pin.numel() * 2
+
+        def e2e_step():
+            if world == 1:
+                ms, _ = tensor_join_vectors(L_pin, S_pin, theta, device=dev, sims=args.sims)
+                return len(ms)
+            Rd = L_pin.to(dev, non_blocking=True)
+            Sd = MG.gather_right_raw(S_pin.to(dev, non_blocking=True), lay)
+            mm = D.join_prepared(D.prepare_bf16(Rd), D.prepare_bf16(Sd), theta, left_base=r0,
+                                 sims=args.sims)
+            return len(mm.to_host()[0])
+    elif c["kind"] == "vectors":
         L_pin = torch.from_numpy(L[r0:r1]).pin_memory()
         if world == 1:
             S_pin = torch.from_numpy(S).pin_memory()
@@ -569,8 +678,8 @@ def run_ours(args):
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            if c["kind"] == "vectors":
-                Lc, Sc = L, S
+            if c["kind"] in ("vectors", "wide"):
+                Lc, Sc = L[r0:r1], S
                 emb = None
             else:
                 sys.path.insert(0, os.path.join(HERE, "oracle"))
@@ -586,16 +695,17 @@ def run_ours(args):
                        "what": "oracle/sj_oracle.c subword embedding of both relations "
                                f"(left {t_l:.2f} s)"}
             v, info, ref_cols = cpu_reference_sample(Lc, Sc, theta, args.cpu_seconds,
-                                                     host_threads(), c["n_left"])
+                                                     host_threads(), len(Lc))
             cpu = dict(info, value=v, unit=UNIT)
             if emb:
                 cpu["embedding"] = emb
-            parity = sample_parity(ref_cols, ours_cols, info["sample_rows"])
+            parity = sample_parity(ref_cols, ours_cols, info["sample_rows"], left_base=r0,
+                                   sims_tol=c["kind"] == "wide" and args.sims == "tensor")
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "error": f"{type(exc).__name__}: {exc}"}
     if parity is None:
         parity = {}
-    parity.update({"matches": n_matches, "digest": digest})
+    parity.update({"matches": n_matches, "digest": digest, "pairs_digest": pairs_digest})
 
     if rank == 0:
         line = {
@@ -663,12 +773,17 @@ def main():
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
                     help="cfg1 is the reference's own CPU-sized case (parity, launch tests)")
     ap.add_argument("--theta", type=float, default=None)
+    ap.add_argument("--sims", choices=["exact", "tensor"], default="exact",
+                    help="cfg4: canonical similarities (bitwise) or the epilogue's "
+                         "(within 1e-5; pair set exact)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-steps", type=int, default=2,
                     help="reference arm: full joins timed (each is a whole 1e11-pair join)")
     ap.add_argument("--ref-warmup", type=int, default=1)
+    ap.add_argument("--ref-step-seconds", type=float, default=20.0,
+                    help="reference arm, cfg4: CPU seconds per sampled step")
     ap.add_argument("--nlj-pairs", type=float, default=2e9,
                     help="reference arm: pairs in the one nlj_prefetch sample")
     args = ap.parse_args()

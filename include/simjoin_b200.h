@@ -41,10 +41,10 @@ int sjb_sm_count(int device);
  * threads); lets callers count the GPU launches inside a timed region. */
 int64_t sjb_launch_count(void);
 
-/* Padded reduction depth of the fp16 operand image for `dim`: a multiple of
+/* Padded reduction depth of the 16-bit operand image for `dim`: a multiple of
  * 16 for dim <= 128, of 64 above (K-streaming kernel). */
 int64_t sjb_kpad(int64_t dim);
-/* Elements of the fp16 operand image of an n-row relation: n rounded up to a
+/* Elements of the 16-bit operand image (bf16 for kpad <= 128, fp16 above) of an n-row relation: n rounded up to a
  * multiple of 512 rows, times kpad.  Layout: 256-row tiles, each
  * [k-group (kpad/8)][row (256)][8 elements] (UMMA K-major, no swizzle). */
 int64_t sjb_operand_elems(int64_t n, int64_t dim);
@@ -61,10 +61,11 @@ int64_t sjb_tile_count(int64_t n);
 /* ---- prefetch stage: embedding + normalise-and-cast -------------------- */
 
 /* Row L2 normalisation, bitwise equal to sj_normalize_rows
- * (_kernelcore.h:8, _kernelcore.c:79-114): fp64 sequential sum of squares,
+ * (_kernelcore.h:8, _kernelcore.c:52-87): fp64 sequential sum of squares,
  * zero rows repaired (component 0 := 1), fp64 divide, fp32 store.
  * d_in may equal d_out32 (in place).  d_out16 (optional, may be NULL) gets the
- * fp16 operand image (sjb_operand_elems elements).  *d_repaired (optional
+ * 16-bit operand image (sjb_operand_elems elements; bf16 for kpad <= 128, fp16
+ * above).  *d_repaired (optional
  * device u64) is incremented by the number of repaired rows. */
 int sjb_normalize_rows(const float* d_in, int64_t n, int64_t dim, float* d_out32,
                        void* d_out16, unsigned long long* d_repaired, float* d_row_err,
@@ -86,6 +87,21 @@ int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int6
  * largest norms; see kernels.nlj_rows). */
 int sjb_cast_rows(const float* d_in, int64_t n, int64_t dim, void* d_out16, void* stream);
 
+/* bf16 relation prep for the raw-operand wide filter (dim > 128): d_in is
+ * n x dim bf16 (row-major).  d_out32 = canonical normalised fp32 rows
+ * (bitwise sj_normalize_rows of the rows' exact fp32 values); d_out16 = the
+ * RAW bf16 rows in the tiled operand layout (sjb_operand_elems elements; a
+ * repaired row has component 0 = 1 like the reference's); d_inv_norm
+ * (sjb_operand_elems / kpad floats: rows padded to 512, 0 past n) =
+ * RN(1 / ||x_i||). */
+int sjb_prepare_bf16(const void* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
+                     float* d_inv_norm, unsigned long long* d_repaired, void* stream);
+
+/* Filter band of the raw-operand mode: the bf16 products are exact, so
+ * |approx - canonical| is fp32 accumulation (both sums) plus the inverse
+ * norms' and the epilogue products' roundings: 4 dim 2^-24 + 8 2^-24 + 2e-6. */
+float sjb_raw_band(int64_t dim);
+
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
 
@@ -104,7 +120,7 @@ int sjb_synthetic_fill_many(const uint64_t* d_seeds, int64_t n, int64_t dim, flo
 /* FastText-style subword model (cfg3; no reference counterpart, see
  * DESIGN.md): row = mean of table rows of the word hash and every
  * minn..maxn-gram of '<'w'>' (fnv1a64 mod n_buckets).  normalize != 0 also
- * applies sjb_normalize_rows and writes the fp16 image (d_out16 optional). */
+ * applies sjb_normalize_rows and writes the 16-bit operand image (d_out16 optional). */
 int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
                       const float* d_table, int64_t n_buckets, int64_t dim, int minn,
                       int maxn, int normalize, float* d_out32, void* d_out16,
@@ -137,6 +153,18 @@ typedef struct sjb_join_args {
    * 1 = deferred to a full-occupancy kernel after the filter (best when
    * candidates are dense, e.g. > 2e-4 of the pairs).  Same result. */
   int32_t recheck;
+  /* Raw-operand mode (bf16 relations, sjb_prepare_bf16; dim > 128): both
+   * relations' RN(1/||x||) from the prep; the operand images then hold the
+   * raw bf16 rows and the filter normalises after the GEMM.  Use
+   * band = sjb_raw_band(dim).  NULL: normalised operands (default). */
+  const float* left_inv_norm;
+  const float* right_inv_norm;
+  /* Similarity values (raw-operand mode only): 0 = canonical (every
+   * candidate rechecked, bitwise sj_dot_seq; default), 1 = tensor: pairs
+   * with approx >= theta + band are emitted with the epilogue similarity
+   * (|approx - canonical| < band, measured ~1e-6), only pairs within the
+   * band are rechecked canonically.  The pair SET is exact either way. */
+  int32_t sims_mode;
 } sjb_join_args;
 
 typedef struct sjb_join_info {
@@ -158,7 +186,7 @@ float sjb_default_band(int64_t dim);
 float sjb_accum_slack(int64_t dim);
 
 /* Join two prepared (normalised) relations on the device; asynchronous.
- * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: fp16 operand images.
+ * d_l32/d_r32: canonical fp32 rows; d_l16/d_r16: 16-bit operand images.
  * Replaces tensor_join's tile loop (join.py:338-359: tile_similarity +
  * threshold_scan + MatchSink.merge) with filter -> canonical recheck ->
  * row bucketing -> per-row sort.  Writes the canonical MatchSet columns to

@@ -211,7 +211,7 @@ def _run_workers(n, target):
 
 
 def pack_transpose(nr: np.ndarray) -> np.ndarray:
-    """sj_pack_transpose (_kernelcore.c:140-144), done once per join (join.py:342)."""
+    """sj_pack_transpose (_kernelcore.c:113-117), done once per join (join.py:342)."""
     packed = np.empty((nr.shape[1], nr.shape[0]), dtype=np.float32)
     lib().sj_pack_transpose(_p(nr, _c_f32p), nr.shape[0], nr.shape[1], _p(packed, _c_f32p))
     return packed

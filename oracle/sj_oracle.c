@@ -7,11 +7,11 @@
  * Every function restates one reference routine (paths relative to
  * /root/reference/pkg/src/simjoin/):
  *
- *   oc_fnv1a64          <- sj_fnv1a64            _kernelcore.c:60-67
- *   oc_synthetic_fill   <- splitmix64 + sj_synthetic_fill  _kernelcore.c:69-74, 99-107
- *   oc_normalize_rows   <- normalize_row + sj_normalize_rows _kernelcore.c:79-97, 109-114
- *   oc_row_norms        <- sj_row_norms           _kernelcore.c:116-124
- *   oc_dot_seq          <- sj_dot_seq + MADD      _kernelcore.c:48-52, 128-133
+ *   oc_fnv1a64          <- sj_fnv1a64            _kernelcore.c:33-40
+ *   oc_synthetic_fill   <- splitmix64 + sj_synthetic_fill  _kernelcore.c:42-50, 72-80
+ *   oc_normalize_rows   <- normalize_row + sj_normalize_rows _kernelcore.c:52-70, 82-87
+ *   oc_row_norms        <- sj_row_norms           _kernelcore.c:89-99
+ *   oc_dot_seq          <- sj_dot_seq + MADD      _kernelcore.c:21-25, 101-106
  *                          (x86 FMA build: one fmaf per component, sequential in d)
  *   oc_join_count/fill  <- tensor_join semantics  join.py:317-373 (tile_dot cell ==
  *                          sj_dot_seq, scan `>= theta`, canonical (l, r) order

@@ -90,7 +90,7 @@ struct JoinPlan {
   uint32_t smem;
   uint64_t seg_cap;
   bool pair;  // CTA-pair (cta_group::2) filter kernel
-  bool ts;    // R block in tensor memory (sjb_join_ts.cu; default for kpad <= 128)
+  bool ts;    // R block in tensor memory (sjb_join_ts.cu; opt-in A/B, SJB_FILTER=ts)
   bool wide;  // K-streaming kernel (kpad > 128)
   bool wide_fused;        // wide: recheck inside the filter (A/B only)
   bool defer;             // d <= 128: row-grouped recheck after the filter (dense joins)
@@ -187,7 +187,18 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->wide_fused = false;
   pl->tile_stride = 0;
   pl->defer = false;
-  if (pl->kpad > 128) return make_wide_plan(a, pl, sms, max_dyn_smem(dev));
+  const bool raw = a->left_inv_norm != nullptr || a->right_inv_norm != nullptr;
+  if (raw && (a->left_inv_norm == nullptr || a->right_inv_norm == nullptr))
+    return fail(SJB_E_INVALID, "raw-operand mode needs both relations' inverse norms");
+  if (raw && pl->kpad <= 128)
+    return fail(SJB_E_UNSUPPORTED, "raw-operand mode is for dim > 128 (the wide filter)");
+  if (a->sims_mode == 1 && !raw)
+    return fail(SJB_E_INVALID, "sims_mode 1 (tensor similarities) needs raw-operand mode");
+  if (pl->kpad > 128) {
+    if (int rc = make_wide_plan(a, pl, sms, max_dyn_smem(dev))) return rc;
+    if (a->sims_mode == 1) pl->wide_fused = false;   // pending lists need the separate recheck
+    return SJB_OK;
+  }
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
   // the row-grouped recheck stages candidates in the output-sized key buffer
   pl->defer = use_deferred_recheck(a) && a->out_cap >= a->cand_cap;
@@ -256,6 +267,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
       work, total;
+  size_t pend, pendn;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -280,6 +292,10 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   w.tiles = o;    o = align256(o + (size_t)grid * (size_t)tile_stride * 4);
   w.ncand = o;    o = align256(o + 16);
   w.work = o;     o = align256(o + 16);
+  // tolerance emission: per-CTA pending slot lists + counts
+  const bool tol = a->sims_mode == 1;
+  w.pend = o;     o = align256(o + (tol ? ccap * 4 : 0));
+  w.pendn = o;    o = align256(o + (tol ? (size_t)grid * 4 : 0));
   w.total = o;
   return w;
 }
@@ -350,7 +366,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// The fp16 operand image (sjb_operand_elems elements, 256-row tiles of
+// The 16-bit operand image (sjb_operand_elems elements, 256-row tiles of
 // [k-group][row][8]) as a 3-D tensor (256 elements = 32 rows x 8, 8 row
 // blocks, kgroups * tiles); box {256, box_rows/32, kgroups} = one
 // [k-group][box_rows][8] block.  The 512 B inner extent keeps every request
@@ -577,6 +593,31 @@ int sjb_gather_normalize_rows(const float* d_table, const int64_t* d_index, int6
                         d_tile_err, stream);
 }
 
+int sjb_prepare_bf16(const void* d_in, int64_t n, int64_t dim, float* d_out32, void* d_out16,
+                     float* d_inv_norm, unsigned long long* d_repaired, void* stream) {
+  if (n < 0 || dim < 1 || !d_out32 || !d_out16 || !d_inv_norm)
+    return fail(SJB_E_INVALID, "bad bf16 prep arguments");
+  const int kpad = (int)sjb_kpad(dim);
+  if (kpad <= 128) return fail(SJB_E_UNSUPPORTED, "sjb_prepare_bf16 is for dim > 128");
+  const int64_t tiles = sjb_operand_elems(n, dim) / (kpad * (int64_t)sjb::kTileRows);
+  if (tiles == 0) return SJB_OK;
+  const int smem = sjb::kWideRows * (int)(dim | 1) * 4;
+  if (int rc = set_smem_attr((const void*)sjb::prepare_bf16_kernel, smem)) return rc;
+  sjb::prepare_bf16_kernel<<<(unsigned)tiles, sjb::kPrepThreads, smem, as_stream(stream)>>>(
+      reinterpret_cast<const uint16_t*>(d_in), n, (int)dim, kpad, d_out32,
+      reinterpret_cast<sjb::op16_t*>(d_out16), d_inv_norm, d_repaired);
+  SJB_CK_LAUNCH("prepare_bf16");
+  return SJB_OK;
+}
+
+float sjb_raw_band(int64_t dim) {
+  // exact bf16 products: fp32 accumulation of the tensor-core and canonical
+  // sums (<= 2 dim 2^-24 each, generous), the canonical rows' and the inverse
+  // norms' roundings and the two epilogue products (8 u), + 2e-6 for the fp32
+  // evaluation of the cutoffs
+  return (float)(4.0 * (double)dim * 5.9604644775390625e-08 + 8 * 5.9604644775390625e-08 + 2e-6);
+}
+
 int sjb_cast_rows(const float* d_in, int64_t n, int64_t dim, void* d_out16, void* stream) {
   if (n < 0 || dim < 1 || d_out16 == nullptr) return fail(SJB_E_INVALID, "bad cast arguments");
   const int kpad = (int)sjb_kpad(dim);
@@ -704,6 +745,8 @@ struct JoinCtx {
   uint64_t* ncand;  // dense recheck: number of grouped candidates
   unsigned int* work;  // wide group recheck: dynamic item counter
   bool empty;  // n_left == 0 or n_right == 0
+  uint32_t* pend;
+  uint32_t* pend_count;
 };
 
 int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_bytes, JoinCtx* c) {
@@ -736,6 +779,8 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
   c->ncand = reinterpret_cast<uint64_t*>(ws + w.ncand);
   c->work = reinterpret_cast<unsigned int*>(ws + w.work);
+  c->pend = reinterpret_cast<uint32_t*>(ws + w.pend);
+  c->pend_count = reinterpret_cast<uint32_t*>(ws + w.pendn);
   return SJB_OK;
 }
 
@@ -856,6 +901,16 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
     wp.debug = jp.debug_mode;
     wp.tile_off = c.tile_off;
     wp.tile_stride = pl.tile_stride;
+    wp.inv_a = args->left_inv_norm;
+    wp.inv_b = args->right_inv_norm;
+    wp.tol = args->sims_mode == 1 ? 1 : 0;
+    wp.hi_cut = args->theta + args->band;
+    wp.pend = c.pend;
+    wp.pend_count = c.pend_count;
+    if (wp.inv_a != nullptr) {   // raw operands: the uniform accumulation band only
+      wp.row_err = nullptr;
+      wp.tile_err = nullptr;
+    }
     if (pl.wide_fused) {
       if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<true>, (int)pl.smem)) return rc;
       sjb::wide::filter_kernel<true>
@@ -866,7 +921,13 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       sjb::wide::filter_kernel<false>
           <<<pl.grid, sjb::wide::Cfg<false>::kThreads, pl.smem, st>>>(wp);
       SJB_CK_LAUNCH("wide_filter");
-      if (jp.debug_mode != 1) {
+      if (wp.tol && jp.debug_mode != 1) {
+        // tolerance emission: only the band pairs need the canonical chain
+        sjb::wide::recheck_pending_kernel<<<sjb_sm_count(current_device()) * 8, 256, 0, st>>>(
+            c.cand, pl.seg_cap, c.pend, c.pend_count, c.cta, pl.grid, d_l32, d_r32,
+            (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+        SJB_CK_LAUNCH("recheck_pending");
+      } else if (jp.debug_mode != 1) {
         sjb::wide::RecheckParams rp;
         rp.cand = c.cand;
         rp.seg_cap = pl.seg_cap;

@@ -29,7 +29,7 @@ __device__ __forceinline__ float from_op16(op16_t h, bool bf) {
 }
 
 
-// Rows per fp16 operand tile.  Both relations are stored as a sequence of
+// Rows per 16-bit operand tile.  Both relations are stored as a sequence of
 // 256-row tiles in the UMMA canonical K-major no-swizzle layout
 // ([k-group of 8 elements][row][8 elements], 16 B core-matrix rows), so one
 // 1-D bulk copy moves a whole tile into shared memory and the tensor core
@@ -40,7 +40,7 @@ constexpr int kTileRows = 256;
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
-// Element offset of (row, k) inside the tiled fp16 image of a relation with
+// Element offset of (row, k) inside the tiled 16-bit image of a relation with
 // `kpad` padded columns.
 __host__ __device__ inline int64_t tiled_offset(int64_t row, int64_t k, int64_t kpad) {
   int64_t t = row / kTileRows, r = row % kTileRows;
@@ -254,7 +254,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Canonical similarity: sequential fp32 fused multiply-add over d, exactly
-// the reference's sj_dot_seq with MADD = fmaf (_kernelcore.c:48-52, 128-133).
+// the reference's sj_dot_seq with MADD = fmaf (_kernelcore.c:21-25, 101-106).
 __device__ __forceinline__ float dot_seq_dev(const float* __restrict__ a,
                                              const float* __restrict__ b, int dim) {
   float acc = 0.0f;
@@ -416,6 +416,93 @@ __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, fl
     if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
     pos++;
   }
+}
+
+// Tolerance emission (raw-operand wide filter, sims_mode 1): the same hit
+// masks and slot reservation as emit_row_chunk64 (every pair with approx >=
+// cutoff gets a slot), but each slot's sim is written here: approx itself for
+// pairs at or above hi_cut (final matches -- |approx - canonical| < band, so
+// the canonical decision is certain -- counted into the row), kPending for
+// the band pairs, whose slots are appended to the CTA's pending list.
+constexpr uint32_t kPending = 0x7fc00002u;   // a NaN payload: recheck pending
+
+__device__ __forceinline__ void emit_row_chunk64_tol(
+    const float* v, bool row_ok, float cutoff, float hi_cut, uint32_t gi, uint32_t j0,
+    int64_t col_lim, uint32_t* cta_cnt, uint32_t* cta_sat, uint64_t* seg, uint64_t seg_cap,
+    uint32_t* sims, uint32_t* rowcount, uint32_t* pend_cnt, uint32_t* pend) {
+  const int lane = threadIdx.x & 31;
+  float g[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const float* x = v + 8 * k;
+    g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
+  }
+  const float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
+  const bool hit = row_ok && m >= cutoff;
+  if (!__any_sync(0xffffffffu, hit)) return;
+  uint32_t mk0 = 0, mk1 = 0;
+  if (hit) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (g[k] >= cutoff) {
+        uint32_t b = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) b |= (v[8 * k + e] >= cutoff ? 1u : 0u) << e;
+        if (k < 4) mk0 |= b << (8 * k);
+        else mk1 |= b << (8 * (k - 4));
+      }
+    }
+    if (col_lim < 64) {
+      const int cl = col_lim < 0 ? 0 : (int)col_lim;
+      mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
+      mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
+    }
+  }
+  const uint32_t cnt = __popc(mk0) + __popc(mk1);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t base = 0;
+  if (lane == 31 && wtot) {
+    base = atomicAdd(cta_cnt, wtot);
+    if (base + wtot < base) *cta_sat = 1u;
+  }
+  base = __shfl_sync(0xffffffffu, base, 31);
+  const uint64_t pos0 = (uint64_t)base + (incl - cnt);
+  uint32_t finals = 0;
+  if (cnt) {
+    // static column indices keep v[] in registers: groups of 8 columns, each
+    // hit's slot = pos0 + the hits below it
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const uint32_t gb = ((k < 4 ? mk0 : mk1) >> (8 * (k & 3))) & 0xFFu;
+      if (gb == 0) continue;
+      const uint32_t below = k < 4 ? __popc(mk0 & ((1u << (8 * k)) - 1u))
+                                   : __popc(mk0) + __popc(mk1 & ((1u << (8 * (k - 4))) - 1u));
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        if (gb & (1u << e)) {
+          const uint64_t pos = pos0 + below + __popc(gb & ((1u << e) - 1u));
+          const float x = v[8 * k + e];
+          if (pos < seg_cap) {
+            seg[pos] = pack_pair(gi, j0 + 8 * k + e);
+            if (x >= hi_cut) {
+              sims[pos] = __float_as_uint(x);
+              finals++;
+            } else {
+              sims[pos] = kPending;
+              pend[atomicAdd(pend_cnt, 1u)] = (uint32_t)pos;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (finals) atomicAdd(rowcount + gi, finals);
 }
 
 // One canonical recheck of a written candidate slot.

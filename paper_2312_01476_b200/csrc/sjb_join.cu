@@ -1,12 +1,12 @@
 // sjb_join.cu -- the fused R.S^T threshold filter (the hot path).
 //
 // Replaces the reference's tile_similarity + threshold_scan pair
-// (linalg.py:116-153 -> sj_tile_dot _kernelcore.c:300-323 + sj_scan_count/fill
-// :327-350) with one persistent, warp-specialised tcgen05 kernel that never
+// (linalg.py:116-153 -> sj_tile_dot _kernelcore.c:273-296 + sj_scan_count/fill
+// :300-323) with one persistent, warp-specialised tcgen05 kernel that never
 // materialises the similarity matrix:
 //
 //   warp 0       S producer: 1-D bulk copies (TMA, cp.async.bulk) of pre-tiled
-//                fp16 operand tiles into a shared-memory ring (mbarriers)
+//                16-bit (bf16) operand tiles into a shared-memory ring (mbarriers)
 //   warp 0 ln 1  R-block producer (resident operand, one copy per item)
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..17  epilogue: tcgen05.ld of the fp32 accumulators, 3-input max

@@ -68,6 +68,19 @@ struct Params {
   uint32_t* sims_bits;
   uint32_t* rowcount;
   int debug;  // 1: fused recheck warps idle (filter timing only; results invalid)
+  // raw-operand mode (bf16 inputs, sjb_prepare_bf16): the operands are the
+  // raw bf16 rows and the epilogue normalises after the GEMM,
+  // approx = (acc * inv_a[i]) * inv_b[j]; nullptr: normalised operands
+  const float* inv_a;
+  const float* inv_b;
+  // tolerance emission (sims_mode 1, raw mode): pairs with approx >= hi_cut
+  // are final (sim = approx, counted here); pairs in [cutoff, hi_cut) are
+  // pending -- their slots go to the CTA's pending list for the canonical
+  // recheck (recheck_pending_kernel)
+  int tol;
+  float hi_cut;
+  uint32_t* pend;        // [grid][seg_cap] pending slot indices
+  uint32_t* pend_count;  // [grid] pending entries of this launch
 };
 
 __host__ __device__ inline uint32_t smem_bytes(int stages) {
@@ -101,6 +114,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   uint32_t* cta_cnt = tmem_slot + 2;
   uint32_t* cta_sat = tmem_slot + 3;
   uint32_t* epi_done = tmem_slot + 4;
+  uint32_t* pend_cnt = tmem_slot + 5;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -113,6 +127,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     }
     init_segment_count(p.cta_count, p.append != 0, cta_cnt, cta_sat);
     *epi_done = 0u;
+    *pend_cnt = 0u;
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -157,7 +172,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer
     // whole warp, warp-uniform; one elected lane issues (lean issue)
-    const uint32_t idesc = umma_idesc_f16_f32(128, 256);
+    const uint32_t idesc = umma_idesc_f16_f32(128, 256, p.inv_a != nullptr);
     const uint32_t lbo = kTileRows * 16, sbo = 128;
     const uint64_t kstep = (2 * lbo) >> 4, half_step = (128 * 16) >> 4;
     const uint64_t ring_desc = umma_desc_kmajor_noswz(smem_u32(ring), lbo, sbo);
@@ -230,6 +245,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
           const int64_t gi64 = rb * kTileRows + h * 128 + lane_base + lane;
           const float cutoff =
               row_cutoff(p.cutoff, p.theta, p.slack, p.row_err, p.tile_err, gi64, p.n_a, t);
+          const float inv_i = (p.inv_a != nullptr && gi64 < p.n_a) ? __ldg(p.inv_a + gi64) : 1.0f;
 #pragma unroll 1
           for (int k = 0; k < kChunksPerWarp; k++) {
             const int cq = cq0 + k * (kEpiWarps / 4);
@@ -244,9 +260,29 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
               if (lane == 0) mbar_arrive_relaxed(&acc_empty[h]);
             }
             const int64_t col_lim = p.n_b - t * kTileRows - cq * 64;
-            emit_row_chunk64(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,
-                             (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt, cta_sat, seg,
-                             seg_cap);
+            if (p.inv_a != nullptr) {
+              // normalise after the GEMM: (acc * inv_i) * inv_j (inv_b is
+              // padded to whole tiles, zero past n_b)
+              const float4* ib = reinterpret_cast<const float4*>(p.inv_b + t * kTileRows + cq * 64);
+#pragma unroll
+              for (int q4 = 0; q4 < 16; q4++) {
+                const float4 w = __ldg(ib + q4);
+                v[4 * q4 + 0] = __fmul_rn(__fmul_rn(v[4 * q4 + 0], inv_i), w.x);
+                v[4 * q4 + 1] = __fmul_rn(__fmul_rn(v[4 * q4 + 1], inv_i), w.y);
+                v[4 * q4 + 2] = __fmul_rn(__fmul_rn(v[4 * q4 + 2], inv_i), w.z);
+                v[4 * q4 + 3] = __fmul_rn(__fmul_rn(v[4 * q4 + 3], inv_i), w.w);
+              }
+            }
+            if (p.tol)
+              emit_row_chunk64_tol(v, gi64 < p.n_a, cutoff, p.hi_cut, (uint32_t)gi64,
+                                   (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt,
+                                   cta_sat, seg, seg_cap,
+                                   p.sims_bits + (uint64_t)blockIdx.x * seg_cap, p.rowcount,
+                                   pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap);
+            else
+              emit_row_chunk64(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,
+                               (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt, cta_sat,
+                               seg, seg_cap);
           }
         }
       }
@@ -268,8 +304,10 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
     p.cta_count[blockIdx.x] = *cta_sat ? ~0ull >> 1 : (unsigned long long)*cta_cnt;
+    if (p.tol) p.pend_count[blockIdx.x] = *pend_cnt;
+  }
 }
 
 // ------------------------------------------------------------- recheck
@@ -906,6 +944,58 @@ __global__ void __launch_bounds__(kRtThreads, 1)
         }
       }
       kg = ke;
+    }
+  }
+}
+
+// Canonical recheck of the pending pairs of tolerance emission (the pairs
+// within the band of theta; everything else was decided by the filter).
+// Pending entry k of CTA c is visited at position p = k * grid + c, so
+// neighbouring threads work on pairs the filter emitted at about the same
+// time -- from the same few S chunks, which are then L2 hits.  Two
+// independent sequential chains per thread (dot_seq2_dev, bitwise
+// sj_dot_seq).  Saturated segments are skipped: the join is retried.
+__global__ void __launch_bounds__(256)
+recheck_pending_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                       const uint32_t* __restrict__ pend, const uint32_t* __restrict__ pend_count,
+                       const unsigned long long* __restrict__ cta_count, int n_cta,
+                       const float* __restrict__ l32, const float* __restrict__ r32, int dim,
+                       float theta, uint32_t* __restrict__ sims_bits,
+                       uint32_t* __restrict__ rowcount) {
+  __shared__ uint32_t s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_cta; c += blockDim.x) atomicMax(&s_max, pend_count[c]);
+  __syncthreads();
+  const uint64_t total = (uint64_t)s_max * (uint64_t)n_cta;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto locate = [&](uint64_t p, uint64_t* slot, uint32_t* gi, uint32_t* gj) -> bool {
+    if (p >= total) return false;
+    const uint64_t k = p / (uint64_t)n_cta, c = p - k * (uint64_t)n_cta;
+    if (k >= pend_count[c] || cta_count[c] > seg_cap) return false;
+    *slot = c * seg_cap + pend[c * seg_cap + k];
+    const uint64_t u = cand[*slot];
+    *gi = (uint32_t)(u >> 32);
+    *gj = (uint32_t)u;
+    return true;
+  };
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += 2 * stride) {
+    uint64_t s0 = 0, s1 = 0;
+    uint32_t i0 = 0, j0 = 0, i1 = 0, j1 = 0;
+    const bool a = locate(p, &s0, &i0, &j0);
+    const bool b = locate(p + stride, &s1, &i1, &j1);
+    if (a && b) {
+      float x0, x1;
+      dot_seq2_dev(l32 + (size_t)i0 * dim, r32 + (size_t)j0 * dim, l32 + (size_t)i1 * dim,
+                   r32 + (size_t)j1 * dim, dim, x0, x1);
+      finish_candidate(sims_bits, s0, i0, x0, theta, rowcount);
+      finish_candidate(sims_bits, s1, i1, x1, theta, rowcount);
+    } else if (a) {
+      finish_candidate(sims_bits, s0, i0, dot_seq_dev(l32 + (size_t)i0 * dim, r32 + (size_t)j0 * dim, dim),
+                       theta, rowcount);
+    } else if (b) {
+      finish_candidate(sims_bits, s1, i1, dot_seq_dev(l32 + (size_t)i1 * dim, r32 + (size_t)j1 * dim, dim),
+                       theta, rowcount);
     }
   }
 }

@@ -7,7 +7,7 @@
 // Same job and output as join_filter_kernel (sjb_join.cu): the fused
 // R.S^T filter replacing tile_similarity + threshold_scan
 // (linalg.py:116-153 -> sj_tile_dot / sj_scan_count / sj_scan_fill,
-// _kernelcore.c:300-350), candidates packed into per-CTA segments and
+// _kernelcore.c:273-323), candidates packed into per-CTA segments and
 // re-decided in canonical fp32 by the recheck warps.  What changes is where
 // the operands live:
 //

@@ -9,8 +9,8 @@
 //
 // plus the dense kernels behind the reference backend API:
 //   tile_dot   canonical dense tile (sj_tile_dot, _kernelcore.c:300-323)
-//   dots_vm    sj_dots_vm (_kernelcore.c:135-138)
-//   scan_hits  row-major threshold scan of a dense buffer (_kernelcore.c:327-350)
+//   dots_vm    sj_dots_vm (_kernelcore.c:108-111)
+//   scan_hits  row-major threshold scan of a dense buffer (_kernelcore.c:300-323)
 #include "sjb_common.cuh"
 
 namespace sjb {
@@ -570,7 +570,7 @@ tile_dot_kernel(const float* __restrict__ left, int64_t lda, const float* __rest
 // fp64 sequential sums rounded to fp32 (sj_row_norms), then one fp32 multiply
 // and one fp32 divide (numpy float32 ufuncs, round to nearest).  flags bit 0:
 // ||a|| == 0, bit 1: some ||m_i|| == 0 (the reference raises ZeroVector).
-// dots_vm (sj_dots_vm, _kernelcore.c:126-133) is the same kernel without the
+// dots_vm (sj_dots_vm, _kernelcore.c:108-111) is the same kernel without the
 // norms.
 __device__ __forceinline__ float row_norm_dev(const float* x, int dim) {
   double ss = 0.0;

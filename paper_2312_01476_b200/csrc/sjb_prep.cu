@@ -4,8 +4,9 @@
 // tile, stages it in shared memory (coalesced loads), runs the per-row
 // canonical arithmetic, then writes
 //   * the canonical fp32 rows (bitwise equal to the reference's
-//     sj_normalize_rows, _kernelcore.c:79-114), and
-//   * optionally the fp16 copy in the tiled UMMA operand layout
+//     sj_normalize_rows, _kernelcore.c:52-87), and
+//   * optionally the 16-bit copy (bf16 for kpad <= 128, fp16 above) in the
+//     tiled UMMA operand layout
 //     (sjb_common.cuh tiled_offset), zero-padded to kpad columns.
 #include "sjb_common.cuh"
 
@@ -14,7 +15,7 @@ namespace sjb {
 constexpr int kPrepThreads = 128;
 
 // Sequential fp64 sum of squares, repair rule, fp64 divide -- the reference's
-// normalize_row (_kernelcore.c:79-97).  Operates on one smem row.  The square
+// normalize_row (_kernelcore.c:52-70).  Operates on one smem row.  The square
 // of an fp32 value is exact in fp64 (<= 48 significant bits), so the
 // reference's ss + x*x (one rounding, in the add) is exactly fma(x, x, ss).
 // With `err` != nullptr the same final pass also measures the row's fp16
@@ -106,7 +107,7 @@ __device__ __forceinline__ double quot_rn(double x, double norm, double y, bool 
 // Normalise the vrows (<= kWideRows) rows staged in sm; row errors to err_out
 // (nullptr: not wanted).  Returns this thread's repaired-row count.
 __device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, float* err_out,
-                                   bool bf) {
+                                   bool bf, float* inv_out = nullptr) {
   __shared__ double s_norm[kWideRows], s_y[kWideRows];
   __shared__ double s_part[kPrepThreads / 32][kWideRows];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -115,6 +116,7 @@ __device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, flo
     const double norm = row_norm_smem(sm + tid * pitch, dim, &rep);
     s_norm[tid] = norm;
     s_y[tid] = __drcp_rn(norm);
+    if (inv_out != nullptr) inv_out[tid] = __double2float_rn(s_y[tid]);  // RN(1 / norm)
   }
   __syncthreads();
   const bool want = err_out != nullptr;
@@ -281,7 +283,7 @@ __device__ void finish_subtile(float* sm, int pitch, int r0, int sub, int rows, 
 // in: n x dim fp32 row-major (or, with `gather`, a table whose row gather[i]
 // is relation row i).  One CTA per 256-row operand tile, staged in sub-tiles
 // of `sub` rows (sub * (dim|1) floats of smem).  The grid may cover tiles past
-// n: those are written as zero operand tiles so the fp16 image can be padded.
+// n: those are written as zero operand tiles so the operand image can be padded.
 __global__ void __launch_bounds__(kPrepThreads)
 normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ gather, int64_t n,
                       int dim, int kpad, int sub, float* __restrict__ out32,
@@ -501,7 +503,71 @@ normalize_pipe_kernel(const float* __restrict__ in, int64_t n, int64_t n_slabs, 
   }
 }
 
-// Synthetic model (_kernelcore.c:69-74, 99-107): stream seed per row, element
+// bf16 relations for the raw-operand wide filter (BASELINE cfg4: d = 768
+// bf16 inputs).  The operand image holds the RAW bf16 rows (exact: the
+// tensor-core products of bf16 values are exact, so the filter's error is
+// only fp32 accumulation), the fp32 outputs are the canonical normalised rows
+// (bitwise sj_normalize_rows of the rows' fp32 values, which the bf16 values
+// are exactly), and inv_norm[i] = RN(1 / ||x_i||) for the epilogue's
+// normalise-after-GEMM.  A repaired (near-zero) row gets component 0 := 1 in
+// its raw image too, like the reference's row.  One CTA per 256-row tile,
+// 32-row sub-tiles (sequential fp64 sums one thread per row, element-parallel
+// divide: normalize_rows_wide).  Rows >= n (tile padding) get zero operands
+// and inv_norm 0.
+__global__ void __launch_bounds__(kPrepThreads)
+prepare_bf16_kernel(const uint16_t* __restrict__ in, int64_t n, int dim, int kpad,
+                    float* __restrict__ out32, op16_t* __restrict__ out16,
+                    float* __restrict__ inv_norm, unsigned long long* __restrict__ repaired) {
+  extern __shared__ float sm[];
+  __shared__ float s_inv[kWideRows];
+  const int pitch = dim | 1;
+  const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
+  const int rows = (int)mx<int64_t>(0, mn<int64_t>(kTileRows, n - row0));
+  op16_t* tile16 = out16 + (row0 / kTileRows) * (int64_t)kTileRows * kpad;
+  const int ngrp = kpad / 8;
+  for (int r0 = 0; r0 < kTileRows; r0 += kWideRows) {
+    const int vrows = max(0, min(kWideRows, rows - r0));
+    // raw operand chunks (8 k of one row: 16 B) straight from the input, and
+    // the rows' fp32 values into shared memory
+    for (int c = threadIdx.x; c < kWideRows * ngrp; c += kPrepThreads) {
+      const int g = c / kWideRows, r = c - g * kWideRows;
+      __align__(16) op16_t v[8];
+      if (r < vrows) {
+        const uint16_t* src = in + (row0 + r0 + r) * (int64_t)dim + g * 8;
+        if (g * 8 + 8 <= dim && ((dim & 7) == 0)) {
+          *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; e++) v[e] = g * 8 + e < dim ? src[e] : (op16_t)0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+          if (g * 8 + e < dim)
+            sm[r * pitch + g * 8 + e] = __bfloat162float(__ushort_as_bfloat16(v[e]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) v[e] = 0;
+      }
+      reinterpret_cast<uint4*>(tile16)[g * kTileRows + r0 + r] = *reinterpret_cast<uint4*>(v);
+    }
+    __syncthreads();
+    int rep = normalize_rows_wide(sm, pitch, vrows, dim, nullptr, true, s_inv);
+    if (threadIdx.x < kWideRows)
+      inv_norm[row0 + r0 + threadIdx.x] = threadIdx.x < vrows ? s_inv[threadIdx.x] : 0.0f;
+    if (rep && threadIdx.x < vrows)   // the reference's repaired row has x[0] = 1
+      tile16[(r0 + threadIdx.x) * 8] = (op16_t)0x3F80;   // bf16(1.0): k-group 0, element 0
+    if (repaired != nullptr) {
+      rep = __reduce_add_sync(0xffffffffu, rep);
+      if ((threadIdx.x & 31) == 0 && rep) atomicAdd(repaired, (unsigned long long)rep);
+    }
+    __syncthreads();
+    float* dst = out32 + (row0 + r0) * (int64_t)dim;
+    for_each_elem(vrows * dim, dim, [&](int e, int r, int d) { dst[e] = sm[r * pitch + d]; });
+    __syncthreads();
+  }
+}
+
+// Synthetic model (_kernelcore.c:42-50, 72-80): stream seed per row, element
 // d = splitmix64 output d+1 mapped to fp64 [-1,1), truncated to fp32, then the
 // row is normalised.  Element-parallel generation, row-serial normalisation.
 __device__ __forceinline__ float splitmix_elem(uint64_t seed, int d) {
@@ -536,7 +602,7 @@ synthetic_fill_kernel(const uint64_t* __restrict__ seeds, int64_t n, int dim, in
   if (tile_err != nullptr && threadIdx.x == 0) tile_err[blockIdx.x] = __uint_as_float(tile_max);
 }
 
-// FNV-1a-64 (_kernelcore.c:60-67) of packed tokens, XOR a 64-bit seed
+// FNV-1a-64 (_kernelcore.c:33-40) of packed tokens, XOR a 64-bit seed
 // (SyntheticModel._stream_seed, embedding.py:87-88).
 __global__ void fnv1a64_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
                                int64_t n, uint64_t xor_seed, uint64_t* __restrict__ out) {
@@ -776,7 +842,7 @@ subword_gather_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restri
   }
 }
 
-// Row L2 norms in fp64, returned as fp32 (sj_row_norms, _kernelcore.c:116-124).
+// Row L2 norms in fp64, returned as fp32 (sj_row_norms, _kernelcore.c:89-99).
 __global__ void row_norms_kernel(const float* __restrict__ m, int64_t n, int dim,
                                  float* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -72,15 +72,38 @@ CONFIGS = {
                  theta=0.8, seed=0),
     # wide embeddings; the full 1M x 4M join is R-sharded over 8 GPUs
     "cfg4": dict(n_left=1_000_000, n_right=4_000_000, dim=768, n_centroids=50_000, sigma=0.6,
-                 theta=0.75, seed=0, zipf=1.1),
+                 theta=0.75, seed=0, zipf=1.1, bf16=True),
 }
 
 
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """fp32 values rounded to the nearest bf16 (ties to even), as fp32: the
+    values a bf16 relation holds, exactly representable in fp32."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = (b + np.uint32(0x7FFF) + ((b >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return r.view(np.float32)
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """The bf16 bit patterns (u16) of bf16-exact fp32 values."""
+    return (np.ascontiguousarray(x, dtype=np.float32).view(np.uint32) >> np.uint32(16)).astype(
+        np.uint16)
+
+
 def config_vectors(name: str, **over):
+    """Inputs of a BASELINE config.  cfg4 is d = 768 *bf16* (BASELINE.json
+    configs[3]): its rows are rounded to bf16 values (returned as fp32 arrays
+    of bf16-exact values -- what the reference receives; the GPU path takes
+    them as bf16 tensors, see bf16_bits).  bf16=False keeps fp32 rows."""
     c = dict(CONFIGS[name])
+    bf = over.pop("bf16", c.pop("bf16", False))
     c.update(over)
-    return clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"], c["sigma"],
-                          c["seed"], zipf=c.get("zipf")), c
+    L, S = clustered_pair(c["n_left"], c["n_right"], c["dim"], c["n_centroids"], c["sigma"],
+                          c["seed"], zipf=c.get("zipf"))
+    if bf:
+        L, S = round_bf16(L), round_bf16(S)
+    c["bf16"] = bf
+    return (L, S), c
 
 
 _ALPHA = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)

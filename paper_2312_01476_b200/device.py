@@ -95,6 +95,9 @@ class PreparedRelation:
     # 16-bit rounding errors (sjb_join_args.left_row_err / right_tile_err):
     row_err: Optional[torch.Tensor] = None       # (n,) >= ||op(x_i) - x_i||
     tile_err: Optional[torch.Tensor] = None      # (tiles,) max over each 256-row tile
+    # raw-operand relations (prepare_bf16): op holds the raw bf16 rows and
+    # inv_norm[i] = RN(1 / ||x_i||) (rows padded to 512, 0 past n)
+    inv_norm: Optional[torch.Tensor] = None
 
     @property
     def device(self) -> torch.device:
@@ -113,7 +116,12 @@ class PreparedRelation:
         return PreparedRelation(self.f32[r0:r1], self.op[t0 * TILE_ROWS * kp:], r1 - r0,
                                 self.dim, self.name, None,
                                 None if self.row_err is None else self.row_err[r0:r1],
-                                None if self.tile_err is None else self.tile_err[t0:])
+                                None if self.tile_err is None else self.tile_err[t0:],
+                                None if self.inv_norm is None else self.inv_norm[r0:])
+
+    @property
+    def raw(self) -> bool:
+        return self.inv_norm is not None
 
 
 def tile_count(n: int) -> int:
@@ -149,6 +157,51 @@ def prepare(raw: torch.Tensor, name: str = "", out32: Optional[torch.Tensor] = N
         _lib.check(L.sjb_normalize_rows(_vp(raw), n, dim, _vp(f32), _vp(op), _vp(rep), _vp(re),
                                         _vp(te), _stream(dev)), "sjb_normalize_rows")
     return PreparedRelation(f32, op, n, dim, name, rep, re, te)
+
+
+def raw_band(dim: int) -> float:
+    """Filter band of raw-operand (bf16) joins (C ABI sjb_raw_band): exact
+    products, so only accumulation and the normalisation roundings."""
+    return float(_lib.lib().sjb_raw_band(dim))
+
+
+def prepare_bf16(raw: torch.Tensor, name: str = "") -> PreparedRelation:
+    """A bf16 relation (n, dim > 128) for the raw-operand wide filter
+    (sjb_prepare_bf16): canonical normalised fp32 rows (bitwise the
+    reference's normalize_rows of the rows' exact fp32 values), the RAW bf16
+    rows as the operand image, and the rows' inverse norms."""
+    if not raw.is_cuda or raw.dtype != torch.bfloat16 or raw.dim() != 2:
+        raise ValueError("prepare_bf16 needs a 2-D bfloat16 CUDA tensor")
+    raw = raw.contiguous()
+    n, dim = raw.shape
+    if kpad(dim) <= 128:
+        raise ValueError("raw-operand relations are for dim > 128 (the wide filter)")
+    dev = raw.device
+    f32 = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    op = torch.empty(operand_elems(n, dim), dtype=torch.bfloat16, device=dev)
+    inv = torch.empty(max(operand_elems(n, dim) // kpad(dim), 1), dtype=torch.float32, device=dev)
+    rep = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().sjb_prepare_bf16(_vp(raw), n, dim, _vp(f32), _vp(op), _vp(inv),
+                                               _vp(rep), _stream(dev)), "sjb_prepare_bf16")
+    return PreparedRelation(f32, op, n, dim, name, rep, None, None, inv)
+
+
+def _raw_mode(L: PreparedRelation, R: PreparedRelation) -> bool:
+    if L.raw != R.raw:
+        raise ValueError("both relations must be raw-operand (prepare_bf16) or neither")
+    return L.raw
+
+
+SIMS_MODES = {"exact": 0, "tensor": 1}
+
+
+def _sims_mode(sims: str, raw: bool) -> int:
+    if sims not in SIMS_MODES:
+        raise ValueError(f"sims must be one of {sorted(SIMS_MODES)}, got {sims!r}")
+    if sims == "tensor" and not raw:
+        raise ValueError("sims='tensor' needs raw-operand (bf16, dim > 128) relations")
+    return SIMS_MODES[sims]
 
 
 def prepare_pieces(raw: torch.Tensor, pieces, name: str = ""):
@@ -349,7 +402,7 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
                   left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
                   max_bytes: Optional[int] = None,
                   filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None,
-                  per_row_band: bool = True) -> DeviceMatches:
+                  per_row_band: bool = True, sims: str = "exact") -> DeviceMatches:
     """Canonical threshold join of two prepared relations (device-resident).
 
     Blocks once at the end to read the match count (the output size is data
@@ -359,7 +412,7 @@ def join_prepared(L: PreparedRelation, R: PreparedRelation, theta: float,
     candidates to recheck).
     """
     return join_prepared_async(L, R, theta, band, cand_cap, left_base, grid, tiles_per_chunk,
-                               max_bytes, filter_events, per_row_band).result()
+                               max_bytes, filter_events, per_row_band, sims=sims).result()
 
 
 def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
@@ -367,19 +420,25 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
                         left_base: int = 0, grid: int = 0, tiles_per_chunk: int = 0,
                         max_bytes: Optional[int] = None,
                         filter_events: Optional[Tuple[torch.cuda.Event, torch.cuda.Event]] = None,
-                        per_row_band: bool = True, _retries: int = 0) -> PendingJoin:
+                        per_row_band: bool = True, _retries: int = 0,
+                        sims: str = "exact") -> PendingJoin:
     """join_prepared without the final read-back: the kernels are queued on
-    the current stream and a PendingJoin is returned."""
+    the current stream and a PendingJoin is returned.  Raw-operand (bf16)
+    relations filter with raw_band; sims='tensor' then emits the epilogue
+    similarity for pairs clear of the band (the pair set stays exact)."""
     if L.dim != R.dim:
         raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
     if L.device != R.device:
         raise ValueError("relations live on different devices")
     lib = _lib.lib()
     dev = L.device
+    raw = _raw_mode(L, R)
+    smode = _sims_mode(sims, raw)
     theta32 = float(np.float32(theta))
-    band = default_band(L.dim) if band is None else float(band)
-    use_err = per_row_band and L.row_err is not None and R.tile_err is not None
-    key = (L.n, R.n, L.dim, theta32, float(np.float32(band)), grid, tiles_per_chunk, use_err)
+    band = (raw_band(L.dim) if raw else default_band(L.dim)) if band is None else float(band)
+    use_err = per_row_band and not raw and L.row_err is not None and R.tile_err is not None
+    key = (L.n, R.n, L.dim, theta32, float(np.float32(band)), grid, tiles_per_chunk, use_err,
+           raw, smode)
     if cand_cap is None:
         with _cap_lock:
             cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
@@ -399,7 +458,10 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
                              ev_filter_begin=ev0, ev_filter_end=ev1,
                              left_row_err=L.row_err.data_ptr() if use_err else None,
                              right_tile_err=R.tile_err.data_ptr() if use_err else None,
-                             recheck=_recheck_mode(key, L.n * R.n))
+                             recheck=_recheck_mode(key, L.n * R.n),
+                             left_inv_norm=L.inv_norm.data_ptr() if raw else None,
+                             right_inv_norm=R.inv_norm.data_ptr() if raw else None,
+                             sims_mode=smode)
         ws_bytes = int(lib.sjb_join_workspace_bytes(ctypes.byref(args)))
         if ws_bytes < 0:
             _lib.check(-3, "sjb_join_workspace_bytes")
@@ -414,11 +476,11 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
         ws = _workspace(ws_bytes, dev)
         lefts = torch.empty(max(int(cand_cap), 1), dtype=torch.int64, device=dev)
         rights = torch.empty_like(lefts)
-        sims = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
+        sims_out = torch.empty(max(int(cand_cap), 1), dtype=torch.float32, device=dev)
         info_t = torch.zeros(5, dtype=torch.int64, device=dev)
         _lib.check(lib.sjb_join_prepared_async(
             _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(args), _vp(ws),
-            ws_bytes, _vp(lefts), _vp(rights), _vp(sims), _vp(info_t), stream),
+            ws_bytes, _vp(lefts), _vp(rights), _vp(sims_out), _vp(info_t), stream),
             "sjb_join_prepared_async")
 
     def finish(info) -> DeviceMatches:
@@ -433,10 +495,10 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
                 return join_prepared_async(
                     L, R, theta, band, max(needed, n_matches, int(cand_cap) + 1), left_base, grid,
                     tiles_per_chunk, max_bytes, filter_events, per_row_band,
-                    _retries + 1).result()
+                    _retries + 1, sims=sims).result()
         with _cap_lock:
             _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
-        return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims[:n_matches], n_matches,
+        return DeviceMatches(lefts[:n_matches], rights[:n_matches], sims_out[:n_matches], n_matches,
                              n_cand, int(cand_cap), _retries, used_grid)
 
     return PendingJoin(info_t, finish)
@@ -444,13 +506,17 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
 
 def _join_args(L: PreparedRelation, n_right: int, theta32: float, band: float, cand_cap: int,
                left_base: int, use_err: bool, right_tile_err: Optional[torch.Tensor],
-               recheck: int = 0, grid: int = 0) -> "_lib.JoinArgs":
+               recheck: int = 0, grid: int = 0, right_inv: Optional[torch.Tensor] = None,
+               sims_mode: int = 0) -> "_lib.JoinArgs":
     return _lib.JoinArgs(n_left=L.n, n_right=n_right, dim=L.dim, theta=theta32, band=band,
                          cand_cap=int(cand_cap), out_cap=int(cand_cap), left_base=int(left_base),
                          grid=int(grid), tiles_per_chunk=0, ev_filter_begin=None, ev_filter_end=None,
                          left_row_err=L.row_err.data_ptr() if use_err else None,
                          right_tile_err=right_tile_err.data_ptr() if use_err else None,
-                         recheck=recheck)
+                         recheck=recheck,
+                         left_inv_norm=L.inv_norm.data_ptr() if right_inv is not None else None,
+                         right_inv_norm=right_inv.data_ptr() if right_inv is not None else None,
+                         sims_mode=sims_mode)
 
 
 def _stream_chunks(n: int, chunks: int, lead: int = 4):
@@ -482,25 +548,31 @@ class JoinSession:
     filter (NCCL's collective kernels in the multi-GPU streamed join)."""
 
     def __init__(self, L: PreparedRelation, R: PreparedRelation, theta: float,
-                 band: Optional[float] = None, left_base: int = 0, grid: int = 0):
+                 band: Optional[float] = None, left_base: int = 0, grid: int = 0,
+                 sims: str = "exact"):
         if L.dim != R.dim:
             raise DimensionMismatch(f"dimension mismatch: {L.dim} vs {R.dim}")
         self.L, self.R, self.theta, self.left_base, self.grid = L, R, theta, left_base, grid
+        self.sims = sims
         self.lib = _lib.lib()
         dev = self.dev = L.device
         n, dim = R.n, R.dim
+        raw = _raw_mode(L, R)
+        smode = _sims_mode(sims, raw)
         theta32 = float(np.float32(theta))
-        self.band = band = default_band(dim) if band is None else float(band)
-        self.key = (L.n, n, dim, theta32, float(np.float32(band)), grid, 0, True)
+        self.band = band = ((raw_band(dim) if raw else default_band(dim)) if band is None
+                            else float(band))
+        self.key = (L.n, n, dim, theta32, float(np.float32(band)), grid, 0, not raw, raw, smode)
         with _cap_lock:
             self.cand_cap = max(_cap_cache.get(self.key, 0), initial_capacity(L.n, n))
         self.empty = L.n == 0 or n == 0
         if self.empty:
             return
-        use_err = L.row_err is not None and R.tile_err is not None
+        use_err = not raw and L.row_err is not None and R.tile_err is not None
         with torch.cuda.device(dev):
             self.args = _join_args(L, n, theta32, band, self.cand_cap, left_base, use_err,
-                                   R.tile_err, _recheck_mode(self.key, L.n * n), grid)
+                                   R.tile_err, _recheck_mode(self.key, L.n * n), grid,
+                                   R.inv_norm if raw else None, smode)
             self.ws_bytes = int(self.lib.sjb_join_workspace_bytes(ctypes.byref(self.args)))
             if self.ws_bytes < 0:
                 _lib.check(-3, "sjb_join_workspace_bytes")
@@ -508,7 +580,7 @@ class JoinSession:
             cap = max(int(self.cand_cap), 1)
             self.lefts = torch.empty(cap, dtype=torch.int64, device=dev)
             self.rights = torch.empty_like(self.lefts)
-            self.sims = torch.empty(cap, dtype=torch.float32, device=dev)
+            self.sims_out = torch.empty(cap, dtype=torch.float32, device=dev)
             self.info_t = torch.zeros(5, dtype=torch.int64, device=dev)
             _lib.check(self.lib.sjb_join_begin(ctypes.byref(self.args), _vp(self.ws),
                                                self.ws_bytes, _stream(dev)), "sjb_join_begin")
@@ -528,11 +600,12 @@ class JoinSession:
     def finish(self) -> PendingJoin:
         L, R, dev = self.L, self.R, self.dev
         if self.empty:
-            return join_prepared_async(L, R, self.theta, self.band, left_base=self.left_base)
+            return join_prepared_async(L, R, self.theta, self.band, left_base=self.left_base,
+                                       sims=self.sims)
         with torch.cuda.device(dev):
             _lib.check(self.lib.sjb_join_finish(
                 _vp(L.f32), _vp(R.f32), ctypes.byref(self.args), _vp(self.ws), self.ws_bytes,
-                _vp(self.lefts), _vp(self.rights), _vp(self.sims), _vp(self.info_t),
+                _vp(self.lefts), _vp(self.rights), _vp(self.sims_out), _vp(self.info_t),
                 _stream(dev)), "sjb_join_finish")
         cand_cap, key = self.cand_cap, self.key
 
@@ -544,13 +617,13 @@ class JoinSession:
                 with torch.cuda.device(dev):
                     m = join_prepared(L, R, self.theta, self.band,
                                       cand_cap=max(needed, n_matches, cand_cap + 1),
-                                      left_base=self.left_base, grid=self.grid)
+                                      left_base=self.left_base, grid=self.grid, sims=self.sims)
                 m.retries += 1
                 return m
             with _cap_lock:
                 _cap_cache[key] = max(_cap_cache.get(key, 0), needed)
             return DeviceMatches(self.lefts[:n_matches], self.rights[:n_matches],
-                                 self.sims[:n_matches], n_matches, n_cand, int(cand_cap), 0,
+                                 self.sims_out[:n_matches], n_matches, n_cand, int(cand_cap), 0,
                                  int(flags[1]))
 
         return PendingJoin(self.info_t, finish)
@@ -767,7 +840,7 @@ def synthetic_rows(seeds: torch.Tensor, dim: int) -> torch.Tensor:
 def subword_rows(tokens, table: torch.Tensor, minn: int, maxn: int,
                  prepared: bool = False, name: str = ""):
     """Subword-model rows; prepared=True returns a PreparedRelation (embed +
-    normalise + fp16 image in one kernel), else the raw (n, dim) embedding."""
+    normalise + operand image), else the raw (n, dim) embedding."""
     _check_matrix(table, "bucket table")
     dev = table.device
     b, o = pack_tokens(tokens, dev)

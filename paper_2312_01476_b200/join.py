@@ -153,7 +153,7 @@ def copy_prepared(p: D.PreparedRelation, dev: torch.device) -> D.PreparedRelatio
     with torch.cuda.device(dev):
         cp = (lambda x: None if x is None else x.to(dev, non_blocking=True))
         return D.PreparedRelation(cp(p.f32), cp(p.op), p.n, p.dim, p.name, cp(p.repaired_dev),
-                                  cp(p.row_err), cp(p.tile_err))
+                                  cp(p.row_err), cp(p.tile_err), cp(p.inv_norm))
 
 
 def _run_devices(left: RawRelation, right: RawRelation, model: EmbeddingModel, t: Threshold,
@@ -374,15 +374,49 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
                     bufs[1][:done].numpy().view(np.uint64), bufs[2][:done].numpy())
 
 
+def _is_bf16(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.dtype == torch.bfloat16
+
+
 def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                         band: Optional[float] = None, left_name: str = "left",
-                        right_name: str = "right", device=None) -> Tuple[MatchSet, JoinStats]:
+                        right_name: str = "right", device=None,
+                        sims: str = "exact") -> Tuple[MatchSet, JoinStats]:
     """Join prefetched (un-normalised) vectors: the LookupModel path of the
     reference's tensor_join without the per-token dictionary.  Host or device
-    inputs; host MatchSet output."""
+    inputs; host MatchSet output.
+
+    bfloat16 tensors with dim > 128 (BASELINE cfg4) take the raw-operand
+    path: the bf16 rows feed the tensor cores as they are (exact products)
+    and are normalised after the GEMM, so the filter band is ~2e-4 instead
+    of the 16-bit rounding band.  The result is the reference's join of the
+    rows' (exact) fp32 values.  sims='tensor' (raw-operand path only)
+    returns the epilogue similarity for pairs clear of the band -- within
+    ~1e-6 of the canonical value -- and rechecks only the band pairs; the
+    pair set is exact either way."""
     t = Threshold.of(theta)
     dev = _device(device)
     t0 = time.perf_counter_ns()
+    if _is_bf16(left) and _is_bf16(right) and left.dim() == 2 and right.dim() == 2 and \
+            D.kpad(left.shape[1]) > 128:
+        check_dims(left.shape[1], right.shape[1])
+        with torch.cuda.device(dev):
+            pl = D.prepare_bf16(left.to(dev, non_blocking=True))
+            pr = D.prepare_bf16(right.to(dev, non_blocking=True))
+            m = D.join_prepared(pl, pr, t.value, band, sims=sims)
+            matches = _to_matchset(m, left_name, right_name)
+        wall = time.perf_counter_ns() - t0
+        return matches, JoinStats(wall_nanos=wall, model_calls_left=left.shape[0],
+                                  model_calls_right=right.shape[0],
+                                  pairs_compared=left.shape[0] * right.shape[0],
+                                  matches=len(matches), peak_buffer_bytes=0, threads=1,
+                                  algo="tensor", inner_relation="right")
+    if sims != "exact":
+        raise ValueError("sims='tensor' needs bfloat16 inputs with dim > 128")
+    if _is_bf16(left):
+        left = left.float()                  # exact: bf16 values are fp32 values
+    if _is_bf16(right):
+        right = right.float()
     with torch.cuda.device(dev):
         if _is_host(right) and right.shape[0] >= _STREAM_MIN_ROWS:
             # overlap the right relation's H2D copy with the filter, and the

@@ -36,7 +36,10 @@ def _dev() -> torch.device:
 
 
 def _h2d(a: np.ndarray) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(a)).to(_dev())
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:          # read-only views (EmbeddedRelation data): copy
+        a = a.copy()
+    return torch.from_numpy(a).to(_dev())
 
 
 def _stream():

@@ -234,6 +234,29 @@ def sharded_join_owned(R_shard, S_local, layout: PieceLayout, theta: float, left
     return (pending.result() if sync else pending), PR
 
 
+def gather_right_raw(S_local: torch.Tensor, layout: PieceLayout, group=None) -> torch.Tensor:
+    """The whole right relation on every rank from each rank's raw pieces
+    (layout order): one in-place all-gather per round.  For relations whose
+    preparation is cheap next to the join (cfg4: bf16 rows, d = 768 -- the
+    raw bf16 rows are half the bytes of the prepared fp32 rows, and each rank
+    prepares all of S in ~1% of its join), the raw rows travel and every
+    rank prepares locally."""
+    rank, w = world()
+    dim = S_local.shape[1]
+    out = torch.empty((layout.rows, dim), dtype=S_local.dtype, device=S_local.device)
+    off = 0
+    for _, r0, r1 in layout.owned(rank):
+        out[r0:r1].copy_(S_local[off:off + (r1 - r0)])
+        off += r1 - r0
+    if w > 1:
+        flat = out.view(-1).view(torch.uint8)
+        per_row = dim * out.element_size()
+        for j in range(layout.rounds):
+            for wk in _gather_round([(flat, per_row, 1)], layout, j, rank, group):
+                wk.wait()
+    return out[:layout.n]
+
+
 # ---- root-broadcast variant (S on one rank) --------------------------------
 
 def broadcast_right(S: torch.Tensor, root: int = 0, group=None, chunk_rows: int = 0) -> torch.Tensor:

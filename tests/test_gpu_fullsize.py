@@ -155,12 +155,27 @@ def test_cfg3_full_set_equals_reference():
 
 
 def test_cfg4_shard_full_set_equals_reference():
-    """BASELINE configs[3]'s distribution (d = 768, 50k centroids, sigma 0.6,
-    Zipf(1.1) cluster sizes, theta = 0.75): the wide filter and tile-group
-    recheck on a 16k x 1M slice, the whole set against the reference kernels."""
+    """BASELINE configs[3] (d = 768 bf16, 50k centroids, sigma 0.6, Zipf(1.1)
+    cluster sizes, theta = 0.75) on a 16k x 1M slice, the whole set against
+    the reference kernels on the rows' fp32 values: the raw-operand path
+    (bf16 operands, normalise after the GEMM) with canonical sims (bitwise)
+    and with tensor sims (same set, every sim within 1e-5), and the fp32
+    path (16-bit normalised operands, tile-group recheck)."""
     from paper_2312_01476_b200 import datagen
+    from paper_2312_01476_b200 import device as D
     (L, S), c = datagen.config_vectors("cfg4", n_left=16_000, n_right=1_000_000)
+    assert c["bf16"]
     theta = c["theta"]
-    got = _device_join(L, S, theta)
+    want = _refkern_join(L, S, theta)
+    dev = torch.device("cuda", 0)
+    bf = lambda x: torch.from_numpy(datagen.bf16_bits(x).view(np.int16)).view(  # noqa: E731
+        torch.bfloat16).to(dev)
+    pl, pr = D.prepare_bf16(bf(L)), D.prepare_bf16(bf(S))
+    got = D.join_prepared(pl, pr, theta).to_host()
     _check_canonical(*got, theta)
-    _assert_same(got, _refkern_join(L, S, theta))
+    _assert_same(got, want)
+    tl, tr, ts = D.join_prepared(pl, pr, theta, sims="tensor").to_host()
+    assert np.array_equal(tl, want[0]) and np.array_equal(tr, want[1])
+    assert np.abs(ts.astype(np.float64) - want[2]).max() <= 1e-5
+    del pl, pr
+    _assert_same(_device_join(L, S, theta), want)

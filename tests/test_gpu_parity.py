@@ -750,3 +750,94 @@ def test_host_input_join_input_kinds(cuda, left_kind):
 def datagen_pair(nl, nr, dim, seed):
     from paper_2312_01476_b200 import datagen
     return datagen.clustered_pair(nl, nr, dim, 60, 0.4, seed)
+
+
+# ---- raw-operand (bf16) wide path: BASELINE cfg4's bf16 relations ---------
+
+def _bf16_tensor(x, dev):
+    from paper_2312_01476_b200 import datagen
+    return torch.from_numpy(datagen.bf16_bits(x).view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+def _bf16_case(nl, nr, dim, c, sigma, seed):
+    from paper_2312_01476_b200 import datagen
+    L, S = datagen.clustered_pair(nl, nr, dim, c, sigma, seed)
+    L, S = datagen.round_bf16(L), datagen.round_bf16(S)
+    L[5] = 0.0                              # a repaired row
+    S[3, :] = 0.0
+    S[3, 7] = np.float32(2.0 ** -100)       # below the repair threshold, not zero
+    return L, S
+
+
+@pytest.mark.parametrize("dim", [136, 200, 768])
+def test_prepare_bf16(cuda, dim):
+    """sjb_prepare_bf16: canonical fp32 rows bitwise the oracle's
+    normalize_rows of the exact fp32 values, the raw bf16 operand image
+    (component 0 := 1 for repaired rows), and RN(1 / ||x||)."""
+    from paper_2312_01476_b200 import device as D
+    L, _ = _bf16_case(700, 10, dim, 20, 0.6, dim)
+    p = D.prepare_bf16(_bf16_tensor(L, cuda))
+    want, rep = O.normalize_rows(L)
+    assert np.array_equal(p.f32.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    assert p.repaired() == rep == 1
+    rows, full = _decode_operand(p.op, len(L), dim)
+    raw = L.copy()
+    raw[5, 0] = 1.0                         # the reference's repaired row
+    from paper_2312_01476_b200 import datagen
+    assert np.array_equal(rows[:, :dim].view(np.uint16), datagen.bf16_bits(raw))
+    assert (rows[:, dim:] == 0).all() and (full[len(L):] == 0).all()
+    x64 = raw.astype(np.float64)
+    ss = np.cumsum(x64 * x64, axis=1)[:, -1]            # sequential, exact squares
+    inv = (1.0 / np.sqrt(ss)).astype(np.float32)
+    got = p.inv_norm.cpu().numpy()
+    assert np.array_equal(got[:len(L)].view(np.uint32), inv.view(np.uint32))
+    assert (got[len(L):] == 0).all()
+
+
+@pytest.mark.parametrize("theta", [0.75, 0.3, -1.0])
+def test_bf16_join_exact_and_tensor_sims(cuda, theta):
+    """The raw-operand filter (bf16 operands, normalise after the GEMM,
+    band = sjb_raw_band): sims='exact' is bitwise the oracle's join of the
+    fp32 values; sims='tensor' returns the same pair SET with every
+    similarity within 1e-5 of the canonical one (the north star's bound)."""
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    nl, nr = (900, 2300) if theta > -1 else (300, 400)
+    L, S = _bf16_case(nl, nr, 768, 30, 0.6, 17)
+    wl, wr, ws = O.join_raw(L, S, theta, threads=4)
+    assert len(wl) > 0
+    pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+    m = D.join_prepared(pl, pr, theta)
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
+    # raw band: far fewer non-matching candidates than the 16-bit per-row band
+    mf = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                         D.prepare(torch.from_numpy(S).to(cuda)), theta)
+    assert m.n_candidates <= mf.n_candidates
+    for api in (False, True):
+        if api:
+            ms, _ = tensor_join_vectors(_bf16_tensor(L, cuda), _bf16_tensor(S, cuda), theta,
+                                        sims="tensor")
+            tl, tr, ts = ms.lefts, ms.rights, ms.sims
+        else:
+            tl, tr, ts = D.join_prepared(pl, pr, theta, sims="tensor").to_host()
+        assert np.array_equal(tl, wl) and np.array_equal(tr, wr)
+        err = np.abs(ts.astype(np.float64) - ws.astype(np.float64))
+        assert err.max() <= 1e-5, err.max()
+        assert (ts >= np.float32(theta)).all()
+
+
+def test_bf16_overflow_retry_tensor_sims(cuda):
+    """Tolerance emission under candidate overflow: the retry with the
+    measured capacity returns the exact set."""
+    from paper_2312_01476_b200 import device as D
+    L, S = _bf16_case(600, 900, 256, 4, 0.4, 5)
+    theta = 0.5
+    wl, wr, ws = O.join_raw(L, S, theta, threads=4)
+    pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+    m = D.join_prepared(pl, pr, theta, cand_cap=4096, sims="tensor")
+    assert m.retries >= 1
+    lo, ro, so = m.to_host()
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5

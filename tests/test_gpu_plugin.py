@@ -121,8 +121,8 @@ def test_kernel_functions_bitwise(sj):
     assert np.array_equal(cu.pack_transpose(a[:200]), bt)
     o1 = np.empty((100, 200), np.float32)
     o2 = np.empty((100, 200), np.float32)
-    cu.tile_dot(a[100:], bt, o1)
-    cc.tile_dot(a[100:], bt, o2)
+    cu.tile_dot(a[100:200], bt, o1)
+    cc.tile_dot(a[100:200], bt, o2)
     assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
     h1, h2 = cu.scan_hits(o1, np.float32(0.1), 5, 7), cc.scan_hits(o2, np.float32(0.1), 5, 7)
     assert all(np.array_equal(x, y) for x, y in zip(h1, h2))

@@ -470,6 +470,7 @@ def run_ours(args):
 
         def step(events=None):
             Sx = S_bf if world == 1 else MG.gather_right_raw(S_loc, lay)
+            PR_last["p"] = None
             PR_last["p"] = pr = D.prepare_bf16(Sx)
             return D.join_prepared(D.prepare_bf16(R_dev), pr, theta, left_base=r0,
                                    filter_events=events, sims=args.sims)
@@ -512,8 +513,19 @@ def run_ours(args):
             return D.join_prepared(embed(Lb, Lo, n_shard), embed(Sb, So, n_right), theta,
                                    left_base=r0, filter_events=events)
 
+    # cold call: no capacity / placement history for the shape (the first
+    # join a process runs), timed on the wall clock around the whole call
+    D._cap_cache.clear()
     torch.cuda.synchronize()
+    barrier()
+    t_cold = time.perf_counter()
+    m = step()
+    torch.cuda.synchronize()
+    cold_ms = max_over_ranks((time.perf_counter() - t_cold) * 1e3)
+    cold_retries = int(getattr(m, "retries", 0))
+    m = None
     for _ in range(args.warmup):
+        m = None                           # free the previous result before the next
         m = step()
     torch.cuda.synchronize()
     barrier()
@@ -525,6 +537,7 @@ def run_ours(args):
             flush.fill_(1)                       # L2 flush between timed steps
             torch.cuda.synchronize()
             barrier()
+            m = None
             ev[0].record()
             m = step((ev[2], ev[3]) if world == 1 else None)
             ev[1].record()
@@ -720,6 +733,7 @@ def run_ours(args):
                                                          "timed steps",
                        "matches": n_matches, "candidates": n_cand,
                        "output_pairs_per_s": n_matches / (ms_per_step / 1e3),
+                       "cold_first_call_ms": cold_ms, "cold_first_call_retries": cold_retries,
                        "launches_per_step": launches / args.steps},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,

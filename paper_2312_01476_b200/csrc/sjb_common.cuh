@@ -426,10 +426,14 @@ __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, fl
 // the band pairs, whose slots are appended to the CTA's pending list.
 constexpr uint32_t kPending = 0x7fc00002u;   // a NaN payload: recheck pending
 
-__device__ __forceinline__ void emit_row_chunk64_tol(
+// Returns the chunk's final matches of this lane's row (the caller adds them
+// to the row count once per work item: one global atomic per row and item
+// instead of one per chunk -- every epilogue warp of a CTA works on the same
+// 256 rows, so per-chunk atomics on them serialise).
+__device__ __forceinline__ uint32_t emit_row_chunk64_tol(
     const float* v, bool row_ok, float cutoff, float hi_cut, uint32_t gi, uint32_t j0,
     int64_t col_lim, uint32_t* cta_cnt, uint32_t* cta_sat, uint64_t* seg, uint64_t seg_cap,
-    uint32_t* sims, uint32_t* rowcount, uint32_t* pend_cnt, uint32_t* pend) {
+    uint32_t* sims, uint32_t* pend_cnt, uint32_t* pend) {
   const int lane = threadIdx.x & 31;
   float g[8];
 #pragma unroll
@@ -439,7 +443,7 @@ __device__ __forceinline__ void emit_row_chunk64_tol(
   }
   const float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
   const bool hit = row_ok && m >= cutoff;
-  if (!__any_sync(0xffffffffu, hit)) return;
+  if (!__any_sync(0xffffffffu, hit)) return 0u;
   uint32_t mk0 = 0, mk1 = 0;
   if (hit) {
 #pragma unroll
@@ -502,7 +506,7 @@ __device__ __forceinline__ void emit_row_chunk64_tol(
       }
     }
   }
-  if (finals) atomicAdd(rowcount + gi, finals);
+  return finals;
 }
 
 // One canonical recheck of a written candidate slot.

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       const int64_t rb = item % nb, sc = item / nb;
       const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
+      uint32_t fin0 = 0u, fin1 = 0u;   // tolerance emission: this lane's rows' final matches
       for (int64_t t = t0; t < t1; t++, tile_it++) {
         mbar_wait(acc_full, tile_it & 1u);
         tc_fence_after();
@@ -273,18 +274,23 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
                 v[4 * q4 + 3] = __fmul_rn(__fmul_rn(v[4 * q4 + 3], inv_i), w.w);
               }
             }
-            if (p.tol)
-              emit_row_chunk64_tol(v, gi64 < p.n_a, cutoff, p.hi_cut, (uint32_t)gi64,
-                                   (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt,
-                                   cta_sat, seg, seg_cap,
-                                   p.sims_bits + (uint64_t)blockIdx.x * seg_cap, p.rowcount,
-                                   pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap);
-            else
+            if (p.tol) {
+              const uint32_t f = emit_row_chunk64_tol(v, gi64 < p.n_a, cutoff, p.hi_cut, (uint32_t)gi64,
+                                             (uint32_t)(t * kTileRows + cq * 64), col_lim,
+                                             cta_cnt, cta_sat, seg, seg_cap,
+                                             p.sims_bits + (uint64_t)blockIdx.x * seg_cap,
+                                             pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap);
+              if (h) fin1 += f; else fin0 += f;
+            } else
               emit_row_chunk64(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,
                                (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt, cta_sat,
                                seg, seg_cap);
           }
         }
+      }
+      if (p.tol) {   // rows >= n_a never have finals
+        if (fin0) atomicAdd(p.rowcount + rb * kTileRows + lane_base + lane, fin0);
+        if (fin1) atomicAdd(p.rowcount + rb * kTileRows + 128 + lane_base + lane, fin1);
       }
     }
     if (!kFused) {

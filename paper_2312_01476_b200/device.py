@@ -373,6 +373,29 @@ def initial_capacity(n_left: int, n_right: int) -> int:
     return int(max(1 << 20, min(pairs, 1 << 24)))
 
 
+# Cold joins (no capacity history for the shape) above this many pairs size
+# their candidate buffers from a sampled pre-pass instead of the fixed first
+# guess, so a selective-but-dense join (cfg5 at theta 0.4: 8.1e7 candidates)
+# does not run twice; smaller joins retry cheaply if they overflow.
+PREPASS_MIN_PAIRS = 2_000_000_000
+PREPASS_ROWS = 2048
+
+
+def _prepass_capacity(L: PreparedRelation, R: PreparedRelation, theta: float, band,
+                      per_row_band: bool, sims: str) -> int:
+    """Candidates of a contiguous 2048-row sample of the left relation (from
+    its middle, on a 512-row boundary) joined with all of R, scaled to all
+    of L, plus 20% and 64k slack: the first call's capacity.  The sample's
+    own capacity is the fixed first guess (it retries if that overflows)."""
+    rows = min(L.n, PREPASS_ROWS)
+    r0 = ((L.n - rows) // 2) // (2 * TILE_ROWS) * (2 * TILE_ROWS)
+    sample = L.rows(r0, r0 + rows)
+    m = join_prepared(sample, R, theta, band, cand_cap=initial_capacity(rows, R.n),
+                      per_row_band=per_row_band, sims=sims)
+    est = m.n_candidates * (L.n / max(rows, 1))
+    return int(est * 1.2) + (1 << 16)
+
+
 class PendingJoin:
     """A join whose kernels are queued but whose match count (data dependent)
     has not been read back yet.  result() blocks on that count, reruns the
@@ -441,7 +464,12 @@ def join_prepared_async(L: PreparedRelation, R: PreparedRelation, theta: float,
            raw, smode)
     if cand_cap is None:
         with _cap_lock:
-            cand_cap = max(_cap_cache.get(key, 0), initial_capacity(L.n, R.n))
+            known = _cap_cache.get(key, 0)
+        if known == 0 and L.n * R.n >= PREPASS_MIN_PAIRS and L.n >= 2 * PREPASS_ROWS:
+            known = _prepass_capacity(L, R, theta, band, per_row_band, sims)
+            with _cap_lock:               # also picks the recheck placement below
+                _cap_cache[key] = max(_cap_cache.get(key, 0), known)
+        cand_cap = max(known, initial_capacity(L.n, R.n))
     ev0 = ev1 = None
     if filter_events is not None:
         for e in filter_events:
@@ -696,6 +724,72 @@ def join_chunked(L: PreparedRelation, raw: torch.Tensor, arrive, theta: float,
     return (pending if not sync else pending.result()), R
 
 
+class _Bounce:
+    """Pinned staging ring for PAGEABLE host -> device copies.  A pageable
+    cudaMemcpy is staged by the driver one buffer at a time (~9 GB/s here);
+    instead several host threads fill a pinned slot (numpy copies release
+    the GIL) while the copy engine drains the previous slot.  Slots are
+    reused once their copy's event has fired."""
+
+    SLOT_BYTES = 16 << 20
+    N_SLOTS = 4
+    THREADS = 4
+
+    def __init__(self):
+        from concurrent.futures import ThreadPoolExecutor
+        self.slots = [torch.empty(self.SLOT_BYTES, dtype=torch.uint8, pin_memory=True)
+                      for _ in range(self.N_SLOTS)]
+        self.views = [t.numpy() for t in self.slots]
+        self.events: list = [None] * self.N_SLOTS
+        self.k = 0
+        self.pool = ThreadPoolExecutor(self.THREADS)
+        self.lock = threading.Lock()
+
+    def copy(self, dst: torch.Tensor, src: np.ndarray, stream: torch.cuda.Stream) -> None:
+        """Queue dst <- src (same byte size; dst a contiguous CUDA tensor) on
+        `stream`; returns once the last slot has been filled."""
+        sb = np.ascontiguousarray(src).reshape(-1).view(np.uint8)
+        db = dst.reshape(-1).view(torch.uint8)
+        if sb.size != db.numel():
+            raise ValueError("bounce copy: size mismatch")
+        with self.lock:
+            for off in range(0, sb.size, self.SLOT_BYTES):
+                n = min(self.SLOT_BYTES, sb.size - off)
+                i = self.k % self.N_SLOTS
+                self.k += 1
+                if self.events[i] is not None:
+                    self.events[i].synchronize()
+                per = -(-n // self.THREADS)
+                step = -(-per // 4096) * 4096
+                futs = [self.pool.submit(np.copyto, self.views[i][a:min(n, a + step)],
+                                         sb[off + a:off + min(n, a + step)])
+                        for a in range(0, n, step)]
+                for f in futs:
+                    f.result()
+                with torch.cuda.stream(stream):
+                    db[off:off + n].copy_(self.slots[i][:n], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                self.events[i] = ev
+
+
+_bounce: Optional[_Bounce] = None
+
+
+def bounce_copy(dst: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream) -> None:
+    """dst (CUDA) <- src (host): pinned sources copy directly (async); pageable
+    ones go through the pinned staging ring (_Bounce)."""
+    global _bounce
+    if src.is_pinned():
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)
+        return
+    with _cap_lock:
+        if _bounce is None:
+            _bounce = _Bounce()
+    _bounce.copy(dst, src.numpy(), stream)
+
+
 class StagedCopy:
     """A host matrix copied to the device in row chunks on a side stream
     (`stage_host`): `raw` is the device buffer and chunk k covers rows
@@ -713,8 +807,8 @@ class StagedCopy:
 
     def _issue(self, k: int) -> None:
         r0, r1 = self.spans[k]
+        bounce_copy(self.raw[r0:r1], self.src[r0:r1], self.stream)
         with torch.cuda.stream(self.stream):
-            self.raw[r0:r1].copy_(self.src[r0:r1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.stream)
         self.events[k] = ev

@@ -440,8 +440,8 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                 spans = [(r0, r1) for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0]
 
                 def copy_rows(r0: int, r1: int) -> None:
+                    D.bounce_copy(L[r0:r1], lh[r0:r1], copy)   # pinned ring if pageable
                     with torch.cuda.stream(copy):
-                        L[r0:r1].copy_(lh[r0:r1], non_blocking=True)
                         ev = torch.cuda.Event()
                         ev.record(copy)
                     pieces.append((r0, r1, ev))

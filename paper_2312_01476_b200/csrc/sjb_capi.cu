@@ -119,10 +119,11 @@ int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   pl->a_bufs = 0;
   pl->a_tiles = 1;
   int stages = 0;
-  while (stages < 6 && (int)W::smem_bytes(stages + 1) <= max_smem) stages++;
+  const bool tol = a->sims_mode == 1;
+  while (stages < 6 && (int)W::smem_bytes(stages + 1, tol) <= max_smem) stages++;
   if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for the wide kernel");
   pl->stages = stages;
-  pl->smem = W::smem_bytes(stages);
+  pl->smem = W::smem_bytes(stages, tol);
   pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kTileRows);
   pl->n_btiles = (int)sjb::ceil_div(a->n_right, sjb::kTileRows);
   int tpc = a->tiles_per_chunk;

@@ -429,11 +429,15 @@ constexpr uint32_t kPending = 0x7fc00002u;   // a NaN payload: recheck pending
 // Returns the chunk's final matches of this lane's row (the caller adds them
 // to the row count once per work item: one global atomic per row and item
 // instead of one per chunk -- every epilogue warp of a CTA works on the same
-// 256 rows, so per-chunk atomics on them serialise).
+// 256 rows, so per-chunk atomics on them serialise).  `scr` is this lane's
+// 32-float shared scratch row: per 32-column half with hits, the 8-column
+// groups holding hits are parked there, so the hit loop reads the similarity
+// of a dynamic column without spilling v[] (static indices only) and the
+// code stays as compact as emit_row_chunk64's.
 __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
     const float* v, bool row_ok, float cutoff, float hi_cut, uint32_t gi, uint32_t j0,
     int64_t col_lim, uint32_t* cta_cnt, uint32_t* cta_sat, uint64_t* seg, uint64_t seg_cap,
-    uint32_t* sims, uint32_t* pend_cnt, uint32_t* pend) {
+    uint32_t* sims, uint32_t* pend_cnt, uint32_t* pend, float* scr) {
   const int lane = threadIdx.x & 31;
   float g[8];
 #pragma unroll
@@ -476,34 +480,30 @@ __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
     if (base + wtot < base) *cta_sat = 1u;
   }
   base = __shfl_sync(0xffffffffu, base, 31);
-  const uint64_t pos0 = (uint64_t)base + (incl - cnt);
+  uint64_t pos = (uint64_t)base + (incl - cnt);
   uint32_t finals = 0;
-  if (cnt) {
-    // static column indices keep v[] in registers: groups of 8 columns, each
-    // hit's slot = pos0 + the hits below it
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const uint32_t gb = ((k < 4 ? mk0 : mk1) >> (8 * (k & 3))) & 0xFFu;
-      if (gb == 0) continue;
-      const uint32_t below = k < 4 ? __popc(mk0 & ((1u << (8 * k)) - 1u))
-                                   : __popc(mk0) + __popc(mk1 & ((1u << (8 * (k - 4))) - 1u));
+  for (int hh = 0; hh < 2; hh++) {
+    uint32_t w = hh ? mk1 : mk0;
+    if (w == 0) continue;
 #pragma unroll
-      for (int e = 0; e < 8; e++) {
-        if (gb & (1u << e)) {
-          const uint64_t pos = pos0 + below + __popc(gb & ((1u << e) - 1u));
-          const float x = v[8 * k + e];
-          if (pos < seg_cap) {
-            seg[pos] = pack_pair(gi, j0 + 8 * k + e);
-            if (x >= hi_cut) {
-              sims[pos] = __float_as_uint(x);
-              finals++;
-            } else {
-              sims[pos] = kPending;
-              pend[atomicAdd(pend_cnt, 1u)] = (uint32_t)pos;
-            }
-          }
-        }
+    for (int k = 0; k < 4; k++)
+      if ((w >> (8 * k)) & 0xFFu) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) scr[8 * k + e] = v[32 * hh + 8 * k + e];
       }
+    while (w) {
+      const int b = __ffs(w) - 1;
+      w &= w - 1;
+      if (pos < seg_cap) {
+        const float x = scr[b];
+        seg[pos] = pack_pair(gi, j0 + 32 * hh + b);
+        const bool fin = x >= hi_cut;
+        sims[pos] = fin ? __float_as_uint(x) : kPending;
+        finals += fin ? 1u : 0u;
+        if (!fin) pend[atomicAdd(pend_cnt, 1u)] = (uint32_t)pos;
+      }
+      pos++;
     }
   }
   return finals;

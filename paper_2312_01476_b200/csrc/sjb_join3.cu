@@ -83,8 +83,14 @@ struct Params {
   uint32_t* pend_count;  // [grid] pending entries of this launch
 };
 
-__host__ __device__ inline uint32_t smem_bytes(int stages) {
-  return (uint32_t)stages * 2 * kChunkBytes + (4 + 2 * stages) * 8 + 32;
+// Tolerance emission: each epilogue lane's 32-column scratch row (pitch 33
+// floats: a lane's row is conflict-free against the other lanes')
+constexpr int kTolPitch = 33;
+constexpr uint32_t kTolScratchBytes = kEpiWarps * 32 * kTolPitch * 4;
+
+__host__ __device__ inline uint32_t smem_bytes(int stages, bool tol = false) {
+  return (uint32_t)stages * 2 * kChunkBytes + (4 + 2 * stages) * 8 + 32 +
+         (tol ? kTolScratchBytes : 0u);
 }
 
 // Max tiles one CTA walks in one launch (+1 for the end offset), for any
@@ -115,6 +121,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   uint32_t* cta_sat = tmem_slot + 3;
   uint32_t* epi_done = tmem_slot + 4;
   uint32_t* pend_cnt = tmem_slot + 5;
+  float* tol_scratch = reinterpret_cast<float*>(tmem_slot + 8);   // kTolScratchBytes (tol only)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -279,7 +286,8 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
                                              (uint32_t)(t * kTileRows + cq * 64), col_lim,
                                              cta_cnt, cta_sat, seg, seg_cap,
                                              p.sims_bits + (uint64_t)blockIdx.x * seg_cap,
-                                             pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap);
+                                             pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap,
+                                             tol_scratch + (ew * 32 + lane) * kTolPitch);
               if (h) fin1 += f; else fin0 += f;
             } else
               emit_row_chunk64(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,

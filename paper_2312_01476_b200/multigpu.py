@@ -108,12 +108,15 @@ def piece_layout(n: int, world: int, rounds: int = 0, growth: float = 1.5,
     later round's gather (time ~ rows) runs behind the previous round's
     filter (time ~ rows / world ... rows), which is longer once
     growth <= filter time per row / gather time per row.  rounds=0 picks up
-    to 8 rounds, fewer when S is small (no round below one 512-row piece per
-    rank)."""
+    to 4 rounds, fewer when S is small (no round below one 512-row piece per
+    rank).  Four rounds: each filter launch of a round costs ~0.05 ms of
+    launch and tail at cfg2 / 8 ranks (tools/shard_probe.py: 2.2 ms per rank
+    step with 1 or 4 rounds, 2.6-2.8 ms with 8)."""
     world = max(1, int(world))
     unit = world * align
     if rounds <= 0:
-        rounds = max(1, min(8, n // (4 * unit)))
+        rounds = int(os.environ.get("SJB_SHARD_ROUNDS", "0")) or max(1, min(4, n // (4 * unit)))
+    growth = float(os.environ.get("SJB_SHARD_GROWTH", growth))
     weights = [growth ** j for j in range(rounds)]
     total = sum(weights)
     pieces = []

@@ -26,7 +26,8 @@ ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 sms = int(_lib.lib().sjb_sm_count(0))
 reserve = MG.nccl_reserve_sms()
 base = None
-for world in (1, 2, 4, 8):
+worlds = [int(w) for w in os.environ.get("PROBE_WORLDS", "1,2,4,8").split(",")]
+for world in worlds:
     r0, r1 = MG.shard_range(L.shape[0], 0, world)
     R = Ld[r0:r1]
     lay = MG.piece_layout(S.shape[0], world)
@@ -35,7 +36,7 @@ for world in (1, 2, 4, 8):
         for _, a, b in lay.owned(k):
             D.prepare_into(Sd[a:b], PR, a)
     mine = lay.owned(0)
-    grid = sms - reserve if world > 1 else 0
+    grid = sms - reserve if world > 1 and reserve > 0 else 0
 
     def rank0_step():
         PL = D.prepare(R)

@@ -585,6 +585,11 @@ def run_ours(args):
 
     if not filt_ms:
         filt_ms = [filter_only_ms() for _ in range(3)]
+    # free the last step's device result and prepared S before the e2e joins
+    # (a cfg4 share's result alone is ~40 GB)
+    m = None
+    PR_last.clear()
+    torch.cuda.empty_cache()
 
     # ---- end to end through the public API with host buffers ----------------
     from paper_2312_01476_b200.join import tensor_join, tensor_join_vectors

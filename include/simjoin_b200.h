@@ -165,6 +165,11 @@ typedef struct sjb_join_args {
    * (|approx - canonical| < band, measured ~1e-6), only pairs within the
    * band are rechecked canonically.  The pair SET is exact either way. */
   int32_t sims_mode;
+  /* CTAs of this filter launch (dim <= 128 kernel; 0 = the plan's grid,
+   * i.e. args->grid or one per SM).  Fewer CTAs than the plan leave SMs free
+   * for kernels that must run beside the filter (NCCL's all-gathers of later
+   * S rounds); the segments of the plan's other CTAs stay empty. */
+  int32_t launch_grid;
 } sjb_join_args;
 
 typedef struct sjb_join_info {

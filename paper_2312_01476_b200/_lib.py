@@ -35,7 +35,7 @@ class JoinArgs(ctypes.Structure):
         ("left_row_err", ctypes.c_void_p), ("right_tile_err", ctypes.c_void_p),
         ("recheck", ctypes.c_int32),
         ("left_inv_norm", ctypes.c_void_p), ("right_inv_norm", ctypes.c_void_p),
-        ("sims_mode", ctypes.c_int32),
+        ("sims_mode", ctypes.c_int32), ("launch_grid", ctypes.c_int32),
     ]
 
 

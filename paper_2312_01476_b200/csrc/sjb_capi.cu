@@ -688,14 +688,26 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
       int dev = 0;
       cudaGetDevice(&dev);
       const int64_t want = sjb::ceil_div(n, sjb::kGatherThreads / 32);
-      const int grid = (int)sjb::mn<int64_t>(want, (int64_t)sjb_sm_count(dev) * 3);
       auto st = as_stream(stream);
-      if (dim <= 128)
-        sjb::subword_gather_kernel<1, 12><<<grid, sjb::kGatherThreads, 0, st>>>(
-            d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32);
-      else
-        sjb::subword_gather_kernel<2, 4><<<grid, sjb::kGatherThreads, 0, st>>>(
-            d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32);
+      // items in flight per warp (KU) against warps per SM (registers): an
+      // A/B switch, SJB_SUBWORD_KU = 8 (4 CTAs/SM), 12 (3), 16 or 24 (2)
+      // measured at cfg3 (200k strings, 2M x 100 table): KU 8: 0.48 ms,
+      // 12: 0.56, 16: 0.75, 24: 0.80 -- warps beat items per warp
+      const char* ke = getenv("SJB_SUBWORD_KU");
+      const int ku = ke ? atoi(ke) : 8;
+      const int per_sm = ku <= 4 ? 6 : (ku <= 6 ? 5 : (ku <= 8 ? 4 : (ku <= 12 ? 3 : 2)));
+      const int grid = (int)sjb::mn<int64_t>(want, (int64_t)sjb_sm_count(dev) * per_sm);
+#define SJB_GATHER(V, KU, MB)                                                          \
+  sjb::subword_gather_kernel<V, KU, MB><<<grid, sjb::kGatherThreads, 0, st>>>(          \
+      d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32)
+      if (dim > 128) SJB_GATHER(2, 4, 3);
+      else if (ku <= 4) SJB_GATHER(1, 4, 6);
+      else if (ku <= 6) SJB_GATHER(1, 6, 5);
+      else if (ku <= 8) SJB_GATHER(1, 8, 4);
+      else if (ku <= 12) SJB_GATHER(1, 12, 3);
+      else if (ku <= 16) SJB_GATHER(1, 16, 2);
+      else SJB_GATHER(1, 24, 2);
+#undef SJB_GATHER
       SJB_CK_LAUNCH("subword_gather");
     }
     if (!normalize) return SJB_OK;
@@ -1009,8 +1021,10 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
     if (int rc = encode_operand_map(&pp.tmap_a, d_l16, nl, pl.kpad, sjb::pair::kARows)) return rc;
     if (int rc = encode_operand_map(&pp.tmap_b, d_r16, nr, pl.kpad, sjb::pair::kHalfN)) return rc;
     if (int rc = launch_pair_filter(pp, pl.grid, pl.smem, st)) return rc;
-  } else if (int rc = launch_join_filter(jp, pl.grid, pl.smem, st)) {
-    return rc;
+  } else {
+    const int lg = args->launch_grid > 0 && args->launch_grid < pl.grid ? args->launch_grid
+                                                                         : pl.grid;
+    if (int rc = launch_join_filter(jp, lg, pl.smem, st)) return rc;
   }
   if (args->ev_filter_end)
     SJB_CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(args->ev_filter_end), st));

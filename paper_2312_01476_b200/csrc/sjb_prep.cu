@@ -781,8 +781,8 @@ __device__ __forceinline__ uint64_t subword_item_bucket(const uint8_t* __restric
 
 constexpr int kGatherThreads = 256;
 
-template <int V, int KU>
-__global__ void __launch_bounds__(kGatherThreads, 3)
+template <int V, int KU, int MINB>
+__global__ void __launch_bounds__(kGatherThreads, MINB)
 subword_gather_kernel(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ offs,
                       int64_t n, const float* __restrict__ table, uint64_t n_buckets,
                       uint64_t magic, int dim, int minn, int maxn, float* __restrict__ out) {

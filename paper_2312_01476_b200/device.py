@@ -613,12 +613,15 @@ class JoinSession:
             _lib.check(self.lib.sjb_join_begin(ctypes.byref(self.args), _vp(self.ws),
                                                self.ws_bytes, _stream(dev)), "sjb_join_begin")
 
-    def filter_rows(self, r0: int, r1: int) -> None:
+    def filter_rows(self, r0: int, r1: int, launch_grid: int = 0) -> None:
+        """Filter rows [r0, r1) of R; launch_grid > 0 launches the (dim <=
+        128) filter on that many CTAs only (SMs left for NCCL)."""
         if self.empty or r1 <= r0:
             return
         if r0 % TILE_ROWS:
             raise ValueError(f"row range [{r0}, {r1}) does not start on a tile boundary")
         L, R = self.L, self.R
+        self.args.launch_grid = int(launch_grid)
         with torch.cuda.device(self.dev):
             _lib.check(self.lib.sjb_join_filter_tiles(
                 _vp(L.f32), _vp(L.op), _vp(R.f32), _vp(R.op), ctypes.byref(self.args),

@@ -23,9 +23,10 @@ whole job (``sharded_join_owned``):
   buffers, then round j is ONE in-place all-gather per buffer: the round's
   pieces are contiguous in S, so the world's pieces land in row order.
 * Every rank filters round j's rows as soon as its all-gather has landed
-  (device.JoinSession), while rounds j+1.. are still on the wire.  The
-  filter runs on ``grid`` = SMs - reserve CTAs so NCCL's kernels always have
-  SMs to run on beside the persistent filter.
+  (device.JoinSession), while rounds j+1.. are still on the wire.  While
+  later gathers are in flight the filter launches on SMs - reserve CTAs so
+  NCCL's kernels always have SMs beside the persistent filter; the last
+  round runs on the whole GPU.
 
 ``sharded_join_streamed`` (rank 0 holds raw S and broadcasts it in row
 chunks; every rank normalises all of S) is kept for callers whose S exists on
@@ -185,7 +186,7 @@ class DeviceOps:
 
     def session(self, PL, PR, theta: float, band, left_base: int):
         from . import device as D
-        return D.JoinSession(PL, PR, theta, band, left_base, self.grid)
+        return D.JoinSession(PL, PR, theta, band, left_base)
 
 
 def nccl_reserve_sms() -> int:
@@ -232,7 +233,10 @@ def sharded_join_owned(R_shard, S_local, layout: PieceLayout, theta: float, left
     for j in range(layout.rounds):
         for wk in (works[j] if works else ()):
             wk.wait()                                    # the stream waits, not the host
-        session.filter_rows(*layout.round_rows(j))
+        # while later rounds' gathers are in flight the filter leaves NCCL its
+        # SMs; the last round has nothing in flight and takes the whole GPU
+        last = j == layout.rounds - 1
+        session.filter_rows(*layout.round_rows(j), launch_grid=0 if last else ops.grid)
     pending = session.finish()
     return (pending.result() if sync else pending), PR
 

@@ -155,6 +155,8 @@ def _cpu_prepare(raw):
 
 
 class _CpuOps:
+    grid = 0          # launch grid of the non-final rounds (device: SMs - NCCL reserve)
+
     def prepare_left(self, R):
         import oracle as O
         return O.normalize_rows(R.numpy())[0]
@@ -187,7 +189,7 @@ class _CpuSession:
         self.PL, self.PR, self.theta, self.base = PL, PR, theta, left_base
         self.parts, self.seen = [], []
 
-    def filter_rows(self, r0, r1):
+    def filter_rows(self, r0, r1, launch_grid=0):
         import oracle as O
         if r1 <= r0:
             return

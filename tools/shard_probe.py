@@ -42,9 +42,9 @@ for world in worlds:
         PL = D.prepare(R)
         for _, a, b in mine:                     # rank 0 prepares only its pieces
             D.prepare_into(Sd[a:b], PR, a)
-        sess = D.JoinSession(PL, PR, c["theta"], None, r0, grid)
-        for j in range(lay.rounds):
-            sess.filter_rows(*lay.round_rows(j))
+        sess = D.JoinSession(PL, PR, c["theta"], None, r0)
+        for j in range(lay.rounds):                # as multigpu.sharded_join_owned
+            sess.filter_rows(*lay.round_rows(j), launch_grid=0 if j == lay.rounds - 1 else grid)
         return sess.finish().result()
 
     for _ in range(3):

@@ -691,16 +691,18 @@ int sjb_subword_embed(const uint8_t* d_bytes, const int64_t* d_offs, int64_t n,
       auto st = as_stream(stream);
       // items in flight per warp (KU) against warps per SM (registers): an
       // A/B switch, SJB_SUBWORD_KU = 8 (4 CTAs/SM), 12 (3), 16 or 24 (2)
-      // measured at cfg3 (200k strings, 2M x 100 table): KU 8: 0.48 ms,
-      // 12: 0.56, 16: 0.75, 24: 0.80 -- warps beat items per warp
+      // measured at cfg3 (200k strings, 2M x 100 table): KU 2: see DESIGN,
+      // 4: 0.40 ms, 6: 0.45, 8: 0.48, 12: 0.56, 16: 0.75, 24: 0.80 -- warps
+      // in flight beat items in flight per warp
       const char* ke = getenv("SJB_SUBWORD_KU");
-      const int ku = ke ? atoi(ke) : 8;
-      const int per_sm = ku <= 4 ? 6 : (ku <= 6 ? 5 : (ku <= 8 ? 4 : (ku <= 12 ? 3 : 2)));
+      const int ku = ke ? atoi(ke) : 4;
+      const int per_sm = ku <= 2 ? 8 : (ku <= 4 ? 6 : (ku <= 6 ? 5 : (ku <= 8 ? 4 : (ku <= 12 ? 3 : 2))));
       const int grid = (int)sjb::mn<int64_t>(want, (int64_t)sjb_sm_count(dev) * per_sm);
 #define SJB_GATHER(V, KU, MB)                                                          \
   sjb::subword_gather_kernel<V, KU, MB><<<grid, sjb::kGatherThreads, 0, st>>>(          \
       d_bytes, d_offs, n, d_table, nb, magic, (int)dim, minn, maxn, d_out32)
       if (dim > 128) SJB_GATHER(2, 4, 3);
+      else if (ku <= 2) SJB_GATHER(1, 2, 8);
       else if (ku <= 4) SJB_GATHER(1, 4, 6);
       else if (ku <= 6) SJB_GATHER(1, 6, 5);
       else if (ku <= 8) SJB_GATHER(1, 8, 4);

@@ -281,7 +281,29 @@ def _pinned(n: int, dtype) -> torch.Tensor:
     return torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
 
 
-def _split_bounds(n: int, min_rows: int = 4096):
+# Result bytes of the last host-input join of a shape: output-heavy joins
+# (cfg5 at theta 0.4: 1.6 GB of MatchSet against a 21 ms join) are bound by
+# the device->host copy of the result, which only starts once a part's join
+# is done, so they split the left rows into many equal parts instead.
+_result_bytes: dict = {}
+HEAVY_RESULT_BYTES = 64 << 20
+HEAVY_PARTS = 8
+
+
+def _split_bounds(n: int, min_rows: int = 4096, heavy: bool = False):
+    """Left row bounds of the host-input join: `heavy` (the shape's last
+    result exceeded HEAVY_RESULT_BYTES) -> HEAVY_PARTS equal parts, so the
+    result copy starts after the first eighth; else _split_bounds_light."""
+    if heavy:
+        step = max(min_rows, -(-n // HEAVY_PARTS)) // 1024 * 1024 or 1024
+        bounds = list(range(0, n, step)) + [n]
+        if len(bounds) > 2 and bounds[-1] - bounds[-2] < min_rows:
+            del bounds[-2]               # fold a short tail into the last part
+        return bounds
+    return _split_bounds_light(n, min_rows)
+
+
+def _split_bounds_light(n: int, min_rows: int = 4096):
     """Left row bounds of the host-input join: 60% of the rows in the first
     part, whose filter hides the S copy (both scale with |S|.d; the filter
     must just outlast the copy plus its last chunk), then the rest as 70% +
@@ -303,7 +325,8 @@ def _split_bounds(n: int, min_rows: int = 4096):
 
 
 def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
-                     left_name: str, right_name: str, ready=None) -> MatchSet:
+                     left_name: str, right_name: str, ready=None,
+                     heavy: bool = False) -> MatchSet:
     """Host-input join in `parts` left row ranges: the first streams S in
     (H2D overlapped with its filter); each later part is queued on the
     resident S before the previous part's count is read back, so the GPU
@@ -313,7 +336,7 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
     and ordered, so the result is the canonical MatchSet (bounds:
     _split_bounds)."""
     n = PL.n
-    bounds = _split_bounds(n)
+    bounds = _split_bounds(n, heavy=heavy)
     if ready is None:
         ready = lambda r: None                          # noqa: E731  (rows all prepared)
     if len(bounds) <= 2:
@@ -428,6 +451,8 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
             comp = torch.cuda.current_stream(dev)
             copy = torch.cuda.Stream(dev)
             pieces = []
+            shape_key = (left.shape[0], right.shape[0], right.shape[1], float(np.float32(t.value)))
+            heavy = _result_bytes.get(shape_key, 0) > HEAVY_RESULT_BYTES
             if _is_host(left):
                 lh = _host_tensor(left)
                 if lh.dim() != 2:
@@ -435,7 +460,7 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                 check_dims(lh.shape[1], right.shape[1])
                 L = torch.empty(tuple(lh.shape), dtype=torch.float32, device=dev)
                 copy.wait_stream(comp)
-                b = _split_bounds(L.shape[0])
+                b = _split_bounds(L.shape[0], heavy=heavy)
                 cuts = [0, b[1], L.shape[0]] if len(b) > 2 else [0, L.shape[0]]
                 spans = [(r0, r1) for r0, r1 in zip(cuts[:-1], cuts[1:]) if r1 > r0]
 
@@ -458,7 +483,8 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
                 copy_rows(*sp)
             PL, ready = D.prepare_pieces(L, pieces)
             matches = _join_host_split(PL, staged, t.value, band, left_name, right_name,
-                                       ready=ready)
+                                       ready=ready, heavy=heavy)
+            _result_bytes[shape_key] = len(matches) * 20
         else:
             L = _as_device_matrix(left, dev)
             check_dims(L.shape[1], right.shape[1])

@@ -841,3 +841,24 @@ def test_bf16_overflow_retry_tensor_sims(cuda):
     lo, ro, so = m.to_host()
     assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
     assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
+
+
+def test_host_input_join_heavy_split(cuda, monkeypatch):
+    """Output-heavy host-input joins split the left rows into 8 equal parts
+    once the shape's previous result was large (join._result_bytes): the
+    same canonical MatchSet, pinned and pageable inputs."""
+    from paper_2312_01476_b200 import join as J
+    L, S = O_pair(9000, 70_000, 16, 6, 0.5, 77)
+    theta = 0.7
+    wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+    assert len(wl) > 0
+    monkeypatch.setattr(J, "HEAVY_RESULT_BYTES", 0)
+    for pinned in (True, False):
+        for _ in range(2):                        # the second call splits 8 ways
+            lh = torch.from_numpy(L)
+            sh = torch.from_numpy(S)
+            if pinned:
+                lh, sh = lh.pin_memory(), sh.pin_memory()
+            ms, _ = J.tensor_join_vectors(lh, sh, theta, device=cuda)
+            assert _bits_equal(ms, wl, wr, ws)
+    assert max(J._result_bytes.values()) == len(wl) * 20

@@ -102,6 +102,12 @@ int sjb_prepare_bf16(const void* d_in, int64_t n, int64_t dim, float* d_out32, v
  * norms' and the epilogue products' roundings: 4 dim 2^-24 + 8 2^-24 + 2e-6. */
 float sjb_raw_band(int64_t dim);
 
+/* 1 when the library was built with the measured-and-rejected A/B kernels
+ * (-DSJB_AB_KERNELS=1: SJB_FILTER=pair|ts, SJB_RBLOCK=512,
+ * SJB_WIDE_RECHECK=fused|tile); 0 in the default build, where those
+ * switches fail with SJB_E_UNSUPPORTED. */
+int sjb_ab_kernels(void);
+
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);
 

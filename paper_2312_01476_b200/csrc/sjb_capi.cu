@@ -15,8 +15,18 @@
 #include "../../include/simjoin_b200.h"
 #include "sjb_common.cuh"
 #include "sjb_join.cu"
+// The measured-and-rejected A/B kernels (DESIGN.md "Measured and rejected":
+// TS-mode filter, CTA-pair filter, 512-row R blocks, the wide filter with
+// fused recheck warps, the per-tile staged wide recheck) are built only with
+// -DSJB_AB_KERNELS=1 (SJB_NVCC_EXTRA); the default library holds the
+// measured-best kernels.
+#ifndef SJB_AB_KERNELS
+#define SJB_AB_KERNELS 0
+#endif
+#if SJB_AB_KERNELS
 #include "sjb_join_ts.cu"
 #include "sjb_join2.cu"
+#endif
 #include "sjb_join3.cu"
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
@@ -147,6 +157,12 @@ bool use_pair_filter() {
   return f != nullptr && strcmp(f, "pair") == 0;
 }
 
+int ab_missing(const char* what) {
+  return fail(SJB_E_UNSUPPORTED, "%s is an A/B kernel: rebuild with SJB_NVCC_EXTRA=-DSJB_AB_KERNELS=1",
+              what);
+}
+
+#if SJB_AB_KERNELS
 // CTA-pair plan: pair R block = 512 rows, pair S tile = 128 rows.
 int make_pair_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) {
   namespace P = sjb::pair;
@@ -177,6 +193,7 @@ int make_pair_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   pl->seg_cap = (uint64_t)(a->cand_cap / pl->grid);
   return SJB_OK;
 }
+#endif
 
 int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   const int dev = current_device();
@@ -198,12 +215,19 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   if (pl->kpad > 128) {
     if (int rc = make_wide_plan(a, pl, sms, max_dyn_smem(dev))) return rc;
     if (a->sims_mode == 1) pl->wide_fused = false;   // pending lists need the separate recheck
+    if (!SJB_AB_KERNELS && pl->wide_fused) return ab_missing("SJB_WIDE_RECHECK=fused");
     return SJB_OK;
   }
+#if SJB_AB_KERNELS
   if (use_pair_filter()) return make_pair_plan(a, pl, sms, max_dyn_smem(dev));
+#else
+  if (use_pair_filter()) return ab_missing("SJB_FILTER=pair");
+#endif
   // the row-grouped recheck stages candidates in the output-sized key buffer
   pl->defer = use_deferred_recheck(a) && a->out_cap >= a->cand_cap;
   const char* fe = getenv("SJB_FILTER");
+  if (!SJB_AB_KERNELS && fe != nullptr && strcmp(fe, "ts") == 0) return ab_missing("SJB_FILTER=ts");
+#if SJB_AB_KERNELS
   if (fe != nullptr && strcmp(fe, "ts") == 0) {
     // R block in tensor memory (A/B): one shared-memory image + B stages.
     // cfg2 filter 16.8 ms vs 16.45 for the SS kernel (MMA-only 14.65 in
@@ -220,7 +244,9 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
     pl->a_tiles = 1;
     pl->smem = T::smem_layout(pl->kpad, stages).total;
     pl->n_ablk = (int)sjb::ceil_div(a->n_left, sjb::kTileRows);
-  } else {
+  } else
+#endif
+  {
   // Shared memory: the resident R block is one 256-row tile (two M=128
   // halves per S tile).  SJB_RBLOCK=512 selects two-tile blocks (four halves
   // per S tile: half the S traffic per MMA; cfg2 filter 14.55 vs 15.2 ms
@@ -230,6 +256,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   const int max_smem = max_dyn_smem(dev);
   const char* rbe = getenv("SJB_RBLOCK");
   int a_tiles = (rbe != nullptr && atoi(rbe) == 512) ? 2 : 1;
+  if (!SJB_AB_KERNELS && a_tiles == 2) return ab_missing("SJB_RBLOCK=512");
   int stages = 0, a_bufs = 2;
   for (;; a_tiles--) {
     for (a_bufs = 2; a_bufs >= 1; a_bufs--) {
@@ -342,14 +369,16 @@ int launch_filter_kat(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaSt
 }
 template <int KS>
 int launch_filter_ks(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
+#if SJB_AB_KERNELS
   if (jp.ts) {
     if (int rc = set_smem_attr((const void*)sjb::ts::filter_kernel<KS>, (int)smem)) return rc;
     sjb::ts::filter_kernel<KS><<<grid, sjb::ts::kThreads, smem, st>>>(jp);
     SJB_CK_LAUNCH("join_filter_ts");
     return SJB_OK;
   }
-  return jp.a_tiles == 2 ? launch_filter_kat<KS, 2>(jp, grid, smem, st)
-                         : launch_filter_kat<KS, 1>(jp, grid, smem, st);
+  if (jp.a_tiles == 2) return launch_filter_kat<KS, 2>(jp, grid, smem, st);
+#endif
+  return launch_filter_kat<KS, 1>(jp, grid, smem, st);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -407,6 +436,7 @@ int encode_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
   return SJB_OK;
 }
 
+#if SJB_AB_KERNELS
 template <int KS>
 int launch_pair_ks(const sjb::pair::Params& pp, int grid, uint32_t smem, cudaStream_t st) {
   if (int rc = set_smem_attr((const void*)sjb::pair::filter_kernel<KS>, (int)smem)) return rc;
@@ -428,6 +458,7 @@ int launch_pair_filter(const sjb::pair::Params& pp, int grid, uint32_t smem, cud
     default: return fail(SJB_E_UNSUPPORTED, "kpad %d", pp.kpad);
   }
 }
+#endif
 
 int launch_join_filter(const sjb::JoinParams& jp, int grid, uint32_t smem, cudaStream_t st) {
   switch (jp.kpad / 16) {
@@ -610,6 +641,8 @@ int sjb_prepare_bf16(const void* d_in, int64_t n, int64_t dim, float* d_out32, v
   SJB_CK_LAUNCH("prepare_bf16");
   return SJB_OK;
 }
+
+int sjb_ab_kernels(void) { return SJB_AB_KERNELS; }
 
 float sjb_raw_band(int64_t dim) {
   // exact bf16 products: fp32 accumulation of the tensor-core and canonical
@@ -836,7 +869,11 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
   if (tile_end > nt256) tile_end = nt256;
   if (tile_end <= tile_begin) return SJB_OK;
   // kernel tile units: 256 rows, or 128 for the CTA-pair kernel
+#if SJB_AB_KERNELS
   const int64_t unit = pl.pair ? sjb::kTileRows / sjb::pair::kUmmaN : 1;
+#else
+  const int64_t unit = 1;
+#endif
   const int64_t tb = tile_begin * unit;
   const int64_t te = tile_end * unit > pl.n_btiles ? pl.n_btiles : tile_end * unit;
   int tpc = 0;
@@ -927,10 +964,14 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       wp.tile_err = nullptr;
     }
     if (pl.wide_fused) {
+#if SJB_AB_KERNELS
       if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<true>, (int)pl.smem)) return rc;
       sjb::wide::filter_kernel<true>
           <<<pl.grid, sjb::wide::Cfg<true>::kThreads, pl.smem, st>>>(wp);
       SJB_CK_LAUNCH("wide_filter_fused");
+#else
+      return ab_missing("SJB_WIDE_RECHECK=fused");
+#endif
     } else {
       if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<false>, (int)pl.smem)) return rc;
       sjb::wide::filter_kernel<false>
@@ -973,9 +1014,13 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
           if (int rc = encode_rows_map(&tp.tmap_r, d_r32, nr, (int)args->dim)) return rc;
           const char* wr = getenv("SJB_WIDE_RECHECK");
           if (wr != nullptr && strcmp(wr, "tile") == 0) {  // A/B: A restaged per tile
+#if SJB_AB_KERNELS
             const int rs = (int)sjb::wide::recheck_tma_smem_bytes();
             if (int rc = set_smem_attr((const void*)sjb::wide::recheck_tma_kernel, rs)) return rc;
             sjb::wide::recheck_tma_kernel<<<pl.grid, sjb::wide::kRtThreads, rs, st>>>(tp);
+#else
+            return ab_missing("SJB_WIDE_RECHECK=tile");
+#endif
           } else {
             const int rs = (int)sjb::wide::recheck_group_smem_bytes();
             if (int rc = set_smem_attr((const void*)sjb::wide::recheck_group_kernel, rs)) return rc;
@@ -993,6 +1038,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       }
     }
   } else if (pl.pair) {
+#if SJB_AB_KERNELS
     sjb::pair::Params pp;
     pp.a16 = jp.a16;
     pp.b16 = jp.b16;
@@ -1023,6 +1069,9 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
     if (int rc = encode_operand_map(&pp.tmap_a, d_l16, nl, pl.kpad, sjb::pair::kARows)) return rc;
     if (int rc = encode_operand_map(&pp.tmap_b, d_r16, nr, pl.kpad, sjb::pair::kHalfN)) return rc;
     if (int rc = launch_pair_filter(pp, pl.grid, pl.smem, st)) return rc;
+#else
+    return ab_missing("SJB_FILTER=pair");
+#endif
   } else {
     const int lg = args->launch_grid > 0 && args->launch_grid < pl.grid ? args->launch_grid
                                                                          : pl.grid;

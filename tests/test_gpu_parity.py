@@ -167,6 +167,13 @@ def test_wide_recheck_variants(cuda, manifest, golden, monkeypatch, variant):
     """All wide recheck variants are exact: fused warps, the per-tile staged
     kernel, and the tile-group kernel (default) that reuses the A chunks."""
     from paper_2312_01476_b200 import device as D
+    if variant != "group":
+        meta0 = manifest["cases"]["c_d200"]
+        L0, S0 = case_inputs(meta0)
+        if _ab_gate(D, monkeypatch, ("SJB_WIDE_RECHECK", variant), lambda: D.join_prepared(
+                D.prepare(torch.from_numpy(L0).to(cuda)),
+                D.prepare(torch.from_numpy(S0).to(cuda)), meta0["theta"])):
+            return
     monkeypatch.setenv("SJB_WIDE_RECHECK", variant)
     for name in ("c_d200", "c_d768"):
         meta = manifest["cases"][name]
@@ -380,11 +387,29 @@ def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
 
 @pytest.mark.parametrize("variant", [("SJB_FILTER", "ts"), ("SJB_FILTER", "pair"),
                                      ("SJB_RBLOCK", "512")])
+def _ab_gate(D, monkeypatch, variant, call):
+    """The A/B kernels are built only with -DSJB_AB_KERNELS=1: in the default
+    library their switch must fail loudly (no silent fallback)."""
+    from paper_2312_01476_b200 import _lib
+    if _lib.lib().sjb_ab_kernels():
+        return False
+    monkeypatch.setenv(*variant)
+    with pytest.raises(_lib.SjbError, match="A/B kernel"):
+        call()
+    return True
+
+
 def test_filter_variants(cuda, manifest, golden, monkeypatch, variant):
     """d <= 128 filter kernels kept for A/B (TS-mode R block in tensor memory,
     CTA pair, two-tile R block) give the reference's bits on the golden cases,
     with and without the overflow retry, under both recheck placements."""
     from paper_2312_01476_b200 import device as D
+    meta0 = manifest["cases"]["c_small"]
+    L0, S0 = case_inputs(meta0)
+    if _ab_gate(D, monkeypatch, variant, lambda: D.join_prepared(
+            D.prepare(torch.from_numpy(L0).to(cuda)), D.prepare(torch.from_numpy(S0).to(cuda)),
+            meta0["theta"])):
+        return
     monkeypatch.setenv(*variant)
     for recheck in ("fused", "deferred"):
         monkeypatch.setenv("SJB_RECHECK", recheck)

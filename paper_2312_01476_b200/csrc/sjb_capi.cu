@@ -396,6 +396,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+#if SJB_AB_KERNELS
+
 // The 16-bit operand image (sjb_operand_elems elements, 256-row tiles of
 // [k-group][row][8]) as a 3-D tensor (256 elements = 32 rows x 8, 8 row
 // blocks, kgroups * tiles); box {256, box_rows/32, kgroups} = one
@@ -419,6 +421,7 @@ int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad,
   if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return SJB_OK;
 }
+#endif
 
 // fp32 canonical rows f32[n][dim] (dim % 4 == 0) as a 2-D tensor; box =
 // 32 elements x 256 rows = one K chunk of a tile, 128 B swizzle.

@@ -355,6 +355,12 @@ __device__ __forceinline__ float load_err(const float* e, int64_t i, int64_t n) 
   return (e != nullptr && i < n) ? __ldg(e + i) : 0.0f;
 }
 
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
                                                  uint32_t gi, uint32_t j0, int64_t col_lim,
                                                  uint32_t* cta_cnt, uint32_t* cta_sat,
@@ -466,44 +472,49 @@ __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
       mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
     }
   }
-  const uint32_t cnt = __popc(mk0) + __popc(mk1);
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t wtot = __reduce_add_sync(0xffffffffu, __popc(mk0) + __popc(mk1));
   uint32_t base = 0;
-  if (lane == 31 && wtot) {
+  if (lane == 0) {
     base = atomicAdd(cta_cnt, wtot);
     if (base + wtot < base) *cta_sat = 1u;
   }
-  base = __shfl_sync(0xffffffffu, base, 31);
-  uint64_t pos = (uint64_t)base + (incl - cnt);
+  uint64_t run = __shfl_sync(0xffffffffu, base, 0);
+  const uint32_t lt = lanemask_lt();
   uint32_t finals = 0;
 #pragma unroll
   for (int hh = 0; hh < 2; hh++) {
     uint32_t w = hh ? mk1 : mk0;
-    if (w == 0) continue;
+    if (w != 0u) {
 #pragma unroll
-    for (int k = 0; k < 4; k++)
-      if ((w >> (8 * k)) & 0xFFu) {
+      for (int k = 0; k < 4; k++)
+        if ((w >> (8 * k)) & 0xFFu) {
 #pragma unroll
-        for (int e = 0; e < 8; e++) scr[8 * k + e] = v[32 * hh + 8 * k + e];
+          for (int e = 0; e < 8; e++) scr[8 * k + e] = v[32 * hh + 8 * k + e];
+        }
+    }
+    // rounds of lane-interleaved, consecutive slots: round i writes the i-th
+    // hit of every lane that still has one, so each round is one coalesced
+    // store instead of 32 scattered ones (the pending recheck and the row
+    // bucketing are order-free; the canonical-sims group recheck prefers a
+    // row's candidates adjacent, so emit_row_chunk64 keeps per-lane runs)
+    for (;;) {
+      const bool act = w != 0u;
+      const uint32_t am = __ballot_sync(0xffffffffu, act);
+      if (am == 0u) break;
+      if (act) {
+        const int b = __ffs(w) - 1;
+        w &= w - 1;
+        const uint64_t pos = run + __popc(am & lt);
+        if (pos < seg_cap) {
+          const float x = scr[b];
+          seg[pos] = pack_pair(gi, j0 + 32 * hh + b);
+          const bool fin = x >= hi_cut;
+          sims[pos] = fin ? __float_as_uint(x) : kPending;
+          finals += fin ? 1u : 0u;
+          if (!fin) pend[atomicAdd(pend_cnt, 1u)] = (uint32_t)pos;
+        }
       }
-    while (w) {
-      const int b = __ffs(w) - 1;
-      w &= w - 1;
-      if (pos < seg_cap) {
-        const float x = scr[b];
-        seg[pos] = pack_pair(gi, j0 + 32 * hh + b);
-        const bool fin = x >= hi_cut;
-        sims[pos] = fin ? __float_as_uint(x) : kPending;
-        finals += fin ? 1u : 0u;
-        if (!fin) pend[atomicAdd(pend_cnt, 1u)] = (uint32_t)pos;
-      }
-      pos++;
+      run += __popc(am);
     }
   }
   return finals;

@@ -34,6 +34,10 @@
 // rowcount[i] counts the matches of left row i for sjb_post.cu's bucketing.
 #include "sjb_common.cuh"
 
+#ifndef SJB_EMIT_RUNS
+#define SJB_EMIT_RUNS 0
+#endif
+
 #ifndef SJB_PROFILE
 #define SJB_PROFILE 0
 #endif
@@ -324,14 +328,16 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
         }
       }
     };
-    // one warp's candidates: slots reserved with one shared atomic, pairs
-    // written in column order (mask bit b of word w = column 32w + b)
+    // one warp's candidates: slots reserved with one shared atomic; then
+    // round r writes the r-th candidate of every lane that still has one to
+    // consecutive slots (rank among the round's lanes), so a round is one
+    // coalesced store (SJB_EMIT_RUNS=1 at build: per-lane runs, round 1).
+    // Nothing downstream depends on the order inside a warp's slot range.
     auto emit = [&](const uint32_t (&mk)[4], uint32_t gi, uint32_t j0) {
       const uint32_t cnt = __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
+#if SJB_EMIT_RUNS
       uint64_t pos;
       if (__popc(__ballot_sync(0xffffffffu, cnt != 0)) <= 1) {
-        // common case (~1 candidate per hit chunk): the only lane with
-        // candidates reserves its own slots -- no scan, no broadcast
         uint32_t base = 0;
         if (cnt) {
           base = atomicAdd(cta_cnt, cnt);
@@ -364,6 +370,32 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_filter_kernel(const Join
           pos++;
         }
       }
+#else
+      const uint32_t wtot = __reduce_add_sync(0xffffffffu, cnt);
+      uint32_t base = 0;
+      if (lane == 0) {
+        base = atomicAdd(cta_cnt, wtot);
+        if (base + wtot < base) *cta_sat = 1u;
+      }
+      uint64_t run = __shfl_sync(0xffffffffu, base, 0);
+      const uint32_t lt = lanemask_lt();
+      uint32_t w0 = mk[0], w1 = mk[1], w2 = mk[2], w3 = mk[3];
+      for (;;) {
+        const bool act = (w0 | w1 | w2 | w3) != 0u;
+        const uint32_t am = __ballot_sync(0xffffffffu, act);
+        if (am == 0u) break;
+        if (act) {
+          int col;
+          if (w0) { col = __ffs(w0) - 1; w0 &= w0 - 1; }
+          else if (w1) { col = 32 + __ffs(w1) - 1; w1 &= w1 - 1; }
+          else if (w2) { col = 64 + __ffs(w2) - 1; w2 &= w2 - 1; }
+          else { col = 96 + __ffs(w3) - 1; w3 &= w3 - 1; }
+          const uint64_t pos = run + __popc(am & lt);
+          if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + col);
+        }
+        run += __popc(am);
+      }
+#endif
     };
     uint32_t tph = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {

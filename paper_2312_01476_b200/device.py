@@ -24,6 +24,7 @@ remembered, so repeated joins of the same shape run once.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import Dict, Optional, Tuple
@@ -734,9 +735,9 @@ class _Bounce:
     the GIL) while the copy engine drains the previous slot.  Slots are
     reused once their copy's event has fired."""
 
-    SLOT_BYTES = 16 << 20
-    N_SLOTS = 4
-    THREADS = 4
+    SLOT_BYTES = int(os.environ.get("SJB_BOUNCE_SLOT_MB", "16")) << 20
+    N_SLOTS = int(os.environ.get("SJB_BOUNCE_SLOTS", "4"))
+    THREADS = int(os.environ.get("SJB_BOUNCE_THREADS", "4"))
 
     def __init__(self):
         from concurrent.futures import ThreadPoolExecutor

@@ -385,8 +385,6 @@ def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
             assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
 
 
-@pytest.mark.parametrize("variant", [("SJB_FILTER", "ts"), ("SJB_FILTER", "pair"),
-                                     ("SJB_RBLOCK", "512")])
 def _ab_gate(D, monkeypatch, variant, call):
     """The A/B kernels are built only with -DSJB_AB_KERNELS=1: in the default
     library their switch must fail loudly (no silent fallback)."""
@@ -399,6 +397,8 @@ def _ab_gate(D, monkeypatch, variant, call):
     return True
 
 
+@pytest.mark.parametrize("variant", [("SJB_FILTER", "ts"), ("SJB_FILTER", "pair"),
+                                     ("SJB_RBLOCK", "512")])
 def test_filter_variants(cuda, manifest, golden, monkeypatch, variant):
     """d <= 128 filter kernels kept for A/B (TS-mode R block in tensor memory,
     CTA pair, two-tile R block) give the reference's bits on the golden cases,

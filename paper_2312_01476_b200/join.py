@@ -284,9 +284,11 @@ def _pinned(n: int, dtype) -> torch.Tensor:
 # Result bytes of the last host-input join of a shape: output-heavy joins
 # (cfg5 at theta 0.4: 1.6 GB of MatchSet against a 21 ms join) are bound by
 # the device->host copy of the result, which only starts once a part's join
-# is done, so they split the left rows into many equal parts instead.
+# is done, so they split the left rows into many equal parts instead
+# (cfg5 e2e 60 -> 33 ms).  Below 512 MB the three-part split wins: cfg2's
+# 107 MB result, 17.4 ms e2e, took 21.6 ms in eight parts.
 _result_bytes: dict = {}
-HEAVY_RESULT_BYTES = 64 << 20
+HEAVY_RESULT_BYTES = 512 << 20
 HEAVY_PARTS = 8
 
 
@@ -326,7 +328,8 @@ def _split_bounds_light(n: int, min_rows: int = 4096):
 
 def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
                      left_name: str, right_name: str, ready=None,
-                     heavy: bool = False) -> MatchSet:
+                     heavy: bool = False, PR: Optional[D.PreparedRelation] = None,
+                     sims: str = "exact") -> MatchSet:
     """Host-input join in `parts` left row ranges: the first streams S in
     (H2D overlapped with its filter); each later part is queued on the
     resident S before the previous part's count is read back, so the GPU
@@ -341,7 +344,10 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
         ready = lambda r: None                          # noqa: E731  (rows all prepared)
     if len(bounds) <= 2:
         ready(n)
-        m, _ = D.join_streamed(PL, right_host, theta, band)
+        if PR is not None:
+            m = D.join_prepared(PL, PR, theta, band, sims=sims)
+        else:
+            m, _ = D.join_streamed(PL, right_host, theta, band)
         return _to_matchset(m, left_name, right_name)
     dev = PL.device
     comp = torch.cuda.current_stream(dev)
@@ -376,13 +382,13 @@ def _join_host_split(PL: D.PreparedRelation, right_host, theta: float, band,
         state["done"] = done + k
 
     prev = None
-    PR = None
     for idx, (r0, r1) in enumerate(ranges):
         ready(r1)                                       # this part's left rows, normalised
         if PR is None:
             p, PR = D.join_streamed(PL.rows(r0, r1), right_host, theta, band, sync=False)
         else:
-            p = D.join_prepared_async(PL.rows(r0, r1), PR, theta, band, left_base=r0)
+            p = D.join_prepared_async(PL.rows(r0, r1), PR, theta, band, left_base=r0,
+                                      sims=sims)
         ev = torch.cuda.Event()
         ev.record(comp)
         if prev is not None:
@@ -426,8 +432,14 @@ def tensor_join_vectors(left: ArrayLike, right: ArrayLike, theta, *,
         with torch.cuda.device(dev):
             pl = D.prepare_bf16(left.to(dev, non_blocking=True))
             pr = D.prepare_bf16(right.to(dev, non_blocking=True))
-            m = D.join_prepared(pl, pr, t.value, band, sims=sims)
-            matches = _to_matchset(m, left_name, right_name)
+            if left.shape[0] >= HEAVY_PARTS * 4096:
+                # left rows in equal parts on the resident S: each part's
+                # matches copy to the host while the next part joins
+                matches = _join_host_split(pl, None, t.value, band, left_name, right_name,
+                                           heavy=True, PR=pr, sims=sims)
+            else:
+                m = D.join_prepared(pl, pr, t.value, band, sims=sims)
+                matches = _to_matchset(m, left_name, right_name)
         wall = time.perf_counter_ns() - t0
         return matches, JoinStats(wall_nanos=wall, model_calls_left=left.shape[0],
                                   model_calls_right=right.shape[0],

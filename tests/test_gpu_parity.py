@@ -887,3 +887,67 @@ def test_host_input_join_heavy_split(cuda, monkeypatch):
             ms, _ = J.tensor_join_vectors(lh, sh, theta, device=cuda)
             assert _bits_equal(ms, wl, wr, ws)
     assert max(J._result_bytes.values()) == len(wl) * 20
+
+
+@pytest.mark.parametrize("sims", ["exact", "tensor"])
+def test_bf16_vectors_api_in_parts(cuda, sims):
+    """tensor_join_vectors on bf16 host tensors with >= 8 x 4096 left rows:
+    the left rows join in 8 parts on the resident prepared S, each part's
+    matches copied out while the next joins; the same set as the oracle."""
+    from paper_2312_01476_b200.join import tensor_join_vectors
+    L, S = _bf16_case(33_000, 2_500, 256, 40, 0.6, 23)
+    theta = 0.8
+    wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+    assert len(wl) > 0
+    for pinned in (False, True):
+        lt, st = _bf16_tensor(L, "cpu"), _bf16_tensor(S, "cpu")
+        if pinned:
+            lt, st = lt.pin_memory(), st.pin_memory()
+        ms, stats = tensor_join_vectors(lt, st, theta, sims=sims, device=cuda)
+        assert stats.pairs_compared == len(L) * len(S)
+        assert np.array_equal(ms.lefts, wl) and np.array_equal(ms.rights, wr)
+        if sims == "exact":
+            assert np.array_equal(ms.sims.view(np.uint32), ws.view(np.uint32))
+        else:
+            assert np.abs(ms.sims.astype(np.float64) - ws).max() <= 1e-5
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_owner_prepared_layout_on_device(cuda, manifest, golden, world):
+    """The device side of multigpu.sharded_join_owned for `world` ranks on
+    one GPU: every rank's pieces prepared into the padded buffers at their
+    layout offsets (what the all-gathers deliver), then each rank's R shard
+    filtered round by round (reduced grid but the last round) -- the shards
+    concatenate to the golden cfg1 set, and the assembled prepared S equals
+    a one-shot prepare (rows, operand image, errors, tile maxima)."""
+    from paper_2312_01476_b200 import device as D
+    from paper_2312_01476_b200 import multigpu as MG
+    meta = manifest["cases"]["cfg1"]
+    L, S = case_inputs(meta)
+    lay = MG.piece_layout(len(S), world, rounds=3)
+    assert lay.rounds == 3 and lay.rows >= len(S)
+    Sd = torch.from_numpy(S).to(cuda)
+    PR = D.empty_prepared(len(S), S.shape[1], cuda, rows=lay.rows)
+    for k in range(world):
+        local = torch.from_numpy(MG.local_pieces(S, lay, k)).to(cuda)
+        off = 0
+        for _, a, b in lay.owned(k):
+            D.prepare_into(local[off:off + (b - a)], PR, a)
+            off += b - a
+    ref = D.prepare(Sd)
+    n = len(S)
+    assert torch.equal(PR.f32[:n], ref.f32)
+    assert torch.equal(PR.op[:ref.op.numel()].view(torch.int16), ref.op.view(torch.int16))
+    assert torch.equal(PR.row_err[:n], ref.row_err[:n])
+    assert torch.equal(PR.tile_err[:D.tile_count(n)], ref.tile_err[:D.tile_count(n)])
+    parts = []
+    for k in range(world):
+        r0, r1 = MG.shard_range(len(L), k, world)
+        sess = D.JoinSession(D.prepare(torch.from_numpy(L[r0:r1]).to(cuda)), PR, meta["theta"],
+                             None, r0)
+        for j in range(lay.rounds):
+            sess.filter_rows(*lay.round_rows(j), launch_grid=0 if j == lay.rounds - 1 else 100)
+        parts.append(sess.finish().result().to_host())
+    lo, ro, so = MG.concat_shards(parts)
+    assert np.array_equal(lo, golden["cfg1_l"]) and np.array_equal(ro, golden["cfg1_r"])
+    assert np.array_equal(so.view(np.uint32), golden["cfg1_s"].view(np.uint32))

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -114,6 +115,18 @@ bool use_deferred_recheck(const sjb_join_args* a) {
   if (f != nullptr && strcmp(f, "fused") == 0) return false;
   if (f != nullptr && strcmp(f, "deferred") == 0) return true;
   return a->recheck == 1;
+}
+
+// Deferred recheck through recheck_rows_kernel (sorted rows, bulk-copied S
+// rows) where its 1-D copies apply: dim % 4 == 0, 16-byte aligned rows;
+// SJB_DENSE_RECHECK=grouped keeps the per-lane gather kernel (A/B).
+constexpr int kRowsSmemMax = 227 * 1024;
+bool use_rows_recheck(const sjb_join_args* a, const float* l32, const float* r32) {
+  const char* f = getenv("SJB_DENSE_RECHECK");
+  if (f != nullptr && strcmp(f, "grouped") == 0) return false;
+  return a->dim % 4 == 0 && a->dim <= 128 &&
+         ((reinterpret_cast<uintptr_t>(l32) | reinterpret_cast<uintptr_t>(r32)) & 15) == 0 &&
+         sjb::rows_warp_smem((int)a->dim) <= kRowsSmemMax;
 }
 
 bool use_wide_fused() {
@@ -1093,6 +1106,45 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
   const int64_t nl = args->n_left;
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
   uint64_t* keys = c.keys;
+  if (pl.defer && use_rows_recheck(args, d_l32, d_r32)) {
+    // dense: group the candidates by left row; one warp per row sorts its
+    // right offsets, rechecks them with bulk-copied S rows and compacts the
+    // matches in place; then the match offsets and one copy to the columns
+    const dim3 sgrid(8, (unsigned)pl.grid);
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    SJB_CK_LAUNCH("count_rows");
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+    sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
+                                                  reinterpret_cast<unsigned long long*>(c.cursor),
+                                                  c.keys);
+    SJB_CK_LAUNCH("group_rows");
+    SJB_CK(cudaMemsetAsync(c.work, 0, 4, st));
+    const int dev = current_device();
+    const int per_warp = sjb::rows_warp_smem((int)args->dim);
+    const int nw = std::min(8, kRowsSmemMax / per_warp);
+    if (int rc = set_smem_attr((const void*)sjb::recheck_rows_kernel, nw * per_warp)) return rc;
+    sjb::recheck_rows_kernel<<<sjb_sm_count(dev), nw * 32, nw * per_warp, st>>>(
+        c.keys, c.rowoff, nl, d_l32, d_r32, (int)args->dim, args->theta, c.rowcount, c.work);
+    SJB_CK_LAUNCH("recheck_rows");
+    // match offsets into `cursor`; `rowoff` keeps the candidate offsets
+    if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
+    sjb::gate_kernel<<<1, 1, 0, st>>>(c.cursor, nl, args->out_cap, c.nbig);
+    SJB_CK_LAUNCH("gate");
+    sjb::emit_rows_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(
+        c.keys, c.rowoff, c.cursor, nl, d_lefts, d_rights, d_sims, c.cand, c.bigrows, c.nbig,
+        args->left_base);
+    SJB_CK_LAUNCH("emit_rows");
+    const int big_smem = sjb::kSortBigCap * 8;
+    if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
+    sjb::segsort_big_kernel<<<sjb_sm_count(dev), sjb::kSortBigThreads, big_smem, st>>>(
+        c.cursor, c.cand, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base,
+        args->n_right);
+    SJB_CK_LAUNCH("segsort_big");
+    sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.cursor, nl,
+                                                 args->out_cap, info);
+    SJB_CK_LAUNCH("finalize");
+    return SJB_OK;
+  }
   if (pl.defer) {
     // dense: group the candidates by left row, recheck them row-grouped,
     // then compact the matches by row (the segment buffer is free by then)

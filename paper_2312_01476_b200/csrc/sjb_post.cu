@@ -213,6 +213,211 @@ recheck_grouped_kernel(const uint64_t* __restrict__ grouped, const uint64_t* __r
   }
 }
 
+// ------------------------------------ dense recheck, sorted rows, TMA rows
+// The row-grouped recheck above gathers S rows with per-lane loads: every
+// load instruction touches 32 lines, so the kernel is bound by L1 wavefronts
+// (68% of peak, 6.3 ms at cfg5 theta = 0.4), and the row sort, the compaction
+// and the keys round trip after it cost 3.8 ms more.  Here one warp owns one
+// left row at a time (rows handed out by a global counter):
+//  * a row of n <= kRowSortCap candidates has its right offsets sorted
+//    ascending in registers (u32 bitonic) and parked in the warp's shared
+//    list, so the recheck already runs in canonical order;
+//  * batches of 32 candidates (lane p: candidate 32b + p): each lane's S row
+//    arrives by ONE 1-D bulk copy (TMA engine; no LSU gather wavefronts) in a
+//    double-buffered per-warp staging area while the previous batch runs its
+//    canonical chains (dot_seq_dev's fmaf order) from shared memory; the row
+//    pitch is an odd number of 16-byte units, so the lanes' 128-bit reads are
+//    conflict-free;
+//  * matches are written back IN PLACE, compacted, as (j << 32 | sim bits)
+//    at the row's candidate offset (writes trail the reads), and
+//    rowcount[i] = matches.
+// Rows above kRowSortCap candidates are rechecked in grouped order (the big
+// row sort orders them).  Requires dim % 4 == 0 and 16-byte aligned rows.
+constexpr int kRowSortCap = 1024;
+
+template <int E>
+__device__ __forceinline__ void warp_sort_u32(uint32_t (&v)[E]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j >= 1; j >>= 1) {
+      if (j >= 32) {
+        const int rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < E; r++) {
+          if (r & rj) continue;
+          const bool asc = ((32 * r + lane) & k) == 0;
+          const uint32_t x = v[r], y = v[r | rj];
+          const bool sw = asc ? (y < x) : (x < y);
+          v[r] = sw ? y : x;
+          v[r | rj] = sw ? x : y;
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < E; r++) {
+          const bool asc = ((32 * r + lane) & k) == 0;
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const uint32_t mnv = min(v[r], y), mxv = max(v[r], y);
+          v[r] = (asc == lower) ? mnv : mxv;
+        }
+      }
+    }
+  }
+}
+
+// keys[c0 .. c0 + n) low halves sorted into list[0 .. n) (n <= 32 E)
+template <int E>
+__device__ __forceinline__ void sort_row_js(const uint64_t* __restrict__ keys, uint64_t c0, int n,
+                                            uint32_t* list) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v[E];
+#pragma unroll
+  for (int r = 0; r < E; r++) {
+    const int t = 32 * r + lane;
+    v[r] = t < n ? (uint32_t)keys[c0 + t] : ~0u;
+  }
+  warp_sort_u32<E>(v);
+#pragma unroll
+  for (int r = 0; r < E; r++) list[32 * r + lane] = v[r];
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// dynamic shared memory per warp: 2 mbarriers, the sorted list, 2 x 32 rows
+__host__ __device__ inline int rows_pitch(int dim) { return ((dim / 4) & 1) ? dim : dim + 4; }
+__host__ __device__ inline int rows_warp_smem(int dim) {
+  return 16 + kRowSortCap * 4 + 2 * 32 * rows_pitch(dim) * 4;
+}
+
+__global__ void __launch_bounds__(256, 1)
+recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
+                    int64_t n_rows, const float* __restrict__ l32, const float* __restrict__ r32,
+                    int dim, float theta, uint32_t* __restrict__ rowcount,
+                    unsigned int* __restrict__ work) {
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pitch = rows_pitch(dim);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm) + 2 * warp;
+  uint32_t* list = reinterpret_cast<uint32_t*>(rsm + 16 * nw) + warp * kRowSortCap;
+  float* stage = reinterpret_cast<float*>(rsm + 16 * nw + (size_t)nw * kRowSortCap * 4) +
+                 (size_t)warp * 2 * 32 * pitch;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  fence_mbar_init();
+  __syncwarp();
+  const uint64_t pol = policy_evict_last();   // S rows: re-read by the rows of their cluster
+  const uint32_t rowbytes = (uint32_t)dim * 4;
+  const int nq = dim >> 2;
+  uint32_t phase = 0;
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(work, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if ((int64_t)i >= n_rows) break;
+    const uint64_t c0 = rowoff[i], n = rowoff[i + 1] - c0;
+    if (n == 0) {
+      if (lane == 0) rowcount[i] = 0u;
+      continue;
+    }
+    const bool small = n <= (uint64_t)kRowSortCap;
+    if (small) {
+      const int m = (int)n;
+      if (m <= 32) sort_row_js<1>(keys, c0, m, list);
+      else if (m <= 64) sort_row_js<2>(keys, c0, m, list);
+      else if (m <= 128) sort_row_js<4>(keys, c0, m, list);
+      else if (m <= 256) sort_row_js<8>(keys, c0, m, list);
+      else if (m <= 512) sort_row_js<16>(keys, c0, m, list);
+      else sort_row_js<32>(keys, c0, m, list);
+      __syncwarp();
+    }
+    const float4* a4 = reinterpret_cast<const float4*>(l32 + (size_t)i * dim);
+    const uint64_t nb = (n + 31) >> 5;
+    // batch b -> buffer b & 1; returns this lane's right offset
+    auto issue = [&](uint64_t b) -> uint32_t {
+      const int buf = (int)(b & 1);
+      const uint64_t k = b * 32 + lane;
+      const uint32_t cnt = (uint32_t)mn<uint64_t>(32, n - b * 32);
+      uint32_t j = 0;
+      if (k < n) j = small ? list[k] : (uint32_t)keys[c0 + k];
+      fence_proxy_async_smem();   // this buffer's previous reads precede the copy
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(bar + buf, cnt * rowbytes);
+      __syncwarp();
+      if (k < n)
+        bulk_g2s(stage + (size_t)(buf * 32 + lane) * pitch, r32 + (size_t)j * dim, rowbytes,
+                 bar + buf, pol);
+      return j;
+    };
+    uint32_t j_cur = issue(0);
+    uint32_t kept = 0;
+    for (uint64_t b = 0; b < nb; b++) {
+      const uint32_t j_next = b + 1 < nb ? issue(b + 1) : 0u;
+      const int buf = (int)(b & 1);
+      mbar_wait(bar + buf, (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      const uint64_t k = b * 32 + lane;
+      float x = 0.0f;
+      if (k < n) {
+        const float4* s4 = reinterpret_cast<const float4*>(stage + (size_t)(buf * 32 + lane) * pitch);
+#pragma unroll 5
+        for (int q = 0; q < nq; q++) {
+          const float4 s = s4[q], r = __ldg(a4 + q);
+          x = __fmaf_rn(r.x, s.x, x);
+          x = __fmaf_rn(r.y, s.y, x);
+          x = __fmaf_rn(r.z, s.z, x);
+          x = __fmaf_rn(r.w, s.w, x);
+        }
+      }
+      const bool ok = k < n && x >= theta;
+      const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) keys[c0 + kept + __popc(bal & lanemask_lt())] = (uint64_t(j_cur) << 32) | __float_as_uint(x);
+      kept += __popc(bal);
+      j_cur = j_next;
+    }
+    __syncwarp();
+    if (lane == 0) rowcount[i] = kept;
+  }
+}
+
+// Each row's matches (sorted, compacted at its candidate offset coff[i]) to
+// the MatchSet columns at its match offset moff[i]; rows that were too long
+// to sort go to the big-row list with their keys at moff[i] of bigkeys.
+__global__ void __launch_bounds__(256)
+emit_rows_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ coff,
+                 const uint64_t* __restrict__ moff, int64_t n_rows, uint64_t* __restrict__ lefts,
+                 uint64_t* __restrict__ rights, float* __restrict__ sims,
+                 uint64_t* __restrict__ bigkeys, uint32_t* __restrict__ big_rows,
+                 unsigned int* __restrict__ n_big, uint64_t left_base) {
+  if (n_big[1] == 0) return;  // gate: outputs would overflow
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n_rows;
+       i += (int64_t)gridDim.x * wpb) {
+    const uint64_t m0 = moff[i], kept = moff[i + 1] - m0;
+    if (kept == 0) continue;
+    const uint64_t c0 = coff[i];
+    if (coff[i + 1] - c0 > (uint64_t)kRowSortCap) {
+      if (lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
+      for (uint64_t t = lane; t < kept; t += 32) bigkeys[m0 + t] = keys[c0 + t];
+      continue;
+    }
+    const uint64_t ir = left_base + (uint64_t)i;
+    for (uint64_t t = lane; t < kept; t += 32) {
+      const uint64_t key = keys[c0 + t];
+      lefts[m0 + t] = ir;
+      rights[m0 + t] = key >> 32;
+      sims[m0 + t] = __uint_as_float((uint32_t)key);
+    }
+  }
+}
+
 // Matches of the grouped candidates into per-row runs (j << 32 | sim bits)
 // at the match offsets (cursor = row offsets), for the segmented sort.
 __global__ void compact_rows_kernel(const uint64_t* __restrict__ grouped,

@@ -367,12 +367,22 @@ def test_tensor_join_devices(cuda, manifest, golden):
         assert st.pairs_compared == len(L) * len(S) and st.matches == len(ms)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred"])
+def _set_recheck(monkeypatch, recheck):
+    """fused | deferred (sorted-row kernel with bulk-copied S rows) |
+    deferred-grouped (the per-lane gather kernel, kept for A/B)."""
+    monkeypatch.setenv("SJB_RECHECK", recheck.split("-")[0])
+    if recheck.endswith("-grouped"):
+        monkeypatch.setenv("SJB_DENSE_RECHECK", "grouped")
+    else:
+        monkeypatch.delenv("SJB_DENSE_RECHECK", raising=False)
+
+
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
 def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
-    """d <= 128: fused recheck warps and the deferred full-occupancy kernel
+    """d <= 128: fused recheck warps and the deferred full-occupancy kernels
     give the same bits (golden cases, overflow retry, theta = -1)."""
     from paper_2312_01476_b200 import device as D
-    monkeypatch.setenv("SJB_RECHECK", recheck)
+    _set_recheck(monkeypatch, recheck)
     for name in ("cfg1", "c_small", "c_all", "c_d16_neg"):
         meta = manifest["cases"][name]
         L, S = case_inputs(meta)
@@ -456,12 +466,12 @@ def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
         top_k(model, embed_relation(model, rel), rel, "p", 0)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred"])
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
 def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
     """Thousands of rows (several work items and S tiles per CTA, partial
     last tiles), dense and sparse thresholds, both recheck placements."""
     from paper_2312_01476_b200 import device as D
-    monkeypatch.setenv("SJB_RECHECK", recheck)
+    _set_recheck(monkeypatch, recheck)
     rng = np.random.default_rng(77)
     for inst in range(4):
         nl, nr = int(rng.integers(3000, 7000)), int(rng.integers(4000, 9000))
@@ -500,13 +510,14 @@ def test_budget_and_thread_invariance(cuda, manifest, golden):
         assert _bits_equal(ms, golden["c_ragged_l"], golden["c_ragged_r"], golden["c_ragged_s"])
 
 
-@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (200, "fused")])
+@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (16, "deferred-grouped"),
+                                         (200, "fused")])
 def test_nan_and_inf_rows(cuda, monkeypatch, dim, recheck):
     """Rows with NaN or +-Inf normalise to NaN rows (inf / inf) exactly as the
     reference's normalize_row; their similarities are NaN, so they match
     nothing -- the filter, the per-row band and the recheck must agree."""
     from paper_2312_01476_b200 import device as D
-    monkeypatch.setenv("SJB_RECHECK", recheck)
+    _set_recheck(monkeypatch, recheck)
     rng = np.random.default_rng(dim)
     L = rng.standard_normal((300, dim)).astype(np.float32)
     S = rng.standard_normal((400, dim)).astype(np.float32)

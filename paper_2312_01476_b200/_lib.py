@@ -13,7 +13,7 @@ from .build import LIB_PATH
 
 EXPORTS = (
     "sjb_version", "sjb_last_error", "sjb_launch_count", "sjb_sm_count", "sjb_kpad", "sjb_operand_elems",
-    "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_cast_rows", "sjb_prepare_bf16", "sjb_raw_band", "sjb_ab_kernels", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
+    "sjb_normalize_rows", "sjb_gather_normalize_rows", "sjb_cast_rows", "sjb_prepare_bf16", "sjb_raw_band", "sjb_ab_kernels", "sjb_debug_blk_stats", "sjb_row_norms", "sjb_fnv1a64_many", "sjb_synthetic_fill_many",
     "sjb_subword_embed", "sjb_join_workspace_bytes", "sjb_default_band", "sjb_accum_slack",
     "sjb_tile_count", "sjb_join_begin", "sjb_join_filter_tiles", "sjb_join_finish",
     "sjb_join_prepared_async", "sjb_join_prepared", "sjb_tile_dot", "sjb_dots_vm", "sjb_cosine_vm",
@@ -89,6 +89,7 @@ def lib(path: str = LIB_PATH):
     L.sjb_raw_band.argtypes = [_i64]
     L.sjb_raw_band.restype = ctypes.c_float
     L.sjb_ab_kernels.restype = ctypes.c_int
+    L.sjb_debug_blk_stats.argtypes = [_vp]
     L.sjb_fnv1a64_many.argtypes = [_vp, _vp, _i64, ctypes.c_uint64, _vp, _vp]
     L.sjb_synthetic_fill_many.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]
     L.sjb_subword_embed.argtypes = [_vp, _vp, _i64, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int,

@@ -126,7 +126,14 @@ bool use_rows_recheck(const sjb_join_args* a, const float* l32, const float* r32
   if (f != nullptr && strcmp(f, "grouped") == 0) return false;
   return a->dim % 4 == 0 && a->dim <= 128 &&
          ((reinterpret_cast<uintptr_t>(l32) | reinterpret_cast<uintptr_t>(r32)) & 15) == 0 &&
-         sjb::rows_warp_smem((int)a->dim) <= kRowsSmemMax;
+         sjb::rows_warp_smem((int)a->dim, false) + 128 <= kRowsSmemMax;
+}
+
+// Dense recheck variant (A/B): 0 cluster-blocked rows (default), 1 one warp
+// per sorted row (SJB_DENSE_RECHECK=rows); "grouped" = use_rows_recheck false.
+int dense_mode() {
+  const char* f = getenv("SJB_DENSE_RECHECK");
+  return (f != nullptr && strcmp(f, "rows") == 0) ? 1 : 0;
 }
 
 bool use_wide_fused() {
@@ -307,7 +314,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 // ------------------------------------------------------------ workspace
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
-      work, total;
+      work, sig, desc, total;
   size_t pend, pendn;
 };
 
@@ -333,6 +340,8 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   w.tiles = o;    o = align256(o + (size_t)grid * (size_t)tile_stride * 4);
   w.ncand = o;    o = align256(o + 16);
   w.work = o;     o = align256(o + 16);
+  w.sig = o;      o = align256(o + nl * 4);   // dense recheck: row signatures
+  w.desc = o;     o = align256(o + nl * 8);   // dense recheck: block descriptors
   // tolerance emission: per-CTA pending slot lists + counts
   const bool tol = a->sims_mode == 1;
   w.pend = o;     o = align256(o + (tol ? ccap * 4 : 0));
@@ -452,6 +461,22 @@ int encode_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
   return SJB_OK;
 }
 
+// fp32 rows f32[n][dim] (dim % 4 == 0, dim <= 256) for tile::gather4: box =
+// one whole row, no swizzle (recheck_rows_kernel).
+int encode_gather_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)dim * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)dim, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(rows), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled (gather rows) failed (%d)", (int)r);
+  return SJB_OK;
+}
+
 #if SJB_AB_KERNELS
 template <int KS>
 int launch_pair_ks(const sjb::pair::Params& pp, int grid, uint32_t smem, cudaStream_t st) {
@@ -531,6 +556,23 @@ __global__ void gate_kernel(const uint64_t* __restrict__ rowoff, int64_t n_left,
 extern "C" {
 
 int sjb_version(void) { return 1; }
+
+// Diagnostics of the cluster-blocked dense recheck (built with
+// -DSJB_BLK_STATS=1; otherwise returns SJB_E_UNSUPPORTED): copies the 8
+// counters and zeroes them.
+int sjb_debug_blk_stats(int64_t* out8) {
+#if SJB_BLK_STATS
+  unsigned long long h[8];
+  SJB_CK(cudaMemcpyFromSymbol(h, sjb::g_blk_stats, sizeof(h)));
+  for (int k = 0; k < 8; k++) out8[k] = (int64_t)h[k];
+  memset(h, 0, sizeof(h));
+  SJB_CK(cudaMemcpyToSymbol(sjb::g_blk_stats, h, sizeof(h)));
+  return SJB_OK;
+#else
+  (void)out8;
+  return fail(SJB_E_UNSUPPORTED, "built without SJB_BLK_STATS");
+#endif
+}
 
 int64_t sjb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -808,6 +850,8 @@ struct JoinCtx {
   uint32_t* tile_off;
   uint64_t* ncand;  // dense recheck: number of grouped candidates
   unsigned int* work;  // wide group recheck: dynamic item counter
+  uint32_t* sig;       // dense recheck: row signatures (smallest right offset)
+  uint64_t* desc;      // dense recheck: blocks (start | rows << 32)
   bool empty;  // n_left == 0 or n_right == 0
   uint32_t* pend;
   uint32_t* pend_count;
@@ -843,6 +887,8 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->tile_off = reinterpret_cast<uint32_t*>(ws + w.tiles);
   c->ncand = reinterpret_cast<uint64_t*>(ws + w.ncand);
   c->work = reinterpret_cast<unsigned int*>(ws + w.work);
+  c->sig = reinterpret_cast<uint32_t*>(ws + w.sig);
+  c->desc = reinterpret_cast<uint64_t*>(ws + w.desc);
   c->pend = reinterpret_cast<uint32_t*>(ws + w.pend);
   c->pend_count = reinterpret_cast<uint32_t*>(ws + w.pendn);
   return SJB_OK;
@@ -1106,6 +1152,63 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
   const int64_t nl = args->n_left;
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
   uint64_t* keys = c.keys;
+  if (pl.defer && use_rows_recheck(args, d_l32, d_r32) && dense_mode() == 0) {
+    // dense: group the candidates by left row, sort each row, order the rows
+    // by signature and recheck them in blocks of 32 (sjb_post.cu)
+    const dim3 sgrid(8, (unsigned)pl.grid);
+    const int dev = current_device();
+    const int sms = sjb_sm_count(dev);
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    SJB_CK_LAUNCH("count_rows");
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
+    sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
+                                                  reinterpret_cast<unsigned long long*>(c.cursor),
+                                                  c.keys);
+    SJB_CK_LAUNCH("group_rows");
+    sjb::sort_rows_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(c.keys, c.rowoff,
+                                                                                nl, c.sig);
+    SJB_CK_LAUNCH("sort_rows");
+    // rows grouped by signature (hashed over nl buckets), order in bigrows
+    const int shift = 0;
+    SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
+    const int fg = grid_for((uint64_t)nl, 256, 8);
+    sjb::sig_hist_kernel<<<fg, 256, 0, st>>>(c.sig, nl, shift, c.rowcount);
+    SJB_CK_LAUNCH("sig_hist");
+    if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
+    sjb::sig_scatter_kernel<<<fg, 256, 0, st>>>(
+        c.sig, nl, shift, reinterpret_cast<unsigned long long*>(c.cursor), c.bigrows);
+    SJB_CK_LAUNCH("sig_scatter");
+    SJB_CK(cudaMemsetAsync(c.work, 0, 8, st));   // [0] block counter, [1] blocks
+    sjb::sig_blocks_kernel<<<fg, 256, 0, st>>>(c.rowcount, c.cursor, nl, c.desc, c.work + 1);
+    SJB_CK_LAUNCH("sig_blocks");
+    const int bsmem = sjb::blk_smem_bytes((int)args->dim);
+    if (int rc = set_smem_attr((const void*)sjb::recheck_blocks_kernel, bsmem)) return rc;
+    int per_sm = 0;
+    SJB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sjb::recheck_blocks_kernel,
+                                                         sjb::kBlkThreads, bsmem));
+    sjb::recheck_blocks_kernel<<<sms * std::max(1, per_sm), sjb::kBlkThreads, bsmem, st>>>(
+        c.keys, c.rowoff, c.bigrows, c.desc, c.work + 1, d_l32, d_r32, (int)args->dim,
+        args->theta, c.sims_bits, c.rowcount, c.work);
+    SJB_CK_LAUNCH("recheck_blocks");
+    // match offsets into `cursor`; `rowoff` keeps the candidate offsets
+    if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
+    sjb::gate_kernel<<<1, 1, 0, st>>>(c.cursor, nl, args->out_cap, c.nbig);
+    SJB_CK_LAUNCH("gate");
+    sjb::emit_sims_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(
+        c.keys, c.sims_bits, c.rowoff, c.cursor, nl, d_lefts, d_rights, d_sims, c.cand,
+        c.bigrows, c.nbig, args->left_base);
+    SJB_CK_LAUNCH("emit_sims");
+    const int big_smem = sjb::kSortBigCap * 8;
+    if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
+    sjb::segsort_big_kernel<<<sms, sjb::kSortBigThreads, big_smem, st>>>(
+        c.cursor, c.cand, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base,
+        args->n_right);
+    SJB_CK_LAUNCH("segsort_big");
+    sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.cursor, nl,
+                                                 args->out_cap, info);
+    SJB_CK_LAUNCH("finalize");
+    return SJB_OK;
+  }
   if (pl.defer && use_rows_recheck(args, d_l32, d_r32)) {
     // dense: group the candidates by left row; one warp per row sorts its
     // right offsets, rechecks them with bulk-copied S rows and compacts the
@@ -1120,11 +1223,26 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     SJB_CK_LAUNCH("group_rows");
     SJB_CK(cudaMemsetAsync(c.work, 0, 4, st));
     const int dev = current_device();
-    const int per_warp = sjb::rows_warp_smem((int)args->dim);
-    const int nw = std::min(8, kRowsSmemMax / per_warp);
-    if (int rc = set_smem_attr((const void*)sjb::recheck_rows_kernel, nw * per_warp)) return rc;
-    sjb::recheck_rows_kernel<<<sjb_sm_count(dev), nw * 32, nw * per_warp, st>>>(
-        c.keys, c.rowoff, nl, d_l32, d_r32, (int)args->dim, args->theta, c.rowcount, c.work);
+    // S rows by tile::gather4 tensor copies (4 rows per copy) unless the map
+    // cannot be encoded or SJB_ROWS_G4=0 (per-lane 1-D copies, A/B)
+    CUtensorMap rmap;
+    const char* g4env = getenv("SJB_ROWS_G4");
+    const bool g4 = !(g4env && strcmp(g4env, "0") == 0) &&
+                    encode_gather_rows_map(&rmap, d_r32, args->n_right, (int)args->dim) == SJB_OK;
+    if (!g4) memset(&rmap, 0, sizeof(rmap));
+    const int per_warp = sjb::rows_warp_smem((int)args->dim, g4);
+    const int nw = std::min(8, (kRowsSmemMax - 128) / per_warp);
+    const void* fn = g4 ? (const void*)sjb::recheck_rows_kernel<true>
+                        : (const void*)sjb::recheck_rows_kernel<false>;
+    if (int rc = set_smem_attr(fn, nw * per_warp + 128)) return rc;
+    if (g4)
+      sjb::recheck_rows_kernel<true><<<sjb_sm_count(dev), nw * 32, nw * per_warp + 128, st>>>(
+          c.keys, c.rowoff, nl, d_l32, d_r32, (int)args->dim, args->theta, c.rowcount, c.work,
+          rmap);
+    else
+      sjb::recheck_rows_kernel<false><<<sjb_sm_count(dev), nw * 32, nw * per_warp + 128, st>>>(
+          c.keys, c.rowoff, nl, d_l32, d_r32, (int)args->dim, args->theta, c.rowcount, c.work,
+          rmap);
     SJB_CK_LAUNCH("recheck_rows");
     // match offsets into `cursor`; `rowoff` keeps the candidate offsets
     if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;

@@ -288,24 +288,54 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// dynamic shared memory per warp: 2 mbarriers, the sorted list, 2 x 32 rows
-__host__ __device__ inline int rows_pitch(int dim) { return ((dim / 4) & 1) ? dim : dim + 4; }
-__host__ __device__ inline int rows_warp_smem(int dim) {
-  return 16 + kRowSortCap * 4 + 2 * 32 * rows_pitch(dim) * 4;
+// Staging of one 32-candidate batch: 8 groups of 4 rows.  kG4: one
+// tile::gather4 tensor copy per group (lane 0 issues 8 per batch instead of
+// 32 per-lane 1-D copies, whose uniform-register operands make the compiler
+// loop over the lanes); a tensor copy's destination must be 128-byte
+// aligned, so groups are 128-byte padded (rows within a group at pitch dim).
+// Otherwise: per-lane 1-D bulk copies at a pitch of an odd number of 16-byte
+// units (conflict-free 128-bit reads).
+__host__ __device__ inline int rows_pitch(int dim, bool g4) {
+  return g4 ? dim : (((dim / 4) & 1) ? dim : dim + 4);
+}
+__host__ __device__ inline int rows_group_bytes(int dim, bool g4) {
+  return g4 ? (int)round_up(16 * dim, 128) : 16 * rows_pitch(dim, false);
+}
+// dynamic shared memory per warp: 2 batch buffers, 2 mbarriers, the sorted
+// list (+128 for aligning the staging area)
+__host__ __device__ inline int rows_warp_smem(int dim, bool g4) {
+  return 2 * 8 * rows_group_bytes(dim, g4) + 16 + kRowSortCap * 4;
 }
 
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int c, uint32_t r0,
+                                            uint32_t r1, uint32_t r2, uint32_t r3, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+template <bool kG4>
 __global__ void __launch_bounds__(256, 1)
 recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
                     int64_t n_rows, const float* __restrict__ l32, const float* __restrict__ r32,
                     int dim, float theta, uint32_t* __restrict__ rowcount,
-                    unsigned int* __restrict__ work) {
+                    unsigned int* __restrict__ work, const __grid_constant__ CUtensorMap rmap) {
   extern __shared__ __align__(16) uint8_t rsm[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pitch = rows_pitch(dim);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm) + 2 * warp;
-  uint32_t* list = reinterpret_cast<uint32_t*>(rsm + 16 * nw) + warp * kRowSortCap;
-  float* stage = reinterpret_cast<float*>(rsm + 16 * nw + (size_t)nw * kRowSortCap * 4) +
-                 (size_t)warp * 2 * 32 * pitch;
+  const int gbytes = rows_group_bytes(dim, kG4), bufbytes = 8 * gbytes;
+  const int pitch = rows_pitch(dim, kG4);
+  // staging first (128-byte aligned), then mbarriers, then the lists
+  uint8_t* base = rsm + ((128 - (smem_u32(rsm) & 127)) & 127);
+  uint8_t* stage = base + (size_t)warp * 2 * bufbytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + (size_t)nw * 2 * bufbytes) + 2 * warp;
+  uint32_t* list = reinterpret_cast<uint32_t*>(base + (size_t)nw * 2 * bufbytes + 16 * nw) +
+                   warp * kRowSortCap;
+  // lane p's row in buffer b: group p / 4, row p % 4
+  uint8_t* myrow0 = stage + (lane >> 2) * gbytes + (lane & 3) * pitch * 4;
+  auto myrow = [&](int buf) { return reinterpret_cast<float*>(myrow0 + buf * bufbytes); };
   if (lane == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
@@ -348,11 +378,28 @@ recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ ro
       if (k < n) j = small ? list[k] : (uint32_t)keys[c0 + k];
       fence_proxy_async_smem();   // this buffer's previous reads precede the copy
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(bar + buf, cnt * rowbytes);
-      __syncwarp();
-      if (k < n)
-        bulk_g2s(stage + (size_t)(buf * 32 + lane) * pitch, r32 + (size_t)j * dim, rowbytes,
-                 bar + buf, pol);
+      if (kG4) {
+        // pad the last group with its first row (copied, never read)
+        const uint32_t jp = __shfl_sync(0xffffffffu, j, (int)((cnt - 1) & ~3u));
+        if (k >= n) j = jp;
+        const uint32_t groups = (cnt + 3) >> 2;
+        if (lane == 0) mbar_arrive_expect_tx(bar + buf, groups * 4 * rowbytes);
+#pragma unroll
+        for (int g = 0; g < 8; g++) {
+          const uint32_t j0 = __shfl_sync(0xffffffffu, j, 4 * g);
+          const uint32_t j1 = __shfl_sync(0xffffffffu, j, 4 * g + 1);
+          const uint32_t j2 = __shfl_sync(0xffffffffu, j, 4 * g + 2);
+          const uint32_t j3 = __shfl_sync(0xffffffffu, j, 4 * g + 3);
+          if (lane == 0 && (uint32_t)g < groups)
+            tma_gather4(stage + buf * bufbytes + g * gbytes, &rmap, 0, j0, j1, j2, j3, bar + buf,
+                        pol);
+        }
+      } else {
+        if (lane == 0) mbar_arrive_expect_tx(bar + buf, cnt * rowbytes);
+        __syncwarp();
+        if (k < n)
+          bulk_g2s(myrow(buf), r32 + (size_t)j * dim, rowbytes, bar + buf, pol);
+      }
       return j;
     };
     uint32_t j_cur = issue(0);
@@ -365,7 +412,7 @@ recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ ro
       const uint64_t k = b * 32 + lane;
       float x = 0.0f;
       if (k < n) {
-        const float4* s4 = reinterpret_cast<const float4*>(stage + (size_t)(buf * 32 + lane) * pitch);
+        const float4* s4 = reinterpret_cast<const float4*>(myrow(buf));
 #pragma unroll 5
         for (int q = 0; q < nq; q++) {
           const float4 s = s4[q], r = __ldg(a4 + q);
@@ -418,6 +465,424 @@ emit_rows_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
   }
 }
 
+// ----------------------------------- dense recheck, cluster-blocked rows
+// The staged per-candidate recheck above is bound by the bytes it can keep
+// in flight from L2 (32 GB of S rows at cfg5 theta = 0.4, ~5 ms).  Dense
+// joins of clustered data re-read the same S rows: the left rows of one
+// cluster match (nearly) the same right rows.  So:
+//  1. sort_rows: each row's candidates sorted by right offset in place (the
+//     canonical order), and the row's signature = its smallest right offset;
+//  2. rows grouped by signature (counting sort over hashed buckets: bucket,
+//     scan, scatter), so consecutive rows tend to share their candidates;
+//  3. recheck_blocks: a CTA takes up to 32 consecutive rows of one bucket, builds
+//     the UNION of their right offsets (shared-memory hash set, then sorted),
+//     and -- when the block is dense (candidates >= kBlkDense x rows x union)
+//     -- stages each union S row ONCE (1-D bulk copies) and the 32 R rows,
+//     and runs the canonical chains with lane = left row and the S row a
+//     shared-memory broadcast: four union rows per step (independent chains,
+//     the R row's 128-bit read shared), every read conflict-free.  The
+//     similarity goes to the candidate's slot of the sorted row: its rank =
+//     the candidates of the row before it in the union (a running count per
+//     lane).  Sparse blocks (or unions above kBlkUnion) run the per-candidate
+//     staged recheck instead, one warp per row;
+//  4. emit_sims: per row, the rechecked slots compacted into the MatchSet.
+template <bool kWarp, class T>
+__device__ void smem_bitonic(T* s, int n, int tid, int nthr);
+
+constexpr int kBlkRows = 32;
+constexpr int kBlkThreads = 256;
+constexpr int kBlkWarps = kBlkThreads / 32;
+constexpr int kBlkHashBits = 12;
+constexpr int kBlkHash = 1 << kBlkHashBits;   // holds <= kBlkUnion + kBlkThreads keys
+constexpr int kBlkUnion = 1024;
+constexpr float kBlkDense = 0.25f;
+constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;
+#ifndef SJB_BLK_STATS
+#define SJB_BLK_STATS 0
+#endif
+#if SJB_BLK_STATS
+// diagnostics (-DSJB_BLK_STATS=1): dense / big / union-overflow / low-density
+// blocks, candidates in dense and sparse blocks, summed dense unions
+__device__ unsigned long long g_blk_stats[8];
+#endif
+
+// candidates of row i sorted in place; sig[i] = smallest right offset (rows
+// of 1 .. kRowSortCap candidates), ~0 otherwise (empty and unsorted big rows)
+__global__ void __launch_bounds__(256)
+sort_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff, int64_t n_rows,
+                 uint32_t* __restrict__ sig) {
+  __shared__ uint32_t lists[8][kRowSortCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* list = lists[warp];
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n_rows; i += (int64_t)gridDim.x * 8) {
+    const uint64_t c0 = rowoff[i], n = rowoff[i + 1] - c0;
+    if (n == 0 || n > (uint64_t)kRowSortCap) {
+      if (lane == 0) sig[i] = ~0u;
+      continue;
+    }
+    const int m = (int)n;
+    if (m <= 32) sort_row_js<1>(keys, c0, m, list);
+    else if (m <= 64) sort_row_js<2>(keys, c0, m, list);
+    else if (m <= 128) sort_row_js<4>(keys, c0, m, list);
+    else if (m <= 256) sort_row_js<8>(keys, c0, m, list);
+    else if (m <= 512) sort_row_js<16>(keys, c0, m, list);
+    else sort_row_js<32>(keys, c0, m, list);
+    __syncwarp();
+    const uint64_t hi = (uint64_t)i << 32;
+    for (int t = lane; t < m; t += 32) keys[c0 + t] = hi | list[t];
+    if (lane == 0) sig[i] = list[0];
+    __syncwarp();
+  }
+}
+
+// Rows are grouped, not sorted, by signature: bucket = a multiplicative hash
+// of it over nbk - 1 buckets (the last one for big and empty rows).  Equal
+// signatures share a bucket; distinct ones rarely do (k distinct signatures
+// collide ~k^2 / 2 nbk times), whereas contiguous ranges of signatures would
+// merge clusters whose smallest members are neighbours -- and the rows of a
+// shared bucket interleave, so every block of two such clusters overflows.
+__device__ __forceinline__ uint32_t sig_bucket(uint32_t s, int shift, int64_t nbk) {
+  (void)shift;
+  if (nbk < 2) return 0u;
+  if (s == ~0u) return (uint32_t)(nbk - 1);
+  const uint32_t h = (uint32_t)(((uint64_t)s * 0x9E3779B97F4A7C15ull) >> 32);
+  return (uint32_t)(((uint64_t)h * (uint64_t)(nbk - 1)) >> 32);
+}
+__global__ void sig_hist_kernel(const uint32_t* __restrict__ sig, int64_t n, int shift,
+                                uint32_t* __restrict__ hist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(hist + sig_bucket(sig[i], shift, n), 1u);
+}
+__global__ void sig_scatter_kernel(const uint32_t* __restrict__ sig, int64_t n, int shift,
+                                   unsigned long long* __restrict__ cursor,
+                                   uint32_t* __restrict__ perm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    perm[atomicAdd(cursor + sig_bucket(sig[i], shift, n), 1ull)] = (uint32_t)i;
+}
+
+// Blocks never span two buckets: bucket b (rows [end_b - cnt_b, end_b) of
+// the order, `cursor` holding the ends after the scatter) becomes
+// ceil(cnt_b / 32) blocks, appended in any order: desc = start | count << 32.
+__global__ void sig_blocks_kernel(const uint32_t* __restrict__ hist,
+                                  const uint64_t* __restrict__ ends, int64_t nbk,
+                                  uint64_t* __restrict__ desc, unsigned int* __restrict__ n_desc) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t cnt = hist[b];
+    if (cnt == 0) continue;
+    const uint64_t start = ends[b] - cnt;
+    const uint32_t nb = (cnt + kBlkRows - 1) / kBlkRows;
+    const uint32_t base = atomicAdd(n_desc, nb);
+    for (uint32_t k = 0; k < nb; k++)
+      desc[base + k] = (start + (uint64_t)k * kBlkRows) |
+                       ((uint64_t)mn<uint32_t>(kBlkRows, cnt - k * kBlkRows) << 32);
+  }
+}
+
+// shared memory: staging area of kBlkStage rows (sparse: warps 0..5 x 32
+// rows; dense: 32 R rows + a window of 168 union S rows), then the fixed
+// part (33 KB): 113 KB at d = 100, two CTAs per SM
+constexpr int kBlkStage = 200;
+constexpr int kBlkSparseWarps = kBlkStage / 32;
+static_assert(kBlkStage + kBlkRows <= kBlkThreads, "one copy-issuing thread per staged row");
+__host__ __device__ inline int blk_stage_bytes(int dim) {
+  return kBlkStage * rows_pitch(dim, false) * 4;
+}
+__host__ __device__ inline int blk_window_rows(int dim) { return kBlkStage - kBlkRows; }
+struct BlkShared {
+  uint32_t hkeys[kBlkHash];
+  uint16_t hidx[kBlkHash];
+  uint32_t uniq[kBlkUnion];
+  uint32_t mask[kBlkUnion];
+  uint64_t c0[kBlkRows];
+  uint32_t n[kBlkRows], row[kBlkRows], kept[kBlkRows], rank[2][kBlkRows];
+  uint64_t sbar[kBlkWarps];
+  uint64_t dbar;
+  uint32_t item, count, ucnt, ovf, big, cand;
+};
+__host__ __device__ inline int blk_smem_bytes(int dim) {
+  return blk_stage_bytes(dim) + (int)sizeof(BlkShared) + 16;
+}
+
+__global__ void __launch_bounds__(kBlkThreads)
+recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
+                      const uint32_t* __restrict__ perm, const uint64_t* __restrict__ desc,
+                      const unsigned int* __restrict__ n_desc,
+                      const float* __restrict__ l32, const float* __restrict__ r32, int dim,
+                      float theta, uint32_t* __restrict__ sims_out,
+                      uint32_t* __restrict__ rowcount, unsigned int* __restrict__ work) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int pitch = rows_pitch(dim, false), nq = dim >> 2;
+  const uint32_t rowbytes = (uint32_t)dim * 4;
+  float* stage = reinterpret_cast<float*>(bsm);
+  BlkShared& sh = *reinterpret_cast<BlkShared*>(bsm + blk_stage_bytes(dim));
+  const int win = blk_window_rows(dim);
+  if (tid < kBlkWarps) mbar_init(&sh.sbar[tid], 1);
+  if (tid == 0) mbar_init(&sh.dbar, 1);
+  fence_mbar_init();
+  __syncthreads();
+  const uint64_t pol = policy_evict_last();
+  uint32_t sphase = 0, dphase = 0;
+  for (;;) {
+    if (tid == 0) sh.item = atomicAdd(work, 1u);
+    if (tid < kBlkRows) sh.kept[tid] = 0u;
+    __syncthreads();
+    if (sh.item >= *n_desc) break;
+    const uint64_t dsc = desc[sh.item];
+    const int64_t p0 = (int64_t)(uint32_t)dsc;
+    const int nrows = (int)(dsc >> 32);
+    if (tid < kBlkRows) {
+      uint32_t i = 0, n = 0;
+      uint64_t c0 = 0;
+      if (tid < nrows) {
+        i = perm[p0 + tid];
+        c0 = rowoff[i];
+        n = (uint32_t)mn<uint64_t>(rowoff[i + 1] - c0, 0xFFFFFFFFull);
+      }
+      sh.row[tid] = i;
+      sh.c0[tid] = c0;
+      sh.n[tid] = n;
+      // block totals (warp 0)
+      const uint32_t cand = __reduce_add_sync(0xffffffffu, mn<uint32_t>(n, 1u << 20));
+      const bool big = __any_sync(0xffffffffu, n > (uint32_t)kRowSortCap);
+      if (tid == 0) {
+        sh.cand = cand;
+        sh.big = big ? 1u : 0u;
+        sh.count = 0u;
+        sh.ovf = big ? 1u : 0u;
+      }
+    }
+    for (int h = tid; h < kBlkHash; h += kBlkThreads) sh.hkeys[h] = kHashEmpty;
+    __syncthreads();
+    // ---- union of the block's right offsets (hash set; gives up above
+    // kBlkUnion).  Each lane loads four candidates before inserting them, so
+    // the global loads overlap.
+    auto hash_of = [](uint32_t j) { return (j * 0x9E3779B1u) >> (32 - kBlkHashBits); };
+    auto for_block_js = [&](auto&& fn) {
+      for (int r = warp; r < nrows; r += kBlkWarps) {
+        const uint64_t c0 = sh.c0[r];
+        const uint32_t n = sh.n[r];
+        for (uint32_t t0 = lane; t0 < n; t0 += 128) {
+          uint32_t j[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) j[e] = t0 + 32 * e < n ? (uint32_t)keys[c0 + t0 + 32 * e] : 0u;
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (t0 + 32 * e < n) fn(r, j[e]);
+        }
+      }
+    };
+    if (!sh.ovf) {
+      for_block_js([&](int, uint32_t j) {
+        uint32_t h = hash_of(j);
+        for (;;) {
+          if (*(volatile uint32_t*)&sh.ovf) break;
+          const uint32_t prev = atomicCAS(&sh.hkeys[h], kHashEmpty, j);
+          if (prev == kHashEmpty) {
+            if (atomicAdd(&sh.count, 1u) >= (uint32_t)kBlkUnion) sh.ovf = 1u;
+            break;
+          }
+          if (prev == j) break;
+          h = (h + 1) & (kBlkHash - 1);
+        }
+      });
+    }
+    __syncthreads();
+    const uint32_t U = sh.count;
+    const bool dense = !sh.ovf && U > 0 && (float)sh.cand >= kBlkDense * (float)nrows * (float)U;
+#if SJB_BLK_STATS
+    if (tid == 0) {
+      atomicAdd(&g_blk_stats[dense ? 0 : (sh.big ? 1 : (sh.ovf ? 2 : 3))], 1ull);
+      atomicAdd(&g_blk_stats[dense ? 4 : 5], (unsigned long long)sh.cand);
+      if (dense) atomicAdd(&g_blk_stats[6], (unsigned long long)U);
+    }
+#endif
+    if (dense) {
+      // compact the set into uniq[0..U), sort it (ascending right offsets)
+      // and record each key's sorted index in its hash slot
+      if (tid == 0) sh.ucnt = 0u;
+      __syncthreads();
+      for (int h = tid; h < kBlkHash; h += kBlkThreads) {
+        const uint32_t k = sh.hkeys[h];
+        if (k != kHashEmpty) sh.uniq[atomicAdd(&sh.ucnt, 1u)] = k;
+      }
+      for (uint32_t u = tid; u < U; u += kBlkThreads) sh.mask[u] = 0u;
+      __syncthreads();
+      smem_bitonic<false>(sh.uniq, (int)U, tid, kBlkThreads);
+      __syncthreads();
+      for (uint32_t u = tid; u < U; u += kBlkThreads) {
+        const uint32_t j = sh.uniq[u];
+        uint32_t h = hash_of(j);
+        while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
+        sh.hidx[h] = (uint16_t)u;
+      }
+      __syncthreads();
+      // membership masks: bit r of mask[u] <=> (row r, uniq[u]) is a candidate
+      for_block_js([&](int r, uint32_t j) {
+        uint32_t h = hash_of(j);
+        while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
+        atomicOr(&sh.mask[sh.hidx[h]], 1u << r);
+      });
+      if (tid < kBlkRows) sh.rank[0][tid] = 0u;
+      int wpar = 0;
+      const float* Rs = stage;
+      const float* Ss = stage + (size_t)kBlkRows * pitch;
+      for (uint32_t u0 = 0; u0 < U; u0 += (uint32_t)win) {
+        const uint32_t u1 = mn<uint32_t>(U, u0 + (uint32_t)win);
+        fence_proxy_async_smem();
+        __syncthreads();   // masks complete / the previous window consumed
+        if (tid == 0)
+          mbar_arrive_expect_tx(&sh.dbar, (u1 - u0) * rowbytes + (u0 == 0 ? nrows * rowbytes : 0u));
+        __syncthreads();
+        if (tid < (int)(u1 - u0))
+          bulk_g2s(stage + (size_t)(kBlkRows + tid) * pitch,
+                   r32 + (size_t)(uint32_t)sh.uniq[u0 + tid] * dim, rowbytes, &sh.dbar, pol);
+        if (u0 == 0 && tid >= kBlkStage && tid - kBlkStage < nrows) {
+          const int r = tid - kBlkStage;
+          bulk_g2s(stage + (size_t)r * pitch, l32 + (size_t)sh.row[r] * dim, rowbytes, &sh.dbar,
+                   pol);
+        }
+        mbar_wait(&sh.dbar, dphase);
+        dphase ^= 1u;
+        // warp w: union rows [ua, ub) of the window, four at a time; lane = row
+        const uint32_t span = u1 - u0;
+        const uint32_t ua = u0 + span * warp / kBlkWarps, ub = u0 + span * (warp + 1) / kBlkWarps;
+        uint32_t rank = sh.rank[wpar][lane];
+        for (uint32_t u = u0; u < ua; u++) rank += (sh.mask[u] >> lane) & 1u;
+        uint32_t kept = 0;
+        const float4* R4 = reinterpret_cast<const float4*>(Rs + (size_t)lane * pitch);
+        const uint64_t c0 = sh.c0[lane];
+        for (uint32_t u = ua; u < ub; u += 4) {
+          uint32_t m[4];
+          const float4* S4[4];
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            const uint32_t uc = u + c < ub ? u + c : u;
+            m[c] = u + c < ub ? sh.mask[uc] : 0u;
+            S4[c] = reinterpret_cast<const float4*>(Ss + (size_t)(uc - u0) * pitch);
+          }
+          if ((m[0] | m[1] | m[2] | m[3]) == 0u) continue;
+          float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 5
+          for (int q = 0; q < nq; q++) {
+            const float4 a = R4[q];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+              const float4 b = S4[c][q];
+              x[c] = __fmaf_rn(a.x, b.x, x[c]);
+              x[c] = __fmaf_rn(a.y, b.y, x[c]);
+              x[c] = __fmaf_rn(a.z, b.z, x[c]);
+              x[c] = __fmaf_rn(a.w, b.w, x[c]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            if ((m[c] >> lane) & 1u) {
+              const bool ok = x[c] >= theta;
+              sims_out[c0 + rank] = ok ? __float_as_uint(x[c]) : kRejected;
+              rank++;
+              kept += ok ? 1u : 0u;
+            }
+          }
+        }
+        if (kept) atomicAdd(&sh.kept[lane], kept);
+        // the rank at the window's end, for the next window (other parity:
+        // this window's readers may still be reading theirs)
+        if (warp == kBlkWarps - 1) sh.rank[wpar ^ 1][lane] = rank;
+        wpar ^= 1;
+      }
+    } else {
+      // ---- sparse block: per-candidate staged recheck, one warp per row
+      float* buf = stage + (size_t)warp * 32 * pitch;
+      float* myrow = buf + (size_t)lane * pitch;
+      for (int r = warp; r < nrows && warp < kBlkSparseWarps; r += kBlkSparseWarps) {
+        const uint64_t c0 = sh.c0[r];
+        const uint32_t n = sh.n[r];
+        const float4* a4 = reinterpret_cast<const float4*>(l32 + (size_t)sh.row[r] * dim);
+        uint32_t kept = 0;
+        for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+          const uint32_t k = b0 + lane, cnt = mn<uint32_t>(32u, n - b0);
+          const uint32_t j = k < n ? (uint32_t)keys[c0 + k] : 0u;
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(&sh.sbar[warp], cnt * rowbytes);
+          __syncwarp();
+          if (k < n) bulk_g2s(myrow, r32 + (size_t)j * dim, rowbytes, &sh.sbar[warp], pol);
+          mbar_wait(&sh.sbar[warp], sphase);
+          sphase ^= 1u;
+          if (k < n) {
+            const float4* s4 = reinterpret_cast<const float4*>(myrow);
+            float x = 0.0f;
+#pragma unroll 5
+            for (int q = 0; q < nq; q++) {
+              const float4 s = s4[q], a = __ldg(a4 + q);
+              x = __fmaf_rn(a.x, s.x, x);
+              x = __fmaf_rn(a.y, s.y, x);
+              x = __fmaf_rn(a.z, s.z, x);
+              x = __fmaf_rn(a.w, s.w, x);
+            }
+            const bool ok = x >= theta;
+            sims_out[c0 + k] = ok ? __float_as_uint(x) : kRejected;
+            kept += ok ? 1u : 0u;
+          }
+        }
+        kept = __reduce_add_sync(0xffffffffu, kept);
+        if (lane == 0) sh.kept[r] = kept;
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid < nrows) rowcount[sh.row[tid]] = sh.kept[tid];
+  }
+}
+
+// Rechecked candidate slots (sorted rows; sims_bits or kRejected) compacted
+// into the MatchSet columns at the match offsets moff; big rows (unsorted)
+// go to the big-row list with (j << 32 | sim) keys at moff of bigkeys.
+__global__ void __launch_bounds__(256)
+emit_sims_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sims_bits,
+                 const uint64_t* __restrict__ coff, const uint64_t* __restrict__ moff,
+                 int64_t n_rows, uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
+                 float* __restrict__ sims, uint64_t* __restrict__ bigkeys,
+                 uint32_t* __restrict__ big_rows, unsigned int* __restrict__ n_big,
+                 uint64_t left_base) {
+  if (n_big[1] == 0) return;  // gate: outputs would overflow
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n_rows;
+       i += (int64_t)gridDim.x * wpb) {
+    const uint64_t m0 = moff[i];
+    if (moff[i + 1] == m0) continue;
+    const uint64_t c0 = coff[i], n = coff[i + 1] - c0;
+    const bool big = n > (uint64_t)kRowSortCap;
+    if (big && lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
+    const uint64_t ir = left_base + (uint64_t)i;
+    uint64_t run = m0;
+    for (uint64_t t0 = 0; t0 < n; t0 += 32) {
+      const uint64_t t = t0 + lane;
+      const uint32_t sb = t < n ? sims_bits[c0 + t] : kRejected;
+      const bool ok = sb != kRejected;
+      const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const uint64_t pos = run + __popc(bal & lt);
+        const uint32_t j = (uint32_t)keys[c0 + t];
+        if (big) {
+          bigkeys[pos] = (uint64_t(j) << 32) | sb;
+        } else {
+          lefts[pos] = ir;
+          rights[pos] = j;
+          sims[pos] = __uint_as_float(sb);
+        }
+      }
+      run += __popc(bal);
+    }
+  }
+}
+
 // Matches of the grouped candidates into per-row runs (j << 32 | sim bits)
 // at the match offsets (cursor = row offsets), for the segmented sort.
 __global__ void compact_rows_kernel(const uint64_t* __restrict__ grouped,
@@ -462,8 +927,9 @@ __global__ void scatter_kernel(const uint64_t* __restrict__ cand, uint64_t seg_c
 // Bitonic network in its "mirror" form: every compare-exchange puts the
 // smaller key at the lower index, so a segment of any length sorts with
 // virtual +inf padding that never moves.
-__device__ __forceinline__ void cmpx(uint64_t* s, int a, int b) {
-  uint64_t x = s[a], y = s[b];
+template <class T>
+__device__ __forceinline__ void cmpx(T* s, int a, int b) {
+  T x = s[a], y = s[b];
   if (y < x) {
     s[a] = y;
     s[b] = x;
@@ -479,8 +945,8 @@ __device__ __forceinline__ void nsync() {
 
 // k and j are powers of two: block/offset by shift and mask (a runtime
 // integer division per compare-exchange dominated the sort).
-template <bool kWarp>
-__device__ void smem_bitonic(uint64_t* s, int n, int tid, int nthr) {
+template <bool kWarp, class T>
+__device__ void smem_bitonic(T* s, int n, int tid, int nthr) {
   int P = 1, lp = 0;
   while (P < n) {
     P <<= 1;

@@ -368,16 +368,18 @@ def test_tensor_join_devices(cuda, manifest, golden):
 
 
 def _set_recheck(monkeypatch, recheck):
-    """fused | deferred (sorted-row kernel with bulk-copied S rows) |
-    deferred-grouped (the per-lane gather kernel, kept for A/B)."""
+    """fused | deferred (cluster-blocked rows: dense blocks share staged S
+    rows, sparse blocks per candidate) | deferred-rows (one warp per sorted
+    row, bulk-copied S rows) | deferred-grouped (the per-lane gather kernel);
+    the last two are kept for A/B."""
     monkeypatch.setenv("SJB_RECHECK", recheck.split("-")[0])
-    if recheck.endswith("-grouped"):
-        monkeypatch.setenv("SJB_DENSE_RECHECK", "grouped")
+    if "-" in recheck:
+        monkeypatch.setenv("SJB_DENSE_RECHECK", recheck.split("-")[1])
     else:
         monkeypatch.delenv("SJB_DENSE_RECHECK", raising=False)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-rows", "deferred-grouped"])
 def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
     """d <= 128: fused recheck warps and the deferred full-occupancy kernels
     give the same bits (golden cases, overflow retry, theta = -1)."""
@@ -466,7 +468,7 @@ def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
         top_k(model, embed_relation(model, rel), rel, "p", 0)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-rows", "deferred-grouped"])
 def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
     """Thousands of rows (several work items and S tiles per CTA, partial
     last tiles), dense and sparse thresholds, both recheck placements."""
@@ -485,6 +487,28 @@ def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
         wl, wr, ws = O.join_raw(L, S, theta, threads=16)
         assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta)
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), inst
+
+
+@pytest.mark.parametrize("dim", [16, 64, 100, 128])
+def test_dense_blocks_match_oracle(cuda, monkeypatch, dim):
+    """The cluster-blocked dense recheck: clusters whose right members fit one
+    staging window (~60), span several windows (~400 of the 512-row union
+    cap) and overflow the union (~900: sparse per-candidate blocks), plus a
+    theta low enough for rows above the sortable 1024 candidates -- every
+    MatchSet equal to the oracle's, bit for bit."""
+    from paper_2312_01476_b200 import device as D
+    _set_recheck(monkeypatch, "deferred")
+    cases = [(2000, 3000, 50, 0.3, 0.3), (1500, 4000, 10, 0.3, 0.3), (1200, 4500, 5, 0.3, 0.3),
+             (700, 2600, 2, 0.6, -0.2)]
+    for k, (nl, nr, c, sigma, theta) in enumerate(cases):
+        L, S = O_pair(nl, nr, dim, c, sigma, 900 + k)
+        m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                            D.prepare(torch.from_numpy(S).to(cuda)), theta)
+        lo, ro, so = m.to_host()
+        wl, wr, ws = O.join_raw(L, S, theta, threads=16)
+        assert len(wl) > 0
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (dim, k)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), (dim, k)
 
 
 def test_budget_and_thread_invariance(cuda, manifest, golden):
@@ -510,8 +534,8 @@ def test_budget_and_thread_invariance(cuda, manifest, golden):
         assert _bits_equal(ms, golden["c_ragged_l"], golden["c_ragged_r"], golden["c_ragged_s"])
 
 
-@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (16, "deferred-grouped"),
-                                         (200, "fused")])
+@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (16, "deferred-rows"),
+                                         (16, "deferred-grouped"), (200, "fused")])
 def test_nan_and_inf_rows(cuda, monkeypatch, dim, recheck):
     """Rows with NaN or +-Inf normalise to NaN rows (inf / inf) exactly as the
     reference's normalize_row; their similarities are NaN, so they match

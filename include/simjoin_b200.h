@@ -108,11 +108,12 @@ float sjb_raw_band(int64_t dim);
  * switches fail with SJB_E_UNSUPPORTED. */
 int sjb_ab_kernels(void);
 
-/* Diagnostics of the dense (deferred) recheck: copies and zeroes 8 counters
+/* Diagnostics of the dense (deferred) recheck: copies and zeroes 16 counters
  * -- dense / big-row / union-overflow / low-density blocks, candidates in
- * dense and in sparse blocks, summed dense union sizes.  Only in a build
- * with -DSJB_BLK_STATS=1; otherwise SJB_E_UNSUPPORTED. */
-int sjb_debug_blk_stats(int64_t* out8);
+ * dense and in sparse blocks, summed dense union sizes, then SM cycles per
+ * block phase.  Only in a build with -DSJB_BLK_STATS=1; otherwise
+ * SJB_E_UNSUPPORTED. */
+int sjb_debug_blk_stats(int64_t* out16);
 
 /* Row norms (sj_row_norms, _kernelcore.h:9). */
 int sjb_row_norms(const float* d_m, int64_t n, int64_t dim, float* d_out, void* stream);

@@ -314,13 +314,19 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 // ------------------------------------------------------------ workspace
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
-      work, sig, desc, total;
+      work, sig, desc, pos, total;
   size_t pend, pendn;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
+// slot scratch of recheck_blocks_kernel: (union row, row) u16 per CTA, two
+// CTAs per SM
+size_t blk_pos_bytes() {
+  return (size_t)2 * sjb_sm_count(current_device()) * sjb::kBlkUnion * sjb::kBlkRows * 2;
+}
+
+JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride, bool defer) {
   JoinWs w;
   size_t o = 0;
   const size_t ccap = (size_t)(a->cand_cap > 0 ? a->cand_cap : 0);
@@ -342,6 +348,8 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   w.work = o;     o = align256(o + 16);
   w.sig = o;      o = align256(o + nl * 4);   // dense recheck: row signatures
   w.desc = o;     o = align256(o + nl * 8);   // dense recheck: block descriptors
+  // dense recheck: per-CTA slot scratch of the blocked kernel (<= 2 CTAs per SM)
+  w.pos = o;      o = align256(o + (defer ? blk_pos_bytes() : 0));
   // tolerance emission: per-CTA pending slot lists + counts
   const bool tol = a->sims_mode == 1;
   w.pend = o;     o = align256(o + (tol ? ccap * 4 : 0));
@@ -558,18 +566,18 @@ extern "C" {
 int sjb_version(void) { return 1; }
 
 // Diagnostics of the cluster-blocked dense recheck (built with
-// -DSJB_BLK_STATS=1; otherwise returns SJB_E_UNSUPPORTED): copies the 8
+// -DSJB_BLK_STATS=1; otherwise returns SJB_E_UNSUPPORTED): copies the 16
 // counters and zeroes them.
-int sjb_debug_blk_stats(int64_t* out8) {
+int sjb_debug_blk_stats(int64_t* out16) {
 #if SJB_BLK_STATS
-  unsigned long long h[8];
+  unsigned long long h[16];
   SJB_CK(cudaMemcpyFromSymbol(h, sjb::g_blk_stats, sizeof(h)));
-  for (int k = 0; k < 8; k++) out8[k] = (int64_t)h[k];
+  for (int k = 0; k < 16; k++) out16[k] = (int64_t)h[k];
   memset(h, 0, sizeof(h));
   SJB_CK(cudaMemcpyToSymbol(sjb::g_blk_stats, h, sizeof(h)));
   return SJB_OK;
 #else
-  (void)out8;
+  (void)out16;
   return fail(SJB_E_UNSUPPORTED, "built without SJB_BLK_STATS");
 #endif
 }
@@ -824,12 +832,14 @@ int64_t sjb_join_workspace_bytes(const sjb_join_args* args) {
   JoinPlan pl;
   int grid = 1;
   int64_t tstride = 0;
+  bool defer = false;
   if (args->n_left > 0 && args->n_right > 0) {
     if (make_plan(args, &pl) != SJB_OK) return -1;
     grid = pl.grid;
     tstride = pl.tile_stride;
+    defer = pl.defer;
   }
-  return (int64_t)join_ws_layout(args, grid, tstride).total;
+  return (int64_t)join_ws_layout(args, grid, tstride, defer).total;
 }
 
 }  // extern "C"
@@ -852,6 +862,7 @@ struct JoinCtx {
   unsigned int* work;  // wide group recheck: dynamic item counter
   uint32_t* sig;       // dense recheck: row signatures (smallest right offset)
   uint64_t* desc;      // dense recheck: blocks (start | rows << 32)
+  uint16_t* pos;       // dense recheck: per-CTA slot scratch
   bool empty;  // n_left == 0 or n_right == 0
   uint32_t* pend;
   uint32_t* pend_count;
@@ -867,7 +878,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   if (c->empty) return SJB_OK;
   if (int rc = make_plan(args, &c->pl)) return rc;
   const JoinPlan& pl = c->pl;
-  const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride);
+  const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride, pl.defer);
   if ((int64_t)w.total > workspace_bytes)
     return fail(SJB_E_INVALID, "workspace %lld B < required %lld B", (long long)workspace_bytes,
                 (long long)w.total);
@@ -889,6 +900,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->work = reinterpret_cast<unsigned int*>(ws + w.work);
   c->sig = reinterpret_cast<uint32_t*>(ws + w.sig);
   c->desc = reinterpret_cast<uint64_t*>(ws + w.desc);
+  c->pos = reinterpret_cast<uint16_t*>(ws + w.pos);
   c->pend = reinterpret_cast<uint32_t*>(ws + w.pend);
   c->pend_count = reinterpret_cast<uint32_t*>(ws + w.pendn);
   return SJB_OK;
@@ -1158,25 +1170,23 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     const dim3 sgrid(8, (unsigned)pl.grid);
     const int dev = current_device();
     const int sms = sjb_sm_count(dev);
-    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    SJB_CK(cudaMemsetAsync(c.sig, 0xFF, (size_t)nl * 4, st));
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount, c.sig);
     SJB_CK_LAUNCH("count_rows");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
     sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
                                                   reinterpret_cast<unsigned long long*>(c.cursor),
                                                   c.keys);
     SJB_CK_LAUNCH("group_rows");
-    sjb::sort_rows_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(c.keys, c.rowoff,
-                                                                                nl, c.sig);
-    SJB_CK_LAUNCH("sort_rows");
     // rows grouped by signature (hashed over nl buckets), order in bigrows
     const int shift = 0;
     SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
     const int fg = grid_for((uint64_t)nl, 256, 8);
-    sjb::sig_hist_kernel<<<fg, 256, 0, st>>>(c.sig, nl, shift, c.rowcount);
+    sjb::sig_hist_kernel<<<fg, 256, 0, st>>>(c.sig, c.rowoff, nl, shift, c.rowcount);
     SJB_CK_LAUNCH("sig_hist");
     if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
     sjb::sig_scatter_kernel<<<fg, 256, 0, st>>>(
-        c.sig, nl, shift, reinterpret_cast<unsigned long long*>(c.cursor), c.bigrows);
+        c.sig, c.rowoff, nl, shift, reinterpret_cast<unsigned long long*>(c.cursor), c.bigrows);
     SJB_CK_LAUNCH("sig_scatter");
     SJB_CK(cudaMemsetAsync(c.work, 0, 8, st));   // [0] block counter, [1] blocks
     sjb::sig_blocks_kernel<<<fg, 256, 0, st>>>(c.rowcount, c.cursor, nl, c.desc, c.work + 1);
@@ -1186,9 +1196,10 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     int per_sm = 0;
     SJB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sjb::recheck_blocks_kernel,
                                                          sjb::kBlkThreads, bsmem));
-    sjb::recheck_blocks_kernel<<<sms * std::max(1, per_sm), sjb::kBlkThreads, bsmem, st>>>(
-        c.keys, c.rowoff, c.bigrows, c.desc, c.work + 1, d_l32, d_r32, (int)args->dim,
-        args->theta, c.sims_bits, c.rowcount, c.work);
+    sjb::recheck_blocks_kernel<<<sms * std::min(2, std::max(1, per_sm)), sjb::kBlkThreads, bsmem,
+                                 st>>>(c.keys, c.rowoff, c.bigrows, c.desc, c.work + 1, d_l32,
+                                       d_r32, (int)args->dim, args->theta, c.sims_bits, c.rowcount,
+                                       c.work, c.pos);
     SJB_CK_LAUNCH("recheck_blocks");
     // match offsets into `cursor`; `rowoff` keeps the candidate offsets
     if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
@@ -1214,7 +1225,7 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     // right offsets, rechecks them with bulk-copied S rows and compacts the
     // matches in place; then the match offsets and one copy to the columns
     const dim3 sgrid(8, (unsigned)pl.grid);
-    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount, nullptr);
     SJB_CK_LAUNCH("count_rows");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
     sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
@@ -1267,7 +1278,7 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     // dense: group the candidates by left row, recheck them row-grouped,
     // then compact the matches by row (the segment buffer is free by then)
     const dim3 sgrid(8, (unsigned)pl.grid);
-    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount);
+    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount, nullptr);
     SJB_CK_LAUNCH("count_rows");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
     SJB_CK(cudaMemcpyAsync(c.ncand, c.rowoff + nl, 8, cudaMemcpyDeviceToDevice, st));

@@ -124,15 +124,19 @@ scan_down_kernel(const uint32_t* __restrict__ in, int64_t n, const uint64_t* __r
 // row's candidates and only the S rows come from L2:
 //   count_rows -> scan -> group_rows -> recheck_grouped -> scan -> compact
 // Segment kernels run on a 2-D grid: blockIdx.y = segment.
+// (+ sig != nullptr: each row's smallest right offset, sig preset to ~0)
 __global__ void count_rows_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
                                   const unsigned long long* __restrict__ cta_count,
-                                  uint32_t* __restrict__ rowcount) {
+                                  uint32_t* __restrict__ rowcount, uint32_t* __restrict__ sig) {
   const unsigned long long cc = cta_count[blockIdx.y];
   if (cc > seg_cap) return;  // saturated segment: the join is retried with room
   const uint64_t* seg = cand + (uint64_t)blockIdx.y * seg_cap;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cc;
-       k += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(rowcount + (uint32_t)(seg[k] >> 32), 1u);
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = seg[k];
+    atomicAdd(rowcount + (uint32_t)(u >> 32), 1u);
+    if (sig) atomicMin(sig + (uint32_t)(u >> 32), (uint32_t)u);
+  }
 }
 
 __global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
@@ -470,21 +474,22 @@ emit_rows_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
 // in flight from L2 (32 GB of S rows at cfg5 theta = 0.4, ~5 ms).  Dense
 // joins of clustered data re-read the same S rows: the left rows of one
 // cluster match (nearly) the same right rows.  So:
-//  1. sort_rows: each row's candidates sorted by right offset in place (the
-//     canonical order), and the row's signature = its smallest right offset;
+//  1. count_rows also takes each row's signature = its smallest right offset;
 //  2. rows grouped by signature (counting sort over hashed buckets: bucket,
 //     scan, scatter), so consecutive rows tend to share their candidates;
 //  3. recheck_blocks: a CTA takes up to 32 consecutive rows of one bucket, builds
-//     the UNION of their right offsets (shared-memory hash set, then sorted),
-//     and -- when the block is dense (candidates >= kBlkDense x rows x union)
-//     -- stages each union S row ONCE (1-D bulk copies) and the 32 R rows,
-//     and runs the canonical chains with lane = left row and the S row a
-//     shared-memory broadcast: four union rows per step (independent chains,
-//     the R row's 128-bit read shared), every read conflict-free.  The
-//     similarity goes to the candidate's slot of the sorted row: its rank =
-//     the candidates of the row before it in the union (a running count per
-//     lane).  Sparse blocks (or unions above kBlkUnion) run the per-candidate
-//     staged recheck instead, one warp per row;
+//     the UNION of their right offsets (shared-memory hash set), and -- when
+//     the block is dense (candidates >= kBlkDense x rows x union) -- stages
+//     each union S row ONCE (1-D bulk copies) and the 32 R rows, and runs the
+//     canonical chains with lane = left row and the S row a shared-memory
+//     broadcast: eight union rows per step (independent chains sharing the R
+//     row's 128-bit reads), every read conflict-free.  Each similarity goes to
+//     its candidate's slot of the sorted row, recorded per (union row, row)
+//     in a per-CTA global scratch while the masks are built.  Sparse blocks
+//     (or unions above kBlkUnion) run the per-candidate staged recheck
+//     instead, one warp per row;
+//     Every row of <= kRowSortCap candidates is first sorted by right offset
+//     in registers and written back (the canonical order the slots follow);
 //  4. emit_sims: per row, the rechecked slots compacted into the MatchSet.
 template <bool kWarp, class T>
 __device__ void smem_bitonic(T* s, int n, int tid, int nthr);
@@ -496,6 +501,7 @@ constexpr int kBlkHashBits = 12;
 constexpr int kBlkHash = 1 << kBlkHashBits;   // holds <= kBlkUnion + kBlkThreads keys
 constexpr int kBlkUnion = 1024;
 constexpr float kBlkDense = 0.25f;
+constexpr int kBlkChains = 8;       // union rows per step of a warp
 constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;
 #ifndef SJB_BLK_STATS
 #define SJB_BLK_STATS 0
@@ -503,37 +509,18 @@ constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;
 #if SJB_BLK_STATS
 // diagnostics (-DSJB_BLK_STATS=1): dense / big / union-overflow / low-density
 // blocks, candidates in dense and sparse blocks, summed dense unions
-__device__ unsigned long long g_blk_stats[8];
+__device__ unsigned long long g_blk_stats[16];   // [8..15]: cycles per phase (CTA thread 0)
+#define BLK_MARK(k)                                                   \
+  do {                                                                \
+    if (tid == 0) {                                                   \
+      const long long now_ = clock64();                               \
+      atomicAdd(&g_blk_stats[8 + (k)], (unsigned long long)(now_ - t_mark)); \
+      t_mark = now_;                                                  \
+    }                                                                 \
+  } while (0)
+#else
+#define BLK_MARK(k) do { } while (0)
 #endif
-
-// candidates of row i sorted in place; sig[i] = smallest right offset (rows
-// of 1 .. kRowSortCap candidates), ~0 otherwise (empty and unsorted big rows)
-__global__ void __launch_bounds__(256)
-sort_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff, int64_t n_rows,
-                 uint32_t* __restrict__ sig) {
-  __shared__ uint32_t lists[8][kRowSortCap];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* list = lists[warp];
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n_rows; i += (int64_t)gridDim.x * 8) {
-    const uint64_t c0 = rowoff[i], n = rowoff[i + 1] - c0;
-    if (n == 0 || n > (uint64_t)kRowSortCap) {
-      if (lane == 0) sig[i] = ~0u;
-      continue;
-    }
-    const int m = (int)n;
-    if (m <= 32) sort_row_js<1>(keys, c0, m, list);
-    else if (m <= 64) sort_row_js<2>(keys, c0, m, list);
-    else if (m <= 128) sort_row_js<4>(keys, c0, m, list);
-    else if (m <= 256) sort_row_js<8>(keys, c0, m, list);
-    else if (m <= 512) sort_row_js<16>(keys, c0, m, list);
-    else sort_row_js<32>(keys, c0, m, list);
-    __syncwarp();
-    const uint64_t hi = (uint64_t)i << 32;
-    for (int t = lane; t < m; t += 32) keys[c0 + t] = hi | list[t];
-    if (lane == 0) sig[i] = list[0];
-    __syncwarp();
-  }
-}
 
 // Rows are grouped, not sorted, by signature: bucket = a multiplicative hash
 // of it over nbk - 1 buckets (the last one for big and empty rows).  Equal
@@ -548,18 +535,59 @@ __device__ __forceinline__ uint32_t sig_bucket(uint32_t s, int shift, int64_t nb
   const uint32_t h = (uint32_t)(((uint64_t)s * 0x9E3779B97F4A7C15ull) >> 32);
   return (uint32_t)(((uint64_t)h * (uint64_t)(nbk - 1)) >> 32);
 }
-__global__ void sig_hist_kernel(const uint32_t* __restrict__ sig, int64_t n, int shift,
+// empty rows and rows above kRowSortCap candidates share the last bucket
+__device__ __forceinline__ uint32_t row_sig(const uint32_t* sig, const uint64_t* rowoff,
+                                            int64_t i) {
+  const uint64_t n = rowoff[i + 1] - rowoff[i];
+  return (n == 0 || n > (uint64_t)kRowSortCap) ? ~0u : sig[i];
+}
+__global__ void sig_hist_kernel(const uint32_t* __restrict__ sig,
+                                const uint64_t* __restrict__ rowoff, int64_t n, int shift,
                                 uint32_t* __restrict__ hist) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(hist + sig_bucket(sig[i], shift, n), 1u);
+    atomicAdd(hist + sig_bucket(row_sig(sig, rowoff, i), shift, n), 1u);
 }
-__global__ void sig_scatter_kernel(const uint32_t* __restrict__ sig, int64_t n, int shift,
+__global__ void sig_scatter_kernel(const uint32_t* __restrict__ sig,
+                                   const uint64_t* __restrict__ rowoff, int64_t n, int shift,
                                    unsigned long long* __restrict__ cursor,
                                    uint32_t* __restrict__ perm) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    perm[atomicAdd(cursor + sig_bucket(sig[i], shift, n), 1ull)] = (uint32_t)i;
+    perm[atomicAdd(cursor + sig_bucket(row_sig(sig, rowoff, i), shift, n), 1ull)] = (uint32_t)i;
+}
+
+// keys[c0 .. c0 + n) (row i) sorted by right offset in registers (n <= 32 E),
+// written back in place and, when list != nullptr, their j's to list[0..n)
+template <int E>
+__device__ __forceinline__ void sort_row_back(uint64_t* __restrict__ keys, uint64_t c0, int n,
+                                              uint32_t i, uint32_t* list) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v[E];
+#pragma unroll
+  for (int r = 0; r < E; r++) {
+    const int t = 32 * r + lane;
+    v[r] = t < n ? (uint32_t)keys[c0 + t] : ~0u;
+  }
+  warp_sort_u32<E>(v);
+  const uint64_t hi = (uint64_t)i << 32;
+#pragma unroll
+  for (int r = 0; r < E; r++) {
+    const int t = 32 * r + lane;
+    if (t < n) {
+      keys[c0 + t] = hi | v[r];
+      if (list) list[t] = v[r];
+    }
+  }
+}
+__device__ __forceinline__ void sort_row_dispatch(uint64_t* keys, uint64_t c0, int m, uint32_t i,
+                                                  uint32_t* list) {
+  if (m <= 32) sort_row_back<1>(keys, c0, m, i, list);
+  else if (m <= 64) sort_row_back<2>(keys, c0, m, i, list);
+  else if (m <= 128) sort_row_back<4>(keys, c0, m, i, list);
+  else if (m <= 256) sort_row_back<8>(keys, c0, m, i, list);
+  else if (m <= 512) sort_row_back<16>(keys, c0, m, i, list);
+  else sort_row_back<32>(keys, c0, m, i, list);
 }
 
 // Blocks never span two buckets: bucket b (rows [end_b - cnt_b, end_b) of
@@ -597,22 +625,23 @@ struct BlkShared {
   uint32_t uniq[kBlkUnion];
   uint32_t mask[kBlkUnion];
   uint64_t c0[kBlkRows];
-  uint32_t n[kBlkRows], row[kBlkRows], kept[kBlkRows], rank[2][kBlkRows];
+  uint32_t n[kBlkRows], off[kBlkRows], row[kBlkRows], kept[kBlkRows];
   uint64_t sbar[kBlkWarps];
   uint64_t dbar;
-  uint32_t item, count, ucnt, ovf, big, cand;
+  uint32_t item, count, ucnt, ovf, big, cand, sorted;
 };
 __host__ __device__ inline int blk_smem_bytes(int dim) {
   return blk_stage_bytes(dim) + (int)sizeof(BlkShared) + 16;
 }
 
 __global__ void __launch_bounds__(kBlkThreads)
-recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
+recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
                       const uint32_t* __restrict__ perm, const uint64_t* __restrict__ desc,
                       const unsigned int* __restrict__ n_desc,
                       const float* __restrict__ l32, const float* __restrict__ r32, int dim,
                       float theta, uint32_t* __restrict__ sims_out,
-                      uint32_t* __restrict__ rowcount, unsigned int* __restrict__ work) {
+                      uint32_t* __restrict__ rowcount, unsigned int* __restrict__ work,
+                      uint16_t* __restrict__ pos_scratch) {
   extern __shared__ __align__(16) uint8_t bsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int pitch = rows_pitch(dim, false), nq = dim >> 2;
@@ -620,16 +649,23 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
   float* stage = reinterpret_cast<float*>(bsm);
   BlkShared& sh = *reinterpret_cast<BlkShared*>(bsm + blk_stage_bytes(dim));
   const int win = blk_window_rows(dim);
+  const uint32_t jcap = (uint32_t)blk_stage_bytes(dim) / 4;   // j cache entries
+  uint32_t* jc = reinterpret_cast<uint32_t*>(bsm);
+  uint16_t* pos = pos_scratch + (size_t)blockIdx.x * kBlkUnion * kBlkRows;
   if (tid < kBlkWarps) mbar_init(&sh.sbar[tid], 1);
   if (tid == 0) mbar_init(&sh.dbar, 1);
   fence_mbar_init();
   __syncthreads();
   const uint64_t pol = policy_evict_last();
   uint32_t sphase = 0, dphase = 0;
+#if SJB_BLK_STATS
+  long long t_mark = clock64();
+#endif
   for (;;) {
     if (tid == 0) sh.item = atomicAdd(work, 1u);
     if (tid < kBlkRows) sh.kept[tid] = 0u;
     __syncthreads();
+    BLK_MARK(0);
     if (sh.item >= *n_desc) break;
     const uint64_t dsc = desc[sh.item];
     const int64_t p0 = (int64_t)(uint32_t)dsc;
@@ -645,52 +681,66 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
       sh.row[tid] = i;
       sh.c0[tid] = c0;
       sh.n[tid] = n;
-      // block totals (warp 0)
-      const uint32_t cand = __reduce_add_sync(0xffffffffu, mn<uint32_t>(n, 1u << 20));
+      // block totals and the rows' offsets in the shared j cache (warp 0)
+      const uint32_t nc = mn<uint32_t>(n, 1u << 20);
+      uint32_t incl = nc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      sh.off[tid] = incl - nc;
+      const uint32_t cand = __shfl_sync(0xffffffffu, incl, 31);
       const bool big = __any_sync(0xffffffffu, n > (uint32_t)kRowSortCap);
       if (tid == 0) {
         sh.cand = cand;
         sh.big = big ? 1u : 0u;
         sh.count = 0u;
-        sh.ovf = big ? 1u : 0u;
+        sh.sorted = 0u;
+        // the block's right offsets must fit the j cache (the staging area)
+        sh.ovf = (big || cand > jcap) ? 1u : 0u;
       }
     }
     for (int h = tid; h < kBlkHash; h += kBlkThreads) sh.hkeys[h] = kHashEmpty;
     __syncthreads();
-    // ---- union of the block's right offsets (hash set; gives up above
-    // kBlkUnion).  Each lane loads four candidates before inserting them, so
-    // the global loads overlap.
+    BLK_MARK(1);
+    // ---- union of the block's right offsets: a shared-memory hash set
+    // (gives up above kBlkUnion keys).  The block's j's are cached in the
+    // staging area on the way (row r at off[r]); each lane loads four
+    // before inserting them, and looks before it CASes (the rows of a block
+    // mostly share their keys).
     auto hash_of = [](uint32_t j) { return (j * 0x9E3779B1u) >> (32 - kBlkHashBits); };
-    auto for_block_js = [&](auto&& fn) {
-      for (int r = warp; r < nrows; r += kBlkWarps) {
-        const uint64_t c0 = sh.c0[r];
-        const uint32_t n = sh.n[r];
-        for (uint32_t t0 = lane; t0 < n; t0 += 128) {
-          uint32_t j[4];
-#pragma unroll
-          for (int e = 0; e < 4; e++) j[e] = t0 + 32 * e < n ? (uint32_t)keys[c0 + t0 + 32 * e] : 0u;
-#pragma unroll
-          for (int e = 0; e < 4; e++)
-            if (t0 + 32 * e < n) fn(r, j[e]);
-        }
-      }
-    };
     if (!sh.ovf) {
-      for_block_js([&](int, uint32_t j) {
+      // (a) each row sorted by right offset (registers; written back for
+      // the emission) into the j cache at off[r]
+      for (int r = warp; r < nrows; r += kBlkWarps)
+        if (sh.n[r]) sort_row_dispatch(keys, sh.c0[r], (int)sh.n[r], sh.row[r], jc + sh.off[r]);
+      if (tid == 0) sh.sorted = 1u;
+      __syncthreads();
+      // (b) insert in cache order: the CTA's threads walk ~one row at a time,
+      // so concurrent inserts are distinct keys, and the later rows mostly
+      // find theirs (a read, no CAS)
+      const uint32_t C = sh.cand;
+      for (uint32_t k = tid; k < C; k += kBlkThreads) {
+        if (*(volatile uint32_t*)&sh.ovf) break;
+        const uint32_t j = jc[k];
         uint32_t h = hash_of(j);
         for (;;) {
-          if (*(volatile uint32_t*)&sh.ovf) break;
-          const uint32_t prev = atomicCAS(&sh.hkeys[h], kHashEmpty, j);
-          if (prev == kHashEmpty) {
-            if (atomicAdd(&sh.count, 1u) >= (uint32_t)kBlkUnion) sh.ovf = 1u;
-            break;
+          uint32_t cur = sh.hkeys[h];
+          if (cur == kHashEmpty) {
+            cur = atomicCAS(&sh.hkeys[h], kHashEmpty, j);
+            if (cur == kHashEmpty) {
+              if (atomicAdd(&sh.count, 1u) >= (uint32_t)kBlkUnion) sh.ovf = 1u;
+              break;
+            }
           }
-          if (prev == j) break;
+          if (cur == j) break;
           h = (h + 1) & (kBlkHash - 1);
         }
-      });
+      }
     }
     __syncthreads();
+    BLK_MARK(2);
     const uint32_t U = sh.count;
     const bool dense = !sh.ovf && U > 0 && (float)sh.cand >= kBlkDense * (float)nrows * (float)U;
 #if SJB_BLK_STATS
@@ -701,45 +751,51 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
     }
 #endif
     if (dense) {
-      // compact the set into uniq[0..U), sort it (ascending right offsets)
-      // and record each key's sorted index in its hash slot
+      // union index u of every key (slot order), its row in uniq[u]
       if (tid == 0) sh.ucnt = 0u;
       __syncthreads();
       for (int h = tid; h < kBlkHash; h += kBlkThreads) {
         const uint32_t k = sh.hkeys[h];
-        if (k != kHashEmpty) sh.uniq[atomicAdd(&sh.ucnt, 1u)] = k;
+        if (k != kHashEmpty) {
+          const uint32_t u = atomicAdd(&sh.ucnt, 1u);
+          sh.uniq[u] = k;
+          sh.hidx[h] = (uint16_t)u;
+        }
       }
       for (uint32_t u = tid; u < U; u += kBlkThreads) sh.mask[u] = 0u;
       __syncthreads();
-      smem_bitonic<false>(sh.uniq, (int)U, tid, kBlkThreads);
-      __syncthreads();
-      for (uint32_t u = tid; u < U; u += kBlkThreads) {
-        const uint32_t j = sh.uniq[u];
-        uint32_t h = hash_of(j);
-        while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
-        sh.hidx[h] = (uint16_t)u;
+      BLK_MARK(3);
+      // membership: bit r of mask[u] <=> (row r, uniq[u]) is a candidate, at
+      // index pos[u][r] of row r's sorted candidates
+      {
+        const uint32_t C = sh.cand;
+        int r = 0;
+        for (uint32_t k = tid; k < C; k += kBlkThreads) {
+          while (r + 1 < nrows && k >= sh.off[r + 1]) r++;
+          const uint32_t j = jc[k];
+          uint32_t h = hash_of(j);
+          while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
+          const uint32_t u = sh.hidx[h];
+          atomicOr(&sh.mask[u], 1u << r);
+          pos[u * kBlkRows + r] = (uint16_t)(k - sh.off[r]);
+        }
       }
-      __syncthreads();
-      // membership masks: bit r of mask[u] <=> (row r, uniq[u]) is a candidate
-      for_block_js([&](int r, uint32_t j) {
-        uint32_t h = hash_of(j);
-        while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
-        atomicOr(&sh.mask[sh.hidx[h]], 1u << r);
-      });
-      if (tid < kBlkRows) sh.rank[0][tid] = 0u;
-      int wpar = 0;
       const float* Rs = stage;
       const float* Ss = stage + (size_t)kBlkRows * pitch;
+      const float4* R4 = reinterpret_cast<const float4*>(Rs + (size_t)lane * pitch);
+      const uint64_t c0 = sh.c0[lane];
+      uint32_t kept = 0;
       for (uint32_t u0 = 0; u0 < U; u0 += (uint32_t)win) {
         const uint32_t u1 = mn<uint32_t>(U, u0 + (uint32_t)win);
         fence_proxy_async_smem();
-        __syncthreads();   // masks complete / the previous window consumed
+        __syncthreads();   // masks complete (and the j cache dead) / the previous window consumed
+        BLK_MARK(u0 == 0 ? 4 : 6);
         if (tid == 0)
           mbar_arrive_expect_tx(&sh.dbar, (u1 - u0) * rowbytes + (u0 == 0 ? nrows * rowbytes : 0u));
         __syncthreads();
         if (tid < (int)(u1 - u0))
           bulk_g2s(stage + (size_t)(kBlkRows + tid) * pitch,
-                   r32 + (size_t)(uint32_t)sh.uniq[u0 + tid] * dim, rowbytes, &sh.dbar, pol);
+                   r32 + (size_t)sh.uniq[u0 + tid] * dim, rowbytes, &sh.dbar, pol);
         if (u0 == 0 && tid >= kBlkStage && tid - kBlkStage < nrows) {
           const int r = tid - kBlkStage;
           bulk_g2s(stage + (size_t)r * pitch, l32 + (size_t)sh.row[r] * dim, rowbytes, &sh.dbar,
@@ -747,30 +803,29 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
         }
         mbar_wait(&sh.dbar, dphase);
         dphase ^= 1u;
-        // warp w: union rows [ua, ub) of the window, four at a time; lane = row
-        const uint32_t span = u1 - u0;
-        const uint32_t ua = u0 + span * warp / kBlkWarps, ub = u0 + span * (warp + 1) / kBlkWarps;
-        uint32_t rank = sh.rank[wpar][lane];
-        for (uint32_t u = u0; u < ua; u++) rank += (sh.mask[u] >> lane) & 1u;
-        uint32_t kept = 0;
-        const float4* R4 = reinterpret_cast<const float4*>(Rs + (size_t)lane * pitch);
-        const uint64_t c0 = sh.c0[lane];
-        for (uint32_t u = ua; u < ub; u += 4) {
-          uint32_t m[4];
-          const float4* S4[4];
+        BLK_MARK(5);
+        // warp w: groups w, w + 8, .. of kBlkChains union rows; lane = row;
+        // a group's chains are independent and share the R row's reads
+        for (uint32_t u = u0 + kBlkChains * warp; u < u1; u += kBlkChains * kBlkWarps) {
+          uint32_t m[kBlkChains], any = 0u, t[kBlkChains];
+          const float4* S4[kBlkChains];
 #pragma unroll
-          for (int c = 0; c < 4; c++) {
-            const uint32_t uc = u + c < ub ? u + c : u;
-            m[c] = u + c < ub ? sh.mask[uc] : 0u;
+          for (int c = 0; c < kBlkChains; c++) {
+            const uint32_t uc = u + c < u1 ? u + c : u;
+            m[c] = u + c < u1 ? sh.mask[uc] : 0u;
+            any |= m[c];
+            t[c] = ((m[c] >> lane) & 1u) ? pos[uc * kBlkRows + lane] : 0u;
             S4[c] = reinterpret_cast<const float4*>(Ss + (size_t)(uc - u0) * pitch);
           }
-          if ((m[0] | m[1] | m[2] | m[3]) == 0u) continue;
-          float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (any == 0u) continue;
+          float x[kBlkChains];
+#pragma unroll
+          for (int c = 0; c < kBlkChains; c++) x[c] = 0.0f;
 #pragma unroll 5
           for (int q = 0; q < nq; q++) {
             const float4 a = R4[q];
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
+            for (int c = 0; c < kBlkChains; c++) {
               const float4 b = S4[c][q];
               x[c] = __fmaf_rn(a.x, b.x, x[c]);
               x[c] = __fmaf_rn(a.y, b.y, x[c]);
@@ -779,28 +834,28 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
             }
           }
 #pragma unroll
-          for (int c = 0; c < 4; c++) {
+          for (int c = 0; c < kBlkChains; c++) {
             if ((m[c] >> lane) & 1u) {
               const bool ok = x[c] >= theta;
-              sims_out[c0 + rank] = ok ? __float_as_uint(x[c]) : kRejected;
-              rank++;
+              sims_out[c0 + t[c]] = ok ? __float_as_uint(x[c]) : kRejected;
               kept += ok ? 1u : 0u;
             }
           }
         }
-        if (kept) atomicAdd(&sh.kept[lane], kept);
-        // the rank at the window's end, for the next window (other parity:
-        // this window's readers may still be reading theirs)
-        if (warp == kBlkWarps - 1) sh.rank[wpar ^ 1][lane] = rank;
-        wpar ^= 1;
       }
+      if (kept) atomicAdd(&sh.kept[lane], kept);
     } else {
       // ---- sparse block: per-candidate staged recheck, one warp per row
       float* buf = stage + (size_t)warp * 32 * pitch;
       float* myrow = buf + (size_t)lane * pitch;
+      const bool sorted = sh.sorted != 0u;
       for (int r = warp; r < nrows && warp < kBlkSparseWarps; r += kBlkSparseWarps) {
         const uint64_t c0 = sh.c0[r];
         const uint32_t n = sh.n[r];
+        if (!sorted && n > 0 && n <= (uint32_t)kRowSortCap) {
+          sort_row_dispatch(keys, c0, (int)n, sh.row[r], nullptr);
+          __syncwarp();   // (the batches below read the sorted keys back)
+        }
         const float4* a4 = reinterpret_cast<const float4*>(l32 + (size_t)sh.row[r] * dim);
         uint32_t kept = 0;
         for (uint32_t b0 = 0; b0 < n; b0 += 32) {
@@ -835,6 +890,7 @@ recheck_blocks_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
     }
     fence_proxy_async_smem();
     __syncthreads();
+    BLK_MARK(dense ? 6 : 7);
     if (tid < nrows) rowcount[sh.row[tid]] = sh.kept[tid];
   }
 }

@@ -10,7 +10,7 @@ theta = float(sys.argv[2]) if len(sys.argv) > 2 else 0.4
 (L, S), c = datagen.config_vectors(cfg)
 PL, PS = D.prepare(torch.from_numpy(L).cuda()), D.prepare(torch.from_numpy(S).cuda())
 lib = _lib.lib()
-out = (ctypes.c_int64 * 8)()
+out = (ctypes.c_int64 * 16)()
 for it in range(2):
     lib.sjb_debug_blk_stats(out)
     m = D.join_prepared(PL, PS, theta)
@@ -20,3 +20,7 @@ for it in range(2):
     print(f"{cfg} theta={theta} matches={m.n_matches} cand={m.n_candidates}: blocks dense {v[0]} "
           f"big {v[1]} union-overflow {v[2]} low-density {v[3]}; candidates dense {v[4]} "
           f"sparse {v[5]}; mean dense union {v[6] / max(1, v[0]):.1f}", flush=True)
+    names = ["fetch", "rows", "insert", "sort+hidx", "mask", "tma-wait", "compute", "sparse"]
+    tot = sum(v[8:16]) or 1
+    print("  cycles (CTA thread 0): " + ", ".join(f"{n} {100 * c / tot:.1f}%" for n, c in zip(names, v[8:16])),
+          f"total {tot:.3e}", flush=True)

@@ -1171,13 +1171,16 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     const int dev = current_device();
     const int sms = sjb_sm_count(dev);
     SJB_CK(cudaMemsetAsync(c.sig, 0xFF, (size_t)nl * 4, st));
-    sjb::count_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta, c.rowcount, c.sig);
-    SJB_CK_LAUNCH("count_rows");
+    // chunks of 2048 candidates aggregated per row in shared memory; enough
+    // CTAs per segment for ~4 per SM
+    const dim3 agrid((unsigned)std::max(1, 4 * sms / pl.grid), (unsigned)pl.grid);
+    sjb::count_rows_agg_kernel<<<agrid, sjb::kAggThreads, 0, st>>>(c.cand, pl.seg_cap, c.cta,
+                                                                   c.rowcount, c.sig);
+    SJB_CK_LAUNCH("count_rows_agg");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
-    sjb::group_rows_kernel<<<sgrid, 256, 0, st>>>(c.cand, pl.seg_cap, c.cta,
-                                                  reinterpret_cast<unsigned long long*>(c.cursor),
-                                                  c.keys);
-    SJB_CK_LAUNCH("group_rows");
+    sjb::group_rows_agg_kernel<<<agrid, sjb::kAggThreads, 0, st>>>(
+        c.cand, pl.seg_cap, c.cta, reinterpret_cast<unsigned long long*>(c.cursor), c.keys);
+    SJB_CK_LAUNCH("group_rows_agg");
     // rows grouped by signature (hashed over nl buckets), order in bigrows
     const int shift = 0;
     SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));

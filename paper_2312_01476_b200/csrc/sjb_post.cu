@@ -153,6 +153,163 @@ __global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t se
   }
 }
 
+// The same two passes with per-chunk aggregation: a CTA takes 2048
+// consecutive candidates of one segment.  A filter CTA appends its work
+// items (256-row R blocks) one after another, so a chunk's rows nearly always
+// lie within one or two blocks: when they span < kAggSpan rows, counts (and
+// signature minima) are taken in shared memory and folded into the global
+// arrays with one atomic per distinct row, and the grouping reserves each
+// row's run of the chunk with one returning atomic (local ranks from the
+// shared counters).  Wider chunks fall back to per-candidate atomics.
+constexpr int kAggThreads = 256;
+constexpr int kAggPer = 8;
+constexpr int kAggChunk = kAggThreads * kAggPer;
+constexpr int kAggSpan = 2048;
+
+__device__ __forceinline__ void agg_row_range(const uint64_t (&u)[kAggPer], int n, uint32_t* s_mm,
+                                              uint32_t& rmin, uint32_t& rmax) {
+  uint32_t lo = ~0u, hi = 0u;
+#pragma unroll
+  for (int e = 0; e < kAggPer; e++) {
+    const int k = threadIdx.x + kAggThreads * e;
+    if (k < n) {
+      const uint32_t r = (uint32_t)(u[e] >> 32);
+      lo = min(lo, r);
+      hi = max(hi, r);
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&s_mm[0], lo);
+    atomicMax(&s_mm[1], hi);
+  }
+  __syncthreads();
+  rmin = s_mm[0];
+  rmax = s_mm[1];
+}
+
+__global__ void __launch_bounds__(kAggThreads)
+count_rows_agg_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                      const unsigned long long* __restrict__ cta_count,
+                      uint32_t* __restrict__ rowcount, uint32_t* __restrict__ sig) {
+  __shared__ uint32_t hcnt[kAggSpan], hmin[kAggSpan];
+  __shared__ uint32_t s_mm[2];
+  const unsigned long long cc = cta_count[blockIdx.y];
+  if (cc > seg_cap) return;  // saturated segment: the join is retried with room
+  const uint64_t* seg = cand + (uint64_t)blockIdx.y * seg_cap;
+  for (uint64_t k0 = (uint64_t)blockIdx.x * kAggChunk; k0 < cc;
+       k0 += (uint64_t)gridDim.x * kAggChunk) {
+    const int n = (int)mn<uint64_t>(kAggChunk, cc - k0);
+    uint64_t u[kAggPer];
+#pragma unroll
+    for (int e = 0; e < kAggPer; e++) {
+      const int k = threadIdx.x + kAggThreads * e;
+      u[e] = k < n ? seg[k0 + k] : 0ull;
+    }
+    if (threadIdx.x == 0) {
+      s_mm[0] = ~0u;
+      s_mm[1] = 0u;
+    }
+    __syncthreads();
+    uint32_t rmin, rmax;
+    agg_row_range(u, n, s_mm, rmin, rmax);
+    const uint32_t span = rmax - rmin + 1;
+    if (span <= (uint32_t)kAggSpan) {
+      for (uint32_t r = threadIdx.x; r < span; r += kAggThreads) {
+        hcnt[r] = 0u;
+        hmin[r] = ~0u;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < kAggPer; e++) {
+        const int k = threadIdx.x + kAggThreads * e;
+        if (k < n) {
+          const uint32_t r = (uint32_t)(u[e] >> 32) - rmin;
+          atomicAdd(&hcnt[r], 1u);
+          atomicMin(&hmin[r], (uint32_t)u[e]);
+        }
+      }
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < span; r += kAggThreads) {
+        const uint32_t c = hcnt[r];
+        if (c) {
+          atomicAdd(rowcount + rmin + r, c);
+          atomicMin(sig + rmin + r, hmin[r]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kAggPer; e++) {
+        const int k = threadIdx.x + kAggThreads * e;
+        if (k < n) {
+          atomicAdd(rowcount + (uint32_t)(u[e] >> 32), 1u);
+          atomicMin(sig + (uint32_t)(u[e] >> 32), (uint32_t)u[e]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kAggThreads)
+group_rows_agg_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                      const unsigned long long* __restrict__ cta_count,
+                      unsigned long long* __restrict__ cursor, uint64_t* __restrict__ grouped) {
+  __shared__ uint32_t hcnt[kAggSpan];
+  __shared__ unsigned long long hbase[kAggSpan];
+  __shared__ uint32_t s_mm[2];
+  const unsigned long long cc = cta_count[blockIdx.y];
+  if (cc > seg_cap) return;
+  const uint64_t* seg = cand + (uint64_t)blockIdx.y * seg_cap;
+  for (uint64_t k0 = (uint64_t)blockIdx.x * kAggChunk; k0 < cc;
+       k0 += (uint64_t)gridDim.x * kAggChunk) {
+    const int n = (int)mn<uint64_t>(kAggChunk, cc - k0);
+    uint64_t u[kAggPer];
+#pragma unroll
+    for (int e = 0; e < kAggPer; e++) {
+      const int k = threadIdx.x + kAggThreads * e;
+      u[e] = k < n ? seg[k0 + k] : 0ull;
+    }
+    if (threadIdx.x == 0) {
+      s_mm[0] = ~0u;
+      s_mm[1] = 0u;
+    }
+    __syncthreads();
+    uint32_t rmin, rmax;
+    agg_row_range(u, n, s_mm, rmin, rmax);
+    const uint32_t span = rmax - rmin + 1;
+    if (span <= (uint32_t)kAggSpan) {
+      for (uint32_t r = threadIdx.x; r < span; r += kAggThreads) hcnt[r] = 0u;
+      __syncthreads();
+      uint32_t rank[kAggPer];
+#pragma unroll
+      for (int e = 0; e < kAggPer; e++) {
+        const int k = threadIdx.x + kAggThreads * e;
+        rank[e] = k < n ? atomicAdd(&hcnt[(uint32_t)(u[e] >> 32) - rmin], 1u) : 0u;
+      }
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < span; r += kAggThreads) {
+        const uint32_t c = hcnt[r];
+        if (c) hbase[r] = atomicAdd(cursor + rmin + r, (unsigned long long)c);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < kAggPer; e++) {
+        const int k = threadIdx.x + kAggThreads * e;
+        if (k < n) grouped[hbase[(uint32_t)(u[e] >> 32) - rmin] + rank[e]] = u[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kAggPer; e++) {
+        const int k = threadIdx.x + kAggThreads * e;
+        if (k < n) grouped[atomicAdd(cursor + (uint32_t)(u[e] >> 32), 1ull)] = u[e];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // grouped[0 .. *total) holds (i << 32 | j) grouped by i: consecutive threads
 // share the R row (L1), S rows come from L2 (the sequential chain of
 // dot_seq_dev = sj_dot_seq).  Staging the warp's S rows in shared memory was

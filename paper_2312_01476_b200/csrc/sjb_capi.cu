@@ -1047,10 +1047,39 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       return ab_missing("SJB_WIDE_RECHECK=fused");
 #endif
     } else {
-      if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<false>, (int)pl.smem)) return rc;
-      sjb::wide::filter_kernel<false>
-          <<<pl.grid, sjb::wide::Cfg<false>::kThreads, pl.smem, st>>>(wp);
-      SJB_CK_LAUNCH("wide_filter");
+      // A/B (SJB_WIDE_PAIR=1, tolerance emission only): CTA pairs sharing
+      // each S chunk by TMA multicast -- measured slower (cfg4 slice 33.8 vs
+      // 31.1 ms: the coupled rings wait on the slower CTA's epilogue)
+      const char* wpv = getenv("SJB_WIDE_PAIR");
+      const bool wpair = wp.tol && (pl.grid % 2) == 0 && wpv && strcmp(wpv, "1") == 0;
+      if (wpair) {
+#if !SJB_AB_KERNELS
+        return ab_missing("SJB_WIDE_PAIR=1");
+#else
+        const void* fn = (const void*)sjb::wide::filter_kernel<false, true>;
+        if (int rc = set_smem_attr(fn, (int)pl.smem)) return rc;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)pl.grid);
+        cfg.blockDim = dim3(sjb::wide::Cfg<false>::kThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SJB_CK(cudaLaunchKernelEx(&cfg, sjb::wide::filter_kernel<false, true>, wp));
+        SJB_CK_LAUNCH("wide_filter_pair");
+#endif
+      } else {
+        if (int rc = set_smem_attr((const void*)sjb::wide::filter_kernel<false>, (int)pl.smem))
+          return rc;
+        sjb::wide::filter_kernel<false>
+            <<<pl.grid, sjb::wide::Cfg<false>::kThreads, pl.smem, st>>>(wp);
+        SJB_CK_LAUNCH("wide_filter");
+      }
       if (wp.tol && jp.debug_mode != 1) {
         // tolerance emission: only the band pairs need the canonical chain
         sjb::wide::recheck_pending_kernel<<<sjb_sm_count(current_device()) * 8, 256, 0, st>>>(

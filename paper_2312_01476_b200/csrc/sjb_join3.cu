@@ -106,9 +106,43 @@ __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
 }
 
-template <bool kFused>
+// ---- CTA pairs (kPair): two CTAs of a cluster take R blocks 2p and 2p + 1
+// against the same S tiles; each loads its own R chunk, rank 0 multicasts
+// the S chunk into both CTAs' rings (the per-tile L2 operand traffic falls
+// from 2 x 256 rows to 1.5 x 256 rows per CTA: the filter at d = 768 is L2
+// bound).  A ring slot is refilled only when BOTH CTAs' MMAs are done with
+// it: the MMA commit arrives on the slot's `empty` barrier in both CTAs
+// (count 2).
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_mc(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+template <bool kFused, bool kPair = false>
 __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const Params p) {
   constexpr int kRecheckWarps = Cfg<kFused>::kRecheckWarps;
+  static_assert(!(kFused && kPair), "pairs: separate recheck only");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;  // stage s: A chunk at s*64K, B chunk at s*64K + 32K
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * 2 * kChunkBytes);
@@ -130,7 +164,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     mbar_init(&acc_empty[1], kEpiWarps);
     for (int s = 0; s < p.stages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kPair ? 2 : 1);
     }
     init_segment_count(p.cta_count, p.append != 0, cta_cnt, cta_sat);
     *epi_done = 0u;
@@ -140,11 +174,21 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_barrier();   // the peer's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int64_t n_items = p.n_items;
-  const int nb = p.n_ablk;
+  // work items: (R block, S chunk), S-chunk-major.  kPair: the pair's items
+  // are (R block pair, S chunk); this CTA takes block 2 bp + rank (a block
+  // past the end -- odd block count -- is a phantom: loaded, never emitted)
+  const uint32_t rank = kPair ? cta_rank_in_cluster() : 0u;
+  const int nb = kPair ? (p.n_ablk + 1) / 2 : p.n_ablk;
+  const int64_t n_items = kPair ? (int64_t)nb * (p.n_items / p.n_ablk) : p.n_items;
+  const int64_t item0 = kPair ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+  const int64_t item_step = kPair ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+  auto item_rb = [&](int64_t item) -> int64_t {
+    return kPair ? 2 * (item % nb) + rank : item % nb;
+  };
   const int nchunks = p.kpad / kKChunk;
   const size_t tile_elems = (size_t)kTileRows * p.kpad;
   const size_t chunk_elems = (size_t)kChunkBytes / 2;
@@ -156,8 +200,8 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       const uint64_t pol_b = policy_evict_normal();
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int64_t rb = item % nb, sc = item / nb;
+      for (int64_t item = item0; item < n_items; item += item_step) {
+        const int64_t rb = mn<int64_t>(item_rb(item), p.n_ablk - 1), sc = item / nb;
         const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
         for (int64_t t = t0; t < t1; t++) {
@@ -166,8 +210,12 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
             mbar_arrive_expect_tx(&full[s], 2 * kChunkBytes);
             uint8_t* dst = ring + (size_t)s * 2 * kChunkBytes;
             bulk_g2s(dst, p.a16 + rb * tile_elems + c * chunk_elems, kChunkBytes, &full[s], pol_a);
-            bulk_g2s(dst + kChunkBytes, p.b16 + t * tile_elems + c * chunk_elems, kChunkBytes,
-                     &full[s], pol_b);
+            if (!kPair)
+              bulk_g2s(dst + kChunkBytes, p.b16 + t * tile_elems + c * chunk_elems, kChunkBytes,
+                       &full[s], pol_b);
+            else if (rank == 0)   // the S chunk into both CTAs' slot s
+              bulk_g2s_mc(dst + kChunkBytes, p.b16 + t * tile_elems + c * chunk_elems, kChunkBytes,
+                          &full[s], (uint16_t)0x3, pol_b);
             if (++s == p.stages) {
               s = 0;
               ph ^= 1u;
@@ -186,7 +234,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     const uint64_t stage_step = (2 * kChunkBytes) >> 4, b_off = kChunkBytes >> 4;
     int s = 0;
     uint32_t ph = 0, tile_it = 0;
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int64_t item = item0; item < n_items; item += item_step) {
       const int64_t sc = item / nb;
       const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
@@ -206,7 +254,10 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
               tc_mma_f16_elect(tmem_base + h * 256, ad + h * half_step + kk * kstep,
                                 bd + kk * kstep, idesc, (c | kk) ? 1u : 0u);
           }
-          tc_commit_elect(&empty[s]);
+          if (kPair)
+            tc_commit_mc_elect(&empty[s], (uint16_t)0x3);   // both CTAs' slot s
+          else
+            tc_commit_elect(&empty[s]);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1u;
@@ -234,8 +285,8 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     const uint64_t seg_cap = p.seg_cap;
     uint32_t* toff = kFused ? nullptr : p.tile_off + (int64_t)blockIdx.x * p.tile_stride;
     uint32_t tile_it = 0;
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int64_t rb = item % nb, sc = item / nb;
+    for (int64_t item = item0; item < n_items; item += item_step) {
+      const int64_t rb = item_rb(item), sc = item / nb;   // rb >= n_ablk: phantom (no rows)
       const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       uint32_t fin0 = 0u, fin1 = 0u;   // tolerance emission: this lane's rows' final matches
@@ -296,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
           }
         }
       }
-      if (p.tol) {   // rows >= n_a never have finals
+      if (p.tol) {   // rows >= n_a (phantom blocks included) never have finals
         if (fin0) atomicAdd(p.rowcount + rb * kTileRows + lane_base + lane, fin0);
         if (fin1) atomicAdd(p.rowcount + rb * kTileRows + 128 + lane_base + lane, fin1);
       }
@@ -322,6 +373,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
     p.cta_count[blockIdx.x] = *cta_sat ? ~0ull >> 1 : (unsigned long long)*cta_cnt;
     if (p.tol) p.pend_count[blockIdx.x] = *pend_cnt;
   }
+  if (kPair) cluster_barrier();   // no peer multicast or commit targets an exited CTA
 }
 
 // ------------------------------------------------------------- recheck

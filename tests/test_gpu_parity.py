@@ -903,6 +903,32 @@ def test_bf16_overflow_retry_tensor_sims(cuda):
     assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_wide_pair_multicast(cuda, monkeypatch, pair):
+    """A/B: wide-path tensor sims with CTA pairs sharing each S chunk by TMA
+    multicast (SJB_WIDE_PAIR=1, built with -DSJB_AB_KERNELS=1; the default
+    library rejects the switch); odd R block counts give the last pair a
+    phantom block.  Same pair set as the oracle either way."""
+    from paper_2312_01476_b200 import _lib, device as D
+    if pair == "1" and not _lib.lib().sjb_ab_kernels():
+        L, S = _bf16_case(300, 500, 384, 12, 0.5, 30)
+        monkeypatch.setenv("SJB_WIDE_PAIR", pair)
+        with pytest.raises(_lib.SjbError, match="A/B kernel"):
+            D.join_prepared(D.prepare_bf16(_bf16_tensor(L, cuda)),
+                            D.prepare_bf16(_bf16_tensor(S, cuda)), 0.6, sims="tensor")
+        return
+    monkeypatch.setenv("SJB_WIDE_PAIR", pair)
+    for nl, nr, seed in ((600, 1700, 31), (1300, 2100, 32), (200, 900, 33)):
+        L, S = _bf16_case(nl, nr, 384, 12, 0.5, seed)
+        theta = 0.6
+        wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+        assert len(wl) > 0
+        pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+        lo, ro, so = D.join_prepared(pl, pr, theta, sims="tensor").to_host()
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (nl, nr)
+        assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
+
+
 def test_host_input_join_heavy_split(cuda, monkeypatch):
     """Output-heavy host-input joins split the left rows into 8 equal parts
     once the shape's previous result was large (join._result_bytes): the

@@ -1253,6 +1253,9 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     return SJB_OK;
   }
   if (pl.defer && use_rows_recheck(args, d_l32, d_r32)) {
+#if !SJB_AB_KERNELS
+    return ab_missing("SJB_DENSE_RECHECK=rows");
+#else
     // dense: group the candidates by left row; one warp per row sorts its
     // right offsets, rechecks them with bulk-copied S rows and compacts the
     // matches in place; then the match offsets and one copy to the columns
@@ -1305,6 +1308,7 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
                                                  args->out_cap, info);
     SJB_CK_LAUNCH("finalize");
     return SJB_OK;
+#endif
   }
   if (pl.defer) {
     // dense: group the candidates by left row, recheck them row-grouped,

@@ -478,6 +478,7 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+#if SJB_AB_KERNELS
 template <bool kG4>
 __global__ void __launch_bounds__(256, 1)
 recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
@@ -594,6 +595,9 @@ recheck_rows_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ ro
   }
 }
 
+#endif  // SJB_AB_KERNELS
+
+#if SJB_AB_KERNELS
 // Each row's matches (sorted, compacted at its candidate offset coff[i]) to
 // the MatchSet columns at its match offset moff[i]; rows that were too long
 // to sort go to the big-row list with their keys at moff[i] of bigkeys.
@@ -625,6 +629,8 @@ emit_rows_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
     }
   }
 }
+
+#endif  // SJB_AB_KERNELS
 
 // ----------------------------------- dense recheck, cluster-blocked rows
 // The staged per-candidate recheck above is bound by the bytes it can keep

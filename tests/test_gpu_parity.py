@@ -369,9 +369,8 @@ def test_tensor_join_devices(cuda, manifest, golden):
 
 def _set_recheck(monkeypatch, recheck):
     """fused | deferred (cluster-blocked rows: dense blocks share staged S
-    rows, sparse blocks per candidate) | deferred-rows (one warp per sorted
-    row, bulk-copied S rows) | deferred-grouped (the per-lane gather kernel);
-    the last two are kept for A/B."""
+    rows, sparse blocks per candidate) | deferred-grouped (the per-lane
+    gather kernel: the dim % 4 != 0 fallback, and the A/B baseline)."""
     monkeypatch.setenv("SJB_RECHECK", recheck.split("-")[0])
     if "-" in recheck:
         monkeypatch.setenv("SJB_DENSE_RECHECK", recheck.split("-")[1])
@@ -379,7 +378,7 @@ def _set_recheck(monkeypatch, recheck):
         monkeypatch.delenv("SJB_DENSE_RECHECK", raising=False)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-rows", "deferred-grouped"])
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
 def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
     """d <= 128: fused recheck warps and the deferred full-occupancy kernels
     give the same bits (golden cases, overflow retry, theta = -1)."""
@@ -395,6 +394,33 @@ def test_recheck_placements(cuda, manifest, golden, monkeypatch, recheck):
             lo, ro, so = m.to_host()
             assert np.array_equal(lo, golden[name + "_l"]) and np.array_equal(ro, golden[name + "_r"])
             assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
+
+
+def test_dense_rows_variant(cuda, manifest, golden, monkeypatch):
+    """A/B: the one-warp-per-sorted-row dense recheck (SJB_DENSE_RECHECK=rows,
+    per-lane 1-D copies or tile::gather4 of the S rows) -- built only with
+    -DSJB_AB_KERNELS=1; the default library must reject the switch."""
+    from paper_2312_01476_b200 import device as D
+    meta0 = manifest["cases"]["c_small"]
+    L0, S0 = case_inputs(meta0)
+    monkeypatch.setenv("SJB_RECHECK", "deferred")
+    if _ab_gate(D, monkeypatch, ("SJB_DENSE_RECHECK", "rows"), lambda: D.join_prepared(
+            D.prepare(torch.from_numpy(L0).to(cuda)), D.prepare(torch.from_numpy(S0).to(cuda)),
+            meta0["theta"])):
+        return
+    monkeypatch.setenv("SJB_DENSE_RECHECK", "rows")
+    for g4 in ("1", "0"):
+        monkeypatch.setenv("SJB_ROWS_G4", g4)
+        for name in ("cfg1", "c_small", "c_all", "c_d16_neg"):
+            meta = manifest["cases"][name]
+            L, S = case_inputs(meta)
+            for cap in (None, 300):
+                m = D.join_prepared(D.prepare(torch.from_numpy(L).to(cuda)),
+                                    D.prepare(torch.from_numpy(S).to(cuda)), meta["theta"],
+                                    cand_cap=cap)
+                lo, ro, so = m.to_host()
+                assert np.array_equal(lo, golden[name + "_l"]) and np.array_equal(ro, golden[name + "_r"])
+                assert np.array_equal(so.view(np.uint32), golden[name + "_s"].view(np.uint32))
 
 
 def _ab_gate(D, monkeypatch, variant, call):
@@ -468,7 +494,7 @@ def test_cosine_vm_e_selection_top_k(cuda, golden, manifest):
         top_k(model, embed_relation(model, rel), rel, "p", 0)
 
 
-@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-rows", "deferred-grouped"])
+@pytest.mark.parametrize("recheck", ["fused", "deferred", "deferred-grouped"])
 def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
     """Thousands of rows (several work items and S tiles per CTA, partial
     last tiles), dense and sparse thresholds, both recheck placements."""
@@ -534,8 +560,8 @@ def test_budget_and_thread_invariance(cuda, manifest, golden):
         assert _bits_equal(ms, golden["c_ragged_l"], golden["c_ragged_r"], golden["c_ragged_s"])
 
 
-@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (16, "deferred-rows"),
-                                         (16, "deferred-grouped"), (200, "fused")])
+@pytest.mark.parametrize("dim,recheck", [(16, "fused"), (16, "deferred"), (16, "deferred-grouped"),
+                                         (200, "fused")])
 def test_nan_and_inf_rows(cuda, monkeypatch, dim, recheck):
     """Rows with NaN or +-Inf normalise to NaN rows (inf / inf) exactly as the
     reference's normalize_row; their similarities are NaN, so they match

@@ -314,17 +314,12 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 // ------------------------------------------------------------ workspace
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
-      work, sig, desc, pos, total;
+      work, sig, desc, total;
   size_t pend, pendn;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// slot scratch of recheck_blocks_kernel: (union row, row) u16 per CTA, two
-// CTAs per SM
-size_t blk_pos_bytes() {
-  return (size_t)2 * sjb_sm_count(current_device()) * sjb::kBlkUnion * sjb::kBlkRows * 2;
-}
 
 JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride, bool defer) {
   JoinWs w;
@@ -348,8 +343,6 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride, boo
   w.work = o;     o = align256(o + 16);
   w.sig = o;      o = align256(o + nl * 4);   // dense recheck: row signatures
   w.desc = o;     o = align256(o + nl * 8);   // dense recheck: block descriptors
-  // dense recheck: per-CTA slot scratch of the blocked kernel (<= 2 CTAs per SM)
-  w.pos = o;      o = align256(o + (defer ? blk_pos_bytes() : 0));
   // tolerance emission: per-CTA pending slot lists + counts
   const bool tol = a->sims_mode == 1;
   w.pend = o;     o = align256(o + (tol ? ccap * 4 : 0));
@@ -862,7 +855,6 @@ struct JoinCtx {
   unsigned int* work;  // wide group recheck: dynamic item counter
   uint32_t* sig;       // dense recheck: row signatures (smallest right offset)
   uint64_t* desc;      // dense recheck: blocks (start | rows << 32)
-  uint16_t* pos;       // dense recheck: per-CTA slot scratch
   bool empty;  // n_left == 0 or n_right == 0
   uint32_t* pend;
   uint32_t* pend_count;
@@ -900,7 +892,6 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->work = reinterpret_cast<unsigned int*>(ws + w.work);
   c->sig = reinterpret_cast<uint32_t*>(ws + w.sig);
   c->desc = reinterpret_cast<uint64_t*>(ws + w.desc);
-  c->pos = reinterpret_cast<uint16_t*>(ws + w.pos);
   c->pend = reinterpret_cast<uint32_t*>(ws + w.pend);
   c->pend_count = reinterpret_cast<uint32_t*>(ws + w.pendn);
   return SJB_OK;
@@ -1230,15 +1221,14 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
                                                          sjb::kBlkThreads, bsmem));
     sjb::recheck_blocks_kernel<<<sms * std::min(2, std::max(1, per_sm)), sjb::kBlkThreads, bsmem,
                                  st>>>(c.keys, c.rowoff, c.bigrows, c.desc, c.work + 1, d_l32,
-                                       d_r32, (int)args->dim, args->theta, c.sims_bits, c.rowcount,
-                                       c.work, c.pos);
+                                       d_r32, (int)args->dim, args->theta, c.rowcount, c.work);
     SJB_CK_LAUNCH("recheck_blocks");
     // match offsets into `cursor`; `rowoff` keeps the candidate offsets
     if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
     sjb::gate_kernel<<<1, 1, 0, st>>>(c.cursor, nl, args->out_cap, c.nbig);
     SJB_CK_LAUNCH("gate");
     sjb::emit_sims_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(
-        c.keys, c.sims_bits, c.rowoff, c.cursor, nl, d_lefts, d_rights, d_sims, c.cand,
+        c.keys, c.rowoff, c.cursor, nl, d_lefts, d_rights, d_sims, c.cand,
         c.bigrows, c.nbig, args->left_base);
     SJB_CK_LAUNCH("emit_sims");
     const int big_smem = sjb::kSortBigCap * 8;

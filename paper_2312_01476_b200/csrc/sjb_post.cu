@@ -788,10 +788,10 @@ struct BlkShared {
   uint32_t uniq[kBlkUnion];
   uint32_t mask[kBlkUnion];
   uint64_t c0[kBlkRows];
-  uint32_t n[kBlkRows], off[kBlkRows], row[kBlkRows], kept[kBlkRows];
+  uint32_t n[kBlkRows], off[kBlkRows], row[kBlkRows], kept[kBlkRows], rank[2][kBlkRows];
   uint64_t sbar[kBlkWarps];
   uint64_t dbar;
-  uint32_t item, count, ucnt, ovf, big, cand, sorted;
+  uint32_t item, count, ucnt, ovf, big, cand;
 };
 __host__ __device__ inline int blk_smem_bytes(int dim) {
   return blk_stage_bytes(dim) + (int)sizeof(BlkShared) + 16;
@@ -802,9 +802,8 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
                       const uint32_t* __restrict__ perm, const uint64_t* __restrict__ desc,
                       const unsigned int* __restrict__ n_desc,
                       const float* __restrict__ l32, const float* __restrict__ r32, int dim,
-                      float theta, uint32_t* __restrict__ sims_out,
-                      uint32_t* __restrict__ rowcount, unsigned int* __restrict__ work,
-                      uint16_t* __restrict__ pos_scratch) {
+                      float theta, uint32_t* __restrict__ rowcount,
+                      unsigned int* __restrict__ work) {
   extern __shared__ __align__(16) uint8_t bsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int pitch = rows_pitch(dim, false), nq = dim >> 2;
@@ -814,7 +813,6 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
   const int win = blk_window_rows(dim);
   const uint32_t jcap = (uint32_t)blk_stage_bytes(dim) / 4;   // j cache entries
   uint32_t* jc = reinterpret_cast<uint32_t*>(bsm);
-  uint16_t* pos = pos_scratch + (size_t)blockIdx.x * kBlkUnion * kBlkRows;
   if (tid < kBlkWarps) mbar_init(&sh.sbar[tid], 1);
   if (tid == 0) mbar_init(&sh.dbar, 1);
   fence_mbar_init();
@@ -859,7 +857,6 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
         sh.cand = cand;
         sh.big = big ? 1u : 0u;
         sh.count = 0u;
-        sh.sorted = 0u;
         // the block's right offsets must fit the j cache (the staging area)
         sh.ovf = (big || cand > jcap) ? 1u : 0u;
       }
@@ -874,11 +871,19 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
     // mostly share their keys).
     auto hash_of = [](uint32_t j) { return (j * 0x9E3779B1u) >> (32 - kBlkHashBits); };
     if (!sh.ovf) {
-      // (a) each row sorted by right offset (registers; written back for
-      // the emission) into the j cache at off[r]
-      for (int r = warp; r < nrows; r += kBlkWarps)
-        if (sh.n[r]) sort_row_dispatch(keys, sh.c0[r], (int)sh.n[r], sh.row[r], jc + sh.off[r]);
-      if (tid == 0) sh.sorted = 1u;
+      // (a) the j cache, row by row (coalesced, four loads in flight)
+      for (int r = warp; r < nrows; r += kBlkWarps) {
+        const uint64_t c0 = sh.c0[r];
+        const uint32_t n = sh.n[r], off = sh.off[r];
+        for (uint32_t t0 = lane; t0 < n; t0 += 128) {
+          uint32_t j[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) j[e] = t0 + 32 * e < n ? (uint32_t)keys[c0 + t0 + 32 * e] : 0u;
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (t0 + 32 * e < n) jc[off + t0 + 32 * e] = j[e];
+        }
+      }
       __syncthreads();
       // (b) insert in cache order: the CTA's threads walk ~one row at a time,
       // so concurrent inserts are distinct keys, and the later rows mostly
@@ -914,22 +919,28 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
     }
 #endif
     if (dense) {
-      // union index u of every key (slot order), its row in uniq[u]
+      // the union sorted (ascending right offsets), each key's sorted index
+      // recorded in its hash slot
       if (tid == 0) sh.ucnt = 0u;
       __syncthreads();
       for (int h = tid; h < kBlkHash; h += kBlkThreads) {
         const uint32_t k = sh.hkeys[h];
-        if (k != kHashEmpty) {
-          const uint32_t u = atomicAdd(&sh.ucnt, 1u);
-          sh.uniq[u] = k;
-          sh.hidx[h] = (uint16_t)u;
-        }
+        if (k != kHashEmpty) sh.uniq[atomicAdd(&sh.ucnt, 1u)] = k;
       }
       for (uint32_t u = tid; u < U; u += kBlkThreads) sh.mask[u] = 0u;
       __syncthreads();
+      smem_bitonic<false>(sh.uniq, (int)U, tid, kBlkThreads);
+      __syncthreads();
+      for (uint32_t u = tid; u < U; u += kBlkThreads) {
+        const uint32_t j = sh.uniq[u];
+        uint32_t h = hash_of(j);
+        while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
+        sh.hidx[h] = (uint16_t)u;
+      }
+      if (tid < kBlkRows) sh.rank[0][tid] = 0u;
+      __syncthreads();
       BLK_MARK(3);
-      // membership: bit r of mask[u] <=> (row r, uniq[u]) is a candidate, at
-      // index pos[u][r] of row r's sorted candidates
+      // membership: bit r of mask[u] <=> (row r, uniq[u]) is a candidate
       {
         const uint32_t C = sh.cand;
         int r = 0;
@@ -938,9 +949,7 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
           const uint32_t j = jc[k];
           uint32_t h = hash_of(j);
           while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
-          const uint32_t u = sh.hidx[h];
-          atomicOr(&sh.mask[u], 1u << r);
-          pos[u * kBlkRows + r] = (uint16_t)(k - sh.off[r]);
+          atomicOr(&sh.mask[sh.hidx[h]], 1u << r);
         }
       }
       const float* Rs = stage;
@@ -948,6 +957,7 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
       const float4* R4 = reinterpret_cast<const float4*>(Rs + (size_t)lane * pitch);
       const uint64_t c0 = sh.c0[lane];
       uint32_t kept = 0;
+      int wpar = 0;
       for (uint32_t u0 = 0; u0 < U; u0 += (uint32_t)win) {
         const uint32_t u1 = mn<uint32_t>(U, u0 + (uint32_t)win);
         fence_proxy_async_smem();
@@ -967,17 +977,24 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
         mbar_wait(&sh.dbar, dphase);
         dphase ^= 1u;
         BLK_MARK(5);
-        // warp w: groups w, w + 8, .. of kBlkChains union rows; lane = row;
-        // a group's chains are independent and share the R row's reads
-        for (uint32_t u = u0 + kBlkChains * warp; u < u1; u += kBlkChains * kBlkWarps) {
-          uint32_t m[kBlkChains], any = 0u, t[kBlkChains];
+        // warp w: a contiguous run of the window's groups of kBlkChains union
+        // rows; lane = row.  The union is sorted, so row r's candidate at
+        // union row u is its rank-th: rank = bit r set in the masks before u
+        // (a running count); the chains of a group are independent and
+        // share the R row's reads.  Result: keys[c0 + rank] = j << 32 | sim.
+        const uint32_t groups = (u1 - u0 + kBlkChains - 1) / kBlkChains;
+        const uint32_t ua = mn<uint32_t>(u1, u0 + kBlkChains * (groups * warp / kBlkWarps));
+        const uint32_t ub = mn<uint32_t>(u1, u0 + kBlkChains * (groups * (warp + 1) / kBlkWarps));
+        uint32_t rank = sh.rank[wpar][lane];
+        for (uint32_t u = u0; u < ua; u++) rank += (sh.mask[u] >> lane) & 1u;
+        for (uint32_t u = ua; u < ub; u += kBlkChains) {
+          uint32_t m[kBlkChains], any = 0u;
           const float4* S4[kBlkChains];
 #pragma unroll
           for (int c = 0; c < kBlkChains; c++) {
-            const uint32_t uc = u + c < u1 ? u + c : u;
-            m[c] = u + c < u1 ? sh.mask[uc] : 0u;
+            const uint32_t uc = u + c < ub ? u + c : u;
+            m[c] = u + c < ub ? sh.mask[uc] : 0u;
             any |= m[c];
-            t[c] = ((m[c] >> lane) & 1u) ? pos[uc * kBlkRows + lane] : 0u;
             S4[c] = reinterpret_cast<const float4*>(Ss + (size_t)(uc - u0) * pitch);
           }
           if (any == 0u) continue;
@@ -1000,22 +1017,27 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
           for (int c = 0; c < kBlkChains; c++) {
             if ((m[c] >> lane) & 1u) {
               const bool ok = x[c] >= theta;
-              sims_out[c0 + t[c]] = ok ? __float_as_uint(x[c]) : kRejected;
+              keys[c0 + rank] = ((uint64_t)sh.uniq[u + c] << 32) |
+                                (ok ? __float_as_uint(x[c]) : kRejected);
+              rank++;
               kept += ok ? 1u : 0u;
             }
           }
         }
+        // the rank at the window's end, for the next window (the other
+        // parity: this window's readers may still be reading theirs)
+        if (warp == kBlkWarps - 1) sh.rank[wpar ^ 1][lane] = rank;
+        wpar ^= 1;
       }
       if (kept) atomicAdd(&sh.kept[lane], kept);
     } else {
       // ---- sparse block: per-candidate staged recheck, one warp per row
       float* buf = stage + (size_t)warp * 32 * pitch;
       float* myrow = buf + (size_t)lane * pitch;
-      const bool sorted = sh.sorted != 0u;
       for (int r = warp; r < nrows && warp < kBlkSparseWarps; r += kBlkSparseWarps) {
         const uint64_t c0 = sh.c0[r];
         const uint32_t n = sh.n[r];
-        if (!sorted && n > 0 && n <= (uint32_t)kRowSortCap) {
+        if (n > 0 && n <= (uint32_t)kRowSortCap) {
           sort_row_dispatch(keys, c0, (int)n, sh.row[r], nullptr);
           __syncwarp();   // (the batches below read the sorted keys back)
         }
@@ -1043,7 +1065,7 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
               x = __fmaf_rn(a.w, s.w, x);
             }
             const bool ok = x >= theta;
-            sims_out[c0 + k] = ok ? __float_as_uint(x) : kRejected;
+            keys[c0 + k] = ((uint64_t)j << 32) | (ok ? __float_as_uint(x) : kRejected);
             kept += ok ? 1u : 0u;
           }
         }
@@ -1058,12 +1080,12 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
   }
 }
 
-// Rechecked candidate slots (sorted rows; sims_bits or kRejected) compacted
-// into the MatchSet columns at the match offsets moff; big rows (unsorted)
-// go to the big-row list with (j << 32 | sim) keys at moff of bigkeys.
+// Rechecked candidate slots (j << 32 | sim bits or kRejected; rows sorted)
+// compacted into the MatchSet columns at the match offsets moff; big rows
+// (unsorted) go to the big-row list with their keys at moff of bigkeys.
 __global__ void __launch_bounds__(256)
-emit_sims_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sims_bits,
-                 const uint64_t* __restrict__ coff, const uint64_t* __restrict__ moff,
+emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ coff,
+                 const uint64_t* __restrict__ moff,
                  int64_t n_rows, uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                  float* __restrict__ sims, uint64_t* __restrict__ bigkeys,
                  uint32_t* __restrict__ big_rows, unsigned int* __restrict__ n_big,
@@ -1083,17 +1105,17 @@ emit_sims_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__
     uint64_t run = m0;
     for (uint64_t t0 = 0; t0 < n; t0 += 32) {
       const uint64_t t = t0 + lane;
-      const uint32_t sb = t < n ? sims_bits[c0 + t] : kRejected;
+      const uint64_t kv = t < n ? keys[c0 + t] : (uint64_t)kRejected;
+      const uint32_t sb = (uint32_t)kv;
       const bool ok = sb != kRejected;
       const uint32_t bal = __ballot_sync(0xffffffffu, ok);
       if (ok) {
         const uint64_t pos = run + __popc(bal & lt);
-        const uint32_t j = (uint32_t)keys[c0 + t];
         if (big) {
-          bigkeys[pos] = (uint64_t(j) << 32) | sb;
+          bigkeys[pos] = kv;
         } else {
           lefts[pos] = ir;
-          rights[pos] = j;
+          rights[pos] = kv >> 32;
           sims[pos] = __uint_as_float(sb);
         }
       }

@@ -314,7 +314,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
 // ------------------------------------------------------------ workspace
 struct JoinWs {
   size_t cand, sims, cta, rowcount, rowoff, cursor, keys, bsums, bigrows, nbig, tiles, ncand,
-      work, sig, desc, total;
+      work, sig, desc, ccnt, total;
   size_t pend, pendn;
 };
 
@@ -343,6 +343,7 @@ JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride, boo
   w.work = o;     o = align256(o + 16);
   w.sig = o;      o = align256(o + nl * 4);   // dense recheck: row signatures
   w.desc = o;     o = align256(o + nl * 8);   // dense recheck: block descriptors
+  w.ccnt = o;     o = align256(o + nl * 4);   // dense recheck: candidates per row
   // tolerance emission: per-CTA pending slot lists + counts
   const bool tol = a->sims_mode == 1;
   w.pend = o;     o = align256(o + (tol ? ccap * 4 : 0));
@@ -855,6 +856,7 @@ struct JoinCtx {
   unsigned int* work;  // wide group recheck: dynamic item counter
   uint32_t* sig;       // dense recheck: row signatures (smallest right offset)
   uint64_t* desc;      // dense recheck: blocks (start | rows << 32)
+  uint32_t* ccnt;      // dense recheck: candidates per row
   bool empty;  // n_left == 0 or n_right == 0
   uint32_t* pend;
   uint32_t* pend_count;
@@ -892,6 +894,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   c->work = reinterpret_cast<unsigned int*>(ws + w.work);
   c->sig = reinterpret_cast<uint32_t*>(ws + w.sig);
   c->desc = reinterpret_cast<uint64_t*>(ws + w.desc);
+  c->ccnt = reinterpret_cast<uint32_t*>(ws + w.ccnt);
   c->pend = reinterpret_cast<uint32_t*>(ws + w.pend);
   c->pend_count = reinterpret_cast<uint32_t*>(ws + w.pendn);
   return SJB_OK;
@@ -1185,59 +1188,68 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
   const uint64_t slots = (uint64_t)pl.grid * pl.seg_cap;
   uint64_t* keys = c.keys;
   if (pl.defer && use_rows_recheck(args, d_l32, d_r32) && dense_mode() == 0) {
-    // dense: group the candidates by left row, sort each row, order the rows
-    // by signature and recheck them in blocks of 32 (sjb_post.cu)
-    const dim3 sgrid(8, (unsigned)pl.grid);
+    // dense (sjb_post.cu): count per row (+ signature); order the rows by
+    // hashed signature and cut the order into blocks; lay the candidates out
+    // in that order (each block contiguous, right offsets only); recheck the
+    // blocks; match offsets; one pass to the MatchSet columns
     const int dev = current_device();
     const int sms = sjb_sm_count(dev);
+    const int fg = grid_for((uint64_t)nl, 256, 8);
     SJB_CK(cudaMemsetAsync(c.sig, 0xFF, (size_t)nl * 4, st));
+    SJB_CK(cudaMemsetAsync(c.ccnt, 0, (size_t)nl * 4, st));
     // chunks of 2048 candidates aggregated per row in shared memory; enough
     // CTAs per segment for ~4 per SM
     const dim3 agrid((unsigned)std::max(1, 4 * sms / pl.grid), (unsigned)pl.grid);
     sjb::count_rows_agg_kernel<<<agrid, sjb::kAggThreads, 0, st>>>(c.cand, pl.seg_cap, c.cta,
-                                                                   c.rowcount, c.sig);
+                                                                   c.ccnt, c.sig);
     SJB_CK_LAUNCH("count_rows_agg");
-    if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
-    sjb::group_rows_agg_kernel<<<agrid, sjb::kAggThreads, 0, st>>>(
-        c.cand, pl.seg_cap, c.cta, reinterpret_cast<unsigned long long*>(c.cursor), c.keys);
-    SJB_CK_LAUNCH("group_rows_agg");
-    // rows grouped by signature (hashed over nl buckets), order in bigrows
+    // the order: hashed signature buckets (perm in bigrows), blocks in desc
     const int shift = 0;
     SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
-    const int fg = grid_for((uint64_t)nl, 256, 8);
-    sjb::sig_hist_kernel<<<fg, 256, 0, st>>>(c.sig, c.rowoff, nl, shift, c.rowcount);
+    sjb::sig_hist_kernel<<<fg, 256, 0, st>>>(c.sig, c.ccnt, nl, shift, c.rowcount);
     SJB_CK_LAUNCH("sig_hist");
     if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
     sjb::sig_scatter_kernel<<<fg, 256, 0, st>>>(
-        c.sig, c.rowoff, nl, shift, reinterpret_cast<unsigned long long*>(c.cursor), c.bigrows);
+        c.sig, c.ccnt, nl, shift, reinterpret_cast<unsigned long long*>(c.cursor), c.bigrows);
     SJB_CK_LAUNCH("sig_scatter");
     SJB_CK(cudaMemsetAsync(c.work, 0, 8, st));   // [0] block counter, [1] blocks
     sjb::sig_blocks_kernel<<<fg, 256, 0, st>>>(c.rowcount, c.cursor, nl, c.desc, c.work + 1);
     SJB_CK_LAUNCH("sig_blocks");
+    // candidate offsets in the blocks' order (rowoff = poff), row starts in cursor
+    sjb::perm_counts_kernel<<<fg, 256, 0, st>>>(c.bigrows, c.ccnt, nl, c.rowcount);
+    SJB_CK_LAUNCH("perm_counts");
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, nullptr, c.bsums, st)) return rc;
+    sjb::perm_starts_kernel<<<fg, 256, 0, st>>>(c.bigrows, c.rowoff, nl, c.cursor);
+    SJB_CK_LAUNCH("perm_starts");
+    // right offsets grouped (u32, in the sims buffer: the filter wrote none)
+    sjb::group_rows_agg_kernel<uint32_t><<<agrid, sjb::kAggThreads, 0, st>>>(
+        c.cand, pl.seg_cap, c.cta, reinterpret_cast<unsigned long long*>(c.cursor), c.sims_bits);
+    SJB_CK_LAUNCH("group_rows_agg");
     const int bsmem = sjb::blk_smem_bytes((int)args->dim);
     if (int rc = set_smem_attr((const void*)sjb::recheck_blocks_kernel, bsmem)) return rc;
     int per_sm = 0;
     SJB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sjb::recheck_blocks_kernel,
                                                          sjb::kBlkThreads, bsmem));
     sjb::recheck_blocks_kernel<<<sms * std::min(2, std::max(1, per_sm)), sjb::kBlkThreads, bsmem,
-                                 st>>>(c.keys, c.rowoff, c.bigrows, c.desc, c.work + 1, d_l32,
-                                       d_r32, (int)args->dim, args->theta, c.rowcount, c.work);
+                                 st>>>(c.sims_bits, c.rowoff, c.ccnt, c.keys, c.bigrows, c.desc,
+                                       c.work + 1, d_l32, d_r32, (int)args->dim, args->theta,
+                                       c.rowcount, c.work);
     SJB_CK_LAUNCH("recheck_blocks");
-    // match offsets into `cursor`; `rowoff` keeps the candidate offsets
-    if (int rc = run_scan(c.rowcount, nl, c.cursor, nullptr, c.bsums, st)) return rc;
-    sjb::gate_kernel<<<1, 1, 0, st>>>(c.cursor, nl, args->out_cap, c.nbig);
+    // match offsets (row order) into `rowoff`; `cursor` holds the rows' candidate ends
+    if (int rc = run_scan(c.rowcount, nl, c.rowoff, nullptr, c.bsums, st)) return rc;
+    sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);
     SJB_CK_LAUNCH("gate");
     sjb::emit_sims_kernel<<<grid_for((uint64_t)nl * 32, 256, 8), 256, 0, st>>>(
-        c.keys, c.rowoff, c.cursor, nl, d_lefts, d_rights, d_sims, c.cand,
-        c.bigrows, c.nbig, args->left_base);
+        c.keys, c.cursor, c.ccnt, c.rowoff, nl, d_lefts, d_rights, d_sims, c.cand, c.bigrows,
+        c.nbig, args->left_base);
     SJB_CK_LAUNCH("emit_sims");
     const int big_smem = sjb::kSortBigCap * 8;
     if (int rc = set_smem_attr((const void*)sjb::segsort_big_kernel, big_smem)) return rc;
     sjb::segsort_big_kernel<<<sms, sjb::kSortBigThreads, big_smem, st>>>(
-        c.cursor, c.cand, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base,
+        c.rowoff, c.cand, d_lefts, d_rights, d_sims, c.bigrows, c.nbig, args->left_base,
         args->n_right);
     SJB_CK_LAUNCH("segsort_big");
-    sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.cursor, nl,
+    sjb::join_finalize_kernel<<<1, 256, 0, st>>>(c.cta, pl.grid, pl.seg_cap, c.rowoff, nl,
                                                  args->out_cap, info);
     SJB_CK_LAUNCH("finalize");
     return SJB_OK;

@@ -252,10 +252,13 @@ count_rows_agg_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
   }
 }
 
+// OutT = uint32_t: only the right offset is stored (the dense recheck's
+// grouped array: rows at cursor-given offsets, the row known from them)
+template <class OutT>
 __global__ void __launch_bounds__(kAggThreads)
 group_rows_agg_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
                       const unsigned long long* __restrict__ cta_count,
-                      unsigned long long* __restrict__ cursor, uint64_t* __restrict__ grouped) {
+                      unsigned long long* __restrict__ cursor, OutT* __restrict__ grouped) {
   __shared__ uint32_t hcnt[kAggSpan];
   __shared__ unsigned long long hbase[kAggSpan];
   __shared__ uint32_t s_mm[2];
@@ -297,13 +300,13 @@ group_rows_agg_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
 #pragma unroll
       for (int e = 0; e < kAggPer; e++) {
         const int k = threadIdx.x + kAggThreads * e;
-        if (k < n) grouped[hbase[(uint32_t)(u[e] >> 32) - rmin] + rank[e]] = u[e];
+        if (k < n) grouped[hbase[(uint32_t)(u[e] >> 32) - rmin] + rank[e]] = (OutT)u[e];
       }
     } else {
 #pragma unroll
       for (int e = 0; e < kAggPer; e++) {
         const int k = threadIdx.x + kAggThreads * e;
-        if (k < n) grouped[atomicAdd(cursor + (uint32_t)(u[e] >> 32), 1ull)] = u[e];
+        if (k < n) grouped[atomicAdd(cursor + (uint32_t)(u[e] >> 32), 1ull)] = (OutT)u[e];
       }
     }
     __syncthreads();
@@ -699,58 +702,73 @@ __device__ __forceinline__ uint32_t sig_bucket(uint32_t s, int shift, int64_t nb
   return (uint32_t)(((uint64_t)h * (uint64_t)(nbk - 1)) >> 32);
 }
 // empty rows and rows above kRowSortCap candidates share the last bucket
-__device__ __forceinline__ uint32_t row_sig(const uint32_t* sig, const uint64_t* rowoff,
+__device__ __forceinline__ uint32_t row_sig(const uint32_t* sig, const uint32_t* ccnt,
                                             int64_t i) {
-  const uint64_t n = rowoff[i + 1] - rowoff[i];
-  return (n == 0 || n > (uint64_t)kRowSortCap) ? ~0u : sig[i];
+  const uint32_t n = ccnt[i];
+  return (n == 0 || n > (uint32_t)kRowSortCap) ? ~0u : sig[i];
 }
 __global__ void sig_hist_kernel(const uint32_t* __restrict__ sig,
-                                const uint64_t* __restrict__ rowoff, int64_t n, int shift,
+                                const uint32_t* __restrict__ ccnt, int64_t n, int shift,
                                 uint32_t* __restrict__ hist) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(hist + sig_bucket(row_sig(sig, rowoff, i), shift, n), 1u);
+    atomicAdd(hist + sig_bucket(row_sig(sig, ccnt, i), shift, n), 1u);
 }
 __global__ void sig_scatter_kernel(const uint32_t* __restrict__ sig,
-                                   const uint64_t* __restrict__ rowoff, int64_t n, int shift,
+                                   const uint32_t* __restrict__ ccnt, int64_t n, int shift,
                                    unsigned long long* __restrict__ cursor,
                                    uint32_t* __restrict__ perm) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    perm[atomicAdd(cursor + sig_bucket(row_sig(sig, rowoff, i), shift, n), 1ull)] = (uint32_t)i;
+    perm[atomicAdd(cursor + sig_bucket(row_sig(sig, ccnt, i), shift, n), 1ull)] = (uint32_t)i;
 }
 
-// keys[c0 .. c0 + n) (row i) sorted by right offset in registers (n <= 32 E),
-// written back in place and, when list != nullptr, their j's to list[0..n)
+// Candidate offsets in the order of the blocks: pcnt[p] = ccnt[perm[p]]
+// (scanned into poff), then each row's start: start[perm[p]] = poff[p].  The
+// grouping then lays every block's candidates out contiguously.
+__global__ void perm_counts_kernel(const uint32_t* __restrict__ perm,
+                                   const uint32_t* __restrict__ ccnt, int64_t n,
+                                   uint32_t* __restrict__ pcnt) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    pcnt[p] = ccnt[perm[p]];
+}
+__global__ void perm_starts_kernel(const uint32_t* __restrict__ perm,
+                                   const uint64_t* __restrict__ poff, int64_t n,
+                                   uint64_t* __restrict__ start) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    start[perm[p]] = poff[p];
+}
+
+// the u32 right offsets g[c0 .. c0 + n) sorted in place (registers)
 template <int E>
-__device__ __forceinline__ void sort_row_back(uint64_t* __restrict__ keys, uint64_t c0, int n,
-                                              uint32_t i, uint32_t* list) {
+__device__ __forceinline__ void sort_js_back(uint32_t* __restrict__ g, uint64_t c0, int n) {
   const int lane = threadIdx.x & 31;
   uint32_t v[E];
 #pragma unroll
   for (int r = 0; r < E; r++) {
     const int t = 32 * r + lane;
-    v[r] = t < n ? (uint32_t)keys[c0 + t] : ~0u;
+    v[r] = t < n ? g[c0 + t] : ~0u;
   }
   warp_sort_u32<E>(v);
-  const uint64_t hi = (uint64_t)i << 32;
 #pragma unroll
   for (int r = 0; r < E; r++) {
     const int t = 32 * r + lane;
-    if (t < n) {
-      keys[c0 + t] = hi | v[r];
-      if (list) list[t] = v[r];
-    }
+    if (t < n) g[c0 + t] = v[r];
   }
 }
-__device__ __forceinline__ void sort_row_dispatch(uint64_t* keys, uint64_t c0, int m, uint32_t i,
-                                                  uint32_t* list) {
-  if (m <= 32) sort_row_back<1>(keys, c0, m, i, list);
-  else if (m <= 64) sort_row_back<2>(keys, c0, m, i, list);
-  else if (m <= 128) sort_row_back<4>(keys, c0, m, i, list);
-  else if (m <= 256) sort_row_back<8>(keys, c0, m, i, list);
-  else if (m <= 512) sort_row_back<16>(keys, c0, m, i, list);
-  else sort_row_back<32>(keys, c0, m, i, list);
+__device__ __forceinline__ void sort_js_dispatch(uint32_t* g, uint64_t c0, int m) {
+  if (m <= 32) sort_js_back<1>(g, c0, m);
+  else if (m <= 64) sort_js_back<2>(g, c0, m);
+  else if (m <= 128) sort_js_back<4>(g, c0, m);
+  else if (m <= 256) sort_js_back<8>(g, c0, m);
+  else if (m <= 512) sort_js_back<16>(g, c0, m);
+  else sort_js_back<32>(g, c0, m);
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // Blocks never span two buckets: bucket b (rows [end_b - cnt_b, end_b) of
@@ -791,14 +809,15 @@ struct BlkShared {
   uint32_t n[kBlkRows], off[kBlkRows], row[kBlkRows], kept[kBlkRows], rank[2][kBlkRows];
   uint64_t sbar[kBlkWarps];
   uint64_t dbar;
-  uint32_t item, count, ucnt, ovf, big, cand;
+  uint32_t item, next, count, ucnt, ovf, big, cand;
 };
 __host__ __device__ inline int blk_smem_bytes(int dim) {
   return blk_stage_bytes(dim) + (int)sizeof(BlkShared) + 16;
 }
 
 __global__ void __launch_bounds__(kBlkThreads)
-recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ rowoff,
+recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ poff,
+                      const uint32_t* __restrict__ ccnt, uint64_t* __restrict__ keys,
                       const uint32_t* __restrict__ perm, const uint64_t* __restrict__ desc,
                       const unsigned int* __restrict__ n_desc,
                       const float* __restrict__ l32, const float* __restrict__ r32, int dim,
@@ -822,22 +841,36 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
 #if SJB_BLK_STATS
   long long t_mark = clock64();
 #endif
+  const unsigned int nd = *n_desc;
+  if (tid == 0) sh.next = atomicAdd(work, 1u);
   for (;;) {
-    if (tid == 0) sh.item = atomicAdd(work, 1u);
+    if (tid == 0) {
+      sh.item = sh.next;
+      sh.next = atomicAdd(work, 1u);
+    }
     if (tid < kBlkRows) sh.kept[tid] = 0u;
     __syncthreads();
     BLK_MARK(0);
-    if (sh.item >= *n_desc) break;
+    if (sh.item >= nd) break;
     const uint64_t dsc = desc[sh.item];
     const int64_t p0 = (int64_t)(uint32_t)dsc;
     const int nrows = (int)(dsc >> 32);
+    if (tid == 32 && sh.next < nd) {
+      // the next block's candidates (contiguous in the blocks' order) on
+      // their way to L2 while this block runs
+      const uint64_t dn = desc[sh.next];
+      const int64_t q0 = (int64_t)(uint32_t)dn;
+      const uint64_t a = poff[q0] & ~3ull, b = (poff[q0 + (int64_t)(dn >> 32)] + 3) & ~3ull;
+      for (uint64_t x = a; x < b; x += 8192)
+        prefetch_l2_bulk(g32 + x, (uint32_t)mn<uint64_t>(32768, (b - x) * 4));
+    }
     if (tid < kBlkRows) {
       uint32_t i = 0, n = 0;
       uint64_t c0 = 0;
       if (tid < nrows) {
         i = perm[p0 + tid];
-        c0 = rowoff[i];
-        n = (uint32_t)mn<uint64_t>(rowoff[i + 1] - c0, 0xFFFFFFFFull);
+        c0 = poff[p0 + tid];
+        n = ccnt[i];
       }
       sh.row[tid] = i;
       sh.c0[tid] = c0;
@@ -857,8 +890,9 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
         sh.cand = cand;
         sh.big = big ? 1u : 0u;
         sh.count = 0u;
-        // the block's right offsets must fit the j cache (the staging area)
-        sh.ovf = (big || cand > jcap) ? 1u : 0u;
+        // the block's right offsets (+ 16-byte alignment slack) must fit
+        // the j cache (the staging area)
+        sh.ovf = (big || cand == 0 || cand + 8 > jcap) ? 1u : 0u;
       }
     }
     for (int h = tid; h < kBlkHash; h += kBlkThreads) sh.hkeys[h] = kHashEmpty;
@@ -870,28 +904,26 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
     // before inserting them, and looks before it CASes (the rows of a block
     // mostly share their keys).
     auto hash_of = [](uint32_t j) { return (j * 0x9E3779B1u) >> (32 - kBlkHashBits); };
+    const uint32_t jhead = (uint32_t)(sh.c0[0] & 3u);
+    const uint32_t* jcb = jc + jhead;
     if (!sh.ovf) {
-      // (a) the j cache, row by row (coalesced, four loads in flight)
-      for (int r = warp; r < nrows; r += kBlkWarps) {
-        const uint64_t c0 = sh.c0[r];
-        const uint32_t n = sh.n[r], off = sh.off[r];
-        for (uint32_t t0 = lane; t0 < n; t0 += 128) {
-          uint32_t j[4];
-#pragma unroll
-          for (int e = 0; e < 4; e++) j[e] = t0 + 32 * e < n ? (uint32_t)keys[c0 + t0 + 32 * e] : 0u;
-#pragma unroll
-          for (int e = 0; e < 4; e++)
-            if (t0 + 32 * e < n) jc[off + t0 + 32 * e] = j[e];
-        }
+      // (a) the j cache: the block's candidates are contiguous (grouped in
+      // the blocks' order) -- one bulk copy of the 16-byte aligned span;
+      // candidate k of the block is jcb[k]
+      if (tid == 0) {
+        const uint32_t bytes = ((jhead + sh.cand + 3) & ~3u) * 4;
+        mbar_arrive_expect_tx(&sh.dbar, bytes);
+        bulk_g2s(jc, g32 + (sh.c0[0] - jhead), bytes, &sh.dbar, pol);
       }
-      __syncthreads();
+      mbar_wait(&sh.dbar, dphase);
+      dphase ^= 1u;
       // (b) insert in cache order: the CTA's threads walk ~one row at a time,
       // so concurrent inserts are distinct keys, and the later rows mostly
       // find theirs (a read, no CAS)
       const uint32_t C = sh.cand;
       for (uint32_t k = tid; k < C; k += kBlkThreads) {
         if (*(volatile uint32_t*)&sh.ovf) break;
-        const uint32_t j = jc[k];
+        const uint32_t j = jcb[k];
         uint32_t h = hash_of(j);
         for (;;) {
           uint32_t cur = sh.hkeys[h];
@@ -946,7 +978,7 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
         int r = 0;
         for (uint32_t k = tid; k < C; k += kBlkThreads) {
           while (r + 1 < nrows && k >= sh.off[r + 1]) r++;
-          const uint32_t j = jc[k];
+          const uint32_t j = jcb[k];
           uint32_t h = hash_of(j);
           while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
           atomicOr(&sh.mask[sh.hidx[h]], 1u << r);
@@ -1038,14 +1070,14 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
         const uint64_t c0 = sh.c0[r];
         const uint32_t n = sh.n[r];
         if (n > 0 && n <= (uint32_t)kRowSortCap) {
-          sort_row_dispatch(keys, c0, (int)n, sh.row[r], nullptr);
-          __syncwarp();   // (the batches below read the sorted keys back)
+          sort_js_dispatch(g32, c0, (int)n);
+          __syncwarp();   // (the batches below read the sorted offsets back)
         }
         const float4* a4 = reinterpret_cast<const float4*>(l32 + (size_t)sh.row[r] * dim);
         uint32_t kept = 0;
         for (uint32_t b0 = 0; b0 < n; b0 += 32) {
           const uint32_t k = b0 + lane, cnt = mn<uint32_t>(32u, n - b0);
-          const uint32_t j = k < n ? (uint32_t)keys[c0 + k] : 0u;
+          const uint32_t j = k < n ? g32[c0 + k] : 0u;
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive_expect_tx(&sh.sbar[warp], cnt * rowbytes);
@@ -1080,12 +1112,13 @@ recheck_blocks_kernel(uint64_t* __restrict__ keys, const uint64_t* __restrict__ 
   }
 }
 
-// Rechecked candidate slots (j << 32 | sim bits or kRejected; rows sorted)
-// compacted into the MatchSet columns at the match offsets moff; big rows
-// (unsorted) go to the big-row list with their keys at moff of bigkeys.
+// Rechecked candidate slots (j << 32 | sim bits or kRejected; rows sorted;
+// row i's at [cend[i] - ccnt[i], cend[i])) compacted into the MatchSet
+// columns at the match offsets moff; big rows (unsorted) go to the big-row
+// list with their keys at moff of bigkeys.
 __global__ void __launch_bounds__(256)
-emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ coff,
-                 const uint64_t* __restrict__ moff,
+emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ cend,
+                 const uint32_t* __restrict__ ccnt, const uint64_t* __restrict__ moff,
                  int64_t n_rows, uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                  float* __restrict__ sims, uint64_t* __restrict__ bigkeys,
                  uint32_t* __restrict__ big_rows, unsigned int* __restrict__ n_big,
@@ -1098,7 +1131,7 @@ emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
        i += (int64_t)gridDim.x * wpb) {
     const uint64_t m0 = moff[i];
     if (moff[i + 1] == m0) continue;
-    const uint64_t c0 = coff[i], n = coff[i + 1] - c0;
+    const uint64_t n = ccnt[i], c0 = cend[i] - n;   // rows laid out in the blocks' order
     const bool big = n > (uint64_t)kRowSortCap;
     if (big && lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
     const uint64_t ir = left_base + (uint64_t)i;

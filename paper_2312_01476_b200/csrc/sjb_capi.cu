@@ -1198,8 +1198,10 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     SJB_CK(cudaMemsetAsync(c.sig, 0xFF, (size_t)nl * 4, st));
     SJB_CK(cudaMemsetAsync(c.ccnt, 0, (size_t)nl * 4, st));
     // chunks of 2048 candidates aggregated per row in shared memory; enough
-    // CTAs per segment for ~4 per SM
-    const dim3 agrid((unsigned)std::max(1, 4 * sms / pl.grid), (unsigned)pl.grid);
+    // CTAs per segment for kAggCtasPerSm per SM (SJB_AGG_CTAS overrides)
+    const char* acv = getenv("SJB_AGG_CTAS");
+    const int kAggCtasPerSm = acv ? std::max(1, atoi(acv)) : 16;
+    const dim3 agrid((unsigned)std::max(1, kAggCtasPerSm * sms / pl.grid), (unsigned)pl.grid);
     sjb::count_rows_agg_kernel<<<agrid, sjb::kAggThreads, 0, st>>>(c.cand, pl.seg_cap, c.cta,
                                                                    c.ccnt, c.sig);
     SJB_CK_LAUNCH("count_rows_agg");

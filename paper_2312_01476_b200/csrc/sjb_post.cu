@@ -800,6 +800,57 @@ __host__ __device__ inline int blk_stage_bytes(int dim) {
   return kBlkStage * rows_pitch(dim, false) * 4;
 }
 __host__ __device__ inline int blk_window_rows(int dim) { return kBlkStage - kBlkRows; }
+// Sort a[0 .. U) (U <= kBlkUnion, u32, distinct keys; tmp: kBlkUnion
+// words, clobbered) by kBlkThreads threads: each warp sorts a run of 128 in
+// registers (bitonic, no barriers), then runs merge pairwise (128 -> 1024):
+// an element's place = its index + its rank in the other run (lower bound
+// from the left run, upper bound from the right: the ~0 padding ties stay
+// stable).  Three barriers per round instead of the 55 stages of a shared
+// bitonic network.  Leaves the result in a.
+__device__ void block_sort_u32(uint32_t* a, uint32_t* tmp, int U) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Up = (U + 127) & ~127;
+  if (warp * 128 < Up) {
+    uint32_t v[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const int k = warp * 128 + 32 * r + lane;
+      v[r] = k < U ? a[k] : ~0u;
+    }
+    warp_sort_u32<4>(v);
+#pragma unroll
+    for (int r = 0; r < 4; r++) a[warp * 128 + 32 * r + lane] = v[r];
+  }
+  __syncthreads();
+  uint32_t* src = a;
+  uint32_t* dst = tmp;
+  for (int L = 128; L < Up; L <<= 1) {
+    for (int k = tid; k < Up; k += kBlkThreads) {
+      const int base = k & ~(2 * L - 1), off = k - base;
+      const bool left = off < L;
+      const uint32_t x = src[k];
+      // rank of x in the other run (bounded by the elements that exist)
+      const int ob = left ? base + L : base;
+      const int on = left ? min(L, Up - (base + L)) : L;
+      int lo = 0, hi = max(on, 0);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t y = src[ob + mid];
+        if (left ? (y < x) : (y <= x)) lo = mid + 1; else hi = mid;
+      }
+      dst[base + (left ? off : off - L) + lo] = x;
+    }
+    __syncthreads();
+    uint32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != a) {
+    for (int k = tid; k < U; k += kBlkThreads) a[k] = src[k];
+    __syncthreads();
+  }
+}
+
 struct BlkShared {
   uint32_t hkeys[kBlkHash];
   uint16_t hidx[kBlkHash];
@@ -959,10 +1010,9 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
         const uint32_t k = sh.hkeys[h];
         if (k != kHashEmpty) sh.uniq[atomicAdd(&sh.ucnt, 1u)] = k;
       }
+      __syncthreads();
+      block_sort_u32(sh.uniq, sh.mask, (int)U);   // (mask: scratch, zeroed next)
       for (uint32_t u = tid; u < U; u += kBlkThreads) sh.mask[u] = 0u;
-      __syncthreads();
-      smem_bitonic<false>(sh.uniq, (int)U, tid, kBlkThreads);
-      __syncthreads();
       for (uint32_t u = tid; u < U; u += kBlkThreads) {
         const uint32_t j = sh.uniq[u];
         uint32_t h = hash_of(j);
@@ -1136,23 +1186,31 @@ emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
     if (big && lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
     const uint64_t ir = left_base + (uint64_t)i;
     uint64_t run = m0;
-    for (uint64_t t0 = 0; t0 < n; t0 += 32) {
-      const uint64_t t = t0 + lane;
-      const uint64_t kv = t < n ? keys[c0 + t] : (uint64_t)kRejected;
-      const uint32_t sb = (uint32_t)kv;
-      const bool ok = sb != kRejected;
-      const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const uint64_t pos = run + __popc(bal & lt);
-        if (big) {
-          bigkeys[pos] = kv;
-        } else {
-          lefts[pos] = ir;
-          rights[pos] = kv >> 32;
-          sims[pos] = __uint_as_float(sb);
-        }
+    // four 32-candidate chunks per step: their loads in flight together
+    for (uint64_t t0 = 0; t0 < n; t0 += 128) {
+      uint64_t kv[4];
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const uint64_t t = t0 + 32 * e + lane;
+        kv[e] = t < n ? keys[c0 + t] : (uint64_t)kRejected;
       }
-      run += __popc(bal);
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const uint32_t sb = (uint32_t)kv[e];
+        const bool ok = sb != kRejected;
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+          const uint64_t pos = run + __popc(bal & lt);
+          if (big) {
+            bigkeys[pos] = kv[e];
+          } else {
+            lefts[pos] = ir;
+            rights[pos] = kv[e] >> 32;
+            sims[pos] = __uint_as_float(sb);
+          }
+        }
+        run += __popc(bal);
+      }
     }
   }
 }

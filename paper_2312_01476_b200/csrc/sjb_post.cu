@@ -790,10 +790,10 @@ __global__ void sig_blocks_kernel(const uint32_t* __restrict__ hist,
   }
 }
 
-// shared memory: staging area of kBlkStage rows (sparse: warps 0..5 x 32
-// rows; dense: 32 R rows + a window of 168 union S rows), then the fixed
-// part (33 KB): 113 KB at d = 100, two CTAs per SM
-constexpr int kBlkStage = 200;
+// shared memory: staging area of kBlkStage rows (sparse: warps 0..4 x 32
+// rows; dense: 32 R rows + a window of 148 union S rows), then the fixed
+// part (41 KB): 113 KB at d = 100, two CTAs per SM
+constexpr int kBlkStage = 180;
 constexpr int kBlkSparseWarps = kBlkStage / 32;
 static_assert(kBlkStage + kBlkRows <= kBlkThreads, "one copy-issuing thread per staged row");
 __host__ __device__ inline int blk_stage_bytes(int dim) {
@@ -853,7 +853,7 @@ __device__ void block_sort_u32(uint32_t* a, uint32_t* tmp, int U) {
 
 struct BlkShared {
   uint32_t hkeys[kBlkHash];
-  uint16_t hidx[kBlkHash];
+  uint32_t hmask[kBlkHash];   // per hash slot: bit r <=> row r has the key
   uint32_t uniq[kBlkUnion];
   uint32_t mask[kBlkUnion];
   uint64_t c0[kBlkRows];
@@ -946,7 +946,10 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
         sh.ovf = (big || cand == 0 || cand + 8 > jcap) ? 1u : 0u;
       }
     }
-    for (int h = tid; h < kBlkHash; h += kBlkThreads) sh.hkeys[h] = kHashEmpty;
+    for (int h = tid; h < kBlkHash; h += kBlkThreads) {
+      sh.hkeys[h] = kHashEmpty;
+      sh.hmask[h] = 0u;
+    }
     __syncthreads();
     BLK_MARK(1);
     // ---- union of the block's right offsets: a shared-memory hash set
@@ -971,9 +974,13 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
       // (b) insert in cache order: the CTA's threads walk ~one row at a time,
       // so concurrent inserts are distinct keys, and the later rows mostly
       // find theirs (a read, no CAS)
+      // and each candidate's row bit set in its key's slot (the membership
+      // masks, indexed by slot until the union is sorted)
       const uint32_t C = sh.cand;
+      int r = 0;
       for (uint32_t k = tid; k < C; k += kBlkThreads) {
         if (*(volatile uint32_t*)&sh.ovf) break;
+        while (r + 1 < nrows && k >= sh.off[r + 1]) r++;
         const uint32_t j = jcb[k];
         uint32_t h = hash_of(j);
         for (;;) {
@@ -988,6 +995,7 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
           if (cur == j) break;
           h = (h + 1) & (kBlkHash - 1);
         }
+        atomicOr(&sh.hmask[h], 1u << r);
       }
     }
     __syncthreads();
@@ -1011,29 +1019,18 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
         if (k != kHashEmpty) sh.uniq[atomicAdd(&sh.ucnt, 1u)] = k;
       }
       __syncthreads();
-      block_sort_u32(sh.uniq, sh.mask, (int)U);   // (mask: scratch, zeroed next)
-      for (uint32_t u = tid; u < U; u += kBlkThreads) sh.mask[u] = 0u;
+      block_sort_u32(sh.uniq, sh.mask, (int)U);   // (mask: scratch, written next)
+      // membership in sorted order: bit r of mask[u] <=> (row r, uniq[u]) is
+      // a candidate
       for (uint32_t u = tid; u < U; u += kBlkThreads) {
         const uint32_t j = sh.uniq[u];
         uint32_t h = hash_of(j);
         while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
-        sh.hidx[h] = (uint16_t)u;
+        sh.mask[u] = sh.hmask[h];
       }
       if (tid < kBlkRows) sh.rank[0][tid] = 0u;
       __syncthreads();
       BLK_MARK(3);
-      // membership: bit r of mask[u] <=> (row r, uniq[u]) is a candidate
-      {
-        const uint32_t C = sh.cand;
-        int r = 0;
-        for (uint32_t k = tid; k < C; k += kBlkThreads) {
-          while (r + 1 < nrows && k >= sh.off[r + 1]) r++;
-          const uint32_t j = jcb[k];
-          uint32_t h = hash_of(j);
-          while (sh.hkeys[h] != j) h = (h + 1) & (kBlkHash - 1);
-          atomicOr(&sh.mask[sh.hidx[h]], 1u << r);
-        }
-      }
       const float* Rs = stage;
       const float* Ss = stage + (size_t)kBlkRows * pitch;
       const float4* R4 = reinterpret_cast<const float4*>(Rs + (size_t)lane * pitch);

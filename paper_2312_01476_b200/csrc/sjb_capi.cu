@@ -150,7 +150,7 @@ int make_wide_plan(const sjb_join_args* a, JoinPlan* pl, int sms, int max_smem) 
   pl->a_tiles = 1;
   int stages = 0;
   const bool tol = a->sims_mode == 1;
-  while (stages < 6 && (int)W::smem_bytes(stages + 1, tol) <= max_smem) stages++;
+  while (stages < W::kMaxStages && (int)W::smem_bytes(stages + 1, tol) <= max_smem) stages++;
   if (stages < 2) return fail(SJB_E_UNSUPPORTED, "not enough shared memory for the wide kernel");
   pl->stages = stages;
   pl->smem = W::smem_bytes(stages, tol);

@@ -38,7 +38,11 @@ struct Cfg {
   static constexpr int kRecheckWarps = kFused ? 10 : 0;
   static constexpr int kThreads = 32 * (2 + kEpiWarps + kRecheckWarps);
 };
-constexpr int kKChunk = 64;                           // K elements per stage
+#ifndef SJB_WIDE_KCHUNK
+#define SJB_WIDE_KCHUNK 64
+#endif
+constexpr int kKChunk = SJB_WIDE_KCHUNK;              // K elements per stage
+constexpr int kMaxStages = 6 * 64 / kKChunk;          // ring depth cap (same bytes)
 constexpr int kChunkBytes = kTileRows * kKChunk * 2;  // 32 KB per operand
 
 struct Params {

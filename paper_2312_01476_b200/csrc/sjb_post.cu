@@ -161,7 +161,10 @@ __global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t se
 // arrays with one atomic per distinct row, and the grouping reserves each
 // row's run of the chunk with one returning atomic (local ranks from the
 // shared counters).  Wider chunks fall back to per-candidate atomics.
-constexpr int kAggThreads = 256;
+#ifndef SJB_AGG_THREADS
+#define SJB_AGG_THREADS 256
+#endif
+constexpr int kAggThreads = SJB_AGG_THREADS;
 constexpr int kAggPer = 8;
 constexpr int kAggChunk = kAggThreads * kAggPer;
 constexpr int kAggSpan = 2048;
@@ -1183,16 +1186,16 @@ emit_sims_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
     if (big && lane == 0) big_rows[atomicAdd(n_big, 1u)] = (uint32_t)i;
     const uint64_t ir = left_base + (uint64_t)i;
     uint64_t run = m0;
-    // four 32-candidate chunks per step: their loads in flight together
-    for (uint64_t t0 = 0; t0 < n; t0 += 128) {
-      uint64_t kv[4];
+    // eight 32-candidate chunks per step: their loads in flight together
+    for (uint64_t t0 = 0; t0 < n; t0 += 256) {
+      uint64_t kv[8];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
+      for (int e = 0; e < 8; e++) {
         const uint64_t t = t0 + 32 * e + lane;
         kv[e] = t < n ? keys[c0 + t] : (uint64_t)kRejected;
       }
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
+      for (int e = 0; e < 8; e++) {
         const uint32_t sb = (uint32_t)kv[e];
         const bool ok = sb != kRejected;
         const uint32_t bal = __ballot_sync(0xffffffffu, ok);

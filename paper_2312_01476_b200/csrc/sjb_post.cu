@@ -1069,17 +1069,18 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
         const uint32_t ub = mn<uint32_t>(u1, u0 + kBlkChains * (groups * (warp + 1) / kBlkWarps));
         uint32_t rank = sh.rank[wpar][lane];
         for (uint32_t u = u0; u < ua; u++) rank += (sh.mask[u] >> lane) & 1u;
+        const int p4 = pitch >> 2;
         for (uint32_t u = ua; u < ub; u += kBlkChains) {
           uint32_t m[kBlkChains], any = 0u;
-          const float4* S4[kBlkChains];
 #pragma unroll
           for (int c = 0; c < kBlkChains; c++) {
-            const uint32_t uc = u + c < ub ? u + c : u;
-            m[c] = u + c < ub ? sh.mask[uc] : 0u;
+            m[c] = u + c < ub ? sh.mask[u + c] : 0u;
             any |= m[c];
-            S4[c] = reinterpret_cast<const float4*>(Ss + (size_t)(uc - u0) * pitch);
           }
           if (any == 0u) continue;
+          // union rows u .. u + kBlkChains - 1 at a constant pitch (rows past
+          // ub read staged or scratch words; their results are dropped)
+          const float4* S4 = reinterpret_cast<const float4*>(Ss + (size_t)(u - u0) * pitch);
           float x[kBlkChains];
 #pragma unroll
           for (int c = 0; c < kBlkChains; c++) x[c] = 0.0f;
@@ -1088,7 +1089,7 @@ recheck_blocks_kernel(uint32_t* __restrict__ g32, const uint64_t* __restrict__ p
             const float4 a = R4[q];
 #pragma unroll
             for (int c = 0; c < kBlkChains; c++) {
-              const float4 b = S4[c][q];
+              const float4 b = S4[c * p4 + q];
               x[c] = __fmaf_rn(a.x, b.x, x[c]);
               x[c] = __fmaf_rn(a.y, b.y, x[c]);
               x[c] = __fmaf_rn(a.z, b.z, x[c]);

@@ -518,10 +518,10 @@ def test_medium_instances_match_oracle(cuda, monkeypatch, recheck):
 @pytest.mark.parametrize("dim", [16, 64, 100, 128])
 def test_dense_blocks_match_oracle(cuda, monkeypatch, dim):
     """The cluster-blocked dense recheck: clusters whose right members fit one
-    staging window (~60), span several windows (~400 of the 512-row union
-    cap) and overflow the union (~900: sparse per-candidate blocks), plus a
-    theta low enough for rows above the sortable 1024 candidates -- every
-    MatchSet equal to the oracle's, bit for bit."""
+    staging window (~60), span several windows (~400) and approach the
+    1024-row union cap (~900), plus a theta low enough for rows above the
+    sortable 1024 candidates (sparse per-candidate blocks) -- every MatchSet
+    equal to the oracle's, bit for bit."""
     from paper_2312_01476_b200 import device as D
     _set_recheck(monkeypatch, "deferred")
     cases = [(2000, 3000, 50, 0.3, 0.3), (1500, 4000, 10, 0.3, 0.3), (1200, 4500, 5, 0.3, 0.3),
@@ -535,6 +535,37 @@ def test_dense_blocks_match_oracle(cuda, monkeypatch, dim):
         assert len(wl) > 0
         assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (dim, k)
         assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), (dim, k)
+
+
+def test_dense_recheck_random_shapes(cuda, monkeypatch):
+    """Deferred (dense) recheck on random small shapes: 1-row and 1-column
+    relations, every dim % 4 == 0 up to 128 (and odd dims: the gather
+    fallback), duplicate rows (equal similarities), zero rows (repaired),
+    thetas from -0.3 to 0.95, and a tiny candidate capacity forcing the
+    overflow retry -- each MatchSet bitwise the oracle's."""
+    from paper_2312_01476_b200 import device as D
+    _set_recheck(monkeypatch, "deferred")
+    rng = np.random.default_rng(4242)
+    for inst in range(24):
+        nl = int(rng.choice([1, 2, 33, int(rng.integers(40, 2500))]))
+        nr = int(rng.choice([1, 7, int(rng.integers(50, 4000))]))
+        dim = int(rng.choice([4, 8, 16, 36, 64, 100, 128, 37, 101]))
+        c = int(rng.integers(1, 60))
+        L, S = O_pair(nl, nr, dim, c, float(rng.uniform(0.2, 0.8)), 7000 + inst)
+        if nr > 10:
+            S[3] = S[5]            # duplicate right rows
+            S[7] = 0.0             # a zero row (repaired to e0)
+        if nl > 10:
+            L[2] = L[4]
+        theta = float(rng.choice([-0.3, 0.0, 0.3, 0.6, 0.8, 0.95]))
+        wl, wr, ws = O.join_raw(L, S, theta, threads=16)
+        pl = D.prepare(torch.from_numpy(L).to(cuda))
+        pr = D.prepare(torch.from_numpy(S).to(cuda))
+        for cap in (None, 256):
+            m = D.join_prepared(pl, pr, theta, cand_cap=cap)
+            lo, ro, so = m.to_host()
+            assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (inst, nl, nr, dim, theta, cap)
+            assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), (inst, cap)
 
 
 def test_budget_and_thread_invariance(cuda, manifest, golden):

@@ -321,7 +321,7 @@ struct JoinWs {
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 
-JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride, bool defer) {
+JoinWs join_ws_layout(const sjb_join_args* a, int grid, int64_t tile_stride) {
   JoinWs w;
   size_t o = 0;
   const size_t ccap = (size_t)(a->cand_cap > 0 ? a->cand_cap : 0);
@@ -463,8 +463,9 @@ int encode_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
   return SJB_OK;
 }
 
+#if SJB_AB_KERNELS
 // fp32 rows f32[n][dim] (dim % 4 == 0, dim <= 256) for tile::gather4: box =
-// one whole row, no swizzle (recheck_rows_kernel).
+// one whole row, no swizzle (recheck_rows_kernel, A/B).
 int encode_gather_rows_map(CUtensorMap* map, const float* rows, int64_t n, int dim) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -478,6 +479,7 @@ int encode_gather_rows_map(CUtensorMap* map, const float* rows, int64_t n, int d
   if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled (gather rows) failed (%d)", (int)r);
   return SJB_OK;
 }
+#endif
 
 #if SJB_AB_KERNELS
 template <int KS>
@@ -826,14 +828,12 @@ int64_t sjb_join_workspace_bytes(const sjb_join_args* args) {
   JoinPlan pl;
   int grid = 1;
   int64_t tstride = 0;
-  bool defer = false;
   if (args->n_left > 0 && args->n_right > 0) {
     if (make_plan(args, &pl) != SJB_OK) return -1;
     grid = pl.grid;
     tstride = pl.tile_stride;
-    defer = pl.defer;
   }
-  return (int64_t)join_ws_layout(args, grid, tstride, defer).total;
+  return (int64_t)join_ws_layout(args, grid, tstride).total;
 }
 
 }  // extern "C"
@@ -872,7 +872,7 @@ int join_ctx(const sjb_join_args* args, void* d_workspace, int64_t workspace_byt
   if (c->empty) return SJB_OK;
   if (int rc = make_plan(args, &c->pl)) return rc;
   const JoinPlan& pl = c->pl;
-  const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride, pl.defer);
+  const JoinWs w = join_ws_layout(args, pl.grid, pl.tile_stride);
   if ((int64_t)w.total > workspace_bytes)
     return fail(SJB_E_INVALID, "workspace %lld B < required %lld B", (long long)workspace_bytes,
                 (long long)w.total);

@@ -29,6 +29,9 @@
 #include "sjb_join2.cu"
 #endif
 #include "sjb_join3.cu"
+#if SJB_AB_KERNELS
+#include "sjb_join4.cu"
+#endif
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
 #include "sjb_fmt.cu"
@@ -420,15 +423,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-#if SJB_AB_KERNELS
-
 // The 16-bit operand image (sjb_operand_elems elements, 256-row tiles of
 // [k-group][row][8]) as a 3-D tensor (256 elements = 32 rows x 8, 8 row
-// blocks, kgroups * tiles); box {256, box_rows/32, kgroups} = one
-// [k-group][box_rows][8] block.  The 512 B inner extent keeps every request
-// at full 32 B sectors (a 16 B inner box over-fetched 2x and issued ~900
-// requests per stage).
-int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad, int box_rows) {
+// blocks, kgroups * tiles); box {256, box_rows/32, box_kgroups (0: all)} =
+// one [k-group][box_rows][8] block.  The 512 B inner extent keeps every
+// request at full 32 B sectors (a 16 B inner box over-fetched 2x and issued
+// ~900 requests per stage).
+int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad, int box_rows,
+                       int box_kgroups = 0) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (box_rows % 32) return fail(SJB_E_INVALID, "box rows %d not a multiple of 32", box_rows);
@@ -437,7 +439,8 @@ int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad,
   const cuuint64_t dims[3] = {256, (cuuint64_t)sjb::kTileRows / 32,
                               kgroups * (cuuint64_t)(rows / sjb::kTileRows)};
   const cuuint64_t strides[2] = {512, (cuuint64_t)sjb::kTileRows * 16};
-  const cuuint32_t box[3] = {256, (cuuint32_t)box_rows / 32, (cuuint32_t)kgroups};
+  const cuuint32_t box[3] = {256, (cuuint32_t)box_rows / 32,
+                             (cuuint32_t)(box_kgroups > 0 ? box_kgroups : (int)kgroups)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(image), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -445,7 +448,6 @@ int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad,
   if (r != CUDA_SUCCESS) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return SJB_OK;
 }
-#endif
 
 // fp32 canonical rows f32[n][dim] (dim % 4 == 0) as a 2-D tensor; box =
 // 32 elements x 256 rows = one K chunk of a tile, 128 B swizzle.
@@ -1046,7 +1048,51 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       // 31.1 ms: the coupled rings wait on the slower CTA's epilogue)
       const char* wpv = getenv("SJB_WIDE_PAIR");
       const bool wpair = wp.tol && (pl.grid % 2) == 0 && wpv && strcmp(wpv, "1") == 0;
-      if (wpair) {
+      // A/B (SJB_WIDE_MMA2=1): tensor sims on raw bf16 operands through the
+      // cta_group::2 kernel of sjb_join4.cu (256 x 512 tiles per SM pair, 25%
+      // fewer operand bytes per SM) -- measured no faster (cfg4 slice 32.8 vs
+      // 31.0 ms; filter 15.8 vs 15.4 ms under ncu)
+      const char* m2v = getenv("SJB_WIDE_MMA2");
+      const bool mma2 = wp.tol && wp.inv_a != nullptr && (pl.grid % 2) == 0 && (tb % 2) == 0 &&
+                        !wpair && m2v != nullptr && strcmp(m2v, "1") == 0;
+      if (mma2) {
+#if !SJB_AB_KERNELS
+        return ab_missing("SJB_WIDE_MMA2=1");
+#else
+        sjb::wide2::Params q;
+        if (int rc = encode_operand_map(&q.tmap_a, d_l16, nl, pl.kpad, 128, 8)) return rc;
+        if (int rc = encode_operand_map(&q.tmap_b, d_r16, nr, pl.kpad, 128, 8)) return rc;
+        q.n_a = nl;
+        q.n_b = nr;
+        q.kpad = pl.kpad;
+        q.n_ablk = pl.n_ablk;
+        const int64_t pb = tb / 2, pe = (te + 1) / 2;   // 512-row pair tiles (the image is padded)
+        const int64_t tt = (int64_t)pl.n_ablk * (pe - pb) / (8LL * (pl.grid / 2));
+        const int tpc2 = (int)(tt < 1 ? 1 : (tt > 32 ? 32 : tt));
+        q.n_ptiles = (int)pe;
+        q.tiles_per_chunk = tpc2;
+        q.tile_begin = (int)pb;
+        q.append = 1;
+        q.n_items = (int64_t)pl.n_ablk * sjb::ceil_div(pe - pb, (int64_t)tpc2);
+        q.stages = sjb::wide2::kMaxStages;
+        q.bf16 = 1;
+        q.cutoff = wp.cutoff;
+        q.hi_cut = wp.hi_cut;
+        q.cand = c.cand;
+        q.seg_cap = pl.seg_cap;
+        q.cta_count = c.cta;
+        q.inv_a = wp.inv_a;
+        q.inv_b = wp.inv_b;
+        q.sims_bits = c.sims_bits;
+        q.rowcount = c.rowcount;
+        q.pend = c.pend;
+        q.pend_count = c.pend_count;
+        const uint32_t sm2 = sjb::wide2::smem_bytes(q.stages);
+        if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel, (int)sm2)) return rc;
+        sjb::wide2::filter_kernel<<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);
+        SJB_CK_LAUNCH("wide2_filter");
+#endif
+      } else if (wpair) {
 #if !SJB_AB_KERNELS
         return ab_missing("SJB_WIDE_PAIR=1");
 #else

@@ -960,6 +960,35 @@ def test_bf16_overflow_retry_tensor_sims(cuda):
     assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
 
 
+@pytest.mark.parametrize("mma2", ["1", "0"])
+def test_wide_mma2_pair_kernel(cuda, monkeypatch, mma2):
+    """A/B: tensor sims on raw bf16 operands through the cta_group::2 wide
+    kernel (SJB_WIDE_MMA2=1, -DSJB_AB_KERNELS=1: 256 x 512 tiles per SM pair,
+    operands by 2-SM tensor TMA; the default library rejects the switch) and
+    the 1-CTA kernel: odd R tile counts, partial pair tiles, an overflow
+    retry -- the oracle's pair set, sims within 1e-5."""
+    from paper_2312_01476_b200 import _lib, device as D
+    if mma2 == "1" and not _lib.lib().sjb_ab_kernels():
+        L, S = _bf16_case(300, 500, 384, 12, 0.5, 40)
+        monkeypatch.setenv("SJB_WIDE_MMA2", mma2)
+        with pytest.raises(_lib.SjbError, match="A/B kernel"):
+            D.join_prepared(D.prepare_bf16(_bf16_tensor(L, cuda)),
+                            D.prepare_bf16(_bf16_tensor(S, cuda)), 0.6, sims="tensor")
+        return
+    monkeypatch.setenv("SJB_WIDE_MMA2", mma2)
+    for nl, nr, dim, seed in ((600, 1700, 384, 41), (1300, 2100, 256, 42), (200, 900, 768, 43),
+                              (257, 513, 192, 44)):
+        L, S = _bf16_case(nl, nr, dim, 12, 0.5, seed)
+        theta = 0.6
+        wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+        assert len(wl) > 0
+        pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+        for cap in (None, 4096):
+            lo, ro, so = D.join_prepared(pl, pr, theta, sims="tensor", cand_cap=cap).to_host()
+            assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (nl, nr, dim, cap)
+            assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
+
+
 @pytest.mark.parametrize("pair", ["1", "0"])
 def test_wide_pair_multicast(cuda, monkeypatch, pair):
     """A/B: wide-path tensor sims with CTA pairs sharing each S chunk by TMA

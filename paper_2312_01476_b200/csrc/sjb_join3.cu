@@ -31,7 +31,10 @@
 namespace sjb {
 namespace wide {
 
-constexpr int kEpiWarps = 8;
+#ifndef SJB_WIDE_EPI
+#define SJB_WIDE_EPI 8
+#endif
+constexpr int kEpiWarps = SJB_WIDE_EPI;
 constexpr int kChunksPerWarp = 16 / kEpiWarps;  // 64-column chunks per half
 template <bool kFused>
 struct Cfg {

@@ -165,7 +165,10 @@ __global__ void group_rows_kernel(const uint64_t* __restrict__ cand, uint64_t se
 #define SJB_AGG_THREADS 256
 #endif
 constexpr int kAggThreads = SJB_AGG_THREADS;
-constexpr int kAggPer = 8;
+#ifndef SJB_AGG_PER
+#define SJB_AGG_PER 8
+#endif
+constexpr int kAggPer = SJB_AGG_PER;
 constexpr int kAggChunk = kAggThreads * kAggPer;
 constexpr int kAggSpan = 2048;
 

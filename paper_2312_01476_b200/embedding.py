@@ -220,9 +220,15 @@ class LookupModel(EmbeddingModel):
         return t
 
     def indices(self, tokens: Sequence[str]) -> np.ndarray:
-        """Table row of every token (-1 for OOV under the synthetic policy)."""
-        get = self._index.get
-        idx = np.fromiter((get(t, -1) for t in tokens), dtype=np.int64, count=len(tokens))
+        """Table row of every token (-1 for OOV under the synthetic policy):
+        one C loop of dict probes (csrc/sjb_pack.c) when the native helper is
+        built, else the same probes in Python (host marshalling only)."""
+        try:
+            from . import _sjbpack
+            idx = np.frombuffer(_sjbpack.lookup(self._index, tokens), dtype=np.int64)
+        except (ImportError, AttributeError, TypeError):
+            get = self._index.get
+            idx = np.fromiter((get(t, -1) for t in tokens), dtype=np.int64, count=len(tokens))
         if self.oov == "error" and len(idx) and idx.min() < 0:
             raise OutOfVocabulary(tokens[int(np.argmin(idx))])
         return idx

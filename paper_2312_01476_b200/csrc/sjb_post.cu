@@ -802,8 +802,10 @@ __global__ void sig_blocks_kernel(const uint32_t* __restrict__ hist,
 constexpr int kBlkStage = 180;
 constexpr int kBlkSparseWarps = kBlkStage / 32;
 static_assert(kBlkStage + kBlkRows <= kBlkThreads, "one copy-issuing thread per staged row");
+// (at least 64 KB: the area is also the block's j cache, ~13k candidates at
+// cfg5 -- small dims would otherwise send every block to the sparse path)
 __host__ __device__ inline int blk_stage_bytes(int dim) {
-  return kBlkStage * rows_pitch(dim, false) * 4;
+  return mx(kBlkStage * rows_pitch(dim, false) * 4, 64 * 1024);
 }
 __host__ __device__ inline int blk_window_rows(int dim) { return kBlkStage - kBlkRows; }
 // Sort a[0 .. U) (U <= kBlkUnion, u32, distinct keys; tmp: kBlkUnion

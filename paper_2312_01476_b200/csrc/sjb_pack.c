@@ -81,7 +81,8 @@ fail:
   return NULL;
 }
 
-/* lookup(index, tokens) -> int64 bytes: index[token] for every token, -1
+/* lookup(index, tokens) -> int64 bytearray (writable, so numpy/torch views
+ * of it are too): index[token] for every token, -1
  * where absent (LookupModel.indices: the reference's per-token table probe,
  * embedding.py:143-152, as one C loop -- str objects cache their hash, so a
  * probe is a table read; the next tokens' objects are prefetched). */
@@ -93,12 +94,12 @@ static PyObject* lookup(PyObject* self, PyObject* args) {
   if (!fast) return NULL;
   const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
   PyObject** items = PySequence_Fast_ITEMS(fast);
-  PyObject* out = PyBytes_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(int64_t));
+  PyObject* out = PyByteArray_FromStringAndSize(NULL, n * (Py_ssize_t)sizeof(int64_t));
   if (!out) {
     Py_DECREF(fast);
     return NULL;
   }
-  int64_t* o = (int64_t*)PyBytes_AS_STRING(out);
+  int64_t* o = (int64_t*)PyByteArray_AS_STRING(out);
   for (Py_ssize_t i = 0; i < n; i++) {
     if (i + 8 < n) __builtin_prefetch(items[i + 8]);
     PyObject* v = PyDict_GetItemWithError(index, items[i]);   /* borrowed */
@@ -121,7 +122,7 @@ fail:
 
 static PyMethodDef methods[] = {
     {"pack", pack, METH_O, "pack(tokens) -> (utf8 bytes + NUL, int64 offsets bytes)"},
-    {"lookup", lookup, METH_VARARGS, "lookup(index dict, tokens) -> int64 bytes (-1: absent)"},
+    {"lookup", lookup, METH_VARARGS, "lookup(index dict, tokens) -> int64 bytearray (-1: absent)"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_sjbpack", NULL, -1, methods};

@@ -91,7 +91,7 @@ def build_pack(force: bool = False) -> str:
     if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(src):
         return out
     tmp = f"{out}.tmp{os.getpid()}"
-    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC",
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-pthread",
            "-I" + sysconfig.get_paths()["include"], src, "-o", tmp]
     subprocess.check_call(cmd)
     os.replace(tmp, out)

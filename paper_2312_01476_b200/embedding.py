@@ -17,6 +17,8 @@ import threading
 import time
 from typing import Dict, Optional, Sequence
 
+import os
+
 import numpy as np
 import torch
 
@@ -219,14 +221,25 @@ class LookupModel(EmbeddingModel):
             self._dev_tables[dev] = t
         return t
 
+    LOOKUP_THREADS = int(os.environ.get("SJB_LOOKUP_THREADS", str(min(16, os.cpu_count() or 1))))
+
     def indices(self, tokens: Sequence[str]) -> np.ndarray:
-        """Table row of every token (-1 for OOV under the synthetic policy):
-        one C loop of dict probes (csrc/sjb_pack.c) when the native helper is
-        built, else the same probes in Python (host marshalling only)."""
+        """Table row of every token (-1 for OOV under the synthetic policy).
+        With the native helper (csrc/sjb_pack.c): a C hash table of the
+        vocabulary, built once, probed by several threads without the GIL;
+        tokens that are not compact-ASCII str objects go through the dict.
+        Without it, the same dict probes in Python (host marshalling only)."""
         try:
             from . import _sjbpack
-            idx = np.frombuffer(_sjbpack.lookup(self._index, tokens), dtype=np.int64)
-        except (ImportError, AttributeError, TypeError):
+            if getattr(self, "_cindex", None) is None:
+                self._cindex = _sjbpack.build_index(self._index)
+            idx = np.frombuffer(_sjbpack.lookup_mt(self._cindex, tokens, self.LOOKUP_THREADS),
+                                dtype=np.int64)
+            rest = np.nonzero(idx == -2)[0]
+            if len(rest):
+                get = self._index.get
+                idx[rest] = [get(tokens[int(i)], -1) for i in rest]
+        except (ImportError, AttributeError):
             get = self._index.get
             idx = np.fromiter((get(t, -1) for t in tokens), dtype=np.int64, count=len(tokens))
         if self.oov == "error" and len(idx) and idx.min() < 0:

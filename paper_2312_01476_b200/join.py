@@ -80,10 +80,14 @@ class JoinStats:
             "peak_buffer_bytes", "threads", "algo", "inner_relation")}
 
 
-def plan_batches(left_rows: int, right_rows: int, dim: int, budget_bytes: int) -> BatchPlan:
-    """Exact-cover grid of near-square blocks under the budget (join.py:88-108)."""
+def _check_budget(budget_bytes: int) -> None:
     if budget_bytes < 4:
         raise BudgetTooSmall(f"budget {budget_bytes} bytes cannot hold one fp32 cell")
+
+
+def plan_batches(left_rows: int, right_rows: int, dim: int, budget_bytes: int) -> BatchPlan:
+    """Exact-cover grid of near-square blocks under the budget (join.py:88-108)."""
+    _check_budget(budget_bytes)
     budget_elems = budget_bytes // 4
     b = math.isqrt(budget_elems)
     lb = max(1, min(b, left_rows))
@@ -211,7 +215,9 @@ def tensor_join(left: RawRelation, right: RawRelation, model: EmbeddingModel, th
     Threshold.of(theta)
     if threads < 1:
         raise ValueError("threads must be >= 1")
-    plan_batches(len(left), len(right), model.dim, budget_bytes)  # validates the budget
+    # the budget is validated as plan_batches does; no dense buffer exists, so
+    # the tile plan itself is not built (join.py:88-108: ~6k tiles at cfg2)
+    _check_budget(budget_bytes)
     return _run(left, right, model, theta, threads, "tensor", "right", band, device, devices)
 
 

@@ -429,7 +429,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // one [k-group][box_rows][8] block.  The 512 B inner extent keeps every
 // request at full 32 B sectors (a 16 B inner box over-fetched 2x and issued
 // ~900 requests per stage).
-int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad, int box_rows,
+[[maybe_unused]] int encode_operand_map(CUtensorMap* map, const void* image, int64_t n, int kpad, int box_rows,
                        int box_kgroups = 0) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SJB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -639,11 +639,12 @@ static int normalize_impl(const float* d_in, const int64_t* d_gather, int64_t n,
   if (tiles == 0) return SJB_OK;
   if (d_gather == nullptr && (dim & 3) == 0 && kpad <= 128 && ((uintptr_t)d_in & 15) == 0 &&
       ((uintptr_t)d_out32 & 15) == 0 && getenv("SJB_PREP_STAGED") == nullptr) {
-    // pipelined kernel: per-warp double-buffered 32-row slabs
+    // pipelined kernel: per-warp 32-row slabs, double-buffered (8 warps per SM;
+    // SJB_PREP_BUFS=1: one buffer, 16 warps)
     int dev = 0;
     cudaGetDevice(&dev);
     const char* pb = getenv("SJB_PREP_BUFS");
-    const int nbuf = pb != nullptr && atoi(pb) == 2 ? 2 : 1;
+    const int nbuf = pb != nullptr && atoi(pb) == 1 ? 1 : 2;
     const int warps = sjb::pipe_warps((int)dim, nbuf, 210 * 1024);
     const int smem = sjb::pipe_smem_bytes((int)dim, nbuf, warps);
     if (int rc = set_smem_attr((const void*)sjb::normalize_pipe_kernel, smem)) return rc;

@@ -10,9 +10,31 @@
 //     (sjb_common.cuh tiled_offset), zero-padded to kpad columns.
 #include "sjb_common.cuh"
 
+#include <type_traits>
+
 namespace sjb {
 
 constexpr int kPrepThreads = 128;
+
+// RN_f32(x / norm) with the correctly rounded fp64 quotient in between.
+// kFast (finite norm): y = RN(1/norm) and q0 = RN(x*y) lie within 1 ulp of
+// the quotient, the residual r = x - q0*norm is exact in one fma and
+// RN(q0 + r*y) is the correctly rounded quotient (Markstein's theorem), i.e.
+// bitwise __ddiv_rn, for every finite norm >= 1e-12 and finite float x;
+// the sign goes on the float (rounding is symmetric), which keeps -0.0.
+// Otherwise (inf/NaN norms) the true divide.  Callers choose kFast once per
+// row (or warp), outside their element loops: a per-element test compiles to
+// a divergence region around every quotient.
+template <bool kFast>
+__device__ __forceinline__ float quot_f32(float xf, double norm, double y) {
+  const double x = (double)xf;
+  if (kFast) {
+    const double q0 = __dmul_rn(x, y);
+    const float q = __double2float_rn(__fma_rn(__fma_rn(-q0, norm, x), y, q0));
+    return __int_as_float((__float_as_int(q) & 0x7fffffff) | (__float_as_int(xf) & 0x80000000));
+  }
+  return __double2float_rn(__ddiv_rn(x, norm));
+}
 
 // Sequential fp64 sum of squares, repair rule, fp64 divide -- the reference's
 // normalize_row (_kernelcore.c:52-70).  Operates on one smem row.  The square
@@ -39,33 +61,30 @@ __device__ __forceinline__ int normalize_row_smem(float* row, int dim, float* er
     norm = sqrt(ss);
     repaired = 1;
   }
-  // x / norm, correctly rounded, without a full divide per element: with
-  // y = RN(1/norm) and q0 = RN(x*y) within 1 ulp of the quotient, the residual
-  // r = x - q0*norm is exact in one fma and RN(q0 + r*y) is the correctly
-  // rounded quotient (Markstein's theorem), i.e. bitwise __ddiv_rn.  Holds for
-  // every finite norm >= 1e-12 and finite float x (no over/underflow in the
-  // residual); non-finite norms keep the true divide (inf/inf = NaN etc.).
-  const bool hoist = isfinite(norm);
+  // x / norm, correctly rounded, without a full divide per element (quot_f32)
   const double y = __drcp_rn(norm);
-  auto quot = [&](double x) -> double {
-    if (!hoist) return __ddiv_rn(x, norm);
-    const double q0 = __dmul_rn(x, y);
-    return copysign(__fma_rn(__fma_rn(-q0, norm, x), y, q0), x);  // keeps -0.0
-  };
-  if (err == nullptr) {
-    for (int d = 0; d < dim; d++) row[d] = __double2float_rn(quot((double)row[d]));
-  } else {
-    double es = 0.0;
-    for (int d = 0; d < dim; d++) {
-      const float x = __double2float_rn(quot((double)row[d]));
-      row[d] = x;
-      // fp16(x) - x is exact in fp32 (at most 13 significant bits, or x itself
-      // when it rounds to zero), so the fp32 difference equals the fp64 one
-      const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
-      es = __fma_rn(e, e, es);
+  auto pass = [&](auto fast) {
+    constexpr bool kFast = decltype(fast)::value;
+    if (err == nullptr) {
+      for (int d = 0; d < dim; d++) row[d] = quot_f32<kFast>(row[d], norm, y);
+    } else {
+      double es = 0.0;
+      for (int d = 0; d < dim; d++) {
+        const float x = quot_f32<kFast>(row[d], norm, y);
+        row[d] = x;
+        // fp16(x) - x is exact in fp32 (at most 13 significant bits, or x
+        // itself when it rounds to zero), so the fp32 difference equals the
+        // fp64 one
+        const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
+        es = __fma_rn(e, e, es);
+      }
+      *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
     }
-    *err = __double2float_ru(__dmul_ru(sqrt(es), 1.0 + 1e-12));
-  }
+  };
+  if (isfinite(norm))
+    pass(std::true_type{});
+  else
+    pass(std::false_type{});
   return repaired;
 }
 
@@ -98,11 +117,6 @@ __device__ __forceinline__ double row_norm_smem(float* row, int dim, int* repair
   return norm;
 }
 
-__device__ __forceinline__ double quot_rn(double x, double norm, double y, bool hoist) {
-  if (!hoist) return __ddiv_rn(x, norm);
-  const double q0 = __dmul_rn(x, y);
-  return copysign(__fma_rn(__fma_rn(-q0, norm, x), y, q0), x);  // keeps -0.0
-}
 
 // Normalise the vrows (<= kWideRows) rows staged in sm; row errors to err_out
 // (nullptr: not wanted).  Returns this thread's repaired-row count.
@@ -122,17 +136,23 @@ __device__ int normalize_rows_wide(float* sm, int pitch, int vrows, int dim, flo
   const bool want = err_out != nullptr;
   for (int r = 0; r < vrows; r++) {
     const double norm = s_norm[r], y = s_y[r];
-    const bool hoist = isfinite(norm);
     float* row = sm + r * pitch;
     double es = 0.0;
-    for (int d = tid; d < dim; d += kPrepThreads) {
-      const float x = __double2float_rn(quot_rn((double)row[d], norm, y, hoist));
-      row[d] = x;
-      if (want) {
-        const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
-        es = __fma_rn(e, e, es);
+    auto pass = [&](auto fast) {  // norm is CTA-uniform: no divergence
+      constexpr bool kFast = decltype(fast)::value;
+      for (int d = tid; d < dim; d += kPrepThreads) {
+        const float x = quot_f32<kFast>(row[d], norm, y);
+        row[d] = x;
+        if (want) {
+          const double e = (double)__fsub_rn(from_op16(to_op16(x, bf), bf), x);
+          es = __fma_rn(e, e, es);
+        }
       }
-    }
+    };
+    if (isfinite(norm))
+      pass(std::true_type{});
+    else
+      pass(std::false_type{});
     if (want) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
@@ -323,7 +343,7 @@ normalize_cast_kernel(const float* __restrict__ in, const int64_t* __restrict__ 
 //   1. the reference's sequential fp64 sum of squares + repair
 //      (_kernelcore.c:52-70), reading the row as float4 (row pitch = an odd
 //      number of float4: conflict-free 128-bit shared loads);
-//   2. the correctly rounded quotients (quot_rn, in place), the 16-bit cast
+//   2. the correctly rounded quotients (quot_f32, in place), the 16-bit cast
 //      stored as the row's 16-byte chunks of the operand tile (a warp writes
 //      one 512 B run per k-group), and the row's rounding error (exact
 //      squares, fp64 sum, rounded up: the same value as the staged kernel);
@@ -335,8 +355,9 @@ constexpr int kPipeMaxWarps = 16;
 
 __host__ __device__ inline int pipe_pitch4(int dim) { return (dim / 4) | 1; }
 
-// bufs = 1: each warp loads its next slab after finishing the current one
-// (16 warps per SM hide the latency); 2: double-buffered (8 warps)
+// bufs = 2 (default): double-buffered, 8 warps per SM -- the next slab's
+// load is in flight through the current one's arithmetic; bufs = 1: each
+// warp loads its next slab after finishing the current one (16 warps)
 __host__ inline int pipe_warps(int dim, int bufs, int smem_budget) {
   const int per_warp = bufs * kPipeSlab * pipe_pitch4(dim) * 16 + 16;
   return mn(kPipeMaxWarps, smem_budget / per_warp);
@@ -344,6 +365,57 @@ __host__ inline int pipe_warps(int dim, int bufs, int smem_budget) {
 
 __host__ __device__ inline int pipe_smem_bytes(int dim, int bufs, int warps) {
   return warps * (bufs * kPipeSlab * pipe_pitch4(dim) * 16 + 16);
+}
+
+// Pass 2 of normalize_pipe_kernel for one row (lane = row): the correctly
+// rounded quotients in place, the bf16 chunks of the operand tile and the
+// row's rounding-error sum.  kFast: every lane's norm is finite, so the
+// quotient is quot_f32<true> with no per-element test; otherwise
+// the true divide for all lanes (the same bits where the norm is finite).
+template <bool kFast>
+__device__ __forceinline__ float pipe_pass2(float4* row, bool valid, int q4, int kpad, double norm,
+                                            double y, uint4* dst16, int rin, bool want_err) {
+  auto quot = [&](float xf) -> float { return quot_f32<kFast>(xf, norm, y); };
+  float es = 0.0f;
+  for (int g = 0; g < kpad / 8; g++) {
+    __align__(16) float x[8];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int q = 2 * g + h;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid && q < q4) {
+        v = row[q];
+        v.x = quot(v.x);
+        v.y = quot(v.y);
+        v.z = quot(v.z);
+        v.w = quot(v.w);
+        row[q] = v;
+      }
+      x[4 * h + 0] = v.x;
+      x[4 * h + 1] = v.y;
+      x[4 * h + 2] = v.z;
+      x[4 * h + 3] = v.w;
+    }
+    if (dst16 != nullptr) {
+      // kpad <= 128: bf16 operands, converted in pairs (one F2FP per two)
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+        o[e] = *reinterpret_cast<const uint32_t*>(&h);
+        if (want_err) {
+          // op(x) - x is exact in fp32; the squares are summed in fp32
+          // rounding UP, so es bounds the exact sum from above
+          const float d0 = __fsub_rn(__uint_as_float(o[e] << 16), x[2 * e]);
+          const float d1 = __fsub_rn(__uint_as_float(o[e] & 0xffff0000u), x[2 * e + 1]);
+          es = __fmaf_ru(d0, d0, es);
+          es = __fmaf_ru(d1, d1, es);
+        }
+      }
+      dst16[g * kTileRows + rin] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  return es;
 }
 
 __global__ void __launch_bounds__(kPipeMaxWarps * 32, 1)
@@ -366,18 +438,30 @@ normalize_pipe_kernel(const float* __restrict__ in, int64_t n, int64_t n_slabs, 
   }
   __syncwarp();
   const uint64_t pol = policy_evict_first();
-  const bool bf = op_is_bf16(kpad);
   const int64_t nw = (int64_t)gridDim.x * warps;
 
   auto slab_rows = [&](int64_t slab) -> int {
     return (int)mx<int64_t>(0, mn<int64_t>(kPipeSlab, n - slab * kPipeSlab));
   };
+  // q4 odd (d = 100: 25 float4): the conflict-free pitch is the row itself,
+  // so a slab is one contiguous run in both global and shared memory: one
+  // bulk copy in, one bulk store out (per-lane copies issue as a
+  // serialised loop, and the row-by-row store loop was a quarter of the
+  // kernel's stall samples)
+  const bool contig = p4 == q4;
   auto issue = [&](int64_t slab, int b) {
     const int rows = slab_rows(slab);
     if (rows == 0) return;  // padding slab: nothing to load, no barrier phase
-    if (lane == 0) mbar_arrive_expect_tx(&bars[b], (uint32_t)(rows * dim * 4));
+    if (lane == 0) {
+      // the buffer's previous bulk store must have read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive_expect_tx(&bars[b], (uint32_t)(rows * dim * 4));
+      if (contig)
+        bulk_g2s(bufs + (size_t)b * kPipeSlab * p4, in + slab * kPipeSlab * (int64_t)dim,
+                 (uint32_t)(rows * dim * 4), &bars[b], pol);
+    }
     __syncwarp();
-    if (lane < rows)
+    if (!contig && lane < rows)
       bulk_g2s(bufs + (size_t)b * kPipeSlab * p4 + lane * p4,
                in + (slab * kPipeSlab + lane) * (int64_t)dim, (uint32_t)(dim * 4), &bars[b], pol);
   };
@@ -439,49 +523,33 @@ normalize_pipe_kernel(const float* __restrict__ in, int64_t n, int64_t n_slabs, 
       y = __drcp_rn(norm);
     }
     // ---- 2. quotients (in place), operand chunks, rounding error --------
-    float es = 0.0f;
     const int64_t tile = r0 / kTileRows;
     const int rin = (int)(r0 - tile * kTileRows) + lane;
     uint4* dst16 = out16 != nullptr
                        ? reinterpret_cast<uint4*>(out16 + tile * (int64_t)kTileRows * kpad)
                        : nullptr;
-    for (int g = 0; g < kpad / 8; g++) {
-      __align__(16) float x[8];
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int q = 2 * g + h;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && q < q4) {
-          v = row[q];
-          v.x = __double2float_rn(quot_rn((double)v.x, norm, y, hoist));
-          v.y = __double2float_rn(quot_rn((double)v.y, norm, y, hoist));
-          v.z = __double2float_rn(quot_rn((double)v.z, norm, y, hoist));
-          v.w = __double2float_rn(quot_rn((double)v.w, norm, y, hoist));
-          row[q] = v;
-        }
-        x[4 * h + 0] = v.x;
-        x[4 * h + 1] = v.y;
-        x[4 * h + 2] = v.z;
-        x[4 * h + 3] = v.w;
-      }
-      if (dst16 != nullptr) {
-        __align__(16) op16_t o[8];
-#pragma unroll
-        for (int e = 0; e < 8; e++) {
-          o[e] = to_op16(x[e], bf);
-          if (row_err != nullptr) {
-            // op(x) - x is exact in fp32; the squares are summed in fp32
-            // rounding UP, so es bounds the exact sum from above
-            const float d = __fsub_rn(from_op16(o[e], bf), x[e]);
-            es = __fmaf_ru(d, d, es);
-          }
-        }
-        dst16[g * kTileRows + rin] = *reinterpret_cast<const uint4*>(o);
-      }
-    }
+    // warp-uniform choice: the per-element loop carries no branch (a per-lane
+    // hoist test around every quotient compiled to a divergence region per
+    // element and doubled the kernel's issue count)
+    const float es = __all_sync(0xffffffffu, hoist)
+                         ? pipe_pass2<true>(row, valid, q4, kpad, norm, y, dst16, rin, row_err != nullptr)
+                         : pipe_pass2<false>(row, valid, q4, kpad, norm, y, dst16, rin, row_err != nullptr);
     __syncwarp();
     // ---- 3. fp32 rows out, errors, counters -----------------------------
-    if (out32 != nullptr) {
+    if (out32 != nullptr && contig) {
+      if (rows > 0) {
+        // pass 2's shared writes become visible to the async proxy, then
+        // one bulk store (completion awaited before the buffer's next load)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          asm volatile(
+              "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+              "cp.async.bulk.commit_group;" ::"l"(out32 + r0 * (int64_t)dim),
+              "r"(smem_u32(buf)), "r"((uint32_t)(rows * dim * 4))
+              : "memory");
+      }
+    } else if (out32 != nullptr) {
       float4* o4 = reinterpret_cast<float4*>(out32 + r0 * (int64_t)dim);
       for (int r = 0; r < rows; r++)
         for (int q = lane; q < q4; q += 32) o4[r * q4 + q] = buf[r * p4 + q];
@@ -501,6 +569,7 @@ normalize_pipe_kernel(const float* __restrict__ in, int64_t n, int64_t n_slabs, 
     }
     __syncwarp();
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // bf16 relations for the raw-operand wide filter (BASELINE cfg4: d = 768

@@ -1088,6 +1088,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         q.rowcount = c.rowcount;
         q.pend = c.pend;
         q.pend_count = c.pend_count;
+        q.debug = jp.debug_mode;
         const uint32_t sm2 = sjb::wide2::smem_bytes(q.stages);
         if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel, (int)sm2)) return rc;
         sjb::wide2::filter_kernel<<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);

@@ -125,6 +125,7 @@ struct alignas(64) Params {
   uint32_t* rowcount;
   uint32_t* pend;
   uint32_t* pend_count;
+  int debug;   // diagnostics (results invalid): 1 no emission, 2 no drain, 20 no operand traffic
 };
 
 __host__ __device__ inline uint32_t smem_bytes(int stages) {
@@ -181,13 +182,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = policy_evict_normal();
       int s = 0;
       uint32_t ph = 0;
+      int64_t fills = 0;
       for (int64_t item = pair_id; item < n_items; item += n_pairs) {
         const int64_t rb = item % nb, sc = item / nb;
         const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
         const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_ptiles);
         for (int64_t t = t0; t < t1; t++) {
-          for (int c = 0; c < nchunks; c++) {
+          for (int c = 0; c < nchunks; c++, fills++) {
             mbar_wait(&empty[s], ph ^ 1u);
+            if (p.debug == 20 && fills >= p.stages) {   // diagnostics: no operand traffic
+              if (leader) mbar_arrive(&full[s]);
+              if (++s == p.stages) {
+                s = 0;
+                ph ^= 1u;
+              }
+              continue;
+            }
             if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
             uint8_t* dst = ring + (size_t)s * kStageBytes;
             tma3d_2sm(dst, &p.tmap_a, 0, 4 * (int)rank, (int)(rb * kg + c * 8), &full[s],
@@ -275,6 +285,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 2; k++) {
             const int cq = cq0 + 2 * k;
             const uint32_t taddr = tmem_base + (lane_base << 16) + h * 256 + cq * 64;
+            if (p.debug == 2) {   // diagnostics: no drain
+              if (k == 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                  if (leader) mbar_arrive_relaxed(&acc_empty[h]);
+                  else arrive_leader_relaxed(&acc_empty[h]);
+                }
+              }
+              continue;
+            }
             float v[64];
             SJB_TMEM_LD32(taddr, v, 0);
             SJB_TMEM_LD32(taddr + 32, v, 32);
@@ -286,6 +307,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (leader) mbar_arrive_relaxed(&acc_empty[h]);
                 else arrive_leader_relaxed(&acc_empty[h]);
               }
+            }
+            if (p.debug == 1) {   // diagnostics: drain, no emission
+              float m = v[0];
+#pragma unroll
+              for (int e = 1; e < 64; e++) m = fmaxf(m, v[e]);
+              if (m > 3.0e38f) cta_sat[0] = 1u;
+              continue;
             }
             const int64_t col0 = t * 2 * kTileRows + h * kTileRows + cq * 64;
             // normalise after the GEMM: (acc * inv_i) * inv_j (inv_b is

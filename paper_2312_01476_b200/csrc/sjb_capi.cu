@@ -29,9 +29,7 @@
 #include "sjb_join2.cu"
 #endif
 #include "sjb_join3.cu"
-#if SJB_AB_KERNELS
 #include "sjb_join4.cu"
-#endif
 #include "sjb_post.cu"
 #include "sjb_prep.cu"
 #include "sjb_fmt.cu"
@@ -1049,17 +1047,22 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       // 31.1 ms: the coupled rings wait on the slower CTA's epilogue)
       const char* wpv = getenv("SJB_WIDE_PAIR");
       const bool wpair = wp.tol && (pl.grid % 2) == 0 && wpv && strcmp(wpv, "1") == 0;
-      // A/B (SJB_WIDE_MMA2=1): tensor sims on raw bf16 operands through the
-      // cta_group::2 kernel of sjb_join4.cu (256 x 512 tiles per SM pair, 25%
-      // fewer operand bytes per SM) -- measured no faster (cfg4 slice 32.8 vs
-      // 31.0 ms; filter 15.8 vs 15.4 ms under ncu)
+      // Tensor sims on raw bf16 operands run on CTA pairs (sjb_join4.cu,
+      // cta_group::2): by default 256 x 256 pair tiles with TWO accumulator
+      // stages, so a tile's drain, normalisation and emission overlap the next
+      // tile's MMAs (cfg4 slice: filter 22.0 -> 15.2 ms, tensor pipe 51 -> 97%
+      // active).  SJB_WIDE_MMA2=0: the 1-CTA kernel of sjb_join3.cu (A/B);
+      // =1 (A/B build): 256 x 512 pair tiles, one accumulator tile -- measured
+      // no faster than the 1-CTA kernel (32.8 vs 31.0 ms).
       const char* m2v = getenv("SJB_WIDE_MMA2");
-      const bool mma2 = wp.tol && wp.inv_a != nullptr && (pl.grid % 2) == 0 && (tb % 2) == 0 &&
-                        !wpair && m2v != nullptr && strcmp(m2v, "1") == 0;
+      const bool mma2_one = m2v != nullptr && strcmp(m2v, "1") == 0;
+      const bool mma2_two = !mma2_one && !(m2v != nullptr && strcmp(m2v, "0") == 0);
+      const bool mma2 = wp.tol && wp.inv_a != nullptr && (pl.grid % 2) == 0 && !wpair &&
+                        (mma2_two || (mma2_one && (tb % 2) == 0));
       if (mma2) {
 #if !SJB_AB_KERNELS
-        return ab_missing("SJB_WIDE_MMA2=1");
-#else
+        if (mma2_one) return ab_missing("SJB_WIDE_MMA2=1");
+#endif
         sjb::wide2::Params q;
         if (int rc = encode_operand_map(&q.tmap_a, d_l16, nl, pl.kpad, 128, 8)) return rc;
         if (int rc = encode_operand_map(&q.tmap_b, d_r16, nr, pl.kpad, 128, 8)) return rc;
@@ -1067,7 +1070,8 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         q.n_b = nr;
         q.kpad = pl.kpad;
         q.n_ablk = pl.n_ablk;
-        const int64_t pb = tb / 2, pe = (te + 1) / 2;   // 512-row pair tiles (the image is padded)
+        // 512-row pair tiles (the image is padded); two-stage: the 256-row tiles themselves
+        const int64_t pb = mma2_two ? tb : tb / 2, pe = mma2_two ? te : (te + 1) / 2;
         const int64_t tt = (int64_t)pl.n_ablk * (pe - pb) / (8LL * (pl.grid / 2));
         const int tpc2 = (int)(tt < 1 ? 1 : (tt > 32 ? 32 : tt));
         q.n_ptiles = (int)pe;
@@ -1075,7 +1079,7 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         q.tile_begin = (int)pb;
         q.append = 1;
         q.n_items = (int64_t)pl.n_ablk * sjb::ceil_div(pe - pb, (int64_t)tpc2);
-        q.stages = sjb::wide2::kMaxStages;
+        q.stages = sjb::wide2::max_stages(mma2_two);
         q.bf16 = 1;
         q.cutoff = wp.cutoff;
         q.hi_cut = wp.hi_cut;
@@ -1089,11 +1093,17 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         q.pend = c.pend;
         q.pend_count = c.pend_count;
         q.debug = jp.debug_mode;
-        const uint32_t sm2 = sjb::wide2::smem_bytes(q.stages);
-        if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel, (int)sm2)) return rc;
-        sjb::wide2::filter_kernel<<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);
-        SJB_CK_LAUNCH("wide2_filter");
+        const uint32_t sm2 = sjb::wide2::smem_bytes(q.stages, mma2_two);
+        if (mma2_two) {
+          if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel<true>, (int)sm2)) return rc;
+          sjb::wide2::filter_kernel<true><<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);
+        } else {
+#if SJB_AB_KERNELS
+          if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel<false>, (int)sm2)) return rc;
+          sjb::wide2::filter_kernel<false><<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);
 #endif
+        }
+        SJB_CK_LAUNCH("wide2_filter");
       } else if (wpair) {
 #if !SJB_AB_KERNELS
         return ab_missing("SJB_WIDE_PAIR=1");

@@ -440,24 +440,31 @@ constexpr uint32_t kPending = 0x7fc00002u;   // a NaN payload: recheck pending
 // groups holding hits are parked there, so the hit loop reads the similarity
 // of a dynamic column without spilling v[] (static indices only) and the
 // code stays as compact as emit_row_chunk64's.
-__device__ __forceinline__ uint32_t emit_row_chunk64_tol(
+template <int CW>   // chunk width: 64 columns, or 32 (16 epilogue warps: half the live registers)
+__device__ __forceinline__ uint32_t emit_row_chunk_tol(
     const float* v, bool row_ok, float cutoff, float hi_cut, uint32_t gi, uint32_t j0,
     int64_t col_lim, uint32_t* cta_cnt, uint32_t* cta_sat, uint64_t* seg, uint64_t seg_cap,
     uint32_t* sims, uint32_t* pend_cnt, uint32_t* pend, float* scr) {
+  static_assert(CW == 64 || CW == 32, "chunk width");
+  constexpr int kG = CW / 8;
   const int lane = threadIdx.x & 31;
-  float g[8];
+  float g[kG];
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
+  for (int k = 0; k < kG; k++) {
     const float* x = v + 8 * k;
     g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
   }
-  const float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
+  float m;
+  if (CW == 64)
+    m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[kG - 2], g[kG - 1]));
+  else
+    m = fmaxf(fmax3(g[0], g[1], g[2]), g[3]);
   const bool hit = row_ok && m >= cutoff;
   if (!__any_sync(0xffffffffu, hit)) return 0u;
   uint32_t mk0 = 0, mk1 = 0;
   if (hit) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kG; k++) {
       if (g[k] >= cutoff) {
         uint32_t b = 0;
 #pragma unroll
@@ -466,7 +473,7 @@ __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
         else mk1 |= b << (8 * (k - 4));
       }
     }
-    if (col_lim < 64) {
+    if (col_lim < CW) {
       const int cl = col_lim < 0 ? 0 : (int)col_lim;
       mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
       mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
@@ -482,7 +489,7 @@ __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
   const uint32_t lt = lanemask_lt();
   uint32_t finals = 0;
 #pragma unroll
-  for (int hh = 0; hh < 2; hh++) {
+  for (int hh = 0; hh < CW / 32; hh++) {
     uint32_t w = hh ? mk1 : mk0;
     if (w != 0u) {
 #pragma unroll
@@ -518,6 +525,13 @@ __device__ __forceinline__ uint32_t emit_row_chunk64_tol(
     }
   }
   return finals;
+}
+__device__ __forceinline__ uint32_t emit_row_chunk64_tol(
+    const float* v, bool row_ok, float cutoff, float hi_cut, uint32_t gi, uint32_t j0,
+    int64_t col_lim, uint32_t* cta_cnt, uint32_t* cta_sat, uint64_t* seg, uint64_t seg_cap,
+    uint32_t* sims, uint32_t* pend_cnt, uint32_t* pend, float* scr) {
+  return emit_row_chunk_tol<64>(v, row_ok, cutoff, hi_cut, gi, j0, col_lim, cta_cnt, cta_sat, seg,
+                                seg_cap, sims, pend_cnt, pend, scr);
 }
 
 // One canonical recheck of a written candidate slot.

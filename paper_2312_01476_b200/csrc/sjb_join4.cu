@@ -1,31 +1,44 @@
 // sjb_join4.cu -- the K-streaming (d > 128) filter on CTA PAIRS (cta_group::2),
 // tolerance emission (raw bf16 operands, tensor similarities; BASELINE cfg4).
+// The default filter of that mode (kTwo = true).
 //
-// The 1-CTA wide filter (sjb_join3.cu) computes a 256 x 256 output tile per
-// SM from 2 x 256 operand rows per K chunk: 64 KB of shared-memory operands
-// per 1024 MMA cycles, 64 B per cycle per SM at the full tensor rate.  ncu
-// puts the delivered L2 -> SM operand traffic at ~29 B per cycle per SM
-// (tensor pipe 49% active): the kernel is operand-delivery bound, and neither
-// a deeper ring nor S multicast (the SM still receives every byte) moves it.
-// A pair of SMs sharing one UMMA (cta_group::2, M = 256 across the pair)
-// changes the ratio: each CTA holds 128 rows of the R block (its M half) and
-// 256 S rows (its halves of TWO N = 256 operands), and the pair computes a
-// 256 x 512 tile.  Per SM: 128 x 512 outputs per 48 KB per K chunk (was
-// 256 x 256 per 64 KB): 25% fewer operand bytes for the same MMA work.
+// The 1-CTA wide filter (sjb_join3.cu) computes a 256 x 256 output tile per SM
+// and that tile fills the SM's tensor memory (2 x 256 columns), so there is no
+// second accumulator: after a tile's last MMA the tensor pipe waits until the
+// epilogue has drained, normalised and emitted most of the tile.  At the cfg4
+// selectivity (4e-3: 98% of the 32 x 64 warp chunks hold a candidate) that is
+// ~45% of the tile's time: `tools/wide_modes.py` on a 16k x 1M slice gives
+// filter 22.0 ms, tensor pipe 51% active, against 14.9 ms / 95% with the
+// epilogue switched off -- operand delivery is NOT the limit.
 //
-//   * TMEM per CTA: 128 lanes (its R rows) x 512 columns: S rows 0-255 of the
-//     pair tile (half h = 0) and 256-511 (h = 1).  One accumulator tile;
-//     each half goes back to the MMA as soon as both CTAs drained it.
+// A pair of SMs sharing one UMMA (cta_group::2, M = 256 across the pair) halves
+// the accumulator per SM: each CTA holds 128 rows of the R block (its M half)
+// and 128 rows of the S tile (its half of the N = 256 operand), and gets 128
+// lanes x 256 columns of the 256 x 256 pair tile -- HALF its tensor memory.
+// The other half is a second accumulator stage: the pair's MMAs run on tile
+// t + 1 while both CTAs drain tile t (kTwo).  Operand bytes per MMA and per SM
+// are those of the 1-CTA kernel (32 KB per 512 MMA cycles).  With 16 epilogue
+// warps on 32-column chunks (90 registers, four warps per scheduler to hide the
+// emission's latencies) the same slice's filter takes 15.2 ms, tensor pipe 97%
+// active (8 warps on 64-column chunks: 17.0 ms, 79%).
+//
+//   * TMEM per CTA: 128 lanes (its R rows) x 2 stages x 256 columns.
 //   * Operands: 3-D tensor TMA (.cta_group::2, completing on the leader's
 //     barrier) of the [k-group][row][8] operand image: box {256, 4, 8} =
 //     [8 k-groups][128 rows][8] of one image tile = 16 KB, the UMMA K-major
-//     layout (k-group stride 2 KB).  Three per CTA per K chunk: its R half,
-//     and its 128-row halves of image tiles 2t and 2t + 1.
+//     layout (k-group stride 2 KB).  Two per CTA per K chunk: its R half and
+//     its 128-row half of the S tile.
 //   * The leader's warp 1 issues every MMA of the pair; commits are multicast
 //     to both CTAs (ring slots, accumulator full); the epilogue warps of both
 //     CTAs arrive on the leader's accumulator-empty barriers.
-//   * Epilogue: sjb_join3.cu's tolerance emission per 64-column chunk
-//     (normalise after the GEMM, final / pending / no candidate).
+//   * Epilogue: normalise after the GEMM (the tile's inverse norms prefetched
+//     per warp into shared memory before the accumulator wait), then the
+//     tolerance emission (final / pending / no candidate) per chunk.
+//
+// kTwo = false (A/B build, SJB_WIDE_MMA2=1) is the first form tried: a 256 x 512
+// pair tile in one accumulator (each CTA: 128 x 512 outputs per 48 KB per K
+// chunk, 25% fewer operand bytes) -- no faster than the 1-CTA kernel, which is
+// what showed the operand stream was not the limit.
 #include "sjb_common.cuh"
 
 namespace sjb {
@@ -91,15 +104,39 @@ __device__ __forceinline__ void commit2(uint64_t* bar) {
       : "memory");
 }
 
-constexpr int kEpiWarps = 8;
+#ifndef SJB_WIDE2_EPI
+#define SJB_WIDE2_EPI 16
+#endif
+// epilogue warps: 8 (64-column chunks) or 16 (32-column chunks: half the live
+// accumulator registers per thread, four warps per scheduler to hide the
+// emission's latencies)
+constexpr int kEpiWarps = SJB_WIDE2_EPI;
+static_assert(kEpiWarps == 8 || kEpiWarps == 16, "SJB_WIDE2_EPI: 8 or 16");
+constexpr int kCW = kEpiWarps == 8 ? 64 : 32;   // columns per drained chunk
 constexpr int kThreads = 32 * (2 + kEpiWarps);
+// first column (within a 256-column accumulator half) of chunk k of the warps of column group cw
+__device__ __forceinline__ int chunk_col(int cw, int k) {
+  return kEpiWarps == 8 ? (cw + 2 * k) * 64 : cw * 64 + k * 32;
+}
 constexpr int kKChunk = 64;
 constexpr int kHalfRows = 128;
 constexpr uint32_t kPieceBytes = kHalfRows * kKChunk * 2;   // 16 KB
-constexpr uint32_t kStageBytes = 3 * kPieceBytes;           // R half + two S halves
+// ring stage: the R half + two S halves (256 x 512 pair tile, one accumulator
+// tile), or -- kTwo -- the R half + one S half (256 x 256 pair tile, TWO
+// accumulator stages of 256 columns: the drain of one tile overlaps the MMAs
+// of the next; same operand bytes per MMA as the 1-CTA kernel)
+__host__ __device__ constexpr uint32_t stage_bytes(bool two) {
+  return (two ? 2u : 3u) * kPieceBytes;
+}
 constexpr int kTolPitch = 33;
 constexpr uint32_t kTolScratchBytes = kEpiWarps * 32 * kTolPitch * 4;
-constexpr int kMaxStages = 4;
+// kTwo: each epilogue warp's copy of the tile's inverse norms of its two 64-column
+// chunks (32 float4), prefetched before the accumulator wait: the normalisation reads
+// them as shared-memory broadcasts instead of 16 L2-latency loads per chunk
+constexpr uint32_t kInvStageBytes = kEpiWarps * 32 * 16;
+__host__ __device__ constexpr int max_stages(bool two) {
+  return (two ? 5 : 4) - (kEpiWarps == 16 ? 1 : 0);   // 16 warps: twice the emission scratch
+}
 
 struct alignas(64) Params {
   CUtensorMap tmap_a;   // R image as (256, 8, kgroups * tiles), box {256, 4, 8}
@@ -107,7 +144,7 @@ struct alignas(64) Params {
   int64_t n_a, n_b;
   int kpad;
   int n_ablk;           // 256-row R tiles (one per pair)
-  int n_ptiles;         // 512-row pair S tiles in this launch's range end
+  int n_ptiles;         // 512-row pair S tiles (kTwo: 256-row tiles) in this launch's range end
   int tiles_per_chunk;  // pair tiles per work item
   int tile_begin;       // first pair tile of this launch
   int append;
@@ -125,20 +162,24 @@ struct alignas(64) Params {
   uint32_t* rowcount;
   uint32_t* pend;
   uint32_t* pend_count;
-  int debug;   // diagnostics (results invalid): 1 no emission, 2 no drain, 20 no operand traffic
+  int debug;   // diagnostics (results invalid): 1 no emission, 2 no drain, 3 drain + normalise only,
+               // 20 no operand traffic
 };
 
-__host__ __device__ inline uint32_t smem_bytes(int stages) {
-  return (uint32_t)stages * kStageBytes + (4 + 2 * stages) * 8 + 32 + kTolScratchBytes;
+__host__ __device__ inline uint32_t smem_bytes(int stages, bool two) {
+  return (uint32_t)stages * stage_bytes(two) + (4 + 2 * stages) * 8 + 32 + kTolScratchBytes +
+         (two ? kInvStageBytes : 0u);
 }
 
+template <bool kTwo>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     filter_kernel(const __grid_constant__ Params p) {
+  constexpr uint32_t kStageBytes = stage_bytes(kTwo);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * kStageBytes);
-  uint64_t* acc_full = bars + 0;    // both: MMA commit (multicast)
-  uint64_t* acc_empty = bars + 1;   // [2], leader: epilogue warps of both CTAs
+  uint64_t* acc_full = bars + 0;    // [2] (kTwo: per accumulator stage), both: MMA commit (multicast)
+  uint64_t* acc_empty = bars + 2;   // [2], leader: epilogue warps of both CTAs
   uint64_t* full = bars + 4;        // leader: the pair's operand bytes
   uint64_t* empty = bars + 4 + p.stages;   // both: MMA commit (multicast)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * p.stages);
@@ -146,13 +187,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* cta_sat = tmem_slot + 3;
   uint32_t* pend_cnt = tmem_slot + 5;
   float* tol_scratch = reinterpret_cast<float*>(tmem_slot + 8);
+  float4* inv_stage = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(tol_scratch) +
+                                                kTolScratchBytes);   // kTwo only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int64_t pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   if (threadIdx.x == 0) {
-    mbar_init(acc_full, 1);
+    mbar_init(&acc_full[0], 1);
+    mbar_init(&acc_full[1], 1);
     mbar_init(&acc_empty[0], 2 * kEpiWarps);
     mbar_init(&acc_empty[1], 2 * kEpiWarps);
     for (int s = 0; s < p.stages; s++) {
@@ -202,10 +246,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint8_t* dst = ring + (size_t)s * kStageBytes;
             tma3d_2sm(dst, &p.tmap_a, 0, 4 * (int)rank, (int)(rb * kg + c * 8), &full[s],
                             pol_a);
-            tma3d_2sm(dst + kPieceBytes, &p.tmap_b, 0, 4 * (int)rank,
-                            (int)(2 * t * kg + c * 8), &full[s], pol_b);
-            tma3d_2sm(dst + 2 * kPieceBytes, &p.tmap_b, 0, 4 * (int)rank,
-                            (int)((2 * t + 1) * kg + c * 8), &full[s], pol_b);
+            if (kTwo) {
+              tma3d_2sm(dst + kPieceBytes, &p.tmap_b, 0, 4 * (int)rank, (int)(t * kg + c * 8),
+                        &full[s], pol_b);
+            } else {
+              tma3d_2sm(dst + kPieceBytes, &p.tmap_b, 0, 4 * (int)rank,
+                        (int)(2 * t * kg + c * 8), &full[s], pol_b);
+              tma3d_2sm(dst + 2 * kPieceBytes, &p.tmap_b, 0, 4 * (int)rank,
+                        (int)((2 * t + 1) * kg + c * 8), &full[s], pol_b);
+            }
             if (++s == p.stages) {
               s = 0;
               ph ^= 1u;
@@ -233,17 +282,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             const uint64_t ad = ring_desc + (uint64_t)s * stage_step;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-              if (c == 0) {   // both CTAs drained half h of the previous tile?
-                mbar_wait(&acc_empty[h], (tile_it & 1u) ^ 1u);
+            if (kTwo) {
+              const uint32_t st = tile_it & 1u;
+              if (c == 0) {   // both CTAs drained the tile before last (same stage)?
+                mbar_wait(&acc_empty[st], ((tile_it >> 1) & 1u) ^ 1u);
                 tc_fence_after();
               }
-              const uint64_t bd = ad + (uint64_t)(1 + h) * piece;
+              const uint64_t bd = ad + piece;
 #pragma unroll
               for (int kk = 0; kk < kKChunk / 16; kk++)
-                mma2(tmem_base + h * 256, ad + kk * kstep, bd + kk * kstep, idesc,
-                           (c | kk) ? 1u : 0u);
+                mma2(tmem_base + st * 256, ad + kk * kstep, bd + kk * kstep, idesc,
+                     (c | kk) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                if (c == 0) {   // both CTAs drained half h of the previous tile?
+                  mbar_wait(&acc_empty[h], (tile_it & 1u) ^ 1u);
+                  tc_fence_after();
+                }
+                const uint64_t bd = ad + (uint64_t)(1 + h) * piece;
+#pragma unroll
+                for (int kk = 0; kk < kKChunk / 16; kk++)
+                  mma2(tmem_base + h * 256, ad + kk * kstep, bd + kk * kstep, idesc,
+                       (c | kk) ? 1u : 0u);
+              }
             }
             commit2(&empty[s]);
             if (++s == p.stages) {
@@ -251,7 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ph ^= 1u;
             }
           }
-          commit2(acc_full);
+          commit2(&acc_full[kTwo ? (tile_it & 1u) : 0u]);
         }
       }
     }
@@ -261,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // chunks c, c + 2 (64 each) of both halves; a half is handed back to the
     // leader after its last chunk is loaded
     const int ew = warp - 2;
-    const int cq0 = ew >> 2, q = warp & 3;
+    const int cw = ew >> 2, q = warp & 3;
     const uint32_t lane_base = (uint32_t)q * 32;
     uint64_t* seg = p.cand + (uint64_t)blockIdx.x * p.seg_cap;
     uint32_t* sims = p.sims_bits + (uint64_t)blockIdx.x * p.seg_cap;
@@ -277,14 +339,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float inv_i = row_ok ? __ldg(p.inv_a + gi64) : 1.0f;
       uint32_t fin = 0u;
       for (int64_t t = t0; t < t1; t++, tile_it++) {
-        mbar_wait(acc_full, tile_it & 1u);
+        float4 inv4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kTwo && lane < 2 * (kCW / 4))   // the warp's two chunks' float4s; land during the wait
+          inv4 = __ldg(reinterpret_cast<const float4*>(p.inv_b + t * kTileRows +
+                                                       chunk_col(cw, lane / (kCW / 4))) +
+                       (lane % (kCW / 4)));
+        if (kTwo)
+          mbar_wait(&acc_full[tile_it & 1u], (tile_it >> 1) & 1u);
+        else
+          mbar_wait(&acc_full[0], tile_it & 1u);
         tc_fence_after();
+        if (kTwo) {
+          __syncwarp();   // the previous tile's reads are done
+          inv_stage[ew * 32 + lane] = inv4;
+          __syncwarp();
+        }
 #pragma unroll 1
-        for (int h = 0; h < 2; h++) {
+        for (int h = kTwo ? (int)(tile_it & 1u) : 0; h < 2; h += kTwo ? 2 : 1) {
 #pragma unroll 1
           for (int k = 0; k < 2; k++) {
-            const int cq = cq0 + 2 * k;
-            const uint32_t taddr = tmem_base + (lane_base << 16) + h * 256 + cq * 64;
+            const int cc = chunk_col(cw, k);
+            const uint32_t taddr = tmem_base + (lane_base << 16) + h * 256 + cc;
             if (p.debug == 2) {   // diagnostics: no drain
               if (k == 1) {
                 tc_fence_before();
@@ -296,9 +371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
               continue;
             }
-            float v[64];
+            float v[kCW];
             SJB_TMEM_LD32(taddr, v, 0);
-            SJB_TMEM_LD32(taddr + 32, v, 32);
+            if (kCW == 64) SJB_TMEM_LD32(taddr + 32, v, kCW - 32);
             tc_wait_ld();
             if (k == 1) {
               tc_fence_before();
@@ -311,25 +386,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (p.debug == 1) {   // diagnostics: drain, no emission
               float m = v[0];
 #pragma unroll
-              for (int e = 1; e < 64; e++) m = fmaxf(m, v[e]);
+              for (int e = 1; e < kCW; e++) m = fmaxf(m, v[e]);
               if (m > 3.0e38f) cta_sat[0] = 1u;
               continue;
             }
-            const int64_t col0 = t * 2 * kTileRows + h * kTileRows + cq * 64;
+            const int64_t col0 =
+                kTwo ? t * kTileRows + cc : t * 2 * kTileRows + h * kTileRows + cc;
             // normalise after the GEMM: (acc * inv_i) * inv_j (inv_b is
             // padded to whole 512-row tile pairs, zero past n_b)
             const float4* ib = reinterpret_cast<const float4*>(p.inv_b + col0);
+            const float4* is = inv_stage + ew * 32 + (kCW / 4) * k;
 #pragma unroll
-            for (int q4 = 0; q4 < 16; q4++) {
-              const float4 w = __ldg(ib + q4);
+            for (int q4 = 0; q4 < kCW / 4; q4++) {
+              const float4 w = kTwo ? is[q4] : __ldg(ib + q4);
               v[4 * q4 + 0] = __fmul_rn(__fmul_rn(v[4 * q4 + 0], inv_i), w.x);
               v[4 * q4 + 1] = __fmul_rn(__fmul_rn(v[4 * q4 + 1], inv_i), w.y);
               v[4 * q4 + 2] = __fmul_rn(__fmul_rn(v[4 * q4 + 2], inv_i), w.z);
               v[4 * q4 + 3] = __fmul_rn(__fmul_rn(v[4 * q4 + 3], inv_i), w.w);
             }
-            fin += emit_row_chunk64_tol(v, row_ok, p.cutoff, p.hi_cut, (uint32_t)gi64,
-                                        (uint32_t)col0, p.n_b - col0, cta_cnt, cta_sat, seg,
-                                        p.seg_cap, sims, pend_cnt, pend, scr);
+            if (p.debug == 3) {   // diagnostics: drain + normalise, no emission
+              float m = v[0];
+#pragma unroll
+              for (int e = 1; e < kCW; e++) m = fmaxf(m, v[e]);
+              if (m > 3.0e38f) cta_sat[0] = 1u;
+              continue;
+            }
+            fin += emit_row_chunk_tol<kCW>(v, row_ok, p.cutoff, p.hi_cut, (uint32_t)gi64,
+                                           (uint32_t)col0, p.n_b - col0, cta_cnt, cta_sat, seg,
+                                           p.seg_cap, sims, pend_cnt, pend, scr);
           }
         }
       }

@@ -960,11 +960,12 @@ def test_bf16_overflow_retry_tensor_sims(cuda):
     assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
 
 
-@pytest.mark.parametrize("mma2", ["1", "0"])
+@pytest.mark.parametrize("mma2", ["1", "2", "0"])
 def test_wide_mma2_pair_kernel(cuda, monkeypatch, mma2):
-    """A/B: tensor sims on raw bf16 operands through the cta_group::2 wide
-    kernel (SJB_WIDE_MMA2=1, -DSJB_AB_KERNELS=1: 256 x 512 tiles per SM pair,
-    operands by 2-SM tensor TMA; the default library rejects the switch) and
+    """Tensor sims on raw bf16 operands through the cta_group::2 wide kernel
+    (default, SJB_WIDE_MMA2=2: 256 x 256 tiles per SM pair with two accumulator
+    stages, operands by 2-SM tensor TMA; =1, -DSJB_AB_KERNELS=1 only: 256 x 512
+    tiles, one accumulator tile -- the default library rejects that switch) and
     the 1-CTA kernel: odd R tile counts, partial pair tiles, an overflow
     retry -- the oracle's pair set, sims within 1e-5."""
     from paper_2312_01476_b200 import _lib, device as D

@@ -35,6 +35,8 @@ for var in variants:
         os.environ.pop(k, None)
     if var == "mma2":
         os.environ["SJB_WIDE_MMA2"] = "1"
+    elif var == "mma2s":   # 256 x 256 pair tiles, two accumulator stages
+        os.environ["SJB_WIDE_MMA2"] = "2"
     elif var == "pair":
         os.environ["SJB_WIDE_PAIR"] = "1"
     for mode in modes:

@@ -1134,9 +1134,25 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       }
       if (wp.tol && jp.debug_mode != 1) {
         // tolerance emission: only the band pairs need the canonical chain
-        sjb::wide::recheck_pending_kernel<<<sjb_sm_count(current_device()) * 8, 256, 0, st>>>(
-            c.cand, pl.seg_cap, c.pend, c.pend_count, c.cta, pl.grid, d_l32, d_r32,
-            (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+        // rows staged through shared memory by whole warps (default; dim % 4 = 0 and
+        // 16-byte aligned rows); SJB_PENDING=gather: the thread-per-pair gather (A/B)
+        const char* pv = getenv("SJB_PENDING");
+        const bool staged = (args->dim % 4) == 0 &&
+                            ((reinterpret_cast<uintptr_t>(d_l32) | reinterpret_cast<uintptr_t>(d_r32)) & 15) == 0 &&
+                            !(pv != nullptr && strcmp(pv, "gather") == 0);
+        if (staged) {
+          const uint32_t psm = sjb::wide::pending_staged_smem();
+          if (int rc = set_smem_attr((const void*)sjb::wide::recheck_pending_staged_kernel, (int)psm))
+            return rc;
+          sjb::wide::recheck_pending_staged_kernel<<<sjb_sm_count(current_device()),
+                                                     sjb::wide::kPsWarps * 32, psm, st>>>(
+              c.cand, pl.seg_cap, c.pend, c.pend_count, c.cta, pl.grid, d_l32, d_r32,
+              (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+        } else {
+          sjb::wide::recheck_pending_kernel<<<sjb_sm_count(current_device()) * 8, 256, 0, st>>>(
+              c.cand, pl.seg_cap, c.pend, c.pend_count, c.cta, pl.grid, d_l32, d_r32,
+              (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+        }
         SJB_CK_LAUNCH("recheck_pending");
       } else if (jp.debug_mode != 1) {
         sjb::wide::RecheckParams rp;

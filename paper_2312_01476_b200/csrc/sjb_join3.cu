@@ -1098,5 +1098,112 @@ recheck_pending_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
   }
 }
 
+// The same recheck with the rows STAGED: a warp takes 32 consecutive positions
+// (lane = pair) and walks both rows of every pair in 32-element chunks.  The
+// whole warp copies a chunk of all 64 rows with 16-byte cp.async (8 lanes per
+// 128-byte line: full sectors, coalesced) into its shared-memory ring, and each
+// lane then advances its own pair's chain from shared memory (16-byte pieces
+// XOR-swizzled by the pair index: conflict-free for lane = row reads).  The
+// thread-per-pair gather above touches 32 different sectors per load
+// instruction and re-fetches each sector's other half from L2 once the SM's
+// 2048 threads' working set outgrows L1; this kernel moves each row byte once.
+// dim % 4 = 0 and 16-byte aligned rows (the caller checks).
+constexpr int kPsWarps = 8;
+constexpr int kPsBufs = 3;                       // chunks in the ring (two in flight)
+constexpr int kPsChunk = 32;                     // elements per chunk (128 B per row)
+constexpr uint32_t kPsBufBytes = 2u * 32u * kPsChunk * 4u;   // 32 pairs x 2 rows
+__host__ __device__ constexpr uint32_t pending_staged_smem() {
+  return kPsWarps * kPsBufs * kPsBufBytes;
+}
+
+__device__ __forceinline__ void cp_async_wait_two() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kPsWarps * 32, 1)
+recheck_pending_staged_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                              const uint32_t* __restrict__ pend,
+                              const uint32_t* __restrict__ pend_count,
+                              const unsigned long long* __restrict__ cta_count, int n_cta,
+                              const float* __restrict__ l32, const float* __restrict__ r32, int dim,
+                              float theta, uint32_t* __restrict__ sims_bits,
+                              uint32_t* __restrict__ rowcount) {
+  extern __shared__ __align__(128) uint8_t ps_smem[];
+  __shared__ uint32_t s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_cta; c += blockDim.x) atomicMax(&s_max, pend_count[c]);
+  __syncthreads();
+  const uint64_t total = (uint64_t)s_max * (uint64_t)n_cta;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = ps_smem + (size_t)warp * kPsBufs * kPsBufBytes;
+  const int nchunks = (dim + kPsChunk - 1) / kPsChunk;
+  const int sub = lane >> 3, piece = lane & 7;   // this lane's share of every copy round
+  const uint64_t n_groups = (total + 31) / 32;
+  for (uint64_t g = (uint64_t)blockIdx.x * kPsWarps + warp; g < n_groups;
+       g += (uint64_t)gridDim.x * kPsWarps) {
+    const uint64_t p = g * 32 + lane;
+    bool ok = false;
+    uint64_t slot = 0;
+    uint32_t gi = 0, gj = 0;
+    if (p < total) {
+      const uint64_t k = p / (uint64_t)n_cta, c = p - k * (uint64_t)n_cta;
+      if (k < pend_count[c] && cta_count[c] <= seg_cap) {
+        slot = c * seg_cap + pend[c * seg_cap + k];
+        const uint64_t u = cand[slot];
+        gi = (uint32_t)(u >> 32);
+        gj = (uint32_t)u;
+        ok = true;
+      }
+    }
+    if (!__any_sync(0xffffffffu, ok)) continue;
+    // the 8 pairs whose lines this lane copies in every chunk: sub, sub + 4, ...
+    const float* srcA[8];
+    const float* srcB[8];
+#pragma unroll
+    for (int it = 0; it < 8; it++) {
+      const uint32_t i = __shfl_sync(0xffffffffu, gi, it * 4 + sub);
+      const uint32_t j = __shfl_sync(0xffffffffu, gj, it * 4 + sub);
+      srcA[it] = l32 + (size_t)i * dim + piece * 4;
+      srcB[it] = r32 + (size_t)j * dim + piece * 4;
+    }
+    auto issue = [&](int c) {
+      if (c < nchunks && c * kPsChunk + piece * 4 < dim) {
+        uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes;
+#pragma unroll
+        for (int it = 0; it < 8; it++) {
+          const int pr = it * 4 + sub;
+          const uint32_t off = (uint32_t)pr * 128u + (uint32_t)((piece ^ (pr & 7)) * 16);
+          cp_async16(reinterpret_cast<float*>(buf + off), srcA[it] + c * kPsChunk);
+          cp_async16(reinterpret_cast<float*>(buf + 4096u + off), srcB[it] + c * kPsChunk);
+        }
+      }
+      cp_async_commit();
+    };
+    issue(0);
+    issue(1);
+    float acc = 0.0f;
+    for (int c = 0; c < nchunks; c++) {
+      issue(c + 2);
+      cp_async_wait_two();   // chunk c has landed (this lane's copies)
+      __syncwarp();          // ... and every lane's
+      const uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes + (uint32_t)lane * 128u;
+      const int np = mn<int>(8, (dim - c * kPsChunk) >> 2);
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if (q < np) {
+          const uint32_t o = (uint32_t)((q ^ (lane & 7)) * 16);
+          const float4 x = *reinterpret_cast<const float4*>(buf + o);
+          const float4 y = *reinterpret_cast<const float4*>(buf + 4096u + o);
+          acc = __fmaf_rn(x.x, y.x, acc);
+          acc = __fmaf_rn(x.y, y.y, acc);
+          acc = __fmaf_rn(x.z, y.z, acc);
+          acc = __fmaf_rn(x.w, y.w, acc);
+        }
+      }
+      __syncwarp();          // the buffer may be refilled (chunk c + 3)
+    }
+    if (ok) finish_candidate(sims_bits, slot, gi, acc, theta, rowcount);
+  }
+}
+
 }  // namespace wide
 }  // namespace sjb

@@ -990,6 +990,31 @@ def test_wide_mma2_pair_kernel(cuda, monkeypatch, mma2):
             assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
 
 
+def test_pending_recheck_staged_equals_gather(cuda, monkeypatch):
+    """Tensor sims: the band pairs' canonical recheck with rows staged through
+    shared memory by whole warps (default) against the thread-per-pair gather
+    (SJB_PENDING=gather): the same MatchSet bit for bit (pending pairs carry
+    the canonical chain's bits), and the oracle's pair set.  Dims that are not
+    a multiple of the 32-element chunk end in a partial chunk."""
+    from paper_2312_01476_b200 import device as D
+    for nl, nr, dim, seed in ((700, 1900, 768, 51), (513, 1100, 260, 52), (300, 2300, 388, 53)):
+        L, S = _bf16_case(nl, nr, dim, 6, 0.7, seed)
+        theta = 0.55
+        wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+        assert len(wl) > 0
+        pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+        out = {}
+        for mode in ("staged", "gather"):
+            monkeypatch.setenv("SJB_PENDING", mode)
+            out[mode] = D.join_prepared(pl, pr, theta, sims="tensor").to_host()
+            lo, ro, so = out[mode]
+            assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (dim, mode)
+            assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
+        assert np.array_equal(out["staged"][2].view(np.uint32), out["gather"][2].view(np.uint32))
+        # some pairs were decided by the canonical chain: their sims are the oracle's bits
+        assert (out["staged"][2].view(np.uint32) == ws.view(np.uint32)).any()
+
+
 @pytest.mark.parametrize("pair", ["1", "0"])
 def test_wide_pair_multicast(cuda, monkeypatch, pair):
     """A/B: wide-path tensor sims with CTA pairs sharing each S chunk by TMA

@@ -738,7 +738,8 @@ def run_ours(args):
             "config": {"workload": c["desc"], "global_batch": pairs_total,
                        "parallelism": f"R-shard x{world}" + (
                            ", S owner-prepared + all-gathered per round" if world > 1 else ""),
-                       "band": D.default_band(dim), "l2": "flushed (256 MiB write) between "
+                       "band": D.raw_band(dim) if c["kind"] == "wide" else D.default_band(dim),
+                       "l2": "flushed (256 MiB write) between "
                                                          "timed steps",
                        "matches": n_matches, "candidates": n_cand,
                        "output_pairs_per_s": n_matches / (ms_per_step / 1e3),
@@ -753,8 +754,11 @@ def run_ours(args):
                          "k_pad_cap": dim / D.kpad(dim)},
             "e2e": {"value": pairs_total / e2e_time, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_time,
-                    "inputs": "pinned host" if c["kind"] == "vectors" else
-                              "host strings through tensor_join(RawRelation, SubwordModel)"},
+                    "inputs": {"vectors": "pinned host",
+                               "wide": "pinned host bf16 rows (tensor_join_vectors), MatchSet "
+                                       "columns copied back per left-row part"}.get(
+                        c["kind"], "host strings through tensor_join(RawRelation, "
+                                   "SubwordModel)")},
             **e2e_extra,
             "gpu_launches": launches,
             "clocks": clk.summary(),

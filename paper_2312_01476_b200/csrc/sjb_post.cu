@@ -1453,14 +1453,20 @@ __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0,
     }
     __syncthreads();
     // group sums, then an exclusive scan over the 1024 groups (warp 0)
-    for (int q = tid; q < kRankGroups; q += nthr) {
-      uint32_t c = 0;
-#pragma unroll 8
-      for (int k = 0; k < 32; k++) {
-        wpre[q * 32 + k] = (uint16_t)c;
-        c += __popc(bits[q * 32 + k]);
+    // one warp per group, lane = word: conflict-free reads and writes (a thread
+    // per group walked its 32 words at a 128-byte stride: 32-way bank conflicts,
+    // ~49k cycles of shared-memory wavefronts per window)
+    for (int q = tid >> 5; q < kRankGroups; q += nthr >> 5) {
+      const int lane = tid & 31;
+      const uint32_t c = __popc(bits[q * 32 + lane]);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      gpre[q] = c;
+      wpre[q * 32 + lane] = (uint16_t)(incl - c);
+      if (lane == 31) gpre[q] = incl;
     }
     __syncthreads();
     if (tid < 32) {

@@ -910,6 +910,8 @@ int join_begin(const sjb_join_args* args, const JoinCtx& c, cudaStream_t st) {
   SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)args->n_left * 4, st));
   SJB_CK(cudaMemsetAsync(c.nbig, 0, 16, st));
   SJB_CK(cudaMemsetAsync(c.cta, 0, (size_t)pl.grid * 8, st));
+  if (args->sims_mode == 1 && c.pend_count != nullptr)   // a filter may launch fewer CTAs than pl.grid
+    SJB_CK(cudaMemsetAsync(c.pend_count, 0, (size_t)pl.grid * 4, st));
   // candidate slots start empty: the fused recheck waits for each slot's write
   if (fused_recheck(pl))
     SJB_CK(cudaMemsetAsync(c.cand, 0xFF, (size_t)pl.grid * pl.seg_cap * 8, st));
@@ -1096,7 +1098,28 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         const uint32_t sm2 = sjb::wide2::smem_bytes(q.stages, mma2_two);
         if (mma2_two) {
           if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel<true>, (int)sm2)) return rc;
-          sjb::wide2::filter_kernel<true><<<pl.grid, sjb::wide2::kThreads, sm2, st>>>(q);
+          // the kernel is persistent with a static item -> pair map: every pair must be
+          // resident at once.  A GPC with an odd number of free SMs strands one, so ask
+          // how many 2-CTA clusters fit and launch no more (CTAs beyond them keep empty
+          // candidate segments; the count is the same for every launch of a join)
+          static int max_pairs[64] = {};
+          const int dv = current_device();
+          if (dv >= 0 && dv < 64 && max_pairs[dv] == 0) {
+            cudaLaunchConfig_t oc = {};
+            oc.gridDim = dim3((unsigned)pl.grid);
+            oc.blockDim = dim3(sjb::wide2::kThreads);
+            oc.dynamicSmemBytes = sm2;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, sjb::wide2::filter_kernel<true>, &oc) !=
+                    cudaSuccess || nc <= 0) {
+              (void)cudaGetLastError();
+              nc = 1 << 20;   // unknown: do not limit
+            }
+            max_pairs[dv] = nc;
+          }
+          const int lim = (dv >= 0 && dv < 64) ? max_pairs[dv] : (1 << 20);
+          const int g2 = 2 * (pl.grid / 2 < lim ? pl.grid / 2 : lim);
+          sjb::wide2::filter_kernel<true><<<g2, sjb::wide2::kThreads, sm2, st>>>(q);
         } else {
 #if SJB_AB_KERNELS
           if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel<false>, (int)sm2)) return rc;

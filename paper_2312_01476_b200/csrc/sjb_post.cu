@@ -1433,71 +1433,94 @@ constexpr int kSortBigCap = 26624;   // keys sorted whole in shared memory (208 
 // q0 + (keys in earlier windows) + rank: three shared reads per key.
 constexpr int kRankWindow = 1 << 20;                  // bits: 128 KB of shared memory
 constexpr int kRankWords = kRankWindow / 32;
-constexpr int kRankGroups = kRankWords / 32;           // 1024 groups of 32 words
-static_assert(kRankWords * 4 + (kRankGroups + 1) * 4 + kRankWords * 2 <= kSortBigCap * 8,
+constexpr int kRankSub = 8;                            // words per prefix group (256 bits)
+constexpr int kRankGroups = kRankWords / kRankSub;     // 4096 groups
+constexpr int kRankPer = kRankGroups / kSortBigThreads;   // consecutive groups scanned per thread
+static_assert(kRankGroups % kSortBigThreads == 0 && kRankPer == 8, "group scan layout");
+static_assert(kRankWords * 4 + (kRankGroups + 1) * 4 + 64 <= kSortBigCap * 8,
               "bitmap + prefixes fit the buffer");
 
+// Per window: clear the bitmap (16-byte stores), set the keys' bits, count each
+// 8-word group (two 16-byte loads per group), exclusive-scan the 4096 group
+// counts (8 consecutive counts per thread + one block scan), then place each
+// key: group prefix + the popcounts of the <= 7 words before its word + the
+// masked popcount of its word.  (A u16 prefix per WORD cost a pass over all
+// 32768 words per window -- 25k warp instructions even with conflict-free
+// warp-per-group scans -- for 3 reads per key; rows of a few thousand keys are
+// far cheaper with 4096 prefixes and ~6 reads per key.)
 __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0, uint64_t i_row,
                          int64_t n_right, uint32_t* bits, uint32_t* gpre,
                          uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                          float* __restrict__ sims) {
-  uint16_t* wpre = reinterpret_cast<uint16_t*>(gpre + kRankGroups + 1);  // in-group word prefix
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  uint32_t* wsum = gpre + kRankGroups + 1;   // per-warp totals of the block scan (16)
+  const int tid = threadIdx.x, nthr = blockDim.x;   // nthr == kSortBigThreads
+  const int lane = tid & 31, warp = tid >> 5;
+  uint4* b4 = reinterpret_cast<uint4*>(bits);
   uint64_t base = 0;
   for (int64_t w0 = 0; w0 < n_right; w0 += kRankWindow) {
-    for (int t = tid; t < kRankWords; t += nthr) bits[t] = 0u;
+    for (int t = tid; t < kRankWords / 4; t += nthr) b4[t] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     for (int64_t t = tid; t < n; t += nthr) {
       const uint64_t o = (g[t] >> 32) - (uint64_t)w0;
       if (o < (uint64_t)kRankWindow) atomicOr(&bits[o >> 5], 1u << (o & 31));
     }
     __syncthreads();
-    // group sums, then an exclusive scan over the 1024 groups (warp 0)
-    // one warp per group, lane = word: conflict-free reads and writes (a thread
-    // per group walked its 32 words at a 128-byte stride: 32-way bank conflicts,
-    // ~49k cycles of shared-memory wavefronts per window)
-    for (int q = tid >> 5; q < kRankGroups; q += nthr >> 5) {
-      const int lane = tid & 31;
-      const uint32_t c = __popc(bits[q * 32 + lane]);
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      wpre[q * 32 + lane] = (uint16_t)(incl - c);
-      if (lane == 31) gpre[q] = incl;
+    // group counts: thread t counts groups t, t + nthr, ... (neighbouring
+    // lanes read neighbouring 32-byte groups)
+    for (int q = tid; q < kRankGroups; q += nthr) {
+      const uint4 x = b4[2 * q], y = b4[2 * q + 1];
+      gpre[q] = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w) + __popc(y.x) +
+                __popc(y.y) + __popc(y.z) + __popc(y.w);
     }
     __syncthreads();
-    if (tid < 32) {
-      uint32_t carry = 0;
-      for (int q0g = 0; q0g < kRankGroups; q0g += 32) {
-        const uint32_t v = gpre[q0g + tid];
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (tid >= o) incl += y;
-        }
-        gpre[q0g + tid] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (tid == 0) gpre[kRankGroups] = carry;
+    // exclusive scan: thread t owns counts 8t .. 8t + 7
+    uint32_t c[kRankPer];
+    {
+      const uint4 x = reinterpret_cast<const uint4*>(gpre)[2 * tid];
+      const uint4 y = reinterpret_cast<const uint4*>(gpre)[2 * tid + 1];
+      c[0] = x.x; c[1] = x.y; c[2] = x.z; c[3] = x.w;
+      c[4] = y.x; c[5] = y.y; c[6] = y.z; c[7] = y.w;
     }
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < kRankPer; k++) {
+      const uint32_t v = c[k];
+      c[k] = tot;
+      tot += v;
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, all = 0;
+    for (int w = 0; w < (nthr >> 5); w++) {
+      const uint32_t v = wsum[w];
+      if (w < warp) wbase += v;
+      all += v;
+    }
+    const uint32_t tb = wbase + incl - tot;
+    reinterpret_cast<uint4*>(gpre)[2 * tid] =
+        make_uint4(tb + c[0], tb + c[1], tb + c[2], tb + c[3]);
+    reinterpret_cast<uint4*>(gpre)[2 * tid + 1] =
+        make_uint4(tb + c[4], tb + c[5], tb + c[6], tb + c[7]);
     __syncthreads();
     for (int64_t t = tid; t < n; t += nthr) {
       const uint64_t key = g[t];
       const uint64_t o = (key >> 32) - (uint64_t)w0;
       if (o >= (uint64_t)kRankWindow) continue;
-      const uint32_t word = (uint32_t)(o >> 5), grp = word >> 5;
-      const uint32_t rank =
-          gpre[grp] + wpre[word] + __popc(bits[word] & ((1u << (o & 31)) - 1u));
+      const uint32_t word = (uint32_t)(o >> 5), grp = word / kRankSub;
+      uint32_t rank = gpre[grp] + __popc(bits[word] & ((1u << (o & 31)) - 1u));
+      for (uint32_t w = grp * kRankSub; w < word; w++) rank += __popc(bits[w]);
       const uint64_t pos = q0 + base + rank;
       lefts[pos] = i_row;
       rights[pos] = key >> 32;
       sims[pos] = __uint_as_float((uint32_t)key);
     }
-    base += gpre[kRankGroups];
+    base += all;
     __syncthreads();
   }
 }
@@ -1507,7 +1530,7 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
                    uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
                    float* __restrict__ sims, const uint32_t* __restrict__ big_rows,
                    const unsigned int* __restrict__ n_big, uint64_t left_base, int64_t n_right) {
-  extern __shared__ uint64_t sbuf[];
+  extern __shared__ __align__(16) uint64_t sbuf[];
   if (n_big[1] == 0) return;  // gate: outputs would overflow
   const unsigned nb = n_big[0];
   for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
@@ -1521,7 +1544,7 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
     while ((1ll << lg) < n) lg++;
     const int64_t windows = (n_right + kRankWindow - 1) / kRankWindow;
     const bool rank = n > kSortBigCap ||
-                      windows * (2 * (int64_t)kRankWords + 2 * n) < (1ll << lg) * lg * (lg + 1);
+                      windows * ((int64_t)kRankWords / 2 + 6 * n) < (1ll << lg) * lg * (lg + 1);
     if (!rank) {
       for (int t = threadIdx.x; t < n; t += blockDim.x) sbuf[t] = g[t];
       __syncthreads();

@@ -990,6 +990,31 @@ def test_wide_mma2_pair_kernel(cuda, monkeypatch, mma2):
             assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
 
 
+@pytest.mark.parametrize("grid", [0, 132, 131])
+def test_bf16_tensor_sims_incremental_rounds(cuda, grid):
+    """Tensor sims through the incremental join (JoinSession: the multi-GPU
+    rounds' entry): S filtered in uneven row ranges that start on odd and even
+    tiles, on the full grid, a reduced even grid (CTA pairs) and an odd grid
+    (which falls back to the 1-CTA wide filter) -- the oracle's pair set, sims
+    within 1e-5, identical to the one-launch join."""
+    from paper_2312_01476_b200 import device as D
+    L, S = _bf16_case(700, 2900, 384, 10, 0.6, 61)
+    theta = 0.6
+    wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+    assert len(wl) > 0
+    pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+    one = D.join_prepared(pl, pr, theta, sims="tensor").to_host()
+    sess = D.JoinSession(pl, pr, theta, None, 0, grid=grid, sims="tensor")
+    for r0, r1 in ((0, 256), (256, 1024), (1024, 1280), (1280, 2900)):
+        sess.filter_rows(r0, r1)
+    lo, ro, so = sess.finish().result().to_host()
+    assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+    assert np.abs(so.astype(np.float64) - ws).max() <= 1e-5
+    assert np.array_equal(lo, one[0]) and np.array_equal(ro, one[1])
+    if grid != 131:   # the same kernel and K order: the same accumulator bits
+        assert np.array_equal(so.view(np.uint32), one[2].view(np.uint32))
+
+
 def test_pending_recheck_staged_equals_gather(cuda, monkeypatch):
     """Tensor sims: the band pairs' canonical recheck with rows staged through
     shared memory by whole warps (default) against the thread-per-pair gather

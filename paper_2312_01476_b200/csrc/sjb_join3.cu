@@ -96,9 +96,16 @@ struct Params {
 constexpr int kTolPitch = 33;
 constexpr uint32_t kTolScratchBytes = kEpiWarps * 32 * kTolPitch * 4;
 
+// Without the tolerance scratch the same place holds each epilogue warp's copy
+// of the tile's inverse norms (raw-operand mode, canonical sims): its chunks'
+// 64 floats each, prefetched before the accumulator wait and read as
+// shared-memory broadcasts -- the per-chunk __ldg's of inv_b sat on the tile's
+// critical path (one L2 round trip per chunk before the half is released).
+constexpr uint32_t kInvStageBytes = kEpiWarps * 32 * 16;
+
 __host__ __device__ inline uint32_t smem_bytes(int stages, bool tol = false) {
   return (uint32_t)stages * 2 * kChunkBytes + (4 + 2 * stages) * 8 + 32 +
-         (tol ? kTolScratchBytes : 0u);
+         (tol ? kTolScratchBytes : kInvStageBytes);
 }
 
 // Max tiles one CTA walks in one launch (+1 for the end offset), for any
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
   uint32_t* epi_done = tmem_slot + 4;
   uint32_t* pend_cnt = tmem_slot + 5;
   float* tol_scratch = reinterpret_cast<float*>(tmem_slot + 8);   // kTolScratchBytes (tol only)
+  float4* inv_stage = reinterpret_cast<float4*>(tmem_slot + 8);   // kInvStageBytes (!tol, raw mode)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -308,8 +316,19 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_btiles);
       uint32_t fin0 = 0u, fin1 = 0u;   // tolerance emission: this lane's rows' final matches
       for (int64_t t = t0; t < t1; t++, tile_it++) {
+        const bool stage_inv = p.inv_a != nullptr && !p.tol;
+        float4 inv4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (stage_inv && lane < 16 * kChunksPerWarp)   // lands during the accumulator wait
+          inv4 = __ldg(reinterpret_cast<const float4*>(
+                           p.inv_b + t * kTileRows +
+                           (cq0 + (lane >> 4) * (kEpiWarps / 4)) * 64) + (lane & 15));
         mbar_wait(acc_full, tile_it & 1u);
         tc_fence_after();
+        if (stage_inv) {
+          __syncwarp();   // the previous tile's reads are done
+          inv_stage[ew * 32 + lane] = inv4;
+          __syncwarp();
+        }
         if (!kFused) {
           // every epilogue warp is done with the previous tile's emission:
           // the counter is this tile's first slot
@@ -355,9 +374,10 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
               // normalise after the GEMM: (acc * inv_i) * inv_j (inv_b is
               // padded to whole tiles, zero past n_b)
               const float4* ib = reinterpret_cast<const float4*>(p.inv_b + t * kTileRows + cq * 64);
+              const float4* is = inv_stage + ew * 32 + 16 * k;
 #pragma unroll
               for (int q4 = 0; q4 < 16; q4++) {
-                const float4 w = __ldg(ib + q4);
+                const float4 w = stage_inv ? is[q4] : __ldg(ib + q4);
                 v[4 * q4 + 0] = __fmul_rn(__fmul_rn(v[4 * q4 + 0], inv_i), w.x);
                 v[4 * q4 + 1] = __fmul_rn(__fmul_rn(v[4 * q4 + 1], inv_i), w.y);
                 v[4 * q4 + 2] = __fmul_rn(__fmul_rn(v[4 * q4 + 2], inv_i), w.z);

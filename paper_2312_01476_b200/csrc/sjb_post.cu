@@ -1437,8 +1437,11 @@ constexpr int kRankSub = 8;                            // words per prefix group
 constexpr int kRankGroups = kRankWords / kRankSub;     // 4096 groups
 constexpr int kRankPer = kRankGroups / kSortBigThreads;   // consecutive groups scanned per thread
 static_assert(kRankGroups % kSortBigThreads == 0 && kRankPer == 8, "group scan layout");
-static_assert(kRankWords * 4 + (kRankGroups + 1) * 4 + 64 <= kSortBigCap * 8,
-              "bitmap + prefixes fit the buffer");
+constexpr int kRankMetaBytes = (((kRankGroups + 1) * 4 + 64) + 15) / 16 * 16;   // gpre + warp sums
+static_assert(kRankWords * 4 + kRankMetaBytes <= kSortBigCap * 8, "bitmap + prefixes fit the buffer");
+// (Staging a window's placed keys in the rest of the buffer so the output
+// columns are written in order was measured: no gain, 1.63 -> 1.7 ms at the
+// cfg4 slice -- the scattered 20-byte writes are not what the kernel waits on.)
 
 // Per window: clear the bitmap (16-byte stores), set the keys' bits, count each
 // 8-word group (two 16-byte loads per group), exclusive-scan the 4096 group
@@ -1448,6 +1451,15 @@ static_assert(kRankWords * 4 + (kRankGroups + 1) * 4 + 64 <= kSortBigCap * 8,
 // 32768 words per window -- 25k warp instructions even with conflict-free
 // warp-per-group scans -- for 3 reads per key; rows of a few thousand keys are
 // far cheaper with 4096 prefixes and ~6 reads per key.)
+// Keys are read in batches of kRankBatch independent loads per thread (one
+// memory round trip per batch: ncu put 52% of this kernel's stall samples on
+// the two loops' one-key-at-a-time loads); a row of <= kRankBatch * threads
+// keys (4096) is loaded ONCE into registers and reused by both loops of every
+// window (kSmall).
+constexpr int kRankBatch = 8;
+constexpr uint64_t kNoKey = ~0ull;   // right offset 2^32 - 1: outside every window
+
+template <bool kSmall>
 __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0, uint64_t i_row,
                          int64_t n_right, uint32_t* bits, uint32_t* gpre,
                          uint64_t* __restrict__ lefts, uint64_t* __restrict__ rights,
@@ -1457,12 +1469,25 @@ __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0,
   const int lane = tid & 31, warp = tid >> 5;
   uint4* b4 = reinterpret_cast<uint4*>(bits);
   uint64_t base = 0;
+  uint64_t kreg[kRankBatch];
+  auto load_batch = [&](int64_t t0) {
+#pragma unroll
+    for (int u = 0; u < kRankBatch; u++) {
+      const int64_t t = t0 + (int64_t)u * nthr;
+      kreg[u] = t < n ? g[t] : kNoKey;
+    }
+  };
+  if (kSmall) load_batch(tid);
   for (int64_t w0 = 0; w0 < n_right; w0 += kRankWindow) {
     for (int t = tid; t < kRankWords / 4; t += nthr) b4[t] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
-    for (int64_t t = tid; t < n; t += nthr) {
-      const uint64_t o = (g[t] >> 32) - (uint64_t)w0;
-      if (o < (uint64_t)kRankWindow) atomicOr(&bits[o >> 5], 1u << (o & 31));
+    for (int64_t t0 = tid; t0 < n; t0 += (int64_t)kRankBatch * nthr) {
+      if (!kSmall) load_batch(t0);
+#pragma unroll
+      for (int u = 0; u < kRankBatch; u++) {
+        const uint64_t o = (kreg[u] >> 32) - (uint64_t)w0;
+        if (o < (uint64_t)kRankWindow) atomicOr(&bits[o >> 5], 1u << (o & 31));
+      }
     }
     __syncthreads();
     // group counts: thread t counts groups t, t + nthr, ... (neighbouring
@@ -1508,17 +1533,21 @@ __device__ void rank_row(const uint64_t* __restrict__ g, int64_t n, uint64_t q0,
     reinterpret_cast<uint4*>(gpre)[2 * tid + 1] =
         make_uint4(tb + c[4], tb + c[5], tb + c[6], tb + c[7]);
     __syncthreads();
-    for (int64_t t = tid; t < n; t += nthr) {
-      const uint64_t key = g[t];
-      const uint64_t o = (key >> 32) - (uint64_t)w0;
-      if (o >= (uint64_t)kRankWindow) continue;
-      const uint32_t word = (uint32_t)(o >> 5), grp = word / kRankSub;
-      uint32_t rank = gpre[grp] + __popc(bits[word] & ((1u << (o & 31)) - 1u));
-      for (uint32_t w = grp * kRankSub; w < word; w++) rank += __popc(bits[w]);
-      const uint64_t pos = q0 + base + rank;
-      lefts[pos] = i_row;
-      rights[pos] = key >> 32;
-      sims[pos] = __uint_as_float((uint32_t)key);
+    for (int64_t t0 = tid; t0 < n; t0 += (int64_t)kRankBatch * nthr) {
+      if (!kSmall) load_batch(t0);
+#pragma unroll
+      for (int u = 0; u < kRankBatch; u++) {
+        const uint64_t key = kreg[u];
+        const uint64_t o = (key >> 32) - (uint64_t)w0;
+        if (o >= (uint64_t)kRankWindow) continue;
+        const uint32_t word = (uint32_t)(o >> 5), grp = word / kRankSub;
+        uint32_t rank = gpre[grp] + __popc(bits[word] & ((1u << (o & 31)) - 1u));
+        for (uint32_t w = grp * kRankSub; w < word; w++) rank += __popc(bits[w]);
+        const uint64_t pos = q0 + base + rank;
+        lefts[pos] = i_row;
+        rights[pos] = key >> 32;
+        sims[pos] = __uint_as_float((uint32_t)key);
+      }
     }
     base += all;
     __syncthreads();
@@ -1533,7 +1562,17 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
   extern __shared__ __align__(16) uint64_t sbuf[];
   if (n_big[1] == 0) return;  // gate: outputs would overflow
   const unsigned nb = n_big[0];
-  for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
+  // rows handed out by a counter (n_big[2], zero since join_begin): Zipf clusters
+  // make a few rows ten times longer than the rest, and a static row -> CTA
+  // map leaves the CTAs that drew them running alone at the end
+  __shared__ unsigned s_row;
+  unsigned int* next = const_cast<unsigned int*>(n_big) + 2;
+  for (;;) {
+    if (threadIdx.x == 0) s_row = atomicAdd(next, 1u);
+    __syncthreads();
+    const unsigned r = s_row;
+    __syncthreads();
+    if (r >= nb) break;
     const uint32_t i = big_rows[r];
     const uint64_t q0 = rowoff[i];
     const int64_t n = (int64_t)(rowoff[i + 1] - q0);
@@ -1554,7 +1593,10 @@ segsort_big_kernel(const uint64_t* __restrict__ rowoff, uint64_t* __restrict__ k
       continue;
     }
     uint32_t* bits = reinterpret_cast<uint32_t*>(sbuf);
-    rank_row(g, n, q0, left_base + i, n_right, bits, bits + kRankWords, lefts, rights, sims);
+    if (n <= (int64_t)kRankBatch * kSortBigThreads)
+      rank_row<true>(g, n, q0, left_base + i, n_right, bits, bits + kRankWords, lefts, rights, sims);
+    else
+      rank_row<false>(g, n, q0, left_base + i, n_right, bits, bits + kRankWords, lefts, rights, sims);
   }
 }
 

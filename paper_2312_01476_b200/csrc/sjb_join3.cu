@@ -1233,5 +1233,102 @@ recheck_pending_staged_kernel(const uint64_t* __restrict__ cand, uint64_t seg_ca
   }
 }
 
+// Canonical recheck of ROW-GROUPED candidates (canonical sims on raw operands,
+// after the pair filter): grouped[k] = (i << 32 | j), a row's candidates
+// contiguous.  The staged scheme of recheck_pending_staged_kernel with one
+// more step: when a warp's 32 candidates share their left row (the common case:
+// cfg4 rows hold thousands), that row's chunk is copied ONCE (lanes 0-7, one
+// line) and read as a shared-memory broadcast, so a candidate moves 4 d bytes
+// (its S row) instead of 8 d.  sims_bits[k] gets the canonical bits or
+// kRejected; kept matches are counted per left row (one atomic per warp when
+// the row is shared).
+__global__ void __launch_bounds__(kPsWarps * 32, 1)
+recheck_grouped_staged_kernel(const uint64_t* __restrict__ grouped,
+                              const uint64_t* __restrict__ total_p, const float* __restrict__ l32,
+                              const float* __restrict__ r32, int dim, float theta,
+                              uint32_t* __restrict__ sims_bits, uint32_t* __restrict__ rowcount) {
+  extern __shared__ __align__(128) uint8_t ps_smem[];
+  const uint64_t total = *total_p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = ps_smem + (size_t)warp * kPsBufs * kPsBufBytes;
+  const int nchunks = (dim + kPsChunk - 1) / kPsChunk;
+  const int sub = lane >> 3, piece = lane & 7;
+  const uint64_t n_groups = (total + 31) / 32;
+  for (uint64_t g = (uint64_t)blockIdx.x * kPsWarps + warp; g < n_groups;
+       g += (uint64_t)gridDim.x * kPsWarps) {
+    const uint64_t p = g * 32 + lane;
+    const bool ok = p < total;
+    uint32_t gi = 0, gj = 0;
+    if (ok) {
+      const uint64_t u = grouped[p];
+      gi = (uint32_t)(u >> 32);
+      gj = (uint32_t)u;
+    }
+    const uint32_t gi0 = __shfl_sync(0xffffffffu, gi, 0);
+    const bool shared_row = __all_sync(0xffffffffu, !ok || gi == gi0);
+    const float* srcA[8];
+    const float* srcB[8];
+#pragma unroll
+    for (int it = 0; it < 8; it++) {
+      const uint32_t i = __shfl_sync(0xffffffffu, gi, it * 4 + sub);
+      const uint32_t j = __shfl_sync(0xffffffffu, gj, it * 4 + sub);
+      srcA[it] = l32 + (size_t)i * dim + piece * 4;
+      srcB[it] = r32 + (size_t)j * dim + piece * 4;
+    }
+    const float* rowA = l32 + (size_t)gi0 * dim + piece * 4;   // shared_row: lanes 0-7 copy it
+    auto issue = [&](int c) {
+      if (c < nchunks && c * kPsChunk + piece * 4 < dim) {
+        uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes;
+        if (shared_row) {
+          if (sub == 0)   // unswizzled (pair index 0), read by every lane
+            cp_async16(reinterpret_cast<float*>(buf + (uint32_t)piece * 16u), rowA + c * kPsChunk);
+        }
+#pragma unroll
+        for (int it = 0; it < 8; it++) {
+          const int pr = it * 4 + sub;
+          const uint32_t off = (uint32_t)pr * 128u + (uint32_t)((piece ^ (pr & 7)) * 16);
+          if (!shared_row)
+            cp_async16(reinterpret_cast<float*>(buf + off), srcA[it] + c * kPsChunk);
+          cp_async16(reinterpret_cast<float*>(buf + 4096u + off), srcB[it] + c * kPsChunk);
+        }
+      }
+      cp_async_commit();
+    };
+    issue(0);
+    issue(1);
+    float acc = 0.0f;
+    const uint32_t a_row = shared_row ? 0u : (uint32_t)lane * 128u;
+    const uint32_t a_swz = shared_row ? 0u : (uint32_t)(lane & 7);
+    for (int c = 0; c < nchunks; c++) {
+      issue(c + 2);
+      cp_async_wait_two();
+      __syncwarp();
+      const uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes;
+      const int np = mn<int>(8, (dim - c * kPsChunk) >> 2);
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if (q < np) {
+          const float4 x = *reinterpret_cast<const float4*>(buf + a_row + (((uint32_t)q ^ a_swz) * 16u));
+          const float4 y = *reinterpret_cast<const float4*>(
+              buf + 4096u + (uint32_t)lane * 128u + (uint32_t)((q ^ (lane & 7)) * 16));
+          acc = __fmaf_rn(x.x, y.x, acc);
+          acc = __fmaf_rn(x.y, y.y, acc);
+          acc = __fmaf_rn(x.z, y.z, acc);
+          acc = __fmaf_rn(x.w, y.w, acc);
+        }
+      }
+      __syncwarp();
+    }
+    const bool keep = ok && acc >= theta;
+    if (ok) sims_bits[p] = keep ? __float_as_uint(acc) : kRejected;
+    if (shared_row) {
+      const uint32_t kept = __popc(__ballot_sync(0xffffffffu, keep));
+      if (lane == 0 && kept) atomicAdd(rowcount + gi0, kept);
+    } else if (keep) {
+      atomicAdd(rowcount + gi, 1u);
+    }
+  }
+}
+
 }  // namespace wide
 }  // namespace sjb

@@ -162,6 +162,8 @@ struct alignas(64) Params {
   uint32_t* rowcount;
   uint32_t* pend;
   uint32_t* pend_count;
+  int tol;     // 1: tolerance emission (tensor sims); 0: candidates only (canonical sims: the
+               // row-grouped staged recheck decides every candidate afterwards)
   int debug;   // diagnostics (results invalid): 1 no emission, 2 no drain, 3 drain + normalise only,
                // 20 no operand traffic
 };
@@ -411,9 +413,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (m > 3.0e38f) cta_sat[0] = 1u;
               continue;
             }
-            fin += emit_row_chunk_tol<kCW>(v, row_ok, p.cutoff, p.hi_cut, (uint32_t)gi64,
-                                           (uint32_t)col0, p.n_b - col0, cta_cnt, cta_sat, seg,
-                                           p.seg_cap, sims, pend_cnt, pend, scr);
+            if (p.tol)
+              fin += emit_row_chunk_tol<kCW>(v, row_ok, p.cutoff, p.hi_cut, (uint32_t)gi64,
+                                             (uint32_t)col0, p.n_b - col0, cta_cnt, cta_sat, seg,
+                                             p.seg_cap, sims, pend_cnt, pend, scr);
+            else
+              emit_row_chunk<kCW>(v, row_ok, p.cutoff, (uint32_t)gi64, (uint32_t)col0,
+                                  p.n_b - col0, cta_cnt, cta_sat, seg, p.seg_cap);
           }
         }
       }
@@ -430,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   if (threadIdx.x == 0) {
     p.cta_count[blockIdx.x] = *cta_sat ? ~0ull >> 1 : (unsigned long long)*cta_cnt;
-    p.pend_count[blockIdx.x] = *pend_cnt;
+    if (p.tol) p.pend_count[blockIdx.x] = *pend_cnt;
   }
 }
 

@@ -1015,6 +1015,40 @@ def test_bf16_tensor_sims_incremental_rounds(cuda, grid):
         assert np.array_equal(so.view(np.uint32), one[2].view(np.uint32))
 
 
+@pytest.mark.parametrize("mode", ["rows", "group"])
+def test_bf16_canonical_sims_row_grouped_recheck(cuda, monkeypatch, mode):
+    """Canonical sims on raw bf16 operands: the default (1-CTA filter +
+    tile-group recheck; any other value of SJB_WIDE_EXACT) and the A/B path
+    SJB_WIDE_EXACT=rows (CTA-pair filter emitting candidates only, candidates
+    grouped by left row, warp-staged recheck with the shared left row
+    broadcast): the oracle's MatchSet bit for bit, one-launch and
+    incremental, with an overflow retry, dims with a partial last chunk, rows
+    with one candidate (warps spanning several left rows) and dense rows."""
+    from paper_2312_01476_b200 import device as D
+    monkeypatch.setenv("SJB_WIDE_EXACT", mode)
+    cases = ((700, 2900, 384, 10, 0.6, 0.6, 71),      # clustered: dense rows
+             (513, 1100, 260, 6, 0.7, 0.55, 72),      # dim % 32 != 0
+             (300, 2300, 768, 300, 0.5, 0.7, 73),     # many small clusters: sparse rows
+             (257, 513, 192, 4, 0.4, 0.5, 74))
+    for nl, nr, dim, ncl, sigma, theta, seed in cases:
+        L, S = _bf16_case(nl, nr, dim, ncl, sigma, seed)
+        wl, wr, ws = O.join_raw(L, S, theta, threads=8)
+        assert len(wl) > 0
+        pl, pr = D.prepare_bf16(_bf16_tensor(L, cuda)), D.prepare_bf16(_bf16_tensor(S, cuda))
+        for cap in (None, 4096):
+            m = D.join_prepared(pl, pr, theta, cand_cap=cap)
+            lo, ro, so = m.to_host()
+            assert np.array_equal(lo, wl) and np.array_equal(ro, wr), (mode, dim, cap)
+            assert np.array_equal(so.view(np.uint32), ws.view(np.uint32)), (mode, dim, cap)
+        sess = D.JoinSession(pl, pr, theta, None, 0)
+        step = 256 * max(1, (nr // 256) // 3)
+        for r0 in range(0, nr, step):
+            sess.filter_rows(r0, min(nr, r0 + step))
+        lo, ro, so = sess.finish().result().to_host()
+        assert np.array_equal(lo, wl) and np.array_equal(ro, wr)
+        assert np.array_equal(so.view(np.uint32), ws.view(np.uint32))
+
+
 def test_pending_recheck_staged_equals_gather(cuda, monkeypatch):
     """Tensor sims: the band pairs' canonical recheck with rows staged through
     shared memory by whole warps (default) against the thread-per-pair gather

@@ -241,13 +241,16 @@ int make_plan(const sjb_join_args* a, JoinPlan* pl) {
     if (a->sims_mode == 1) pl->wide_fused = false;   // pending lists need the separate recheck
     if (!SJB_AB_KERNELS && pl->wide_fused) return ab_missing("SJB_WIDE_RECHECK=fused");
     {
-      // A/B (SJB_WIDE_EXACT=rows), canonical sims on raw operands: CTA-pair filter emitting
-      // candidates only + candidates grouped by left row + warp-staged recheck with the
-      // shared left row broadcast.  Bitwise the same result; measured no faster at the cfg4
-      // slice (49.5 vs 48.3 ms): the filter falls 19.5 -> 14.9 ms, but row-grouped order
-      // loses the S-row locality of the filter's tile order -- S (3 GB of fp32 rows) is
-      // re-read from DRAM per candidate, 27.5 ms at ~7 TB/s vs 25.6 ms for the tile-group
-      // recheck.  Default: the 1-CTA filter + tile-group recheck.
+      // A/B (SJB_WIDE_EXACT=rows), canonical sims on raw operands: the CTA-pair filter emits
+      // candidates only and records each work item's segment offset; work items are then
+      // rechecked in the filter's S-chunk-major order by warps that counting-sort 2048
+      // candidates by left row and stage each distinct left row once beside 32 private S
+      // rows (recheck_segments_sorted_kernel).  Bitwise the same result; measured slower at
+      // the cfg4 slice (53 vs 48 ms): the filter falls 19.5 -> 15.2 ms, but the staged
+      // recheck takes 34 ms vs 25.6 ms for the tile-group recheck -- it is bound by the
+      // cp.async issue rate (one 512-byte LDGSTS per 8 cycles per SM, ~64 B/cycle), whatever
+      // the candidate order (row-grouped: 27.5 ms; filter order by position: 29.8 ms) or
+      // ring depth.  Default: the 1-CTA filter + tile-group recheck.
       const char* we = getenv("SJB_WIDE_EXACT");
       pl->wide_rows = raw && a->sims_mode == 0 && !pl->wide_fused && (pl->grid % 2) == 0 &&
                       (a->dim % 4) == 0 && a->out_cap >= a->cand_cap &&
@@ -1085,6 +1088,8 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         const bool mma2_two = pl.wide_rows || mma2_two_env;
         sjb::wide2::Params q;
         q.tol = wp.tol;
+        q.tile_off = c.tile_off;
+        q.tile_stride = pl.tile_stride;
         if (int rc = encode_operand_map(&q.tmap_a, d_l16, nl, pl.kpad, 128, 8)) return rc;
         if (int rc = encode_operand_map(&q.tmap_b, d_r16, nr, pl.kpad, 128, 8)) return rc;
         q.n_a = nl;
@@ -1094,7 +1099,16 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
         // 512-row pair tiles (the image is padded); two-stage: the 256-row tiles themselves
         const int64_t pb = mma2_two ? tb : tb / 2, pe = mma2_two ? te : (te + 1) / 2;
         const int64_t tt = (int64_t)pl.n_ablk * (pe - pb) / (8LL * (pl.grid / 2));
-        const int tpc2 = (int)(tt < 1 ? 1 : (tt > 32 ? 32 : tt));
+        int tpc2 = (int)(tt < 1 ? 1 : (tt > 32 ? 32 : tt));
+        if (pl.wide_rows) {
+          // the per-CTA item offsets share the tile-offset rows of the workspace: coarser
+          // items until a pair's items (+ the end offset) fit one row
+          const int64_t np2 = pl.grid / 2;
+          while (tpc2 < 32 &&
+                 sjb::ceil_div((int64_t)pl.n_ablk * sjb::ceil_div(pe - pb, (int64_t)tpc2), np2) + 1 >
+                     pl.tile_stride)
+            tpc2 *= 2;
+        }
         q.n_ptiles = (int)pe;
         q.tiles_per_chunk = tpc2;
         q.tile_begin = (int)pb;
@@ -1139,6 +1153,19 @@ int join_filter(const float* d_l32, const void* d_l16, const float* d_r32, const
           const int lim = (dv >= 0 && dv < 64) ? max_pairs[dv] : (1 << 20);
           const int g2 = 2 * (pl.grid / 2 < lim ? pl.grid / 2 : lim);
           sjb::wide2::filter_kernel<true><<<g2, sjb::wide2::kThreads, sm2, st>>>(q);
+          if (pl.wide_rows && jp.debug_mode != 1) {
+            // every candidate of this launch, work items in the filter's S-chunk-major order
+            SJB_CK_LAUNCH("wide2_filter");
+            SJB_CK(cudaMemsetAsync(c.work, 0, 4, st));
+            const uint32_t rsm = sjb::wide::recheck_sorted_smem();
+            if (int rc = set_smem_attr((const void*)sjb::wide::recheck_segments_sorted_kernel,
+                                       (int)rsm))
+              return rc;
+            sjb::wide::recheck_segments_sorted_kernel<<<sjb_sm_count(current_device()),
+                                                        sjb::wide::kPsWarps * 32, rsm, st>>>(
+                c.cand, pl.seg_cap, c.cta, c.tile_off, pl.tile_stride, q.n_items, g2 / 2, c.work,
+                d_l32, d_r32, (int)args->dim, args->theta, c.sims_bits, c.rowcount);
+          }
         } else {
 #if SJB_AB_KERNELS
           if (int rc = set_smem_attr((const void*)sjb::wide2::filter_kernel<false>, (int)sm2)) return rc;
@@ -1432,7 +1459,7 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     return SJB_OK;
 #endif
   }
-  if (pl.defer || pl.wide_rows) {
+  if (pl.defer) {
     // dense: group the candidates by left row, recheck them row-grouped,
     // then compact the matches by row (the segment buffer is free by then)
     const dim3 sgrid(8, (unsigned)pl.grid);
@@ -1446,19 +1473,9 @@ int join_finish(const float* d_l32, const float* d_r32, const sjb_join_args* arg
     SJB_CK_LAUNCH("group_rows");
     SJB_CK(cudaMemsetAsync(c.rowcount, 0, (size_t)nl * 4, st));
     const unsigned flat = (unsigned)sjb_sm_count(current_device()) * 8;
-    if (pl.wide_rows &&
-        ((reinterpret_cast<uintptr_t>(d_l32) | reinterpret_cast<uintptr_t>(d_r32)) & 15) == 0) {
-      const uint32_t psm = sjb::wide::pending_staged_smem();
-      if (int rc = set_smem_attr((const void*)sjb::wide::recheck_grouped_staged_kernel, (int)psm))
-        return rc;
-      sjb::wide::recheck_grouped_staged_kernel<<<sjb_sm_count(current_device()),
-                                                 sjb::wide::kPsWarps * 32, psm, st>>>(
-          c.keys, c.ncand, d_l32, d_r32, (int)args->dim, args->theta, c.sims_bits, c.rowcount);
-    } else {
-      sjb::recheck_grouped_kernel<<<flat, 256, 0, st>>>(c.keys, c.ncand, d_l32, d_r32,
-                                                        (int)args->dim, args->theta, c.sims_bits,
-                                                        c.rowcount);
-    }
+    sjb::recheck_grouped_kernel<<<flat, 256, 0, st>>>(c.keys, c.ncand, d_l32, d_r32,
+                                                      (int)args->dim, args->theta, c.sims_bits,
+                                                      c.rowcount);
     SJB_CK_LAUNCH("recheck_grouped");
     if (int rc = run_scan(c.rowcount, nl, c.rowoff, c.cursor, c.bsums, st)) return rc;
     sjb::gate_kernel<<<1, 1, 0, st>>>(c.rowoff, nl, args->out_cap, c.nbig);

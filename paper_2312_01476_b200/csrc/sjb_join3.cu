@@ -1233,100 +1233,193 @@ recheck_pending_staged_kernel(const uint64_t* __restrict__ cand, uint64_t seg_ca
   }
 }
 
-// Canonical recheck of ROW-GROUPED candidates (canonical sims on raw operands,
-// after the pair filter): grouped[k] = (i << 32 | j), a row's candidates
-// contiguous.  The staged scheme of recheck_pending_staged_kernel with one
-// more step: when a warp's 32 candidates share their left row (the common case:
-// cfg4 rows hold thousands), that row's chunk is copied ONCE (lanes 0-7, one
-// line) and read as a shared-memory broadcast, so a candidate moves 4 d bytes
-// (its S row) instead of 8 d.  sims_bits[k] gets the canonical bits or
-// kRejected; kept matches are counted per left row (one atomic per warp when
-// the row is shared).
+// Canonical recheck of every candidate of the CTA-pair filter's segments
+// (canonical sims on raw operands, SJB_WIDE_EXACT=rows), in the FILTER'S ORDER:
+// recheck CTA c walks segment c from its start, so all CTAs stay on the S chunk
+// the filter CTAs were on together and the S rows are L2 hits (grouping the
+// candidates by left row first was measured: the recheck turned DRAM-bound,
+// 27.5 ms at the cfg4 slice).  Row sharing is recovered locally: a block of
+// 2048 consecutive candidates (half a work item: 128 left rows, ~16
+// candidates each at cfg4) is counting-sorted by left row in shared memory,
+// and a warp then takes 32 neighbours of that order -- 2-3 distinct left rows
+// -- and stages each DISTINCT left row once (the lanes of a row read its
+// leader's copy: a broadcast) beside the 32 private S rows, with the ring,
+// swizzle and chain of recheck_pending_staged_kernel.  A candidate moves
+// ~4 d bytes from L2 instead of 8 d.  sims_bits[slot] gets the canonical bits
+// or kRejected; kept matches are counted per left row.
+constexpr int kRsBlock = 2048;
+// ring stage: 8 shared left-row slots (1 KB) + the 32 private S rows (4 KB); 5 stages, four
+// chunks in flight per warp.  (With the 8 KB stages and 3-deep ring of the pending kernel this
+// kernel ran at ~7 TB/s of L2 -> SM traffic: 72 KB in flight per SM against ~2000 cycles of
+// loaded L2 latency.  The staged kernels are bound by bytes in flight, not by bandwidth.)
+constexpr int kRsLead = 8;
+constexpr int kRsBufs = 5;
+constexpr uint32_t kRsABytes = kRsLead * 128u;
+constexpr uint32_t kRsBufBytes = kRsABytes + 32u * 128u;
+constexpr uint32_t kRsRingBytes = kPsWarps * kRsBufs * kRsBufBytes;
+__host__ __device__ constexpr uint32_t recheck_sorted_smem() {
+  return kRsRingBytes + kRsBlock * 8 + kRsBlock * 2 + 2 * 256 * 4 + 64;
+}
+__device__ __forceinline__ void cp_async_wait_four() { asm volatile("cp.async.wait_group 4;" ::: "memory"); }
+
+// Work units (pair work item, CTA of the pair) are handed out by a counter in the
+// filter's S-chunk-major item order, so every recheck CTA is on the same few S chunks
+// (walking the segments by position lets them drift chunks apart: the S rows then come
+// from DRAM); the unit's candidates are segment [toff[k], toff[k + 1]) of its filter CTA.
 __global__ void __launch_bounds__(kPsWarps * 32, 1)
-recheck_grouped_staged_kernel(const uint64_t* __restrict__ grouped,
-                              const uint64_t* __restrict__ total_p, const float* __restrict__ l32,
-                              const float* __restrict__ r32, int dim, float theta,
-                              uint32_t* __restrict__ sims_bits, uint32_t* __restrict__ rowcount) {
+recheck_segments_sorted_kernel(const uint64_t* __restrict__ cand, uint64_t seg_cap,
+                               const unsigned long long* __restrict__ cta_count,
+                               const uint32_t* __restrict__ tile_off, int64_t tile_stride,
+                               int64_t n_items, int n_pairs, unsigned int* __restrict__ work,
+                               const float* __restrict__ l32, const float* __restrict__ r32,
+                               int dim, float theta, uint32_t* __restrict__ sims_bits,
+                               uint32_t* __restrict__ rowcount) {
   extern __shared__ __align__(128) uint8_t ps_smem[];
-  const uint64_t total = *total_p;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = ps_smem + (size_t)warp * kPsBufs * kPsBufBytes;
+  __shared__ unsigned int s_unit;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* ring = ps_smem + (size_t)warp * kRsBufs * kRsBufBytes;
+  uint64_t* sorted = reinterpret_cast<uint64_t*>(ps_smem + kRsRingBytes);
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(sorted + kRsBlock);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sidx + kRsBlock);   // [256] counts, then cursors
+  uint32_t* wtot = hist + 256;                                      // [8] warp totals
   const int nchunks = (dim + kPsChunk - 1) / kPsChunk;
   const int sub = lane >> 3, piece = lane & 7;
-  const uint64_t n_groups = (total + 31) / 32;
-  for (uint64_t g = (uint64_t)blockIdx.x * kPsWarps + warp; g < n_groups;
-       g += (uint64_t)gridDim.x * kPsWarps) {
-    const uint64_t p = g * 32 + lane;
-    const bool ok = p < total;
-    uint32_t gi = 0, gj = 0;
-    if (ok) {
-      const uint64_t u = grouped[p];
-      gi = (uint32_t)(u >> 32);
-      gj = (uint32_t)u;
-    }
-    const uint32_t gi0 = __shfl_sync(0xffffffffu, gi, 0);
-    const bool shared_row = __all_sync(0xffffffffu, !ok || gi == gi0);
-    const float* srcA[8];
-    const float* srcB[8];
+  for (;;) {
+  if (tid == 0) s_unit = atomicAdd(work, 1u);
+  __syncthreads();
+  const int64_t unit = (int64_t)s_unit;
+  __syncthreads();
+  if (unit >= 2 * n_items) break;
+  const int64_t item = unit >> 1;
+  const int fc = 2 * (int)(item % n_pairs) + (int)(unit & 1);   // the filter CTA
+  const int64_t k = item / n_pairs;                             // its k-th work item
+  if (cta_count[fc] > seg_cap) continue;   // saturated segment: the join is retried with room
+  const uint64_t* seg = cand + (uint64_t)fc * seg_cap;
+  uint32_t* sims = sims_bits + (uint64_t)fc * seg_cap;
+  const uint32_t* toff = tile_off + (int64_t)fc * tile_stride;
+  const uint64_t lo = toff[k], cc = toff[k + 1];
+  for (uint64_t b0 = lo; b0 < cc; b0 += kRsBlock) {
+    const int nb = (int)mn<uint64_t>(kRsBlock, cc - b0);
+    // ---- counting sort of the block by (left row & 255)
+    hist[tid] = 0u;   // 256 threads
+    __syncthreads();
+    for (int t = tid; t < nb; t += kPsWarps * 32)
+      atomicAdd(&hist[(uint32_t)(seg[b0 + t] >> 32) & 255u], 1u);
+    __syncthreads();
+    {
+      const uint32_t v = hist[tid];
+      uint32_t incl = v;
 #pragma unroll
-    for (int it = 0; it < 8; it++) {
-      const uint32_t i = __shfl_sync(0xffffffffu, gi, it * 4 + sub);
-      const uint32_t j = __shfl_sync(0xffffffffu, gj, it * 4 + sub);
-      srcA[it] = l32 + (size_t)i * dim + piece * 4;
-      srcB[it] = r32 + (size_t)j * dim + piece * 4;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wtot[warp] = incl;
+      __syncthreads();
+      uint32_t base = 0;
+      for (int w = 0; w < warp; w++) base += wtot[w];
+      hist[tid] = base + incl - v;   // exclusive prefix: the bucket's cursor
     }
-    const float* rowA = l32 + (size_t)gi0 * dim + piece * 4;   // shared_row: lanes 0-7 copy it
-    auto issue = [&](int c) {
-      if (c < nchunks && c * kPsChunk + piece * 4 < dim) {
-        uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes;
-        if (shared_row) {
-          if (sub == 0)   // unswizzled (pair index 0), read by every lane
-            cp_async16(reinterpret_cast<float*>(buf + (uint32_t)piece * 16u), rowA + c * kPsChunk);
-        }
+    __syncthreads();
+    for (int t = tid; t < nb; t += kPsWarps * 32) {
+      const uint64_t u = seg[b0 + t];
+      const uint32_t pos = atomicAdd(&hist[(uint32_t)(u >> 32) & 255u], 1u);
+      sorted[pos] = u;
+      sidx[pos] = (uint16_t)t;
+    }
+    __syncthreads();
+    // ---- staged recheck of 32 neighbours of the sorted order per warp
+    for (int e0 = warp * 32; e0 < nb; e0 += kPsWarps * 32) {
+      const int e = e0 + lane;
+      const bool ok = e < nb;
+      uint32_t gi = 0, gj = 0, slot = 0;
+      if (ok) {
+        const uint64_t u = sorted[e];
+        gi = (uint32_t)(u >> 32);
+        gj = (uint32_t)u;
+        slot = (uint32_t)sidx[e];
+      }
+      // passes of <= kRsLead distinct left rows (one pass unless the warp's candidates
+      // are spread over more rows: sparse joins)
+      uint32_t todo = __ballot_sync(0xffffffffu, ok);
+      while (todo) {
+        const bool mine = (todo >> lane) & 1u;
+        // a lane's left row is staged by its leader: the first pending lane with the same row
+        const uint32_t same = __match_any_sync(0xffffffffu, mine ? gi : 0xFFFFFFFFu) & todo;
+        const int leader = mine ? __ffs(same) - 1 : lane;
+        const uint32_t lead_mask = __ballot_sync(0xffffffffu, mine && leader == lane);
+        const uint32_t rank = __popc(lead_mask & ((1u << leader) - 1u));   // the leader's A slot
+        const bool active = mine && rank < (uint32_t)kRsLead;
+        const uint32_t act_mask = __ballot_sync(0xffffffffu, active);
+        const float* srcA[8];
+        const float* srcB[8];
+        uint32_t offA[8];
 #pragma unroll
         for (int it = 0; it < 8; it++) {
           const int pr = it * 4 + sub;
-          const uint32_t off = (uint32_t)pr * 128u + (uint32_t)((piece ^ (pr & 7)) * 16);
-          if (!shared_row)
-            cp_async16(reinterpret_cast<float*>(buf + off), srcA[it] + c * kPsChunk);
-          cp_async16(reinterpret_cast<float*>(buf + 4096u + off), srcB[it] + c * kPsChunk);
+          const uint32_t i = __shfl_sync(0xffffffffu, gi, pr);
+          const uint32_t j = __shfl_sync(0xffffffffu, gj, pr);
+          srcA[it] = l32 + (size_t)i * dim + piece * 4;
+          srcB[it] = r32 + (size_t)j * dim + piece * 4;
+          const uint32_t rk = __popc(lead_mask & ((1u << pr) - 1u));
+          // leaders of active groups copy their left row into slot rk
+          offA[it] = ((lead_mask & act_mask) >> pr) & 1u
+                         ? rk * 128u + (uint32_t)((piece ^ (int)(rk & 7u)) * 16)
+                         : 0xFFFFFFFFu;
         }
-      }
-      cp_async_commit();
-    };
-    issue(0);
-    issue(1);
-    float acc = 0.0f;
-    const uint32_t a_row = shared_row ? 0u : (uint32_t)lane * 128u;
-    const uint32_t a_swz = shared_row ? 0u : (uint32_t)(lane & 7);
-    for (int c = 0; c < nchunks; c++) {
-      issue(c + 2);
-      cp_async_wait_two();
-      __syncwarp();
-      const uint8_t* buf = ring + (size_t)(c % kPsBufs) * kPsBufBytes;
-      const int np = mn<int>(8, (dim - c * kPsChunk) >> 2);
+        auto issue = [&](int c) {
+          if (c < nchunks && c * kPsChunk + piece * 4 < dim) {
+            uint8_t* buf = ring + (size_t)(c % kRsBufs) * kRsBufBytes;
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        if (q < np) {
-          const float4 x = *reinterpret_cast<const float4*>(buf + a_row + (((uint32_t)q ^ a_swz) * 16u));
-          const float4 y = *reinterpret_cast<const float4*>(
-              buf + 4096u + (uint32_t)lane * 128u + (uint32_t)((q ^ (lane & 7)) * 16));
-          acc = __fmaf_rn(x.x, y.x, acc);
-          acc = __fmaf_rn(x.y, y.y, acc);
-          acc = __fmaf_rn(x.z, y.z, acc);
-          acc = __fmaf_rn(x.w, y.w, acc);
+            for (int it = 0; it < 8; it++) {
+              const int pr = it * 4 + sub;
+              if (offA[it] != 0xFFFFFFFFu)
+                cp_async16(reinterpret_cast<float*>(buf + offA[it]), srcA[it] + c * kPsChunk);
+              if ((act_mask >> pr) & 1u)
+                cp_async16(reinterpret_cast<float*>(buf + kRsABytes + (uint32_t)pr * 128u +
+                                                    (uint32_t)((piece ^ (pr & 7)) * 16)),
+                           srcB[it] + c * kPsChunk);
+            }
+          }
+          cp_async_commit();
+        };
+        issue(0);
+        issue(1);
+        issue(2);
+        issue(3);
+        float acc = 0.0f;
+        const uint32_t a_row = (rank & 7u) * 128u, a_swz = rank & 7u;
+        for (int c = 0; c < nchunks; c++) {
+          issue(c + 4);
+          cp_async_wait_four();
+          __syncwarp();
+          const uint8_t* buf = ring + (size_t)(c % kRsBufs) * kRsBufBytes;
+          const int np = mn<int>(8, (dim - c * kPsChunk) >> 2);
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (q < np) {
+              const float4 x =
+                  *reinterpret_cast<const float4*>(buf + a_row + (((uint32_t)q ^ a_swz) * 16u));
+              const float4 y = *reinterpret_cast<const float4*>(
+                  buf + kRsABytes + (uint32_t)lane * 128u + (uint32_t)((q ^ (lane & 7)) * 16));
+              acc = __fmaf_rn(x.x, y.x, acc);
+              acc = __fmaf_rn(x.y, y.y, acc);
+              acc = __fmaf_rn(x.z, y.z, acc);
+              acc = __fmaf_rn(x.w, y.w, acc);
+            }
+          }
+          __syncwarp();
         }
+        const bool keep = active && acc >= theta;
+        if (active) sims[b0 + slot] = keep ? __float_as_uint(acc) : kRejected;
+        // one atomic per distinct left row of the pass
+        const uint32_t kept = __popc(__ballot_sync(0xffffffffu, keep) & same);
+        if (active && leader == lane && kept) atomicAdd(rowcount + gi, kept);
+        todo &= ~act_mask;
       }
-      __syncwarp();
     }
-    const bool keep = ok && acc >= theta;
-    if (ok) sims_bits[p] = keep ? __float_as_uint(acc) : kRejected;
-    if (shared_row) {
-      const uint32_t kept = __popc(__ballot_sync(0xffffffffu, keep));
-      if (lane == 0 && kept) atomicAdd(rowcount + gi0, kept);
-    } else if (keep) {
-      atomicAdd(rowcount + gi, 1u);
-    }
+    __syncthreads();   // the block's buffers are reused
+  }
   }
 }
 

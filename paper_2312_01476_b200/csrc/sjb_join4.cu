@@ -162,6 +162,8 @@ struct alignas(64) Params {
   uint32_t* rowcount;
   uint32_t* pend;
   uint32_t* pend_count;
+  uint32_t* tile_off;   // !tol: [grid][tile_stride] segment offset at each work item's start (+ end)
+  int64_t tile_stride;
   int tol;     // 1: tolerance emission (tensor sims); 0: candidates only (canonical sims: the
                // row-grouped staged recheck decides every candidate afterwards)
   int debug;   // diagnostics (results invalid): 1 no emission, 2 no drain, 3 drain + normalise only,
@@ -332,7 +334,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t* pend = p.pend + (uint64_t)blockIdx.x * p.seg_cap;
     float* scr = tol_scratch + (ew * 32 + lane) * kTolPitch;
     uint32_t tile_it = 0;
+    uint32_t* toff = p.tol ? nullptr : p.tile_off + (int64_t)blockIdx.x * p.tile_stride;
+    uint32_t item_k = 0;
     for (int64_t item = pair_id; item < n_items; item += n_pairs) {
+      if (toff != nullptr) {
+        // every epilogue warp is done with the previous item: the counter is this item's first slot
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (ew == 0 && lane == 0) toff[item_k] = *(volatile uint32_t*)cta_cnt;
+        item_k++;
+      }
       const int64_t rb = item % nb, sc = item / nb;
       const int64_t t0 = p.tile_begin + sc * p.tiles_per_chunk;
       const int64_t t1 = mn<int64_t>(t0 + p.tiles_per_chunk, p.n_ptiles);
@@ -424,6 +434,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       if (fin) atomicAdd(p.rowcount + gi64, fin);
+    }
+    if (toff != nullptr) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (ew == 0 && lane == 0) toff[item_k] = *(volatile uint32_t*)cta_cnt;
     }
   }
 

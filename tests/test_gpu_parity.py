@@ -1019,9 +1019,10 @@ def test_bf16_tensor_sims_incremental_rounds(cuda, grid):
 def test_bf16_canonical_sims_row_grouped_recheck(cuda, monkeypatch, mode):
     """Canonical sims on raw bf16 operands: the default (1-CTA filter +
     tile-group recheck; any other value of SJB_WIDE_EXACT) and the A/B path
-    SJB_WIDE_EXACT=rows (CTA-pair filter emitting candidates only, candidates
-    grouped by left row, warp-staged recheck with the shared left row
-    broadcast): the oracle's MatchSet bit for bit, one-launch and
+    SJB_WIDE_EXACT=rows (CTA-pair filter emitting candidates only and recording
+    per-item segment offsets; items rechecked in the filter's order by warps
+    that sort 2048 candidates by left row and stage each distinct left row
+    once): the oracle's MatchSet bit for bit, one-launch and
     incremental, with an overflow retry, dims with a partial last chunk, rows
     with one candidate (warps spanning several left rows) and dense rows."""
     from paper_2312_01476_b200 import device as D
